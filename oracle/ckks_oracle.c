@@ -1,0 +1,722 @@
+/*
+ * ckks_oracle.c -- plain, slow, obviously-correct CPU oracle for the Blind-Match
+ * encrypted 1:N cosine scan (HE-C^3, Algorithm 2).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load, call or execute anything under
+ * oracle/.  The product library (paper_2408_06167_b200/) never includes, links
+ * or imports this file, and this file includes nothing from the product.
+ *
+ * Everything is textbook: canonical residues in [0,q), modular products via
+ * unsigned __int128 '%', polynomials kept in the COEFFICIENT domain, and a
+ * negacyclic product built from the standard pre-twisted radix-2 cyclic NTT
+ * (the only "library primitive" step; pinned against schoolbook
+ * multiplication in tests/test_oracle_ring.py).  No blocking, no fusion, no
+ * lazy reduction, no reordering beyond what the op definitions state.
+ *
+ * Scheme (RNS-CKKS, the paper's HE library setting, PAPER.md:155-170, 850-862;
+ * parameters fixed by BASELINE.json configs / SURVEY.md Appendix A):
+ *   ring   R = Z[X]/(X^N+1), N = 2^logN (8192 in every config; small N only in pins)
+ *   primes q0 (58-bit), q1 (40-bit), special P (60-bit), each the largest prime
+ *          below 2^k with q = 1 mod 16384 (BASELINE.json configs[0]).
+ *   level 1 = {q0,q1}, level 0 = {q0}.  Key-switching uses one RNS digit per
+ *   Q-prime and the special prime P (reading R3).
+ *
+ * Randomness: ChaCha20 block function (RFC 8439 sec. 2.3), addressed by
+ * (seed, purpose, object, sub-stream, block counter); samplers in or_sample().
+ * Both sides (oracle and product) implement this generator independently
+ * (reading R14).
+ *
+ * Data layouts (all coefficient domain, u64 residues, limb-major):
+ *   ct level 1   [2 comps][2 limbs q0,q1][N]
+ *   ct level 0   [2 comps][1 limb  q0][N]
+ *   pk           [2 comps (b,a)][2 limbs][N]
+ *   rlk          [2 digits j][2 comps (b,a)][3 limbs q0,q1,P][N]
+ *   gk           [n_rot][2 comps (b,a)][2 limbs q0,P][N]; entry i is rotation 2^i
+ *   sk           int8[N] in {-1,0,1}
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+/* ------------------------------------------------------------------ */
+/* scalar modular arithmetic (plain definitions)                        */
+/* ------------------------------------------------------------------ */
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a * b) % q); }
+static uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a + b) % q); }
+static uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a + q - b) % q); }
+static uint64_t powmod(uint64_t a, uint64_t e, uint64_t q)
+{
+    uint64_t r = 1 % q;
+    a %= q;
+    while (e) {
+        if (e & 1) r = mulmod(r, a, q);
+        a = mulmod(a, a, q);
+        e >>= 1;
+    }
+    return r;
+}
+/* q prime: Fermat inverse */
+static uint64_t invmod(uint64_t a, uint64_t q) { return powmod(a, q - 2, q); }
+/* signed integer -> residue in [0,q) */
+static uint64_t from_signed(int64_t x, uint64_t q)
+{
+    i128 r = (i128)x % (i128)q;
+    if (r < 0) r += q;
+    return (uint64_t)r;
+}
+/* residue in [0,q) -> centred representative in (-q/2, q/2]  (q odd) */
+static int64_t centred(uint64_t x, uint64_t q) { return (x > q / 2) ? (int64_t)x - (int64_t)q : (int64_t)x; }
+
+/* ------------------------------------------------------------------ */
+/* primes (BASELINE.json configs[0]: "largest below 2^k with q=1 mod 16384") */
+/* ------------------------------------------------------------------ */
+/* deterministic Miller-Rabin; the first 12 prime bases are exact for n < 3.3e24 */
+int or_is_prime(uint64_t n)
+{
+    static const uint64_t bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    if (n < 2) return 0;
+    for (int i = 0; i < 12; i++) {
+        if (n == bases[i]) return 1;
+        if (n % bases[i] == 0) return 0;
+    }
+    uint64_t d = n - 1;
+    int r = 0;
+    while ((d & 1) == 0) { d >>= 1; r++; }
+    for (int i = 0; i < 12; i++) {
+        uint64_t x = powmod(bases[i], d, n);
+        if (x == 1 || x == n - 1) continue;
+        int comp = 1;
+        for (int k = 1; k < r; k++) {
+            x = mulmod(x, x, n);
+            if (x == n - 1) { comp = 0; break; }
+        }
+        if (comp) return 0;
+    }
+    return 1;
+}
+
+/* largest prime q < 2^bits with q = 1 (mod m) */
+uint64_t or_find_prime(int bits, uint64_t m)
+{
+    uint64_t q = ((uint64_t)1 << bits) - m + 1;   /* 2^bits = 0 mod m, so this is the largest candidate */
+    while (!or_is_prime(q)) q -= m;
+    return q;
+}
+
+/* fills {q0, q1, P} */
+void or_primes(uint64_t out[3])
+{
+    out[0] = or_find_prime(58, 16384);
+    out[1] = or_find_prime(40, 16384);
+    out[2] = or_find_prime(60, 16384);
+}
+
+/* ------------------------------------------------------------------ */
+/* ring: negacyclic product via pre-twisted cyclic NTT                 */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int N, logN;
+    uint64_t q;
+    uint64_t psi;        /* primitive 2N-th root of unity mod q */
+    uint64_t *psi_pow;   /* psi^k, k < N            */
+    uint64_t *ipsi_pow;  /* psi^-k, k < N           */
+    uint64_t *omega_pow; /* omega^k, omega = psi^2, k < N */
+    uint64_t *iomega_pow;
+    uint64_t n_inv;
+} ring_t;
+
+static void ring_init(ring_t *R, int logN, uint64_t q)
+{
+    R->logN = logN;
+    R->N = 1 << logN;
+    R->q = q;
+    const uint64_t twoN = 2 * (uint64_t)R->N;
+    /* psi = x^((q-1)/2N) has order dividing 2N; order is exactly 2N iff psi^N = -1 */
+    for (uint64_t x = 2;; x++) {
+        uint64_t c = powmod(x, (q - 1) / twoN, q);
+        if (powmod(c, R->N, q) == q - 1) { R->psi = c; break; }
+    }
+    R->psi_pow = malloc(sizeof(uint64_t) * R->N);
+    R->ipsi_pow = malloc(sizeof(uint64_t) * R->N);
+    R->omega_pow = malloc(sizeof(uint64_t) * R->N);
+    R->iomega_pow = malloc(sizeof(uint64_t) * R->N);
+    uint64_t ipsi = invmod(R->psi, q), om = mulmod(R->psi, R->psi, q), iom = invmod(om, q);
+    uint64_t a = 1, b = 1, c = 1, d = 1;
+    for (int k = 0; k < R->N; k++) {
+        R->psi_pow[k] = a; a = mulmod(a, R->psi, q);
+        R->ipsi_pow[k] = b; b = mulmod(b, ipsi, q);
+        R->omega_pow[k] = c; c = mulmod(c, om, q);
+        R->iomega_pow[k] = d; d = mulmod(d, iom, q);
+    }
+    R->n_inv = invmod((uint64_t)R->N, q);
+}
+
+static void ring_free(ring_t *R)
+{
+    free(R->psi_pow); free(R->ipsi_pow); free(R->omega_pow); free(R->iomega_pow);
+}
+
+static unsigned bitrev(unsigned x, int bits)
+{
+    unsigned r = 0;
+    for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+/* textbook iterative radix-2 cyclic NTT (bit-reverse copy, then log N butterfly levels):
+ * A_i = sum_k a_k w^(ik) with w = omega (forward) or omega^-1 (inverse, unscaled). */
+static void cyclic_ntt(const ring_t *R, uint64_t *a, const uint64_t *wpow)
+{
+    const int N = R->N;
+    const uint64_t q = R->q;
+    for (int i = 0; i < N; i++) {
+        unsigned j = bitrev((unsigned)i, R->logN);
+        if (j > (unsigned)i) { uint64_t t = a[i]; a[i] = a[j]; a[j] = t; }
+    }
+    for (int len = 2; len <= N; len <<= 1) {
+        int step = N / len; /* w_len = w^(N/len) */
+        for (int start = 0; start < N; start += len) {
+            for (int k = 0; k < len / 2; k++) {
+                uint64_t w = wpow[k * step];
+                uint64_t u = a[start + k];
+                uint64_t v = mulmod(a[start + k + len / 2], w, q);
+                a[start + k] = addmod(u, v, q);
+                a[start + k + len / 2] = submod(u, v, q);
+            }
+        }
+    }
+}
+
+/* c = a * b mod (X^N + 1, q).  Negacyclic convolution = cyclic convolution of the
+ * psi-twisted inputs, untwisted by psi^-k.  c may alias a or b. */
+static void poly_mul(const ring_t *R, const uint64_t *a, const uint64_t *b, uint64_t *c)
+{
+    const int N = R->N;
+    const uint64_t q = R->q;
+    uint64_t *A = malloc(sizeof(uint64_t) * N), *B = malloc(sizeof(uint64_t) * N);
+    for (int k = 0; k < N; k++) {
+        A[k] = mulmod(a[k], R->psi_pow[k], q);
+        B[k] = mulmod(b[k], R->psi_pow[k], q);
+    }
+    cyclic_ntt(R, A, R->omega_pow);
+    cyclic_ntt(R, B, R->omega_pow);
+    for (int k = 0; k < N; k++) A[k] = mulmod(A[k], B[k], q);
+    cyclic_ntt(R, A, R->iomega_pow);
+    for (int k = 0; k < N; k++) c[k] = mulmod(mulmod(A[k], R->n_inv, q), R->ipsi_pow[k], q);
+    free(A); free(B);
+}
+
+static void poly_add(uint64_t q, int N, const uint64_t *a, const uint64_t *b, uint64_t *c)
+{
+    for (int k = 0; k < N; k++) c[k] = addmod(a[k], b[k], q);
+}
+static void poly_sub(uint64_t q, int N, const uint64_t *a, const uint64_t *b, uint64_t *c)
+{
+    for (int k = 0; k < N; k++) c[k] = submod(a[k], b[k], q);
+}
+static void poly_scale(uint64_t q, int N, const uint64_t *a, uint64_t s, uint64_t *c)
+{
+    for (int k = 0; k < N; k++) c[k] = mulmod(a[k], s, q);
+}
+
+/* exported for the schoolbook pin: c = a*b mod (X^N+1, q) */
+void or_poly_mul(int logN, uint64_t q, const uint64_t *a, const uint64_t *b, uint64_t *c)
+{
+    ring_t R;
+    ring_init(&R, logN, q);
+    poly_mul(&R, a, b, c);
+    ring_free(&R);
+}
+
+/* Galois automorphism sigma_g: a(X) -> a(X^g), g odd.  Coefficient k moves to
+ * t = k*g mod 2N; since X^N = -1 it lands at t-N with a sign flip when t >= N. */
+static void automorphism(uint64_t q, int N, const uint64_t *a, uint64_t g, uint64_t *out)
+{
+    const uint64_t twoN = 2 * (uint64_t)N;
+    for (int k = 0; k < N; k++) {
+        uint64_t t = ((uint64_t)k * g) % twoN;
+        if (t < (uint64_t)N) out[t] = a[k];
+        else out[t - N] = submod(0, a[k], q);
+    }
+}
+
+void or_automorphism(int logN, uint64_t q, const uint64_t *a, uint64_t g, uint64_t *out)
+{
+    automorphism(q, 1 << logN, a, g, out);
+}
+
+/* ------------------------------------------------------------------ */
+/* ChaCha20 (RFC 8439 sec. 2.1-2.3) and samplers                       */
+/* ------------------------------------------------------------------ */
+static uint32_t rotl32(uint32_t x, int n) { return (x << n) | (x >> (32 - n)); }
+
+void or_chacha_quarter(uint32_t *a, uint32_t *b, uint32_t *c, uint32_t *d)
+{
+    *a += *b; *d ^= *a; *d = rotl32(*d, 16);
+    *c += *d; *b ^= *c; *b = rotl32(*b, 12);
+    *a += *b; *d ^= *a; *d = rotl32(*d, 8);
+    *c += *d; *b ^= *c; *b = rotl32(*b, 7);
+}
+
+void or_chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3], uint32_t out[16])
+{
+    uint32_t s[16], x[16];
+    s[0] = 0x61707865u; s[1] = 0x3320646eu; s[2] = 0x79622d32u; s[3] = 0x6b206574u;
+    for (int i = 0; i < 8; i++) s[4 + i] = key[i];
+    s[12] = counter;
+    s[13] = nonce[0]; s[14] = nonce[1]; s[15] = nonce[2];
+    memcpy(x, s, sizeof s);
+    for (int r = 0; r < 10; r++) {
+        or_chacha_quarter(&x[0], &x[4], &x[8], &x[12]);
+        or_chacha_quarter(&x[1], &x[5], &x[9], &x[13]);
+        or_chacha_quarter(&x[2], &x[6], &x[10], &x[14]);
+        or_chacha_quarter(&x[3], &x[7], &x[11], &x[15]);
+        or_chacha_quarter(&x[0], &x[5], &x[10], &x[15]);
+        or_chacha_quarter(&x[1], &x[6], &x[11], &x[12]);
+        or_chacha_quarter(&x[2], &x[7], &x[8], &x[13]);
+        or_chacha_quarter(&x[3], &x[4], &x[9], &x[14]);
+    }
+    for (int i = 0; i < 16; i++) out[i] = x[i] + s[i];
+}
+
+/* Draw number n (u64) of stream (seed, purpose, obj, sub):
+ * key = {seed lo, seed hi, purpose, 0,0,0,0,0}, nonce = {obj lo, obj hi, sub},
+ * block counter = n / 8, u64 = word[2(n%8)] | word[2(n%8)+1] << 32. */
+uint64_t or_draw(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t sub, uint64_t n)
+{
+    uint32_t key[8] = {(uint32_t)seed, (uint32_t)(seed >> 32), purpose, 0, 0, 0, 0, 0};
+    uint32_t nonce[3] = {(uint32_t)obj, (uint32_t)(obj >> 32), sub};
+    uint32_t blk[16];
+    or_chacha20_block(key, (uint32_t)(n / 8), nonce, blk);
+    int w = (int)(n % 8) * 2;
+    return (uint64_t)blk[w] | ((uint64_t)blk[w + 1] << 32);
+}
+
+/* purposes of the random streams */
+enum { P_SK = 1, P_PK_A = 2, P_PK_E = 3, P_RLK_A = 4, P_RLK_E = 5, P_GK_A = 6, P_GK_E = 7,
+       P_ENC_U = 8, P_ENC_E0 = 9, P_ENC_E1 = 10 };
+
+/* Discrete Gaussian CDT, sigma = 3.2, support |x| <= 19:
+ * OR_CDT[k] = floor(2^63 * Pr(|X| <= k)), k = 0..18, generated exactly by
+ * oracle/gen_cdt.py (Python Decimal, 60 digits). */
+#include "cdt_table.h"
+
+/* kind 0: uniform mod q from a 128-bit draw (draws 2k, 2k+1);
+ * kind 1: ternary (draw k mod 3) - 1;
+ * kind 2: Gaussian: v = low 63 bits of draw k, mag = #{j : v >= CDT[j]}, sign = top bit.
+ * Output: residues mod q (q = 0 requests the signed integers cast to uint64). */
+void or_sample(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t sub, int kind, int n, uint64_t q, uint64_t *out)
+{
+    for (int k = 0; k < n; k++) {
+        int64_t v;
+        if (kind == 0) {
+            u128 x = ((u128)or_draw(seed, purpose, obj, sub, 2 * (uint64_t)k + 1) << 64) |
+                     or_draw(seed, purpose, obj, sub, 2 * (uint64_t)k);
+            out[k] = (uint64_t)(x % q);
+            continue;
+        } else if (kind == 1) {
+            v = (int64_t)(or_draw(seed, purpose, obj, sub, (uint64_t)k) % 3) - 1;
+        } else {
+            uint64_t x = or_draw(seed, purpose, obj, sub, (uint64_t)k);
+            uint64_t u = x & 0x7fffffffffffffffull;
+            int mag = 0;
+            for (int j = 0; j < 19; j++)
+                if (u >= OR_CDT[j]) mag++;
+            v = (x >> 63) ? -mag : mag;
+        }
+        out[k] = q ? from_signed(v, q) : (uint64_t)v;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* parameter context                                                   */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int logN, N;
+    uint64_t q[3];      /* q0, q1, P */
+    ring_t R[3];
+    uint64_t P_mod[2];  /* P mod q0, P mod q1 */
+    uint64_t P_inv[2];  /* P^-1 mod q0, q1   */
+    uint64_t q1_inv_q0; /* q1^-1 mod q0      */
+} ctx_t;
+
+static void ctx_init(ctx_t *c, int logN)
+{
+    c->logN = logN;
+    c->N = 1 << logN;
+    or_primes(c->q);
+    for (int k = 0; k < 3; k++) ring_init(&c->R[k], logN, c->q[k]);
+    for (int k = 0; k < 2; k++) {
+        c->P_mod[k] = c->q[2] % c->q[k];
+        c->P_inv[k] = invmod(c->P_mod[k], c->q[k]);
+    }
+    c->q1_inv_q0 = invmod(c->q[1] % c->q[0], c->q[0]);
+}
+static void ctx_free(ctx_t *c)
+{
+    for (int k = 0; k < 3; k++) ring_free(&c->R[k]);
+}
+
+/* Galois element for a left slot rotation by r: g = 5^r mod 2N (reading R6) */
+static uint64_t galois_elt(int N, uint64_t r) { return powmod(5, r, 2 * (uint64_t)N); }
+
+/* ------------------------------------------------------------------ */
+/* key generation (rows a0 of SURVEY.md sec. 8a)     */
+/* ------------------------------------------------------------------ */
+/* sk: ternary s.  pk = (b, a) over {q0,q1}: b = -a s + e.
+ * rlk_j (digit j in {0,1}) over {q0,q1,P}: b = -a s + e + [k==j] (P mod q_k) s^2, P-limb b = -a s + e.
+ * gk_i (rotation 2^i) over {q0,P}: b = -a s + e + (P mod q0) sigma_g(s) in q0; -a s + e in P.
+ * zero_error != 0 sets every key error to 0 (used only by the key-switch identity pin). */
+int or_keygen(int logN, uint64_t seed, int n_rot, int zero_error,
+              int8_t *sk, uint64_t *pk, uint64_t *rlk, uint64_t *gk)
+{
+    ctx_t C;
+    ctx_init(&C, logN);
+    const int N = C.N;
+    uint64_t *tmp = malloc(sizeof(uint64_t) * N), *e = malloc(sizeof(uint64_t) * N);
+    uint64_t *s = malloc(sizeof(uint64_t) * N), *a = malloc(sizeof(uint64_t) * N);
+    uint64_t *s2 = malloc(sizeof(uint64_t) * N), *ss = malloc(sizeof(uint64_t) * N);
+    int64_t *sv = malloc(sizeof(int64_t) * N), *ev = malloc(sizeof(int64_t) * N);
+
+    or_sample(seed, P_SK, 0, 0, 1, N, 0, (uint64_t *)sv);
+    for (int k = 0; k < N; k++) sk[k] = (int8_t)sv[k];
+
+    /* public key */
+    or_sample(seed, P_PK_E, 0, 0, 2, N, 0, (uint64_t *)ev);
+    if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+    for (int l = 0; l < 2; l++) {
+        uint64_t q = C.q[l];
+        for (int k = 0; k < N; k++) { s[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+        or_sample(seed, P_PK_A, 0, (uint32_t)l, 0, N, q, a);
+        poly_mul(&C.R[l], a, s, tmp);
+        uint64_t *b = pk + (size_t)(0 * 2 + l) * N, *aa = pk + (size_t)(1 * 2 + l) * N;
+        poly_sub(q, N, e, tmp, b);
+        memcpy(aa, a, sizeof(uint64_t) * N);
+    }
+
+    /* relinearization key: rlk[j][comp][limb][N] */
+    for (int j = 0; j < 2; j++) {
+        or_sample(seed, P_RLK_E, (uint64_t)j, 0, 2, N, 0, (uint64_t *)ev);
+        if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+        for (int l = 0; l < 3; l++) {
+            uint64_t q = C.q[l];
+            for (int k = 0; k < N; k++) { s[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+            or_sample(seed, P_RLK_A, (uint64_t)j, (uint32_t)l, 0, N, q, a);
+            uint64_t *b = rlk + ((size_t)(j * 2 + 0) * 3 + l) * N;
+            uint64_t *aa = rlk + ((size_t)(j * 2 + 1) * 3 + l) * N;
+            poly_mul(&C.R[l], a, s, tmp);
+            poly_sub(q, N, e, tmp, b);
+            if (l == j) {
+                poly_mul(&C.R[l], s, s, s2);
+                poly_scale(q, N, s2, C.P_mod[l], tmp);
+                poly_add(q, N, b, tmp, b);
+            }
+            memcpy(aa, a, sizeof(uint64_t) * N);
+        }
+    }
+
+    /* Galois keys: gk[i][comp][limb in {q0,P}][N], rotation r = 2^i */
+    for (int i = 0; i < n_rot; i++) {
+        uint64_t g = galois_elt(N, (uint64_t)1 << i);
+        or_sample(seed, P_GK_E, (uint64_t)i, 0, 2, N, 0, (uint64_t *)ev);
+        if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+        for (int li = 0; li < 2; li++) {
+            int l = li == 0 ? 0 : 2;
+            uint64_t q = C.q[l];
+            for (int k = 0; k < N; k++) { s[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+            or_sample(seed, P_GK_A, (uint64_t)i, (uint32_t)l, 0, N, q, a);
+            uint64_t *b = gk + ((size_t)(i * 2 + 0) * 2 + li) * N;
+            uint64_t *aa = gk + ((size_t)(i * 2 + 1) * 2 + li) * N;
+            poly_mul(&C.R[l], a, s, tmp);
+            poly_sub(q, N, e, tmp, b);
+            if (l == 0) {
+                automorphism(q, N, s, g, ss);
+                poly_scale(q, N, ss, C.P_mod[0], tmp);
+                poly_add(q, N, b, tmp, b);
+            }
+            memcpy(aa, a, sizeof(uint64_t) * N);
+        }
+    }
+    free(tmp); free(e); free(s); free(a); free(s2); free(ss); free(sv); free(ev);
+    ctx_free(&C);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* encryption / decryption                */
+/* ------------------------------------------------------------------ */
+/* Public-key encryption of integer plaintexts pt[n_cts][N] at level 1:
+ * ct_o = (u*b + e0 + pt, u*a + e1) mod {q0,q1}, u ternary, e0/e1 Gaussian,
+ * drawn from streams (seed, ENC_*, obj = first_obj + index, sub 0). */
+void or_encrypt(int logN, const uint64_t *pk, const int64_t *pt, int64_t n_cts, uint64_t first_obj,
+                uint64_t seed, uint64_t *out)
+{
+    ctx_t C;
+    ctx_init(&C, logN);
+    const int N = C.N;
+    int64_t *uv = malloc(sizeof(int64_t) * N), *e0v = malloc(sizeof(int64_t) * N), *e1v = malloc(sizeof(int64_t) * N);
+    uint64_t *u = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * N), *x = malloc(sizeof(uint64_t) * N);
+    for (int64_t c = 0; c < n_cts; c++) {
+        uint64_t obj = first_obj + (uint64_t)c;
+        or_sample(seed, P_ENC_U, obj, 0, 1, N, 0, (uint64_t *)uv);
+        or_sample(seed, P_ENC_E0, obj, 0, 2, N, 0, (uint64_t *)e0v);
+        or_sample(seed, P_ENC_E1, obj, 0, 2, N, 0, (uint64_t *)e1v);
+        for (int l = 0; l < 2; l++) {
+            uint64_t q = C.q[l];
+            const uint64_t *b = pk + (size_t)(0 * 2 + l) * N, *a = pk + (size_t)(1 * 2 + l) * N;
+            uint64_t *c0 = out + ((size_t)c * 4 + 0 * 2 + l) * N, *c1 = out + ((size_t)c * 4 + 1 * 2 + l) * N;
+            for (int k = 0; k < N; k++) u[k] = from_signed(uv[k], q);
+            poly_mul(&C.R[l], u, b, t);
+            for (int k = 0; k < N; k++)
+                x[k] = addmod(from_signed(e0v[k], q), from_signed(pt[(size_t)c * N + k], q), q);
+            poly_add(q, N, t, x, c0);
+            poly_mul(&C.R[l], u, a, t);
+            for (int k = 0; k < N; k++) x[k] = from_signed(e1v[k], q);
+            poly_add(q, N, t, x, c1);
+        }
+    }
+    free(uv); free(e0v); free(e1v); free(u); free(t); free(x);
+    ctx_free(&C);
+}
+
+/* m = c0 + c1*s mod q_l for each limb l < n_limbs; ct layout [2][n_limbs][N] */
+void or_decrypt(int logN, const int8_t *sk, const uint64_t *ct, int n_limbs, uint64_t *m)
+{
+    ctx_t C;
+    ctx_init(&C, logN);
+    const int N = C.N;
+    uint64_t *s = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * N);
+    for (int l = 0; l < n_limbs; l++) {
+        uint64_t q = C.q[l];
+        for (int k = 0; k < N; k++) s[k] = from_signed(sk[k], q);
+        poly_mul(&C.R[l], ct + (size_t)(1 * n_limbs + l) * N, s, t);
+        poly_add(q, N, ct + (size_t)(0 * n_limbs + l) * N, t, m + (size_t)l * N);
+    }
+    free(s); free(t);
+    ctx_free(&C);
+}
+
+/* ------------------------------------------------------------------ */
+/* evaluation ops                          */
+/* ------------------------------------------------------------------ */
+/* ModDown by P of a key-switch accumulator: out[k] = (KS[k] - centred_P(KS[P])) * P^-1 mod q_k,
+ * for k < n_q (KS layout [n_q + 1 limbs][N], P limb last). */
+static void moddown(const ctx_t *C, int n_q, const uint64_t *KS, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t P = C->q[2];
+    const uint64_t *ksP = KS + (size_t)n_q * N;
+    for (int l = 0; l < n_q; l++) {
+        uint64_t q = C->q[l];
+        for (int k = 0; k < N; k++) {
+            uint64_t y = from_signed(centred(ksP[k], P), q);
+            out[(size_t)l * N + k] = mulmod(submod(KS[(size_t)l * N + k], y, q), C->P_inv[l], q);
+        }
+    }
+}
+
+/* Relinearization (the "re-linearization" inside Mul):
+ * (d0, d1, d2) at level 1 -> (d0 + KS'_0, d1 + KS'_1), digits x_j = [d2]_{q_j} lifted
+ * non-centred to {q0,q1,P}; KS_c = sum_j x_j * rlk_j[c]; KS' = ModDown(KS).
+ * d layout [3][2][N]; out layout [2][2][N]. */
+static void relinearize(const ctx_t *C, const uint64_t *d, const uint64_t *rlk, uint64_t *out)
+{
+    const int N = C->N;
+    uint64_t *KS = calloc((size_t)3 * N, sizeof(uint64_t));
+    uint64_t *x = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * N);
+    uint64_t *ksd = malloc(sizeof(uint64_t) * 2 * N);
+    for (int c = 0; c < 2; c++) {
+        memset(KS, 0, sizeof(uint64_t) * 3 * N);
+        for (int j = 0; j < 2; j++) {
+            const uint64_t *xj = d + (size_t)(2 * 2 + j) * N; /* [d2]_{q_j}, entries in [0,q_j) */
+            for (int l = 0; l < 3; l++) {
+                uint64_t q = C->q[l];
+                for (int k = 0; k < N; k++) x[k] = xj[k] % q;
+                poly_mul(&C->R[l], x, rlk + ((size_t)(j * 2 + c) * 3 + l) * N, t);
+                poly_add(q, N, KS + (size_t)l * N, t, KS + (size_t)l * N);
+            }
+        }
+        moddown(C, 2, KS, ksd);
+        for (int l = 0; l < 2; l++)
+            poly_add(C->q[l], N, d + (size_t)(c * 2 + l) * N, ksd + (size_t)l * N, out + (size_t)(c * 2 + l) * N);
+    }
+    free(KS); free(x); free(t); free(ksd);
+}
+
+/* Rescale (Res): level 1 -> 0; c' = (c[q0] - centred_{q1}(c[q1])) * q1^-1 mod q0.
+ * in [2][2][N] -> out [2][1][N] */
+static void rescale(const ctx_t *C, const uint64_t *in, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t q0 = C->q[0], q1 = C->q[1];
+    for (int c = 0; c < 2; c++)
+        for (int k = 0; k < N; k++) {
+            uint64_t z = from_signed(centred(in[(size_t)(c * 2 + 1) * N + k], q1), q0);
+            out[(size_t)c * N + k] = mulmod(submod(in[(size_t)(c * 2 + 0) * N + k], z, q0), C->q1_inv_q0, q0);
+        }
+}
+
+/* Rot (left rotation by r, reading R6) at level 0 with Galois key gk_r
+ * ([2 comps][2 limbs q0,P][N]): (sigma_g(c0) + KS'_0, KS'_1), KS_c = x * gk[c], x = sigma_g(c1)
+ * lifted non-centred to {q0,P}. in/out [2][1][N] (out may not alias in). */
+static void rotate(const ctx_t *C, const uint64_t *in, uint64_t r, const uint64_t *gkr, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t q0 = C->q[0], P = C->q[2];
+    const uint64_t g = galois_elt(N, r);
+    uint64_t *a0 = malloc(sizeof(uint64_t) * N), *a1 = malloc(sizeof(uint64_t) * N);
+    uint64_t *xP = malloc(sizeof(uint64_t) * N);
+    uint64_t *KS = malloc(sizeof(uint64_t) * 2 * N), *ksd = malloc(sizeof(uint64_t) * N);
+    automorphism(q0, N, in, g, a0);
+    automorphism(q0, N, in + N, g, a1);
+    for (int k = 0; k < N; k++) xP[k] = a1[k] % P;
+    for (int c = 0; c < 2; c++) {
+        /* KS layout for moddown: [q0][P] */
+        poly_mul(&C->R[0], a1, gkr + (size_t)(c * 2 + 0) * N, KS);
+        poly_mul(&C->R[2], xP, gkr + (size_t)(c * 2 + 1) * N, KS + N);
+        moddown(C, 1, KS, ksd);
+        if (c == 0) poly_add(q0, N, a0, ksd, out);
+        else memcpy(out + N, ksd, sizeof(uint64_t) * N);
+    }
+    free(a0); free(a1); free(xP); free(KS); free(ksd);
+}
+
+/* exported single-op entry points for the pins */
+void or_relinearize(int logN, const uint64_t *d, const uint64_t *rlk, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); relinearize(&C, d, rlk, out); ctx_free(&C);
+}
+void or_rescale(int logN, const uint64_t *in, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); rescale(&C, in, out); ctx_free(&C);
+}
+void or_rotate(int logN, const uint64_t *in, uint64_t r, const uint64_t *gkr, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); rotate(&C, in, r, gkr, out); ctx_free(&C);
+}
+void or_moddown(int logN, int n_q, const uint64_t *KS, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); moddown(&C, n_q, KS, out); ctx_free(&C);
+}
+
+/* Mul(C) tensor part for one pair of level-1 ciphertexts, accumulated into d [3][2][N]:
+ * d0 += a0 b0, d1 += a0 b1 + a1 b0, d2 += a1 b1 (negacyclic products per limb). */
+static void tensor_acc(const ctx_t *C, const uint64_t *ca, const uint64_t *cb, uint64_t *d)
+{
+    const int N = C->N;
+    uint64_t *t = malloc(sizeof(uint64_t) * N);
+    for (int l = 0; l < 2; l++) {
+        uint64_t q = C->q[l];
+        const uint64_t *a0 = ca + (size_t)(0 * 2 + l) * N, *a1 = ca + (size_t)(1 * 2 + l) * N;
+        const uint64_t *b0 = cb + (size_t)(0 * 2 + l) * N, *b1 = cb + (size_t)(1 * 2 + l) * N;
+        uint64_t *d0 = d + (size_t)(0 * 2 + l) * N, *d1 = d + (size_t)(1 * 2 + l) * N, *d2 = d + (size_t)(2 * 2 + l) * N;
+        poly_mul(&C->R[l], a0, b0, t); poly_add(q, N, d0, t, d0);
+        poly_mul(&C->R[l], a0, b1, t); poly_add(q, N, d1, t, d1);
+        poly_mul(&C->R[l], a1, b0, t); poly_add(q, N, d1, t, d1);
+        poly_mul(&C->R[l], a1, b1, t); poly_add(q, N, d2, t, d2);
+    }
+    free(t);
+}
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 2, HE-C^3 for one (query, set) pair    */
+/* ------------------------------------------------------------------ */
+/* order 0 (HOISTED): C = Res(Relin(sum_i tensor(C_u,i, C_s,i)))
+ * order 1 (PAPER):   C = sum_i Res(Relin(tensor(C_u,i, C_s,i))), C_out starting as the
+ *                    trivial zero ciphertext (line 3; reading R9).
+ * then for i = 1..log2(s): C = Add(Rot(C, 2^(i-1)), C)   (lines 7-9, reading R7).
+ * qct, sct: [p][2][2][N]; out: [2][1][N]. */
+static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64_t *rlk, const uint64_t *gk,
+                       const uint64_t *qct, const uint64_t *sct, uint64_t *out)
+{
+    const int N = C->N;
+    const size_t ct1 = (size_t)4 * N;
+    uint64_t *d = calloc((size_t)6 * N, sizeof(uint64_t));
+    uint64_t *r1 = malloc(sizeof(uint64_t) * 4 * N);
+    uint64_t *r0 = malloc(sizeof(uint64_t) * 2 * N);
+    uint64_t *rot = malloc(sizeof(uint64_t) * 2 * N);
+    const uint64_t q0 = C->q[0];
+    memset(out, 0, sizeof(uint64_t) * 2 * N);
+    if (order == 0) {
+        for (int i = 0; i < p; i++) tensor_acc(C, qct + i * ct1, sct + i * ct1, d);
+        relinearize(C, d, rlk, r1);
+        rescale(C, r1, out);
+    } else {
+        for (int i = 0; i < p; i++) {
+            memset(d, 0, sizeof(uint64_t) * 6 * N);
+            tensor_acc(C, qct + i * ct1, sct + i * ct1, d);
+            relinearize(C, d, rlk, r1);
+            rescale(C, r1, r0);
+            poly_add(q0, 2 * N, out, r0, out); /* Add at level 0, both components */
+        }
+    }
+    for (int i = 1; i <= log_s; i++) {
+        rotate(C, out, (uint64_t)1 << (i - 1), gk + (size_t)(i - 1) * 4 * N, rot);
+        poly_add(q0, 2 * N, rot, out, out);
+    }
+    free(d); free(r1); free(r0); free(rot);
+}
+
+typedef struct {
+    const ctx_t *C;
+    int p, log_s, order;
+    const uint64_t *rlk, *gk, *db, *q;
+    int64_t n_sets;
+    const int64_t *pairs; /* [n_pairs][2] = (query, set) */
+    int64_t n_pairs;
+    uint64_t *out;        /* [n_pairs][2][N] */
+    int64_t next;
+    pthread_mutex_t mu;
+} job_t;
+
+static void *worker(void *arg)
+{
+    job_t *J = (job_t *)arg;
+    const int N = J->C->N;
+    const size_t set_stride = (size_t)J->p * 4 * N;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        int64_t i = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (i >= J->n_pairs) break;
+        int64_t qi = J->pairs[2 * i], si = J->pairs[2 * i + 1];
+        he_c3_pair(J->C, J->p, J->log_s, J->order, J->rlk, J->gk, J->q + (size_t)qi * set_stride,
+                   J->db + (size_t)si * set_stride, J->out + (size_t)i * 2 * N);
+    }
+    return NULL;
+}
+
+/* The scan: for each listed (query, set) pair run HE-C^3.  db [n_sets][p][2][2][N],
+ * q [nq][p][2][2][N], rlk/gk as in or_keygen, out [n_pairs][2][1][N].
+ * Pairs are independent; they are spread over n_threads threads. */
+int or_match(int logN, int d, int p, int order, const uint64_t *rlk, const uint64_t *gk,
+             const uint64_t *db, int64_t n_sets, const uint64_t *q, int64_t nq,
+             const int64_t *pairs, int64_t n_pairs, uint64_t *out, int n_threads)
+{
+    if (p <= 0 || d % p) return -1;
+    int s = d / p, log_s = 0;
+    while ((1 << log_s) < s) log_s++;
+    if ((1 << log_s) != s) return -1;
+    for (int64_t i = 0; i < n_pairs; i++)
+        if (pairs[2 * i] < 0 || pairs[2 * i] >= nq || pairs[2 * i + 1] < 0 || pairs[2 * i + 1] >= n_sets) return -2;
+    ctx_t C;
+    ctx_init(&C, logN);
+    job_t J;
+    memset(&J, 0, sizeof J);
+    J.C = &C; J.p = p; J.log_s = log_s; J.order = order; J.rlk = rlk; J.gk = gk; J.db = db; J.q = q;
+    J.n_sets = n_sets; J.pairs = pairs; J.n_pairs = n_pairs; J.out = out; J.next = 0;
+    pthread_mutex_init(&J.mu, NULL);
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, worker, &J);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+    pthread_mutex_destroy(&J.mu);
+    ctx_free(&C);
+    return 0;
+}

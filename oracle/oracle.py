@@ -1,0 +1,312 @@
+"""Python face of the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and --impl reference)
+may import this module.  It loads oracle/liboracle.so (plain C, ckks_oracle.c) and adds
+the floating-point client-side steps in plain numpy:
+
+  * encode  (CKKS canonical embedding, "encrypts ... feature vector";
+             slot j <-> root zeta^(5^j), zeta = exp(i pi / N); readings R1, R15)
+  * decode  (direct formula z_j = sum_k m_k cos(pi k e_j / N) / scale)
+  * packing of templates into sets and of the query into p replicated parts
+             (readings R10, R11)
+  * score extraction at slot k*s and argmax
+
+Nothing here is shared with the product package; the only common module is the seeded
+input generator paper_2408_06167_b200/inputs.py (no CKKS arithmetic in it).
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+
+DELTA = 2.0 ** 40          # encoding scale (BASELINE.json configs[0]: "scale 2^40")
+ORDER_HOISTED = 0
+ORDER_PAPER = 1
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i8p = ctypes.POINTER(ctypes.c_int8)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+def build(force=False):
+    """Compile liboracle.so (plain C, no optimisation flags beyond -O2)."""
+    src = os.path.join(HERE, "ckks_oracle.c")
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-Wall", "-fPIC", "-shared", "-o", LIB_PATH, src, "-lpthread"])
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.or_is_prime.argtypes = [ctypes.c_uint64]
+        L.or_is_prime.restype = ctypes.c_int
+        L.or_find_prime.argtypes = [ctypes.c_int, ctypes.c_uint64]
+        L.or_find_prime.restype = ctypes.c_uint64
+        L.or_primes.argtypes = [_u64p]
+        L.or_poly_mul.argtypes = [ctypes.c_int, ctypes.c_uint64, _u64p, _u64p, _u64p]
+        L.or_automorphism.argtypes = [ctypes.c_int, ctypes.c_uint64, _u64p, ctypes.c_uint64, _u64p]
+        L.or_chacha_quarter.argtypes = [_u32p, _u32p, _u32p, _u32p]
+        L.or_chacha20_block.argtypes = [_u32p, ctypes.c_uint32, _u32p, _u32p]
+        L.or_draw.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64]
+        L.or_draw.restype = ctypes.c_uint64
+        L.or_sample.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
+                                ctypes.c_int, ctypes.c_uint64, _u64p]
+        L.or_keygen.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _i8p, _u64p, _u64p, _u64p]
+        L.or_keygen.restype = ctypes.c_int
+        L.or_encrypt.argtypes = [ctypes.c_int, _u64p, _i64p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
+        L.or_decrypt.argtypes = [ctypes.c_int, _i8p, _u64p, ctypes.c_int, _u64p]
+        L.or_relinearize.argtypes = [ctypes.c_int, _u64p, _u64p, _u64p]
+        L.or_rescale.argtypes = [ctypes.c_int, _u64p, _u64p]
+        L.or_rotate.argtypes = [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p]
+        L.or_moddown.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p]
+        L.or_match.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p,
+                               ctypes.c_int64, _u64p, ctypes.c_int64, _i64p, ctypes.c_int64, _u64p, ctypes.c_int]
+        L.or_match.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a, t):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(t)
+
+
+def primes():
+    out = np.zeros(3, np.uint64)
+    lib().or_primes(_p(out, _u64p))
+    return [int(x) for x in out]
+
+
+def poly_mul(logN, q, a, b):
+    a = np.ascontiguousarray(a, np.uint64)
+    b = np.ascontiguousarray(b, np.uint64)
+    c = np.zeros(1 << logN, np.uint64)
+    lib().or_poly_mul(logN, q, _p(a, _u64p), _p(b, _u64p), _p(c, _u64p))
+    return c
+
+
+def automorphism(logN, q, a, g):
+    a = np.ascontiguousarray(a, np.uint64)
+    c = np.zeros(1 << logN, np.uint64)
+    lib().or_automorphism(logN, q, _p(a, _u64p), g, _p(c, _u64p))
+    return c
+
+
+def chacha20_block(key, counter, nonce):
+    k = np.array(key, np.uint32)
+    n = np.array(nonce, np.uint32)
+    out = np.zeros(16, np.uint32)
+    lib().or_chacha20_block(_p(k, _u32p), counter, _p(n, _u32p), _p(out, _u32p))
+    return out
+
+
+def chacha_quarter(a, b, c, d):
+    v = [ctypes.c_uint32(x) for x in (a, b, c, d)]
+    lib().or_chacha_quarter(*[ctypes.byref(x) for x in v])
+    return [x.value for x in v]
+
+
+def draw(seed, purpose, obj, sub, n):
+    return int(lib().or_draw(seed, purpose, obj, sub, n))
+
+
+KIND_UNIFORM, KIND_TERNARY, KIND_GAUSS = 0, 1, 2
+
+
+def sample(seed, purpose, obj, sub, kind, n, q=0):
+    out = np.zeros(n, np.uint64)
+    lib().or_sample(seed, purpose, obj, sub, kind, n, q, _p(out, _u64p))
+    return out if q else out.view(np.int64)
+
+
+# ---------------------------------------------------------------------------- keys / enc / dec
+def n_rot_for(d, p):
+    s = d // p
+    return max(0, s.bit_length() - 1)   # rotations 2^i, i < log2 s
+
+
+def keygen(logN, seed, n_rot, zero_error=False):
+    N = 1 << logN
+    sk = np.zeros(N, np.int8)
+    pk = np.zeros((2, 2, N), np.uint64)
+    rlk = np.zeros((2, 2, 3, N), np.uint64)
+    gk = np.zeros((max(n_rot, 1), 2, 2, N), np.uint64)
+    lib().or_keygen(logN, seed, n_rot, int(zero_error), _p(sk, _i8p), _p(pk, _u64p), _p(rlk, _u64p), _p(gk, _u64p))
+    return sk, pk, rlk, gk[:n_rot]
+
+
+def encrypt(logN, pk, pt, first_obj, seed):
+    """pt int64 [n][N] -> level-1 cts [n][2][2][N] (coefficient domain)."""
+    pt = np.ascontiguousarray(pt, np.int64)
+    n = pt.shape[0]
+    out = np.zeros((n, 2, 2, 1 << logN), np.uint64)
+    lib().or_encrypt(logN, _p(np.ascontiguousarray(pk), _u64p), _p(pt, _i64p), n, first_obj, seed, _p(out, _u64p))
+    return out
+
+
+def decrypt(logN, sk, ct, n_limbs):
+    """ct [2][n_limbs][N] -> m residues [n_limbs][N]."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    m = np.zeros((n_limbs, 1 << logN), np.uint64)
+    lib().or_decrypt(logN, _p(np.ascontiguousarray(sk), _i8p), _p(ct, _u64p), n_limbs, _p(m, _u64p))
+    return m
+
+
+def relinearize(logN, d, rlk):
+    d = np.ascontiguousarray(d, np.uint64)
+    out = np.zeros((2, 2, 1 << logN), np.uint64)
+    lib().or_relinearize(logN, _p(d, _u64p), _p(np.ascontiguousarray(rlk), _u64p), _p(out, _u64p))
+    return out
+
+
+def rescale(logN, ct):
+    ct = np.ascontiguousarray(ct, np.uint64)
+    out = np.zeros((2, 1, 1 << logN), np.uint64)
+    lib().or_rescale(logN, _p(ct, _u64p), _p(out, _u64p))
+    return out
+
+
+def rotate(logN, ct, r, gkr):
+    ct = np.ascontiguousarray(ct, np.uint64)
+    out = np.zeros((2, 1, 1 << logN), np.uint64)
+    lib().or_rotate(logN, _p(ct, _u64p), r, _p(np.ascontiguousarray(gkr), _u64p), _p(out, _u64p))
+    return out
+
+
+def moddown(logN, n_q, KS):
+    KS = np.ascontiguousarray(KS, np.uint64)
+    out = np.zeros((n_q, 1 << logN), np.uint64)
+    lib().or_moddown(logN, n_q, _p(KS, _u64p), _p(out, _u64p))
+    return out
+
+
+def match(logN, d, p, order, rlk, gk, db, q, pairs=None, n_threads=1):
+    """Algorithm 2 over (query, set) pairs. db [T][p][2][2][N], q [Q][p][2][2][N].
+    Returns out [n_pairs][2][1][N] and the pairs array."""
+    N = 1 << logN
+    db = np.ascontiguousarray(db, np.uint64)
+    q = np.ascontiguousarray(q, np.uint64)
+    T, Q = db.shape[0], q.shape[0]
+    if pairs is None:
+        pairs = np.array([(j, t) for j in range(Q) for t in range(T)], np.int64).reshape(-1, 2)
+    pairs = np.ascontiguousarray(pairs, np.int64)
+    out = np.zeros((pairs.shape[0], 2, 1, N), np.uint64)
+    gk = np.ascontiguousarray(gk if len(gk) else np.zeros((1, 2, 2, N), np.uint64), np.uint64)
+    rc = lib().or_match(logN, d, p, order, _p(np.ascontiguousarray(rlk), _u64p), _p(gk, _u64p), _p(db, _u64p), T,
+                        _p(q, _u64p), Q, _p(pairs, _i64p), pairs.shape[0], _p(out, _u64p), n_threads)
+    if rc != 0:
+        raise ValueError(f"or_match failed: {rc}")
+    return out, pairs
+
+
+# ---------------------------------------------------------------------------- encode / decode
+def slot_exponents(logN):
+    """e_j = 5^j mod 2N for the S = N/2 slots."""
+    N = 1 << logN
+    e = np.empty(N // 2, np.int64)
+    x = 1
+    for j in range(N // 2):
+        e[j] = x
+        x = (x * 5) % (2 * N)
+    return e
+
+
+def encode(z, logN, scale=DELTA):
+    """Real slot vector(s) z [..., S] -> integer plaintext [..., N] (int64).
+
+    m_k = (2/N) sum_j z_j cos(pi k e_j / N) = (2/N) Re(sum_t X[t] zeta^(k t)), X[e_j] = z_j,
+    evaluated with a 2N-point inverse FFT (library primitive); pt_k = round(scale * m_k),
+    halves away from zero (reading R15)."""
+    N = 1 << logN
+    z = np.asarray(z, np.float64)
+    X = np.zeros(z.shape[:-1] + (2 * N,), np.complex128)
+    X[..., slot_exponents(logN)] = z
+    m = 4.0 * np.fft.ifft(X, axis=-1).real[..., :N]      # (2/N) * 2N * ifft
+    v = scale * m
+    return (np.sign(v) * np.floor(np.abs(v) + 0.5)).astype(np.int64)
+
+
+def encode_direct(z, logN, scale=DELTA):
+    """The same encoding by the O(N*S) direct formula (for small-N pins)."""
+    N = 1 << logN
+    e = slot_exponents(logN)
+    k = np.arange(N)
+    C = np.cos(np.pi * ((k[:, None] * e[None, :]) % (2 * N)) / N)
+    v = scale * (2.0 / N) * (C @ np.asarray(z, np.float64))
+    return (np.sign(v) * np.floor(np.abs(v) + 0.5)).astype(np.int64)
+
+
+def decode_slots(m_centred, logN, scale, slots=None):
+    """z_j = sum_k m_k cos(pi k e_j / N) / scale for the requested slots j (default all)."""
+    N = 1 << logN
+    e = slot_exponents(logN)
+    if slots is not None:
+        e = e[np.asarray(slots)]
+    k = np.arange(N)
+    C = np.cos(np.pi * ((e[:, None] * k[None, :]) % (2 * N)) / N)
+    return (C @ np.asarray(m_centred, np.float64)) / scale
+
+
+def centred(x, q):
+    x = np.asarray(x, np.uint64).astype(object)
+    return np.array([int(v) - q if int(v) > q // 2 else int(v) for v in x.ravel()], dtype=object).reshape(x.shape)
+
+
+def centred_i64(x, q):
+    x = np.asarray(x, np.uint64)
+    half = np.uint64(q // 2)
+    out = x.astype(np.int64)
+    neg = x > half
+    out[neg] = (x[neg] - np.uint64(q)).astype(np.int64)
+    return out
+
+
+# ---------------------------------------------------------------------------- packing (client side)
+def layout(logN, d, p):
+    S = (1 << logN) // 2
+    s = d // p
+    B = S // s
+    return S, s, B
+
+
+def pack_db(tmpl, logN, d, p, first_set, n_sets):
+    """Slot vectors z[t][i][k*s + j] = v_{tB+k}[i*s + j]; zeros past n."""
+    S, s, B = layout(logN, d, p)
+    tmpl = np.asarray(tmpl, np.float64)
+    n = tmpl.shape[0]
+    z = np.zeros((n_sets, p, S))
+    for t in range(n_sets):
+        u0 = (first_set + t) * B
+        cnt = max(0, min(B, n - u0))
+        if cnt == 0:
+            continue
+        blk = tmpl[u0:u0 + cnt].reshape(cnt, p, s)          # [k][i][j]
+        z[t, :, :cnt * s] = blk.transpose(1, 0, 2).reshape(p, cnt * s)
+    return z
+
+
+def pack_query(qv, logN, d, p):
+    """w_i[x] = q[i*s + (x mod s)] for x < S."""
+    S, s, B = layout(logN, d, p)
+    qv = np.asarray(qv, np.float64).reshape(-1, p, s)
+    return np.tile(qv, (1, 1, B))                            # [Q][p][S]
+
+
+def scores_from_output(logN, d, p, sk, out_ct, q0):
+    """Decrypt a level-0 result [2][1][N] and read slot k*s for k < B."""
+    S, s, B = layout(logN, d, p)
+    m = decrypt(logN, sk, out_ct, 1)[0]
+    P = primes()
+    scale = DELTA * DELTA / P[1]
+    return decode_slots(centred_i64(m, q0), logN, scale, slots=np.arange(B) * s)

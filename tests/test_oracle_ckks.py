@@ -1,0 +1,340 @@
+"""Pins for the oracle's CKKS layer and for Algorithm 2 (HE-C^3).
+
+Pins used (each independent of the oracle code path it checks):
+  * encode: direct O(N*S) definition at small N; decode(encode(z)) ~ z; slot j <-> zeta^(5^j)
+  * Dec(Enc(m)) ~ m
+  * ModDown / rescale: Python big-integer closed forms on the CRT lift
+  * relinearization: Dec(relin(d)) - (d0 + d1 s + d2 s^2) is the ModDown rounding term,
+    bounded by (N+1)/2 for error-free keys (exact algebra, see DESIGN.md sec. Oracle)
+  * automorphism == slot rotation: decode(sigma_{5^r}(encode(z))) = rot_left(z, r)
+  * trivial ciphertexts (c1 = 0): the whole scan equals a big-integer closed form
+  * end-to-end: decrypted scores vs float64 cosine (north_star 1e-4, internal guard 1e-6)
+  * SPEC.md worked examples at S = 8 in real CKKS at N = 16
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from paper_2408_06167_b200 import inputs as I
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")
+
+
+def _rot_left(z, r):
+    return np.roll(z, -r, axis=-1)
+
+
+# ----------------------------------------------------------------------------- encoding
+@pytest.mark.parametrize("logN", [3, 5, 7])
+def test_encode_fft_equals_direct_definition(O, logN):
+    S = (1 << logN) // 2
+    z = np.random.default_rng(logN).uniform(-1, 1, S)
+    assert np.array_equal(O.encode(z, logN), O.encode_direct(z, logN))
+
+
+@pytest.mark.parametrize("logN", [4, 13])
+def test_decode_encode_roundtrip(O, logN):
+    S = (1 << logN) // 2
+    z = np.random.default_rng(1).uniform(-1, 1, S)
+    pt = O.encode(z, logN)
+    back = O.decode_slots(pt, logN, O.DELTA)
+    assert np.abs(back - z).max() < 1e-9
+
+
+def test_encoding_evaluates_at_5_power_roots(O):
+    """m(zeta^(5^j)) = z_j: evaluate the real polynomial at the slot roots with complex numbers."""
+    logN = 5
+    N = 1 << logN
+    z = np.random.default_rng(2).uniform(-1, 1, N // 2)
+    m = O.encode(z, logN).astype(np.float64) / O.DELTA
+    for j in range(N // 2):
+        root = np.exp(1j * np.pi * pow(5, j, 2 * N) / N)
+        val = np.polyval(m[::-1], root)
+        assert abs(val.real - z[j]) < 1e-9 and abs(val.imag) < 1e-9
+
+
+# ----------------------------------------------------------------------------- rotation semantics
+@pytest.mark.parametrize("r", [1, 2, 3, 8])
+def test_automorphism_rotates_slots_left(O, r):
+    logN = 6
+    S = 32
+    q0 = O.primes()[0]
+    z = np.random.default_rng(r).uniform(-1, 1, S)
+    pt = O.encode(z, logN)
+    res = np.array([int(x) % q0 for x in pt], np.uint64)
+    g = pow(5, r, 2 << logN)
+    rot = O.automorphism(logN, q0, res, g)
+    back = O.decode_slots(O.centred_i64(rot, q0), logN, O.DELTA)
+    assert np.abs(back - _rot_left(z, r)).max() < 1e-9
+    # rotation by S is the identity (ord(5) = S mod 2N)
+    assert pow(5, S, 2 << logN) == 1
+
+
+# ----------------------------------------------------------------------------- enc / dec
+def test_encrypt_decrypt_roundtrip(O):
+    logN = 13
+    S = 4096
+    sk, pk, rlk, gk = O.keygen(logN, 1, 0)
+    z = np.random.default_rng(4).uniform(-1, 1, (2, S))
+    ct = O.encrypt(logN, pk, O.encode(z, logN), 0, 9)
+    q0 = O.primes()[0]
+    for i in range(2):
+        m = O.decrypt(logN, sk, ct[i], 2)
+        back = O.decode_slots(O.centred_i64(m[0], q0), logN, O.DELTA)
+        assert np.abs(back - z[i]).max() < 1e-6
+
+
+def test_public_key_relation(O):
+    """pk = (b, a) with b + a s = e small (RLWE sample)."""
+    logN = 8
+    sk, pk, rlk, gk = O.keygen(logN, 5, 2)
+    for l in range(2):
+        q = O.primes()[l]
+        s = np.array([int(x) % q for x in sk], np.uint64)
+        e = (pk[0, l].astype(object) + O.poly_mul(logN, q, pk[1, l], s).astype(object)) % q
+        e = [int(x) - q if int(x) > q // 2 else int(x) for x in e]
+        assert max(abs(x) for x in e) <= 19
+
+
+# ----------------------------------------------------------------------------- ModDown / rescale closed forms
+def _crt(res, mods):
+    M = 1
+    for m in mods:
+        M *= m
+    x = 0
+    for r, m in zip(res, mods):
+        Mi = M // m
+        x += int(r) * Mi * pow(Mi, -1, m)
+    return x % M
+
+
+def _cent(x, m):
+    x %= m
+    return x - m if x > m // 2 else x
+
+
+def test_moddown_closed_form(O):
+    """ModDown(X) = (X - c_P(X)) / P mod Q for the CRT lift X (SURVEY.md sec. 8c pins)."""
+    q0, q1, P = O.primes()
+    logN = 4
+    N = 16
+    rnd = random.Random(7)
+    KS = np.array([[rnd.randrange(m) for _ in range(N)] for m in (q0, q1, P)], np.uint64)
+    got = O.moddown(logN, 2, KS)
+    for k in range(N):
+        X = _crt([KS[0, k], KS[1, k], KS[2, k]], [q0, q1, P])
+        y = (X - _cent(X, P)) // P
+        assert (X - _cent(X, P)) % P == 0
+        assert int(got[0, k]) == y % q0 and int(got[1, k]) == y % q1
+
+
+def test_rescale_closed_form(O):
+    """Res: (X - c_q1(X)) / q1 mod q0 for X = CRT(c[q0], c[q1]) (round to nearest, reading R5)."""
+    q0, q1, P = O.primes()
+    logN = 4
+    N = 16
+    rnd = random.Random(8)
+    ct = np.array([[[rnd.randrange(m) for _ in range(N)] for m in (q0, q1)] for _ in range(2)], np.uint64)
+    got = O.rescale(logN, ct)
+    for c in range(2):
+        for k in range(N):
+            X = _crt([ct[c, 0, k], ct[c, 1, k]], [q0, q1])
+            y = (X - _cent(X, q1)) // q1
+            assert int(got[c, 0, k]) == y % q0
+            # same thing as round(X / q1) on the centred integer (no ties: q1 odd)
+            Xc = _cent(X, q0 * q1)
+            assert (Xc - _cent(Xc, q1)) // q1 % q0 == y % q0
+
+
+# ----------------------------------------------------------------------------- key switching
+def _negacyclic_big(a, b):
+    n = len(a)
+    c = [0] * n
+    for i in range(n):
+        if a[i] == 0:
+            continue
+        for j in range(n):
+            if i + j < n:
+                c[i + j] += a[i] * b[j]
+            else:
+                c[i + j - n] -= a[i] * b[j]
+    return c
+
+
+@pytest.mark.parametrize("zero_error,bound", [(True, None), (False, 2 ** 20)])
+def test_relinearization_identity(O, zero_error, bound):
+    """c0' + c1' s = d0 + d1 s + d2 s^2 + e (mod Q) with e the ModDown rounding term:
+    |e| <= (N+1)/2 exactly for error-free keys; small for sigma = 3.2 keys."""
+    logN = 5
+    N = 32
+    q0, q1, P = O.primes()
+    sk, pk, rlk, gk = O.keygen(logN, 3, 0, zero_error=zero_error)
+    rnd = random.Random(9)
+    d = np.array([[[rnd.randrange(m) for _ in range(N)] for m in (q0, q1)] for _ in range(3)], np.uint64)
+    out = O.relinearize(logN, d, rlk)
+    Q = q0 * q1
+    lift = lambda arr: [_crt([arr[0][k], arr[1][k]], [q0, q1]) for k in range(N)]
+    s = [int(x) for x in sk]
+    s2 = _negacyclic_big(s, s)
+    D = [lift(d[i]) for i in range(3)]
+    C = [lift(out[i]) for i in range(2)]
+    lhs = [(C[0][k] + v) for k, v in enumerate(_negacyclic_big(C[1], s))]
+    rhs_1 = _negacyclic_big(D[1], s)
+    rhs_2 = _negacyclic_big(D[2], s2)
+    e = [_cent(lhs[k] - D[0][k] - rhs_1[k] - rhs_2[k], Q) for k in range(N)]
+    lim = (N + 1) // 2 if bound is None else bound
+    assert max(abs(x) for x in e) <= lim
+    # a plausible mistake (wrong gadget digit / sign) makes e of size ~Q: make sure e is not trivially 0
+    assert any(x != 0 for x in e) or zero_error
+
+
+def test_rotation_keyswitch_decrypts_to_rotated_slots(O):
+    logN = 6
+    S = 32
+    q0 = O.primes()[0]
+    sk, pk, rlk, gk = O.keygen(logN, 4, 3)
+    z = np.random.default_rng(5).uniform(-1, 1, S)
+    ct = O.encrypt(logN, pk, O.encode(z[None], logN), 0, 1)[0]
+    # drop to level 0 by keeping the q0 limb (valid ciphertext mod q0 at scale Delta)
+    ct0 = np.ascontiguousarray(ct[:, :1, :])
+    for i, r in enumerate((1, 2, 4)):
+        rot = O.rotate(logN, ct0, r, gk[i])
+        m = O.decrypt(logN, sk, rot, 1)[0]
+        back = O.decode_slots(O.centred_i64(m, q0), logN, O.DELTA)
+        assert np.abs(back - _rot_left(z, r)).max() < 1e-6
+
+
+# ----------------------------------------------------------------------------- trivial-ciphertext closed form
+def _trivial(pt_list, q0, q1, N):
+    """(pt, 0) as a level-1 ciphertext."""
+    ct = np.zeros((len(pt_list), 2, 2, N), np.uint64)
+    for i, pt in enumerate(pt_list):
+        ct[i, 0, 0] = [int(v) % q0 for v in pt]
+        ct[i, 0, 1] = [int(v) % q1 for v in pt]
+    return ct
+
+
+def _sigma_int(a, g):
+    n = len(a)
+    out = [0] * n
+    for k, v in enumerate(a):
+        t = k * g % (2 * n)
+        if t < n:
+            out[t] += v
+        else:
+            out[t - n] -= v
+    return out
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_trivial_ciphertext_scan_closed_form(O, order):
+    """With c1 = 0 every key switch vanishes, so HE-C^3 reduces to integer arithmetic:
+    hoisted:  C = round(sum_i pt_u,i * pt_s,i / q1) mod q0
+    paper:    C = sum_i round(pt_u,i * pt_s,i / q1) mod q0
+    then      out = sum_{delta < s} sigma_{5^delta}(C) mod q0"""
+    logN, d, p = 6, 16, 2              # N = 64, S = 32, s = 8, B = 4
+    N = 1 << logN
+    q0, q1, P = O.primes()
+    s = d // p
+    sk, pk, rlk, gk = O.keygen(logN, 6, O.n_rot_for(d, p))
+    rnd = random.Random(11)
+    pu = [[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(p)]
+    ps = [[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(p)]
+    qct = _trivial(pu, q0, q1, N)[None]
+    sct = _trivial(ps, q0, q1, N)[None]
+    out, _ = O.match(logN, d, p, order, rlk, gk, sct, qct)
+
+    def rnd_div(x, m):  # (X - c_m(X)) / m, the rescale rounding on true integers (|X| < Q/2)
+        return (x - _cent(x, m)) // m
+
+    prods = [_negacyclic_big(pu[i], ps[i]) for i in range(p)]
+    if order == 0:
+        tot = [sum(pr[k] for pr in prods) for k in range(N)]
+        C = [rnd_div(v, q1) for v in tot]
+    else:
+        C = [sum(rnd_div(pr[k], q1) for pr in prods) for k in range(N)]
+    acc = [0] * N
+    for delta in range(s):
+        sg = _sigma_int(C, pow(5, delta, 2 * N))
+        acc = [a + b for a, b in zip(acc, sg)]
+    exp = [v % q0 for v in acc]
+    assert [int(x) for x in out[0, 0, 0]] == exp
+    assert not out[0, 1].any()
+
+
+# ----------------------------------------------------------------------------- end to end
+def _run_scan(O, logN, d, p, tmpl, qv, order=0, key_seed=1, n_threads=4):
+    S, s, B = O.layout(logN, d, p)
+    n_sets = -(-tmpl.shape[0] // B)
+    sk, pk, rlk, gk = O.keygen(logN, key_seed, O.n_rot_for(d, p))
+    zdb = O.pack_db(tmpl, logN, d, p, 0, n_sets)
+    zq = O.pack_query(qv, logN, d, p)
+    db = O.encrypt(logN, pk, O.encode(zdb.reshape(-1, S), logN), 0, 2).reshape(n_sets, p, 2, 2, -1)
+    qc = O.encrypt(logN, pk, O.encode(zq.reshape(-1, S), logN), 0, 3).reshape(len(qv), p, 2, 2, -1)
+    out, pairs = O.match(logN, d, p, order, rlk, gk, db, qc, n_threads=n_threads)
+    q0 = O.primes()[0]
+    scores = np.zeros((len(qv), n_sets * B))
+    for i, (j, t) in enumerate(pairs):
+        scores[j, t * B:(t + 1) * B] = O.scores_from_output(logN, d, p, sk, out[i], q0)
+    return scores[:, :tmpl.shape[0]], out
+
+
+def test_config1_end_to_end(O):
+    """BASELINE.json configs[0]: d=16, p=1, 256 templates, query = T[17] + noise -> top-1 17."""
+    T = I.templates(1)
+    Q, exp = I.queries(1)
+    sc, _ = _run_scan(O, 13, 16, 1, T, Q)
+    ref = Q @ T.T
+    assert np.abs(sc - ref).max() < 1e-6      # internal guard (north_star contract: 1e-4)
+    assert sc.argmax() == ref.argmax() == 17
+
+
+def test_orders_coincide_for_p1_and_agree_in_value(O):
+    logN, d = 8, 8                          # N = 256, S = 128
+    T = I.random_unit(40, d, 1)
+    Q = I.random_unit(2, d, 2)
+    a, oa = _run_scan(O, logN, d, 1, T, Q, order=0)
+    b, ob = _run_scan(O, logN, d, 1, T, Q, order=1)
+    assert np.array_equal(oa, ob)           # p = 1: one relin + rescale either way
+    c, oc = _run_scan(O, logN, d, 4, T, Q, order=0)
+    e, oe = _run_scan(O, logN, d, 4, T, Q, order=1)
+    ref = Q @ T.T
+    for x in (a, c, e):
+        assert np.abs(x - ref).max() < 1e-6
+    assert not np.array_equal(oc, oe)       # residues differ across orders (reading R8)
+
+
+def _spec():
+    with open(GOLD) as f:
+        return json.load(f)
+
+
+def test_spec_layout_examples(O):
+    g = _spec()
+    lay = g["layout"]
+    S, s, B = O.layout(4, lay["m"], lay["N_in"])
+    assert (S, s, B) == (lay["S"], lay["s"], lay["B"])
+    en = g["enroll"]
+    tm = np.zeros((2, 4))
+    tm[en["index"]] = en["vector"]
+    z = O.pack_db(tm, 4, 4, 2, 0, 1)[0]
+    assert np.allclose(z[0], en["ct0"]) and np.allclose(z[1], en["ct1"])
+    ex = g["expand"]
+    w = O.pack_query(np.array([ex["query"]]), 4, 4, 2)[0]
+    assert np.allclose(w[0], ex["out0"]) and np.allclose(w[1], ex["out1"])
+    pc = g["paper_capacity"]
+    assert pc["paper_slots"] * pc["N_in"] // pc["m"] == pc["B_paper"]
+    # reading R1: standard ring, S = N/2 slots -> half the paper's capacity
+    assert O.layout(13, pc["m"], pc["N_in"])[2] == pc["B_paper"] // 2
+
+
+def test_spec_match_example_N16(O):
+    g = _spec()["match"]
+    T = np.array(g["enrolled"], np.float64)
+    Q = np.array([g["query"]], np.float64)
+    sc, out = _run_scan(O, 4, 4, 2, T, Q)
+    # slot 0 = block 0 (template 0), slot 2 = block 1 (template 1)
+    assert abs(sc[0, 0] - g["slot0"]) < 1e-6 and abs(sc[0, 1] - g["slot2"]) < 1e-6
