@@ -1,0 +1,191 @@
+/*
+ * blindmatch.h -- C ABI of the B200-native Blind-Match encrypted 1:N cosine scan.
+ *
+ * The method is HE-C^3 (Algorithm 2) in RNS-CKKS with
+ *   N = 8192 (S = N/2 = 4096 real slots, reading R1),
+ *   q0 = 2^58-835583, q1 = 2^40-147455, special prime P = 2^60-16383
+ *   (largest primes below 2^k with q = 1 mod 16384; BASELINE.json configs[0]),
+ *   scale 2^40, ternary secret, discrete Gaussian errors sigma = 3.2.
+ * The client packs/encrypts, the server scans,
+ * the client decrypts and takes the argmax.
+ *
+ * Conventions (all functions):
+ *  - return 0 (BM_OK) or a negative bm_status; bm_strerror() names it.
+ *  - "host" pointers are ordinary CPU memory, "device" pointers are CUDA device memory
+ *    of the current device (e.g. torch tensors' data_ptr()); all are caller-owned unless
+ *    a function returns a library handle (free it with the matching *_free).
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  Device
+ *    functions are asynchronous and stream-ordered; kernel faults surface at bm_sync().
+ *  - residues are uint64 in [0, q).  Coefficient-domain ("canonical") layouts are
+ *    limb-major: a level-1 ciphertext is [2 comps][2 limbs q0,q1][N], a level-0 one
+ *    [2][1][N].  NTT-domain ("device") layouts have the same shape, with the library's
+ *    internal evaluation order; convert with bm_ct_to_coeff / bm_ct_from_coeff.
+ *  - there is no CPU fallback: device functions fail with BM_ERR_CUDA without a GPU.
+ */
+#ifndef BLINDMATCH_H
+#define BLINDMATCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_LOGN 13
+#define BM_N 8192
+#define BM_SLOTS 4096
+
+typedef enum {
+    BM_OK = 0,
+    BM_ERR_INVALID_ARG = -1,          /* null pointer, negative count, bad enum              */
+    BM_ERR_INVALID_LAYOUT = -2,       /* d, p not powers of two, p > d, d > S  */
+    BM_ERR_INSECURE_PARAMS = -3,      /* log2(q0 q1 P) above the 128-bit bound */
+    BM_ERR_INVALID_PRIME = -4,        /* a modulus is not an NTT-friendly prime              */
+    BM_ERR_CUDA = -5,                 /* CUDA runtime / kernel error, or no device           */
+    BM_ERR_OOM = -6,                  /* device allocation failed                             */
+    BM_ERR_ZERO_VECTOR = -7,          /* a template/query has zero norm        */
+    BM_ERR_MAGNITUDE = -8,            /* non-finite input value                */
+    BM_ERR_CAPACITY = -9,             /* templates do not fit in the given sets              */
+    BM_ERR_LEVEL = -10,               /* wrong ciphertext level for the op      */
+    BM_ERR_MISSING_ROTATION_KEY = -11,/* evk lacks a Galois key the layout needs */
+    BM_ERR_KEY_MISMATCH = -12,        /* key / params digest mismatch          */
+    BM_ERR_WORKSPACE = -13            /* workspace smaller than bm_match_ws_bytes()           */
+} bm_status;
+
+typedef enum {
+    BM_ORDER_HOISTED = 0, /* sum_i tensor_i, then one relin + one rescale (reading R8) */
+    BM_ORDER_PAPER = 1    /* per part Res(Mul(C_u,i, C_s,i)), then Add at level 0 */
+} bm_order;
+
+/* Scheme parameters and the packing layout:
+ * d = feature size (paper's m), p = parts (paper's N_in), s = d/p, B = S/s templates per set,
+ * log_s = log2 s ladder steps, Galois keys for rotations 2^i, i < log_s. */
+typedef struct bm_params {
+    int32_t logN, N, slots;
+    int32_t d, p, s, B, log_s;
+    uint64_t q[3];          /* q0, q1, P                               */
+    double scale;           /* 2^40                                    */
+    double out_scale;       /* 2^80 / q1: scale of bm_match outputs    */
+    uint8_t digest[32];     /* digest of (N, primes, scale, d, p)      */
+} bm_params;
+
+typedef struct bm_sk bm_sk;           /* host: ternary secret (client only)              */
+typedef struct bm_pk bm_pk;           /* host: public key (b, a) over {q0,q1}             */
+typedef struct bm_evk bm_evk;         /* host: relinearization key + Galois keys          */
+typedef struct bm_pk_dev bm_pk_dev;   /* device copy of pk (NTT domain)                   */
+typedef struct bm_evk_dev bm_evk_dev; /* device copy of evk (NTT domain)                  */
+
+/* Fill *out for feature size d and part count p (both powers of two, 1 <= p <= d <= 4096).
+ * Errors: BM_ERR_INVALID_ARG (out null), BM_ERR_INVALID_LAYOUT, BM_ERR_INVALID_PRIME,
+ * BM_ERR_INSECURE_PARAMS. */
+int bm_params_init(bm_params *out, int32_t d, int32_t p);
+
+/* Key generation, host, deterministic in `seed`.
+ * sk: s ternary.  pk = (-a s + e, a) over {q0,q1}.  rlk_j, j in {0,1}, over {q0,q1,P}:
+ * (-a s + e + [k=j](P mod q_k) s^2, a).  gk_i (rotation 2^i, i < log_s) over {q0,P}:
+ * (-a s + e + (P mod q0) sigma_{5^(2^i)}(s) [q0 limb only], a).  Any of sk/pk/evk may be
+ * NULL to skip returning it.  Randomness: ChaCha20 streams (reading R14). */
+int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **sk, bm_pk **pk, bm_evk **evk);
+void bm_sk_free(bm_sk *);
+void bm_pk_free(bm_pk *);
+void bm_evk_free(bm_evk *);
+
+/* Canonical (coefficient-domain) exports.  sk: int8[N].  pk: [2][2][N].
+ * rlk: [2 digits][2 comps][3 limbs q0,q1,P][N].  gk: [log_s][2][2 limbs q0,P][N]
+ * (gk may be NULL; *n_rot receives log_s when non-NULL). */
+int bm_sk_export(const bm_sk *, int8_t *out);
+int bm_pk_export(const bm_pk *, uint64_t *out);
+int bm_evk_export(const bm_evk *, uint64_t *rlk, uint64_t *gk, int32_t *n_rot);
+/* Build host keys from canonical arrays (e.g. keys received over the network). */
+int bm_sk_import(const bm_params *, const int8_t *in, bm_sk **out);
+int bm_pk_import(const bm_params *, const uint64_t *in, bm_pk **out);
+int bm_evk_import(const bm_params *, const uint64_t *rlk, const uint64_t *gk, int32_t n_rot, bm_evk **out);
+
+/* Upload keys to the current device (NTT domain + Shoup companions).  Synchronous.
+ * Errors: BM_ERR_CUDA, BM_ERR_OOM, BM_ERR_KEY_MISMATCH (evk built for other params). */
+int bm_pk_to_device(const bm_params *, const bm_pk *, bm_pk_dev **out);
+int bm_evk_to_device(const bm_params *, const bm_evk *, bm_evk_dev **out);
+void bm_pk_dev_free(bm_pk_dev *);
+void bm_evk_dev_free(bm_evk_dev *);
+
+/* Client-side packing + CKKS encoding (host, FP64).
+ * bm_encode_db: templates tmpl[n][d] (host, row-major; each normalised to unit L2 norm)
+ *   -> pt[n_sets][p][N] int64, for sets first_set .. first_set+n_sets-1 (global set t holds
+ *   templates tB .. tB+B-1; template u = tB+k occupies slots k*s .. k*s+s-1 of part i with
+ *   v[i*s .. i*s+s-1]; empty blocks are zero).  n counts ALL templates (global indexing).
+ * bm_encode_query: q[nq][d] -> pt[nq][p][N], part i holds w_i[x] = q[i*s + (x mod s)].
+ * Encoding: m_k = (2/N) sum_j z_j cos(pi k 5^j / N), pt_k = round(2^40 m_k) (reading R15).
+ * Errors: BM_ERR_ZERO_VECTOR, BM_ERR_MAGNITUDE, BM_ERR_INVALID_ARG. */
+int bm_encode_db(const bm_params *, const double *tmpl, int64_t n, int64_t first_set, int64_t n_sets, int64_t *pt);
+int bm_encode_query(const bm_params *, const double *q, int64_t nq, int64_t *pt);
+
+/* Public-key encryption on the device: for c < n_cts, object o = first_obj + c,
+ * ct_o = (u b + e0 + pt_c, u a + e1) over {q0,q1} with u ternary, e0, e1 Gaussian drawn
+ * from ChaCha20 streams (seed, purpose, o).  d_pt: device int64 [n_cts][N];
+ * d_out: device uint64 [n_cts][2][2][N], NTT domain.  DB objects are numbered
+ * set*p + part, query objects query*p + part, so shards encrypt bit-identically. */
+int bm_encrypt(const bm_params *, const bm_pk_dev *, const int64_t *d_pt, int64_t n_cts, uint64_t first_obj,
+               uint64_t seed, uint64_t *d_out, void *stream);
+/* Convenience: bm_encode_db / bm_encode_query on the host, upload, bm_encrypt.
+ * Blocks until the upload of the plaintexts is done. */
+int bm_encrypt_db(const bm_params *, const bm_pk_dev *, const double *tmpl, int64_t n, int64_t first_set,
+                  int64_t n_sets, uint64_t seed, uint64_t *d_out, void *stream);
+int bm_encrypt_query(const bm_params *, const bm_pk_dev *, const double *q, int64_t nq, int64_t first_query,
+                     uint64_t seed, uint64_t *d_out, void *stream);
+
+/* Domain conversion of n_cts ciphertexts with n_limbs limbs (1 or 2; limbs q0[,q1]),
+ * layout [n_cts][2][n_limbs][N], device in/out (may alias). */
+int bm_ct_to_coeff(const bm_params *, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
+                   void *stream);
+int bm_ct_from_coeff(const bm_params *, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
+                     void *stream);
+
+/* THE HOT PATH: HE-C^3 scan of nq queries against n_sets sets.
+ * d_db:  device [n_sets][p][2][2][N] level-1 NTT-domain DB (bm_encrypt output);
+ * d_q:   device [nq][p][2][2][N] level-1 NTT-domain query parts (client-expanded, reading R10);
+ * d_out: device [nq][n_sets][2][N] level-0 results, COEFFICIENT domain (canonical), scale
+ *        prm->out_scale; slot k*s of (query j, set t) decrypts to cos(q_j, v_{tB+k}).
+ * d_ws:  device workspace of at least bm_match_ws_bytes(prm, n_sets, nq, order) bytes.
+ * Per (query, set): tensor + sum over parts (a4), relinearize (a5), rescale (a6), log2(s)
+ * rotate-and-add steps (a7), all in sm_100a kernels on `stream`; allocates nothing.
+ * Errors: BM_ERR_INVALID_ARG, BM_ERR_MISSING_ROTATION_KEY, BM_ERR_KEY_MISMATCH,
+ * BM_ERR_WORKSPACE, BM_ERR_CUDA (launch errors; faults at bm_sync). nq = 0 or n_sets = 0
+ * is a no-op. */
+size_t bm_match_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);
+int bm_match(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+             int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
+
+/* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
+ * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call, chunked so the
+ * copies overlap the kernels.  Pinned host memory is strongly recommended.  d_ws must hold
+ * bm_match_host_ws_bytes(...) bytes.  Synchronous (returns after h_out is written). */
+size_t bm_match_host_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);
+int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *h_q,
+                  int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
+
+/* Per-kernel-class device time of the last bm_match on this thread when profiling is
+ * enabled (bm_set_profiling(1)); classes: 0 tensor+INTT, 1 ModUp NTT, 2 key-switch INTT,
+ * 3 rescale NTT, 4 rotation digit, 5 rotation key-switch, 6 output INTT.  ms[7] and
+ * launches[7] accumulate until bm_profile_reset(). */
+void bm_set_profiling(int32_t on);
+void bm_profile_reset(void);
+int bm_profile_read(double *ms, int64_t *launches, int64_t *units);
+
+/* Client side (host): decrypt level-0 results h_ct [n][2][1][N] (canonical) and decode the
+ * B scores at slots k*s into scores[n][B].  bm_decrypt_raw returns the
+ * centred message coefficients m = c0 + c1 s mod q0 as int64 [n][N]. */
+int bm_decrypt(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, double *scores);
+int bm_decrypt_raw(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, int64_t *m);
+/* argmax with the lowest index winning ties. */
+int bm_top1(const double *scores, int64_t n, int64_t *idx, double *best);
+
+int bm_sync(void *stream);
+const char *bm_strerror(int status);
+/* Library build information ("sm_100a", git hash...) */
+const char *bm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

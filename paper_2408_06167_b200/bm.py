@@ -1,0 +1,340 @@
+"""Thin ctypes binding of libblindmatch (include/blindmatch.h).  Argument marshalling only:
+every step of the scan runs in the library's sm_100a kernels.  PyTorch supplies device
+memory (tensor.data_ptr()) and streams (torch.cuda.current_stream().cuda_stream).
+
+Importing this module fails loudly if libblindmatch.so is missing: there is no CPU fallback.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libblindmatch.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2408_06167_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+N = 8192
+SLOTS = 4096
+ORDER_HOISTED = 0
+ORDER_PAPER = 1
+
+BM_OK = 0
+ERRORS = {
+    -1: "BM_ERR_INVALID_ARG", -2: "BM_ERR_INVALID_LAYOUT", -3: "BM_ERR_INSECURE_PARAMS", -4: "BM_ERR_INVALID_PRIME",
+    -5: "BM_ERR_CUDA", -6: "BM_ERR_OOM", -7: "BM_ERR_ZERO_VECTOR", -8: "BM_ERR_MAGNITUDE", -9: "BM_ERR_CAPACITY",
+    -10: "BM_ERR_LEVEL", -11: "BM_ERR_MISSING_ROTATION_KEY", -12: "BM_ERR_KEY_MISMATCH", -13: "BM_ERR_WORKSPACE",
+}
+
+
+class BMError(RuntimeError):
+    def __init__(self, code, fn):
+        self.code = code
+        self.name = ERRORS.get(code, str(code))
+        super().__init__(f"{fn}: {self.name} ({_lib.bm_strerror(code).decode()})")
+
+
+class bm_params(ctypes.Structure):
+    _fields_ = [("logN", ctypes.c_int32), ("N", ctypes.c_int32), ("slots", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("p", ctypes.c_int32), ("s", ctypes.c_int32), ("B", ctypes.c_int32),
+                ("log_s", ctypes.c_int32), ("q", ctypes.c_uint64 * 3), ("scale", ctypes.c_double),
+                ("out_scale", ctypes.c_double), ("digest", ctypes.c_uint8 * 32)]
+
+
+_vp = ctypes.c_void_p
+_i32, _i64, _u64, _sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+_P = ctypes.POINTER(bm_params)
+_pp = ctypes.POINTER(ctypes.c_void_p)
+
+_SIGS = {
+    "bm_params_init": (_i32, [_P, _i32, _i32]),
+    "bm_keygen": (_i32, [_P, _u64, _pp, _pp, _pp]),
+    "bm_sk_free": (None, [_vp]), "bm_pk_free": (None, [_vp]), "bm_evk_free": (None, [_vp]),
+    "bm_sk_export": (_i32, [_vp, _vp]), "bm_pk_export": (_i32, [_vp, _vp]),
+    "bm_evk_export": (_i32, [_vp, _vp, _vp, ctypes.POINTER(_i32)]),
+    "bm_sk_import": (_i32, [_P, _vp, _pp]), "bm_pk_import": (_i32, [_P, _vp, _pp]),
+    "bm_evk_import": (_i32, [_P, _vp, _vp, _i32, _pp]),
+    "bm_pk_to_device": (_i32, [_P, _vp, _pp]), "bm_evk_to_device": (_i32, [_P, _vp, _pp]),
+    "bm_pk_dev_free": (None, [_vp]), "bm_evk_dev_free": (None, [_vp]),
+    "bm_encode_db": (_i32, [_P, _vp, _i64, _i64, _i64, _vp]),
+    "bm_encode_query": (_i32, [_P, _vp, _i64, _vp]),
+    "bm_encrypt": (_i32, [_P, _vp, _vp, _i64, _u64, _u64, _vp, _vp]),
+    "bm_encrypt_db": (_i32, [_P, _vp, _vp, _i64, _i64, _i64, _u64, _vp, _vp]),
+    "bm_encrypt_query": (_i32, [_P, _vp, _vp, _i64, _i64, _u64, _vp, _vp]),
+    "bm_ct_to_coeff": (_i32, [_P, _vp, _i64, _i32, _vp, _vp]),
+    "bm_ct_from_coeff": (_i32, [_P, _vp, _i64, _i32, _vp, _vp]),
+    "bm_match_ws_bytes": (_sz, [_P, _i64, _i32, _i32]),
+    "bm_match": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _i32, _vp]),
+    "bm_match_host_ws_bytes": (_sz, [_P, _i64, _i32, _i32]),
+    "bm_match_host": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _i32, _vp]),
+    "bm_set_profiling": (None, [_i32]), "bm_profile_reset": (None, []),
+    "bm_profile_read": (_i32, [_vp, _vp, _vp]),
+    "bm_decrypt": (_i32, [_P, _vp, _vp, _i64, _vp]),
+    "bm_decrypt_raw": (_i32, [_P, _vp, _vp, _i64, _vp]),
+    "bm_top1": (_i32, [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
+    "bm_sync": (_i32, [_vp]),
+    "bm_strerror": (ctypes.c_char_p, [_i32]),
+    "bm_build_info": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = sorted(_SIGS)
+
+
+def _chk(rc, fn):
+    if rc != BM_OK:
+        raise BMError(rc, fn)
+
+
+def _np_ptr(a):
+    assert a.flags["C_CONTIGUOUS"]
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _dptr(t):
+    """device pointer of a contiguous CUDA tensor"""
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# --------------------------------------------------------------------------- handles
+class _Handle:
+    _free = None
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if self.ptr and self._free is not None:
+            getattr(_lib, self._free)(self.ptr)
+            self.ptr = None
+
+
+class SecretKey(_Handle):
+    _free = "bm_sk_free"
+
+
+class PublicKey(_Handle):
+    _free = "bm_pk_free"
+
+
+class EvalKey(_Handle):
+    _free = "bm_evk_free"
+
+
+class PublicKeyDev(_Handle):
+    _free = "bm_pk_dev_free"
+
+
+class EvalKeyDev(_Handle):
+    _free = "bm_evk_dev_free"
+
+
+# --------------------------------------------------------------------------- API (same names as the C ABI)
+def bm_params_init(d, p):
+    prm = bm_params()
+    _chk(_lib.bm_params_init(ctypes.byref(prm), d, p), "bm_params_init")
+    return prm
+
+
+def bm_keygen(prm, seed):
+    sk, pk, evk = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _chk(_lib.bm_keygen(ctypes.byref(prm), seed, ctypes.byref(sk), ctypes.byref(pk), ctypes.byref(evk)), "bm_keygen")
+    return SecretKey(sk), PublicKey(pk), EvalKey(evk)
+
+
+def bm_sk_export(sk):
+    out = np.zeros(N, np.int8)
+    _chk(_lib.bm_sk_export(sk.ptr, _np_ptr(out)), "bm_sk_export")
+    return out
+
+
+def bm_pk_export(pk):
+    out = np.zeros((2, 2, N), np.uint64)
+    _chk(_lib.bm_pk_export(pk.ptr, _np_ptr(out)), "bm_pk_export")
+    return out
+
+
+def bm_evk_export(evk):
+    n = _i32()
+    _chk(_lib.bm_evk_export(evk.ptr, None, None, ctypes.byref(n)), "bm_evk_export")
+    rlk = np.zeros((2, 2, 3, N), np.uint64)
+    gk = np.zeros((max(n.value, 1), 2, 2, N), np.uint64)
+    _chk(_lib.bm_evk_export(evk.ptr, _np_ptr(rlk), _np_ptr(gk), ctypes.byref(n)), "bm_evk_export")
+    return rlk, gk[:n.value]
+
+
+def bm_sk_import(prm, s):
+    out = ctypes.c_void_p()
+    s = np.ascontiguousarray(s, np.int8)
+    _chk(_lib.bm_sk_import(ctypes.byref(prm), _np_ptr(s), ctypes.byref(out)), "bm_sk_import")
+    return SecretKey(out)
+
+
+def bm_pk_import(prm, v):
+    out = ctypes.c_void_p()
+    v = np.ascontiguousarray(v, np.uint64)
+    _chk(_lib.bm_pk_import(ctypes.byref(prm), _np_ptr(v), ctypes.byref(out)), "bm_pk_import")
+    return PublicKey(out)
+
+
+def bm_evk_import(prm, rlk, gk):
+    out = ctypes.c_void_p()
+    rlk = np.ascontiguousarray(rlk, np.uint64)
+    gk = np.ascontiguousarray(gk, np.uint64)
+    n = gk.shape[0] if gk.ndim == 4 else 0
+    _chk(_lib.bm_evk_import(ctypes.byref(prm), _np_ptr(rlk), _np_ptr(gk) if n else None, n, ctypes.byref(out)),
+         "bm_evk_import")
+    return EvalKey(out)
+
+
+def bm_pk_to_device(prm, pk):
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_pk_to_device(ctypes.byref(prm), pk.ptr, ctypes.byref(out)), "bm_pk_to_device")
+    return PublicKeyDev(out)
+
+
+def bm_evk_to_device(prm, evk):
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_evk_to_device(ctypes.byref(prm), evk.ptr, ctypes.byref(out)), "bm_evk_to_device")
+    return EvalKeyDev(out)
+
+
+def bm_encode_db(prm, tmpl, first_set, n_sets):
+    tmpl = np.ascontiguousarray(tmpl, np.float64)
+    out = np.zeros((n_sets, prm.p, N), np.int64)
+    _chk(_lib.bm_encode_db(ctypes.byref(prm), _np_ptr(tmpl), tmpl.shape[0], first_set, n_sets, _np_ptr(out)),
+         "bm_encode_db")
+    return out
+
+
+def bm_encode_query(prm, q):
+    q = np.ascontiguousarray(q, np.float64)
+    out = np.zeros((q.shape[0], prm.p, N), np.int64)
+    _chk(_lib.bm_encode_query(ctypes.byref(prm), _np_ptr(q), q.shape[0], _np_ptr(out)), "bm_encode_query")
+    return out
+
+
+def bm_encrypt(prm, pk_dev, d_pt, first_obj, seed, d_out, stream=None):
+    """d_pt: CUDA int64 [n][N]; d_out: CUDA uint64/int64 [n][2][2][N] (NTT domain)."""
+    n = d_pt.shape[0]
+    _chk(_lib.bm_encrypt(ctypes.byref(prm), pk_dev.ptr, _dptr(d_pt), n, first_obj, seed, _dptr(d_out),
+                         _stream(stream)), "bm_encrypt")
+
+
+def bm_encrypt_db(prm, pk_dev, tmpl, first_set, n_sets, seed, d_out, stream=None):
+    tmpl = np.ascontiguousarray(tmpl, np.float64)
+    _chk(_lib.bm_encrypt_db(ctypes.byref(prm), pk_dev.ptr, _np_ptr(tmpl), tmpl.shape[0], first_set, n_sets, seed,
+                            _dptr(d_out), _stream(stream)), "bm_encrypt_db")
+
+
+def bm_encrypt_query(prm, pk_dev, q, first_query, seed, d_out, stream=None):
+    q = np.ascontiguousarray(q, np.float64)
+    _chk(_lib.bm_encrypt_query(ctypes.byref(prm), pk_dev.ptr, _np_ptr(q), q.shape[0], first_query, seed,
+                               _dptr(d_out), _stream(stream)), "bm_encrypt_query")
+
+
+def bm_ct_to_coeff(prm, d_in, n_limbs, d_out, stream=None):
+    _chk(_lib.bm_ct_to_coeff(ctypes.byref(prm), _dptr(d_in), d_in.numel() // (2 * n_limbs * N), n_limbs, _dptr(d_out),
+                             _stream(stream)), "bm_ct_to_coeff")
+
+
+def bm_ct_from_coeff(prm, d_in, n_limbs, d_out, stream=None):
+    _chk(_lib.bm_ct_from_coeff(ctypes.byref(prm), _dptr(d_in), d_in.numel() // (2 * n_limbs * N), n_limbs,
+                               _dptr(d_out), _stream(stream)), "bm_ct_from_coeff")
+
+
+def bm_match_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):
+    return int(_lib.bm_match_ws_bytes(ctypes.byref(prm), n_sets, nq, order))
+
+
+def bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, d_ws, order=ORDER_HOISTED, stream=None):
+    ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
+    _chk(_lib.bm_match(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
+                       _dptr(d_q) if nq else None, nq, _dptr(d_out) if nq * n_sets else None,
+                       _dptr(d_ws) if ws_bytes else None, ws_bytes, order, _stream(stream)), "bm_match")
+
+
+def bm_match_host_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):
+    return int(_lib.bm_match_host_ws_bytes(ctypes.byref(prm), n_sets, nq, order))
+
+
+def bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, d_ws, order=ORDER_HOISTED, stream=None):
+    """h_q / h_out: (pinned) CPU tensors or numpy arrays."""
+    def hp(x):
+        if isinstance(x, np.ndarray):
+            return _np_ptr(x)
+        assert not x.is_cuda and x.is_contiguous()
+        return ctypes.c_void_p(x.data_ptr())
+    ws_bytes = d_ws.numel() * d_ws.element_size()
+    _chk(_lib.bm_match_host(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets, hp(h_q), nq, hp(h_out),
+                            _dptr(d_ws), ws_bytes, order, _stream(stream)), "bm_match_host")
+
+
+def bm_set_profiling(on):
+    _lib.bm_set_profiling(1 if on else 0)
+
+
+def bm_profile_reset():
+    _lib.bm_profile_reset()
+
+
+def bm_profile_read():
+    ms = np.zeros(7, np.float64)
+    la = np.zeros(7, np.int64)
+    un = np.zeros(7, np.int64)
+    _chk(_lib.bm_profile_read(_np_ptr(ms), _np_ptr(la), _np_ptr(un)), "bm_profile_read")
+    return ms, la, un
+
+
+PROFILE_CLASSES = ["tensor_intt", "modup_ntt", "ks_intt", "rescale_ntt", "rot_digit", "rot_ks", "out_intt"]
+
+
+def bm_decrypt(prm, sk, h_ct):
+    """h_ct: uint64 [n][2][1][N] canonical -> scores float64 [n][B]."""
+    h_ct = np.ascontiguousarray(h_ct, np.uint64)
+    n = h_ct.size // (2 * N)
+    out = np.zeros((n, prm.B), np.float64)
+    _chk(_lib.bm_decrypt(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt")
+    return out
+
+
+def bm_decrypt_raw(prm, sk, h_ct):
+    h_ct = np.ascontiguousarray(h_ct, np.uint64)
+    n = h_ct.size // (2 * N)
+    out = np.zeros((n, N), np.int64)
+    _chk(_lib.bm_decrypt_raw(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt_raw")
+    return out
+
+
+def bm_top1(scores):
+    s = np.ascontiguousarray(scores, np.float64)
+    idx = _i64()
+    best = ctypes.c_double()
+    _chk(_lib.bm_top1(_np_ptr(s), s.size, ctypes.byref(idx), ctypes.byref(best)), "bm_top1")
+    return idx.value, best.value
+
+
+def bm_sync(stream=None):
+    _chk(_lib.bm_sync(_stream(stream)), "bm_sync")
+
+
+def bm_strerror(code):
+    return _lib.bm_strerror(code).decode()
+
+
+def bm_build_info():
+    return _lib.bm_build_info().decode()

@@ -1,0 +1,43 @@
+// bm_host.h -- internal interface between the host C++ part (host.cpp) and the CUDA part
+// (device.cu) of libblindmatch.  Not installed, not part of the C ABI.
+#pragma once
+#include <stdint.h>
+#include <vector>
+#include "blindmatch.h"
+
+namespace bm {
+
+// Host-side NTT tables of the product (its own choice of psi; the oracle picks its own).
+struct HostPrime {
+    uint64_t q;
+    uint64_t psi;                 // primitive 2N-th root of unity
+    std::vector<uint64_t> fwd;    // psi^brev13(k), k < N
+    std::vector<uint64_t> inv;    // psi^-brev13(k)
+    uint64_t ninv;                // N^-1 mod q
+};
+const HostPrime &host_prime(int i); // 0: q0, 1: q1, 2: P
+const uint64_t *host_cdt();          // 19 Gaussian CDT thresholds
+
+uint64_t mulmod_h(uint64_t a, uint64_t b, uint64_t q);
+uint64_t shoup_companion(uint64_t w, uint64_t q); // floor(w 2^64 / q)
+
+// host negacyclic NTT (same ordering as the device kernels)
+void host_ntt_fwd(uint64_t *a, int prime);
+void host_ntt_inv(uint64_t *a, int prime);
+
+} // namespace bm
+
+struct bm_sk {
+    uint8_t digest[32];
+    std::vector<int8_t> s;
+};
+struct bm_pk {
+    uint8_t digest[32];
+    std::vector<uint64_t> v; // [2][2][N]
+};
+struct bm_evk {
+    uint8_t digest[32];
+    int32_t n_rot;
+    std::vector<uint64_t> rlk; // [2][2][3][N]
+    std::vector<uint64_t> gk;  // [n_rot][2][2][N]
+};

@@ -1,0 +1,1007 @@
+// device.cu -- sm_100a kernels and the device-facing C ABI of libblindmatch.
+//
+// Hot path (bm_match, HE-C^3) per (query, set) pair, hoisted order
+// (reading R8), one 256-thread CTA per polynomial transform:
+//   K1 k_tensor_intt  (pair, limb)      a4: d0,d1,d2 = sum_i tensor(C_u,i, C_s,i) (Karatsuba,
+//                                        128-bit accumulation), INTT(d2) -> digits x_l
+//   K2 k_modup_ntt    (pair, 4 targets) a5: ModUp x0 -> {q1,P}, x1 -> {q0,P}, NTT
+//   K3 k_ks_intt      (pair, comp, P|q1) a5: KS = sum_j x_j rlk_j, INTT_P(KS[P]);
+//                                        INTT_q1(d[q1] + P^-1 KS[q1])
+//   K4 k_rescale_ntt  (pair, comp)      a5+a6: ModDown fused with rescale by q1 (exact,
+//                                        DESIGN.md "fused ModDown + rescale"), NTT_q0
+//   per ladder step i = 1..log2 s (a7), r = 2^(i-1), g = 5^r mod 2N:
+//   K5 k_rot_digit    (pair)            sigma_g(c1) (NTT-domain permutation), INTT_q0, NTT_P
+//   K6 k_rot_ks       (pair, comp)      KS = x gk_r, INTT_P, NTT_q0, ModDown, C += Rot(C);
+//                                        the last step also INTTs C into the output (a8)
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "bm_common.cuh"
+#include "bm_host.h"
+#include "ntt.cuh"
+
+using namespace bm;
+typedef unsigned __int128 u128;
+
+// ================================================================== device constants
+__constant__ uint64_t c_cdt[19];
+
+struct MatchK {
+    PrimeK pr[3];
+    ulonglong2 pinv[2]; // P^-1 mod q0, q1
+    ulonglong2 q1inv;   // q1^-1 mod q0
+    uint64_t pmod[2];   // P mod q0, q1
+    const ulonglong2 *rlk, *gk;
+    const uint64_t *db, *qry;
+    uint64_t *out;
+    int64_t n_sets, pair0;
+    int32_t p;
+    uint64_t *D01, *D2, *XC, *XU, *Y, *U, *C, *Cn, *XP;
+};
+
+constexpr int WS_POLYS = 21; // u64 polynomials of workspace per pair
+
+BM_D ulonglong2 ld2(const uint64_t *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
+BM_D void st2(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
+
+BM_D uint64_t submod_d(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// centred P-residue y in [0,P) reduced into q (q < P): y mod q, minus (P mod q) when y > P/2
+BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod)
+{
+    uint64_t r = reduce64(y, q, one_p);
+    return (y > (QP >> 1)) ? submod_d(r, pmod, q) : r;
+}
+
+// ================================================================== K1: tensor + INTT(d2)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int part_lo, int part_hi)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
+    const int64_t g = K.pair0 + pi, jq = g / K.n_sets, t = g - jq * K.n_sets;
+    const PrimeK P = l ? K.pr[1] : K.pr[0];
+    const uint64_t q = P.q;
+    const uint64_t *qa = K.qry + (size_t)jq * K.p * 4 * N + (size_t)l * N;
+    const uint64_t *sb = K.db + (size_t)t * K.p * 4 * N + (size_t)l * N;
+    uint64_t *d0p = K.D01 + ((size_t)pi * 4 + 0 + l) * N;
+    uint64_t *d1p = K.D01 + ((size_t)pi * 4 + 2 + l) * N;
+    uint64_t *d2p = K.D2 + ((size_t)pi * 2 + l) * N;
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        const int j = j_L3(tid, e);
+        u128 s0a = 0, s0b = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
+        for (int i = part_lo; i < part_hi; i++) {
+            const size_t off = (size_t)i * 4 * N + j;
+            ulonglong2 x0 = ld2(qa + off), x1 = ld2(qa + off + 2 * N);
+            ulonglong2 y0 = ld2(sb + off), y1 = ld2(sb + off + 2 * N);
+            s0a += (u128)x0.x * y0.x;
+            s0b += (u128)x0.y * y0.y;
+            s2a += (u128)x1.x * y1.x;
+            s2b += (u128)x1.y * y1.y;
+            s1a += (u128)(x0.x + x1.x) * (y0.x + y1.x); // Karatsuba: (a0+a1)(b0+b1)
+            s1b += (u128)(x0.y + x1.y) * (y0.y + y1.y);
+        }
+        uint64_t d0a = reduce128((uint64_t)(s0a >> 64), (uint64_t)s0a, q, P.r64, P.one_p);
+        uint64_t d0b = reduce128((uint64_t)(s0b >> 64), (uint64_t)s0b, q, P.r64, P.one_p);
+        uint64_t d2a = reduce128((uint64_t)(s2a >> 64), (uint64_t)s2a, q, P.r64, P.one_p);
+        uint64_t d2b = reduce128((uint64_t)(s2b >> 64), (uint64_t)s2b, q, P.r64, P.one_p);
+        uint64_t ka = reduce128((uint64_t)(s1a >> 64), (uint64_t)s1a, q, P.r64, P.one_p);
+        uint64_t kb = reduce128((uint64_t)(s1b >> 64), (uint64_t)s1b, q, P.r64, P.one_p);
+        uint64_t d1a = submod_d(submod_d(ka, d0a, q), d2a, q);
+        uint64_t d1b = submod_d(submod_d(kb, d0b, q), d2b, q);
+        st2(d0p + j, d0a, d0b);
+        st2(d1p + j, d1a, d1b);
+        st2(d2p + j, d2a, d2b);
+        a[e] = d2a;
+        a[e + 1] = d2b;
+    }
+    ntt_inv(a, sm, P);
+    uint64_t *xo = K.XC + ((size_t)pi * 2 + l) * N;
+#pragma unroll
+    for (int e = 0; e < 32; e++) xo[j_L1(tid, e)] = a[e];
+}
+
+// ================================================================== K2: ModUp + NTT
+// t = 0: x0 -> q1, 1: x0 -> P, 2: x1 -> q0, 3: x1 -> P  (non-centred lift, reading R4)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_modup_ntt(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 2;
+    const int t = blockIdx.x & 3;
+    const uint64_t *xs = K.XC + ((size_t)pi * 2 + (t >> 1)) * N;
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = xs[j_L1(tid, e)];
+    if (t == 0) {
+#pragma unroll
+        for (int e = 0; e < 32; e++) a[e] = reduce64(a[e], K.pr[1].q, K.pr[1].one_p);
+    }
+    const PrimeK P = (t == 0) ? K.pr[1] : (t == 2) ? K.pr[0] : K.pr[2];
+    ntt_fwd(a, sm, P);
+    uint64_t *xo = K.XU + ((size_t)pi * 4 + t) * N;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) st2(xo + j_L3(tid, e), a[e], a[e + 1]);
+}
+
+// ================================================================== K3: key-switch inner product + INTT
+// block (pair, c, w): w = 0 -> INTT_P(KS_c[P]) -> Y; w = 1 -> INTT_q1(d_c[q1] + P^-1 KS_c[q1]) -> U
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_ks_intt(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 2;
+    const int c = (blockIdx.x >> 1) & 1, w = blockIdx.x & 1;
+    uint64_t a[32];
+    // rlk layout [j][c][l][N]
+    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + (w ? 1 : 2)) * N;
+    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + (w ? 1 : 2)) * N;
+    if (w == 0) {
+        const PrimeK P = K.pr[2];
+        const uint64_t *x0 = K.XU + ((size_t)pi * 4 + 1) * N, *x1 = K.XU + ((size_t)pi * 4 + 3) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+            const int j = j_L3(tid, e);
+            ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j);
+            ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
+            a[e] = csub(shoup(u.x, ka, P.q) + shoup(v.x, la, P.q), P.q2);
+            a[e + 1] = csub(shoup(u.y, kb, P.q) + shoup(v.y, lb, P.q), P.q2);
+        }
+        ntt_inv(a, sm, P);
+        uint64_t *yo = K.Y + ((size_t)pi * 2 + c) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e++) yo[j_L1(tid, e)] = a[e];
+    } else {
+        const PrimeK P = K.pr[1];
+        const uint64_t q = P.q;
+        const uint64_t *x0 = K.XU + ((size_t)pi * 4 + 0) * N, *x1 = K.D2 + ((size_t)pi * 2 + 1) * N;
+        const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+            const int j = j_L3(tid, e);
+            ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
+            ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
+            uint64_t ksa = csub(csub(shoup(u.x, ka, q) + shoup(v.x, la, q), P.q2), q);
+            uint64_t ksb = csub(csub(shoup(u.y, kb, q) + shoup(v.y, lb, q), P.q2), q);
+            a[e] = csub(dd.x + shoup(ksa, K.pinv[1], q), P.q2);
+            a[e + 1] = csub(dd.y + shoup(ksb, K.pinv[1], q), P.q2);
+        }
+        ntt_inv(a, sm, P);
+        uint64_t *uo = K.U + ((size_t)pi * 2 + c) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e++) uo[j_L1(tid, e)] = a[e];
+    }
+}
+
+// ================================================================== K4: ModDown + rescale + NTT_q0
+// Out_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - NTT_q0(P^-1 y^ + z^)), with y^ = centred_P(Y),
+// R = U - P^-1 y^ (mod q1), z^ = centred_q1(R).  accumulate: C += Out (paper order).
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, int accumulate)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t q0 = K.pr[0].q, q1 = K.pr[1].q;
+    const uint64_t *yi = K.Y + ((size_t)pi * 2 + c) * N, *ui = K.U + ((size_t)pi * 2 + c) * N;
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L1(tid, e);
+        const uint64_t y = yi[j], u = ui[j];
+        const uint64_t y1 = centredP_mod(y, q1, K.pr[1].one_p, K.pmod[1]);
+        const uint64_t R = submod_d(u, csub(shoup(y1, K.pinv[1], q1), q1), q1);
+        const uint64_t z0 = (R > (q1 >> 1)) ? R + (q0 - q1) : R;
+        const uint64_t y0 = centredP_mod(y, q0, K.pr[0].one_p, K.pmod[0]);
+        a[e] = csub(csub(shoup(y0, K.pinv[0], q0), q0) + z0, q0);
+    }
+    ntt_fwd(a, sm, K.pr[0]);
+    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + 0) * N;
+    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + 0) * N;
+    const uint64_t *x0 = K.D2 + ((size_t)pi * 2 + 0) * N, *x1 = K.XU + ((size_t)pi * 4 + 2) * N;
+    const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 0) * N;
+    uint64_t *co = K.C + ((size_t)pi * 2 + c) * N;
+    const uint64_t q2 = 2 * q0;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        const int j = j_L3(tid, e);
+        ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
+        ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
+        uint64_t ksa = csub(csub(shoup(u.x, ka, q0) + shoup(v.x, la, q0), q2), q0);
+        uint64_t ksb = csub(csub(shoup(u.y, kb, q0) + shoup(v.y, lb, q0), q2), q0);
+        uint64_t va = csub(dd.x + csub(shoup(ksa, K.pinv[0], q0), q0), q0);
+        uint64_t vb = csub(dd.y + csub(shoup(ksb, K.pinv[0], q0), q0), q0);
+        uint64_t oa = csub(shoup(va + q0 - a[e], K.q1inv, q0), q0);
+        uint64_t ob = csub(shoup(vb + q0 - a[e + 1], K.q1inv, q0), q0);
+        if (accumulate) {
+            ulonglong2 cc = ld2(co + j);
+            oa = csub(oa + cc.x, q0);
+            ob = csub(ob + cc.y, q0);
+        }
+        st2(co + j, oa, ob);
+    }
+}
+
+// ================================================================== ladder (a7)
+// K5: x = INTT_q0(sigma_g(c1)) (coefficients in [0,q0), lifted to P as is), XP = NTT_P(x)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_digit(MatchK K, const uint64_t *Cin, uint32_t g)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    const uint64_t *c1 = Cin + ((size_t)pi * 2 + 1) * N;
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L1(tid, e);
+        sm[pidx(j)] = c1[j];
+    }
+    __syncthreads();
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = sm[pidx(auto_perm(j_L3(tid, e), g))];
+    ntt_inv(a, sm, K.pr[0]);
+    ntt_fwd(a, sm, K.pr[2]);
+    uint64_t *xo = K.XP + (size_t)pi * N;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) st2(xo + j_L3(tid, e), a[e], a[e + 1]);
+}
+
+// K6: KS_c = XP * gk[c][P] -> INTT_P -> y^ -> NTT_q0;  KS'_c = (sigma(c1) gk[c][q0] - NTT(y^)) P^-1;
+//     Cout_c = Cin_c + [c = 0] sigma(c0) + KS'_c; last step: Out_c = INTT_q0(Cout_c) -> d_out
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, const uint64_t *Cin, uint64_t *Cout, int rot,
+                                                           uint32_t g, int last)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t q0 = K.pr[0].q;
+    const ulonglong2 *gq = K.gk + ((size_t)(rot * 2 + c) * 2 + 0) * N; // q0 limb
+    const ulonglong2 *gp = gq + N;                                     // P limb
+    const uint64_t *xp = K.XP + (size_t)pi * N;
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        const int j = j_L3(tid, e);
+        ulonglong2 x = ld2(xp + j);
+        a[e] = shoup(x.x, ld2k(gp + j), QP);
+        a[e + 1] = shoup(x.y, ld2k(gp + j + 1), QP);
+    }
+    ntt_inv(a, sm, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
+    ntt_fwd(a, sm, K.pr[0]);
+    // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
+    const uint64_t *cin1 = Cin + ((size_t)pi * 2 + 1) * N, *cin0 = Cin + ((size_t)pi * 2 + 0) * N;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L1(tid, e);
+        sm[pidx(j)] = cin1[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L3(tid, e);
+        const uint64_t x = sm[pidx(auto_perm(j, g))];
+        const uint64_t ks = csub(shoup(x, ld2k(gq + j), q0), q0);
+        a[e] = csub(shoup(submod_d(ks, a[e], q0), K.pinv[0], q0), q0);
+    }
+    if (c == 0) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 32; e++) {
+            const int j = j_L1(tid, e);
+            sm[pidx(j)] = cin0[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 32; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_L3(tid, e), g))], q0);
+    }
+    const uint64_t *cc = Cin + ((size_t)pi * 2 + c) * N;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        ulonglong2 v = ld2(cc + j_L3(tid, e));
+        a[e] = csub(a[e] + v.x, q0);
+        a[e + 1] = csub(a[e + 1] + v.y, q0);
+    }
+    if (!last) {
+        uint64_t *co = Cout + ((size_t)pi * 2 + c) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) st2(co + j_L3(tid, e), a[e], a[e + 1]);
+    } else {
+        ntt_inv(a, sm, K.pr[0]);
+        uint64_t *o = K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N;
+#pragma unroll
+        for (int e = 0; e < 32; e++) o[j_L1(tid, e)] = a[e];
+    }
+}
+
+// K7: output INTT when there is no ladder (s = 1)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_out_intt(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t *ci = K.C + ((size_t)pi * 2 + c) * N;
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        ulonglong2 v = ld2(ci + j_L3(tid, e));
+        a[e] = v.x;
+        a[e + 1] = v.y;
+    }
+    ntt_inv(a, sm, K.pr[0]);
+    uint64_t *o = K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N;
+#pragma unroll
+    for (int e = 0; e < 32; e++) o[j_L1(tid, e)] = a[e];
+}
+
+// ================================================================== encryption / conversion / keys
+struct EncK {
+    PrimeK pr[2];
+    const ulonglong2 *pk; // [2][2][N]
+    const int64_t *pt;    // [n][N]
+    uint64_t *out;        // [n][2][2][N]
+    uint64_t first_obj, seed;
+};
+
+// sample a small polynomial of stream st into sm (residues mod q), adding pt if given
+BM_D void sample_to_smem(uint64_t *sm, const Stream &st, int gauss, uint64_t q, uint64_t one_p, const int64_t *pt)
+{
+    for (int r = 0; r < 4; r++) {
+        const int b = threadIdx.x + 256 * r;
+        uint64_t d[8];
+        chacha_draws(st, (uint32_t)b, d);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int k = 8 * b + i;
+            const int v = gauss ? gauss_of(d[i], c_cdt) : ternary_of(d[i]);
+            uint64_t x = v >= 0 ? (uint64_t)v : q - (uint64_t)(-v);
+            if (pt) {
+                const int64_t m = pt[k];
+                uint64_t mr = m >= 0 ? reduce64((uint64_t)m, q, one_p) : submod_d(0, reduce64((uint64_t)(-m), q, one_p), q);
+                x = csub(x + mr, q);
+            }
+            sm[pidx(k)] = x;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_encrypt(EncK E)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t ct = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
+    const uint64_t o = E.first_obj + (uint64_t)ct;
+    const PrimeK P = l ? E.pr[1] : E.pr[0];
+    const uint64_t q = P.q;
+    uint64_t *c0 = E.out + ((size_t)ct * 4 + 0 + l) * N;
+    uint64_t *c1 = E.out + ((size_t)ct * 4 + 2 + l) * N;
+    const ulonglong2 *pb = E.pk + (size_t)(0 + l) * N, *pa = E.pk + (size_t)(2 + l) * N;
+    uint64_t a[32];
+    // NTT(u) -> temporarily in c0
+    sample_to_smem(sm, make_stream(E.seed, P_ENC_U, o, 0), 0, q, P.one_p, nullptr);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
+    ntt_fwd(a, sm, P);
+#pragma unroll
+    for (int e = 0; e < 32; e++) c0[j_L3(tid, e)] = a[e];
+    // c1 = u a + e1
+    __syncthreads();
+    sample_to_smem(sm, make_stream(E.seed, P_ENC_E1, o, 0), 1, q, P.one_p, nullptr);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
+    ntt_fwd(a, sm, P);
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L3(tid, e);
+        c1[j] = csub(csub(shoup(c0[j], ld2k(pa + j), q) + a[e], 2 * q), q);
+    }
+    // c0 = u b + e0 + pt
+    __syncthreads();
+    sample_to_smem(sm, make_stream(E.seed, P_ENC_E0, o, 0), 1, q, P.one_p, E.pt + (size_t)ct * N);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
+    ntt_fwd(a, sm, P);
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const int j = j_L3(tid, e);
+        c0[j] = csub(csub(shoup(c0[j], ld2k(pb + j), q) + a[e], 2 * q), q);
+    }
+}
+
+struct ConvK {
+    PrimeK pr[3];
+    const uint64_t *in;
+    uint64_t *out;
+    int n_limbs;
+    int lp[3]; // prime index of each limb
+};
+
+// one block per polynomial; dir 0: coefficient -> NTT, 1: NTT -> coefficient
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_convert(ConvK C, int dir)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t poly = blockIdx.x;
+    const int li = (int)(poly % C.n_limbs);
+    const int pidx_ = C.lp[li];
+    const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
+    const uint64_t *in = C.in + (size_t)poly * N;
+    uint64_t *out = C.out + (size_t)poly * N;
+    uint64_t a[32];
+    if (dir == 0) {
+#pragma unroll
+        for (int e = 0; e < 32; e++) a[e] = in[j_L1(tid, e)];
+        ntt_fwd(a, sm, P);
+        __syncthreads(); // in may alias out
+#pragma unroll
+        for (int e = 0; e < 32; e++) out[j_L3(tid, e)] = a[e];
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32; e++) a[e] = in[j_L3(tid, e)];
+        ntt_inv(a, sm, P);
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 32; e++) out[j_L1(tid, e)] = a[e];
+    }
+}
+
+// keys: canonical coefficients -> NTT domain Shoup pairs
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_key_ntt(ConvK C, ulonglong2 *dst)
+{
+    extern __shared__ uint64_t sm[];
+    const int tid = threadIdx.x;
+    const int64_t poly = blockIdx.x;
+    const int li = (int)(poly % C.n_limbs);
+    const int pidx_ = C.lp[li];
+    const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
+    uint64_t a[32];
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = C.in[(size_t)poly * N + j_L1(tid, e)];
+    ntt_fwd(a, sm, P);
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const uint64_t w = a[e];
+        dst[(size_t)poly * N + j_L3(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
+    }
+}
+
+// ================================================================== host side: device context
+namespace {
+
+struct DevCtx {
+    int dev = -1;
+    ulonglong2 *tw = nullptr; // [3][2][N]
+    PrimeK pr[3];
+    ulonglong2 pinv[2], q1inv;
+    uint64_t pmod[2];
+};
+
+std::mutex g_mu;
+std::vector<DevCtx *> g_ctx;
+
+ulonglong2 shoup_pair(uint64_t w, uint64_t q) { return make_ulonglong2(w, shoup_companion(w, q)); }
+uint64_t powmod_d(uint64_t a, uint64_t e, uint64_t q)
+{
+    uint64_t r = 1;
+    a %= q;
+    for (; e; e >>= 1, a = mulmod_h(a, a, q))
+        if (e & 1) r = mulmod_h(r, a, q);
+    return r;
+}
+
+const size_t SMEM_BYTES = SMEM_WORDS * sizeof(uint64_t);
+
+template <typename F> void set_smem(F f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES); }
+
+int ctx_get(DevCtx **out)
+{
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
+        cudaGetLastError();
+        return BM_ERR_CUDA;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1, nullptr);
+    if (g_ctx[dev]) {
+        *out = g_ctx[dev];
+        return BM_OK;
+    }
+    DevCtx *C = new DevCtx;
+    C->dev = dev;
+    std::vector<ulonglong2> h(6 * (size_t)N);
+    for (int i = 0; i < 3; i++) {
+        const HostPrime &H = host_prime(i);
+        for (int k = 0; k < N; k++) {
+            h[(size_t)(2 * i) * N + k] = shoup_pair(H.fwd[k], H.q);
+            h[(size_t)(2 * i + 1) * N + k] = shoup_pair(H.inv[k], H.q);
+        }
+    }
+    if (cudaMalloc(&C->tw, h.size() * sizeof(ulonglong2)) != cudaSuccess) {
+        delete C;
+        cudaGetLastError();
+        return BM_ERR_OOM;
+    }
+    cudaMemcpy(C->tw, h.data(), h.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    for (int i = 0; i < 3; i++) {
+        const HostPrime &H = host_prime(i);
+        PrimeK &P = C->pr[i];
+        P.q = H.q;
+        P.q2 = 2 * H.q;
+        P.fwd = C->tw + (size_t)(2 * i) * N;
+        P.inv = C->tw + (size_t)(2 * i + 1) * N;
+        P.ninv = shoup_pair(H.ninv, H.q);
+        P.ninv_w1 = shoup_pair(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
+        uint64_t r64 = (uint64_t)(((u128)1 << 64) % H.q);
+        P.r64 = shoup_pair(r64, H.q);
+        P.one_p = (uint64_t)((((u128)1) << 64) / H.q);
+    }
+    for (int l = 0; l < 2; l++) {
+        uint64_t q = C->pr[l].q;
+        C->pmod[l] = QP % q;
+        C->pinv[l] = shoup_pair(powmod_d(QP % q, q - 2, q), q);
+    }
+    C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
+    cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
+    set_smem(k_tensor_intt);
+    set_smem(k_modup_ntt);
+    set_smem(k_ks_intt);
+    set_smem(k_rescale_ntt);
+    set_smem(k_rot_digit);
+    set_smem(k_rot_ks);
+    set_smem(k_out_intt);
+    set_smem(k_encrypt);
+    set_smem(k_convert);
+    set_smem(k_key_ntt);
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+        cudaFree(C->tw);
+        delete C;
+        return BM_ERR_CUDA;
+    }
+    g_ctx[dev] = C;
+    *out = C;
+    return BM_OK;
+}
+
+int launch_check()
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "blindmatch: CUDA error %s\n", cudaGetErrorString(e));
+        return BM_ERR_CUDA;
+    }
+    return BM_OK;
+}
+
+// ------------------------------------------------------------------ profiling
+struct Prof {
+    bool on = false;
+    double ms[7] = {0};
+    int64_t launches[7] = {0};
+    int64_t units[7] = {0};
+};
+Prof g_prof;
+std::mutex g_prof_mu;
+
+struct Rec {
+    int cls;
+    int64_t units;
+    cudaEvent_t a, b;
+};
+
+} // namespace
+
+struct bm_pk_dev {
+    int dev;
+    uint8_t digest[32];
+    ulonglong2 *pk;
+};
+struct bm_evk_dev {
+    int dev;
+    uint8_t digest[32];
+    int32_t n_rot;
+    ulonglong2 *rlk; // [2][2][3][N]
+    ulonglong2 *gk;  // [n_rot][2][2][N]
+};
+
+static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out)
+{
+    uint64_t *tmp = nullptr;
+    ulonglong2 *dst = nullptr;
+    if (cudaMalloc(&tmp, (size_t)n_polys * N * 8) != cudaSuccess ||
+        cudaMalloc(&dst, (size_t)n_polys * N * sizeof(ulonglong2)) != cudaSuccess) {
+        cudaFree(tmp);
+        cudaGetLastError();
+        return BM_ERR_OOM;
+    }
+    cudaMemcpy(tmp, h, (size_t)n_polys * N * 8, cudaMemcpyHostToDevice);
+    ConvK K;
+    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    K.in = tmp;
+    K.out = nullptr;
+    K.n_limbs = n_limbs;
+    for (int i = 0; i < 3; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
+    k_key_ntt<<<(unsigned)n_polys, NTT_THREADS, SMEM_BYTES>>>(K, dst);
+    int rc = launch_check();
+    if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
+    cudaFree(tmp);
+    if (rc) {
+        cudaFree(dst);
+        return rc;
+    }
+    *out = dst;
+    return BM_OK;
+}
+
+extern "C" {
+
+int bm_pk_to_device(const bm_params *prm, const bm_pk *pk, bm_pk_dev **out)
+{
+    if (!prm || !pk || !out) return BM_ERR_INVALID_ARG;
+    if (memcmp(pk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    bm_pk_dev *d = new bm_pk_dev;
+    d->dev = C->dev;
+    memcpy(d->digest, prm->digest, 32);
+    const int lp[2] = {0, 1};
+    rc = upload_key_polys(C, pk->v.data(), 4, 2, lp, &d->pk);
+    if (rc) {
+        delete d;
+        return rc;
+    }
+    *out = d;
+    return BM_OK;
+}
+
+int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
+{
+    if (!prm || !evk || !out) return BM_ERR_INVALID_ARG;
+    if (memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    bm_evk_dev *d = new bm_evk_dev;
+    d->dev = C->dev;
+    memcpy(d->digest, prm->digest, 32);
+    d->n_rot = evk->n_rot;
+    d->gk = nullptr;
+    const int lr[3] = {0, 1, 2}, lg[2] = {0, 2};
+    rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk);
+    if (!rc && evk->n_rot > 0) rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk);
+    if (rc) {
+        cudaFree(d->rlk);
+        delete d;
+        return rc;
+    }
+    *out = d;
+    return BM_OK;
+}
+
+void bm_pk_dev_free(bm_pk_dev *d)
+{
+    if (!d) return;
+    cudaFree(d->pk);
+    delete d;
+}
+void bm_evk_dev_free(bm_evk_dev *d)
+{
+    if (!d) return;
+    cudaFree(d->rlk);
+    cudaFree(d->gk);
+    delete d;
+}
+
+int bm_encrypt(const bm_params *prm, const bm_pk_dev *pk, const int64_t *d_pt, int64_t n_cts, uint64_t first_obj,
+               uint64_t seed, uint64_t *d_out, void *stream)
+{
+    if (!prm || !pk || n_cts < 0 || (n_cts > 0 && (!d_pt || !d_out))) return BM_ERR_INVALID_ARG;
+    if (memcmp(pk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (n_cts == 0) return BM_OK;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    EncK E;
+    E.pr[0] = C->pr[0];
+    E.pr[1] = C->pr[1];
+    E.pk = pk->pk;
+    E.pt = d_pt;
+    E.out = d_out;
+    E.first_obj = first_obj;
+    E.seed = seed;
+    k_encrypt<<<(unsigned)(2 * n_cts), NTT_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(E);
+    return launch_check();
+}
+
+static int encrypt_host_pt(const bm_params *prm, const bm_pk_dev *pk, const std::vector<int64_t> &pt, int64_t n_cts,
+                           uint64_t first_obj, uint64_t seed, uint64_t *d_out, void *stream)
+{
+    int64_t *d_pt = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMallocAsync(&d_pt, pt.size() * 8, s) != cudaSuccess) {
+        cudaGetLastError();
+        return BM_ERR_OOM;
+    }
+    cudaMemcpyAsync(d_pt, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice, s);
+    int rc = bm_encrypt(prm, pk, d_pt, n_cts, first_obj, seed, d_out, stream);
+    cudaFreeAsync(d_pt, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) rc = BM_ERR_CUDA;
+    return rc;
+}
+
+int bm_encrypt_db(const bm_params *prm, const bm_pk_dev *pk, const double *tmpl, int64_t n, int64_t first_set,
+                  int64_t n_sets, uint64_t seed, uint64_t *d_out, void *stream)
+{
+    if (!prm || !pk || n_sets < 0) return BM_ERR_INVALID_ARG;
+    if (n_sets == 0) return BM_OK;
+    std::vector<int64_t> pt((size_t)n_sets * prm->p * N);
+    int rc = bm_encode_db(prm, tmpl, n, first_set, n_sets, pt.data());
+    if (rc) return rc;
+    return encrypt_host_pt(prm, pk, pt, n_sets * prm->p, (uint64_t)first_set * prm->p, seed, d_out, stream);
+}
+
+int bm_encrypt_query(const bm_params *prm, const bm_pk_dev *pk, const double *q, int64_t nq, int64_t first_query,
+                     uint64_t seed, uint64_t *d_out, void *stream)
+{
+    if (!prm || !pk || nq < 0 || first_query < 0) return BM_ERR_INVALID_ARG;
+    if (nq == 0) return BM_OK;
+    std::vector<int64_t> pt((size_t)nq * prm->p * N);
+    int rc = bm_encode_query(prm, q, nq, pt.data());
+    if (rc) return rc;
+    return encrypt_host_pt(prm, pk, pt, nq * prm->p, (uint64_t)first_query * prm->p, seed, d_out, stream);
+}
+
+static int convert(const bm_params *prm, const uint64_t *in, int64_t n_cts, int32_t n_limbs, uint64_t *out,
+                   void *stream, int dir)
+{
+    if (!prm || n_cts < 0 || (n_limbs != 1 && n_limbs != 2) || (n_cts && (!in || !out))) return BM_ERR_INVALID_ARG;
+    if (n_cts == 0) return BM_OK;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    ConvK K;
+    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    K.in = in;
+    K.out = out;
+    K.n_limbs = n_limbs;
+    K.lp[0] = 0;
+    K.lp[1] = 1;
+    K.lp[2] = 2;
+    k_convert<<<(unsigned)(n_cts * 2 * n_limbs), NTT_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(K, dir);
+    return launch_check();
+}
+
+int bm_ct_to_coeff(const bm_params *prm, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
+                   void *stream)
+{
+    return convert(prm, d_in, n_cts, n_limbs, d_out, stream, 1);
+}
+int bm_ct_from_coeff(const bm_params *prm, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
+                     void *stream)
+{
+    return convert(prm, d_in, n_cts, n_limbs, d_out, stream, 0);
+}
+
+// ------------------------------------------------------------------ the scan
+static int64_t chunk_pairs(int64_t total)
+{
+    int64_t ch = 1024;
+    if (const char *e = getenv("BM_CHUNK_PAIRS")) {
+        long v = atol(e);
+        if (v > 0) ch = v;
+    }
+    return total < ch ? total : ch;
+}
+
+size_t bm_match_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, int32_t order)
+{
+    (void)order;
+    if (!prm || n_sets <= 0 || nq <= 0) return 0;
+    return (size_t)chunk_pairs(n_sets * (int64_t)nq) * WS_POLYS * N * sizeof(uint64_t);
+}
+
+void bm_set_profiling(int32_t on)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.on = on != 0;
+}
+void bm_profile_reset(void)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    bool on = g_prof.on;
+    g_prof = Prof();
+    g_prof.on = on;
+}
+int bm_profile_read(double *ms, int64_t *launches, int64_t *units)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (int i = 0; i < 7; i++) {
+        if (ms) ms[i] = g_prof.ms[i];
+        if (launches) launches[i] = g_prof.launches[i];
+        if (units) units[i] = g_prof.units[i];
+    }
+    return BM_OK;
+}
+
+int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+             int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream)
+{
+    if (!prm || !evk || n_sets < 0 || nq < 0 || (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER))
+        return BM_ERR_INVALID_ARG;
+    if (memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    const int64_t total = n_sets * (int64_t)nq;
+    if (total == 0) return BM_OK;
+    if (!d_db || !d_q || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
+    if (ws_bytes < bm_match_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ch = chunk_pairs(total);
+
+    MatchK K;
+    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    K.pinv[0] = C->pinv[0];
+    K.pinv[1] = C->pinv[1];
+    K.q1inv = C->q1inv;
+    K.pmod[0] = C->pmod[0];
+    K.pmod[1] = C->pmod[1];
+    K.rlk = evk->rlk;
+    K.gk = evk->gk;
+    K.db = d_db;
+    K.qry = d_q;
+    K.out = d_out;
+    K.n_sets = n_sets;
+    K.p = prm->p;
+    uint64_t *ws = (uint64_t *)d_ws;
+    const size_t P1 = (size_t)ch * N;
+    K.D01 = ws;
+    K.D2 = K.D01 + 4 * P1;
+    K.XC = K.D2 + 2 * P1;
+    K.XU = K.XC + 2 * P1;
+    K.Y = K.XU + 4 * P1;
+    K.U = K.Y + 2 * P1;
+    K.C = K.U + 2 * P1;
+    K.Cn = K.C + 2 * P1;
+    K.XP = K.Cn + 2 * P1;
+
+    bool prof;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        prof = g_prof.on;
+    }
+    std::vector<Rec> recs;
+    auto beg = [&](int cls, int64_t units) {
+        if (!prof) return;
+        Rec r;
+        r.cls = cls;
+        r.units = units;
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        cudaEventRecord(r.a, s);
+        recs.push_back(r);
+    };
+    auto end = [&]() {
+        if (prof) cudaEventRecord(recs.back().b, s);
+    };
+
+    const int log_s = prm->log_s;
+    for (int64_t p0 = 0; p0 < total && !rc; p0 += ch) {
+        const int64_t np = (total - p0 < ch) ? total - p0 : ch;
+        K.pair0 = p0;
+        const unsigned npu = (unsigned)np;
+        const int n_rounds = order == BM_ORDER_HOISTED ? 1 : prm->p;
+        for (int r = 0; r < n_rounds && !rc; r++) {
+            const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
+            beg(0, 2 * np);
+            k_tensor_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, lo, hi);
+            end();
+            beg(1, 4 * np);
+            k_modup_ntt<<<4 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            end();
+            beg(2, 4 * np);
+            k_ks_intt<<<4 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            end();
+            beg(3, 2 * np);
+            k_rescale_ntt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, r > 0 ? 1 : 0);
+            end();
+            rc = launch_check();
+        }
+        const uint64_t *cin = K.C;
+        uint64_t *cout = K.Cn;
+        for (int i = 1; i <= log_s && !rc; i++) {
+            const uint64_t r = (uint64_t)1 << (i - 1);
+            const uint32_t g = (uint32_t)powmod_d(5, r, 2 * N);
+            beg(4, 2 * np);
+            k_rot_digit<<<npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin, g);
+            end();
+            const int last = i == log_s;
+            beg(5, (last ? 6 : 4) * np);
+            k_rot_ks<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
+            end();
+            rc = launch_check();
+            const uint64_t *t = cin;
+            cin = cout;
+            cout = const_cast<uint64_t *>(t);
+        }
+        if (log_s == 0 && !rc) {
+            beg(6, 2 * np);
+            k_out_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            end();
+            rc = launch_check();
+        }
+    }
+    if (prof) {
+        if (cudaStreamSynchronize(s) != cudaSuccess) rc = BM_ERR_CUDA;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        for (Rec &r : recs) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            g_prof.ms[r.cls] += ms;
+            g_prof.launches[r.cls] += 1;
+            g_prof.units[r.cls] += r.units;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    }
+    return rc;
+}
+
+size_t bm_match_host_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, int32_t order)
+{
+    if (!prm || n_sets <= 0 || nq <= 0) return 0;
+    const size_t qbytes = (size_t)nq * prm->p * 4 * N * 8, obytes = (size_t)nq * n_sets * 2 * N * 8;
+    return qbytes + obytes + bm_match_ws_bytes(prm, n_sets, nq, order);
+}
+
+int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                  const uint64_t *h_q, int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order,
+                  void *stream)
+{
+    if (!prm || n_sets < 0 || nq < 0) return BM_ERR_INVALID_ARG;
+    if (n_sets == 0 || nq == 0) return BM_OK;
+    if (!h_q || !h_out || !d_ws) return BM_ERR_INVALID_ARG;
+    if (ws_bytes < bm_match_host_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t qbytes = (size_t)nq * prm->p * 4 * N * 8, obytes = (size_t)nq * n_sets * 2 * N * 8;
+    uint64_t *dq = (uint64_t *)d_ws, *dout = dq + qbytes / 8;
+    void *mws = dout + obytes / 8;
+    if (cudaMemcpyAsync(dq, h_q, qbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return BM_ERR_CUDA;
+    int rc = bm_match(prm, evk, d_db, n_sets, dq, nq, dout, mws, ws_bytes - qbytes - obytes, order, stream);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(h_out, dout, obytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return BM_ERR_CUDA;
+    return cudaStreamSynchronize(s) == cudaSuccess ? BM_OK : BM_ERR_CUDA;
+}
+
+int bm_sync(void *stream)
+{
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "blindmatch: %s\n", cudaGetErrorString(e));
+        return BM_ERR_CUDA;
+    }
+    return BM_OK;
+}
+
+#define BM_STR2(x) #x
+#define BM_STR(x) BM_STR2(x)
+const char *bm_build_info(void) { return "libblindmatch sm_100a (nvcc " BM_STR(__CUDACC_VER_MAJOR__) "." BM_STR(__CUDACC_VER_MINOR__) ")"; }
+
+} // extern "C"

@@ -1,0 +1,139 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/blindmatch.h
+declares, and its host (client-side) functions -- key generation, packing/encoding,
+decryption -- agree with the oracle.  No kernel is launched here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2408_06167_b200 import inputs as I
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "blindmatch.h")
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2408_06167_b200 import build
+    build.build(verbose=False)
+    from paper_2408_06167_b200 import bm
+    return bm
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(B):
+    lib = ctypes.CDLL(B.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), n
+    # the Python binding wraps every declared function under the same name
+    assert set(names) == set(B.EXPORTED)
+
+
+def test_params_and_errors(B):
+    prm = B.bm_params_init(128, 8)
+    assert (prm.N, prm.slots, prm.s, prm.B, prm.log_s) == (8192, 4096, 16, 256, 4)
+    assert list(prm.q) == [2 ** 58 - 835583, 2 ** 40 - 147455, 2 ** 60 - 16383]
+    assert prm.scale == 2.0 ** 40 and prm.out_scale == 2.0 ** 80 / prm.q[1]
+    for d, p in ((3, 1), (16, 32), (8192, 1), (16, 0)):
+        with pytest.raises(B.BMError) as e:
+            B.bm_params_init(d, p)
+        assert e.value.name == "BM_ERR_INVALID_LAYOUT"
+
+
+@pytest.mark.parametrize("d,p", [(16, 1), (128, 4)])
+def test_keygen_matches_oracle(B, O, d, p):
+    prm = B.bm_params_init(d, p)
+    sk, pk, evk = B.bm_keygen(prm, 12345)
+    osk, opk, orlk, ogk = O.keygen(13, 12345, O.n_rot_for(d, p))
+    assert np.array_equal(B.bm_sk_export(sk), osk)
+    assert np.array_equal(B.bm_pk_export(pk), opk)
+    rlk, gk = B.bm_evk_export(evk)
+    assert np.array_equal(rlk, orlk)
+    assert gk.shape[0] == prm.log_s and np.array_equal(gk, ogk)
+
+
+def test_encoder_within_one_of_oracle(B, O):
+    """Product FFT encoder vs the oracle's encoder: identical up to the FP rounding of
+    half-way cases (reading R15): |diff| <= 1 and almost all coefficients equal."""
+    prm = B.bm_params_init(128, 4)
+    T = I.templates(2, 300)
+    pt = B.bm_encode_db(prm, T, 0, 3)
+    z = O.pack_db(T, 13, 128, 4, 0, 3).reshape(-1, 4096)
+    opt = O.encode(z, 13).reshape(pt.shape)
+    diff = np.abs(pt - opt)
+    assert diff.max() <= 1 and (diff != 0).mean() < 1e-3
+    Q, _ = I.queries(2, 5)
+    pq = B.bm_encode_query(prm, Q)
+    oq = O.encode(O.pack_query(Q, 13, 128, 4).reshape(-1, 4096), 13).reshape(pq.shape)
+    dq = np.abs(pq - oq)
+    assert dq.max() <= 1 and (dq != 0).mean() < 1e-3
+
+
+def test_encode_errors(B):
+    prm = B.bm_params_init(16, 1)
+    with pytest.raises(B.BMError) as e:
+        B.bm_encode_query(prm, np.zeros((1, 16)))
+    assert e.value.name == "BM_ERR_ZERO_VECTOR"
+    bad = np.ones((1, 16))
+    bad[0, 3] = np.nan
+    with pytest.raises(B.BMError) as e:
+        B.bm_encode_query(prm, bad)
+    assert e.value.name == "BM_ERR_MAGNITUDE"
+
+
+def test_decrypt_matches_oracle(B, O):
+    """Client-side decryption of an oracle-made level-0 scan result."""
+    d, p = 16, 1
+    prm = B.bm_params_init(d, p)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    osk, opk, orlk, ogk = O.keygen(13, 1, O.n_rot_for(d, p))
+    T = I.templates(1)
+    Q, _ = I.queries(1)
+    zdb = O.pack_db(T, 13, d, p, 0, 1)
+    db = O.encrypt(13, opk, O.encode(zdb.reshape(-1, 4096), 13), 0, 2).reshape(1, p, 2, 2, -1)
+    qc = O.encrypt(13, opk, O.encode(O.pack_query(Q, 13, d, p).reshape(-1, 4096), 13), 0, 3).reshape(1, p, 2, 2, -1)
+    out, _ = O.match(13, d, p, 0, orlk, ogk, db, qc)
+    m = B.bm_decrypt_raw(prm, sk, out)
+    q0 = prm.q[0]
+    om = O.decrypt(13, osk, out[0], 1)[0]
+    assert np.array_equal(m[0], O.centred_i64(om, q0))
+    sc = B.bm_decrypt(prm, sk, out)[0]
+    osc = O.scores_from_output(13, d, p, osk, out[0], q0)
+    assert np.abs(sc - osc).max() < 1e-9
+    assert B.bm_top1(sc)[0] == 17
+    assert B.bm_top1(np.array([0.5, 0.7, 0.7, 0.1]))[0] == 1   # lowest index wins ties
+
+
+def test_key_import_roundtrip(B):
+    prm = B.bm_params_init(32, 2)
+    sk, pk, evk = B.bm_keygen(prm, 77)
+    rlk, gk = B.bm_evk_export(evk)
+    evk2 = B.bm_evk_import(prm, rlk, gk)
+    r2, g2 = B.bm_evk_export(evk2)
+    assert np.array_equal(r2, rlk) and np.array_equal(g2, gk)
+    pk2 = B.bm_pk_import(prm, B.bm_pk_export(pk))
+    assert np.array_equal(B.bm_pk_export(pk2), B.bm_pk_export(pk))
+    bad = rlk.copy()
+    bad[0, 0, 0, 0] = prm.q[0]
+    with pytest.raises(B.BMError):
+        B.bm_evk_import(prm, bad, gk)
+
+
+def test_device_calls_fail_loudly_without_gpu(B):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    prm = B.bm_params_init(16, 1)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    with pytest.raises(B.BMError) as e:
+        B.bm_evk_to_device(prm, evk)
+    assert e.value.name == "BM_ERR_CUDA"

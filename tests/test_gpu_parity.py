@@ -1,0 +1,200 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle, bit-exact on every
+RNS residue of the coefficient-domain outputs, given identical seeded keys, plaintexts
+(encoded by the oracle) and encryption randomness (north_star)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2408_06167_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+LOGN = 13
+NTH = max(1, min(16, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the GPU tests need a B200 (there is no CPU fallback)")
+    from paper_2408_06167_b200 import build
+    build.build(verbose=False)
+    from paper_2408_06167_b200 import bm
+    return torch, bm
+
+
+class Setup:
+    """Keys + oracle-encoded plaintexts, encrypted by BOTH sides with the same seeds."""
+
+    def __init__(self, env, O, d, p, T, Q, key_seed=1, db_seed=2, q_seed=3, n_rot=None):
+        torch, B = env
+        self.torch, self.B, self.O = torch, B, O
+        self.d, self.p = d, p
+        self.prm = B.bm_params_init(d, p)
+        S, s, Bk = O.layout(LOGN, d, p)
+        self.n_sets = -(-T.shape[0] // Bk)
+        self.nq = Q.shape[0]
+        self.sk, self.pk, self.evk = B.bm_keygen(self.prm, key_seed)
+        self.osk, self.opk, self.orlk, self.ogk = O.keygen(LOGN, key_seed, O.n_rot_for(d, p))
+        self.pk_dev = B.bm_pk_to_device(self.prm, self.pk)
+        self.evk_dev = B.bm_evk_to_device(self.prm, self.evk)
+        self.db_pt = O.encode(O.pack_db(T, LOGN, d, p, 0, self.n_sets).reshape(-1, S), LOGN)
+        self.q_pt = O.encode(O.pack_query(Q, LOGN, d, p).reshape(-1, S), LOGN)
+        self.db_seed, self.q_seed = db_seed, q_seed
+        dev = torch.device("cuda")
+        self.d_db = torch.empty((self.n_sets, p, 2, 2, 8192), dtype=torch.int64, device=dev)
+        self.d_q = torch.empty((self.nq, p, 2, 2, 8192), dtype=torch.int64, device=dev)
+        B.bm_encrypt(self.prm, self.pk_dev, torch.from_numpy(self.db_pt).to(dev), 0, db_seed, self.d_db)
+        B.bm_encrypt(self.prm, self.pk_dev, torch.from_numpy(self.q_pt).to(dev), 0, q_seed, self.d_q)
+        B.bm_sync()
+
+    def oracle_db(self, sets):
+        O, p = self.O, self.p
+        out = np.zeros((len(sets), p, 2, 2, 8192), np.uint64)
+        for k, t in enumerate(sets):
+            out[k] = O.encrypt(LOGN, self.opk, self.db_pt[t * p:(t + 1) * p], t * p, self.db_seed).reshape(p, 2, 2, -1)
+        return out
+
+    def oracle_q(self, qs):
+        O, p = self.O, self.p
+        out = np.zeros((len(qs), p, 2, 2, 8192), np.uint64)
+        for k, j in enumerate(qs):
+            out[k] = O.encrypt(LOGN, self.opk, self.q_pt[j * p:(j + 1) * p], j * p, self.q_seed).reshape(p, 2, 2, -1)
+        return out
+
+    def gpu_match(self, order=0):
+        torch, B = self.torch, self.B
+        out = torch.empty((self.nq, self.n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+        ws = torch.empty(max(1, B.bm_match_ws_bytes(self.prm, self.n_sets, self.nq, order)), dtype=torch.uint8,
+                         device="cuda")
+        B.bm_match(self.prm, self.evk_dev, self.d_db, self.n_sets, self.d_q, self.nq, out, ws, order)
+        B.bm_sync()
+        return out.cpu().numpy().view(np.uint64)
+
+    def oracle_pairs(self, pairs, order=0):
+        qs = sorted({j for j, _ in pairs})
+        ts = sorted({t for _, t in pairs})
+        qi = {j: k for k, j in enumerate(qs)}
+        ti = {t: k for k, t in enumerate(ts)}
+        local = np.array([(qi[j], ti[t]) for j, t in pairs], np.int64).reshape(-1, 2)
+        out, _ = self.O.match(LOGN, self.d, self.p, order, self.orlk, self.ogk, self.oracle_db(ts), self.oracle_q(qs),
+                              pairs=local, n_threads=NTH)
+        return out.reshape(-1, 2, 8192)
+
+
+def test_encrypt_parity(env, O):
+    """GPU pk-encryption (NTT domain) converted to coefficients == oracle encryption."""
+    torch, B = env
+    T = I.templates(2, 700)
+    st = Setup(env, O, 128, 4, T, I.queries(2, 2)[0])
+    coeff = torch.empty_like(st.d_db)
+    B.bm_ct_to_coeff(st.prm, st.d_db, 2, coeff)
+    got = coeff.cpu().numpy().view(np.uint64)
+    exp = st.oracle_db(list(range(st.n_sets)))
+    assert np.array_equal(got, exp)
+    # from_coeff o to_coeff = identity
+    back = torch.empty_like(coeff)
+    B.bm_ct_from_coeff(st.prm, coeff, 2, back)
+    B.bm_sync()
+    assert torch.equal(back, st.d_db)
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_config1_parity_and_scores(env, O, order):
+    torch, B = env
+    T = I.templates(1)
+    Q, exp = I.queries(1)
+    st = Setup(env, O, 16, 1, T, Q)
+    got = st.gpu_match(order)
+    ref = st.oracle_pairs([(0, 0)], order)
+    assert np.array_equal(got[0, 0], ref[0])
+    sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192))[0][:256]
+    cos = T @ Q[0]
+    assert np.abs(sc - cos).max() < 1e-6
+    assert B.bm_top1(sc)[0] == exp[0] == int(np.argmax(cos))
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_config2_sampled_parity(env, O, p):
+    """BASELINE.json configs[1] (d = 128, 6,144 templates) at each p of the sweep, 3 genuine
+    queries against every set on the GPU; bit-exact parity on sampled pairs incl. the last set."""
+    torch, B = env
+    T = I.templates(2)
+    Q, expq = I.queries(2, 3)
+    st = Setup(env, O, 128, p, T, Q)
+    got = st.gpu_match(0)
+    rng = np.random.default_rng(p)
+    pairs = [(0, 0), (2, st.n_sets - 1), (1, int(rng.integers(st.n_sets)))]
+    ref = st.oracle_pairs(pairs)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k]), (j, t)
+    # decrypted scores of every template vs float64 cosine; top-1 identity
+    sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(3, -1)[:, :T.shape[0]]
+    cos = Q @ T.T
+    assert np.abs(sc - cos).max() < 1e-6
+    assert np.array_equal(sc.argmax(1), cos.argmax(1))
+    assert np.array_equal(sc.argmax(1), expq)
+
+
+def test_paper_order_parity(env, O):
+    T = I.templates(2, 512)
+    Q, _ = I.queries(2, 2)
+    st = Setup(env, O, 128, 4, T, Q)
+    got = st.gpu_match(1)
+    ref = st.oracle_pairs([(1, 3), (0, 1)], 1)
+    assert np.array_equal(got[1, 3], ref[0]) and np.array_equal(got[0, 1], ref[1])
+    hoisted = st.gpu_match(0)
+    assert not np.array_equal(hoisted[1, 3], got[1, 3])  # reading R8: orders differ in residues
+
+
+def test_chunking_ragged(env, O, monkeypatch):
+    """Pairs processed in chunks of 7 (BM_CHUNK_PAIRS): 5 queries x 3 sets = 15 pairs -> 7,7,1."""
+    monkeypatch.setenv("BM_CHUNK_PAIRS", "7")
+    T = I.random_unit(300, 32, 5)
+    Q = I.random_unit(5, 32, 6)
+    st = Setup(env, O, 32, 2, T, Q)       # s = 16, B = 256 -> 2 sets; last set ragged (44 templates)
+    got = st.gpu_match(0)
+    pairs = [(4, 1), (3, 0), (0, 1)]
+    ref = st.oracle_pairs(pairs)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k])
+    monkeypatch.delenv("BM_CHUNK_PAIRS")
+    again = st.gpu_match(0)
+    assert np.array_equal(got, again)
+
+
+@pytest.mark.parametrize("d,p", [(16, 16), (4096, 8)])
+def test_layout_extremes(env, O, d, p):
+    """s = 1 (no ladder, output INTT kernel) and the largest d (s = 512, B = 8, 9 rotations)."""
+    T = I.random_unit(20, d, d)
+    Q = I.random_unit(1, d, d + 1)
+    st = Setup(env, O, d, p, T, Q)
+    got = st.gpu_match(0)
+    ref = st.oracle_pairs([(0, st.n_sets - 1)])
+    assert np.array_equal(got[0, st.n_sets - 1], ref[0])
+    sc = st.B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(-1)[:20]
+    assert np.abs(sc - T @ Q[0]).max() < 1e-6
+
+
+def test_edge_cases_and_errors(env, O):
+    torch, B = env
+    prm = B.bm_params_init(128, 8)
+    sk, pk, evk = B.bm_keygen(prm, 9)
+    evk_dev = B.bm_evk_to_device(prm, evk)
+    dummy = torch.zeros(8, dtype=torch.int64, device="cuda")
+    # empty scans are no-ops
+    B.bm_match(prm, evk_dev, dummy, 0, dummy, 3, dummy, None)
+    B.bm_match(prm, evk_dev, dummy, 5, dummy, 0, dummy, None)
+    # a key set generated for s = 16 lacks the rotations s = 32 needs
+    prm4 = B.bm_params_init(128, 4)
+    with pytest.raises(B.BMError) as e:
+        B.bm_match(prm4, evk_dev, dummy, 1, dummy, 1, dummy, dummy)
+    assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+    with pytest.raises(B.BMError) as e:
+        B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy)
+    assert e.value.name == "BM_ERR_WORKSPACE"
+    with pytest.raises(B.BMError) as e:
+        B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=7)
+    assert e.value.name == "BM_ERR_INVALID_ARG"
