@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the encrypted 1:N cosine scan (HE-C^3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--p P] [--order 0|1]
+
+Workload (N = 1): BASELINE.json configs[1] -- d = 128, 6,144 unit-norm Gaussian templates
+(stand-ins for the paper's IJB-C ArcFace embeddings), 384 genuine queries
+(1 per 16 templates), p = 8 parts (best of the configs[1] sweep), CKKS N = 8192.
+One step = the whole hot path for the whole query batch: bm_match of 384 queries x 24 sets
+(tensor + part sum, relinearise, rescale, 4 rotate-and-add steps, coefficient-domain output);
+for N > 1 also the query broadcast and the result gather (NCCL).  N > 1 is weak scaling: every
+rank holds its own 6,144-template shard (global DB = 6,144 N templates).
+Metric: encrypted templates matched per second = templates x queries / s (BASELINE.json).
+
+--impl reference runs the CPU oracle (oracle/, plain C) on the host cores on a bounded sample of
+the same workload (this tier has no reference implementation).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = 2
+D = 128
+N_RING = 8192
+BFLY = (N_RING // 2) * 13          # butterflies (= modmuls) per 8192-point transform
+SM_COUNT = 148
+IMAD_PER_CLK_SM = 64               # FMA pipe, 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
+MUL32_PER_MODMUL = 10              # 32x32 partial products of one 64-bit Shoup modmul
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p", type=int, default=8)
+    ap.add_argument("--order", type=int, default=0)
+    ap.add_argument("--nq", type=int, default=384)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    return ap.parse_args()
+
+
+def log(args, *a):
+    if not args.quiet:
+        print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- algorithmic work
+def class_modmuls(p, log_s):
+    """Algorithmic 64-bit modular multiplications per (query, set) pair, per kernel class
+    (DESIGN.md "Algorithmic work"): butterflies of every transform + pointwise products."""
+    n = N_RING
+    return {
+        "tensor_intt": 8 * n * p + 2 * BFLY,                       # a0b0, a0b1, a1b0, a1b1 per limb + INTT(d2)
+        "modup_ntt": 4 * BFLY,
+        "ks_intt": 4 * BFLY + 8 * n + 2 * n,                       # rlk products (P, q1) + P^-1 scaling
+        "rescale_ntt": 2 * BFLY + 4 * n + 8 * n,                   # rlk q0 products + P^-1, q1^-1, centring
+        "rot_digit": 2 * BFLY * log_s,
+        "rot_ks": (4 * BFLY + 6 * n) * log_s + (2 * BFLY if log_s else 0),
+        "out_intt": 0 if log_s else 2 * BFLY,
+    }
+
+
+def hbm_bytes_per_step(p, n_sets, nq):
+    """Algorithmic HBM bytes of one step: DB read once, queries read once, results written once."""
+    return n_sets * p * 4 * N_RING * 8 + nq * p * 4 * N_RING * 8 + nq * n_sets * 2 * N_RING * 8
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = []
+        mx = None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                s, m = float(r[0]), float(r[1])
+            except (ValueError, IndexError):
+                continue
+            mx = m
+            if s > 0.5 * m:          # under load
+                sm.append(s)
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(self.rows), "samples_under_load": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (cpu_baseline / reference)
+def oracle_sample(p, seconds_target, n_threads, log=None):
+    """Time the CPU oracle on a bounded sample of (query, set) pairs of the bench workload."""
+    from oracle import oracle as O
+    from paper_2408_06167_b200 import inputs as I
+    logN = 13
+    S, s, B = O.layout(logN, D, p)
+    sk, pk, rlk, gk = O.keygen(logN, 1, O.n_rot_for(D, p))
+    T = I.templates(CFG, 2 * B)            # two full sets
+    Q, _ = I.queries(CFG, 2)
+    db = O.encrypt(logN, pk, O.encode(O.pack_db(T, logN, D, p, 0, 2).reshape(-1, S), logN), 0, 2).reshape(2, p, 2, 2, -1)
+    qc = O.encrypt(logN, pk, O.encode(O.pack_query(Q, logN, D, p).reshape(-1, S), logN), 0, 3).reshape(2, p, 2, 2, -1)
+    t0 = time.perf_counter()
+    O.match(logN, D, p, 0, rlk, gk, db, qc, pairs=np.array([[0, 0]], np.int64), n_threads=1)
+    t1 = time.perf_counter() - t0
+    n_pairs = int(max(n_threads, min(4096, round(seconds_target * n_threads / max(t1, 1e-3)))))
+    pairs = np.array([(k % 2, (k // 2) % 2) for k in range(n_pairs)], np.int64)
+
+    def run():
+        t = time.perf_counter()
+        O.match(logN, D, p, 0, rlk, gk, db, qc, pairs=pairs, n_threads=n_threads)
+        return time.perf_counter() - t
+    return run, n_pairs, B, t1
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2408_06167_b200 import build as pbuild
+    from paper_2408_06167_b200 import dist as pdist
+    from paper_2408_06167_b200 import inputs as I
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        pbuild.build(verbose=False)
+    if world > 1:
+        dist.barrier()
+    from paper_2408_06167_b200 import bm as B
+
+    p, nq, order = args.p, args.nq, args.order
+    prm = B.bm_params_init(D, p)
+    n_tmpl = I.CONFIGS[CFG]["n"]                     # per rank (weak scaling)
+    n_sets = -(-n_tmpl // prm.B)
+    sk, pk, evk = B.bm_keygen(prm, 1)                # deterministic: identical keys on every rank
+    pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
+    T = I.templates(CFG, n_tmpl, rank * n_tmpl)
+    d_db = torch.empty((n_sets, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_db(prm, pk_dev, T, 0, n_sets, 2 + rank, d_db)
+    d_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    if rank == 0:
+        Q, _ = I.queries(CFG, nq)
+        B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
+    d_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
+    ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
+    recv = torch.empty((world, nq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev) if world > 1 else None
+    B.bm_sync()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        pdist.broadcast_queries(d_q)
+        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+        if world > 1:
+            pdist.gather_results(d_out, recv)
+
+    log(args, f"[rank {rank}] setup done: {n_sets} sets x {nq} queries, p={p}, ws={ws.numel() / 2**30:.2f} GiB")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    ms_step = ms / args.steps
+    tq_per_step = world * n_tmpl * nq
+    value = tq_per_step / (ms_step / 1e3)
+
+    # launches of our kernels per step: chunks x (4 per part-round + 2 per ladder step (+1 if s = 1))
+    import math
+    total_pairs = n_sets * nq
+    chunk = int(os.environ.get("BM_CHUNK_PAIRS", "1024"))
+    n_chunks = math.ceil(total_pairs / min(chunk, total_pairs))
+    rounds = 1 if order == 0 else p
+    launches = n_chunks * (4 * rounds + 2 * prm.log_s + (1 if prm.log_s == 0 else 0))
+
+    # per-kernel-class device times (CUDA events on the launching stream), same step, profiled pass
+    B.bm_set_profiling(True)
+    B.bm_profile_reset()
+    for _ in range(args.steps):
+        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+    B.bm_sync()
+    pms, pla, pun = B.bm_profile_read()
+    B.bm_set_profiling(False)
+    mm = class_modmuls(p if order == 0 else 1, prm.log_s)
+    classes = B.PROFILE_CLASSES
+    per_class = {}
+    for i, c in enumerate(classes):
+        if pla[i]:
+            work = mm[c] * total_pairs * args.steps * (rounds if i < 4 else 1)
+            per_class[c] = {"ms_per_step": pms[i] / args.steps, "launches": int(pla[i]),
+                            "gmodmul_s": work / (pms[i] / 1e3) / 1e9}
+    dom = max(per_class, key=lambda c: per_class[c]["ms_per_step"])
+    clocks = clk.summary()
+    f_peak = (clocks["sm_max_mhz"] or 1965.0) * 1e6
+    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / MUL32_PER_MODMUL / 1e9      # Gmodmul/s
+    ach = per_class[dom]["gmodmul_s"]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(dom)
+    hbm_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6548.8
+    hbm_achieved = hbm_bytes_per_step(p, n_sets, nq) / (ms_step / 1e3) / 1e9
+    roofline = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2),
+                "unit": "Gmodmul/s", "frac": round(ach / peak, 4), "traffic": traffic,
+                "peak_basis": f"{SM_COUNT} SMs x {IMAD_PER_CLK_SM} IMAD/clk x {f_peak / 1e6:.0f} MHz / "
+                              f"{MUL32_PER_MODMUL} 32-bit multiplies per 64-bit modmul",
+                "step_gmodmul_s": round(sum(mm.values()) * total_pairs / (ms_step / 1e3) / 1e9, 2),
+                "hbm": {"achieved_gbs": round(hbm_achieved, 2), "peak_gbs": hbm_gbs,
+                        "frac": round(hbm_achieved / hbm_gbs, 5)},
+                "per_class": {c: {k: round(v, 3) for k, v in d.items()} for c, d in per_class.items()}}
+
+    # e2e through the C ABI with host buffers (query H2D + result D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        h_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64).pin_memory()
+        if world > 1:
+            pdist.broadcast_queries(d_q)
+        h_q.copy_(d_q)
+        h_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64).pin_memory()
+        del ws
+        torch.cuda.empty_cache()
+        ws2 = torch.empty(B.bm_match_host_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
+        B.bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, ws2, order)
+        k2 = max(1, min(3, args.steps))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            B.bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, ws2, order)
+        torch.cuda.synchronize()
+        e2e_ms = pdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / k2, dev)
+        # correctness spot check of the e2e output against the device path
+        assert torch.equal(h_out[0, 0], d_out[0, 0].cpu())
+        e2e = {"value": round(tq_per_step / (e2e_ms / 1e3), 1), "unit": "templates*queries/s",
+               "h2d_bytes_per_step": int(h_q.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
+               "ms_per_step": round(e2e_ms, 3), "note": "per rank: query cts H2D + results D2H, wall clock"}
+
+    # CPU oracle on the host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nth = os.cpu_count() or 1
+        run, n_pairs, Bk, t1 = oracle_sample(p, 12.0, nth)
+        secs = run()
+        cpu = {"value": round(n_pairs * Bk / secs, 2), "unit": "templates*queries/s", "cores": nth, "kind": "oracle",
+               "sample": f"{n_pairs} (query, set) pairs of the bench workload (p={p}, {Bk} templates each), "
+                         f"{nth} threads, {secs:.1f} s wall; single pair {t1:.2f} s on 1 thread"}
+
+    if rank == 0:
+        line = {
+            "metric": "encrypted templates matched/sec (d=128, N=8192)", "value": round(value, 1),
+            "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (seeded unit-norm Gaussian templates, genuine noisy queries)",
+            "config": {"workload": f"BASELINE configs[1]: d=128, {n_tmpl} templates/GPU, {nq} queries, p={p}, "
+                                   f"order={'hoisted' if order == 0 else 'paper'}",
+                       "d": D, "p": p, "templates_per_gpu": n_tmpl, "sets_per_gpu": n_sets, "queries": nq,
+                       "ring_N": N_RING, "parallelism": f"db-shard{world}",
+                       "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
+                           nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nth = os.cpu_count() or 1
+    p = args.p
+    run, n_pairs, Bk, t1 = oracle_sample(p, 8.0, nth)
+    for _ in range(args.warmup):
+        run()
+    times = [run() for _ in range(args.steps)]
+    secs = sum(times) / len(times)
+    value = n_pairs * Bk / secs
+    line = {
+        "impl": "reference", "metric": "encrypted templates matched/sec (d=128, N=8192)", "value": round(value, 2),
+        "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"BASELINE configs[1]: d=128, p={p}, bounded sample of {n_pairs} (query, set) pairs "
+                               f"per step", "d": D, "p": p},
+        "cpu_baseline": {"value": round(value, 2), "unit": "templates*queries/s", "cores": nth, "kind": "oracle",
+                         "sample": f"{n_pairs} pairs x {Bk} templates per step on {nth} threads"},
+        "e2e": {"value": round(value, 2), "unit": "templates*queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

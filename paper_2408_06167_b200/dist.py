@@ -1,0 +1,64 @@
+"""Multi-GPU plumbing of the scan ("Cluster Architecture"): the template DB is
+sharded by sets over ranks (one process per GPU), the encrypted query is broadcast from the main
+rank, each rank scans its own sets with bm_match, and the result ciphertexts are gathered.
+No reduction exists on this path: sets are independent.
+
+Gather: query j's results go to a root rank; roots are assigned in contiguous query blocks
+(rank k owns queries [k nq/W, (k+1) nq/W)), so every rank is the root of the same number of
+queries and the exchange is one all_to_all over the [nq][local sets][2][N] result buffers.
+Collectives go through torch.distributed (NCCL on GPUs; gloo in the CPU tests).
+"""
+import torch
+import torch.distributed as dist
+
+
+def world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+def shard_sets(n_sets, world_size, rank):
+    """Contiguous set range of `rank`: [r ceil(T/W), min(T, (r+1) ceil(T/W)))."""
+    per = -(-n_sets // world_size)
+    lo = min(n_sets, rank * per)
+    hi = min(n_sets, lo + per)
+    return lo, hi - lo
+
+
+def query_block(nq, world_size, rank):
+    """Queries whose gathered results land on `rank` (requires nq % world_size == 0)."""
+    assert nq % world_size == 0, "nq must be a multiple of the world size"
+    per = nq // world_size
+    return rank * per, per
+
+
+def broadcast_queries(d_q, src=0, group=None):
+    """a3: replicate the query ciphertexts [nq][p][2][2][N] on every rank."""
+    w, _ = world()
+    if w > 1:
+        dist.broadcast(d_q, src=src, group=group)
+    return d_q
+
+
+def gather_results(d_out, recv=None, group=None):
+    """a8: d_out [nq][n_local][2][N] (this rank's sets) -> recv [W][nq/W][n_local][2][N]:
+    recv[r] holds rank r's sets for the queries this rank is root of."""
+    w, _ = world()
+    if w == 1:
+        return d_out.unsqueeze(0)
+    nq = d_out.shape[0]
+    assert nq % w == 0
+    if recv is None:
+        recv = torch.empty((w, nq // w) + tuple(d_out.shape[1:]), dtype=d_out.dtype, device=d_out.device)
+    dist.all_to_all_single(recv.view(-1), d_out.contiguous().view(-1), group=group)
+    return recv
+
+
+def max_over_ranks(x, device):
+    """max of a float over ranks (timing rule: the job time is the slowest rank)."""
+    w, _ = world()
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if w > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -32,24 +32,26 @@ def templates(cfg, n=None, first=0):
     so any row range is reproducible without drawing the whole database."""
     c = CONFIGS[cfg]
     d = c["d"]
-    total = c["n"]
-    n = total - first if n is None else n
+    n = c["n"] - first if n is None else n
     if cfg == 3:
         rng = np.random.default_rng(DATA_SEED_BASE + cfg)
         cent = _unit(rng.standard_normal((4096, d)))
         noise = rng.standard_normal((4096, 16, d)) * 0.1
         allt = _unit(cent[:, None, :] + noise).reshape(-1, d)
         return allt[first:first + n]
+    # rows are drawn in fixed chunks of 65,536 (row-major, so the first k rows of a chunk do not
+    # depend on how many are drawn); rows past the config's count extend the same stream
+    # (weak-scaling shards of bench.py use them)
     CH = 65536
     out = np.empty((n, d))
     row = first
     while row < first + n:
         ch = row // CH
-        rng = np.random.default_rng([DATA_SEED_BASE + cfg, ch])
-        block = _unit(rng.standard_normal((min(CH, total - ch * CH), d)))
         lo = row - ch * CH
-        take = min(block.shape[0] - lo, first + n - row)
-        out[row - first:row - first + take] = block[lo:lo + take]
+        take = min(CH - lo, first + n - row)
+        rng = np.random.default_rng([DATA_SEED_BASE + cfg, ch])
+        block = rng.standard_normal((lo + take, d))[lo:]
+        out[row - first:row - first + take] = _unit(block)
         row += take
     return out
 
