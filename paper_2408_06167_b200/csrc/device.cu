@@ -29,6 +29,12 @@ typedef unsigned __int128 u128;
 // ================================================================== device constants
 __constant__ uint64_t c_cdt[19];
 
+// Workspace per (query, set) pair, 12 N u64 (aliased across kernels):
+//   D01 [c][l][N]  d_c[q_l] (NTT)      -> U_c aliases d_c[q1] (K3 -> K4)
+//   D2  [l][N]     d2[q_l] (NTT)
+//   XC  [2][N]     digits x0, x1 (coefficients) -> Y_c (K3 -> K4) -> XP (ladder)
+//   XU  [4][N]     ModUp'd digits (NTT) -> C (K4 -> ladder) in XU[0..1], ladder ping-pong XU[2..3]
+// The paper order adds a level-0 accumulator ACC [2][N] (K4 sums into it across parts).
 struct MatchK {
     PrimeK pr[3];
     ulonglong2 pinv[2]; // P^-1 mod q0, q1
@@ -39,10 +45,18 @@ struct MatchK {
     uint64_t *out;
     int64_t n_sets, pair0;
     int32_t p;
-    uint64_t *D01, *D2, *XC, *XU, *Y, *U, *C, *Cn, *XP;
+    uint64_t *D01, *D2, *XC, *XU, *ACC;
 };
 
-constexpr int WS_POLYS = 21; // u64 polynomials of workspace per pair
+// a level-0 ciphertext buffer inside the workspace: pair pi, component c at base + pi*stride + c*N
+struct CtBuf {
+    uint64_t *base;
+    int64_t stride;
+    BM_D uint64_t *at(int64_t pi, int c) const { return base + pi * stride + (int64_t)c * N; }
+};
+
+constexpr int WS_POLYS = 12;      // u64 polynomials of workspace per pair (hoisted order)
+constexpr int WS_POLYS_PAPER = 14;
 
 BM_D ulonglong2 ld2(const uint64_t *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
 BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
@@ -55,6 +69,42 @@ BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod
 {
     uint64_t r = reduce64(y, q, one_p);
     return (y > (QP >> 1)) ? submod_d(r, pmod, q) : r;
+}
+
+// coalesced NTT-domain load/store of the thread's 32 registers (layout L3, storage pos_L3)
+BM_D void load_L3(uint64_t a[32], const uint64_t *p)
+{
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        ulonglong2 v = ld2(p + pos_L3(threadIdx.x, e));
+        a[e] = v.x;
+        a[e + 1] = v.y;
+    }
+}
+BM_D void store_L3(uint64_t *p, const uint64_t a[32])
+{
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) st2(p + pos_L3(threadIdx.x, e), a[e], a[e + 1]);
+}
+BM_D void load_L1(uint64_t a[32], const uint64_t *p)
+{
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = p[j_L1(threadIdx.x, e)];
+}
+BM_D void store_L1(uint64_t *p, const uint64_t a[32])
+{
+#pragma unroll
+    for (int e = 0; e < 32; e++) p[j_L1(threadIdx.x, e)] = a[e];
+}
+// stage an NTT-domain polynomial (storage order) into shared memory by NTT index j
+BM_D void stage_by_j(uint64_t *sm, const uint64_t *p)
+{
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+        ulonglong2 v = ld2(p + pos_L3(threadIdx.x, e));
+        sm[pidx(j_L3(threadIdx.x, e))] = v.x;
+        sm[pidx(j_L3(threadIdx.x, e + 1))] = v.y;
+    }
 }
 
 // ================================================================== K1: tensor + INTT(d2)
@@ -75,7 +125,7 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int pa
     uint64_t a[32];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-        const int j = j_L3(tid, e);
+        const int j = pos_L3(tid, e);
         u128 s0a = 0, s0b = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
         for (int i = part_lo; i < part_hi; i++) {
             const size_t off = (size_t)i * 4 * N + j;
@@ -94,18 +144,14 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int pa
         uint64_t d2b = reduce128((uint64_t)(s2b >> 64), (uint64_t)s2b, q, P.r64, P.one_p);
         uint64_t ka = reduce128((uint64_t)(s1a >> 64), (uint64_t)s1a, q, P.r64, P.one_p);
         uint64_t kb = reduce128((uint64_t)(s1b >> 64), (uint64_t)s1b, q, P.r64, P.one_p);
-        uint64_t d1a = submod_d(submod_d(ka, d0a, q), d2a, q);
-        uint64_t d1b = submod_d(submod_d(kb, d0b, q), d2b, q);
         st2(d0p + j, d0a, d0b);
-        st2(d1p + j, d1a, d1b);
+        st2(d1p + j, submod_d(submod_d(ka, d0a, q), d2a, q), submod_d(submod_d(kb, d0b, q), d2b, q));
         st2(d2p + j, d2a, d2b);
         a[e] = d2a;
         a[e + 1] = d2b;
     }
     ntt_inv(a, sm, P);
-    uint64_t *xo = K.XC + ((size_t)pi * 2 + l) * N;
-#pragma unroll
-    for (int e = 0; e < 32; e++) xo[j_L1(tid, e)] = a[e];
+    store_L1(K.XC + ((size_t)pi * 2 + l) * N, a);
 }
 
 // ================================================================== K2: ModUp + NTT
@@ -113,84 +159,67 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int pa
 __global__ void __launch_bounds__(NTT_THREADS, 2) k_modup_ntt(MatchK K)
 {
     extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 2;
     const int t = blockIdx.x & 3;
-    const uint64_t *xs = K.XC + ((size_t)pi * 2 + (t >> 1)) * N;
     uint64_t a[32];
-#pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = xs[j_L1(tid, e)];
+    load_L1(a, K.XC + ((size_t)pi * 2 + (t >> 1)) * N);
     if (t == 0) {
 #pragma unroll
         for (int e = 0; e < 32; e++) a[e] = reduce64(a[e], K.pr[1].q, K.pr[1].one_p);
     }
     const PrimeK P = (t == 0) ? K.pr[1] : (t == 2) ? K.pr[0] : K.pr[2];
     ntt_fwd(a, sm, P);
-    uint64_t *xo = K.XU + ((size_t)pi * 4 + t) * N;
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) st2(xo + j_L3(tid, e), a[e], a[e + 1]);
+    store_L3(K.XU + ((size_t)pi * 4 + t) * N, a);
 }
 
 // ================================================================== K3: key-switch inner product + INTT
-// block (pair, c, w): w = 0 -> INTT_P(KS_c[P]) -> Y; w = 1 -> INTT_q1(d_c[q1] + P^-1 KS_c[q1]) -> U
+// block (pair, c, w): w = 0 -> Y_c = INTT_P(KS_c[P]);  w = 1 -> U_c = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
+// KS_c[P] = x0~ rlk0[c][P] + x1~ rlk1[c][P];  KS_c[q1] = x0~ rlk0[c][q1] + d2[q1] rlk1[c][q1]
 __global__ void __launch_bounds__(NTT_THREADS, 2) k_ks_intt(MatchK K)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 2;
     const int c = (blockIdx.x >> 1) & 1, w = blockIdx.x & 1;
-    uint64_t a[32];
+    const int lim = w ? 1 : 2;
+    const PrimeK P = w ? K.pr[1] : K.pr[2];
+    const uint64_t q = P.q;
     // rlk layout [j][c][l][N]
-    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + (w ? 1 : 2)) * N;
-    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + (w ? 1 : 2)) * N;
-    if (w == 0) {
-        const PrimeK P = K.pr[2];
-        const uint64_t *x0 = K.XU + ((size_t)pi * 4 + 1) * N, *x1 = K.XU + ((size_t)pi * 4 + 3) * N;
+    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + lim) * N;
+    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + lim) * N;
+    const uint64_t *x0 = K.XU + ((size_t)pi * 4 + (w ? 0 : 1)) * N;
+    const uint64_t *x1 = w ? K.D2 + ((size_t)pi * 2 + 1) * N : K.XU + ((size_t)pi * 4 + 3) * N;
+    uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N; // d_c[q1]; U_c is written over it
+    uint64_t a[32];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-            const int j = j_L3(tid, e);
-            ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j);
-            ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
-            a[e] = csub(shoup(u.x, ka, P.q) + shoup(v.x, la, P.q), P.q2);
-            a[e + 1] = csub(shoup(u.y, kb, P.q) + shoup(v.y, lb, P.q), P.q2);
+    for (int e = 0; e < 32; e += 2) {
+        const int j = pos_L3(tid, e);
+        ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j);
+        uint64_t ka = csub(shoup(u.x, ld2k(k0 + j), q) + shoup(v.x, ld2k(k1 + j), q), P.q2);
+        uint64_t kb = csub(shoup(u.y, ld2k(k0 + j + 1), q) + shoup(v.y, ld2k(k1 + j + 1), q), P.q2);
+        if (w) {
+            ulonglong2 dd = ld2(dc + j);
+            ka = csub(dd.x + shoup(csub(ka, q), K.pinv[1], q), P.q2);
+            kb = csub(dd.y + shoup(csub(kb, q), K.pinv[1], q), P.q2);
         }
-        ntt_inv(a, sm, P);
-        uint64_t *yo = K.Y + ((size_t)pi * 2 + c) * N;
-#pragma unroll
-        for (int e = 0; e < 32; e++) yo[j_L1(tid, e)] = a[e];
-    } else {
-        const PrimeK P = K.pr[1];
-        const uint64_t q = P.q;
-        const uint64_t *x0 = K.XU + ((size_t)pi * 4 + 0) * N, *x1 = K.D2 + ((size_t)pi * 2 + 1) * N;
-        const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N;
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-            const int j = j_L3(tid, e);
-            ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
-            ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
-            uint64_t ksa = csub(csub(shoup(u.x, ka, q) + shoup(v.x, la, q), P.q2), q);
-            uint64_t ksb = csub(csub(shoup(u.y, kb, q) + shoup(v.y, lb, q), P.q2), q);
-            a[e] = csub(dd.x + shoup(ksa, K.pinv[1], q), P.q2);
-            a[e + 1] = csub(dd.y + shoup(ksb, K.pinv[1], q), P.q2);
-        }
-        ntt_inv(a, sm, P);
-        uint64_t *uo = K.U + ((size_t)pi * 2 + c) * N;
-#pragma unroll
-        for (int e = 0; e < 32; e++) uo[j_L1(tid, e)] = a[e];
+        a[e] = ka;
+        a[e + 1] = kb;
     }
+    ntt_inv(a, sm, P);
+    store_L1(w ? dc : K.XC + ((size_t)pi * 2 + c) * N, a);
 }
 
 // ================================================================== K4: ModDown + rescale + NTT_q0
-// Out_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - NTT_q0(P^-1 y^ + z^)), with y^ = centred_P(Y),
-// R = U - P^-1 y^ (mod q1), z^ = centred_q1(R).  accumulate: C += Out (paper order).
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, int accumulate)
+// Out_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - NTT_q0(P^-1 y^ + z^)), with y^ = centred_P(Y_c),
+// R = U_c - P^-1 y^ (mod q1), z^ = centred_q1(R).  accumulate: dst += Out (paper order).
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf dst, int accumulate)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
     const uint64_t q0 = K.pr[0].q, q1 = K.pr[1].q;
-    const uint64_t *yi = K.Y + ((size_t)pi * 2 + c) * N, *ui = K.U + ((size_t)pi * 2 + c) * N;
+    const uint64_t *yi = K.XC + ((size_t)pi * 2 + c) * N, *ui = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N;
     uint64_t a[32];
 #pragma unroll
     for (int e = 0; e < 32; e++) {
@@ -207,15 +236,14 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, int ac
     const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + 0) * N;
     const uint64_t *x0 = K.D2 + ((size_t)pi * 2 + 0) * N, *x1 = K.XU + ((size_t)pi * 4 + 2) * N;
     const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 0) * N;
-    uint64_t *co = K.C + ((size_t)pi * 2 + c) * N;
+    uint64_t *co = dst.at(pi, c);
     const uint64_t q2 = 2 * q0;
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-        const int j = j_L3(tid, e);
+        const int j = pos_L3(tid, e);
         ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
-        ulonglong2 ka = ld2k(k0 + j), kb = ld2k(k0 + j + 1), la = ld2k(k1 + j), lb = ld2k(k1 + j + 1);
-        uint64_t ksa = csub(csub(shoup(u.x, ka, q0) + shoup(v.x, la, q0), q2), q0);
-        uint64_t ksb = csub(csub(shoup(u.y, kb, q0) + shoup(v.y, lb, q0), q2), q0);
+        uint64_t ksa = csub(csub(shoup(u.x, ld2k(k0 + j), q0) + shoup(v.x, ld2k(k1 + j), q0), q2), q0);
+        uint64_t ksb = csub(csub(shoup(u.y, ld2k(k0 + j + 1), q0) + shoup(v.y, ld2k(k1 + j + 1), q0), q2), q0);
         uint64_t va = csub(dd.x + csub(shoup(ksa, K.pinv[0], q0), q0), q0);
         uint64_t vb = csub(dd.y + csub(shoup(ksb, K.pinv[0], q0), q0), q0);
         uint64_t oa = csub(shoup(va + q0 - a[e], K.q1inv, q0), q0);
@@ -231,32 +259,25 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, int ac
 
 // ================================================================== ladder (a7)
 // K5: x = INTT_q0(sigma_g(c1)) (coefficients in [0,q0), lifted to P as is), XP = NTT_P(x)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_digit(MatchK K, const uint64_t *Cin, uint32_t g)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_digit(MatchK K, CtBuf cin, uint32_t g)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
-    const uint64_t *c1 = Cin + ((size_t)pi * 2 + 1) * N;
-#pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L1(tid, e);
-        sm[pidx(j)] = c1[j];
-    }
+    stage_by_j(sm, cin.at(pi, 1));
     __syncthreads();
     uint64_t a[32];
 #pragma unroll
     for (int e = 0; e < 32; e++) a[e] = sm[pidx(auto_perm(j_L3(tid, e), g))];
     ntt_inv(a, sm, K.pr[0]);
     ntt_fwd(a, sm, K.pr[2]);
-    uint64_t *xo = K.XP + (size_t)pi * N;
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) st2(xo + j_L3(tid, e), a[e], a[e + 1]);
+    store_L3(K.XC + (size_t)pi * 2 * N, a);
 }
 
 // K6: KS_c = XP * gk[c][P] -> INTT_P -> y^ -> NTT_q0;  KS'_c = (sigma(c1) gk[c][q0] - NTT(y^)) P^-1;
-//     Cout_c = Cin_c + [c = 0] sigma(c0) + KS'_c; last step: Out_c = INTT_q0(Cout_c) -> d_out
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, const uint64_t *Cin, uint64_t *Cout, int rot,
-                                                           uint32_t g, int last)
+//     cout_c = cin_c + [c = 0] sigma(c0) + KS'_c; last step: out_c = INTT_q0(cout_c) -> d_out (a8)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout, int rot, uint32_t g,
+                                                           int last)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
@@ -264,85 +285,72 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, const uint6
     const int c = blockIdx.x & 1;
     const uint64_t q0 = K.pr[0].q;
     const ulonglong2 *gq = K.gk + ((size_t)(rot * 2 + c) * 2 + 0) * N; // q0 limb
-    const ulonglong2 *gp = gq + N;                                     // P limb
-    const uint64_t *xp = K.XP + (size_t)pi * N;
     uint64_t a[32];
+    {
+        const ulonglong2 *gp = gq + N; // P limb
+        const uint64_t *xp = K.XC + (size_t)pi * 2 * N;
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        const int j = j_L3(tid, e);
-        ulonglong2 x = ld2(xp + j);
-        a[e] = shoup(x.x, ld2k(gp + j), QP);
-        a[e + 1] = shoup(x.y, ld2k(gp + j + 1), QP);
+        for (int e = 0; e < 32; e += 2) {
+            const int j = pos_L3(tid, e);
+            ulonglong2 x = ld2(xp + j);
+            a[e] = shoup(x.x, ld2k(gp + j), QP);
+            a[e + 1] = shoup(x.y, ld2k(gp + j + 1), QP);
+        }
     }
-    ntt_inv(a, sm, K.pr[2]);
+    // phase 0: INTT_P; phase 1: NTT_q0; phase 2 (last step only): INTT_q0 of the new C
+    for (int ph = 0;; ph++) {
+        if (ph == 1) ntt_fwd(a, sm, K.pr[0]);
+        else ntt_inv(a, sm, ph == 0 ? K.pr[2] : K.pr[0]);
+        if (ph == 0) {
 #pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
-    ntt_fwd(a, sm, K.pr[0]);
-    // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
-    const uint64_t *cin1 = Cin + ((size_t)pi * 2 + 1) * N, *cin0 = Cin + ((size_t)pi * 2 + 0) * N;
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L1(tid, e);
-        sm[pidx(j)] = cin1[j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L3(tid, e);
-        const uint64_t x = sm[pidx(auto_perm(j, g))];
-        const uint64_t ks = csub(shoup(x, ld2k(gq + j), q0), q0);
-        a[e] = csub(shoup(submod_d(ks, a[e], q0), K.pinv[0], q0), q0);
-    }
-    if (c == 0) {
+            for (int e = 0; e < 32; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
+            continue;
+        }
+        if (ph == 2) {
+            store_L1(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
+            break;
+        }
+        // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
+        __syncthreads();
+        stage_by_j(sm, cin.at(pi, 1));
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < 32; e++) {
-            const int j = j_L1(tid, e);
-            sm[pidx(j)] = cin0[j];
+            const uint64_t x = sm[pidx(auto_perm(j_L3(tid, e), g))];
+            const uint64_t ks = csub(shoup(x, ld2k(gq + pos_L3(tid, e)), q0), q0);
+            a[e] = csub(shoup(submod_d(ks, a[e], q0), K.pinv[0], q0), q0);
         }
-        __syncthreads();
+        if (c == 0) {
+            __syncthreads();
+            stage_by_j(sm, cin.at(pi, 0));
+            __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 32; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_L3(tid, e), g))], q0);
-    }
-    const uint64_t *cc = Cin + ((size_t)pi * 2 + c) * N;
+            for (int e = 0; e < 32; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_L3(tid, e), g))], q0);
+        }
+        const uint64_t *cc = cin.at(pi, c);
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        ulonglong2 v = ld2(cc + j_L3(tid, e));
-        a[e] = csub(a[e] + v.x, q0);
-        a[e + 1] = csub(a[e + 1] + v.y, q0);
-    }
-    if (!last) {
-        uint64_t *co = Cout + ((size_t)pi * 2 + c) * N;
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) st2(co + j_L3(tid, e), a[e], a[e + 1]);
-    } else {
-        ntt_inv(a, sm, K.pr[0]);
-        uint64_t *o = K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N;
-#pragma unroll
-        for (int e = 0; e < 32; e++) o[j_L1(tid, e)] = a[e];
+        for (int e = 0; e < 32; e += 2) {
+            ulonglong2 v = ld2(cc + pos_L3(tid, e));
+            a[e] = csub(a[e] + v.x, q0);
+            a[e + 1] = csub(a[e + 1] + v.y, q0);
+        }
+        if (!last) {
+            store_L3(cout.at(pi, c), a);
+            break;
+        }
     }
 }
 
 // K7: output INTT when there is no ladder (s = 1)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_out_intt(MatchK K)
+__global__ void __launch_bounds__(NTT_THREADS, 2) k_out_intt(MatchK K, CtBuf cin)
 {
     extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
-    const uint64_t *ci = K.C + ((size_t)pi * 2 + c) * N;
     uint64_t a[32];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        ulonglong2 v = ld2(ci + j_L3(tid, e));
-        a[e] = v.x;
-        a[e + 1] = v.y;
-    }
+    load_L3(a, cin.at(pi, c));
     ntt_inv(a, sm, K.pr[0]);
-    uint64_t *o = K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N;
-#pragma unroll
-    for (int e = 0; e < 32; e++) o[j_L1(tid, e)] = a[e];
+    store_L1(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
 }
 
 // ================================================================== encryption / conversion / keys
@@ -389,37 +397,27 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_encrypt(EncK E)
     uint64_t *c1 = E.out + ((size_t)ct * 4 + 2 + l) * N;
     const ulonglong2 *pb = E.pk + (size_t)(0 + l) * N, *pa = E.pk + (size_t)(2 + l) * N;
     uint64_t a[32];
-    // NTT(u) -> temporarily in c0
-    sample_to_smem(sm, make_stream(E.seed, P_ENC_U, o, 0), 0, q, P.one_p, nullptr);
-    __syncthreads();
+    // phase 0: NTT(u) -> kept in c0 until phase 2;  phase 1: c1 = u a + e1;  phase 2: c0 = u b + e0 + pt
+    for (int ph = 0; ph < 3; ph++) {
+        __syncthreads();
+        const uint32_t purpose = ph == 0 ? P_ENC_U : ph == 1 ? P_ENC_E1 : P_ENC_E0;
+        sample_to_smem(sm, make_stream(E.seed, purpose, o, 0), ph != 0, q, P.one_p,
+                       ph == 2 ? E.pt + (size_t)ct * N : nullptr);
+        __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
-    ntt_fwd(a, sm, P);
+        for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
+        ntt_fwd(a, sm, P);
+        if (ph == 0) {
+            store_L3(c0, a);
+            continue;
+        }
+        uint64_t *dst = ph == 1 ? c1 : c0;
+        const ulonglong2 *key = ph == 1 ? pa : pb;
 #pragma unroll
-    for (int e = 0; e < 32; e++) c0[j_L3(tid, e)] = a[e];
-    // c1 = u a + e1
-    __syncthreads();
-    sample_to_smem(sm, make_stream(E.seed, P_ENC_E1, o, 0), 1, q, P.one_p, nullptr);
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
-    ntt_fwd(a, sm, P);
-#pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L3(tid, e);
-        c1[j] = csub(csub(shoup(c0[j], ld2k(pa + j), q) + a[e], 2 * q), q);
-    }
-    // c0 = u b + e0 + pt
-    __syncthreads();
-    sample_to_smem(sm, make_stream(E.seed, P_ENC_E0, o, 0), 1, q, P.one_p, E.pt + (size_t)ct * N);
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
-    ntt_fwd(a, sm, P);
-#pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L3(tid, e);
-        c0[j] = csub(csub(shoup(c0[j], ld2k(pb + j), q) + a[e], 2 * q), q);
+        for (int e = 0; e < 32; e++) {
+            const int j = pos_L3(tid, e);
+            dst[j] = csub(csub(shoup(c0[j], ld2k(key + j), q) + a[e], 2 * q), q);
+        }
     }
 }
 
@@ -435,7 +433,6 @@ struct ConvK {
 __global__ void __launch_bounds__(NTT_THREADS, 2) k_convert(ConvK C, int dir)
 {
     extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
     const int64_t poly = blockIdx.x;
     const int li = (int)(poly % C.n_limbs);
     const int pidx_ = C.lp[li];
@@ -444,23 +441,19 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_convert(ConvK C, int dir)
     uint64_t *out = C.out + (size_t)poly * N;
     uint64_t a[32];
     if (dir == 0) {
-#pragma unroll
-        for (int e = 0; e < 32; e++) a[e] = in[j_L1(tid, e)];
+        load_L1(a, in);
         ntt_fwd(a, sm, P);
         __syncthreads(); // in may alias out
-#pragma unroll
-        for (int e = 0; e < 32; e++) out[j_L3(tid, e)] = a[e];
+        store_L3(out, a);
     } else {
-#pragma unroll
-        for (int e = 0; e < 32; e++) a[e] = in[j_L3(tid, e)];
+        load_L3(a, in);
         ntt_inv(a, sm, P);
         __syncthreads();
-#pragma unroll
-        for (int e = 0; e < 32; e++) out[j_L1(tid, e)] = a[e];
+        store_L1(out, a);
     }
 }
 
-// keys: canonical coefficients -> NTT domain Shoup pairs
+// keys: canonical coefficients -> NTT domain Shoup pairs (storage order pos_L3)
 __global__ void __launch_bounds__(NTT_THREADS, 2) k_key_ntt(ConvK C, ulonglong2 *dst)
 {
     extern __shared__ uint64_t sm[];
@@ -470,13 +463,12 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_key_ntt(ConvK C, ulonglong2 
     const int pidx_ = C.lp[li];
     const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
     uint64_t a[32];
-#pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = C.in[(size_t)poly * N + j_L1(tid, e)];
+    load_L1(a, C.in + (size_t)poly * N);
     ntt_fwd(a, sm, P);
 #pragma unroll
     for (int e = 0; e < 32; e++) {
         const uint64_t w = a[e];
-        dst[(size_t)poly * N + j_L3(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
+        dst[(size_t)poly * N + pos_L3(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
     }
 }
 
@@ -810,9 +802,9 @@ static int64_t chunk_pairs(int64_t total)
 
 size_t bm_match_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, int32_t order)
 {
-    (void)order;
     if (!prm || n_sets <= 0 || nq <= 0) return 0;
-    return (size_t)chunk_pairs(n_sets * (int64_t)nq) * WS_POLYS * N * sizeof(uint64_t);
+    const int polys = order == BM_ORDER_PAPER ? WS_POLYS_PAPER : WS_POLYS;
+    return (size_t)chunk_pairs(n_sets * (int64_t)nq) * polys * N * sizeof(uint64_t);
 }
 
 void bm_set_profiling(int32_t on)
@@ -875,11 +867,9 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     K.D2 = K.D01 + 4 * P1;
     K.XC = K.D2 + 2 * P1;
     K.XU = K.XC + 2 * P1;
-    K.Y = K.XU + 4 * P1;
-    K.U = K.Y + 2 * P1;
-    K.C = K.U + 2 * P1;
-    K.Cn = K.C + 2 * P1;
-    K.XP = K.Cn + 2 * P1;
+    K.ACC = order == BM_ORDER_PAPER ? K.XU + 4 * P1 : nullptr;
+    const CtBuf bufC = order == BM_ORDER_PAPER ? CtBuf{K.ACC, 2 * N} : CtBuf{K.XU, 4 * N};
+    const CtBuf bufD = CtBuf{K.XU + 2 * N, 4 * N};
 
     bool prof;
     {
@@ -919,12 +909,11 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             k_ks_intt<<<4 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
             end();
             beg(3, 2 * np);
-            k_rescale_ntt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, r > 0 ? 1 : 0);
+            k_rescale_ntt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             end();
             rc = launch_check();
         }
-        const uint64_t *cin = K.C;
-        uint64_t *cout = K.Cn;
+        CtBuf cin = bufC, cout = bufD;
         for (int i = 1; i <= log_s && !rc; i++) {
             const uint64_t r = (uint64_t)1 << (i - 1);
             const uint32_t g = (uint32_t)powmod_d(5, r, 2 * N);
@@ -936,13 +925,13 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             k_rot_ks<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
             end();
             rc = launch_check();
-            const uint64_t *t = cin;
+            CtBuf t = cin;
             cin = cout;
-            cout = const_cast<uint64_t *>(t);
+            cout = t;
         }
         if (log_s == 0 && !rc) {
             beg(6, 2 * np);
-            k_out_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            k_out_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin);
             end();
             rc = launch_check();
         }

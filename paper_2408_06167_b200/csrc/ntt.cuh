@@ -52,6 +52,17 @@ BM_D int j_L2(int tid, int e)
 }
 BM_D int j_L3(int tid, int e) { return 16 * (tid + 256 * (e >> 4)) + (e & 15); }
 
+// Device storage order of NTT-domain polynomials: the element thread tid holds in register e
+// of layout L3 lives at pos_L3(tid, e) = 512 (e/2) + 2 tid + (e&1), so that every NTT-domain
+// global access is one coalesced 16-byte vector per lane (512 contiguous bytes per warp) for
+// the register pair (e, e+1).  j_of_pos inverts it (used by the automorphism gathers).
+BM_D int pos_L3(int tid, int e) { return 512 * (e >> 1) + 2 * tid + (e & 1); }
+BM_D int j_of_pos(int pos)
+{
+    const int tid = (pos >> 1) & 255, e = 2 * (pos >> 9) + (pos & 1);
+    return j_L3(tid, e);
+}
+
 template <int FROM, int TO>
 BM_D void exchange(uint64_t a[32], uint64_t *sm)
 {
