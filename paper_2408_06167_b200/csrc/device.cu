@@ -1,7 +1,7 @@
 // device.cu -- sm_100a kernels and the device-facing C ABI of libblindmatch.
 //
 // Hot path (bm_match, HE-C^3) per (query, set) pair, hoisted order
-// (reading R8), one 256-thread CTA per polynomial transform:
+// (reading R8), one 512-thread CTA per polynomial transform (ntt3.cuh):
 //   K1 k_tensor_intt  (pair, limb)      a4: d0,d1,d2 = sum_i tensor(C_u,i, C_s,i) (Karatsuba,
 //                                        128-bit accumulation), INTT(d2) -> digits x_l
 //   K2 k_modup_ntt    (pair, 4 targets) a5: ModUp x0 -> {q1,P}, x1 -> {q0,P}, NTT
@@ -21,7 +21,8 @@
 
 #include "bm_common.cuh"
 #include "bm_host.h"
-#include "ntt.cuh"
+#include "ntt3.cuh"
+using namespace bm::v3;
 
 using namespace bm;
 typedef unsigned __int128 u128;
@@ -71,44 +72,8 @@ BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod
     return (y > (QP >> 1)) ? submod_d(r, pmod, q) : r;
 }
 
-// coalesced NTT-domain load/store of the thread's 32 registers (layout L3, storage pos_L3)
-BM_D void load_L3(uint64_t a[32], const uint64_t *p)
-{
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        ulonglong2 v = ld2(p + pos_L3(threadIdx.x, e));
-        a[e] = v.x;
-        a[e + 1] = v.y;
-    }
-}
-BM_D void store_L3(uint64_t *p, const uint64_t a[32])
-{
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) st2(p + pos_L3(threadIdx.x, e), a[e], a[e + 1]);
-}
-BM_D void load_L1(uint64_t a[32], const uint64_t *p)
-{
-#pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = p[j_L1(threadIdx.x, e)];
-}
-BM_D void store_L1(uint64_t *p, const uint64_t a[32])
-{
-#pragma unroll
-    for (int e = 0; e < 32; e++) p[j_L1(threadIdx.x, e)] = a[e];
-}
-// stage an NTT-domain polynomial (storage order) into shared memory by NTT index j
-BM_D void stage_by_j(uint64_t *sm, const uint64_t *p)
-{
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        ulonglong2 v = ld2(p + pos_L3(threadIdx.x, e));
-        sm[pidx(j_L3(threadIdx.x, e))] = v.x;
-        sm[pidx(j_L3(threadIdx.x, e + 1))] = v.y;
-    }
-}
-
 // ================================================================== K1: tensor + INTT(d2)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int part_lo, int part_hi)
+__global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
@@ -122,10 +87,10 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int pa
     uint64_t *d0p = K.D01 + ((size_t)pi * 4 + 0 + l) * N;
     uint64_t *d1p = K.D01 + ((size_t)pi * 4 + 2 + l) * N;
     uint64_t *d2p = K.D2 + ((size_t)pi * 2 + l) * N;
-    uint64_t a[32];
+    uint64_t a[E];
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        const int j = pos_L3(tid, e);
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
         u128 s0a = 0, s0b = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
         for (int i = part_lo; i < part_hi; i++) {
             const size_t off = (size_t)i * 4 * N + j;
@@ -150,32 +115,33 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_tensor_intt(MatchK K, int pa
         a[e] = d2a;
         a[e + 1] = d2b;
     }
-    ntt_inv(a, sm, P);
-    store_L1(K.XC + ((size_t)pi * 2 + l) * N, a);
+    inv_rt(a, sm, P, l);
+    store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
 }
 
 // ================================================================== K2: ModUp + NTT
 // t = 0: x0 -> q1, 1: x0 -> P, 2: x1 -> q0, 3: x1 -> P  (non-centred lift, reading R4)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_modup_ntt(MatchK K)
+__global__ void __launch_bounds__(T, 1) k_modup_ntt(MatchK K)
 {
     extern __shared__ uint64_t sm[];
     const int64_t pi = blockIdx.x >> 2;
     const int t = blockIdx.x & 3;
-    uint64_t a[32];
-    load_L1(a, K.XC + ((size_t)pi * 2 + (t >> 1)) * N);
+    uint64_t a[E];
+    load_coef(a, K.XC + ((size_t)pi * 2 + (t >> 1)) * N);
     if (t == 0) {
 #pragma unroll
-        for (int e = 0; e < 32; e++) a[e] = reduce64(a[e], K.pr[1].q, K.pr[1].one_p);
+        for (int e = 0; e < E; e++) a[e] = reduce64(a[e], K.pr[1].q, K.pr[1].one_p);
     }
+    const int tp = (t == 0) ? 1 : (t == 2) ? 0 : 2;
     const PrimeK P = (t == 0) ? K.pr[1] : (t == 2) ? K.pr[0] : K.pr[2];
-    ntt_fwd(a, sm, P);
-    store_L3(K.XU + ((size_t)pi * 4 + t) * N, a);
+    fwd_rt(a, sm, P, tp);
+    store_eval(K.XU + ((size_t)pi * 4 + t) * N, a);
 }
 
 // ================================================================== K3: key-switch inner product + INTT
 // block (pair, c, w): w = 0 -> Y_c = INTT_P(KS_c[P]);  w = 1 -> U_c = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
 // KS_c[P] = x0~ rlk0[c][P] + x1~ rlk1[c][P];  KS_c[q1] = x0~ rlk0[c][q1] + d2[q1] rlk1[c][q1]
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_ks_intt(MatchK K)
+__global__ void __launch_bounds__(T, 1) k_ks_intt(MatchK K)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
@@ -190,10 +156,10 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_ks_intt(MatchK K)
     const uint64_t *x0 = K.XU + ((size_t)pi * 4 + (w ? 0 : 1)) * N;
     const uint64_t *x1 = w ? K.D2 + ((size_t)pi * 2 + 1) * N : K.XU + ((size_t)pi * 4 + 3) * N;
     uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N; // d_c[q1]; U_c is written over it
-    uint64_t a[32];
+    uint64_t a[E];
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        const int j = pos_L3(tid, e);
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
         ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j);
         uint64_t ka = csub(shoup(u.x, ld2k(k0 + j), q) + shoup(v.x, ld2k(k1 + j), q), P.q2);
         uint64_t kb = csub(shoup(u.y, ld2k(k0 + j + 1), q) + shoup(v.y, ld2k(k1 + j + 1), q), P.q2);
@@ -205,14 +171,14 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_ks_intt(MatchK K)
         a[e] = ka;
         a[e + 1] = kb;
     }
-    ntt_inv(a, sm, P);
-    store_L1(w ? dc : K.XC + ((size_t)pi * 2 + c) * N, a);
+    inv_rt(a, sm, P, w ? 1 : 2);
+    store_coef(w ? dc : K.XC + ((size_t)pi * 2 + c) * N, a);
 }
 
 // ================================================================== K4: ModDown + rescale + NTT_q0
 // Out_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - NTT_q0(P^-1 y^ + z^)), with y^ = centred_P(Y_c),
 // R = U_c - P^-1 y^ (mod q1), z^ = centred_q1(R).  accumulate: dst += Out (paper order).
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf dst, int accumulate)
+__global__ void __launch_bounds__(T, 1) k_rescale_ntt(MatchK K, CtBuf dst, int accumulate)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
@@ -220,10 +186,10 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf 
     const int c = blockIdx.x & 1;
     const uint64_t q0 = K.pr[0].q, q1 = K.pr[1].q;
     const uint64_t *yi = K.XC + ((size_t)pi * 2 + c) * N, *ui = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N;
-    uint64_t a[32];
+    uint64_t a[E];
 #pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const int j = j_L1(tid, e);
+    for (int e = 0; e < E; e++) {
+        const int j = j_M1(tid, e);
         const uint64_t y = yi[j], u = ui[j];
         const uint64_t y1 = centredP_mod(y, q1, K.pr[1].one_p, K.pmod[1]);
         const uint64_t R = submod_d(u, csub(shoup(y1, K.pinv[1], q1), q1), q1);
@@ -231,7 +197,7 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf 
         const uint64_t y0 = centredP_mod(y, q0, K.pr[0].one_p, K.pmod[0]);
         a[e] = csub(csub(shoup(y0, K.pinv[0], q0), q0) + z0, q0);
     }
-    ntt_fwd(a, sm, K.pr[0]);
+    fwd<0>(a, sm, K.pr[0]);
     const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + 0) * N;
     const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + 0) * N;
     const uint64_t *x0 = K.D2 + ((size_t)pi * 2 + 0) * N, *x1 = K.XU + ((size_t)pi * 4 + 2) * N;
@@ -239,8 +205,8 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf 
     uint64_t *co = dst.at(pi, c);
     const uint64_t q2 = 2 * q0;
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-        const int j = pos_L3(tid, e);
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
         ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
         uint64_t ksa = csub(csub(shoup(u.x, ld2k(k0 + j), q0) + shoup(v.x, ld2k(k1 + j), q0), q2), q0);
         uint64_t ksb = csub(csub(shoup(u.y, ld2k(k0 + j + 1), q0) + shoup(v.y, ld2k(k1 + j + 1), q0), q2), q0);
@@ -259,24 +225,24 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rescale_ntt(MatchK K, CtBuf 
 
 // ================================================================== ladder (a7)
 // K5: x = INTT_q0(sigma_g(c1)) (coefficients in [0,q0), lifted to P as is), XP = NTT_P(x)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_digit(MatchK K, CtBuf cin, uint32_t g)
+__global__ void __launch_bounds__(T, 1) k_rot_digit(MatchK K, CtBuf cin, uint32_t g)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
     stage_by_j(sm, cin.at(pi, 1));
     __syncthreads();
-    uint64_t a[32];
+    uint64_t a[E];
 #pragma unroll
-    for (int e = 0; e < 32; e++) a[e] = sm[pidx(auto_perm(j_L3(tid, e), g))];
-    ntt_inv(a, sm, K.pr[0]);
-    ntt_fwd(a, sm, K.pr[2]);
-    store_L3(K.XC + (size_t)pi * 2 * N, a);
+    for (int e = 0; e < E; e++) a[e] = sm[pidx(auto_perm(j_M4(tid, e), g))];
+    inv<0>(a, sm, K.pr[0]);
+    fwd<2>(a, sm, K.pr[2]);
+    store_eval(K.XC + (size_t)pi * 2 * N, a);
 }
 
 // K6: KS_c = XP * gk[c][P] -> INTT_P -> y^ -> NTT_q0;  KS'_c = (sigma(c1) gk[c][q0] - NTT(y^)) P^-1;
 //     cout_c = cin_c + [c = 0] sigma(c0) + KS'_c; last step: out_c = INTT_q0(cout_c) -> d_out (a8)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout, int rot, uint32_t g,
+__global__ void __launch_bounds__(T, 1) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout, int rot, uint32_t g,
                                                            int last)
 {
     extern __shared__ uint64_t sm[];
@@ -285,13 +251,13 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, 
     const int c = blockIdx.x & 1;
     const uint64_t q0 = K.pr[0].q;
     const ulonglong2 *gq = K.gk + ((size_t)(rot * 2 + c) * 2 + 0) * N; // q0 limb
-    uint64_t a[32];
+    uint64_t a[E];
     {
         const ulonglong2 *gp = gq + N; // P limb
         const uint64_t *xp = K.XC + (size_t)pi * 2 * N;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-            const int j = pos_L3(tid, e);
+        for (int e = 0; e < E; e += 2) {
+            const int j = pos_M4(tid, e);
             ulonglong2 x = ld2(xp + j);
             a[e] = shoup(x.x, ld2k(gp + j), QP);
             a[e + 1] = shoup(x.y, ld2k(gp + j + 1), QP);
@@ -299,15 +265,16 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, 
     }
     // phase 0: INTT_P; phase 1: NTT_q0; phase 2 (last step only): INTT_q0 of the new C
     for (int ph = 0;; ph++) {
-        if (ph == 1) ntt_fwd(a, sm, K.pr[0]);
-        else ntt_inv(a, sm, ph == 0 ? K.pr[2] : K.pr[0]);
+        if (ph == 1) fwd<0>(a, sm, K.pr[0]);
+        else if (ph == 0) inv<2>(a, sm, K.pr[2]);
+        else inv<0>(a, sm, K.pr[0]);
         if (ph == 0) {
 #pragma unroll
-            for (int e = 0; e < 32; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
+            for (int e = 0; e < E; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
             continue;
         }
         if (ph == 2) {
-            store_L1(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
+            store_coef(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
             break;
         }
         // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
@@ -315,9 +282,9 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, 
         stage_by_j(sm, cin.at(pi, 1));
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 32; e++) {
-            const uint64_t x = sm[pidx(auto_perm(j_L3(tid, e), g))];
-            const uint64_t ks = csub(shoup(x, ld2k(gq + pos_L3(tid, e)), q0), q0);
+        for (int e = 0; e < E; e++) {
+            const uint64_t x = sm[pidx(auto_perm(j_M4(tid, e), g))];
+            const uint64_t ks = csub(shoup(x, ld2k(gq + pos_M4(tid, e)), q0), q0);
             a[e] = csub(shoup(submod_d(ks, a[e], q0), K.pinv[0], q0), q0);
         }
         if (c == 0) {
@@ -325,32 +292,32 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_rot_ks(MatchK K, CtBuf cin, 
             stage_by_j(sm, cin.at(pi, 0));
             __syncthreads();
 #pragma unroll
-            for (int e = 0; e < 32; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_L3(tid, e), g))], q0);
+            for (int e = 0; e < E; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_M4(tid, e), g))], q0);
         }
         const uint64_t *cc = cin.at(pi, c);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-            ulonglong2 v = ld2(cc + pos_L3(tid, e));
+        for (int e = 0; e < E; e += 2) {
+            ulonglong2 v = ld2(cc + pos_M4(tid, e));
             a[e] = csub(a[e] + v.x, q0);
             a[e + 1] = csub(a[e + 1] + v.y, q0);
         }
         if (!last) {
-            store_L3(cout.at(pi, c), a);
+            store_eval(cout.at(pi, c), a);
             break;
         }
     }
 }
 
 // K7: output INTT when there is no ladder (s = 1)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_out_intt(MatchK K, CtBuf cin)
+__global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
 {
     extern __shared__ uint64_t sm[];
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
-    uint64_t a[32];
-    load_L3(a, cin.at(pi, c));
-    ntt_inv(a, sm, K.pr[0]);
-    store_L1(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
+    uint64_t a[E];
+    load_eval(a, cin.at(pi, c));
+    inv<0>(a, sm, K.pr[0]);
+    store_coef(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
 }
 
 // ================================================================== encryption / conversion / keys
@@ -365,8 +332,8 @@ struct EncK {
 // sample a small polynomial of stream st into sm (residues mod q), adding pt if given
 BM_D void sample_to_smem(uint64_t *sm, const Stream &st, int gauss, uint64_t q, uint64_t one_p, const int64_t *pt)
 {
-    for (int r = 0; r < 4; r++) {
-        const int b = threadIdx.x + 256 * r;
+    for (int r = 0; r < N / 8 / T; r++) {
+        const int b = threadIdx.x + T * r;
         uint64_t d[8];
         chacha_draws(st, (uint32_t)b, d);
 #pragma unroll
@@ -384,38 +351,38 @@ BM_D void sample_to_smem(uint64_t *sm, const Stream &st, int gauss, uint64_t q, 
     }
 }
 
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_encrypt(EncK E)
+__global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
     const int64_t ct = blockIdx.x >> 1;
     const int l = blockIdx.x & 1;
-    const uint64_t o = E.first_obj + (uint64_t)ct;
-    const PrimeK P = l ? E.pr[1] : E.pr[0];
+    const uint64_t o = Ek.first_obj + (uint64_t)ct;
+    const PrimeK P = l ? Ek.pr[1] : Ek.pr[0];
     const uint64_t q = P.q;
-    uint64_t *c0 = E.out + ((size_t)ct * 4 + 0 + l) * N;
-    uint64_t *c1 = E.out + ((size_t)ct * 4 + 2 + l) * N;
-    const ulonglong2 *pb = E.pk + (size_t)(0 + l) * N, *pa = E.pk + (size_t)(2 + l) * N;
-    uint64_t a[32];
+    uint64_t *c0 = Ek.out + ((size_t)ct * 4 + 0 + l) * N;
+    uint64_t *c1 = Ek.out + ((size_t)ct * 4 + 2 + l) * N;
+    const ulonglong2 *pb = Ek.pk + (size_t)(0 + l) * N, *pa = Ek.pk + (size_t)(2 + l) * N;
+    uint64_t a[E];
     // phase 0: NTT(u) -> kept in c0 until phase 2;  phase 1: c1 = u a + e1;  phase 2: c0 = u b + e0 + pt
     for (int ph = 0; ph < 3; ph++) {
         __syncthreads();
         const uint32_t purpose = ph == 0 ? P_ENC_U : ph == 1 ? P_ENC_E1 : P_ENC_E0;
-        sample_to_smem(sm, make_stream(E.seed, purpose, o, 0), ph != 0, q, P.one_p,
-                       ph == 2 ? E.pt + (size_t)ct * N : nullptr);
+        sample_to_smem(sm, make_stream(Ek.seed, purpose, o, 0), ph != 0, q, P.one_p,
+                       ph == 2 ? Ek.pt + (size_t)ct * N : nullptr);
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 32; e++) a[e] = sm[pidx(j_L1(tid, e))];
-        ntt_fwd(a, sm, P);
+        for (int e = 0; e < E; e++) a[e] = sm[pidx(j_M1(tid, e))];
+        fwd_rt(a, sm, P, l);
         if (ph == 0) {
-            store_L3(c0, a);
+            store_eval(c0, a);
             continue;
         }
         uint64_t *dst = ph == 1 ? c1 : c0;
         const ulonglong2 *key = ph == 1 ? pa : pb;
 #pragma unroll
-        for (int e = 0; e < 32; e++) {
-            const int j = pos_L3(tid, e);
+        for (int e = 0; e < E; e++) {
+            const int j = pos_M4(tid, e);
             dst[j] = csub(csub(shoup(c0[j], ld2k(key + j), q) + a[e], 2 * q), q);
         }
     }
@@ -430,7 +397,7 @@ struct ConvK {
 };
 
 // one block per polynomial; dir 0: coefficient -> NTT, 1: NTT -> coefficient
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_convert(ConvK C, int dir)
+__global__ void __launch_bounds__(T, 1) k_convert(ConvK C, int dir)
 {
     extern __shared__ uint64_t sm[];
     const int64_t poly = blockIdx.x;
@@ -439,22 +406,22 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_convert(ConvK C, int dir)
     const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
     const uint64_t *in = C.in + (size_t)poly * N;
     uint64_t *out = C.out + (size_t)poly * N;
-    uint64_t a[32];
+    uint64_t a[E];
     if (dir == 0) {
-        load_L1(a, in);
-        ntt_fwd(a, sm, P);
+        load_coef(a, in);
+        fwd_rt(a, sm, P, pidx_);
         __syncthreads(); // in may alias out
-        store_L3(out, a);
+        store_eval(out, a);
     } else {
-        load_L3(a, in);
-        ntt_inv(a, sm, P);
+        load_eval(a, in);
+        inv_rt(a, sm, P, pidx_);
         __syncthreads();
-        store_L1(out, a);
+        store_coef(out, a);
     }
 }
 
 // keys: canonical coefficients -> NTT domain Shoup pairs (storage order pos_L3)
-__global__ void __launch_bounds__(NTT_THREADS, 2) k_key_ntt(ConvK C, ulonglong2 *dst)
+__global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
@@ -462,13 +429,13 @@ __global__ void __launch_bounds__(NTT_THREADS, 2) k_key_ntt(ConvK C, ulonglong2 
     const int li = (int)(poly % C.n_limbs);
     const int pidx_ = C.lp[li];
     const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
-    uint64_t a[32];
-    load_L1(a, C.in + (size_t)poly * N);
-    ntt_fwd(a, sm, P);
+    uint64_t a[E];
+    load_coef(a, C.in + (size_t)poly * N);
+    fwd_rt(a, sm, P, pidx_);
 #pragma unroll
-    for (int e = 0; e < 32; e++) {
+    for (int e = 0; e < E; e++) {
         const uint64_t w = a[e];
-        dst[(size_t)poly * N + pos_L3(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
+        dst[(size_t)poly * N + pos_M4(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
     }
 }
 
@@ -627,7 +594,7 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     K.out = nullptr;
     K.n_limbs = n_limbs;
     for (int i = 0; i < 3; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
-    k_key_ntt<<<(unsigned)n_polys, NTT_THREADS, SMEM_BYTES>>>(K, dst);
+    k_key_ntt<<<(unsigned)n_polys, T, SMEM_BYTES>>>(K, dst);
     int rc = launch_check();
     if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
     cudaFree(tmp);
@@ -708,15 +675,15 @@ int bm_encrypt(const bm_params *prm, const bm_pk_dev *pk, const int64_t *d_pt, i
     DevCtx *C;
     int rc = ctx_get(&C);
     if (rc) return rc;
-    EncK E;
-    E.pr[0] = C->pr[0];
-    E.pr[1] = C->pr[1];
-    E.pk = pk->pk;
-    E.pt = d_pt;
-    E.out = d_out;
-    E.first_obj = first_obj;
-    E.seed = seed;
-    k_encrypt<<<(unsigned)(2 * n_cts), NTT_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(E);
+    EncK Ek;
+    Ek.pr[0] = C->pr[0];
+    Ek.pr[1] = C->pr[1];
+    Ek.pk = pk->pk;
+    Ek.pt = d_pt;
+    Ek.out = d_out;
+    Ek.first_obj = first_obj;
+    Ek.seed = seed;
+    k_encrypt<<<(unsigned)(2 * n_cts), T, SMEM_BYTES, (cudaStream_t)stream>>>(Ek);
     return launch_check();
 }
 
@@ -774,7 +741,7 @@ static int convert(const bm_params *prm, const uint64_t *in, int64_t n_cts, int3
     K.lp[0] = 0;
     K.lp[1] = 1;
     K.lp[2] = 2;
-    k_convert<<<(unsigned)(n_cts * 2 * n_limbs), NTT_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(K, dir);
+    k_convert<<<(unsigned)(n_cts * 2 * n_limbs), T, SMEM_BYTES, (cudaStream_t)stream>>>(K, dir);
     return launch_check();
 }
 
@@ -900,16 +867,16 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
             beg(0, 2 * np);
-            k_tensor_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, lo, hi);
+            k_tensor_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, lo, hi);
             end();
             beg(1, 4 * np);
-            k_modup_ntt<<<4 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            k_modup_ntt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
             end();
             beg(2, 4 * np);
-            k_ks_intt<<<4 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K);
+            k_ks_intt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
             end();
             beg(3, 2 * np);
-            k_rescale_ntt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
+            k_rescale_ntt<<<2 * npu, T, SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             end();
             rc = launch_check();
         }
@@ -918,11 +885,11 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             const uint64_t r = (uint64_t)1 << (i - 1);
             const uint32_t g = (uint32_t)powmod_d(5, r, 2 * N);
             beg(4, 2 * np);
-            k_rot_digit<<<npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin, g);
+            k_rot_digit<<<npu, T, SMEM_BYTES, s>>>(K, cin, g);
             end();
             const int last = i == log_s;
             beg(5, (last ? 6 : 4) * np);
-            k_rot_ks<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
+            k_rot_ks<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
             end();
             rc = launch_check();
             CtBuf t = cin;
@@ -931,7 +898,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         }
         if (log_s == 0 && !rc) {
             beg(6, 2 * np);
-            k_out_intt<<<2 * npu, NTT_THREADS, SMEM_BYTES, s>>>(K, cin);
+            k_out_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin);
             end();
             rc = launch_check();
         }

@@ -1,0 +1,232 @@
+// ntt3.cuh -- NTT core v3: one 8192-point negacyclic transform per 512-thread CTA, 16
+// coefficients per thread (K1 in SURVEY.md sec. 2.2).  Same transform as ntt.cuh (CT forward
+// with psi^brev twiddles, GS inverse with N^-1 folded in; NTT(a)[j] = a(psi^(2 brev13(j)+1)))
+// and the prime-specialised lazy arithmetic of ntt2.cuh.
+//
+// 13 stages = 3 register passes of 4 stages (two shared-memory transposes) + 1 stage done on
+// lane pairs with warp shuffles.  Layouts (tid < 512, register index e < 16):
+//   M1 "coefficient": a[k]      <-> j = tid + 512 k
+//   M2:               a[k]      <-> j = 512 (tid>>5) + 32 k + (tid&31)
+//   M3:               a[k]      <-> j = 32 (tid>>1) + 2 k + (tid&1)
+//   M4 "evaluation":  a[2m + b] <-> j = 32 (tid>>1) + 4 m + 2 (tid&1) + b      (m < 8, b < 2)
+// Forward: M1 -> s0..3 -> M2 -> s4..7 -> M3 -> s8..11 -> shuffle stage s12 -> M4.
+// Inverse: M4 -> s12 (in registers) -> shuffle -> M3 -> s11..8 -> M2 -> s7..4 -> M1 -> s3..0.
+// NTT-domain polynomials are stored in M4 order at pos(tid, 2m+b) = 1024 m + 2 tid + b, so every
+// NTT-domain global access is a coalesced 16-byte vector per lane.
+#pragma once
+#include "ntt2.cuh"
+
+namespace bm {
+namespace v3 {
+
+constexpr int T = 512; // threads per CTA
+constexpr int E = 16;  // coefficients per thread
+
+BM_D int j_M1(int tid, int k) { return tid + 512 * k; }
+BM_D int j_M2(int tid, int k) { return 512 * (tid >> 5) + 32 * k + (tid & 31); }
+BM_D int j_M3(int tid, int k) { return 32 * (tid >> 1) + 2 * k + (tid & 1); }
+BM_D int j_M4(int tid, int e) { return 32 * (tid >> 1) + 4 * (e >> 1) + 2 * (tid & 1) + (e & 1); }
+BM_D int pos_M4(int tid, int e) { return 1024 * (e >> 1) + 2 * tid + (e & 1); }
+
+template <int FROM, int TO>
+BM_D void xchg(uint64_t a[E], uint64_t *sm)
+{
+    const int tid = threadIdx.x;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+        const int j = FROM == 1 ? j_M1(tid, k) : FROM == 2 ? j_M2(tid, k) : j_M3(tid, k);
+        sm[pidx(j)] = a[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+        const int j = TO == 1 ? j_M1(tid, k) : TO == 2 ? j_M2(tid, k) : j_M3(tid, k);
+        a[k] = sm[pidx(j)];
+    }
+}
+
+BM_D uint64_t shfl1(uint64_t v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+
+// ------------------------------------------------------------------ forward (M1 -> M4)
+template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
+{
+    const int tid = threadIdx.x;
+    // pass 1: s = 0..3, t = 512 (8 >> s); partner k + (8 >> s); twiddle (1<<s) + (k >> (4-s))
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        const int half = 8 >> s;
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k & half) continue;
+            ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (k >> (4 - s))));
+        }
+    }
+    xchg<1, 2>(a, sm);
+    // pass 2: s = 4..7; twiddle (1<<s) + (B << (s-4)) + (k >> (8-s)), B = warp index (uniform per warp)
+    {
+        const int B = tid >> 5;
+#pragma unroll
+        for (int s = 4; s < 8; s++) {
+            const int half = 8 >> (s - 4);
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                if (k & half) continue;
+                ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (B << (s - 4)) + (k >> (8 - s))));
+            }
+        }
+    }
+    xchg<2, 3>(a, sm);
+    // pass 3: s = 8..11; twiddle (1<<s) + (G << (s-8)) + (k >> (12-s)), G = tid >> 1
+    const int G = tid >> 1, odd = tid & 1;
+#pragma unroll
+    for (int s = 8; s < 12; s++) {
+        const int half = 8 >> (s - 8);
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k & half) continue;
+            ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (G << (s - 8)) + (k >> (12 - s))));
+        }
+    }
+    // stage 12 (t = 1) on lane pairs: the even lane takes butterflies k = 2m, the odd lane k = 2m+1
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+        const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
+        uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
+        ct4<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd));
+        a[2 * m] = reduce_bnd<PI>(x);
+        a[2 * m + 1] = reduce_bnd<PI>(y);
+    }
+}
+
+// ------------------------------------------------------------------ inverse (M4 -> M1)
+template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
+{
+    const int tid = threadIdx.x;
+    const int G = tid >> 1, odd = tid & 1;
+    // stage 12 (first executed, st = 0): in-register pairs (j, j+1)
+#pragma unroll
+    for (int m = 0; m < 8; m++) gs4<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(P.inv + 4096 + 16 * G + 2 * m + odd));
+    // back to M3: even lane keeps a[2m] and receives a[2m+1]; odd lane keeps a[2m+1]
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+        const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
+        if (odd) a[2 * m] = r;
+        else a[2 * m + 1] = r;
+    }
+    // pass 3: s = 11..8 (st = 1..4)
+#pragma unroll
+    for (int s = 11; s >= 8; s--) {
+        const int half = 8 >> (s - 8);
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k & half) continue;
+            const ulonglong2 w = ldtw(P.inv + (1 << s) + (G << (s - 8)) + (k >> (12 - s)));
+            switch (12 - s) {
+            case 1: gs4<PI, 1>(a[k], a[k + half], w); break;
+            case 2: gs4<PI, 2>(a[k], a[k + half], w); break;
+            case 3: gs4<PI, 3>(a[k], a[k + half], w); break;
+            default: gs4<PI, 4>(a[k], a[k + half], w); break;
+            }
+        }
+    }
+    xchg<3, 2>(a, sm);
+    {
+        const int B = tid >> 5;
+#pragma unroll
+        for (int s = 7; s >= 4; s--) {
+            const int half = 8 >> (s - 4);
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                if (k & half) continue;
+                const ulonglong2 w = ldtw(P.inv + (1 << s) + (B << (s - 4)) + (k >> (8 - s)));
+                switch (12 - s) {
+                case 5: gs4<PI, 5>(a[k], a[k + half], w); break;
+                case 6: gs4<PI, 6>(a[k], a[k + half], w); break;
+                case 7: gs4<PI, 7>(a[k], a[k + half], w); break;
+                default: gs4<PI, 8>(a[k], a[k + half], w); break;
+                }
+            }
+        }
+    }
+    xchg<2, 1>(a, sm);
+#pragma unroll
+    for (int s = 3; s >= 1; s--) {
+        const int half = 8 >> s;
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k & half) continue;
+            const ulonglong2 w = ldtw(P.inv + (1 << s) + (k >> (4 - s)));
+            switch (12 - s) {
+            case 9: gs4<PI, 9>(a[k], a[k + half], w); break;
+            case 10: gs4<PI, 10>(a[k], a[k + half], w); break;
+            default: gs4<PI, 11>(a[k], a[k + half], w); break;
+            }
+        }
+    }
+    // s = 0 with N^-1 folded in; inputs < B q with B of stage 12
+    constexpr uint64_t Bq = (PI == 1 ? (4ull << 12) : 4ull) * PrimeC<PI>::q;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint64_t x = a[k], y = a[k + 8];
+        a[k] = reduce_bnd<PI>(shoup4<PI>(x + y, P.ninv));
+        a[k + 8] = reduce_bnd<PI>(shoup4<PI>(x - y + Bq, P.ninv_w1));
+    }
+}
+
+BM_D void fwd_rt(uint64_t a[E], uint64_t *sm, const PrimeK &P, int pi)
+{
+    if (pi == 0) fwd<0>(a, sm, P);
+    else if (pi == 1) fwd<1>(a, sm, P);
+    else fwd<2>(a, sm, P);
+}
+BM_D void inv_rt(uint64_t a[E], uint64_t *sm, const PrimeK &P, int pi)
+{
+    if (pi == 0) inv<0>(a, sm, P);
+    else if (pi == 1) inv<1>(a, sm, P);
+    else inv<2>(a, sm, P);
+}
+
+// ------------------------------------------------------------------ global <-> register helpers
+BM_D ulonglong2 ldv(const uint64_t *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+BM_D void stv(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
+
+// NTT-domain (M4, storage pos_M4): 8 coalesced 16-byte vectors per thread
+BM_D void load_eval(uint64_t a[E], const uint64_t *p)
+{
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const ulonglong2 v = ldv(p + pos_M4(threadIdx.x, e));
+        a[e] = v.x;
+        a[e + 1] = v.y;
+    }
+}
+BM_D void store_eval(uint64_t *p, const uint64_t a[E])
+{
+#pragma unroll
+    for (int e = 0; e < E; e += 2) stv(p + pos_M4(threadIdx.x, e), a[e], a[e + 1]);
+}
+// coefficient domain (M1): coalesced 8-byte accesses
+BM_D void load_coef(uint64_t a[E], const uint64_t *p)
+{
+#pragma unroll
+    for (int k = 0; k < E; k++) a[k] = p[j_M1(threadIdx.x, k)];
+}
+BM_D void store_coef(uint64_t *p, const uint64_t a[E])
+{
+#pragma unroll
+    for (int k = 0; k < E; k++) p[j_M1(threadIdx.x, k)] = a[k];
+}
+// stage an NTT-domain polynomial into shared memory indexed by NTT index j
+BM_D void stage_by_j(uint64_t *sm, const uint64_t *p)
+{
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const ulonglong2 v = ldv(p + pos_M4(threadIdx.x, e));
+        sm[pidx(j_M4(threadIdx.x, e))] = v.x;
+        sm[pidx(j_M4(threadIdx.x, e + 1))] = v.y;
+    }
+}
+
+} // namespace v3
+} // namespace bm

@@ -1,0 +1,106 @@
+// NTT throughput microbenchmark (diagnostic, not part of the library):
+// each CTA runs `iters` x (forward + inverse) 8192-point transforms on one polynomial held in
+// registers/shared memory, for each of the three primes; checks the round trip is the identity.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../paper_2408_06167_b200/csrc/bm_common.cuh"
+#include "../paper_2408_06167_b200/csrc/bm_host.h"
+#include "../paper_2408_06167_b200/csrc/ntt3.cuh"
+using namespace bm;
+typedef unsigned __int128 u128;
+
+#ifndef MINB
+#define MINB 2
+#endif
+template <int V, int PI>
+__global__ void __launch_bounds__(256, MINB) k_bench(PrimeK P, uint64_t *data, int iters)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t a[32];
+    uint64_t *d = data + (size_t)blockIdx.x * N;
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = d[j_L1(threadIdx.x, e)];
+    for (int it = 0; it < iters; it++) {
+        if (V == 1) {
+            ntt_fwd(a, sm, P);
+            ntt_inv(a, sm, P);
+        } else {
+            ntt_fwd2<PI>(a, sm, P);
+            ntt_inv2<PI>(a, sm, P);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 32; e++) d[j_L1(threadIdx.x, e)] = a[e];
+}
+
+#ifndef MINB3
+#define MINB3 2
+#endif
+template <int PI>
+__global__ void __launch_bounds__(512, MINB3) k_bench3(PrimeK P, uint64_t *data, int iters)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t a[16];
+    uint64_t *d = data + (size_t)blockIdx.x * N;
+    v3::load_coef(a, d);
+    for (int it = 0; it < iters; it++) {
+        v3::fwd<PI>(a, sm, P);
+        v3::inv<PI>(a, sm, P);
+    }
+    v3::store_coef(d, a);
+}
+
+static ulonglong2 sp(uint64_t w, uint64_t q) { return make_ulonglong2(w, shoup_companion(w, q)); }
+
+int main(int argc, char **argv)
+{
+    int blocks = argc > 1 ? atoi(argv[1]) : 296 * 4;
+    int iters = argc > 2 ? atoi(argv[2]) : 20;
+    const size_t SM_BYTES = SMEM_WORDS * 8;
+    typedef void (*KF)(PrimeK, uint64_t *, int);
+    KF kf[3][3] = {{k_bench<1, 0>, k_bench<1, 1>, k_bench<1, 2>}, {k_bench<2, 0>, k_bench<2, 1>, k_bench<2, 2>},
+                   {k_bench3<0>, k_bench3<1>, k_bench3<2>}};
+    for (int v = 0; v < 3; v++)
+        for (int i = 0; i < 3; i++) cudaFuncSetAttribute(kf[v][i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BYTES);
+    for (int v = 0; v < 3; v++)
+    for (int pi = 0; pi < 3; pi++) {
+        const HostPrime &H = host_prime(pi);
+        std::vector<ulonglong2> tw(2 * N);
+        for (int k = 0; k < N; k++) tw[k] = sp(H.fwd[k], H.q), tw[N + k] = sp(H.inv[k], H.q);
+        ulonglong2 *dtw;
+        cudaMalloc(&dtw, tw.size() * 16);
+        cudaMemcpy(dtw, tw.data(), tw.size() * 16, cudaMemcpyHostToDevice);
+        PrimeK P;
+        P.q = H.q; P.q2 = 2 * H.q; P.fwd = dtw; P.inv = dtw + N;
+        P.ninv = sp(H.ninv, H.q);
+        P.ninv_w1 = sp(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
+        P.r64 = sp((uint64_t)(((u128)1 << 64) % H.q), H.q);
+        P.one_p = (uint64_t)(((u128)1 << 64) / H.q);
+        std::vector<uint64_t> h((size_t)blocks * N);
+        srand(pi + 1);
+        for (auto &x : h) x = (((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ rand()) % H.q;
+        uint64_t *dd;
+        cudaMalloc(&dd, h.size() * 8);
+        cudaMemcpy(dd, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        KF k = kf[v][pi];
+        const int thr = v == 2 ? 512 : 256;
+        k<<<blocks, thr, SM_BYTES>>>(P, dd, 1); // warm-up (+ round trip)
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        k<<<blocks, thr, SM_BYTES>>>(P, dd, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        std::vector<uint64_t> back(h.size());
+        cudaMemcpy(back.data(), dd, h.size() * 8, cudaMemcpyDeviceToHost);
+        bool ok = back == h;
+        double bfly = (double)blocks * iters * 2 * (N / 2) * LOGN;
+        int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+        printf("v%d prime %d: %s  %.3f ms  %.1f Gbfly/s  %.2f bfly/clk/SM (at %d MHz)  err=%s\n", v + 1, pi, ok ? "ok" : "MISMATCH", ms,
+               bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
+        cudaFree(dd); cudaFree(dtw);
+    }
+    return 0;
+}
