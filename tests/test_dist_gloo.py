@@ -1,0 +1,110 @@
+"""Multi-rank path of the scan on CPU (world size 2, gloo): DB sharded by sets, query broadcast
+from rank 0, local scan, all_to_all gather to the query-block roots (dist.py).
+The local scan is the oracle (this container has no GPU); the collective plumbing is the same
+code bench.py runs over NCCL.  The gathered result must equal the single-process scan of the
+whole DB bit for bit, and the sharded encryption must be a partition of the unsharded one."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+LOGN, D, P_PARTS = 6, 8, 2   # N = 64, S = 32, s = 4, B = 8 -> small, fast oracle
+N_TMPL, NQ, WORLD = 37, 4, 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _setup():
+    from oracle import oracle as O
+    from paper_2408_06167_b200 import inputs as I
+    S, s, B = O.layout(LOGN, D, P_PARTS)
+    T = I.random_unit(N_TMPL, D, 11)
+    Q = I.random_unit(NQ, D, 12)
+    n_sets = -(-N_TMPL // B)
+    sk, pk, rlk, gk = O.keygen(LOGN, 1, O.n_rot_for(D, P_PARTS))
+    return O, T, Q, n_sets, (sk, pk, rlk, gk)
+
+
+def _encrypt_sets(O, T, pk, first_set, n_sets):
+    S, s, B = O.layout(LOGN, D, P_PARTS)
+    z = O.pack_db(T, LOGN, D, P_PARTS, first_set, n_sets).reshape(-1, S)
+    ct = O.encrypt(LOGN, pk, O.encode(z, LOGN), first_set * P_PARTS, 2)
+    return ct.reshape(n_sets, P_PARTS, 2, 2, -1)
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    lo, cnt = pdist.shard_sets(n_sets, world, rank)
+    local_db = _encrypt_sets(O, T, pk, lo, cnt)
+    # a3: rank 0 (the client-facing main server) encrypts the query; everyone receives it
+    N = 1 << LOGN
+    q = torch.zeros((NQ, P_PARTS, 2, 2, N), dtype=torch.int64)
+    if rank == 0:
+        S = N // 2
+        qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+        q.copy_(torch.from_numpy(qc.reshape(q.shape).view(np.int64)))
+    pdist.broadcast_queries(q)
+    # local scan over this rank's sets (ragged: the last rank may hold fewer sets)
+    per = -(-n_sets // world)
+    out = torch.zeros((NQ, per, 2, N), dtype=torch.int64)
+    if cnt:
+        res, pairs = O.match(LOGN, D, P_PARTS, 0, rlk, gk, local_db, q.numpy().view(np.uint64))
+        for i, (j, t) in enumerate(pairs):
+            out[j, t] = torch.from_numpy(res[i].reshape(2, N).view(np.int64))
+    recv = pdist.gather_results(out)
+    q0, nq_local = pdist.query_block(NQ, world, rank)
+    np.save(os.path.join(out_dir, f"recv{rank}.npy"), recv.numpy())
+    np.save(os.path.join(out_dir, f"db{rank}.npy"), local_db)
+    t = pdist.max_over_ranks(float(rank + 1), torch.device("cpu"))
+    assert t == float(world)
+    dist.destroy_process_group()
+
+
+def test_two_rank_scan_matches_single_process(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(WORLD, port, str(tmp_path)), nprocs=WORLD, join=True)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    N = 1 << LOGN
+    full_db = _encrypt_sets(O, T, pk, 0, n_sets)
+    # sharded encryption is a bit-exact partition of the unsharded DB
+    parts = [np.load(tmp_path / f"db{r}.npy") for r in range(WORLD)]
+    assert np.array_equal(np.concatenate(parts), full_db)
+    S = N // 2
+    qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+    ref, pairs = O.match(LOGN, D, P_PARTS, 0, rlk, gk, full_db, qc.reshape(NQ, P_PARTS, 2, 2, N))
+    ref = ref.reshape(NQ, n_sets, 2, N)
+    per = -(-n_sets // WORLD)
+    for r in range(WORLD):
+        recv = np.load(tmp_path / f"recv{r}.npy").view(np.uint64)  # [src rank][nq/W][per][2][N]
+        q0, nql = pdist.query_block(NQ, WORLD, r)
+        for src in range(WORLD):
+            lo, cnt = pdist.shard_sets(n_sets, WORLD, src)
+            assert np.array_equal(recv[src, :, :cnt], ref[q0:q0 + nql, lo:lo + cnt])
+
+
+def test_shard_ranges_cover_and_balance():
+    from paper_2408_06167_b200 import dist as pdist
+    for T in (1, 7, 24, 4096, 131072):
+        for W in (1, 2, 4, 8):
+            got = [pdist.shard_sets(T, W, r) for r in range(W)]
+            covered = [t for lo, cnt in got for t in range(lo, lo + cnt)]
+            assert covered == list(range(T))
+            assert max(c for _, c in got) - min(c for _, c in got) <= -(-T // W)
+    assert pdist.query_block(384, 8, 3) == (144, 48)
+    with pytest.raises(AssertionError):
+        pdist.query_block(10, 4, 0)
