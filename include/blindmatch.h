@@ -157,9 +157,11 @@ int bm_match(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_
              int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
 
 /* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
- * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call, chunked so the
- * copies overlap the kernels.  Pinned host memory is strongly recommended.  d_ws must hold
- * bm_match_host_ws_bytes(...) bytes.  Synchronous (returns after h_out is written). */
+ * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call.  The queries are
+ * processed in groups (8, or BM_HOST_GROUPS): group g's upload, scan and download overlap the
+ * neighbouring groups (two device slots, two internal copy streams, the scan on `stream`).
+ * Pinned host memory is required for the overlap.  d_ws must hold bm_match_host_ws_bytes(...)
+ * bytes.  Synchronous (returns after h_out is written). */
 size_t bm_match_host_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);
 int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *h_q,
                   int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);

@@ -44,8 +44,11 @@ struct MatchK {
     const ulonglong2 *rlk, *gk;
     const uint64_t *db, *qry;
     uint64_t *out;
-    int64_t n_sets, pair0;
+    int64_t n_sets;       // sets in the DB (output row length)
+    int64_t jq0, t0, ct;  // chunk = queries [jq0, jq0+cq) x sets [t0, t0+ct); pair pi = a*ct + b
+    int32_t cq;
     int32_t p;
+    BM_D int64_t out_row(int64_t pi) const { return (jq0 + pi / ct) * n_sets + t0 + pi % ct; }
     uint64_t *D01, *D2, *XC, *XU, *ACC;
 };
 
@@ -73,50 +76,93 @@ BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod
 }
 
 // ================================================================== K1: tensor + INTT(d2)
+// One CTA per (tile of TQ x TS pairs, limb): the query and DB part values are loaded once per
+// tile and reused from registers (TQ x TS fewer reloads), then the CTA runs the tile's INTTs.
+constexpr int TQ = 2, TS = 2;
+
 __global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x >> 1;
     const int l = blockIdx.x & 1;
-    const int64_t g = K.pair0 + pi, jq = g / K.n_sets, t = g - jq * K.n_sets;
+    const int64_t tile = blockIdx.x >> 1;
+    const int64_t n_tb = (K.ct + TS - 1) / TS;
+    const int64_t ta = tile / n_tb, tb = tile - ta * n_tb;
     const PrimeK P = l ? K.pr[1] : K.pr[0];
     const uint64_t q = P.q;
-    const uint64_t *qa = K.qry + (size_t)jq * K.p * 4 * N + (size_t)l * N;
-    const uint64_t *sb = K.db + (size_t)t * K.p * 4 * N + (size_t)l * N;
-    uint64_t *d0p = K.D01 + ((size_t)pi * 4 + 0 + l) * N;
-    uint64_t *d1p = K.D01 + ((size_t)pi * 4 + 2 + l) * N;
-    uint64_t *d2p = K.D2 + ((size_t)pi * 2 + l) * N;
-    uint64_t a[E];
+    const uint64_t *qa[TQ], *sb[TS];
+    bool vq[TQ], vs[TS];
 #pragma unroll
+    for (int u = 0; u < TQ; u++) {
+        const int64_t a = ta * TQ + u;
+        vq[u] = a < K.cq;
+        qa[u] = K.qry + (size_t)(K.jq0 + (vq[u] ? a : 0)) * K.p * 4 * N + (size_t)l * N;
+    }
+#pragma unroll
+    for (int v = 0; v < TS; v++) {
+        const int64_t b = tb * TS + v;
+        vs[v] = b < K.ct;
+        sb[v] = K.db + (size_t)(K.t0 + (vs[v] ? b : 0)) * K.p * 4 * N + (size_t)l * N;
+    }
+#pragma unroll 1
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
-        u128 s0a = 0, s0b = 0, s1a = 0, s1b = 0, s2a = 0, s2b = 0;
+        u128 s0[TQ][TS][2], s1[TQ][TS][2], s2[TQ][TS][2];
+#pragma unroll
+        for (int u = 0; u < TQ; u++)
+#pragma unroll
+            for (int v = 0; v < TS; v++)
+#pragma unroll
+                for (int h = 0; h < 2; h++) s0[u][v][h] = s1[u][v][h] = s2[u][v][h] = 0;
         for (int i = part_lo; i < part_hi; i++) {
             const size_t off = (size_t)i * 4 * N + j;
-            ulonglong2 x0 = ld2(qa + off), x1 = ld2(qa + off + 2 * N);
-            ulonglong2 y0 = ld2(sb + off), y1 = ld2(sb + off + 2 * N);
-            s0a += (u128)x0.x * y0.x;
-            s0b += (u128)x0.y * y0.y;
-            s2a += (u128)x1.x * y1.x;
-            s2b += (u128)x1.y * y1.y;
-            s1a += (u128)(x0.x + x1.x) * (y0.x + y1.x); // Karatsuba: (a0+a1)(b0+b1)
-            s1b += (u128)(x0.y + x1.y) * (y0.y + y1.y);
+            ulonglong2 x0[TQ], x1[TQ], y0[TS], y1[TS];
+#pragma unroll
+            for (int u = 0; u < TQ; u++) x0[u] = ld2(qa[u] + off), x1[u] = ld2(qa[u] + off + 2 * N);
+#pragma unroll
+            for (int v = 0; v < TS; v++) y0[v] = ld2(sb[v] + off), y1[v] = ld2(sb[v] + off + 2 * N);
+#pragma unroll
+            for (int u = 0; u < TQ; u++)
+#pragma unroll
+                for (int v = 0; v < TS; v++) {
+                    s0[u][v][0] += (u128)x0[u].x * y0[v].x;
+                    s0[u][v][1] += (u128)x0[u].y * y0[v].y;
+                    s2[u][v][0] += (u128)x1[u].x * y1[v].x;
+                    s2[u][v][1] += (u128)x1[u].y * y1[v].y;
+                    s1[u][v][0] += (u128)(x0[u].x + x1[u].x) * (y0[v].x + y1[v].x); // Karatsuba
+                    s1[u][v][1] += (u128)(x0[u].y + x1[u].y) * (y0[v].y + y1[v].y);
+                }
         }
-        uint64_t d0a = reduce128((uint64_t)(s0a >> 64), (uint64_t)s0a, q, P.r64, P.one_p);
-        uint64_t d0b = reduce128((uint64_t)(s0b >> 64), (uint64_t)s0b, q, P.r64, P.one_p);
-        uint64_t d2a = reduce128((uint64_t)(s2a >> 64), (uint64_t)s2a, q, P.r64, P.one_p);
-        uint64_t d2b = reduce128((uint64_t)(s2b >> 64), (uint64_t)s2b, q, P.r64, P.one_p);
-        uint64_t ka = reduce128((uint64_t)(s1a >> 64), (uint64_t)s1a, q, P.r64, P.one_p);
-        uint64_t kb = reduce128((uint64_t)(s1b >> 64), (uint64_t)s1b, q, P.r64, P.one_p);
-        st2(d0p + j, d0a, d0b);
-        st2(d1p + j, submod_d(submod_d(ka, d0a, q), d2a, q), submod_d(submod_d(kb, d0b, q), d2b, q));
-        st2(d2p + j, d2a, d2b);
-        a[e] = d2a;
-        a[e + 1] = d2b;
+#pragma unroll
+        for (int u = 0; u < TQ; u++)
+#pragma unroll
+            for (int v = 0; v < TS; v++) {
+                if (!(vq[u] && vs[v])) continue;
+                const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
+                uint64_t d0[2], d1[2], d2[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    d0[h] = reduce128((uint64_t)(s0[u][v][h] >> 64), (uint64_t)s0[u][v][h], q, P.r64, P.one_p);
+                    d2[h] = reduce128((uint64_t)(s2[u][v][h] >> 64), (uint64_t)s2[u][v][h], q, P.r64, P.one_p);
+                    const uint64_t kk = reduce128((uint64_t)(s1[u][v][h] >> 64), (uint64_t)s1[u][v][h], q, P.r64, P.one_p);
+                    d1[h] = submod_d(submod_d(kk, d0[h], q), d2[h], q);
+                }
+                st2(K.D01 + ((size_t)pi * 4 + 0 + l) * N + j, d0[0], d0[1]);
+                st2(K.D01 + ((size_t)pi * 4 + 2 + l) * N + j, d1[0], d1[1]);
+                st2(K.D2 + ((size_t)pi * 2 + l) * N + j, d2[0], d2[1]);
+            }
     }
-    inv_rt(a, sm, P, l);
-    store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
+    // INTT(d2) of every pair of the tile (the thread re-reads exactly the elements it wrote)
+#pragma unroll 1
+    for (int w = 0; w < TQ * TS; w++) {
+        const int u = w / TS, v = w % TS;
+        if (!(vq[u] && vs[v])) continue;
+        const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
+        uint64_t a[E];
+        load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
+        inv_rt(a, sm, P, l);
+        store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
+    }
 }
 
 // ================================================================== K2: ModUp + NTT
@@ -274,7 +320,7 @@ __global__ void __launch_bounds__(T, 1) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout
             continue;
         }
         if (ph == 2) {
-            store_coef(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
+            store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
             break;
         }
         // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
@@ -317,7 +363,7 @@ __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
     uint64_t a[E];
     load_eval(a, cin.at(pi, c));
     inv<0>(a, sm, K.pr[0]);
-    store_coef(K.out + ((size_t)(K.pair0 + pi) * 2 + c) * N, a);
+    store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
 }
 
 // ================================================================== encryption / conversion / keys
@@ -859,15 +905,23 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     };
 
     const int log_s = prm->log_s;
-    for (int64_t p0 = 0; p0 < total && !rc; p0 += ch) {
-        const int64_t np = (total - p0 < ch) ? total - p0 : ch;
-        K.pair0 = p0;
+    // chunks are rectangles of cq queries x ct sets (cq * ct <= ch pairs)
+    const int64_t ct_full = n_sets < ch ? n_sets : ch;
+    const int64_t cq_full = ch / ct_full < nq ? ch / ct_full : nq;
+    for (int64_t jq0 = 0; jq0 < nq && !rc; jq0 += cq_full)
+    for (int64_t t0 = 0; t0 < n_sets && !rc; t0 += ct_full) {
+        K.jq0 = jq0;
+        K.t0 = t0;
+        K.cq = (int32_t)(nq - jq0 < cq_full ? nq - jq0 : cq_full);
+        K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
+        const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
+        const unsigned ntiles = (unsigned)(((K.cq + TQ - 1) / TQ) * ((K.ct + TS - 1) / TS));
         const int n_rounds = order == BM_ORDER_HOISTED ? 1 : prm->p;
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
             beg(0, 2 * np);
-            k_tensor_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, lo, hi);
+            k_tensor_intt<<<2 * ntiles, T, SMEM_BYTES, s>>>(K, lo, hi);
             end();
             beg(1, 4 * np);
             k_modup_ntt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
@@ -919,11 +973,23 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     return rc;
 }
 
+// End-to-end scan from host buffers: the queries are processed in groups; group g's query
+// upload (copy stream), scan (caller's stream) and result download (second copy stream) overlap
+// with the neighbouring groups through two device buffer slots and events.
+static int host_groups(int32_t nq)
+{
+    int g = 8;
+    if (const char *e = getenv("BM_HOST_GROUPS")) g = atoi(e) > 0 ? atoi(e) : g;
+    return nq < g ? nq : g;
+}
+
 size_t bm_match_host_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, int32_t order)
 {
     if (!prm || n_sets <= 0 || nq <= 0) return 0;
-    const size_t qbytes = (size_t)nq * prm->p * 4 * N * 8, obytes = (size_t)nq * n_sets * 2 * N * 8;
-    return qbytes + obytes + bm_match_ws_bytes(prm, n_sets, nq, order);
+    const int G = host_groups(nq);
+    const int64_t gq = (nq + G - 1) / G;
+    const size_t qbytes = (size_t)gq * prm->p * 4 * N * 8, obytes = (size_t)gq * n_sets * 2 * N * 8;
+    return 2 * (qbytes + obytes) + bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order);
 }
 
 int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
@@ -934,15 +1000,59 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
     if (n_sets == 0 || nq == 0) return BM_OK;
     if (!h_q || !h_out || !d_ws) return BM_ERR_INVALID_ARG;
     if (ws_bytes < bm_match_host_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t qbytes = (size_t)nq * prm->p * 4 * N * 8, obytes = (size_t)nq * n_sets * 2 * N * 8;
-    uint64_t *dq = (uint64_t *)d_ws, *dout = dq + qbytes / 8;
-    void *mws = dout + obytes / 8;
-    if (cudaMemcpyAsync(dq, h_q, qbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return BM_ERR_CUDA;
-    int rc = bm_match(prm, evk, d_db, n_sets, dq, nq, dout, mws, ws_bytes - qbytes - obytes, order, stream);
-    if (rc) return rc;
-    if (cudaMemcpyAsync(h_out, dout, obytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return BM_ERR_CUDA;
-    return cudaStreamSynchronize(s) == cudaSuccess ? BM_OK : BM_ERR_CUDA;
+    const int G = host_groups(nq);
+    const int64_t gq = (nq + G - 1) / G;
+    const size_t qrow = (size_t)prm->p * 4 * N, orow = (size_t)n_sets * 2 * N; // u64 per query
+    uint64_t *dq[2], *dout[2];
+    dq[0] = (uint64_t *)d_ws;
+    dq[1] = dq[0] + gq * qrow;
+    dout[0] = dq[1] + gq * qrow;
+    dout[1] = dout[0] + gq * orow;
+    void *mws = dout[1] + gq * orow;
+    const size_t mws_bytes = ws_bytes - 2 * gq * (qrow + orow) * 8;
+    cudaStream_t sc = (cudaStream_t)stream, su, sd;
+    if (cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking) != cudaSuccess) return BM_ERR_CUDA;
+    if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(su);
+        return BM_ERR_CUDA;
+    }
+    const int ngroups = (int)((nq + gq - 1) / gq);
+    std::vector<cudaEvent_t> ev_up(ngroups), ev_done(ngroups), ev_down(ngroups);
+    for (int g = 0; g < ngroups; g++) {
+        cudaEventCreateWithFlags(&ev_up[g], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_down[g], cudaEventDisableTiming);
+    }
+    int rc = BM_OK;
+    for (int g = 0; g < ngroups && !rc; g++) {
+        const int slot = g & 1;
+        const int64_t q0 = g * gq, nqg = nq - q0 < gq ? nq - q0 : gq;
+        // the query slot is free once the scan of group g-2 has consumed it
+        if (g >= 2) cudaStreamWaitEvent(su, ev_done[g - 2], 0);
+        if (cudaMemcpyAsync(dq[slot], h_q + q0 * qrow, nqg * qrow * 8, cudaMemcpyHostToDevice, su) != cudaSuccess)
+            rc = BM_ERR_CUDA;
+        cudaEventRecord(ev_up[g], su);
+        cudaStreamWaitEvent(sc, ev_up[g], 0);
+        // the output slot is free once group g-2's results are downloaded
+        if (g >= 2) cudaStreamWaitEvent(sc, ev_down[g - 2], 0);
+        if (!rc) rc = bm_match(prm, evk, d_db, n_sets, dq[slot], (int32_t)nqg, dout[slot], mws, mws_bytes, order, stream);
+        cudaEventRecord(ev_done[g], sc);
+        cudaStreamWaitEvent(sd, ev_done[g], 0);
+        if (!rc && cudaMemcpyAsync(h_out + q0 * orow, dout[slot], nqg * orow * 8, cudaMemcpyDeviceToHost, sd) != cudaSuccess)
+            rc = BM_ERR_CUDA;
+        cudaEventRecord(ev_down[g], sd);
+    }
+    if (cudaStreamSynchronize(sd) != cudaSuccess || cudaStreamSynchronize(su) != cudaSuccess ||
+        cudaStreamSynchronize(sc) != cudaSuccess)
+        rc = rc ? rc : BM_ERR_CUDA;
+    for (int g = 0; g < ngroups; g++) {
+        cudaEventDestroy(ev_up[g]);
+        cudaEventDestroy(ev_done[g]);
+        cudaEventDestroy(ev_down[g]);
+    }
+    cudaStreamDestroy(su);
+    cudaStreamDestroy(sd);
+    return rc;
 }
 
 int bm_sync(void *stream)

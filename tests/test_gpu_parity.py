@@ -149,9 +149,11 @@ def test_paper_order_parity(env, O):
     assert not np.array_equal(hoisted[1, 3], got[1, 3])  # reading R8: orders differ in residues
 
 
-def test_chunking_ragged(env, O, monkeypatch):
-    """Pairs processed in chunks of 7 (BM_CHUNK_PAIRS): 5 queries x 3 sets = 15 pairs -> 7,7,1."""
-    monkeypatch.setenv("BM_CHUNK_PAIRS", "7")
+@pytest.mark.parametrize("chunk", ["7", "1"])
+def test_chunking_ragged(env, O, monkeypatch, chunk):
+    """Pairs processed in small chunks (BM_CHUNK_PAIRS): 5 queries x 2 sets; chunk 7 gives query
+    blocks of 3 + 2 (ragged 2x2 tensor tiles), chunk 1 splits the set range too."""
+    monkeypatch.setenv("BM_CHUNK_PAIRS", chunk)
     T = I.random_unit(300, 32, 5)
     Q = I.random_unit(5, 32, 6)
     st = Setup(env, O, 32, 2, T, Q)       # s = 16, B = 256 -> 2 sets; last set ragged (44 templates)
@@ -198,3 +200,19 @@ def test_edge_cases_and_errors(env, O):
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=7)
     assert e.value.name == "BM_ERR_INVALID_ARG"
+
+
+@pytest.mark.parametrize("groups", ["3", "8"])
+def test_match_host_pipelined_equals_device(env, O, monkeypatch, groups):
+    """bm_match_host (host buffers, grouped + overlapped copies) == bm_match on device buffers."""
+    torch, B = env
+    monkeypatch.setenv("BM_HOST_GROUPS", groups)
+    T = I.templates(2, 700)
+    Q, _ = I.queries(2, 7)
+    st = Setup(env, O, 128, 8, T, Q)
+    dev_out = st.gpu_match(0)
+    h_q = st.d_q.cpu().pin_memory()
+    h_out = torch.empty((st.nq, st.n_sets, 2, 8192), dtype=torch.int64).pin_memory()
+    ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq), dtype=torch.uint8, device="cuda")
+    B.bm_match_host(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, h_out, ws)
+    assert np.array_equal(h_out.numpy().view(np.uint64), dev_out)
