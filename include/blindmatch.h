@@ -168,7 +168,7 @@ int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, i
 
 /* Per-kernel-class device time of the last bm_match on this thread when profiling is
  * enabled (bm_set_profiling(1)); classes: 0 tensor+INTT, 1 ModUp NTT, 2 key-switch INTT,
- * 3 rescale NTT, 4 rotation digit, 5 rotation key-switch, 6 output INTT.  ms[7] and
+ * 3 rescale NTT, 4 rotate-and-add ladder (fused), 5 unused, 6 output INTT (s = 1).  ms[7] and
  * launches[7] accumulate until bm_profile_reset(). */
 void bm_set_profiling(int32_t on);
 void bm_profile_reset(void);

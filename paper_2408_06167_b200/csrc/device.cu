@@ -354,6 +354,111 @@ __global__ void __launch_bounds__(T, 1) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout
     }
 }
 
+// ================================================================== fused ladder (a7 + a8)
+// One CTA runs the whole log2(s)-step rotate-and-add ladder of one pair with
+// the level-0 ciphertext C = (c0, c1) resident in shared memory (NTT domain, indexed by NTT index
+// j, padded), so C never leaves the SM between steps.  Per step r = 2^i, g = 5^r mod 2N:
+//   digit   x   = INTT_q0(sigma_g(c1)) in [0, q0), lifted to P as is (reading R4); XP = NTT_P(x)
+//   comp c  y^c = centred_P(INTT_P(XP gk_r[c][P]))
+//           c_c <- c_c + [c = 0] sigma_g(c0) + P^-1 (sigma_g(c1) gk_r[c][q0] - NTT_q0(y^c))
+// The last step leaves the NTT domain directly (INTT is linear, the rounding term y^c is already
+// in coefficient form): out_c = INTT_q0(c_c + [c = 0] sigma(c0) + P^-1 sigma(c1) gk[c][q0])
+// - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.
+constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+
+// centred_P(y) mod q0 for canonical y in [0, P), result in [0, 2 q0): y - P = y + (5 q0 - P) mod q0
+BM_D uint64_t centP_q0(uint64_t y)
+{
+    constexpr uint64_t K5 = 5 * Q0 - QP;
+    const uint64_t x = y > (QP >> 1) ? y + K5 : y;
+    const uint64_t Qe = x >> 58;
+    return x - (Qe << 58) + Qe * ((1ull << 58) - Q0);
+}
+
+__global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    uint64_t *ks1 = K.XC + (size_t)pi * 2 * N, *tsc = ks1 + N;
+    const ulonglong2 pinv = K.pinv[0];
+    stage_by_j(S0, cin.at(pi, 0));
+    stage_by_j(S1, cin.at(pi, 1));
+    uint64_t a[E];
+    uint32_t g = 5; // 5^(2^i) mod 2N
+#pragma unroll 1
+    for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
+        const bool last = i == L - 1;
+        const ulonglong2 *gq0 = K.gk + (size_t)(i * 4 + 0) * N, *gp0 = gq0 + N; // [rot][c][q0|P][N]
+        const ulonglong2 *gq1 = K.gk + (size_t)(i * 4 + 2) * N, *gp1 = gq1 + N;
+        __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
+        // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
+#pragma unroll
+        for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
+        inv<0>(a, XB, K.pr[0]);
+        fwd<2>(a, XB, K.pr[2]);
+        // P-limb key-switch products for both components; component 1's waits in the workspace
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 w0 = ld2k(gp0 + pos), w0b = ld2k(gp0 + pos + 1);
+            const ulonglong2 w1 = ld2k(gp1 + pos), w1b = ld2k(gp1 + pos + 1);
+            st2(ks1 + pos, shoup4<2>(a[e], w1), shoup4<2>(a[e + 1], w1b));
+            a[e] = shoup4<2>(a[e], w0);
+            a[e + 1] = shoup4<2>(a[e + 1], w0b);
+        }
+#pragma unroll 1
+        for (int c = 0; c < 2; c++) {
+            if (c == 1) { // written by this thread above: coherent (not .nc) loads
+#pragma unroll
+                for (int e = 0; e < E; e += 2) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(ks1 + pos_M4(tid, e));
+                    a[e] = v.x;
+                    a[e + 1] = v.y;
+                }
+            }
+            inv<2>(a, XB, K.pr[2]);
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = centP_q0(a[e]); // y^c mod q0, [0, 2 q0)
+            uint64_t *S = c ? S1 : S0;
+            const ulonglong2 *gq = c ? gq1 : gq0;
+            if (!last) {
+                fwd<0>(a, XB, K.pr[0]); // NTT_q0(y^c), canonical
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e))); // [0, 4 q0)
+                    uint64_t v = shoup4<0>(ks + Q0 - a[e], pinv) + S[pidx(j)];                  // < 5 q0
+                    if (c == 0) v += S0[pidx(jp)];                                                // < 6 q0
+                    a[e] = reduce_bnd<0>(v);
+                }
+                __syncthreads(); // every read of the old c_c is done
+#pragma unroll
+                for (int e = 0; e < E; e++) S[pidx(j_M4(tid, e))] = a[e];
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv); // P^-1 y^c, [0, 4 q0)
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e)));
+                    uint64_t v = shoup4<0>(ks, pinv) + S[pidx(j)];
+                    if (c == 0) v += S0[pidx(jp)];
+                    a[e] = reduce_bnd<0>(v);
+                }
+                inv<0>(a, XB, K.pr[0]);
+                uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = j_M1(tid, e);
+                    o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
+                }
+            }
+        }
+    }
+}
+
 // K7: output INTT when there is no ladder (s = 1)
 __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
 {
@@ -569,6 +674,7 @@ int ctx_get(DevCtx **out)
     set_smem(k_rot_digit);
     set_smem(k_rot_ks);
     set_smem(k_out_intt);
+    cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     set_smem(k_encrypt);
     set_smem(k_convert);
     set_smem(k_key_ntt);
@@ -934,25 +1040,33 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             end();
             rc = launch_check();
         }
-        CtBuf cin = bufC, cout = bufD;
-        for (int i = 1; i <= log_s && !rc; i++) {
-            const uint64_t r = (uint64_t)1 << (i - 1);
-            const uint32_t g = (uint32_t)powmod_d(5, r, 2 * N);
-            beg(4, 2 * np);
-            k_rot_digit<<<npu, T, SMEM_BYTES, s>>>(K, cin, g);
-            end();
-            const int last = i == log_s;
-            beg(5, (last ? 6 : 4) * np);
-            k_rot_ks<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
-            end();
-            rc = launch_check();
-            CtBuf t = cin;
-            cin = cout;
-            cout = t;
+        if (log_s > 0 && !rc) {
+            if (getenv("BM_LADDER_UNFUSED")) { // two-kernel-per-step ladder (kept for A/B measurement)
+                CtBuf cin = bufC, cout = bufD;
+                for (int i = 1; i <= log_s && !rc; i++) {
+                    const uint32_t g = (uint32_t)powmod_d(5, (uint64_t)1 << (i - 1), 2 * N);
+                    beg(4, 2 * np);
+                    k_rot_digit<<<npu, T, SMEM_BYTES, s>>>(K, cin, g);
+                    end();
+                    const int last = i == log_s;
+                    beg(4, (last ? 6 : 4) * np);
+                    k_rot_ks<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
+                    end();
+                    rc = launch_check();
+                    CtBuf t = cin;
+                    cin = cout;
+                    cout = t;
+                }
+            } else {
+                beg(4, 6 * log_s * np);
+                k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+                end();
+                rc = launch_check();
+            }
         }
         if (log_s == 0 && !rc) {
             beg(6, 2 * np);
-            k_out_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin);
+            k_out_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, bufC);
             end();
             rc = launch_check();
         }
