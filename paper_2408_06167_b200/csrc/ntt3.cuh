@@ -28,17 +28,28 @@ BM_D int j_M3(int tid, int k) { return 32 * (tid >> 1) + 2 * k + (tid & 1); }
 BM_D int j_M4(int tid, int e) { return 32 * (tid >> 1) + 4 * (e >> 1) + 2 * (tid & 1) + (e & 1); }
 BM_D int pos_M4(int tid, int e) { return 1024 * (e >> 1) + 2 * tid + (e & 1); }
 
+// Layout exchange through shared memory.  M2 and M3 partition j into per-warp 512-point regions
+// (warp w owns j in [512 w, 512 w + 512)), so an M2 <-> M3 exchange stays inside one warp and only
+// needs __syncwarp; exchanges with M1 span the CTA.  Hazards on the shared buffer: a CTA-wide
+// write must wait for every warp's previous reads (__syncthreads before it); a warp-local write
+// into region w only races with other warps' reads of region w, which only CTA-wide (M1) reads
+// do, so xchg<3,2> (the inverse's first exchange, which may follow an M1 read) starts with a
+// CTA barrier while xchg<2,3> (which always follows xchg<1,2>'s region-local reads) does not.
 template <int FROM, int TO>
 BM_D void xchg(uint64_t a[E], uint64_t *sm)
 {
     const int tid = threadIdx.x;
-    __syncthreads();
+    constexpr bool local_w = (FROM != 1);          // writes stay in the warp's region
+    constexpr bool local_r = (TO != 1);            // reads stay in the warp's region
+    if (FROM == 1 || (FROM == 3 && TO == 2)) __syncthreads();
+    else __syncwarp();
 #pragma unroll
     for (int k = 0; k < E; k++) {
         const int j = FROM == 1 ? j_M1(tid, k) : FROM == 2 ? j_M2(tid, k) : j_M3(tid, k);
         sm[pidx(j)] = a[k];
     }
-    __syncthreads();
+    if (local_w && local_r) __syncwarp();
+    else __syncthreads();
 #pragma unroll
     for (int k = 0; k < E; k++) {
         const int j = TO == 1 ? j_M1(tid, k) : TO == 2 ? j_M2(tid, k) : j_M3(tid, k);
