@@ -76,8 +76,13 @@ BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod
 }
 
 // ================================================================== K1: tensor + INTT(d2)
-// One CTA per (tile of TQ x TS pairs, limb): the query and DB part values are loaded once per
-// tile and reused from registers (TQ x TS fewer reloads), then the CTA runs the tile's INTTs.
+// One CTA per (tile of TQ x TS pairs, limb): every query / DB part value loaded is reused by
+// TS / TQ pairs from registers.  The tensor is pointwise, so in that phase thread tid handles
+// storage positions tid + 512 r (coalesced 8-byte loads), accumulating sum_i over the parts in
+// 128 bits with the next part's operands already in flight (software pipelining: the loop is
+// latency-bound otherwise).  Karatsuba: d1 = sum (x0+x1)(y0+y1) - d0 - d2 (exact mod q).  Each
+// product is < (2q)^2 < 2^118, so the 128-bit sums are folded mod q every 512 parts.
+// Then the CTA runs the INTT(d2) of each pair of the tile (digits of the relinearization).
 constexpr int TQ = 2, TS = 2;
 
 __global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int part_hi)
@@ -105,33 +110,52 @@ __global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int
         sb[v] = K.db + (size_t)(K.t0 + (vs[v] ? b : 0)) * K.p * 4 * N + (size_t)l * N;
     }
 #pragma unroll 1
-    for (int e = 0; e < E; e += 2) {
-        const int j = pos_M4(tid, e);
-        u128 s0[TQ][TS][2], s1[TQ][TS][2], s2[TQ][TS][2];
+    for (int r = 0; r < E; r++) {
+        const int j = tid + T * r;
+        u128 s0[TQ][TS], s1[TQ][TS], s2[TQ][TS];
 #pragma unroll
         for (int u = 0; u < TQ; u++)
 #pragma unroll
-            for (int v = 0; v < TS; v++)
+            for (int v = 0; v < TS; v++) s0[u][v] = s1[u][v] = s2[u][v] = 0;
+        uint64_t x0[TQ], x1[TQ], y0[TS], y1[TS];
+        {
+            const size_t off = (size_t)part_lo * 4 * N + j;
 #pragma unroll
-                for (int h = 0; h < 2; h++) s0[u][v][h] = s1[u][v][h] = s2[u][v][h] = 0;
+            for (int u = 0; u < TQ; u++) x0[u] = __ldg(qa[u] + off), x1[u] = __ldg(qa[u] + off + 2 * N);
+#pragma unroll
+            for (int v = 0; v < TS; v++) y0[v] = __ldg(sb[v] + off), y1[v] = __ldg(sb[v] + off + 2 * N);
+        }
+#pragma unroll 1
         for (int i = part_lo; i < part_hi; i++) {
-            const size_t off = (size_t)i * 4 * N + j;
-            ulonglong2 x0[TQ], x1[TQ], y0[TS], y1[TS];
+            uint64_t nx0[TQ], nx1[TQ], ny0[TS], ny1[TS];
+            const int in = i + 1 < part_hi ? i + 1 : i; // prefetch the next part (re-read the last)
+            const size_t off = (size_t)in * 4 * N + j;
 #pragma unroll
-            for (int u = 0; u < TQ; u++) x0[u] = ld2(qa[u] + off), x1[u] = ld2(qa[u] + off + 2 * N);
+            for (int u = 0; u < TQ; u++) nx0[u] = __ldg(qa[u] + off), nx1[u] = __ldg(qa[u] + off + 2 * N);
 #pragma unroll
-            for (int v = 0; v < TS; v++) y0[v] = ld2(sb[v] + off), y1[v] = ld2(sb[v] + off + 2 * N);
+            for (int v = 0; v < TS; v++) ny0[v] = __ldg(sb[v] + off), ny1[v] = __ldg(sb[v] + off + 2 * N);
 #pragma unroll
             for (int u = 0; u < TQ; u++)
 #pragma unroll
                 for (int v = 0; v < TS; v++) {
-                    s0[u][v][0] += (u128)x0[u].x * y0[v].x;
-                    s0[u][v][1] += (u128)x0[u].y * y0[v].y;
-                    s2[u][v][0] += (u128)x1[u].x * y1[v].x;
-                    s2[u][v][1] += (u128)x1[u].y * y1[v].y;
-                    s1[u][v][0] += (u128)(x0[u].x + x1[u].x) * (y0[v].x + y1[v].x); // Karatsuba
-                    s1[u][v][1] += (u128)(x0[u].y + x1[u].y) * (y0[v].y + y1[v].y);
+                    s0[u][v] += (u128)x0[u] * y0[v];
+                    s2[u][v] += (u128)x1[u] * y1[v];
+                    s1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
                 }
+            if (((i - part_lo) & 511) == 511) { // keep the 128-bit sums from overflowing (p > 512)
+#pragma unroll
+                for (int u = 0; u < TQ; u++)
+#pragma unroll
+                    for (int v = 0; v < TS; v++) {
+                        s0[u][v] = reduce128((uint64_t)(s0[u][v] >> 64), (uint64_t)s0[u][v], q, P.r64, P.one_p);
+                        s1[u][v] = reduce128((uint64_t)(s1[u][v] >> 64), (uint64_t)s1[u][v], q, P.r64, P.one_p);
+                        s2[u][v] = reduce128((uint64_t)(s2[u][v] >> 64), (uint64_t)s2[u][v], q, P.r64, P.one_p);
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < TQ; u++) x0[u] = nx0[u], x1[u] = nx1[u];
+#pragma unroll
+            for (int v = 0; v < TS; v++) y0[v] = ny0[v], y1[v] = ny1[v];
         }
 #pragma unroll
         for (int u = 0; u < TQ; u++)
@@ -139,27 +163,28 @@ __global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int
             for (int v = 0; v < TS; v++) {
                 if (!(vq[u] && vs[v])) continue;
                 const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
-                uint64_t d0[2], d1[2], d2[2];
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    d0[h] = reduce128((uint64_t)(s0[u][v][h] >> 64), (uint64_t)s0[u][v][h], q, P.r64, P.one_p);
-                    d2[h] = reduce128((uint64_t)(s2[u][v][h] >> 64), (uint64_t)s2[u][v][h], q, P.r64, P.one_p);
-                    const uint64_t kk = reduce128((uint64_t)(s1[u][v][h] >> 64), (uint64_t)s1[u][v][h], q, P.r64, P.one_p);
-                    d1[h] = submod_d(submod_d(kk, d0[h], q), d2[h], q);
-                }
-                st2(K.D01 + ((size_t)pi * 4 + 0 + l) * N + j, d0[0], d0[1]);
-                st2(K.D01 + ((size_t)pi * 4 + 2 + l) * N + j, d1[0], d1[1]);
-                st2(K.D2 + ((size_t)pi * 2 + l) * N + j, d2[0], d2[1]);
+                const uint64_t d0 = reduce128((uint64_t)(s0[u][v] >> 64), (uint64_t)s0[u][v], q, P.r64, P.one_p);
+                const uint64_t d2 = reduce128((uint64_t)(s2[u][v] >> 64), (uint64_t)s2[u][v], q, P.r64, P.one_p);
+                const uint64_t kk = reduce128((uint64_t)(s1[u][v] >> 64), (uint64_t)s1[u][v], q, P.r64, P.one_p);
+                K.D01[((size_t)pi * 4 + 0 + l) * N + j] = d0;
+                K.D01[((size_t)pi * 4 + 2 + l) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
+                K.D2[((size_t)pi * 2 + l) * N + j] = d2;
             }
     }
-    // INTT(d2) of every pair of the tile (the thread re-reads exactly the elements it wrote)
+    __syncthreads(); // the INTT phase reads D2 in another thread mapping (coherent loads below)
 #pragma unroll 1
     for (int w = 0; w < TQ * TS; w++) {
         const int u = w / TS, v = w % TS;
         if (!(vq[u] && vs[v])) continue;
         const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
+        const uint64_t *src = K.D2 + ((size_t)pi * 2 + l) * N;
         uint64_t a[E];
-        load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(src + pos_M4(tid, e));
+            a[e] = x.x;
+            a[e + 1] = x.y;
+        }
         inv_rt(a, sm, P, l);
         store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
     }
