@@ -75,119 +75,142 @@ BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod
     return (y > (QP >> 1)) ? submod_d(r, pmod, q) : r;
 }
 
-// ================================================================== K1: tensor + INTT(d2)
-// One CTA per (tile of TQ x TS pairs, limb): every query / DB part value loaded is reused by
-// TS / TQ pairs from registers.  The tensor is pointwise, so in that phase thread tid handles
-// storage positions tid + 512 r (coalesced 8-byte loads), accumulating sum_i over the parts in
-// 128 bits with the next part's operands already in flight (software pipelining: the loop is
-// latency-bound otherwise).  Karatsuba: d1 = sum (x0+x1)(y0+y1) - d0 - d2 (exact mod q).  Each
-// product is < (2q)^2 < 2^118, so the 128-bit sums are folded mod q every 512 parts.
-// Then the CTA runs the INTT(d2) of each pair of the tile (digits of the relinearization).
-constexpr int TQ = 2, TS = 2;
+// ================================================================== K1: tensor (a4)
+// d0 = sum_i x0_i y0_i, d2 = sum_i x1_i y1_i, d1 = sum_i (x0_i + x1_i)(y0_i + y1_i) - d0 - d2 per
+// (query x, set y) pair, limb and NTT-domain coefficient (Karatsuba over the ciphertext
+// components, exact mod q) -- for each coefficient a small "query tile x set tile" contraction
+// over the parts, tiled like one: a CTA owns TQB queries x TSB sets x CS coefficients of one limb
+// and stages the operands of up to PCH parts in shared memory with cp.async (each query / set
+// value is fetched from L2 once per CTA and reused TSB / TQB times); every thread then
+// accumulates a 2 x 2 block of pairs for one coefficient in 128-bit sums.  A product is
+// < (2q)^2 < 2^118, so the sums are folded mod q every 512 parts.
+constexpr int TT = 256;                 // threads per tensor CTA
+constexpr int TQB = 8, TSB = 4;         // queries x sets per CTA
+constexpr int CS = 32;                  // coefficients per CTA
+constexpr int PCH = 8;                  // parts staged per round
+constexpr size_t TENSOR_SMEM_BYTES = (size_t)(TQB + TSB) * PCH * 2 * CS * sizeof(uint64_t); // 48 KiB
 
-__global__ void __launch_bounds__(T, 1) k_tensor_intt(MatchK K, int part_lo, int part_hi)
+BM_D void cp_async16(void *smem, const void *gmem)
+{
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+BM_D uint64_t red128(u128 v, const PrimeK &P) { return reduce128((uint64_t)(v >> 64), (uint64_t)v, P.q, P.r64, P.one_p); }
+
+// grid: ((l * nqt + qt) * (N / CS) + slice) * nst + st  (set tiles fastest: the CTAs that share a
+// query slice run together and the query data streams from HBM once)
+__global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
+    uint64_t *Qs = sm, *Ss = sm + TQB * PCH * 2 * CS; // [tile row][part][comp][CS]
     const int tid = threadIdx.x;
-    const int l = blockIdx.x & 1;
-    const int64_t tile = blockIdx.x >> 1;
-    const int64_t n_tb = (K.ct + TS - 1) / TS;
-    const int64_t ta = tile / n_tb, tb = tile - ta * n_tb;
+    const int nst = (int)((K.ct + TSB - 1) / TSB), nqt = (K.cq + TQB - 1) / TQB;
+    int64_t b = blockIdx.x;
+    const int st = (int)(b % nst);
+    b /= nst;
+    const int sl = (int)(b % (N / CS));
+    b /= (N / CS);
+    const int qt = (int)(b % nqt);
+    const int l = (int)(b / nqt);
+    const int c0 = sl * CS;
     const PrimeK P = l ? K.pr[1] : K.pr[0];
-    const uint64_t q = P.q;
-    const uint64_t *qa[TQ], *sb[TS];
-    bool vq[TQ], vs[TS];
+    // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
+    const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
+    u128 a0[2][2], a1[2][2], a2[2][2];
 #pragma unroll
-    for (int u = 0; u < TQ; u++) {
-        const int64_t a = ta * TQ + u;
-        vq[u] = a < K.cq;
-        qa[u] = K.qry + (size_t)(K.jq0 + (vq[u] ? a : 0)) * K.p * 4 * N + (size_t)l * N;
-    }
+    for (int u = 0; u < 2; u++)
 #pragma unroll
-    for (int v = 0; v < TS; v++) {
-        const int64_t b = tb * TS + v;
-        vs[v] = b < K.ct;
-        sb[v] = K.db + (size_t)(K.t0 + (vs[v] ? b : 0)) * K.p * 4 * N + (size_t)l * N;
-    }
+        for (int v = 0; v < 2; v++) a0[u][v] = a1[u][v] = a2[u][v] = 0;
 #pragma unroll 1
-    for (int r = 0; r < E; r++) {
-        const int j = tid + T * r;
-        u128 s0[TQ][TS], s1[TQ][TS], s2[TQ][TS];
-#pragma unroll
-        for (int u = 0; u < TQ; u++)
-#pragma unroll
-            for (int v = 0; v < TS; v++) s0[u][v] = s1[u][v] = s2[u][v] = 0;
-        uint64_t x0[TQ], x1[TQ], y0[TS], y1[TS];
-        {
-            const size_t off = (size_t)part_lo * 4 * N + j;
-#pragma unroll
-            for (int u = 0; u < TQ; u++) x0[u] = __ldg(qa[u] + off), x1[u] = __ldg(qa[u] + off + 2 * N);
-#pragma unroll
-            for (int v = 0; v < TS; v++) y0[v] = __ldg(sb[v] + off), y1[v] = __ldg(sb[v] + off + 2 * N);
+    for (int i0 = part_lo; i0 < part_hi; i0 += PCH) {
+        const int pc = part_hi - i0 < PCH ? part_hi - i0 : PCH; // a power of two (p is)
+        const int lpc = __ffs(pc) - 1;
+        // stage: rows (tile row, part, comp) of CS u64 = 16 chunks of 16 B
+        const int rows = (TQB + TSB) * pc * 2;
+#pragma unroll 4
+        for (int k = tid; k < rows * (CS / 2); k += TT) {
+            const int row = k >> 4, ch = k & 15;
+            const int comp = row & 1, part = (row >> 1) & (pc - 1), tr = (row >> 1) >> lpc;
+            const uint64_t *src;
+            uint64_t *dst;
+            if (tr < TQB) {
+                int64_t a = (int64_t)qt * TQB + tr;
+                a = a < K.cq ? a : K.cq - 1;
+                src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 4 * N;
+                dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
+            } else {
+                int64_t bb = (int64_t)st * TSB + (tr - TQB);
+                bb = bb < K.ct ? bb : K.ct - 1;
+                src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 4 * N;
+                dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
+            }
+            cp_async16(dst + 2 * ch, src + (size_t)(2 * comp + l) * N + c0 + 2 * ch);
         }
-#pragma unroll 1
-        for (int i = part_lo; i < part_hi; i++) {
-            uint64_t nx0[TQ], nx1[TQ], ny0[TS], ny1[TS];
-            const int in = i + 1 < part_hi ? i + 1 : i; // prefetch the next part (re-read the last)
-            const size_t off = (size_t)in * 4 * N + j;
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
 #pragma unroll
-            for (int u = 0; u < TQ; u++) nx0[u] = __ldg(qa[u] + off), nx1[u] = __ldg(qa[u] + off + 2 * N);
+        for (int i = 0; i < PCH; i++) {
+            if (i >= pc) break;
+            uint64_t x0[2], x1[2], y0[2], y1[2];
 #pragma unroll
-            for (int v = 0; v < TS; v++) ny0[v] = __ldg(sb[v] + off), ny1[v] = __ldg(sb[v] + off + 2 * N);
+            for (int u = 0; u < 2; u++) {
+                const uint64_t *r = Qs + (((2 * su + u) * PCH + i) * 2) * CS + c;
+                x0[u] = r[0];
+                x1[u] = r[CS];
+            }
 #pragma unroll
-            for (int u = 0; u < TQ; u++)
+            for (int v = 0; v < 2; v++) {
+                const uint64_t *r = Ss + (((2 * sv + v) * PCH + i) * 2) * CS + c;
+                y0[v] = r[0];
+                y1[v] = r[CS];
+            }
 #pragma unroll
-                for (int v = 0; v < TS; v++) {
-                    s0[u][v] += (u128)x0[u] * y0[v];
-                    s2[u][v] += (u128)x1[u] * y1[v];
-                    s1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    a0[u][v] += (u128)x0[u] * y0[v];
+                    a2[u][v] += (u128)x1[u] * y1[v];
+                    a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
                 }
-            if (((i - part_lo) & 511) == 511) { // keep the 128-bit sums from overflowing (p > 512)
-#pragma unroll
-                for (int u = 0; u < TQ; u++)
-#pragma unroll
-                    for (int v = 0; v < TS; v++) {
-                        s0[u][v] = reduce128((uint64_t)(s0[u][v] >> 64), (uint64_t)s0[u][v], q, P.r64, P.one_p);
-                        s1[u][v] = reduce128((uint64_t)(s1[u][v] >> 64), (uint64_t)s1[u][v], q, P.r64, P.one_p);
-                        s2[u][v] = reduce128((uint64_t)(s2[u][v] >> 64), (uint64_t)s2[u][v], q, P.r64, P.one_p);
-                    }
-            }
-#pragma unroll
-            for (int u = 0; u < TQ; u++) x0[u] = nx0[u], x1[u] = nx1[u];
-#pragma unroll
-            for (int v = 0; v < TS; v++) y0[v] = ny0[v], y1[v] = ny1[v];
         }
+        if (((i0 + pc - part_lo) & 511) == 0 && i0 + pc < part_hi) { // (2q)^2 < 2^118: fold every 512 parts
 #pragma unroll
-        for (int u = 0; u < TQ; u++)
+            for (int u = 0; u < 2; u++)
 #pragma unroll
-            for (int v = 0; v < TS; v++) {
-                if (!(vq[u] && vs[v])) continue;
-                const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
-                const uint64_t d0 = reduce128((uint64_t)(s0[u][v] >> 64), (uint64_t)s0[u][v], q, P.r64, P.one_p);
-                const uint64_t d2 = reduce128((uint64_t)(s2[u][v] >> 64), (uint64_t)s2[u][v], q, P.r64, P.one_p);
-                const uint64_t kk = reduce128((uint64_t)(s1[u][v] >> 64), (uint64_t)s1[u][v], q, P.r64, P.one_p);
-                K.D01[((size_t)pi * 4 + 0 + l) * N + j] = d0;
-                K.D01[((size_t)pi * 4 + 2 + l) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
-                K.D2[((size_t)pi * 2 + l) * N + j] = d2;
-            }
-    }
-    __syncthreads(); // the INTT phase reads D2 in another thread mapping (coherent loads below)
-#pragma unroll 1
-    for (int w = 0; w < TQ * TS; w++) {
-        const int u = w / TS, v = w % TS;
-        if (!(vq[u] && vs[v])) continue;
-        const int64_t pi = (ta * TQ + u) * K.ct + tb * TS + v;
-        const uint64_t *src = K.D2 + ((size_t)pi * 2 + l) * N;
-        uint64_t a[E];
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(src + pos_M4(tid, e));
-            a[e] = x.x;
-            a[e + 1] = x.y;
+                for (int v = 0; v < 2; v++) {
+                    a0[u][v] = red128(a0[u][v], P);
+                    a1[u][v] = red128(a1[u][v], P);
+                    a2[u][v] = red128(a2[u][v], P);
+                }
         }
-        inv_rt(a, sm, P, l);
-        store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
+        __syncthreads(); // before the next round overwrites the stage
     }
+    const uint64_t q = P.q;
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) {
+            const int64_t a = (int64_t)qt * TQB + 2 * su + u, bb = (int64_t)st * TSB + 2 * sv + v;
+            if (a >= K.cq || bb >= K.ct) continue;
+            const int64_t pi = a * K.ct + bb;
+            const int j = c0 + c;
+            const uint64_t d0 = red128(a0[u][v], P), d2 = red128(a2[u][v], P), kk = red128(a1[u][v], P);
+            K.D01[((size_t)pi * 4 + 0 + l) * N + j] = d0;
+            K.D01[((size_t)pi * 4 + 2 + l) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
+            K.D2[((size_t)pi * 2 + l) * N + j] = d2;
+        }
+}
+
+// K1b: digits of the relinearization, x_l = INTT_{q_l}(d2[q_l]) (coefficients in [0, q_l))
+__global__ void __launch_bounds__(T, 1) k_d2_intt(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    const int64_t pi = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
+    uint64_t a[E];
+    load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
+    inv_rt(a, sm, l ? K.pr[1] : K.pr[0], l);
+    store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
 }
 
 // ================================================================== K2: ModUp + NTT
@@ -692,7 +715,8 @@ int ctx_get(DevCtx **out)
     }
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
-    set_smem(k_tensor_intt);
+    cudaFuncSetAttribute(k_tensor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    set_smem(k_d2_intt);
     set_smem(k_modup_ntt);
     set_smem(k_ks_intt);
     set_smem(k_rescale_ntt);
@@ -1047,12 +1071,13 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
         const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
-        const unsigned ntiles = (unsigned)(((K.cq + TQ - 1) / TQ) * ((K.ct + TS - 1) / TS));
+        const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS));
         const int n_rounds = order == BM_ORDER_HOISTED ? 1 : prm->p;
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
             beg(0, 2 * np);
-            k_tensor_intt<<<2 * ntiles, T, SMEM_BYTES, s>>>(K, lo, hi);
+            k_tensor<<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+            k_d2_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K);
             end();
             beg(1, 4 * np);
             k_modup_ntt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
