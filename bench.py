@@ -64,10 +64,9 @@ def class_modmuls(p, log_s):
     (DESIGN.md "Algorithmic work"): butterflies of every transform + pointwise products."""
     n = N_RING
     return {
-        "tensor_intt": 8 * n * p + 2 * BFLY,                       # a0b0, a0b1, a1b0, a1b1 per limb + INTT(d2)
-        "modup_ntt": 4 * BFLY,
-        "ks_intt": 4 * BFLY + 8 * n + 2 * n,                       # rlk products (P, q1) + P^-1 scaling
-        "rescale_ntt": 2 * BFLY + 4 * n + 8 * n,                   # rlk q0 products + P^-1, q1^-1, centring
+        "tensor": 8 * n * p,                                       # a0b0, a1b1, (a0+a1)(b0+b1) per limb (+ adds)
+        "digits": 6 * BFLY + n,                                    # INTT_q0, INTT_q1, NTT_q1, NTT_P x2, NTT_q0
+        "relin": 6 * BFLY + 12 * n + 8 * n,                        # INTT_P, INTT_q1, NTT_q0 x 2 comps; rlk + scalings
         "ladder": (6 * BFLY + 6 * n) * log_s,                      # digit INTT_q0 + NTT_P, 2 x (INTT_P + NTT_q0)
         "out_intt": 0 if log_s else 2 * BFLY,
     }
@@ -226,13 +225,13 @@ def run_ours(args):
     tq_per_step = world * n_tmpl * nq
     value = tq_per_step / (ms_step / 1e3)
 
-    # launches of our kernels per step: chunks x (4 per part-round + 1 fused ladder (or output INTT if s = 1))
+    # launches of our kernels per step: chunks x (3 per part-round + 1 fused ladder (or output INTT if s = 1))
     import math
     total_pairs = n_sets * nq
     chunk = int(os.environ.get("BM_CHUNK_PAIRS", "1024"))
     n_chunks = math.ceil(total_pairs / min(chunk, total_pairs))
     rounds = 1 if order == 0 else p
-    launches = n_chunks * (4 * rounds + 1)
+    launches = n_chunks * (3 * rounds + 1)
 
     # per-kernel-class device times (CUDA events on the launching stream), same step, profiled pass
     B.bm_set_profiling(True)
@@ -247,7 +246,7 @@ def run_ours(args):
     per_class = {}
     for i, c in enumerate(classes):
         if pla[i]:
-            work = mm[c] * total_pairs * args.steps * (rounds if i < 4 else 1)
+            work = mm[c] * total_pairs * args.steps * (rounds if i < 3 else 1)
             per_class[c] = {"ms_per_step": pms[i] / args.steps, "launches": int(pla[i]),
                             "gmodmul_s": work / (pms[i] / 1e3) / 1e9}
     dom = max(per_class, key=lambda c: per_class[c]["ms_per_step"])

@@ -167,8 +167,8 @@ int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, i
                   int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
 
 /* Per-kernel-class device time of the last bm_match on this thread when profiling is
- * enabled (bm_set_profiling(1)); classes: 0 tensor+INTT, 1 ModUp NTT, 2 key-switch INTT,
- * 3 rescale NTT, 4 rotate-and-add ladder (fused), 5 unused, 6 output INTT (s = 1).  ms[7] and
+ * enabled (bm_set_profiling(1)); classes: 0 tensor, 1 digits + ModUp NTTs, 2 key switch +
+ * ModDown + rescale, 3 unused, 4 rotate-and-add ladder (fused), 5 unused, 6 output INTT (s = 1).  ms[7] and
  * launches[7] accumulate until bm_profile_reset(). */
 void bm_set_profiling(int32_t on);
 void bm_profile_reset(void);

@@ -300,7 +300,7 @@ def bm_profile_read():
     return ms, la, un
 
 
-PROFILE_CLASSES = ["tensor_intt", "modup_ntt", "ks_intt", "rescale_ntt", "ladder", "unused", "out_intt"]
+PROFILE_CLASSES = ["tensor", "digits", "relin", "unused3", "ladder", "unused5", "out_intt"]
 
 
 def bm_decrypt(prm, sk, h_ct):

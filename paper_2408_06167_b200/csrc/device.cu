@@ -1,18 +1,17 @@
 // device.cu -- sm_100a kernels and the device-facing C ABI of libblindmatch.
 //
 // Hot path (bm_match, HE-C^3) per (query, set) pair, hoisted order
-// (reading R8), one 512-thread CTA per polynomial transform (ntt3.cuh):
-//   K1 k_tensor_intt  (pair, limb)      a4: d0,d1,d2 = sum_i tensor(C_u,i, C_s,i) (Karatsuba,
-//                                        128-bit accumulation), INTT(d2) -> digits x_l
-//   K2 k_modup_ntt    (pair, 4 targets) a5: ModUp x0 -> {q1,P}, x1 -> {q0,P}, NTT
-//   K3 k_ks_intt      (pair, comp, P|q1) a5: KS = sum_j x_j rlk_j, INTT_P(KS[P]);
-//                                        INTT_q1(d[q1] + P^-1 KS[q1])
-//   K4 k_rescale_ntt  (pair, comp)      a5+a6: ModDown fused with rescale by q1 (exact,
-//                                        DESIGN.md "fused ModDown + rescale"), NTT_q0
-//   per ladder step i = 1..log2 s (a7), r = 2^(i-1), g = 5^r mod 2N:
-//   K5 k_rot_digit    (pair)            sigma_g(c1) (NTT-domain permutation), INTT_q0, NTT_P
-//   K6 k_rot_ks       (pair, comp)      KS = x gk_r, INTT_P, NTT_q0, ModDown, C += Rot(C);
-//                                        the last step also INTTs C into the output (a8)
+// (reading R8); every transform is one 8192-point NTT held by a 512-thread CTA (ntt3.cuh):
+//   K1 k_tensor  (tile of pairs, limb)   a4: d0, d1, d2 = sum_i tensor(C_u,i, C_s,i) (Karatsuba),
+//                                        a contraction over the parts tiled through shared memory
+//   K2 k_digits  (pair, digit l)         a5: x_l = INTT_{q_l}(d2[q_l]); ModUp: x0 -> NTT_{q1,P},
+//                                        x1 -> NTT_{q0,P}  (3 transforms)
+//   K3 k_relin   (pair, component c)     a5+a6: KS_c = sum_j x_j rlk_j over {q0,q1,P}; ModDown fused
+//                                        with the rescale by q1 (exact, R22):
+//                                        INTT_P, INTT_q1, NTT_q0 (3 transforms) -> C_c (level 0)
+//   K4 k_ladder  (pair)                  a7+a8: the log2(s) rotate-and-add steps with C resident in
+//                                        shared memory, 6 transforms per step, coefficient-domain output
+//   K5 k_out_intt (pair, c)              a8 when s = 1 (no ladder): INTT_q0 of C
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -30,12 +29,12 @@ typedef unsigned __int128 u128;
 // ================================================================== device constants
 __constant__ uint64_t c_cdt[19];
 
-// Workspace per (query, set) pair, 12 N u64 (aliased across kernels):
-//   D01 [c][l][N]  d_c[q_l] (NTT)      -> U_c aliases d_c[q1] (K3 -> K4)
-//   D2  [l][N]     d2[q_l] (NTT)
-//   XC  [2][N]     digits x0, x1 (coefficients) -> Y_c (K3 -> K4) -> XP (ladder)
-//   XU  [4][N]     ModUp'd digits (NTT) -> C (K4 -> ladder) in XU[0..1], ladder ping-pong XU[2..3]
-// The paper order adds a level-0 accumulator ACC [2][N] (K4 sums into it across parts).
+// Workspace per (query, set) pair, 12 N u64:
+//   D01 [c][l][N]  d_c[q_l] (NTT)                       K1 -> K3
+//   D2  [l][N]     d2[q_l] (NTT)                        K1 -> K2, K3; then the ladder's scratch
+//   XC  [2][N]     C = (c0, c1), level 0 (NTT)          K3 -> ladder
+//   XU  [4][N]     ModUp'd digits x0~[q1], x0~[P], x1~[q0], x1~[P] (NTT)   K2 -> K3
+// The paper order adds a level-0 accumulator ACC [2][N] (K3 sums into it across parts).
 struct MatchK {
     PrimeK pr[3];
     ulonglong2 pinv[2]; // P^-1 mod q0, q1
@@ -67,13 +66,6 @@ BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
 BM_D void st2(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
 
 BM_D uint64_t submod_d(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
-
-// centred P-residue y in [0,P) reduced into q (q < P): y mod q, minus (P mod q) when y > P/2
-BM_D uint64_t centredP_mod(uint64_t y, uint64_t q, uint64_t one_p, uint64_t pmod)
-{
-    uint64_t r = reduce64(y, q, one_p);
-    return (y > (QP >> 1)) ? submod_d(r, pmod, q) : r;
-}
 
 // ================================================================== K1: tensor (a4)
 // d0 = sum_i x0_i y0_i, d2 = sum_i x1_i y1_i, d1 = sum_i (x0_i + x1_i)(y0_i + y1_i) - d0 - d2 per
@@ -201,204 +193,146 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
         }
 }
 
-// K1b: digits of the relinearization, x_l = INTT_{q_l}(d2[q_l]) (coefficients in [0, q_l))
-__global__ void __launch_bounds__(T, 1) k_d2_intt(MatchK K)
+// ================================================================== prime-specialised pointwise helpers
+// reduce_bnd<PI>: exact x mod q for x < 2^64 (q0, P) / x < 2^62 (q1), ntt2.cuh.
+// centred_P(y) mod q0 for canonical y in [0, P), result in [0, 2 q0): y - P = y + (5 q0 - P) mod q0
+BM_D uint64_t centP_q0(uint64_t y)
+{
+    constexpr uint64_t K5 = 5 * Q0 - QP;
+    const uint64_t x = y > (QP >> 1) ? y + K5 : y;
+    const uint64_t Qe = x >> 58;
+    return x - (Qe << 58) + Qe * ((1ull << 58) - Q0);
+}
+// y in [0, P) canonical -> centred_P(y) mod q1, canonical: y - P = y + (K q1 - P), K = 2^20 + 2
+BM_D uint64_t centP_q1(uint64_t y)
+{
+    constexpr uint64_t K = ((1ull << 20) + 2) * Q1 - QP; // >= 0, and P + K < 2^62
+    return reduce_bnd<1>(y > (QP >> 1) ? y + K : y);
+}
+// x < 8q -> [0, 4q)
+template <int PI> BM_D uint64_t red8to4(uint64_t x)
+{
+    constexpr uint64_t q4 = 4 * PrimeC<PI>::q;
+    return x >= q4 ? x - q4 : x;
+}
+
+// ================================================================== K2: digits + ModUp + NTT
+// CTA (pair, l): x_l = INTT_{q_l}(d2[q_l]) in [0, q_l) (non-centred digit, reading R4), kept in
+// shared memory (thread-private slots) between its two ModUp targets:
+//   l = 0: x0 mod q1 -> NTT_q1 -> XU[0],  x0 -> NTT_P -> XU[1]
+//   l = 1: x1 (< q1 < q0) -> NTT_q0 -> XU[2],  x1 -> NTT_P -> XU[3]
+constexpr size_t K2_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+__global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
 {
     extern __shared__ uint64_t sm[];
+    uint64_t *xs = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int l = blockIdx.x & 1;
     uint64_t a[E];
     load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
-    inv_rt(a, sm, l ? K.pr[1] : K.pr[0], l);
-    store_coef(K.XC + ((size_t)pi * 2 + l) * N, a);
-}
-
-// ================================================================== K2: ModUp + NTT
-// t = 0: x0 -> q1, 1: x0 -> P, 2: x1 -> q0, 3: x1 -> P  (non-centred lift, reading R4)
-__global__ void __launch_bounds__(T, 1) k_modup_ntt(MatchK K)
-{
-    extern __shared__ uint64_t sm[];
-    const int64_t pi = blockIdx.x >> 2;
-    const int t = blockIdx.x & 3;
-    uint64_t a[E];
-    load_coef(a, K.XC + ((size_t)pi * 2 + (t >> 1)) * N);
-    if (t == 0) {
-#pragma unroll
-        for (int e = 0; e < E; e++) a[e] = reduce64(a[e], K.pr[1].q, K.pr[1].one_p);
-    }
-    const int tp = (t == 0) ? 1 : (t == 2) ? 0 : 2;
-    const PrimeK P = (t == 0) ? K.pr[1] : (t == 2) ? K.pr[0] : K.pr[2];
-    fwd_rt(a, sm, P, tp);
-    store_eval(K.XU + ((size_t)pi * 4 + t) * N, a);
-}
-
-// ================================================================== K3: key-switch inner product + INTT
-// block (pair, c, w): w = 0 -> Y_c = INTT_P(KS_c[P]);  w = 1 -> U_c = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
-// KS_c[P] = x0~ rlk0[c][P] + x1~ rlk1[c][P];  KS_c[q1] = x0~ rlk0[c][q1] + d2[q1] rlk1[c][q1]
-__global__ void __launch_bounds__(T, 1) k_ks_intt(MatchK K)
-{
-    extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x >> 2;
-    const int c = (blockIdx.x >> 1) & 1, w = blockIdx.x & 1;
-    const int lim = w ? 1 : 2;
-    const PrimeK P = w ? K.pr[1] : K.pr[2];
-    const uint64_t q = P.q;
-    // rlk layout [j][c][l][N]
-    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + lim) * N;
-    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + lim) * N;
-    const uint64_t *x0 = K.XU + ((size_t)pi * 4 + (w ? 0 : 1)) * N;
-    const uint64_t *x1 = w ? K.D2 + ((size_t)pi * 2 + 1) * N : K.XU + ((size_t)pi * 4 + 3) * N;
-    uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N; // d_c[q1]; U_c is written over it
-    uint64_t a[E];
-#pragma unroll
-    for (int e = 0; e < E; e += 2) {
-        const int j = pos_M4(tid, e);
-        ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j);
-        uint64_t ka = csub(shoup(u.x, ld2k(k0 + j), q) + shoup(v.x, ld2k(k1 + j), q), P.q2);
-        uint64_t kb = csub(shoup(u.y, ld2k(k0 + j + 1), q) + shoup(v.y, ld2k(k1 + j + 1), q), P.q2);
-        if (w) {
-            ulonglong2 dd = ld2(dc + j);
-            ka = csub(dd.x + shoup(csub(ka, q), K.pinv[1], q), P.q2);
-            kb = csub(dd.y + shoup(csub(kb, q), K.pinv[1], q), P.q2);
-        }
-        a[e] = ka;
-        a[e + 1] = kb;
-    }
-    inv_rt(a, sm, P, w ? 1 : 2);
-    store_coef(w ? dc : K.XC + ((size_t)pi * 2 + c) * N, a);
-}
-
-// ================================================================== K4: ModDown + rescale + NTT_q0
-// Out_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - NTT_q0(P^-1 y^ + z^)), with y^ = centred_P(Y_c),
-// R = U_c - P^-1 y^ (mod q1), z^ = centred_q1(R).  accumulate: dst += Out (paper order).
-__global__ void __launch_bounds__(T, 1) k_rescale_ntt(MatchK K, CtBuf dst, int accumulate)
-{
-    extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x >> 1;
-    const int c = blockIdx.x & 1;
-    const uint64_t q0 = K.pr[0].q, q1 = K.pr[1].q;
-    const uint64_t *yi = K.XC + ((size_t)pi * 2 + c) * N, *ui = K.D01 + ((size_t)pi * 4 + c * 2 + 1) * N;
-    uint64_t a[E];
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const int j = j_M1(tid, e);
-        const uint64_t y = yi[j], u = ui[j];
-        const uint64_t y1 = centredP_mod(y, q1, K.pr[1].one_p, K.pmod[1]);
-        const uint64_t R = submod_d(u, csub(shoup(y1, K.pinv[1], q1), q1), q1);
-        const uint64_t z0 = (R > (q1 >> 1)) ? R + (q0 - q1) : R;
-        const uint64_t y0 = centredP_mod(y, q0, K.pr[0].one_p, K.pmod[0]);
-        a[e] = csub(csub(shoup(y0, K.pinv[0], q0), q0) + z0, q0);
-    }
-    fwd<0>(a, sm, K.pr[0]);
-    const ulonglong2 *k0 = K.rlk + ((size_t)(0 * 2 + c) * 3 + 0) * N;
-    const ulonglong2 *k1 = K.rlk + ((size_t)(1 * 2 + c) * 3 + 0) * N;
-    const uint64_t *x0 = K.D2 + ((size_t)pi * 2 + 0) * N, *x1 = K.XU + ((size_t)pi * 4 + 2) * N;
-    const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2 + 0) * N;
-    uint64_t *co = dst.at(pi, c);
-    const uint64_t q2 = 2 * q0;
-#pragma unroll
-    for (int e = 0; e < E; e += 2) {
-        const int j = pos_M4(tid, e);
-        ulonglong2 u = ld2(x0 + j), v = ld2(x1 + j), dd = ld2(dc + j);
-        uint64_t ksa = csub(csub(shoup(u.x, ld2k(k0 + j), q0) + shoup(v.x, ld2k(k1 + j), q0), q2), q0);
-        uint64_t ksb = csub(csub(shoup(u.y, ld2k(k0 + j + 1), q0) + shoup(v.y, ld2k(k1 + j + 1), q0), q2), q0);
-        uint64_t va = csub(dd.x + csub(shoup(ksa, K.pinv[0], q0), q0), q0);
-        uint64_t vb = csub(dd.y + csub(shoup(ksb, K.pinv[0], q0), q0), q0);
-        uint64_t oa = csub(shoup(va + q0 - a[e], K.q1inv, q0), q0);
-        uint64_t ob = csub(shoup(vb + q0 - a[e + 1], K.q1inv, q0), q0);
-        if (accumulate) {
-            ulonglong2 cc = ld2(co + j);
-            oa = csub(oa + cc.x, q0);
-            ob = csub(ob + cc.y, q0);
-        }
-        st2(co + j, oa, ob);
-    }
-}
-
-// ================================================================== ladder (a7)
-// K5: x = INTT_q0(sigma_g(c1)) (coefficients in [0,q0), lifted to P as is), XP = NTT_P(x)
-__global__ void __launch_bounds__(T, 1) k_rot_digit(MatchK K, CtBuf cin, uint32_t g)
-{
-    extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x;
-    stage_by_j(sm, cin.at(pi, 1));
-    __syncthreads();
-    uint64_t a[E];
-#pragma unroll
-    for (int e = 0; e < E; e++) a[e] = sm[pidx(auto_perm(j_M4(tid, e), g))];
-    inv<0>(a, sm, K.pr[0]);
-    fwd<2>(a, sm, K.pr[2]);
-    store_eval(K.XC + (size_t)pi * 2 * N, a);
-}
-
-// K6: KS_c = XP * gk[c][P] -> INTT_P -> y^ -> NTT_q0;  KS'_c = (sigma(c1) gk[c][q0] - NTT(y^)) P^-1;
-//     cout_c = cin_c + [c = 0] sigma(c0) + KS'_c; last step: out_c = INTT_q0(cout_c) -> d_out (a8)
-__global__ void __launch_bounds__(T, 1) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout, int rot, uint32_t g,
-                                                           int last)
-{
-    extern __shared__ uint64_t sm[];
-    const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x >> 1;
-    const int c = blockIdx.x & 1;
-    const uint64_t q0 = K.pr[0].q;
-    const ulonglong2 *gq = K.gk + ((size_t)(rot * 2 + c) * 2 + 0) * N; // q0 limb
-    uint64_t a[E];
-    {
-        const ulonglong2 *gp = gq + N; // P limb
-        const uint64_t *xp = K.XC + (size_t)pi * 2 * N;
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int j = pos_M4(tid, e);
-            ulonglong2 x = ld2(xp + j);
-            a[e] = shoup(x.x, ld2k(gp + j), QP);
-            a[e + 1] = shoup(x.y, ld2k(gp + j + 1), QP);
-        }
-    }
-    // phase 0: INTT_P; phase 1: NTT_q0; phase 2 (last step only): INTT_q0 of the new C
-    for (int ph = 0;; ph++) {
-        if (ph == 1) fwd<0>(a, sm, K.pr[0]);
-        else if (ph == 0) inv<2>(a, sm, K.pr[2]);
-        else inv<0>(a, sm, K.pr[0]);
-        if (ph == 0) {
-#pragma unroll
-            for (int e = 0; e < E; e++) a[e] = centredP_mod(a[e], q0, K.pr[0].one_p, K.pmod[0]);
-            continue;
-        }
-        if (ph == 2) {
-            store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
-            break;
-        }
-        // sigma_g(c1) * gk[c][q0] - NTT(y^), times P^-1
-        __syncthreads();
-        stage_by_j(sm, cin.at(pi, 1));
-        __syncthreads();
+    uint64_t *xu = K.XU + ((size_t)pi * 4 + 2 * l) * N;
+    if (l == 0) {
+        inv<0>(a, sm, K.pr[0]);
 #pragma unroll
         for (int e = 0; e < E; e++) {
-            const uint64_t x = sm[pidx(auto_perm(j_M4(tid, e), g))];
-            const uint64_t ks = csub(shoup(x, ld2k(gq + pos_M4(tid, e)), q0), q0);
-            a[e] = csub(shoup(submod_d(ks, a[e], q0), K.pinv[0], q0), q0);
+            xs[tid + T * e] = a[e];
+            a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
         }
-        if (c == 0) {
-            __syncthreads();
-            stage_by_j(sm, cin.at(pi, 0));
-            __syncthreads();
+        fwd<1>(a, sm, K.pr[1]);
+    } else {
+        inv<1>(a, sm, K.pr[1]);
 #pragma unroll
-            for (int e = 0; e < E; e++) a[e] = csub(a[e] + sm[pidx(auto_perm(j_M4(tid, e), g))], q0);
-        }
-        const uint64_t *cc = cin.at(pi, c);
+        for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
+        fwd<0>(a, sm, K.pr[0]);
+    }
+    store_eval(xu, a);
 #pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            ulonglong2 v = ld2(cc + pos_M4(tid, e));
-            a[e] = csub(a[e] + v.x, q0);
-            a[e + 1] = csub(a[e + 1] + v.y, q0);
+    for (int e = 0; e < E; e++) a[e] = xs[tid + T * e];
+    fwd<2>(a, sm, K.pr[2]);
+    store_eval(xu + N, a);
+}
+
+// ================================================================== K3: key switch + ModDown + rescale
+// CTA (pair, c), R22 (exact rewriting of ModDown followed by the rescale by q1):
+//   KS_c[P]  = x0~[P] rlk0[c][P] + x1~[P] rlk1[c][P]          -> Y = INTT_P  (kept in shared memory)
+//   KS_c[q1] = x0~[q1] rlk0[c][q1] + d2[q1] rlk1[c][q1]        -> U = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
+//   y^ = centred_P(Y);  R = U - P^-1 y^ (mod q1);  z^ = centred_q1(R)
+//   A  = NTT_q0(P^-1 y^ + z^)
+//   KS_c[q0] = d2[q0] rlk0[c][q0] + x1~[q0] rlk1[c][q0]
+//   C_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - A)   (level 0; accumulate: dst += C_c, paper order)
+// (the digit of limb j in its own limb is d2[q_j] itself: no transform needed there)
+constexpr size_t K3_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+__global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumulate)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *ys = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    // rlk layout [j][c][l][N]
+    const ulonglong2 *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * N;
+    const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
+    const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
+    const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N; // d_c[q0], d_c[q1]
+    uint64_t a[E];
+    // ---- P limb
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(xu + 1 * N + j), v = ld2(xu + 3 * N + j);
+        const ulonglong2 k0a = ld2k(r0 + 2 * N + j), k0b = ld2k(r0 + 2 * N + j + 1);
+        const ulonglong2 k1a = ld2k(r1 + 2 * N + j), k1b = ld2k(r1 + 2 * N + j + 1);
+        a[e] = red8to4<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a));
+        a[e + 1] = red8to4<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b));
+    }
+    inv<2>(a, sm, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // Y, canonical [0, P), coefficient j_M1(tid, e)
+    // ---- q1 limb
+    const ulonglong2 pinv1 = K.pinv[1];
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
+        const ulonglong2 k0a = ld2k(r0 + 1 * N + j), k0b = ld2k(r0 + 1 * N + j + 1);
+        const ulonglong2 k1a = ld2k(r1 + 1 * N + j), k1b = ld2k(r1 + 1 * N + j + 1);
+        const uint64_t ka = shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a); // < 8 q1
+        const uint64_t kb = shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b);
+        a[e] = red8to4<1>(dd.x + shoup4<1>(ka, pinv1));                  // < 5 q1 -> < 4 q1
+        a[e + 1] = red8to4<1>(dd.y + shoup4<1>(kb, pinv1));
+    }
+    inv<1>(a, sm, K.pr[1]); // U, canonical
+    // ---- rescale in coefficient form
+    const ulonglong2 pinv0 = K.pinv[0];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = ys[tid + T * e];
+        const uint64_t R = reduce_bnd<1>(a[e] + 4 * Q1 - shoup4<1>(centP_q1(y), pinv1)); // U - P^-1 y^
+        const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                            // centred, in q0
+        a[e] = shoup4<0>(centP_q0(y), pinv0) + z;                                        // < 5 q0
+    }
+    fwd<0>(a, sm, K.pr[0]); // A, canonical
+    // ---- q0 limb and output
+    const ulonglong2 q1inv = K.q1inv;
+    uint64_t *co = dst.at(pi, c);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
+        const ulonglong2 k0a = ld2k(r0 + j), k0b = ld2k(r0 + j + 1);
+        const ulonglong2 k1a = ld2k(r1 + j), k1b = ld2k(r1 + j + 1);
+        const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // < 8 q0
+        const uint64_t kb = shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b);
+        // d + P^-1 KS - A + q0 < q0 + 4 q0 + q0
+        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + shoup4<0>(ka, pinv0) + Q0 - a[e], q1inv));
+        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + shoup4<0>(kb, pinv0) + Q0 - a[e + 1], q1inv));
+        if (accumulate) {
+            const ulonglong2 cc = *reinterpret_cast<const ulonglong2 *>(co + j);
+            oa = csub(oa + cc.x, Q0);
+            ob = csub(ob + cc.y, Q0);
         }
-        if (!last) {
-            store_eval(cout.at(pi, c), a);
-            break;
-        }
+        st2(co + j, oa, ob);
     }
 }
 
@@ -414,14 +348,6 @@ __global__ void __launch_bounds__(T, 1) k_rot_ks(MatchK K, CtBuf cin, CtBuf cout
 // - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.
 constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 
-// centred_P(y) mod q0 for canonical y in [0, P), result in [0, 2 q0): y - P = y + (5 q0 - P) mod q0
-BM_D uint64_t centP_q0(uint64_t y)
-{
-    constexpr uint64_t K5 = 5 * Q0 - QP;
-    const uint64_t x = y > (QP >> 1) ? y + K5 : y;
-    const uint64_t Qe = x >> 58;
-    return x - (Qe << 58) + Qe * ((1ull << 58) - Q0);
-}
 
 __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 {
@@ -429,7 +355,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
-    uint64_t *ks1 = K.XC + (size_t)pi * 2 * N, *tsc = ks1 + N;
+    uint64_t *ks1 = K.D2 + (size_t)pi * 2 * N, *tsc = ks1 + N; // D2 is dead after K3
     const ulonglong2 pinv = K.pinv[0];
     stage_by_j(S0, cin.at(pi, 0));
     stage_by_j(S1, cin.at(pi, 1));
@@ -716,12 +642,8 @@ int ctx_get(DevCtx **out)
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
     cudaFuncSetAttribute(k_tensor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
-    set_smem(k_d2_intt);
-    set_smem(k_modup_ntt);
-    set_smem(k_ks_intt);
-    set_smem(k_rescale_ntt);
-    set_smem(k_rot_digit);
-    set_smem(k_rot_ks);
+    cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
+    cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     set_smem(k_encrypt);
@@ -1036,8 +958,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     K.XC = K.D2 + 2 * P1;
     K.XU = K.XC + 2 * P1;
     K.ACC = order == BM_ORDER_PAPER ? K.XU + 4 * P1 : nullptr;
-    const CtBuf bufC = order == BM_ORDER_PAPER ? CtBuf{K.ACC, 2 * N} : CtBuf{K.XU, 4 * N};
-    const CtBuf bufD = CtBuf{K.XU + 2 * N, 4 * N};
+    const CtBuf bufC = order == BM_ORDER_PAPER ? CtBuf{K.ACC, 2 * N} : CtBuf{K.XC, 2 * N};
 
     bool prof;
     {
@@ -1077,42 +998,20 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
             beg(0, 2 * np);
             k_tensor<<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
-            k_d2_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K);
             end();
-            beg(1, 4 * np);
-            k_modup_ntt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
+            beg(1, 6 * np);
+            k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
             end();
-            beg(2, 4 * np);
-            k_ks_intt<<<4 * npu, T, SMEM_BYTES, s>>>(K);
-            end();
-            beg(3, 2 * np);
-            k_rescale_ntt<<<2 * npu, T, SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
+            beg(2, 6 * np);
+            k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             end();
             rc = launch_check();
         }
         if (log_s > 0 && !rc) {
-            if (getenv("BM_LADDER_UNFUSED")) { // two-kernel-per-step ladder (kept for A/B measurement)
-                CtBuf cin = bufC, cout = bufD;
-                for (int i = 1; i <= log_s && !rc; i++) {
-                    const uint32_t g = (uint32_t)powmod_d(5, (uint64_t)1 << (i - 1), 2 * N);
-                    beg(4, 2 * np);
-                    k_rot_digit<<<npu, T, SMEM_BYTES, s>>>(K, cin, g);
-                    end();
-                    const int last = i == log_s;
-                    beg(4, (last ? 6 : 4) * np);
-                    k_rot_ks<<<2 * npu, T, SMEM_BYTES, s>>>(K, cin, cout, i - 1, g, last);
-                    end();
-                    rc = launch_check();
-                    CtBuf t = cin;
-                    cin = cout;
-                    cout = t;
-                }
-            } else {
-                beg(4, 6 * log_s * np);
-                k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
-                end();
-                rc = launch_check();
-            }
+            beg(4, 6 * log_s * np);
+            k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            end();
+            rc = launch_check();
         }
         if (log_s == 0 && !rc) {
             beg(6, 2 * np);

@@ -30,9 +30,10 @@ template <int PI> BM_D uint64_t mul_q(uint64_t Q)
 // Q = a1 wp1 + hi(a0 wp1) + hi(a1 wp0) (32-bit halves) under-estimates floor(a wp / 2^64) by at
 // most 2; the remainder a w - Q q is formed mod 2^64 as a w + Q (2^64 - q) in one multiply-add
 // chain: 2 IMAD.HI + 3 IMAD.WIDE + 4 IMAD on the FMA-heavy pipe, one carry on the ALU pipe.
-// (IMAD.WIDE / IMAD.HI issue at half the IMAD rate, tools/pipe_bench.cu.  Forming Q q from
-// shifts for q = 2^k - c moves work to the ALU pipe, but ptxas re-balances it back onto IMAD.X
-// and the transform got slower on B200, so the plain chain is kept.)
+// (IMAD.WIDE / IMAD.HI issue at half the IMAD rate, tools/pipe_bench.cu.  Tried and dropped:
+// forming Q q from shifts for q = 2^k - c (ptxas re-balances it back onto IMAD.X, slower), and
+// the quotient's cross terms on the idle FP64 pipe (exact, but the u32 <-> f64 conversions cost
+// more FMA/ALU issue than the two IMAD.HI they replace: 2.36 vs 2.75 butterflies/clk/SM).)
 template <int PI> BM_D uint64_t shoup4(uint64_t a, uint64_t w, uint64_t wp)
 {
 #ifdef BM_SHOUP_C
