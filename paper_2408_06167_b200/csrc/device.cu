@@ -195,20 +195,6 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
 
 // ================================================================== prime-specialised pointwise helpers
 // reduce_bnd<PI>: exact x mod q for x < 2^64 (q0, P) / x < 2^62 (q1), ntt2.cuh.
-// centred_P(y) mod q0 for canonical y in [0, P), result in [0, 2 q0): y - P = y + (5 q0 - P) mod q0
-BM_D uint64_t centP_q0(uint64_t y)
-{
-    constexpr uint64_t K5 = 5 * Q0 - QP;
-    const uint64_t x = y > (QP >> 1) ? y + K5 : y;
-    const uint64_t Qe = x >> 58;
-    return x - (Qe << 58) + Qe * ((1ull << 58) - Q0);
-}
-// y in [0, P) canonical -> centred_P(y) mod q1, canonical: y - P = y + (K q1 - P), K = 2^20 + 2
-BM_D uint64_t centP_q1(uint64_t y)
-{
-    constexpr uint64_t K = ((1ull << 20) + 2) * Q1 - QP; // >= 0, and P + K < 2^62
-    return reduce_bnd<1>(y > (QP >> 1) ? y + K : y);
-}
 // x < 8q -> [0, 4q)
 template <int PI> BM_D uint64_t red8to4(uint64_t x)
 {
@@ -255,6 +241,7 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
 
 // ================================================================== K3: key switch + ModDown + rescale
 // CTA (pair, c), R22 (exact rewriting of ModDown followed by the rescale by q1):
+// (the device rlk carries P^-1 in its Q limbs, so the Q-limb inner products below are P^-1 KS_c)
 //   KS_c[P]  = x0~[P] rlk0[c][P] + x1~[P] rlk1[c][P]          -> Y = INTT_P  (kept in shared memory)
 //   KS_c[q1] = x0~[q1] rlk0[c][q1] + d2[q1] rlk1[c][q1]        -> U = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
 //   y^ = centred_P(Y);  R = U - P^-1 y^ (mod q1);  z^ = centred_q1(R)
@@ -297,20 +284,23 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
         const ulonglong2 k0a = ld2k(r0 + 1 * N + j), k0b = ld2k(r0 + 1 * N + j + 1);
         const ulonglong2 k1a = ld2k(r1 + 1 * N + j), k1b = ld2k(r1 + 1 * N + j + 1);
-        const uint64_t ka = shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a); // < 8 q1
+        // P^-1 KS_c[q1] (P^-1 is folded into the device rlk Q limbs), < 8 q1
+        const uint64_t ka = shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a);
         const uint64_t kb = shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b);
-        a[e] = red8to4<1>(dd.x + shoup4<1>(ka, pinv1));                  // < 5 q1 -> < 4 q1
-        a[e + 1] = red8to4<1>(dd.y + shoup4<1>(kb, pinv1));
+        a[e] = reduce_bnd<1>(dd.x + ka);
+        a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
     inv<1>(a, sm, K.pr[1]); // U, canonical
     // ---- rescale in coefficient form
     const ulonglong2 pinv0 = K.pinv[0];
+    // y^ = y - [y > P/2] P, so P^-1 y^ = P^-1 y - [y > P/2] in every q limb (no centring reduction)
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const uint64_t y = ys[tid + T * e];
-        const uint64_t R = reduce_bnd<1>(a[e] + 4 * Q1 - shoup4<1>(centP_q1(y), pinv1)); // U - P^-1 y^
-        const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                            // centred, in q0
-        a[e] = shoup4<0>(centP_q0(y), pinv0) + z;                                        // < 5 q0
+        const uint64_t f = y > (QP >> 1) ? 1 : 0;
+        const uint64_t R = reduce_bnd<1>(a[e] + f + 4 * Q1 - shoup4<1>(y, pinv1)); // U - P^-1 y^
+        const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
+        a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
     }
     fwd<0>(a, sm, K.pr[0]); // A, canonical
     // ---- q0 limb and output
@@ -322,11 +312,11 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
         const ulonglong2 k0a = ld2k(r0 + j), k0b = ld2k(r0 + j + 1);
         const ulonglong2 k1a = ld2k(r1 + j), k1b = ld2k(r1 + j + 1);
-        const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // < 8 q0
+        const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // P^-1 KS_c[q0], < 8 q0
         const uint64_t kb = shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b);
-        // d + P^-1 KS - A + q0 < q0 + 4 q0 + q0
-        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + shoup4<0>(ka, pinv0) + Q0 - a[e], q1inv));
-        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + shoup4<0>(kb, pinv0) + Q0 - a[e + 1], q1inv));
+        // d + P^-1 KS - A + q0 < 10 q0
+        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + Q0 - a[e], q1inv));
+        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + Q0 - a[e + 1], q1inv));
         if (accumulate) {
             const ulonglong2 cc = *reinterpret_cast<const ulonglong2 *>(co + j);
             oa = csub(oa + cc.x, Q0);
@@ -342,7 +332,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
 // j, padded), so C never leaves the SM between steps.  Per step r = 2^i, g = 5^r mod 2N:
 //   digit   x   = INTT_q0(sigma_g(c1)) in [0, q0), lifted to P as is (reading R4); XP = NTT_P(x)
 //   comp c  y^c = centred_P(INTT_P(XP gk_r[c][P]))
-//           c_c <- c_c + [c = 0] sigma_g(c0) + P^-1 (sigma_g(c1) gk_r[c][q0] - NTT_q0(y^c))
+//           c_c <- c_c + [c = 0] sigma_g(c0) + sigma_g(c1) (P^-1 gk_r[c][q0]) - NTT_q0(P^-1 y^c)
+// (P^-1 is folded into the device Galois keys' q0 limb, and P^-1 y^c = P^-1 y - [y > P/2] needs
+// no centring reduction)
 // The last step leaves the NTT domain directly (INTT is linear, the rounding term y^c is already
 // in coefficient form): out_c = INTT_q0(c_c + [c = 0] sigma(c0) + P^-1 sigma(c1) gk[c][q0])
 // - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.
@@ -393,18 +385,20 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                 }
             }
             inv<2>(a, XB, K.pr[2]);
+            // P^-1 y^c mod q0 with y^c = y - [y > P/2] P:  P^-1 y - [y > P/2], < 5 q0
 #pragma unroll
-            for (int e = 0; e < E; e++) a[e] = centP_q0(a[e]); // y^c mod q0, [0, 2 q0)
+            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
             uint64_t *S = c ? S1 : S0;
             const ulonglong2 *gq = c ? gq1 : gq0;
             if (!last) {
-                fwd<0>(a, XB, K.pr[0]); // NTT_q0(y^c), canonical
+                fwd<0>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), canonical
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const int j = j_M4(tid, e), jp = auto_perm(j, g);
-                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e))); // [0, 4 q0)
-                    uint64_t v = shoup4<0>(ks + Q0 - a[e], pinv) + S[pidx(j)];                  // < 5 q0
-                    if (c == 0) v += S0[pidx(jp)];                                                // < 6 q0
+                    // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e)));
+                    uint64_t v = ks + Q0 - a[e] + S[pidx(j)]; // < 6 q0
+                    if (c == 0) v += S0[pidx(jp)];           // < 7 q0
                     a[e] = reduce_bnd<0>(v);
                 }
                 __syncthreads(); // every read of the old c_c is done
@@ -412,12 +406,12 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                 for (int e = 0; e < E; e++) S[pidx(j_M4(tid, e))] = a[e];
             } else {
 #pragma unroll
-                for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv); // P^-1 y^c, [0, 4 q0)
+                for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = a[e]; // P^-1 y^c (coefficients), < 5 q0
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const int j = j_M4(tid, e), jp = auto_perm(j, g);
                     const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e)));
-                    uint64_t v = shoup4<0>(ks, pinv) + S[pidx(j)];
+                    uint64_t v = ks + S[pidx(j)]; // < 5 q0
                     if (c == 0) v += S0[pidx(jp)];
                     a[e] = reduce_bnd<0>(v);
                 }
@@ -518,7 +512,8 @@ struct ConvK {
     const uint64_t *in;
     uint64_t *out;
     int n_limbs;
-    int lp[3]; // prime index of each limb
+    int lp[3];          // prime index of each limb
+    uint64_t scale[3];  // k_key_ntt: constant folded into each limb (canonical, < q)
 };
 
 // one block per polynomial; dir 0: coefficient -> NTT, 1: NTT -> coefficient
@@ -557,9 +552,10 @@ __global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
     uint64_t a[E];
     load_coef(a, C.in + (size_t)poly * N);
     fwd_rt(a, sm, P, pidx_);
+    const uint64_t sc = C.scale[li];
 #pragma unroll
     for (int e = 0; e < E; e++) {
-        const uint64_t w = a[e];
+        const uint64_t w = (uint64_t)((u128)a[e] * sc % P.q); // setup only: plain 128-bit remainder
         dst[(size_t)poly * N + pos_M4(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
     }
 }
@@ -700,7 +696,9 @@ struct bm_evk_dev {
     ulonglong2 *gk;  // [n_rot][2][2][N]
 };
 
-static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out)
+// keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1)
+static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out,
+                            const uint64_t *scale = nullptr)
 {
     uint64_t *tmp = nullptr;
     ulonglong2 *dst = nullptr;
@@ -717,6 +715,7 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     K.out = nullptr;
     K.n_limbs = n_limbs;
     for (int i = 0; i < 3; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
+    for (int i = 0; i < 3; i++) K.scale[i] = scale && i < n_limbs ? scale[i] : 1;
     k_key_ntt<<<(unsigned)n_polys, T, SMEM_BYTES>>>(K, dst);
     int rc = launch_check();
     if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
@@ -764,8 +763,11 @@ int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
     d->n_rot = evk->n_rot;
     d->gk = nullptr;
     const int lr[3] = {0, 1, 2}, lg[2] = {0, 2};
-    rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk);
-    if (!rc && evk->n_rot > 0) rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk);
+    // device convention: P^-1 is folded into the Q limbs of the key-switching keys (the ModDown
+    // multiplies every Q-limb inner product by P^-1 anyway; exact mod q, saves one product)
+    const uint64_t sr[3] = {C->pinv[0].x, C->pinv[1].x, 1}, sg[2] = {C->pinv[0].x, 1};
+    rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk, sr);
+    if (!rc && evk->n_rot > 0) rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk, sg);
     if (rc) {
         cudaFree(d->rlk);
         delete d;

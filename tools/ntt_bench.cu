@@ -57,7 +57,7 @@ int main(int argc, char **argv)
 {
     int blocks = argc > 1 ? atoi(argv[1]) : 296 * 4;
     int iters = argc > 2 ? atoi(argv[2]) : 20;
-    const size_t SM_BYTES = SMEM_WORDS * 8;
+    const size_t SM_BYTES = argc > 3 ? (size_t)atoi(argv[3]) : SMEM_WORDS * 8; // larger: less L1 left for twiddles
     typedef void (*KF)(PrimeK, uint64_t *, int);
     KF kf[3][3] = {{k_bench<1, 0>, k_bench<1, 1>, k_bench<1, 2>}, {k_bench<2, 0>, k_bench<2, 1>, k_bench<2, 2>},
                    {k_bench3<0>, k_bench3<1>, k_bench3<2>}};
