@@ -35,7 +35,10 @@ N_RING = 8192
 BFLY = (N_RING // 2) * 13          # butterflies (= modmuls) per 8192-point transform
 SM_COUNT = 148
 IMAD_PER_CLK_SM = 64               # FMA pipe, 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
-MUL32_PER_MODMUL = 10              # 32x32 partial products of one 64-bit Shoup modmul
+# FMA-pipe issue slots (in IMAD units) of the cheapest 64-bit Shoup modmul a w mod q: 4 IMAD (low
+# words) + 3 IMAD.WIDE + 2 IMAD.HI, the wide / high forms at half the IMAD rate (measured 25-29 vs
+# 63 lanes/clk/SM, tools/pipe_bench.cu, profiles/r01_pipe_bench.txt): 4 + 2 x 5 = 14
+IMAD_SLOTS_PER_MODMUL = 14
 
 
 def parse():
@@ -252,7 +255,7 @@ def run_ours(args):
     dom = max(per_class, key=lambda c: per_class[c]["ms_per_step"])
     clocks = clk.summary()
     f_peak = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / MUL32_PER_MODMUL / 1e9      # Gmodmul/s
+    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / IMAD_SLOTS_PER_MODMUL / 1e9  # Gmodmul/s
     ach = per_class[dom]["gmodmul_s"]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
@@ -264,7 +267,8 @@ def run_ours(args):
     roofline = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2),
                 "unit": "Gmodmul/s", "frac": round(ach / peak, 4), "traffic": traffic,
                 "peak_basis": f"{SM_COUNT} SMs x {IMAD_PER_CLK_SM} IMAD/clk x {f_peak / 1e6:.0f} MHz / "
-                              f"{MUL32_PER_MODMUL} 32-bit multiplies per 64-bit modmul",
+                              f"{IMAD_SLOTS_PER_MODMUL} IMAD issue slots per 64-bit Shoup modmul "
+                              f"(4 IMAD + 3 IMAD.WIDE + 2 IMAD.HI at half rate)",
                 "step_gmodmul_s": round(sum(mm.values()) * total_pairs / (ms_step / 1e3) / 1e9, 2),
                 "hbm": {"achieved_gbs": round(hbm_achieved, 2), "peak_gbs": hbm_gbs,
                         "frac": round(hbm_achieved / hbm_gbs, 5)},

@@ -15,7 +15,7 @@ import io
 import subprocess
 import sys
 
-MATCH_KERNELS = ("k_tensor_intt", "k_modup_ntt", "k_ks_intt", "k_rescale_ntt", "k_ladder", "k_rot_digit",
+MATCH_KERNELS = ("k_tensor_intt", "k_modup_ntt", "k_ks_intt", "k_rescale_ntt", "k_ladder", "k_rot_digit", "k_digits",
                  "k_rot_ks", "k_out_intt", "k_relin", "k_tensor")
 
 
