@@ -92,6 +92,17 @@ template <int PI> BM_D uint64_t reduce_bnd(uint64_t x)
     return r >= q ? r - q : r;
 }
 
+// x - floor(x / 2^k) q = (x mod 2^k) + floor(x / 2^k) c  in [0, 2q) for any x < 2^64 (q0, P):
+// reduce_bnd without its final conditional subtraction (the lazy reductions of ntt3.cuh)
+template <int PI> BM_D uint64_t reduce_lazy(uint64_t x)
+{
+    static_assert(PI != 1, "q1 transforms never reduce inside");
+    constexpr int k = PI == 0 ? 58 : 60;
+    constexpr uint32_t c = (uint32_t)((1ull << k) - PrimeC<PI>::q); // 835583, 16383
+    const uint32_t Qe = (uint32_t)(x >> k);                         // <= 63 / 15
+    return (x & ((1ull << k) - 1)) + (uint64_t)(Qe * c);
+}
+
 // ------------------------------------------------------------------ forward (L1 -> L3)
 template <int PI> BM_D void ct4(uint64_t &x, uint64_t &y, ulonglong2 w)
 {
@@ -147,6 +158,20 @@ template <int PI> BM_D void ntt_fwd2(uint64_t a[32], uint64_t *sm, const PrimeK 
     for (int e = 0; e < 32; e++) a[e] = reduce_full<PI>(a[e], P.one_p);
 }
 
+// Forward CT butterfly of stage s for ntt3.cuh.  q0, q1: never reduced (bound grows by 4q per
+// stage, < 53 q < 2^64 after 13 stages).  P (16 P < 2^64): the unmultiplied input is reduced
+// lazily to [0, 2q) on stages s = 0 (mod 3), so inputs stay < 14 q (2 + 3 x 4); one 5-instruction
+// lazy reduction every third stage instead of a 6-instruction conditional subtraction each stage.
+template <int PI> BM_D void ct4s(uint64_t &x, uint64_t &y, ulonglong2 w, int s)
+{
+    constexpr uint64_t q = PrimeC<PI>::q;
+    uint64_t X = x;
+    if (PI == 2 && s % 3 == 0) X = reduce_lazy<2>(X);
+    const uint64_t T = shoup4<PI>(y, w); // [0, 4q)
+    x = X + T;
+    y = X - T + 4 * q;
+}
+
 // ------------------------------------------------------------------ inverse (L3 -> L1)
 // GS butterfly of inverse stage number ST (0 = first executed) whose inputs are < B q with
 // B = 4 (q0, P: reduced every stage) or 4 * 2^ST (q1: never reduced): x + y, (x - y + Bq) w
@@ -157,6 +182,24 @@ template <int PI, int ST> BM_D void gs4(uint64_t &x, uint64_t &y, ulonglong2 w)
     uint64_t X = x + y;
     if (PI != 1) X = X >= 4 * q ? X - 4 * q : X; // q0, P: keep [0, 4q)
     const uint64_t T = x - y + (uint64_t)B * q;
+    x = X;
+    y = shoup4<PI>(T, w);
+}
+
+// Inverse GS butterfly of stage ST (0 = first executed) for ntt3.cuh, inputs < B q: the x-side
+// output x + y doubles the bound each stage, the y-side (a Shoup product) is < 4q.
+//   q1: B = 4 << ST, never reduced (< 2^15 q1 after 12 stages);
+//   q0: B = 4 << (ST mod 4), x + y reduced lazily to [0, 2q) when ST = 3 (mod 4) (64 q0 < 2^64);
+//   P:  B = 4 << (ST mod 2), reduced when ST is odd (16 P < 2^64).
+// So B = 4 again at ST = 12 (the last stage, N^-1 folded in, ntt3.cuh) for every prime but q1.
+template <int PI, int ST> BM_D void gs4s(uint64_t &x, uint64_t &y, ulonglong2 w)
+{
+    constexpr uint64_t q = PrimeC<PI>::q;
+    constexpr uint64_t B = PI == 1 ? (4ull << ST) : PI == 0 ? (4ull << (ST % 4)) : (4ull << (ST % 2));
+    constexpr bool RED = PI == 0 ? (ST % 4 == 3) : PI == 2 ? (ST % 2 == 1) : false;
+    uint64_t X = x + y;
+    if (RED) X = reduce_lazy<PI == 1 ? 0 : PI>(X);
+    const uint64_t T = x - y + B * q;
     x = X;
     y = shoup4<PI>(T, w);
 }

@@ -70,7 +70,7 @@ template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (k >> (4 - s))));
+            ct4s<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (k >> (4 - s))), s);
         }
     }
     xchg<1, 2>(a, sm);
@@ -83,7 +83,7 @@ template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
 #pragma unroll
             for (int k = 0; k < E; k++) {
                 if (k & half) continue;
-                ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (B << (s - 4)) + (k >> (8 - s))));
+                ct4s<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (B << (s - 4)) + (k >> (8 - s))), s);
             }
         }
     }
@@ -96,7 +96,7 @@ template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (G << (s - 8)) + (k >> (12 - s))));
+            ct4s<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (G << (s - 8)) + (k >> (12 - s))), s);
         }
     }
     // stage 12 (t = 1) on lane pairs: the even lane takes butterflies k = 2m, the odd lane k = 2m+1
@@ -104,7 +104,7 @@ template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
-        ct4<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd));
+        ct4s<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd), 12);
         a[2 * m] = reduce_bnd<PI>(x);
         a[2 * m + 1] = reduce_bnd<PI>(y);
     }
@@ -117,7 +117,7 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
     const int G = tid >> 1, odd = tid & 1;
     // stage 12 (first executed, st = 0): in-register pairs (j, j+1)
 #pragma unroll
-    for (int m = 0; m < 8; m++) gs4<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(P.inv + 4096 + 16 * G + 2 * m + odd));
+    for (int m = 0; m < 8; m++) gs4s<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(P.inv + 4096 + 16 * G + 2 * m + odd));
     // back to M3: even lane keeps a[2m] and receives a[2m+1]; odd lane keeps a[2m+1]
 #pragma unroll
     for (int m = 0; m < 8; m++) {
@@ -134,10 +134,10 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
             if (k & half) continue;
             const ulonglong2 w = ldtw(P.inv + (1 << s) + (G << (s - 8)) + (k >> (12 - s)));
             switch (12 - s) {
-            case 1: gs4<PI, 1>(a[k], a[k + half], w); break;
-            case 2: gs4<PI, 2>(a[k], a[k + half], w); break;
-            case 3: gs4<PI, 3>(a[k], a[k + half], w); break;
-            default: gs4<PI, 4>(a[k], a[k + half], w); break;
+            case 1: gs4s<PI, 1>(a[k], a[k + half], w); break;
+            case 2: gs4s<PI, 2>(a[k], a[k + half], w); break;
+            case 3: gs4s<PI, 3>(a[k], a[k + half], w); break;
+            default: gs4s<PI, 4>(a[k], a[k + half], w); break;
             }
         }
     }
@@ -152,10 +152,10 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
                 if (k & half) continue;
                 const ulonglong2 w = ldtw(P.inv + (1 << s) + (B << (s - 4)) + (k >> (8 - s)));
                 switch (12 - s) {
-                case 5: gs4<PI, 5>(a[k], a[k + half], w); break;
-                case 6: gs4<PI, 6>(a[k], a[k + half], w); break;
-                case 7: gs4<PI, 7>(a[k], a[k + half], w); break;
-                default: gs4<PI, 8>(a[k], a[k + half], w); break;
+                case 5: gs4s<PI, 5>(a[k], a[k + half], w); break;
+                case 6: gs4s<PI, 6>(a[k], a[k + half], w); break;
+                case 7: gs4s<PI, 7>(a[k], a[k + half], w); break;
+                default: gs4s<PI, 8>(a[k], a[k + half], w); break;
                 }
             }
         }
@@ -169,9 +169,9 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
             if (k & half) continue;
             const ulonglong2 w = ldtw(P.inv + (1 << s) + (k >> (4 - s)));
             switch (12 - s) {
-            case 9: gs4<PI, 9>(a[k], a[k + half], w); break;
-            case 10: gs4<PI, 10>(a[k], a[k + half], w); break;
-            default: gs4<PI, 11>(a[k], a[k + half], w); break;
+            case 9: gs4s<PI, 9>(a[k], a[k + half], w); break;
+            case 10: gs4s<PI, 10>(a[k], a[k + half], w); break;
+            default: gs4s<PI, 11>(a[k], a[k + half], w); break;
             }
         }
     }
