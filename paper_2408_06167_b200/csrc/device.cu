@@ -230,12 +230,12 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
         inv<1>(a, sm, K.pr[1]);
 #pragma unroll
         for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
-        fwd<0>(a, sm, K.pr[0]);
+        fwd<0, false>(a, sm, K.pr[0]); // lazy [0, 2 q0): only ever a Shoup-product operand
     }
     store_eval(xu, a);
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = xs[tid + T * e];
-    fwd<2>(a, sm, K.pr[2]);
+    fwd<2, false>(a, sm, K.pr[2]);
     store_eval(xu + N, a);
 }
 
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
         a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
     }
-    fwd<0>(a, sm, K.pr[0]); // A, canonical
+    fwd<0, false>(a, sm, K.pr[0]); // A, in [0, 2 q0)
     // ---- q0 limb and output
     const ulonglong2 q1inv = K.q1inv;
     uint64_t *co = dst.at(pi, c);
@@ -314,9 +314,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const ulonglong2 k1a = ld2k(r1 + j), k1b = ld2k(r1 + j + 1);
         const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // P^-1 KS_c[q0], < 8 q0
         const uint64_t kb = shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b);
-        // d + P^-1 KS - A + q0 < 10 q0
-        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + Q0 - a[e], q1inv));
-        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + Q0 - a[e + 1], q1inv));
+        // d + P^-1 KS - A + 2 q0 < 11 q0
+        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + 2 * Q0 - a[e], q1inv));
+        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + 2 * Q0 - a[e + 1], q1inv));
         if (accumulate) {
             const ulonglong2 cc = *reinterpret_cast<const ulonglong2 *>(co + j);
             oa = csub(oa + cc.x, Q0);

@@ -60,7 +60,9 @@ BM_D void xchg(uint64_t a[E], uint64_t *sm)
 BM_D uint64_t shfl1(uint64_t v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
 
 // ------------------------------------------------------------------ forward (M1 -> M4)
-template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
+// CANON = false: outputs only reduced to [0, 2q) (q0, P; q1 stays canonical) for consumers that
+// take lazy operands (Shoup products, sums that are reduced afterwards)
+template <int PI, bool CANON = true> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
 {
     const int tid = threadIdx.x;
     // pass 1: s = 0..3, t = 512 (8 >> s); partner k + (8 >> s); twiddle (1<<s) + (k >> (4-s))
@@ -105,8 +107,13 @@ template <int PI> BM_D void fwd(uint64_t a[E], uint64_t *sm, const PrimeK &P)
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
         ct4s<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd), 12);
-        a[2 * m] = reduce_bnd<PI>(x);
-        a[2 * m + 1] = reduce_bnd<PI>(y);
+        if (CANON || PI == 1) {
+            a[2 * m] = reduce_bnd<PI>(x);
+            a[2 * m + 1] = reduce_bnd<PI>(y);
+        } else {
+            a[2 * m] = reduce_lazy<PI == 1 ? 0 : PI>(x);
+            a[2 * m + 1] = reduce_lazy<PI == 1 ? 0 : PI>(y);
+        }
     }
 }
 
