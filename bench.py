@@ -231,7 +231,7 @@ def run_ours(args):
     # launches of our kernels per step: chunks x (3 per part-round + 1 fused ladder (or output INTT if s = 1))
     import math
     total_pairs = n_sets * nq
-    chunk = int(os.environ.get("BM_CHUNK_PAIRS", "1024"))
+    chunk = int(os.environ.get("BM_CHUNK_PAIRS", "16384"))
     n_chunks = math.ceil(total_pairs / min(chunk, total_pairs))
     rounds = 1 if order == 0 else p
     launches = n_chunks * (3 * rounds + 1)

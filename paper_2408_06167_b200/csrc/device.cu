@@ -884,7 +884,7 @@ int bm_ct_from_coeff(const bm_params *prm, const uint64_t *d_in, int64_t n_cts, 
 // ------------------------------------------------------------------ the scan
 static int64_t chunk_pairs(int64_t total)
 {
-    int64_t ch = 1024;
+    int64_t ch = 16384; // large chunks: fewer launches and kernel tails (workspace 768 KiB per pair)
     if (const char *e = getenv("BM_CHUNK_PAIRS")) {
         long v = atol(e);
         if (v > 0) ch = v;
