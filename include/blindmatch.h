@@ -158,8 +158,10 @@ int bm_match(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_
 
 /* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
  * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call.  The queries are
- * processed in groups (8, or BM_HOST_GROUPS): group g's upload, scan and download overlap the
- * neighbouring groups (two device slots, two internal copy streams, the scan on `stream`).
+ * processed in groups of about 576 (query, set) pairs (or BM_HOST_GROUPS groups): group g's
+ * upload, scan and download overlap the neighbouring groups (four device slots, two internal
+ * copy streams, the scans alternating between `stream` and an internal stream, all starting
+ * after the work already queued on `stream`).
  * Pinned host memory is required for the overlap.  d_ws must hold bm_match_host_ws_bytes(...)
  * bytes.  Synchronous (returns after h_out is written). */
 size_t bm_match_host_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);

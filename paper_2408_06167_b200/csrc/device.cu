@@ -1038,23 +1038,28 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     return rc;
 }
 
-// End-to-end scan from host buffers: the queries are processed in groups; group g's query
-// upload (copy stream), scan (caller's stream) and result download (second copy stream) overlap
-// with the neighbouring groups through two device buffer slots and events.
-static int host_groups(int32_t nq)
+// End-to-end scan from host buffers: the queries are processed in G groups.  Group g's query
+// upload (copy stream), scan (one of two compute streams, alternating, so that one group's
+// kernels fill the tails of the previous group's) and result download (second copy stream)
+// overlap with the neighbouring groups through HOST_SLOTS device buffer slots and events.
+constexpr int HOST_SLOTS = 4;
+static int host_groups(int64_t n_sets, int32_t nq)
 {
-    int g = 8;
+    // about 576 (query, set) pairs per group (a few waves of the ladder kernel), at least 4 groups
+    int64_t g = (n_sets * (int64_t)nq + 575) / 576;
+    g = g < 4 ? 4 : g;
     if (const char *e = getenv("BM_HOST_GROUPS")) g = atoi(e) > 0 ? atoi(e) : g;
-    return nq < g ? nq : g;
+    return (int)(nq < g ? nq : g);
 }
 
 size_t bm_match_host_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, int32_t order)
 {
     if (!prm || n_sets <= 0 || nq <= 0) return 0;
-    const int G = host_groups(nq);
+    const int G = host_groups(n_sets, nq);
     const int64_t gq = (nq + G - 1) / G;
     const size_t qbytes = (size_t)gq * prm->p * 4 * N * 8, obytes = (size_t)gq * n_sets * 2 * N * 8;
-    return 2 * (qbytes + obytes) + bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order);
+    const size_t mws = (bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order) + 255) & ~(size_t)255;
+    return HOST_SLOTS * (qbytes + obytes) + 2 * mws;
 }
 
 int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
@@ -1065,22 +1070,22 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
     if (n_sets == 0 || nq == 0) return BM_OK;
     if (!h_q || !h_out || !d_ws) return BM_ERR_INVALID_ARG;
     if (ws_bytes < bm_match_host_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
-    const int G = host_groups(nq);
+    const int G = host_groups(n_sets, nq);
     const int64_t gq = (nq + G - 1) / G;
     const size_t qrow = (size_t)prm->p * 4 * N, orow = (size_t)n_sets * 2 * N; // u64 per query
-    uint64_t *dq[2], *dout[2];
-    dq[0] = (uint64_t *)d_ws;
-    dq[1] = dq[0] + gq * qrow;
-    dout[0] = dq[1] + gq * qrow;
-    dout[1] = dout[0] + gq * orow;
-    void *mws = dout[1] + gq * orow;
-    const size_t mws_bytes = ws_bytes - 2 * gq * (qrow + orow) * 8;
-    cudaStream_t sc = (cudaStream_t)stream, su, sd;
-    if (cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking) != cudaSuccess) return BM_ERR_CUDA;
-    if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) {
-        cudaStreamDestroy(su);
-        return BM_ERR_CUDA;
-    }
+    uint64_t *dq[HOST_SLOTS], *dout[HOST_SLOTS];
+    uint64_t *base = (uint64_t *)d_ws;
+    for (int k = 0; k < HOST_SLOTS; k++) dq[k] = base + k * gq * qrow;
+    base += HOST_SLOTS * gq * qrow;
+    for (int k = 0; k < HOST_SLOTS; k++) dout[k] = base + k * gq * orow;
+    base += HOST_SLOTS * gq * orow;
+    const size_t mws = (bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order) + 255) & ~(size_t)255;
+    void *ws[2] = {base, (uint8_t *)base + mws};
+    cudaStream_t sc[2], su, sd;
+    sc[0] = (cudaStream_t)stream;
+    if (cudaStreamCreateWithFlags(&sc[1], cudaStreamNonBlocking) != cudaSuccess) return BM_ERR_CUDA;
+    cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
     const int ngroups = (int)((nq + gq - 1) / gq);
     std::vector<cudaEvent_t> ev_up(ngroups), ev_done(ngroups), ev_down(ngroups);
     for (int g = 0; g < ngroups; g++) {
@@ -1088,33 +1093,42 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
         cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ev_down[g], cudaEventDisableTiming);
     }
+    cudaEvent_t ev_start;
+    cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    cudaEventRecord(ev_start, sc[0]); // everything starts after the work already on the caller's stream
+    cudaStreamWaitEvent(sc[1], ev_start, 0);
+    cudaStreamWaitEvent(su, ev_start, 0);
     int rc = BM_OK;
     for (int g = 0; g < ngroups && !rc; g++) {
-        const int slot = g & 1;
+        const int slot = g % HOST_SLOTS;
+        cudaStream_t cs = sc[g & 1];
         const int64_t q0 = g * gq, nqg = nq - q0 < gq ? nq - q0 : gq;
-        // the query slot is free once the scan of group g-2 has consumed it
-        if (g >= 2) cudaStreamWaitEvent(su, ev_done[g - 2], 0);
+        // the query slot is free once the scan of group g - HOST_SLOTS has consumed it
+        if (g >= HOST_SLOTS) cudaStreamWaitEvent(su, ev_done[g - HOST_SLOTS], 0);
         if (cudaMemcpyAsync(dq[slot], h_q + q0 * qrow, nqg * qrow * 8, cudaMemcpyHostToDevice, su) != cudaSuccess)
             rc = BM_ERR_CUDA;
         cudaEventRecord(ev_up[g], su);
-        cudaStreamWaitEvent(sc, ev_up[g], 0);
-        // the output slot is free once group g-2's results are downloaded
-        if (g >= 2) cudaStreamWaitEvent(sc, ev_down[g - 2], 0);
-        if (!rc) rc = bm_match(prm, evk, d_db, n_sets, dq[slot], (int32_t)nqg, dout[slot], mws, mws_bytes, order, stream);
-        cudaEventRecord(ev_done[g], sc);
+        cudaStreamWaitEvent(cs, ev_up[g], 0);
+        // the output slot is free once group g - HOST_SLOTS's results are downloaded
+        if (g >= HOST_SLOTS) cudaStreamWaitEvent(cs, ev_down[g - HOST_SLOTS], 0);
+        if (!rc)
+            rc = bm_match(prm, evk, d_db, n_sets, dq[slot], (int32_t)nqg, dout[slot], ws[g & 1], mws, order, cs);
+        cudaEventRecord(ev_done[g], cs);
         cudaStreamWaitEvent(sd, ev_done[g], 0);
         if (!rc && cudaMemcpyAsync(h_out + q0 * orow, dout[slot], nqg * orow * 8, cudaMemcpyDeviceToHost, sd) != cudaSuccess)
             rc = BM_ERR_CUDA;
         cudaEventRecord(ev_down[g], sd);
     }
     if (cudaStreamSynchronize(sd) != cudaSuccess || cudaStreamSynchronize(su) != cudaSuccess ||
-        cudaStreamSynchronize(sc) != cudaSuccess)
+        cudaStreamSynchronize(sc[1]) != cudaSuccess || cudaStreamSynchronize(sc[0]) != cudaSuccess)
         rc = rc ? rc : BM_ERR_CUDA;
     for (int g = 0; g < ngroups; g++) {
         cudaEventDestroy(ev_up[g]);
         cudaEventDestroy(ev_done[g]);
         cudaEventDestroy(ev_down[g]);
     }
+    cudaEventDestroy(ev_start);
+    cudaStreamDestroy(sc[1]);
     cudaStreamDestroy(su);
     cudaStreamDestroy(sd);
     return rc;
