@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--nq", type=int, default=384)
+    ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quiet", action="store_true")
@@ -196,16 +197,23 @@ def run_ours(args):
         Q, _ = I.queries(CFG, nq)
         B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
     d_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
-    ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
-    recv = torch.empty((world, nq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev) if world > 1 else None
+    # N > 1: broadcast (a3), scan and result all_to_all (a8) overlapped over query groups
+    G = args.groups if world > 1 else 1
+    gq = nq // G
+    ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, gq, order), dtype=torch.uint8, device=dev)
+    recv = torch.empty((G, world, gq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev) if world > 1 else None
+    comm_s, comp_s = (torch.cuda.Stream(), torch.cuda.Stream()) if world > 1 else (None, None)
     B.bm_sync()
     stream = torch.cuda.current_stream()
 
+    def match(g, q_g, out_g):
+        B.bm_match(prm, evk_dev, d_db, n_sets, q_g, q_g.shape[0], out_g, ws, order)
+
     def step():
-        pdist.broadcast_queries(d_q)
-        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
-        if world > 1:
-            pdist.gather_results(d_out, recv)
+        if world == 1:
+            B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+        else:
+            pdist.scan_pipelined(match, d_q, d_out, recv, G, comm_s, comp_s)
 
     log(args, f"[rank {rank}] setup done: {n_sets} sets x {nq} queries, p={p}, ws={ws.numel() / 2**30:.2f} GiB")
     for _ in range(args.warmup):
@@ -232,7 +240,7 @@ def run_ours(args):
     import math
     total_pairs = n_sets * nq
     chunk = int(os.environ.get("BM_CHUNK_PAIRS", "16384"))
-    n_chunks = math.ceil(total_pairs / min(chunk, total_pairs))
+    n_chunks = G * math.ceil(n_sets * gq / min(chunk, n_sets * gq))
     rounds = 1 if order == 0 else p
     launches = n_chunks * (3 * rounds + 1)
 
@@ -240,7 +248,8 @@ def run_ours(args):
     B.bm_set_profiling(True)
     B.bm_profile_reset()
     for _ in range(args.steps):
-        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+        for g in range(G):
+            B.bm_match(prm, evk_dev, d_db, n_sets, d_q[g * gq:(g + 1) * gq], gq, d_out[g * gq:(g + 1) * gq], ws, order)
     B.bm_sync()
     pms, pla, pun = B.bm_profile_read()
     B.bm_set_profiling(False)

@@ -55,6 +55,75 @@ def gather_results(d_out, recv=None, group=None):
     return recv
 
 
+def group_query_block(nq, groups, world_size, rank, g):
+    """Pipelined gather: queries [g nq/G, (g+1) nq/G) of group g are split into W equal blocks and
+    block k lands on rank k; returns (first query, count) of the block `rank` is root of."""
+    assert nq % (groups * world_size) == 0, "nq must be a multiple of groups x world size"
+    gq = nq // groups
+    per = gq // world_size
+    return g * gq + rank * per, per
+
+
+def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_stream=None):
+    """a3 + scan + a8 for one query batch, overlapped over `groups` query groups.
+
+    match(g, q_slice, out_slice) runs the local scan of group g (on the current stream).
+    d_q [nq][p][2][2][N] (filled on rank 0), d_out [nq][n_local][2][N], recv
+    [G][W][nq/(G W)][n_local][2][N].  Group g's broadcast and result all_to_all run on
+    `comm_stream` while other groups are scanned on `compute_stream`: the collectives are issued in
+    the same order on every rank (b0, b1, then a_g, b_{g+2}, ...), broadcasts two groups ahead.
+    With one rank, or without CUDA streams (gloo), the same sequence runs in order."""
+    w, _ = world()
+    nq = d_q.shape[0]
+    G = groups
+    assert nq % G == 0
+    gq = nq // G
+    qs = [d_q[g * gq:(g + 1) * gq] for g in range(G)]
+    outs = [d_out[g * gq:(g + 1) * gq] for g in range(G)]
+    cuda = comm_stream is not None and compute_stream is not None
+    if not cuda:
+        for g in range(G):
+            broadcast_queries(qs[g])
+            match(g, qs[g], outs[g])
+            if w > 1:
+                gather_results(outs[g], recv[g])
+        return recv
+    bw = [None] * G
+    done = [None] * G
+
+    def bcast(g):
+        if w > 1:
+            with torch.cuda.stream(comm_stream):
+                bw[g] = dist.broadcast(qs[g], src=0, async_op=True)
+
+    def a2a(g):
+        if w > 1:
+            with torch.cuda.stream(comm_stream):
+                comm_stream.wait_event(done[g])
+                dist.all_to_all_single(recv[g].view(-1), outs[g].view(-1), async_op=True).wait()
+
+    compute_stream.wait_stream(torch.cuda.current_stream())
+    comm_stream.wait_stream(torch.cuda.current_stream())
+    for g in range(min(2, G)):
+        bcast(g)
+    for g in range(G):
+        with torch.cuda.stream(compute_stream):
+            if bw[g] is not None:
+                bw[g].wait()
+            match(g, qs[g], outs[g])
+            done[g] = torch.cuda.Event()
+            done[g].record(compute_stream)
+        if g >= 1:
+            a2a(g - 1)
+        if g + 2 < G:
+            bcast(g + 2)
+    a2a(G - 1)
+    cur = torch.cuda.current_stream()
+    cur.wait_stream(compute_stream)
+    cur.wait_stream(comm_stream)
+    return recv
+
+
 def max_over_ranks(x, device):
     """max of a float over ranks (timing rule: the job time is the slowest rank)."""
     w, _ = world()

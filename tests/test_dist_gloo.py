@@ -108,3 +108,56 @@ def test_shard_ranges_cover_and_balance():
     assert pdist.query_block(384, 8, 3) == (144, 48)
     with pytest.raises(AssertionError):
         pdist.query_block(10, 4, 0)
+
+
+def _worker_pipelined(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    lo, cnt = pdist.shard_sets(n_sets, world, rank)
+    local_db = _encrypt_sets(O, T, pk, lo, cnt)
+    N = 1 << LOGN
+    q = torch.zeros((NQ, P_PARTS, 2, 2, N), dtype=torch.int64)
+    if rank == 0:
+        S = N // 2
+        qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+        q.copy_(torch.from_numpy(qc.reshape(q.shape).view(np.int64)))
+    per = -(-n_sets // world)
+    out = torch.zeros((NQ, per, 2, N), dtype=torch.int64)
+    G = 2
+    recv = torch.zeros((G, world, NQ // (G * world), per, 2, N), dtype=torch.int64)
+
+    def match(g, q_g, out_g):   # the local scan of one query group (the oracle stands in for bm_match)
+        if cnt:
+            res, pairs = O.match(LOGN, D, P_PARTS, 0, rlk, gk, local_db, q_g.numpy().view(np.uint64))
+            for i, (j, t) in enumerate(pairs):
+                out_g[j, t] = torch.from_numpy(res[i].reshape(2, N).view(np.int64))
+
+    pdist.scan_pipelined(match, q, out, recv, G)
+    np.save(os.path.join(out_dir, f"precv{rank}.npy"), recv.numpy())
+    dist.destroy_process_group()
+
+
+def test_two_rank_pipelined_scan_matches_single_process(tmp_path):
+    """bench.py's N > 1 step: broadcast, scan and all_to_all per query group (dist.scan_pipelined);
+    query j of group g lands on rank group_query_block(...) with the results of every rank's sets."""
+    port = _free_port()
+    mp.spawn(_worker_pipelined, args=(WORLD, port, str(tmp_path)), nprocs=WORLD, join=True)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    N = 1 << LOGN
+    full_db = _encrypt_sets(O, T, pk, 0, n_sets)
+    S = N // 2
+    qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+    ref, pairs = O.match(LOGN, D, P_PARTS, 0, rlk, gk, full_db, qc.reshape(NQ, P_PARTS, 2, 2, N))
+    ref = ref.reshape(NQ, n_sets, 2, N)
+    G = 2
+    for r in range(WORLD):
+        recv = np.load(tmp_path / f"precv{r}.npy").view(np.uint64)  # [G][src rank][nq/(G W)][per][2][N]
+        for g in range(G):
+            q0, nql = pdist.group_query_block(NQ, G, WORLD, r, g)
+            for src in range(WORLD):
+                lo, cnt = pdist.shard_sets(n_sets, WORLD, src)
+                assert np.array_equal(recv[g, src, :, :cnt], ref[q0:q0 + nql, lo:lo + cnt])

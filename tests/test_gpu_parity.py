@@ -216,3 +216,25 @@ def test_match_host_pipelined_equals_device(env, O, monkeypatch, groups):
     ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq), dtype=torch.uint8, device="cuda")
     B.bm_match_host(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, h_out, ws)
     assert np.array_equal(h_out.numpy().view(np.uint64), dev_out)
+
+
+def test_scan_pipelined_streams_equal_device(env, O):
+    """bench.py's N > 1 step structure (dist.scan_pipelined: per-group scans on a compute stream,
+    collectives on a comm stream) at world size 1 on the GPU == one bm_match over all queries."""
+    torch, B = env
+    from paper_2408_06167_b200 import dist as pdist
+    T = I.templates(2, 700)
+    Q, _ = I.queries(2, 8)
+    st = Setup(env, O, 128, 8, T, Q)
+    ref = st.gpu_match(0)
+    G = 4
+    gq = st.nq // G
+    out = torch.zeros((st.nq, st.n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_match_ws_bytes(st.prm, st.n_sets, gq), dtype=torch.uint8, device="cuda")
+
+    def match(g, q_g, out_g):
+        B.bm_match(st.prm, st.evk_dev, st.d_db, st.n_sets, q_g, q_g.shape[0], out_g, ws)
+
+    pdist.scan_pipelined(match, st.d_q, out, None, G, torch.cuda.Stream(), torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), ref)
