@@ -238,3 +238,26 @@ def test_scan_pipelined_streams_equal_device(env, O):
     pdist.scan_pipelined(match, st.d_q, out, None, G, torch.cuda.Stream(), torch.cuda.Stream())
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint64), ref)
+
+
+def test_config2_full_size_bench_launch(env, O):
+    """BASELINE.json configs[1] at full size in bench.py's launch configuration: 6,144 templates,
+    384 genuine queries, p = 8, all 9,216 (query, set) pairs in one bm_match launch (one chunk).
+    Bit-exact parity on sampled pairs (incl. the last query and set), and on sampled queries the
+    decrypted scores of every template vs float64 cosine and the top-1 identity."""
+    torch, B = env
+    T = I.templates(2)
+    Q, expq = I.queries(2, 384)
+    st = Setup(env, O, 128, 8, T, Q)
+    assert st.n_sets * st.nq == 9216
+    got = st.gpu_match(0)
+    rng = np.random.default_rng(2024)
+    pairs = [(383, st.n_sets - 1), (0, 0), (int(rng.integers(384)), int(rng.integers(st.n_sets)))]
+    ref = st.oracle_pairs(pairs)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k]), (j, t)
+    qs = np.sort(rng.choice(384, 6, replace=False))
+    sc = B.bm_decrypt(st.prm, st.sk, got[qs].reshape(-1, 2, 1, 8192)).reshape(len(qs), -1)[:, :T.shape[0]]
+    cos = Q[qs] @ T.T
+    assert np.abs(sc - cos).max() < 1e-6
+    assert np.array_equal(sc.argmax(1), expq[qs])
