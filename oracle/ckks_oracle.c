@@ -33,6 +33,7 @@
  *   pk           [2 comps (b,a)][2 limbs][N]
  *   rlk          [2 digits j][2 comps (b,a)][3 limbs q0,q1,P][N]
  *   gk           [n_rot][2 comps (b,a)][2 limbs q0,P][N]; entry i is rotation 2^i
+ *   hgk          [s-1][2 comps][2 limbs q0,P][N]; entry r-1 is rotation r (f2 hoisted sum)
  *   sk           int8[N] in {-1,0,1}
  */
 #include <stdint.h>
@@ -368,6 +369,39 @@ static uint64_t galois_elt(int N, uint64_t r) { return powmod(5, r, 2 * (uint64_
 /* ------------------------------------------------------------------ */
 /* key generation (rows a0 of SURVEY.md sec. 8a)     */
 /* ------------------------------------------------------------------ */
+/* One Galois key for a left rotation by r (g = 5^r mod 2N), PRNG object obj, over {q0,P}:
+ * b = -a s + e + (P mod q0) sigma_g(s) in q0; -a s + e in P; layout [2 comps (b,a)][2 limbs][N].
+ * sv: the secret as signed integers. */
+static void galois_key(const ctx_t *C, uint64_t seed, uint64_t r, uint64_t obj, int zero_error, const int64_t *sv,
+                       uint64_t *gkr)
+{
+    const int N = C->N;
+    uint64_t g = galois_elt(N, r);
+    uint64_t *tmp = malloc(sizeof(uint64_t) * N), *e = malloc(sizeof(uint64_t) * N);
+    uint64_t *s = malloc(sizeof(uint64_t) * N), *a = malloc(sizeof(uint64_t) * N);
+    uint64_t *ss = malloc(sizeof(uint64_t) * N);
+    int64_t *ev = malloc(sizeof(int64_t) * N);
+    or_sample(seed, P_GK_E, obj, 0, 2, N, 0, (uint64_t *)ev);
+    if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+    for (int li = 0; li < 2; li++) {
+        int l = li == 0 ? 0 : 2;
+        uint64_t q = C->q[l];
+        for (int k = 0; k < N; k++) { s[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+        or_sample(seed, P_GK_A, obj, (uint32_t)l, 0, N, q, a);
+        uint64_t *b = gkr + (size_t)(0 * 2 + li) * N;
+        uint64_t *aa = gkr + (size_t)(1 * 2 + li) * N;
+        poly_mul(&C->R[l], a, s, tmp);
+        poly_sub(q, N, e, tmp, b);
+        if (l == 0) {
+            automorphism(q, N, s, g, ss);
+            poly_scale(q, N, ss, C->P_mod[0], tmp);
+            poly_add(q, N, b, tmp, b);
+        }
+        memcpy(aa, a, sizeof(uint64_t) * N);
+    }
+    free(tmp); free(e); free(s); free(a); free(ss); free(ev);
+}
+
 /* sk: ternary s.  pk = (b, a) over {q0,q1}: b = -a s + e.
  * rlk_j (digit j in {0,1}) over {q0,q1,P}: b = -a s + e + [k==j] (P mod q_k) s^2, P-limb b = -a s + e.
  * gk_i (rotation 2^i) over {q0,P}: b = -a s + e + (P mod q0) sigma_g(s) in q0; -a s + e in P.
@@ -420,29 +454,27 @@ int or_keygen(int logN, uint64_t seed, int n_rot, int zero_error,
         }
     }
 
-    /* Galois keys: gk[i][comp][limb in {q0,P}][N], rotation r = 2^i */
-    for (int i = 0; i < n_rot; i++) {
-        uint64_t g = galois_elt(N, (uint64_t)1 << i);
-        or_sample(seed, P_GK_E, (uint64_t)i, 0, 2, N, 0, (uint64_t *)ev);
-        if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
-        for (int li = 0; li < 2; li++) {
-            int l = li == 0 ? 0 : 2;
-            uint64_t q = C.q[l];
-            for (int k = 0; k < N; k++) { s[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
-            or_sample(seed, P_GK_A, (uint64_t)i, (uint32_t)l, 0, N, q, a);
-            uint64_t *b = gk + ((size_t)(i * 2 + 0) * 2 + li) * N;
-            uint64_t *aa = gk + ((size_t)(i * 2 + 1) * 2 + li) * N;
-            poly_mul(&C.R[l], a, s, tmp);
-            poly_sub(q, N, e, tmp, b);
-            if (l == 0) {
-                automorphism(q, N, s, g, ss);
-                poly_scale(q, N, ss, C.P_mod[0], tmp);
-                poly_add(q, N, b, tmp, b);
-            }
-            memcpy(aa, a, sizeof(uint64_t) * N);
-        }
-    }
+    /* Galois keys: gk[i][comp][limb in {q0,P}][N], rotation r = 2^i, PRNG object i */
+    for (int i = 0; i < n_rot; i++)
+        galois_key(&C, seed, (uint64_t)1 << i, (uint64_t)i, zero_error, sv, gk + (size_t)i * 4 * N);
     free(tmp); free(e); free(s); free(a); free(s2); free(ss); free(sv); free(ev);
+    ctx_free(&C);
+    return 0;
+}
+
+/* f2: Galois keys for EVERY rotation r = 1..s-1 (the hoisted rotation sum),
+ * hgk[r-1][2 comps][2 limbs q0,P][N], PRNG object HROT_OBJ + r (disjoint from the ladder's i < 13). */
+#define HROT_OBJ 64
+int or_keygen_hoisted(int logN, uint64_t seed, int s, int zero_error, uint64_t *hgk)
+{
+    ctx_t C;
+    ctx_init(&C, logN);
+    const int N = C.N;
+    int64_t *sv = malloc(sizeof(int64_t) * N);
+    or_sample(seed, P_SK, 0, 0, 1, N, 0, (uint64_t *)sv);
+    for (int r = 1; r < s; r++)
+        galois_key(&C, seed, (uint64_t)r, (uint64_t)(HROT_OBJ + r), zero_error, sv, hgk + (size_t)(r - 1) * 4 * N);
+    free(sv);
     ctx_free(&C);
     return 0;
 }
@@ -586,6 +618,51 @@ static void rotate(const ctx_t *C, const uint64_t *in, uint64_t r, const uint64_
     free(a0); free(a1); free(xP); free(KS); free(ksd);
 }
 
+/* f2 (NOT the paper's ladder): sum_{r=0}^{s-1} Rot(C, r) at level 0 with ONE
+ * hoisted key switch (Halevi-Shoup hoisting): the digit x = c1 in coefficient form (integers in
+ * [0, q0)) is lifted to {q0, P} once; each rotation applies sigma_{5^r} to the lifted digit in each
+ * limb as a signed permutation (a negated coefficient becomes -x mod q in that limb), the products
+ * KS_r[c] = sigma_r(x~) hgk_r[c] are summed over r in {q0, P} and ModDown'ed once:
+ *   out_0 = sum_{r<s} sigma_r(c0) + ModDown(sum_{r>=1} KS_r[0]),  out_1 = c1 + ModDown(sum_{r>=1} KS_r[1]).
+ * Slot k s of the result holds the same block sum as the ladder's (decrypts to the same scores up to
+ * noise), but the residues differ: it has its own parity (order 2).  in/out [2][1][N]. */
+static void hoisted_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t q0 = C->q[0], P = C->q[2];
+    const uint64_t *c0 = in, *c1 = in + N;
+    uint64_t *xr0 = malloc(sizeof(uint64_t) * N), *xrP = malloc(sizeof(uint64_t) * N);
+    uint64_t *t = malloc(sizeof(uint64_t) * N), *xP = malloc(sizeof(uint64_t) * N);
+    uint64_t *acc = calloc((size_t)4 * N, sizeof(uint64_t)); /* [c][q0 | P][N] */
+    uint64_t *c0sum = malloc(sizeof(uint64_t) * N), *ksd = malloc(sizeof(uint64_t) * N);
+    for (int k = 0; k < N; k++) xP[k] = c1[k] % P; /* non-centred lift (reading R4): x < q0 < P */
+    memcpy(c0sum, c0, sizeof(uint64_t) * N);
+    for (int r = 1; r < s; r++) {
+        const uint64_t g = galois_elt(N, (uint64_t)r);
+        const uint64_t *key = hgk + (size_t)(r - 1) * 4 * N;
+        automorphism(q0, N, c1, g, xr0);
+        automorphism(P, N, xP, g, xrP);
+        automorphism(q0, N, c0, g, t);
+        poly_add(q0, N, c0sum, t, c0sum);
+        for (int c = 0; c < 2; c++) {
+            poly_mul(&C->R[0], xr0, key + (size_t)(c * 2 + 0) * N, t);
+            poly_add(q0, N, acc + (size_t)(c * 2 + 0) * N, t, acc + (size_t)(c * 2 + 0) * N);
+            poly_mul(&C->R[2], xrP, key + (size_t)(c * 2 + 1) * N, t);
+            poly_add(P, N, acc + (size_t)(c * 2 + 1) * N, t, acc + (size_t)(c * 2 + 1) * N);
+        }
+    }
+    for (int c = 0; c < 2; c++) {
+        moddown(C, 1, acc + (size_t)c * 2 * N, ksd);
+        poly_add(q0, N, c == 0 ? c0sum : c1, ksd, out + (size_t)c * N);
+    }
+    free(xr0); free(xrP); free(t); free(xP); free(acc); free(c0sum); free(ksd);
+}
+
+void or_hoisted_rot_sum(int logN, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); hoisted_rot_sum(&C, s, hgk, in, out); ctx_free(&C);
+}
+
 /* exported single-op entry points for the pins */
 void or_relinearize(int logN, const uint64_t *d, const uint64_t *rlk, uint64_t *out)
 {
@@ -630,6 +707,7 @@ static void tensor_acc(const ctx_t *C, const uint64_t *ca, const uint64_t *cb, u
  * order 1 (PAPER):   C = sum_i Res(Relin(tensor(C_u,i, C_s,i))), C_out starting as the
  *                    trivial zero ciphertext (line 3; reading R9).
  * then for i = 1..log2(s): C = Add(Rot(C, 2^(i-1)), C)   (lines 7-9, reading R7).
+ * order 2 (f2, not the paper's ladder): order 0's C, then hoisted_rot_sum (gk = hgk).
  * qct, sct: [p][2][2][N]; out: [2][1][N]. */
 static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64_t *rlk, const uint64_t *gk,
                        const uint64_t *qct, const uint64_t *sct, uint64_t *out)
@@ -642,7 +720,7 @@ static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64
     uint64_t *rot = malloc(sizeof(uint64_t) * 2 * N);
     const uint64_t q0 = C->q[0];
     memset(out, 0, sizeof(uint64_t) * 2 * N);
-    if (order == 0) {
+    if (order == 0 || order == 2) {
         for (int i = 0; i < p; i++) tensor_acc(C, qct + i * ct1, sct + i * ct1, d);
         relinearize(C, d, rlk, r1);
         rescale(C, r1, out);
@@ -655,9 +733,14 @@ static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64
             poly_add(q0, 2 * N, out, r0, out); /* Add at level 0, both components */
         }
     }
-    for (int i = 1; i <= log_s; i++) {
-        rotate(C, out, (uint64_t)1 << (i - 1), gk + (size_t)(i - 1) * 4 * N, rot);
-        poly_add(q0, 2 * N, rot, out, out);
+    if (order == 2) { /* f2: gk holds the hoisted keys hgk[s-1] */
+        memcpy(r0, out, sizeof(uint64_t) * 2 * N);
+        hoisted_rot_sum(C, 1 << log_s, gk, r0, out);
+    } else {
+        for (int i = 1; i <= log_s; i++) {
+            rotate(C, out, (uint64_t)1 << (i - 1), gk + (size_t)(i - 1) * 4 * N, rot);
+            poly_add(q0, 2 * N, rot, out, out);
+        }
     }
     free(d); free(r1); free(r0); free(rot);
 }

@@ -73,6 +73,9 @@ def lib():
         L.or_match.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p,
                                ctypes.c_int64, _u64p, ctypes.c_int64, _i64p, ctypes.c_int64, _u64p, ctypes.c_int]
         L.or_match.restype = ctypes.c_int
+        L.or_keygen_hoisted.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u64p]
+        L.or_keygen_hoisted.restype = ctypes.c_int
+        L.or_hoisted_rot_sum.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p]
         _lib = L
     return _lib
 
@@ -146,6 +149,23 @@ def keygen(logN, seed, n_rot, zero_error=False):
     return sk, pk, rlk, gk[:n_rot]
 
 
+def keygen_hoisted(logN, seed, s, zero_error=False):
+    """f2: Galois keys for every rotation r = 1..s-1 (hgk[r-1]), same secret as keygen(seed)."""
+    N = 1 << logN
+    hgk = np.zeros((max(s - 1, 1), 2, 2, N), np.uint64)
+    lib().or_keygen_hoisted(logN, seed, s, int(zero_error), _p(hgk, _u64p))
+    return hgk[:max(s - 1, 0)]
+
+
+def hoisted_rot_sum(logN, s, hgk, ct):
+    """f2: sum_{r<s} Rot(ct, r) with one hoisted key switch; ct [2][1][N] level 0."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    out = np.zeros((2, 1, 1 << logN), np.uint64)
+    h = np.ascontiguousarray(hgk if len(hgk) else np.zeros((1, 2, 2, 1 << logN), np.uint64), np.uint64)
+    lib().or_hoisted_rot_sum(logN, s, _p(h, _u64p), _p(ct, _u64p), _p(out, _u64p))
+    return out
+
+
 def encrypt(logN, pk, pt, first_obj, seed):
     """pt int64 [n][N] -> level-1 cts [n][2][2][N] (coefficient domain)."""
     pt = np.ascontiguousarray(pt, np.int64)
@@ -193,6 +213,7 @@ def moddown(logN, n_q, KS):
 
 def match(logN, d, p, order, rlk, gk, db, q, pairs=None, n_threads=1):
     """Algorithm 2 over (query, set) pairs. db [T][p][2][2][N], q [Q][p][2][2][N].
+    order 0 hoisted relin, 1 paper order, 2 f2 hoisted rotation sum (gk = keygen_hoisted keys).
     Returns out [n_pairs][2][1][N] and the pairs array."""
     N = 1 << logN
     db = np.ascontiguousarray(db, np.uint64)

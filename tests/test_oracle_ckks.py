@@ -229,17 +229,20 @@ def _sigma_int(a, g):
     return out
 
 
-@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("order", [0, 1, 2])
 def test_trivial_ciphertext_scan_closed_form(O, order):
     """With c1 = 0 every key switch vanishes, so HE-C^3 reduces to integer arithmetic:
-    hoisted:  C = round(sum_i pt_u,i * pt_s,i / q1) mod q0
+    hoisted:  C = round(sum_i pt_u,i * pt_s,i / q1) mod q0   (orders 0 and 2)
     paper:    C = sum_i round(pt_u,i * pt_s,i / q1) mod q0
-    then      out = sum_{delta < s} sigma_{5^delta}(C) mod q0"""
+    then      out = sum_{delta < s} sigma_{5^delta}(C) mod q0      (the ladder's
+    doubling steps and the f2 hoisted rotation sum both add every rotation delta < s once)"""
     logN, d, p = 6, 16, 2              # N = 64, S = 32, s = 8, B = 4
     N = 1 << logN
     q0, q1, P = O.primes()
     s = d // p
     sk, pk, rlk, gk = O.keygen(logN, 6, O.n_rot_for(d, p))
+    if order == 2:
+        gk = O.keygen_hoisted(logN, 6, s)
     rnd = random.Random(11)
     pu = [[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(p)]
     ps = [[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(p)]
@@ -251,7 +254,7 @@ def test_trivial_ciphertext_scan_closed_form(O, order):
         return (x - _cent(x, m)) // m
 
     prods = [_negacyclic_big(pu[i], ps[i]) for i in range(p)]
-    if order == 0:
+    if order in (0, 2):
         tot = [sum(pr[k] for pr in prods) for k in range(N)]
         C = [rnd_div(v, q1) for v in tot]
     else:
@@ -265,11 +268,57 @@ def test_trivial_ciphertext_scan_closed_form(O, order):
     assert not out[0, 1].any()
 
 
+# ----------------------------------------------------------------------------- f2: hoisted rotation sum
+def test_hoisted_rotation_sum_decrypts_to_window_sums(O):
+    """f2: sum_{r<s} Rot(ct, r) with one hoisted key switch decrypts to the sum of
+    the s left rotations of the slots (SPEC.md:82 rotation semantics), for s = 1, 2, 8."""
+    logN = 6
+    S = 32
+    q0 = O.primes()[0]
+    sk, pk, rlk, gk = O.keygen(logN, 4, 3)
+    z = np.random.default_rng(7).uniform(-1, 1, S)
+    ct = O.encrypt(logN, pk, O.encode(z[None], logN), 0, 1)[0]
+    ct0 = np.ascontiguousarray(ct[:, :1, :])
+    for s in (1, 2, 8):
+        hgk = O.keygen_hoisted(logN, 4, s)
+        out = O.hoisted_rot_sum(logN, s, hgk, ct0)
+        m = O.decrypt(logN, sk, out, 1)[0]
+        back = O.decode_slots(O.centred_i64(m, q0), logN, O.DELTA)
+        want = sum(_rot_left(z, r) for r in range(s))
+        assert np.abs(back - want).max() < 1e-6, s
+    if True:  # s = 1 is the identity (no key switch at all)
+        assert np.array_equal(O.hoisted_rot_sum(logN, 1, O.keygen_hoisted(logN, 4, 1), ct0), ct0)
+
+
+def test_hoisted_keys_are_galois_keys_of_their_rotation(O):
+    """hgk[r-1] satisfies the Galois-key relation of rotation r: with zero-error keys,
+    b + a s = (P mod q0) sigma_{5^r}(s) in q0 and 0 in P -- an independent big-integer check of the
+    key generator (a wrong rotation amount, limb or sign fails it)."""
+    logN = 5
+    N = 1 << logN
+    q0, q1, P = O.primes()
+    sk, pk, rlk, gk = O.keygen(logN, 9, 2)
+    hgk = O.keygen_hoisted(logN, 9, 6, zero_error=True)
+    s_int = [int(v) for v in sk]
+    for r in range(1, 6):
+        g = pow(5, r, 2 * N)
+        ss = _sigma_int(s_int, g)
+        for li, q in ((0, q0), (1, P)):
+            b = [int(v) for v in hgk[r - 1, 0, li]]
+            a = [int(v) for v in hgk[r - 1, 1, li]]
+            asum = _negacyclic_big(a, s_int)
+            lhs = [(b[k] + asum[k]) % q for k in range(N)]
+            rhs = [((P % q0) * ss[k]) % q if li == 0 else 0 for k in range(N)]
+            assert lhs == rhs, (r, li)
+
+
 # ----------------------------------------------------------------------------- end to end
 def _run_scan(O, logN, d, p, tmpl, qv, order=0, key_seed=1, n_threads=4):
     S, s, B = O.layout(logN, d, p)
     n_sets = -(-tmpl.shape[0] // B)
     sk, pk, rlk, gk = O.keygen(logN, key_seed, O.n_rot_for(d, p))
+    if order == 2:
+        gk = O.keygen_hoisted(logN, key_seed, s)
     zdb = O.pack_db(tmpl, logN, d, p, 0, n_sets)
     zq = O.pack_query(qv, logN, d, p)
     db = O.encrypt(logN, pk, O.encode(zdb.reshape(-1, S), logN), 0, 2).reshape(n_sets, p, 2, 2, -1)
@@ -290,6 +339,16 @@ def test_config1_end_to_end(O):
     ref = Q @ T.T
     assert np.abs(sc - ref).max() < 1e-6      # internal guard (north_star contract: 1e-4)
     assert sc.argmax() == ref.argmax() == 17
+
+
+def test_config1_end_to_end_hoisted_rotations(O):
+    """configs[0] through the f2 order (hoisted rotation sum): same scores within 1e-6, top-1 17."""
+    T = I.templates(1)
+    Q, exp = I.queries(1)
+    sc, _ = _run_scan(O, 13, 16, 1, T, Q, order=2)
+    ref = Q @ T.T
+    assert np.abs(sc - ref).max() < 1e-6
+    assert sc.argmax() == 17
 
 
 def test_orders_coincide_for_p1_and_agree_in_value(O):
