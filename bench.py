@@ -72,6 +72,7 @@ def class_modmuls(p, log_s):
         "digits": 6 * BFLY + n,                                    # INTT_q0, INTT_q1, NTT_q1, NTT_P x2, NTT_q0
         "relin": 6 * BFLY + 12 * n + 8 * n,                        # INTT_P, INTT_q1, NTT_q0 x 2 comps; rlk + scalings
         "ladder": (6 * BFLY + 6 * n) * log_s,                      # digit INTT_q0 + NTT_P, 2 x (INTT_P + NTT_q0)
+        "hrot": (6 * BFLY + 4 * n * ((1 << log_s) - 1)) if log_s else 0,  # f2: 6 transforms + 4 products per rotation
         "out_intt": 0 if log_s else 2 * BFLY,
     }
 
@@ -188,6 +189,8 @@ def run_ours(args):
     n_tmpl = I.CONFIGS[CFG]["n"]                     # per rank (weak scaling)
     n_sets = -(-n_tmpl // prm.B)
     sk, pk, evk = B.bm_keygen(prm, 1)                # deterministic: identical keys on every rank
+    if order == 2:                                   # f2 hoisted rotation sum: keys of every rotation
+        B.bm_evk_add_hoisted(prm, 1, evk)
     pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
     T = I.templates(CFG, n_tmpl, rank * n_tmpl)
     d_db = torch.empty((n_sets, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
@@ -327,7 +330,7 @@ def run_ours(args):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (seeded unit-norm Gaussian templates, genuine noisy queries)",
             "config": {"workload": f"BASELINE configs[1]: d=128, {n_tmpl} templates/GPU, {nq} queries, p={p}, "
-                                   f"order={'hoisted' if order == 0 else 'paper'}",
+                                   f"order={['hoisted', 'paper', 'hoisted-rotations (f2, not the paper ladder)'][order]}",
                        "d": D, "p": p, "templates_per_gpu": n_tmpl, "sets_per_gpu": n_sets, "queries": nq,
                        "ring_N": N_RING, "parallelism": f"db-shard{world}",
                        "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (

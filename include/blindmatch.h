@@ -54,8 +54,11 @@ typedef enum {
 } bm_status;
 
 typedef enum {
-    BM_ORDER_HOISTED = 0, /* sum_i tensor_i, then one relin + one rescale (reading R8) */
-    BM_ORDER_PAPER = 1    /* per part Res(Mul(C_u,i, C_s,i)), then Add at level 0 */
+    BM_ORDER_HOISTED = 0,     /* sum_i tensor_i, then one relin + one rescale (reading R8) */
+    BM_ORDER_PAPER = 1,       /* per part Res(Mul(C_u,i, C_s,i)), then Add at level 0 */
+    BM_ORDER_HOISTED_ROT = 2  /* f2, NOT the paper's ladder: BM_ORDER_HOISTED's C,
+                                 then sum_{r<s} Rot(C, r) with ONE hoisted key switch (Halevi-Shoup):
+                                 same decrypted scores, different residues; needs bm_evk_add_hoisted */
 } bm_order;
 
 /* Scheme parameters and the packing layout:
@@ -90,6 +93,10 @@ int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **sk, bm_pk **pk, bm_ev
 void bm_sk_free(bm_sk *);
 void bm_pk_free(bm_pk *);
 void bm_evk_free(bm_evk *);
+/* f2: add to evk the Galois keys of every rotation r = 1..s-1 (same secret: pass keygen's seed;
+ * PRNG object 64 + r), needed by BM_ORDER_HOISTED_ROT; upload with bm_evk_to_device afterwards.
+ * Errors: BM_ERR_INVALID_ARG, BM_ERR_KEY_MISMATCH (evk made for other params). */
+int bm_evk_add_hoisted(const bm_params *prm, uint64_t seed, bm_evk *evk);
 
 /* Canonical (coefficient-domain) exports.  sk: int8[N].  pk: [2][2][N].
  * rlk: [2 digits][2 comps][3 limbs q0,q1,P][N].  gk: [log_s][2][2 limbs q0,P][N]

@@ -22,6 +22,7 @@ N = 8192
 SLOTS = 4096
 ORDER_HOISTED = 0
 ORDER_PAPER = 1
+ORDER_HOISTED_ROT = 2   # f2: hoisted rotation sum, not the paper's ladder
 
 BM_OK = 0
 ERRORS = {
@@ -53,6 +54,7 @@ _pp = ctypes.POINTER(ctypes.c_void_p)
 _SIGS = {
     "bm_params_init": (_i32, [_P, _i32, _i32]),
     "bm_keygen": (_i32, [_P, _u64, _pp, _pp, _pp]),
+    "bm_evk_add_hoisted": (_i32, [_P, _u64, _vp]),
     "bm_sk_free": (None, [_vp]), "bm_pk_free": (None, [_vp]), "bm_evk_free": (None, [_vp]),
     "bm_sk_export": (_i32, [_vp, _vp]), "bm_pk_export": (_i32, [_vp, _vp]),
     "bm_evk_export": (_i32, [_vp, _vp, _vp, ctypes.POINTER(_i32)]),
@@ -154,6 +156,12 @@ def bm_keygen(prm, seed):
     sk, pk, evk = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     _chk(_lib.bm_keygen(ctypes.byref(prm), seed, ctypes.byref(sk), ctypes.byref(pk), ctypes.byref(evk)), "bm_keygen")
     return SecretKey(sk), PublicKey(pk), EvalKey(evk)
+
+
+def bm_evk_add_hoisted(prm, seed, evk):
+    """f2: add the Galois keys of every rotation 1..s-1 (same seed as bm_keygen) to evk."""
+    _chk(_lib.bm_evk_add_hoisted(ctypes.byref(prm), seed, evk.ptr), "bm_evk_add_hoisted")
+    return evk
 
 
 def bm_sk_export(sk):
@@ -300,7 +308,7 @@ def bm_profile_read():
     return ms, la, un
 
 
-PROFILE_CLASSES = ["tensor", "digits", "relin", "unused3", "ladder", "unused5", "out_intt"]
+PROFILE_CLASSES = ["tensor", "digits", "relin", "unused3", "ladder", "hrot", "out_intt"]
 
 
 def bm_decrypt(prm, sk, h_ct):

@@ -40,4 +40,6 @@ struct bm_evk {
     int32_t n_rot;
     std::vector<uint64_t> rlk; // [2][2][3][N]
     std::vector<uint64_t> gk;  // [n_rot][2][2][N]
+    int32_t n_hrot = 0;        // f2 hoisted rotation keys (s - 1 of them, 0 if not generated)
+    std::vector<uint64_t> hgk; // [n_hrot][2][2][N], entry r-1 = rotation r
 };

@@ -427,6 +427,129 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     }
 }
 
+// ================================================================== f2: hoisted rotation sum
+// SURVEY.md sec. 8f, order BM_ORDER_HOISTED_ROT -- NOT the paper's ladder (oracle: hoisted_rot_sum).
+// One CTA per pair computes out = sum_{r<s} Rot(C, r) with ONE key switch (Halevi-Shoup hoisting):
+//   x = INTT_q0(c1) in [0, q0) (non-centred digit, R4), X~P = NTT_P(x); for r = 1..s-1 the
+//   automorphism acts on each NTT-domain digit limb as an index permutation, and
+//   A[c][q0] = sum_r sigma_r(c1) (P^-1 hgk_r[c][q0]),  A[c][P] = sum_r sigma_r(X~P) hgk_r[c][P]
+//   are accumulated exactly in 128 bits (8-byte keys, no Shoup companions; folded every 64 terms);
+//   then one ModDown per component straight to the coefficient-domain output:
+//   out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c,  y^c = centred_P(INTT_P(A[c][P])),
+//   base_0 = sum_{r<s} sigma_r(c0), base_1 = c1.   6 transforms per pair (the ladder: 6 log2 s).
+constexpr size_t HROT_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int s)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *S1 = sm + SMEM_WORDS, *SP = sm + 2 * SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    // scratch (dead after K3): A -> D01 [c][q0 | P], base_0 -> D2[0], P^-1 y^ -> D2[1]
+    uint64_t *Ab = K.D01 + (size_t)pi * 4 * N, *b0s = K.D2 + (size_t)pi * 2 * N, *tsc = b0s + N;
+    const ulonglong2 pinv = K.pinv[0];
+    // ---- digit: c1 staged by NTT index; X~P = NTT_P(INTT_q0(c1)) staged by NTT index
+    stage_by_j(S1, cin.at(pi, 1));
+    uint64_t a[E];
+    load_eval(a, cin.at(pi, 1));
+    inv<0>(a, XB, K.pr[0]);
+    fwd<2>(a, XB, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+    __syncthreads();
+    // ---- the s-1 rotations' key-switch products, 4 coefficients (two 16-byte positions) at a time
+#pragma unroll 1
+    for (int g4 = 0; g4 < E / 4; g4++) {
+        u128 A[4][4]; // [coefficient][c * 2 + limb (q0, P)]
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int v = 0; v < 4; v++) A[u][v] = 0;
+        uint32_t gr = 1;
+#pragma unroll 1
+        for (int r = 1; r < s; r++) {
+            gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
+            const uint64_t *key = hgk + (size_t)(r - 1) * 4 * N;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int e = 4 * g4 + 2 * h, pos = pos_M4(tid, e);
+                const ulonglong2 k0q = ld2(key + 0 * N + pos), k0p = ld2(key + 1 * N + pos);
+                const ulonglong2 k1q = ld2(key + 2 * N + pos), k1p = ld2(key + 3 * N + pos);
+#pragma unroll
+                for (int b = 0; b < 2; b++) {
+                    const int jp = auto_perm(j_M4(tid, e + b), gr);
+                    const uint64_t x0 = S1[pidx(jp)], xP = SP[pidx(jp)];
+                    u128 *Au = A[2 * h + b];
+                    Au[0] += (u128)x0 * (b ? k0q.y : k0q.x);
+                    Au[1] += (u128)xP * (b ? k0p.y : k0p.x);
+                    Au[2] += (u128)x0 * (b ? k1q.y : k1q.x);
+                    Au[3] += (u128)xP * (b ? k1p.y : k1p.x);
+                }
+            }
+            if ((r & 63) == 0) { // 64 products of < 2^60 x 2^60 stay below 2^128
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int v = 0; v < 4; v++) A[u][v] = red128(A[u][v], (v & 1) ? K.pr[2] : K.pr[0]);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int pos = pos_M4(tid, 4 * g4 + 2 * h);
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const PrimeK &Pv = (v & 1) ? K.pr[2] : K.pr[0];
+                st2(Ab + (size_t)v * N + pos, red128(A[2 * h][v], Pv), red128(A[2 * h + 1][v], Pv));
+            }
+        }
+    }
+    // ---- base_0 = sum_{r<s} sigma_r(c0): c0 staged by NTT index (over X~P, no longer needed)
+    __syncthreads();
+    stage_by_j(SP, cin.at(pi, 0));
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int j = j_M4(tid, e);
+        uint64_t acc = SP[pidx(j)];
+        uint32_t gr = 1;
+#pragma unroll 1
+        for (int r = 1; r < s; r++) {
+            gr = (gr * 5u) & (2 * N - 1);
+            acc = csub(acc + SP[pidx(auto_perm(j, gr))], Q0);
+        }
+        b0s[pos_M4(tid, e)] = acc;
+    }
+    // ---- one ModDown per component, straight to coefficient form
+#pragma unroll 1
+    for (int c = 0; c < 2; c++) {
+#pragma unroll
+        for (int e = 0; e < E; e += 2) { // written by this thread above: coherent loads
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c + 1) * N + pos_M4(tid, e));
+            a[e] = v.x;
+            a[e + 1] = v.y;
+        }
+        inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
+#pragma unroll
+        for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+        const uint64_t *base = c ? cin.at(pi, 1) : b0s;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
+            const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c) * N + pos);
+            a[e] = csub(bv.x + av.x, Q0);
+            a[e + 1] = csub(bv.y + av.y, Q0);
+        }
+        inv<0>(a, XB, K.pr[0]);
+        uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int j = j_M1(tid, e);
+            o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
+        }
+    }
+}
+
 // K7: output INTT when there is no ladder (s = 1)
 __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
 {
@@ -642,6 +765,7 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
     set_smem(k_convert);
     set_smem(k_key_ntt);
@@ -694,6 +818,8 @@ struct bm_evk_dev {
     int32_t n_rot;
     ulonglong2 *rlk; // [2][2][3][N]
     ulonglong2 *gk;  // [n_rot][2][2][N]
+    int32_t n_hrot;  // f2 hoisted rotation keys (0: none)
+    uint64_t *hgk;   // [n_hrot][2][2][N], NTT domain, plain residues (no Shoup companion), P^-1 in q0
 };
 
 // keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1)
@@ -762,14 +888,29 @@ int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
     memcpy(d->digest, prm->digest, 32);
     d->n_rot = evk->n_rot;
     d->gk = nullptr;
+    d->n_hrot = 0;
+    d->hgk = nullptr;
     const int lr[3] = {0, 1, 2}, lg[2] = {0, 2};
     // device convention: P^-1 is folded into the Q limbs of the key-switching keys (the ModDown
     // multiplies every Q-limb inner product by P^-1 anyway; exact mod q, saves one product)
     const uint64_t sr[3] = {C->pinv[0].x, C->pinv[1].x, 1}, sg[2] = {C->pinv[0].x, 1};
     rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk, sr);
     if (!rc && evk->n_rot > 0) rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk, sg);
+    if (!rc && evk->n_hrot > 0) { // f2 keys: keep only the residues (the hoisted sum accumulates in 128 bits)
+        ulonglong2 *pairs = nullptr;
+        const int64_t np = 4 * (int64_t)evk->n_hrot;
+        rc = upload_key_polys(C, evk->hgk.data(), np, 2, lg, &pairs, sg);
+        if (!rc && cudaMalloc(&d->hgk, (size_t)np * N * 8) != cudaSuccess) rc = BM_ERR_OOM;
+        if (!rc && cudaMemcpy2D(d->hgk, 8, pairs, 16, 8, (size_t)np * N, cudaMemcpyDeviceToDevice) != cudaSuccess)
+            rc = BM_ERR_CUDA;
+        cudaFree(pairs);
+        if (!rc) d->n_hrot = evk->n_hrot;
+    }
     if (rc) {
         cudaFree(d->rlk);
+        cudaFree(d->gk);
+        cudaFree(d->hgk);
+        cudaGetLastError();
         delete d;
         return rc;
     }
@@ -788,6 +929,7 @@ void bm_evk_dev_free(bm_evk_dev *d)
     if (!d) return;
     cudaFree(d->rlk);
     cudaFree(d->gk);
+    cudaFree(d->hgk);
     delete d;
 }
 
@@ -925,10 +1067,12 @@ int bm_profile_read(double *ms, int64_t *launches, int64_t *units)
 int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
              int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream)
 {
-    if (!prm || !evk || n_sets < 0 || nq < 0 || (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER))
+    if (!prm || !evk || n_sets < 0 || nq < 0 ||
+        (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT))
         return BM_ERR_INVALID_ARG;
     if (memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
-    if (evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    if (order != BM_ORDER_HOISTED_ROT && evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    if (order == BM_ORDER_HOISTED_ROT && evk->n_hrot < prm->s - 1) return BM_ERR_MISSING_ROTATION_KEY;
     const int64_t total = n_sets * (int64_t)nq;
     if (total == 0) return BM_OK;
     if (!d_db || !d_q || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
@@ -995,9 +1139,10 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
         const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS));
-        const int n_rounds = order == BM_ORDER_HOISTED ? 1 : prm->p;
+        const bool per_part = order == BM_ORDER_PAPER;
+        const int n_rounds = per_part ? prm->p : 1;
         for (int r = 0; r < n_rounds && !rc; r++) {
-            const int lo = order == BM_ORDER_HOISTED ? 0 : r, hi = order == BM_ORDER_HOISTED ? prm->p : r + 1;
+            const int lo = per_part ? r : 0, hi = per_part ? r + 1 : prm->p;
             beg(0, 2 * np);
             k_tensor<<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             end();
@@ -1009,7 +1154,12 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
             end();
             rc = launch_check();
         }
-        if (log_s > 0 && !rc) {
+        if (log_s > 0 && !rc && order == BM_ORDER_HOISTED_ROT) {
+            beg(5, 6 * np);
+            k_hrot<<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufC, evk->hgk, prm->s);
+            end();
+            rc = launch_check();
+        } else if (log_s > 0 && !rc) {
             beg(4, 6 * log_s * np);
             k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
             end();

@@ -240,6 +240,54 @@ int bm_params_init(bm_params *o, int32_t d, int32_t p)
     return BM_OK;
 }
 
+// Galois key of a left rotation by r (g = 5^r mod 2N) over {q0, P}, PRNG object obj:
+// (-a s + e + (P mod q0) sigma_g(s) [q0], a) and (-a s + e [P], a); out [2 comps][2 limbs][N]
+static void galois_key(uint64_t seed, const std::vector<int64_t> &sv, uint64_t r, uint64_t obj, uint64_t *out)
+{
+    const uint64_t Qs[3] = {Q0, Q1, QP};
+    const uint64_t g = powmod_h(5, r, 2 * N);
+    std::vector<int64_t> ev(N);
+    std::vector<uint64_t> s(N), e(N), a(N), t(N), sg(N);
+    sample_small(seed, P_GK_E, obj, 1, ev.data());
+    for (int li = 0; li < 2; li++) {
+        int l = li ? 2 : 0;
+        uint64_t q = Qs[l];
+        for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
+        sample_uniform(seed, P_GK_A, obj, (uint32_t)l, q, a.data());
+        poly_mul_h(a.data(), s.data(), t.data(), l);
+        uint64_t *b = out + (size_t)(0 * 2 + li) * N;
+        uint64_t *aa = out + (size_t)(1 * 2 + li) * N;
+        for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
+        if (l == 0) {
+            // sigma_g(s): coefficient k -> k g mod 2N, negated past N
+            std::fill(sg.begin(), sg.end(), 0);
+            for (int k = 0; k < N; k++) {
+                uint64_t x = (uint64_t)k * g % (2 * N);
+                if (x < (uint64_t)N) sg[x] = s[k];
+                else sg[x - N] = (q - s[k]) % q;
+            }
+            uint64_t pm = QP % q;
+            for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(sg[k], pm, q)) % q;
+        }
+    }
+}
+
+// f2: Galois keys of every rotation r = 1..s-1 for the hoisted rotation sum,
+// PRNG object HROT_OBJ + r (disjoint from the ladder keys' objects i < 13)
+constexpr uint64_t HROT_OBJ = 64;
+int bm_evk_add_hoisted(const bm_params *prm, uint64_t seed, bm_evk *evk)
+{
+    if (!prm || !evk) return BM_ERR_INVALID_ARG;
+    if (memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    std::vector<int64_t> sv(N);
+    sample_small(seed, P_SK, 0, 0, sv.data());
+    const int n = prm->s - 1;
+    evk->n_hrot = n;
+    evk->hgk.assign((size_t)n * 4 * N, 0);
+    for (int r = 1; r <= n; r++) galois_key(seed, sv, (uint64_t)r, HROT_OBJ + r, &evk->hgk[(size_t)(r - 1) * 4 * N]);
+    return BM_OK;
+}
+
 int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **skp, bm_pk **pkp, bm_evk **evkp)
 {
     if (!prm) return BM_ERR_INVALID_ARG;
@@ -290,34 +338,10 @@ int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **skp, bm_pk **pkp, bm_
         }
     }
 
-    // gk_i (rotation r = 2^i) over {q0, P}: (-a s + e + (P mod q0) sigma_g(s) [q0], a), g = 5^r mod 2N
+    // gk_i (rotation r = 2^i), PRNG object i
     evk->n_rot = prm->log_s;
     evk->gk.assign((size_t)evk->n_rot * 4 * N, 0);
-    for (int i = 0; i < evk->n_rot; i++) {
-        uint64_t g = powmod_h(5, (uint64_t)1 << i, 2 * N);
-        sample_small(seed, P_GK_E, (uint64_t)i, 1, ev.data());
-        for (int li = 0; li < 2; li++) {
-            int l = li ? 2 : 0;
-            uint64_t q = Qs[l];
-            for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
-            sample_uniform(seed, P_GK_A, (uint64_t)i, (uint32_t)l, q, a.data());
-            poly_mul_h(a.data(), s.data(), t.data(), l);
-            uint64_t *b = &evk->gk[((size_t)(i * 2 + 0) * 2 + li) * N];
-            uint64_t *aa = &evk->gk[((size_t)(i * 2 + 1) * 2 + li) * N];
-            for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
-            if (l == 0) {
-                // sigma_g(s): coefficient k -> k g mod 2N, negated past N
-                std::fill(sg.begin(), sg.end(), 0);
-                for (int k = 0; k < N; k++) {
-                    uint64_t x = (uint64_t)k * g % (2 * N);
-                    if (x < (uint64_t)N) sg[x] = s[k];
-                    else sg[x - N] = (q - s[k]) % q;
-                }
-                uint64_t pm = QP % q;
-                for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(sg[k], pm, q)) % q;
-            }
-        }
-    }
+    for (int i = 0; i < evk->n_rot; i++) galois_key(seed, sv, (uint64_t)1 << i, (uint64_t)i, &evk->gk[(size_t)i * 4 * N]);
     if (skp) *skp = sk; else delete sk;
     if (pkp) *pkp = pk; else delete pk;
     if (evkp) *evkp = evk; else delete evk;

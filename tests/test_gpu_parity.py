@@ -28,7 +28,7 @@ def env():
 class Setup:
     """Keys + oracle-encoded plaintexts, encrypted by BOTH sides with the same seeds."""
 
-    def __init__(self, env, O, d, p, T, Q, key_seed=1, db_seed=2, q_seed=3, n_rot=None):
+    def __init__(self, env, O, d, p, T, Q, key_seed=1, db_seed=2, q_seed=3, n_rot=None, hoisted=False):
         torch, B = env
         self.torch, self.B, self.O = torch, B, O
         self.d, self.p = d, p
@@ -38,6 +38,9 @@ class Setup:
         self.nq = Q.shape[0]
         self.sk, self.pk, self.evk = B.bm_keygen(self.prm, key_seed)
         self.osk, self.opk, self.orlk, self.ogk = O.keygen(LOGN, key_seed, O.n_rot_for(d, p))
+        if hoisted:   # f2: Galois keys of every rotation 1..s-1 on both sides
+            B.bm_evk_add_hoisted(self.prm, key_seed, self.evk)
+            self.ohgk = O.keygen_hoisted(LOGN, key_seed, s)
         self.pk_dev = B.bm_pk_to_device(self.prm, self.pk)
         self.evk_dev = B.bm_evk_to_device(self.prm, self.evk)
         self.db_pt = O.encode(O.pack_db(T, LOGN, d, p, 0, self.n_sets).reshape(-1, S), LOGN)
@@ -79,7 +82,8 @@ class Setup:
         qi = {j: k for k, j in enumerate(qs)}
         ti = {t: k for k, t in enumerate(ts)}
         local = np.array([(qi[j], ti[t]) for j, t in pairs], np.int64).reshape(-1, 2)
-        out, _ = self.O.match(LOGN, self.d, self.p, order, self.orlk, self.ogk, self.oracle_db(ts), self.oracle_q(qs),
+        gk = self.ohgk if order == 2 else self.ogk
+        out, _ = self.O.match(LOGN, self.d, self.p, order, self.orlk, gk, self.oracle_db(ts), self.oracle_q(qs),
                               pairs=local, n_threads=NTH)
         return out.reshape(-1, 2, 8192)
 
@@ -261,3 +265,38 @@ def test_config2_full_size_bench_launch(env, O):
     cos = Q[qs] @ T.T
     assert np.abs(sc - cos).max() < 1e-6
     assert np.array_equal(sc.argmax(1), expq[qs])
+
+
+# ----------------------------------------------------------------------------- f2: hoisted rotation sum
+@pytest.mark.parametrize("d,p,nt", [(16, 1, 256), (128, 8, 6144), (128, 1, 700), (4096, 8, 20)])
+def test_hoisted_rotation_order_parity(env, O, d, p, nt):
+    """BM_ORDER_HOISTED_ROT (f2; not the paper's ladder): bit-exact vs the oracle's
+    hoisted_rot_sum on sampled pairs, scores vs float64 cosine, and the same top-1 as the ladder.
+    s = 16, 16, 128 and 512 (the 128-bit sums are folded every 64 rotations)."""
+    torch, B = env
+    T = I.templates(1) if d == 16 else (I.templates(2, nt) if d == 128 else I.random_unit(nt, d, 3))
+    Q = I.queries(1)[0] if d == 16 else (I.queries(2, 3)[0] if d == 128 else I.random_unit(1, d, 4))
+    st = Setup(env, O, d, p, T, Q, hoisted=True)
+    got = st.gpu_match(2)
+    pairs = [(0, st.n_sets - 1)] + ([(Q.shape[0] - 1, 0)] if st.n_sets > 1 or Q.shape[0] > 1 else [])
+    ref = st.oracle_pairs(pairs, 2)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k]), (j, t)
+    sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(Q.shape[0], -1)[:, :T.shape[0]]
+    cos = Q @ T.T
+    assert np.abs(sc - cos).max() < 1e-6
+    assert np.array_equal(sc.argmax(1), cos.argmax(1))
+    if d == 128 and p == 8:   # residues differ from the ladder's (own parity), decrypted values agree
+        lad = st.gpu_match(0)
+        assert not np.array_equal(lad[0, 0], got[0, 0])
+
+
+def test_hoisted_rotation_needs_its_keys(env, O):
+    torch, B = env
+    prm = B.bm_params_init(128, 8)
+    sk, pk, evk = B.bm_keygen(prm, 9)
+    evk_dev = B.bm_evk_to_device(prm, evk)
+    dummy = torch.zeros(8, dtype=torch.int64, device="cuda")
+    with pytest.raises(B.BMError) as e:
+        B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=2)
+    assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
