@@ -442,83 +442,89 @@ constexpr size_t HROT_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int s)
 {
     extern __shared__ uint64_t sm[];
-    uint64_t *XB = sm, *S1 = sm + SMEM_WORDS, *SP = sm + 2 * SMEM_WORDS;
+    // XB: transform exchanges; SX: (c1, X~P) pairs by NTT index (one 16-byte gather per rotation)
+    uint64_t *XB = sm;
+    ulonglong2 *SX = reinterpret_cast<ulonglong2 *>(sm + SMEM_WORDS);
+    uint64_t *SP = sm + SMEM_WORDS; // reused for c0 after the rotation products
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
     // scratch (dead after K3): A -> D01 [c][q0 | P], base_0 -> D2[0], P^-1 y^ -> D2[1]
     uint64_t *Ab = K.D01 + (size_t)pi * 4 * N, *b0s = K.D2 + (size_t)pi * 2 * N, *tsc = b0s + N;
     const ulonglong2 pinv = K.pinv[0];
-    // ---- digit: c1 staged by NTT index; X~P = NTT_P(INTT_q0(c1)) staged by NTT index
-    stage_by_j(S1, cin.at(pi, 1));
+    // ---- digit: X~P = NTT_P(INTT_q0(c1)); (c1, X~P) staged by NTT index
     uint64_t a[E];
     load_eval(a, cin.at(pi, 1));
+#pragma unroll
+    for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
     inv<0>(a, XB, K.pr[0]);
     fwd<2>(a, XB, K.pr[2]);
 #pragma unroll
-    for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+    for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
     __syncthreads();
-    // ---- the s-1 rotations' key-switch products, 4 coefficients (two 16-byte positions) at a time
+    // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
+    //      time, the next rotation's keys loaded while this one's are used
 #pragma unroll 1
-    for (int g4 = 0; g4 < E / 4; g4++) {
-        u128 A[4][4]; // [coefficient][c * 2 + limb (q0, P)]
+    for (int g2 = 0; g2 < E / 2; g2++) {
+        const int e0 = 2 * g2, pos = pos_M4(tid, e0);
+        const int j0 = j_M4(tid, e0), j1 = j_M4(tid, e0 + 1);
+        u128 A[2][4]; // [coefficient][c * 2 + limb (q0, P)]
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+        for (int u = 0; u < 2; u++)
 #pragma unroll
             for (int v = 0; v < 4; v++) A[u][v] = 0;
+        ulonglong2 kc[4], kn[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + (size_t)v * N + pos);
         uint32_t gr = 1;
 #pragma unroll 1
         for (int r = 1; r < s; r++) {
             gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
-            const uint64_t *key = hgk + (size_t)(r - 1) * 4 * N;
+            if (r + 1 < s) {
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int e = 4 * g4 + 2 * h, pos = pos_M4(tid, e);
-                const ulonglong2 k0q = ld2(key + 0 * N + pos), k0p = ld2(key + 1 * N + pos);
-                const ulonglong2 k1q = ld2(key + 2 * N + pos), k1p = ld2(key + 3 * N + pos);
+                for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
+            }
+            const ulonglong2 x0 = SX[pidx(auto_perm(j0, gr))], x1 = SX[pidx(auto_perm(j1, gr))];
 #pragma unroll
-                for (int b = 0; b < 2; b++) {
-                    const int jp = auto_perm(j_M4(tid, e + b), gr);
-                    const uint64_t x0 = S1[pidx(jp)], xP = SP[pidx(jp)];
-                    u128 *Au = A[2 * h + b];
-                    Au[0] += (u128)x0 * (b ? k0q.y : k0q.x);
-                    Au[1] += (u128)xP * (b ? k0p.y : k0p.x);
-                    Au[2] += (u128)x0 * (b ? k1q.y : k1q.x);
-                    Au[3] += (u128)xP * (b ? k1p.y : k1p.x);
-                }
+            for (int c = 0; c < 2; c++) {
+                A[0][2 * c] += (u128)x0.x * kc[2 * c].x;
+                A[1][2 * c] += (u128)x1.x * kc[2 * c].y;
+                A[0][2 * c + 1] += (u128)x0.y * kc[2 * c + 1].x;
+                A[1][2 * c + 1] += (u128)x1.y * kc[2 * c + 1].y;
             }
             if ((r & 63) == 0) { // 64 products of < 2^60 x 2^60 stay below 2^128
 #pragma unroll
-                for (int u = 0; u < 4; u++)
+                for (int u = 0; u < 2; u++)
 #pragma unroll
                     for (int v = 0; v < 4; v++) A[u][v] = red128(A[u][v], (v & 1) ? K.pr[2] : K.pr[0]);
             }
+#pragma unroll
+            for (int v = 0; v < 4; v++) kc[v] = kn[v];
         }
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int pos = pos_M4(tid, 4 * g4 + 2 * h);
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-                const PrimeK &Pv = (v & 1) ? K.pr[2] : K.pr[0];
-                st2(Ab + (size_t)v * N + pos, red128(A[2 * h][v], Pv), red128(A[2 * h + 1][v], Pv));
-            }
+        for (int v = 0; v < 4; v++) {
+            const PrimeK &Pv = (v & 1) ? K.pr[2] : K.pr[0];
+            st2(Ab + (size_t)v * N + pos, red128(A[0][v], Pv), red128(A[1][v], Pv));
         }
     }
-    // ---- base_0 = sum_{r<s} sigma_r(c0): c0 staged by NTT index (over X~P, no longer needed)
+    // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
+    //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
     __syncthreads();
     stage_by_j(SP, cin.at(pi, 0));
+#pragma unroll 1
+    for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int j = j_M4(tid, e);
+            a[e] = csub(SP[pidx(j)] + SP[pidx(auto_perm(j, g))], Q0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+    }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < E; e++) {
-        const int j = j_M4(tid, e);
-        uint64_t acc = SP[pidx(j)];
-        uint32_t gr = 1;
-#pragma unroll 1
-        for (int r = 1; r < s; r++) {
-            gr = (gr * 5u) & (2 * N - 1);
-            acc = csub(acc + SP[pidx(auto_perm(j, gr))], Q0);
-        }
-        b0s[pos_M4(tid, e)] = acc;
-    }
+    for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
     // ---- one ModDown per component, straight to coefficient form
 #pragma unroll 1
     for (int c = 0; c < 2; c++) {
