@@ -298,7 +298,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         ws2 = torch.empty(B.bm_match_host_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
         B.bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, ws2, order)
-        k2 = max(1, min(3, args.steps))
+        k2 = max(1, args.steps)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()

@@ -120,7 +120,7 @@ class _Handle:
         self.ptr = ptr
 
     def __del__(self):
-        if self.ptr and self._free is not None:
+        if self.ptr and self._free is not None and _lib is not None:   # not at interpreter exit
             getattr(_lib, self._free)(self.ptr)
             self.ptr = None
 

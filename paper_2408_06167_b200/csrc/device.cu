@@ -1242,7 +1242,21 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
     if (cudaStreamCreateWithFlags(&sc[1], cudaStreamNonBlocking) != cudaSuccess) return BM_ERR_CUDA;
     cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
-    const int ngroups = (int)((nq + gq - 1) / gq);
+    // half-size first and last groups: the pipeline's unoverlapped head (first upload) and tail
+    // (last download) shrink; the middle groups are gq queries
+    std::vector<int64_t> g0, gn;
+    {
+        const int64_t h = nq >= 4 ? (gq + 1) / 2 : nq;
+        int64_t q = 0;
+        g0.push_back(0), gn.push_back(h), q = h;
+        const int64_t tail = nq - q > h ? h : 0;
+        while (q < nq - tail) {
+            const int64_t c = nq - tail - q < gq ? nq - tail - q : gq;
+            g0.push_back(q), gn.push_back(c), q += c;
+        }
+        if (tail) g0.push_back(q), gn.push_back(tail);
+    }
+    const int ngroups = (int)g0.size();
     std::vector<cudaEvent_t> ev_up(ngroups), ev_done(ngroups), ev_down(ngroups);
     for (int g = 0; g < ngroups; g++) {
         cudaEventCreateWithFlags(&ev_up[g], cudaEventDisableTiming);
@@ -1258,7 +1272,7 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
     for (int g = 0; g < ngroups && !rc; g++) {
         const int slot = g % HOST_SLOTS;
         cudaStream_t cs = sc[g & 1];
-        const int64_t q0 = g * gq, nqg = nq - q0 < gq ? nq - q0 : gq;
+        const int64_t q0 = g0[g], nqg = gn[g];
         // the query slot is free once the scan of group g - HOST_SLOTS has consumed it
         if (g >= HOST_SLOTS) cudaStreamWaitEvent(su, ev_done[g - HOST_SLOTS], 0);
         if (cudaMemcpyAsync(dq[slot], h_q + q0 * qrow, nqg * qrow * 8, cudaMemcpyHostToDevice, su) != cudaSuccess)
