@@ -88,6 +88,18 @@ BM_D void cp_async16(void *smem, const void *gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
 }
 BM_D uint64_t red128(u128 v, const PrimeK &P) { return reduce128((uint64_t)(v >> 64), (uint64_t)v, P.q, P.r64, P.one_p); }
+// x mod q for any x < 2^64, canonical (q1: fold 2^40 = c1 once so that reduce_bnd's x < 2^62 holds)
+template <int PI> BM_D uint64_t reduce_any(uint64_t x)
+{
+    if (PI == 1) x = (x & ((1ull << 40) - 1)) + (x >> 40) * ((1ull << 40) - Q1); // < 2^40 + 2^24 c1 < 2^43
+    return reduce_bnd<PI>(x);
+}
+// v mod q for a 128-bit v with the prime-specialised lazy Shoup product: hi (2^64 mod q) + lo
+template <int PI> BM_D uint64_t red128s(u128 v, ulonglong2 r64)
+{
+    const uint64_t t = shoup4<PI>((uint64_t)(v >> 64), r64) + reduce_any<PI>((uint64_t)v); // < 5 q
+    return reduce_bnd<PI>(t);
+}
 
 // grid: ((l * nqt + qt) * (N / CS) + slice) * nst + st  (set tiles fastest: the CTAs that share a
 // query slice run together and the query data streams from HBM once)
@@ -170,9 +182,9 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
-                    a0[u][v] = red128(a0[u][v], P);
-                    a1[u][v] = red128(a1[u][v], P);
-                    a2[u][v] = red128(a2[u][v], P);
+                    a0[u][v] = l ? red128s<1>(a0[u][v], P.r64) : red128s<0>(a0[u][v], P.r64);
+                    a1[u][v] = l ? red128s<1>(a1[u][v], P.r64) : red128s<0>(a1[u][v], P.r64);
+                    a2[u][v] = l ? red128s<1>(a2[u][v], P.r64) : red128s<0>(a2[u][v], P.r64);
                 }
         }
         __syncthreads(); // before the next round overwrites the stage
@@ -186,7 +198,9 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
             if (a >= K.cq || bb >= K.ct) continue;
             const int64_t pi = a * K.ct + bb;
             const int j = c0 + c;
-            const uint64_t d0 = red128(a0[u][v], P), d2 = red128(a2[u][v], P), kk = red128(a1[u][v], P);
+            const uint64_t d0 = l ? red128s<1>(a0[u][v], P.r64) : red128s<0>(a0[u][v], P.r64);
+            const uint64_t d2 = l ? red128s<1>(a2[u][v], P.r64) : red128s<0>(a2[u][v], P.r64);
+            const uint64_t kk = l ? red128s<1>(a1[u][v], P.r64) : red128s<0>(a1[u][v], P.r64);
             K.D01[((size_t)pi * 4 + 0 + l) * N + j] = d0;
             K.D01[((size_t)pi * 4 + 2 + l) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
             K.D2[((size_t)pi * 2 + l) * N + j] = d2;
@@ -495,15 +509,16 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
 #pragma unroll
                 for (int u = 0; u < 2; u++)
 #pragma unroll
-                    for (int v = 0; v < 4; v++) A[u][v] = red128(A[u][v], (v & 1) ? K.pr[2] : K.pr[0]);
+                    for (int v = 0; v < 4; v++)
+                        A[u][v] = (v & 1) ? red128s<2>(A[u][v], K.pr[2].r64) : red128s<0>(A[u][v], K.pr[0].r64);
             }
 #pragma unroll
             for (int v = 0; v < 4; v++) kc[v] = kn[v];
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const PrimeK &Pv = (v & 1) ? K.pr[2] : K.pr[0];
-            st2(Ab + (size_t)v * N + pos, red128(A[0][v], Pv), red128(A[1][v], Pv));
+            if (v & 1) st2(Ab + (size_t)v * N + pos, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
+            else st2(Ab + (size_t)v * N + pos, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
         }
     }
     // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
