@@ -101,30 +101,54 @@ template <int PI> BM_D uint64_t red128s(u128 v, ulonglong2 r64)
     return reduce_bnd<PI>(t);
 }
 
-// grid: ((l * nqt + qt) * (N / CS) + slice) * nst + st  (set tiles fastest: the CTAs that share a
-// query slice run together and the query data streams from HBM once)
-__global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
+// q1 limb on the FP64 pipe, exactly: for 0 <= a, b < 2^42 (integers held in doubles),
+// r = a b - floor(a b / q1) q1 up to +-q1: hi = fl(a b) and lo = a b - hi (one FMA, exact), the
+// quotient from fl(hi / q1) by a round-down add of 1.5 2^52, r = (hi - qt q1) + lo (the FMA's
+// exact result is an integer below 2^43, so nothing rounds).  |r| < 3 q1.  7 FP64 instructions,
+// which run on their own pipe: the q1-limb CTAs of k_tensor share each SM with q0-limb CTAs whose
+// 128-bit integer products load the FMA pipe.
+constexpr double MAGIC52 = 6755399441055744.0; // 1.5 2^52: x + M has ulp 1 for |x| < 2^51
+BM_D double f64_floor(double x) { return __dadd_rd(x, MAGIC52) - MAGIC52; }
+BM_D double mulmod_q1_f64(double a, double b)
 {
-    extern __shared__ uint64_t sm[];
-    uint64_t *Qs = sm, *Ss = sm + TQB * PCH * 2 * CS; // [tile row][part][comp][CS]
+    constexpr double q = (double)Q1, qinv = 1.0 / (double)Q1;
+    const double hi = a * b;
+    const double lo = __fma_rn(a, b, -hi);
+    const double qt = f64_floor(hi * qinv);
+    return __fma_rn(-qt, q, hi) + lo;
+}
+// exact u64 (< 2^52) <-> double through the 2^52 exponent pattern (one LOP3 + one DADD)
+BM_D double u2d(uint64_t x) { return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0; }
+// x mod q1 for an integer-valued double |x| < 2^51, as a canonical u64
+BM_D uint64_t f64_mod_q1(double x)
+{
+    constexpr double q = (double)Q1, qinv = 1.0 / (double)Q1;
+    double r = __fma_rn(-f64_floor(x * qinv), q, x); // in (-q1, 2 q1)
+    r = r < 0 ? r + q : r;
+    r = r >= q ? r - q : r;
+    return (uint64_t)__double_as_longlong(r + 4503599627370496.0) & ((1ull << 52) - 1);
+}
+
+// grid: ((qt * (N / CS) + slice) * nst + st) * 2 + l  (limbs alternate, so each SM holds one
+// q0-limb CTA on the integer pipe and one q1-limb CTA on the FP64 pipe; set tiles next: the CTAs
+// that share a query slice run together and the query data streams from HBM once)
+template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st, int part_lo,
+                                       int part_hi)
+{
     const int tid = threadIdx.x;
-    const int nst = (int)((K.ct + TSB - 1) / TSB), nqt = (K.cq + TQB - 1) / TQB;
-    int64_t b = blockIdx.x;
-    const int st = (int)(b % nst);
-    b /= nst;
-    const int sl = (int)(b % (N / CS));
-    b /= (N / CS);
-    const int qt = (int)(b % nqt);
-    const int l = (int)(b / nqt);
     const int c0 = sl * CS;
-    const PrimeK P = l ? K.pr[1] : K.pr[0];
+    const PrimeK &P = K.pr[L];
     // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
     const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
-    u128 a0[2][2], a1[2][2], a2[2][2];
+    u128 a0[2][2], a1[2][2], a2[2][2];     // q0: 128-bit integer sums
+    double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
 #pragma unroll
     for (int u = 0; u < 2; u++)
 #pragma unroll
-        for (int v = 0; v < 2; v++) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+        for (int v = 0; v < 2; v++) {
+            if (L == 0) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+            else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
+        }
 #pragma unroll 1
     for (int i0 = part_lo; i0 < part_hi; i0 += PCH) {
         const int pc = part_hi - i0 < PCH ? part_hi - i0 : PCH; // a power of two (p is)
@@ -148,7 +172,7 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
                 src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 4 * N;
                 dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
             }
-            cp_async16(dst + 2 * ch, src + (size_t)(2 * comp + l) * N + c0 + 2 * ch);
+            cp_async16(dst + 2 * ch, src + (size_t)(2 * comp + L) * N + c0 + 2 * ch);
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
@@ -168,23 +192,46 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
                 y0[v] = r[0];
                 y1[v] = r[CS];
             }
+            if (L == 0) {
 #pragma unroll
-            for (int u = 0; u < 2; u++)
+                for (int u = 0; u < 2; u++)
 #pragma unroll
-                for (int v = 0; v < 2; v++) {
-                    a0[u][v] += (u128)x0[u] * y0[v];
-                    a2[u][v] += (u128)x1[u] * y1[v];
-                    a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
-                }
+                    for (int v = 0; v < 2; v++) {
+                        a0[u][v] += (u128)x0[u] * y0[v];
+                        a2[u][v] += (u128)x1[u] * y1[v];
+                        a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
+                    }
+            } else {
+                double dx0[2], dx1[2], dxs[2], dy0[2], dy1[2], dys[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++) dx0[u] = u2d(x0[u]), dx1[u] = u2d(x1[u]), dxs[u] = dx0[u] + dx1[u];
+#pragma unroll
+                for (int v = 0; v < 2; v++) dy0[v] = u2d(y0[v]), dy1[v] = u2d(y1[v]), dys[v] = dy0[v] + dy1[v];
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+#pragma unroll
+                    for (int v = 0; v < 2; v++) {
+                        f0[u][v] += mulmod_q1_f64(dx0[u], dy0[v]);
+                        f2[u][v] += mulmod_q1_f64(dx1[u], dy1[v]);
+                        f1[u][v] += mulmod_q1_f64(dxs[u], dys[v]); // operands < 2 q1 < 2^41
+                    }
+            }
         }
-        if (((i0 + pc - part_lo) & 511) == 0 && i0 + pc < part_hi) { // (2q)^2 < 2^118: fold every 512 parts
+        // folds: (2q)^2 < 2^118 in 128 bits (q0) / 3 q1 per part below 2^51 (q1): every 512 parts
+        if (((i0 + pc - part_lo) & 511) == 0 && i0 + pc < part_hi) {
 #pragma unroll
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
-                    a0[u][v] = l ? red128s<1>(a0[u][v], P.r64) : red128s<0>(a0[u][v], P.r64);
-                    a1[u][v] = l ? red128s<1>(a1[u][v], P.r64) : red128s<0>(a1[u][v], P.r64);
-                    a2[u][v] = l ? red128s<1>(a2[u][v], P.r64) : red128s<0>(a2[u][v], P.r64);
+                    if (L == 0) {
+                        a0[u][v] = red128s<0>(a0[u][v], P.r64);
+                        a1[u][v] = red128s<0>(a1[u][v], P.r64);
+                        a2[u][v] = red128s<0>(a2[u][v], P.r64);
+                    } else {
+                        f0[u][v] = (double)f64_mod_q1(f0[u][v]);
+                        f1[u][v] = (double)f64_mod_q1(f1[u][v]);
+                        f2[u][v] = (double)f64_mod_q1(f2[u][v]);
+                    }
                 }
         }
         __syncthreads(); // before the next round overwrites the stage
@@ -198,13 +245,36 @@ __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int par
             if (a >= K.cq || bb >= K.ct) continue;
             const int64_t pi = a * K.ct + bb;
             const int j = c0 + c;
-            const uint64_t d0 = l ? red128s<1>(a0[u][v], P.r64) : red128s<0>(a0[u][v], P.r64);
-            const uint64_t d2 = l ? red128s<1>(a2[u][v], P.r64) : red128s<0>(a2[u][v], P.r64);
-            const uint64_t kk = l ? red128s<1>(a1[u][v], P.r64) : red128s<0>(a1[u][v], P.r64);
-            K.D01[((size_t)pi * 4 + 0 + l) * N + j] = d0;
-            K.D01[((size_t)pi * 4 + 2 + l) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
-            K.D2[((size_t)pi * 2 + l) * N + j] = d2;
+            uint64_t d0, d2, kk;
+            if (L == 0) {
+                d0 = red128s<0>(a0[u][v], P.r64);
+                d2 = red128s<0>(a2[u][v], P.r64);
+                kk = red128s<0>(a1[u][v], P.r64);
+            } else {
+                d0 = f64_mod_q1(f0[u][v]);
+                d2 = f64_mod_q1(f2[u][v]);
+                kk = f64_mod_q1(f1[u][v]);
+            }
+            K.D01[((size_t)pi * 4 + 0 + L) * N + j] = d0;
+            K.D01[((size_t)pi * 4 + 2 + L) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
+            K.D2[((size_t)pi * 2 + L) * N + j] = d2;
         }
+}
+
+__global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *Qs = sm, *Ss = sm + TQB * PCH * 2 * CS; // [tile row][part][comp][CS]
+    const int nst = (int)((K.ct + TSB - 1) / TSB);
+    int64_t b = blockIdx.x;
+    const int l = (int)(b & 1);
+    b >>= 1;
+    const int st = (int)(b % nst);
+    b /= nst;
+    const int sl = (int)(b % (N / CS));
+    const int qt = (int)(b / (N / CS));
+    if (l == 0) tensor_tile<0>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
+    else tensor_tile<1>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
 }
 
 // ================================================================== prime-specialised pointwise helpers
