@@ -120,6 +120,9 @@ struct PrimeK {
     ulonglong2 ninv_w1;        // N^-1 * inv[1]  (folded into the last inverse stage)
     ulonglong2 r64;            // 2^64 mod q
     uint64_t one_p;            // floor(2^64 / q)
+    // q1 only (ntt3f.cuh, the FP64-pipe transforms): (w, fl(w / q1)) as double bit patterns
+    const ulonglong2 *fwdf, *invf;
+    ulonglong2 ninvf, ninv_w1f;
 };
 
 #endif // __CUDACC__

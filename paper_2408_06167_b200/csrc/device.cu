@@ -21,6 +21,7 @@
 #include "bm_common.cuh"
 #include "bm_host.h"
 #include "ntt3.cuh"
+#include "ntt3f.cuh"
 using namespace bm::v3;
 
 using namespace bm;
@@ -309,9 +310,9 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
             xs[tid + T * e] = a[e];
             a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
         }
-        fwd<1>(a, sm, K.pr[1]);
+        fwd_q1f(a, sm, K.pr[1].fwdf); // the FP64 pipe (ntt3f.cuh)
     } else {
-        inv<1>(a, sm, K.pr[1]);
+        inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // the FP64 pipe
 #pragma unroll
         for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
         fwd<0, false>(a, sm, K.pr[0]); // lazy [0, 2 q0): only ever a Shoup-product operand
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         a[e] = reduce_bnd<1>(dd.x + ka);
         a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
-    inv<1>(a, sm, K.pr[1]); // U, canonical
+    inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
     // ---- rescale in coefficient form
     const ulonglong2 pinv0 = K.pinv[0];
     // y^ = y - [y > P/2] P, so P^-1 y^ = P^-1 y - [y > P/2] in every q limb (no centring reduction)
@@ -779,8 +780,9 @@ namespace {
 
 struct DevCtx {
     int dev = -1;
-    ulonglong2 *tw = nullptr; // [3][2][N]
-    PrimeK pr[3];
+    ulonglong2 *tw = nullptr;  // [3][2][N]
+    ulonglong2 *twf = nullptr; // q1 [2][N], FP64 form
+    PrimeK pr[3] = {};
     ulonglong2 pinv[2], q1inv;
     uint64_t pmod[2];
 };
@@ -831,6 +833,31 @@ int ctx_get(DevCtx **out)
         return BM_ERR_OOM;
     }
     cudaMemcpy(C->tw, h.data(), h.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    // q1 twiddles for the FP64-pipe transforms (ntt3f.cuh): (w, fl(w / q1)) as double bit patterns
+    auto fpair = [](uint64_t w) {
+        const double dw = (double)w, dq = dw / (double)Q1;
+        uint64_t a, b;
+        memcpy(&a, &dw, 8);
+        memcpy(&b, &dq, 8);
+        return make_ulonglong2(a, b);
+    };
+    {
+        const HostPrime &H = host_prime(1);
+        std::vector<ulonglong2> hf(2 * (size_t)N);
+        for (int k = 0; k < N; k++) hf[k] = fpair(H.fwd[k]), hf[(size_t)N + k] = fpair(H.inv[k]);
+        if (cudaMalloc(&C->twf, hf.size() * sizeof(ulonglong2)) != cudaSuccess) {
+            cudaFree(C->tw);
+            delete C;
+            cudaGetLastError();
+            return BM_ERR_OOM;
+        }
+        cudaMemcpy(C->twf, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+        PrimeK &P = C->pr[1];
+        P.fwdf = C->twf;
+        P.invf = C->twf + N;
+        P.ninvf = fpair(H.ninv);
+        P.ninv_w1f = fpair(mulmod_h(H.ninv, H.inv[1], H.q));
+    }
     for (int i = 0; i < 3; i++) {
         const HostPrime &H = host_prime(i);
         PrimeK &P = C->pr[i];
