@@ -3,10 +3,12 @@
 // registers/shared memory, for each of the three primes; checks the round trip is the identity.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include "../paper_2408_06167_b200/csrc/bm_common.cuh"
 #include "../paper_2408_06167_b200/csrc/bm_host.h"
 #include "../paper_2408_06167_b200/csrc/ntt3.cuh"
+#include "../paper_2408_06167_b200/csrc/ntt3f.cuh"
 using namespace bm;
 typedef unsigned __int128 u128;
 
@@ -45,8 +47,13 @@ __global__ void __launch_bounds__(512, MINB3) k_bench3(PrimeK P, uint64_t *data,
     uint64_t *d = data + (size_t)blockIdx.x * N;
     v3::load_coef(a, d);
     for (int it = 0; it < iters; it++) {
-        v3::fwd<PI>(a, sm, P);
-        v3::inv<PI>(a, sm, P);
+        if constexpr (PI == 3) { // q1 on the FP64 pipe (ntt3f.cuh)
+            v3::fwd_q1f(a, sm, P.fwdf);
+            v3::inv_q1f(a, sm, P.invf, P.ninvf, P.ninv_w1f);
+        } else {
+            v3::fwd<PI>(a, sm, P);
+            v3::inv<PI>(a, sm, P);
+        }
     }
     v3::store_coef(d, a);
 }
@@ -59,12 +66,13 @@ int main(int argc, char **argv)
     int iters = argc > 2 ? atoi(argv[2]) : 20;
     const size_t SM_BYTES = argc > 3 ? (size_t)atoi(argv[3]) : SMEM_WORDS * 8; // larger: less L1 left for twiddles
     typedef void (*KF)(PrimeK, uint64_t *, int);
-    KF kf[3][3] = {{k_bench<1, 0>, k_bench<1, 1>, k_bench<1, 2>}, {k_bench<2, 0>, k_bench<2, 1>, k_bench<2, 2>},
-                   {k_bench3<0>, k_bench3<1>, k_bench3<2>}};
-    for (int v = 0; v < 3; v++)
+    KF kf[4][3] = {{k_bench<1, 0>, k_bench<1, 1>, k_bench<1, 2>}, {k_bench<2, 0>, k_bench<2, 1>, k_bench<2, 2>},
+                   {k_bench3<0>, k_bench3<1>, k_bench3<2>}, {k_bench3<3>, k_bench3<3>, k_bench3<3>}};
+    for (int v = 0; v < 4; v++)
         for (int i = 0; i < 3; i++) cudaFuncSetAttribute(kf[v][i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BYTES);
-    for (int v = 0; v < 3; v++)
+    for (int v = 1; v < 4; v++)
     for (int pi = 0; pi < 3; pi++) {
+        if (v == 3 && pi != 1) continue; // v4 = q1 on the FP64 pipe
         const HostPrime &H = host_prime(pi);
         std::vector<ulonglong2> tw(2 * N);
         for (int k = 0; k < N; k++) tw[k] = sp(H.fwd[k], H.q), tw[N + k] = sp(H.inv[k], H.q);
@@ -77,6 +85,17 @@ int main(int argc, char **argv)
         P.ninv_w1 = sp(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
         P.r64 = sp((uint64_t)(((u128)1 << 64) % H.q), H.q);
         P.one_p = (uint64_t)(((u128)1 << 64) / H.q);
+        ulonglong2 *dtwf = nullptr;
+        if (v == 3) { // (w, fl(w / q1)) as doubles
+            auto fp = [](uint64_t w) { double a = (double)w, b = a / (double)Q1; uint64_t x, y;
+                                       memcpy(&x, &a, 8); memcpy(&y, &b, 8); return make_ulonglong2(x, y); };
+            std::vector<ulonglong2> tf(2 * N);
+            for (int k = 0; k < N; k++) tf[k] = fp(H.fwd[k]), tf[N + k] = fp(H.inv[k]);
+            cudaMalloc(&dtwf, tf.size() * 16);
+            cudaMemcpy(dtwf, tf.data(), tf.size() * 16, cudaMemcpyHostToDevice);
+            P.fwdf = dtwf; P.invf = dtwf + N;
+            P.ninvf = fp(H.ninv); P.ninv_w1f = fp(mulmod_h(H.ninv, H.inv[1], H.q));
+        }
         std::vector<uint64_t> h((size_t)blocks * N);
         srand(pi + 1);
         for (auto &x : h) x = (((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ rand()) % H.q;
@@ -84,7 +103,7 @@ int main(int argc, char **argv)
         cudaMalloc(&dd, h.size() * 8);
         cudaMemcpy(dd, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         KF k = kf[v][pi];
-        const int thr = v == 2 ? 512 : 256;
+        const int thr = v >= 2 ? 512 : 256;
         k<<<blocks, thr, SM_BYTES>>>(P, dd, 1); // warm-up (+ round trip)
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -100,7 +119,7 @@ int main(int argc, char **argv)
         int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
         printf("v%d prime %d: %s  %.3f ms  %.1f Gbfly/s  %.2f bfly/clk/SM (at %d MHz)  err=%s\n", v + 1, pi, ok ? "ok" : "MISMATCH", ms,
                bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
-        cudaFree(dd); cudaFree(dtw);
+        cudaFree(dd); cudaFree(dtw); cudaFree(dtwf);
     }
     return 0;
 }

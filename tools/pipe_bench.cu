@@ -70,6 +70,19 @@ __global__ void __launch_bounds__(512) k(uint64_t *out, uint32_t s0)
             if (OP == 17) { // IMAD.WIDE alone (chain through the 64-bit accumulator)
                 asm volatile("{.reg .u64 w; mov.b64 w, {%0, %1}; mad.wide.u32 w, %0, %1, w; mov.b64 {%0, %1}, w;}" : "+r"(a[i]), "+r"(b[i]));
             }
+            if (OP == 18) { // I2F.F64.U32 (+DADD to consume)
+                double t;
+                asm volatile("cvt.rn.f64.u32 %0, %1;" : "=d"(t) : "r"(a[i]));
+                f[i] += t; a[i] += 1;
+            }
+            if (OP == 19) { // F2I.S64.F64 floor (+IADD)
+                uint64_t t;
+                asm volatile("cvt.rmi.s64.f64 %0, %1;" : "=l"(t) : "d"(f[i]));
+                a[i] += (uint32_t)t; f[i] += 1.0;
+            }
+            if (OP == 20) { // DADD.RM (magic floor)
+                asm volatile("add.rm.f64 %0, %0, %1;" : "+d"(f[i]) : "d"(g[i]));
+            }
             if (OP == 12) { // f64 -> u64
                 uint64_t t;
                 asm volatile("cvt.rzi.u64.f64 %0, %1;" : "=l"(t) : "d"(f[i]));
@@ -126,5 +139,8 @@ int main()
     run<10>("cvt f64<-u64 (+DADD)", 1, d);
     run<11>("cvt.rmi f64 (floor)", 1, d);
     run<12>("cvt u64<-f64 (+IADD)", 1, d);
+    run<18>("I2F.F64.U32 (+DADD +IADD)", 1, d);
+    run<19>("F2I.S64.F64 floor (+IADD +DADD)", 1, d);
+    run<20>("DADD.RM", 1, d);
     return 0;
 }
