@@ -171,9 +171,10 @@ def test_chunking_ragged(env, O, monkeypatch, chunk):
     assert np.array_equal(got, again)
 
 
-@pytest.mark.parametrize("d,p", [(16, 16), (4096, 8)])
+@pytest.mark.parametrize("d,p", [(16, 16), (4096, 8), (1024, 1024)])
 def test_layout_extremes(env, O, d, p):
-    """s = 1 (no ladder, output INTT kernel) and the largest d (s = 512, B = 8, 9 rotations)."""
+    """s = 1 (no ladder, output INTT kernel), the largest d (s = 512, B = 8, 9 rotations) and
+    p = 1024 parts (the tensor's 128-bit / FP64 sums are folded mod q every 512 parts)."""
     T = I.random_unit(20, d, d)
     Q = I.random_unit(1, d, d + 1)
     st = Setup(env, O, d, p, T, Q)
