@@ -536,110 +536,117 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
     // scratch (dead after K3): A -> D01 [c][q0 | P], base_0 -> D2[0], P^-1 y^ -> D2[1]
     uint64_t *Ab = K.D01 + (size_t)pi * 4 * N, *b0s = K.D2 + (size_t)pi * 2 * N, *tsc = b0s + N;
     const ulonglong2 pinv = K.pinv[0];
-    // ---- digit: X~P = NTT_P(INTT_q0(c1)); (c1, X~P) staged by NTT index
+    // Phases share one call site per transform (an instruction-cache concern: every unrolled
+    // transform is ~40 KB of SASS): ph 0 = the digit, ph 1, 2 = the ModDown of component ph - 1.
     uint64_t a[E];
-    load_eval(a, cin.at(pi, 1));
-#pragma unroll
-    for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
-    inv<0>(a, XB, K.pr[0]);
-    fwd<2>(a, XB, K.pr[2]);
-#pragma unroll
-    for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
-    __syncthreads();
-    // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
-    //      time, the next rotation's keys loaded while this one's are used
 #pragma unroll 1
-    for (int g2 = 0; g2 < E / 2; g2++) {
-        const int e0 = 2 * g2, pos = pos_M4(tid, e0);
-        const int j0 = j_M4(tid, e0), j1 = j_M4(tid, e0 + 1);
-        u128 A[2][4]; // [coefficient][c * 2 + limb (q0, P)]
+    for (int ph = 0; ph < 3; ph++) {
+        const int c = ph - 1;
+        if (ph == 0) { // (c1, .) staged by NTT index; a = c1
+            load_eval(a, cin.at(pi, 1));
 #pragma unroll
-        for (int u = 0; u < 2; u++)
+            for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
+        } else {       // y^c = INTT_P(A[c][P]); a = base_c + A[c][q0]
 #pragma unroll
-            for (int v = 0; v < 4; v++) A[u][v] = 0;
-        ulonglong2 kc[4], kn[4];
-#pragma unroll
-        for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + (size_t)v * N + pos);
-        uint32_t gr = 1;
-#pragma unroll 1
-        for (int r = 1; r < s; r++) {
-            gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
-            if (r + 1 < s) {
-#pragma unroll
-                for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
+            for (int e = 0; e < E; e += 2) { // written by this thread: coherent loads
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c + 1) * N + pos_M4(tid, e));
+                a[e] = v.x;
+                a[e + 1] = v.y;
             }
-            const ulonglong2 x0 = SX[pidx(auto_perm(j0, gr))], x1 = SX[pidx(auto_perm(j1, gr))];
+            inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
 #pragma unroll
-            for (int c = 0; c < 2; c++) {
-                A[0][2 * c] += (u128)x0.x * kc[2 * c].x;
-                A[1][2 * c] += (u128)x1.x * kc[2 * c].y;
-                A[0][2 * c + 1] += (u128)x0.y * kc[2 * c + 1].x;
-                A[1][2 * c + 1] += (u128)x1.y * kc[2 * c + 1].y;
+            for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            const uint64_t *base = c ? cin.at(pi, 1) : b0s;
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                const int pos = pos_M4(tid, e);
+                const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
+                const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c) * N + pos);
+                a[e] = csub(bv.x + av.x, Q0);
+                a[e + 1] = csub(bv.y + av.y, Q0);
             }
-            if ((r & 63) == 0) { // 64 products of < 2^60 x 2^60 stay below 2^128
-#pragma unroll
-                for (int u = 0; u < 2; u++)
-#pragma unroll
-                    for (int v = 0; v < 4; v++)
-                        A[u][v] = (v & 1) ? red128s<2>(A[u][v], K.pr[2].r64) : red128s<0>(A[u][v], K.pr[0].r64);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; v++) kc[v] = kn[v];
-        }
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-            if (v & 1) st2(Ab + (size_t)v * N + pos, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
-            else st2(Ab + (size_t)v * N + pos, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
-        }
-    }
-    // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
-    //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
-    __syncthreads();
-    stage_by_j(SP, cin.at(pi, 0));
-#pragma unroll 1
-    for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < E; e++) {
-            const int j = j_M4(tid, e);
-            a[e] = csub(SP[pidx(j)] + SP[pidx(auto_perm(j, g))], Q0);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
-    // ---- one ModDown per component, straight to coefficient form
-#pragma unroll 1
-    for (int c = 0; c < 2; c++) {
-#pragma unroll
-        for (int e = 0; e < E; e += 2) { // written by this thread above: coherent loads
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c + 1) * N + pos_M4(tid, e));
-            a[e] = v.x;
-            a[e + 1] = v.y;
-        }
-        inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
-#pragma unroll
-        for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
-        const uint64_t *base = c ? cin.at(pi, 1) : b0s;
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int pos = pos_M4(tid, e);
-            const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
-            const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c) * N + pos);
-            a[e] = csub(bv.x + av.x, Q0);
-            a[e + 1] = csub(bv.y + av.y, Q0);
         }
         inv<0>(a, XB, K.pr[0]);
-        uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+        if (ph > 0) { // out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c
+            uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
 #pragma unroll
-        for (int e = 0; e < E; e++) {
-            const int j = j_M1(tid, e);
-            o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
+            for (int e = 0; e < E; e++) {
+                const int j = j_M1(tid, e);
+                o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
+            }
+            continue;
         }
-    }
+        // ---- digit: X~P = NTT_P(x), staged next to c1
+        fwd<2>(a, XB, K.pr[2]);
+#pragma unroll
+        for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
+        __syncthreads();
+        // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
+        //      time, the next rotation's keys loaded while this one's are used
+#pragma unroll 1
+        for (int g2 = 0; g2 < E / 2; g2++) {
+            const int e0 = 2 * g2, pos = pos_M4(tid, e0);
+            const int j0 = j_M4(tid, e0), j1 = j_M4(tid, e0 + 1);
+            u128 A[2][4]; // [coefficient][c * 2 + limb (q0, P)]
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) A[u][v] = 0;
+            ulonglong2 kc[4], kn[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + (size_t)v * N + pos);
+            uint32_t gr = 1;
+#pragma unroll 1
+            for (int r = 1; r < s; r++) {
+                gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
+                if (r + 1 < s) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
+                }
+                const ulonglong2 x0 = SX[pidx(auto_perm(j0, gr))], x1 = SX[pidx(auto_perm(j1, gr))];
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    A[0][2 * c] += (u128)x0.x * kc[2 * c].x;
+                    A[1][2 * c] += (u128)x1.x * kc[2 * c].y;
+                    A[0][2 * c + 1] += (u128)x0.y * kc[2 * c + 1].x;
+                    A[1][2 * c + 1] += (u128)x1.y * kc[2 * c + 1].y;
+                }
+                if ((r & 63) == 0) { // 64 products of < 2^60 x 2^60 stay below 2^128
+#pragma unroll
+                    for (int u = 0; u < 2; u++)
+#pragma unroll
+                        for (int v = 0; v < 4; v++)
+                            A[u][v] = (v & 1) ? red128s<2>(A[u][v], K.pr[2].r64) : red128s<0>(A[u][v], K.pr[0].r64);
+                }
+#pragma unroll
+                for (int v = 0; v < 4; v++) kc[v] = kn[v];
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                if (v & 1) st2(Ab + (size_t)v * N + pos, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
+                else st2(Ab + (size_t)v * N + pos, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
+            }
+        }
+        // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
+        //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
+        __syncthreads();
+        stage_by_j(SP, cin.at(pi, 0));
+#pragma unroll 1
+        for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = j_M4(tid, e);
+                a[e] = csub(SP[pidx(j)] + SP[pidx(auto_perm(j, g))], Q0);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
+}
 }
 
 // K7: output INTT when there is no ladder (s = 1)
