@@ -244,7 +244,7 @@ def run_ours(args):
     total_pairs = n_sets * nq
     chunk = int(os.environ.get("BM_CHUNK_PAIRS", "16384"))
     n_chunks = G * math.ceil(n_sets * gq / min(chunk, n_sets * gq))
-    rounds = 1 if order == 0 else p
+    rounds = p if order == 1 else 1
     launches = n_chunks * (3 * rounds + 1)
 
     # per-kernel-class device times (CUDA events on the launching stream), same step, profiled pass
@@ -256,7 +256,7 @@ def run_ours(args):
     B.bm_sync()
     pms, pla, pun = B.bm_profile_read()
     B.bm_set_profiling(False)
-    mm = class_modmuls(p if order == 0 else 1, prm.log_s)
+    mm = class_modmuls(1 if order == 1 else p, prm.log_s)  # order 1 runs the part rounds one part each
     classes = B.PROFILE_CLASSES
     per_class = {}
     for i, c in enumerate(classes):
