@@ -803,3 +803,264 @@ int or_match(int logN, int d, int p, int order, const uint64_t *rlk, const uint6
     ctx_free(&C);
     return 0;
 }
+
+/* ================================================================== */
+/* f3: server-side query expansion, Algorithm 1    */
+/* "Input Ciphertext Expansion", on the chain        */
+/* extended by one level: Q2 = {q0, q1, q2}, q2 = the largest prime     */
+/* below q1 with q2 = 1 (mod 16384) (reading R24).            */
+/* ================================================================== */
+/* Layouts (coefficient domain):
+ *   ct level 2   [2 comps][3 limbs q0,q1,q2][N]
+ *   pk_q2        [2 comps (b,a)][N]: the q2 limb of the public key (its q0, q1 limbs are pk's)
+ *   gk1          [log2 p][2 digits j][2 comps (b,a)][3 limbs q0,q1,P][N]; entry t is the
+ *                level-1 Galois key of the left rotation by s 2^t
+ *   masks        [p][N] int64 plaintexts of X_i at scale q2 (encoded by the caller)           */
+enum { P_GK1_A = 11, P_GK1_E = 12 };
+
+/* largest prime below `below` with q = 1 (mod m) */
+uint64_t or_find_prime_below(uint64_t below, uint64_t m)
+{
+    uint64_t q = below - m;
+    while (!or_is_prime(q)) q -= m;
+    return q;
+}
+uint64_t or_q2(void)
+{
+    uint64_t q[3];
+    or_primes(q);
+    return or_find_prime_below(q[1], 16384);
+}
+
+typedef struct {
+    ctx_t c;             /* q0, q1, P as everywhere else */
+    uint64_t q2;
+    ring_t R2;
+    uint64_t q2_inv[2];  /* q2^-1 mod q0, q1 */
+} ctx2_t;
+
+static void ctx2_init(ctx2_t *x, int logN)
+{
+    ctx_init(&x->c, logN);
+    x->q2 = or_find_prime_below(x->c.q[1], 16384);
+    ring_init(&x->R2, logN, x->q2);
+    for (int k = 0; k < 2; k++) x->q2_inv[k] = invmod(x->q2 % x->c.q[k], x->c.q[k]);
+}
+static void ctx2_free(ctx2_t *x)
+{
+    ring_free(&x->R2);
+    ctx_free(&x->c);
+}
+/* modulus and ring of level-2 limb l (0: q0, 1: q1, 2: q2) */
+static uint64_t l2_q(const ctx2_t *x, int l) { return l == 2 ? x->q2 : x->c.q[l]; }
+static const ring_t *l2_R(const ctx2_t *x, int l) { return l == 2 ? &x->R2 : &x->c.R[l]; }
+
+/* Expansion keys.  pk_q2 = (-a s + e, a) mod q2 with pk's error e (P_PK_E, object 0) and
+ * a from (P_PK_A, object 0, sub-stream 3): the level-2 public key is pk extended by one limb.
+ * gk1 for rotation r = s 2^t, digit j in {0,1}: over {q0,q1,P},
+ *   b = -a s + e + [l = j] (P mod q_l) sigma_{5^r}(s) in limb q_l,   b = -a s + e in limb P,
+ * a from (P_GK1_A, object 2r + j, sub-stream l), e from (P_GK1_E, object 2r + j). */
+int or_keygen_exp(int logN, uint64_t seed, int d, int p, int zero_error, uint64_t *pk_q2, uint64_t *gk1)
+{
+    if (p <= 0 || d % p) return -1;
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    const ctx_t *C = &X.c;
+    const int N = C->N, s = d / p;
+    uint64_t *tmp = malloc(sizeof(uint64_t) * N), *e = malloc(sizeof(uint64_t) * N);
+    uint64_t *sq = calloc((size_t)N, sizeof(uint64_t)), *a = malloc(sizeof(uint64_t) * N);
+    uint64_t *ss = malloc(sizeof(uint64_t) * N);
+    int64_t *sv = malloc(sizeof(int64_t) * N), *ev = malloc(sizeof(int64_t) * N);
+    or_sample(seed, P_SK, 0, 0, 1, N, 0, (uint64_t *)sv);
+
+    /* pk limb q2 */
+    or_sample(seed, P_PK_E, 0, 0, 2, N, 0, (uint64_t *)ev);
+    if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+    for (int k = 0; k < N; k++) { sq[k] = from_signed(sv[k], X.q2); e[k] = from_signed(ev[k], X.q2); }
+    or_sample(seed, P_PK_A, 0, 3, 0, N, X.q2, a);
+    poly_mul(&X.R2, a, sq, tmp);
+    poly_sub(X.q2, N, e, tmp, pk_q2);
+    memcpy(pk_q2 + N, a, sizeof(uint64_t) * N);
+
+    /* level-1 Galois keys */
+    int log_p = 0;
+    while ((1 << log_p) < p) log_p++;
+    for (int t = 0; t < log_p; t++) {
+        const uint64_t r = (uint64_t)s << t, g = galois_elt(N, r);
+        for (int j = 0; j < 2; j++) {
+            const uint64_t obj = 2 * r + (uint64_t)j;
+            or_sample(seed, P_GK1_E, obj, 0, 2, N, 0, (uint64_t *)ev);
+            if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+            for (int l = 0; l < 3; l++) {
+                const uint64_t q = C->q[l];
+                for (int k = 0; k < N; k++) { sq[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+                or_sample(seed, P_GK1_A, obj, (uint32_t)l, 0, N, q, a);
+                uint64_t *b = gk1 + ((((size_t)t * 2 + j) * 2 + 0) * 3 + l) * N;
+                uint64_t *aa = gk1 + ((((size_t)t * 2 + j) * 2 + 1) * 3 + l) * N;
+                poly_mul(&C->R[l], a, sq, tmp);
+                poly_sub(q, N, e, tmp, b);
+                if (l == j) {
+                    automorphism(q, N, sq, g, ss);
+                    poly_scale(q, N, ss, C->P_mod[l], tmp);
+                    poly_add(q, N, b, tmp, b);
+                }
+                memcpy(aa, a, sizeof(uint64_t) * N);
+            }
+        }
+    }
+    free(tmp); free(e); free(sq); free(a); free(ss); free(sv); free(ev);
+    ctx2_free(&X);
+    return 0;
+}
+
+/* Public-key encryption at level 2 ("a client encrypts the user's feature vector"):
+ * ct_o = (u b + e0 + pt, u a + e1) over {q0,q1,q2}, the same streams as or_encrypt (object
+ * first_obj + c), pk = [2][2][N] over {q0,q1} and pk_q2 = [2][N].  out [n_cts][2][3][N]. */
+void or_encrypt_l2(int logN, const uint64_t *pk, const uint64_t *pk_q2, const int64_t *pt, int64_t n_cts,
+                   uint64_t first_obj, uint64_t seed, uint64_t *out)
+{
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    const int N = X.c.N;
+    int64_t *uv = malloc(sizeof(int64_t) * N), *e0v = malloc(sizeof(int64_t) * N), *e1v = malloc(sizeof(int64_t) * N);
+    uint64_t *u = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * N), *x = malloc(sizeof(uint64_t) * N);
+    for (int64_t c = 0; c < n_cts; c++) {
+        uint64_t obj = first_obj + (uint64_t)c;
+        or_sample(seed, P_ENC_U, obj, 0, 1, N, 0, (uint64_t *)uv);
+        or_sample(seed, P_ENC_E0, obj, 0, 2, N, 0, (uint64_t *)e0v);
+        or_sample(seed, P_ENC_E1, obj, 0, 2, N, 0, (uint64_t *)e1v);
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = l2_q(&X, l);
+            const uint64_t *b = l == 2 ? pk_q2 : pk + (size_t)(0 * 2 + l) * N;
+            const uint64_t *a = l == 2 ? pk_q2 + N : pk + (size_t)(1 * 2 + l) * N;
+            uint64_t *c0 = out + ((size_t)c * 6 + 0 * 3 + l) * N, *c1 = out + ((size_t)c * 6 + 1 * 3 + l) * N;
+            for (int k = 0; k < N; k++) u[k] = from_signed(uv[k], q);
+            poly_mul(l2_R(&X, l), u, b, t);
+            for (int k = 0; k < N; k++)
+                x[k] = addmod(from_signed(e0v[k], q), from_signed(pt[(size_t)c * N + k], q), q);
+            poly_add(q, N, t, x, c0);
+            poly_mul(l2_R(&X, l), u, a, t);
+            for (int k = 0; k < N; k++) x[k] = from_signed(e1v[k], q);
+            poly_add(q, N, t, x, c1);
+        }
+    }
+    free(uv); free(e0v); free(e1v); free(u); free(t); free(x);
+    ctx2_free(&X);
+}
+
+/* m = c0 + c1 s mod q_l for the three level-2 limbs; ct [2][3][N] -> m [3][N] */
+void or_decrypt_l2(int logN, const int8_t *sk, const uint64_t *ct, uint64_t *m)
+{
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    const int N = X.c.N;
+    uint64_t *s = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * N);
+    for (int l = 0; l < 3; l++) {
+        const uint64_t q = l2_q(&X, l);
+        for (int k = 0; k < N; k++) s[k] = from_signed(sk[k], q);
+        poly_mul(l2_R(&X, l), ct + (size_t)(3 + l) * N, s, t);
+        poly_add(q, N, ct + (size_t)l * N, t, m + (size_t)l * N);
+    }
+    free(s); free(t);
+    ctx2_free(&X);
+}
+
+/* Mul(P) then Res (Algorithm 1 line 5): level 2 -> level 1,
+ *   t_l = c_l * pt mod q_l (negacyclic, each comp),  out_k = (t_k - centred_{q2}(t_2)) q2^-1 mod q_k.
+ * in [2][3][N], pt int64 [N], out [2][2][N]. */
+static void mul_plain_rescale_q2(const ctx2_t *X, const uint64_t *in, const int64_t *pt, uint64_t *out)
+{
+    const int N = X->c.N;
+    uint64_t *m = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * 3 * N);
+    for (int c = 0; c < 2; c++) {
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = l2_q(X, l);
+            for (int k = 0; k < N; k++) m[k] = from_signed(pt[k], q);
+            poly_mul(l2_R(X, l), in + (size_t)(c * 3 + l) * N, m, t + (size_t)l * N);
+        }
+        for (int l = 0; l < 2; l++) {
+            const uint64_t q = X->c.q[l];
+            for (int k = 0; k < N; k++) {
+                uint64_t z = from_signed(centred(t[(size_t)2 * N + k], X->q2), q);
+                out[(size_t)(c * 2 + l) * N + k] = mulmod(submod(t[(size_t)l * N + k], z, q), X->q2_inv[l], q);
+            }
+        }
+    }
+    free(m); free(t);
+}
+void or_mul_plain_rescale_q2(int logN, const uint64_t *in, const int64_t *pt, uint64_t *out)
+{
+    ctx2_t X; ctx2_init(&X, logN); mul_plain_rescale_q2(&X, in, pt, out); ctx2_free(&X);
+}
+
+/* Rot at level 1 (reading R6) with a 2-digit Galois key gkr [2 digits][2][3][N]:
+ * a_c = sigma_g(c_c) per limb; digits x_j = [a_1]_{q_j} in [0, q_j) lifted non-centred to
+ * {q0,q1,P} (reading R4); KS_c = sum_j x_j gkr[j][c]; out = (a_0 + ModDown(KS_0), ModDown(KS_1)).
+ * in/out [2][2][N] (out may not alias in). */
+static void rotate1(const ctx_t *C, const uint64_t *in, uint64_t r, const uint64_t *gkr, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t g = galois_elt(N, r);
+    uint64_t *a = malloc(sizeof(uint64_t) * 4 * N), *x = malloc(sizeof(uint64_t) * N);
+    uint64_t *t = malloc(sizeof(uint64_t) * N), *KS = malloc(sizeof(uint64_t) * 3 * N);
+    uint64_t *ksd = malloc(sizeof(uint64_t) * 2 * N);
+    for (int c = 0; c < 2; c++)
+        for (int l = 0; l < 2; l++)
+            automorphism(C->q[l], N, in + (size_t)(c * 2 + l) * N, g, a + (size_t)(c * 2 + l) * N);
+    for (int c = 0; c < 2; c++) {
+        memset(KS, 0, sizeof(uint64_t) * 3 * N);
+        for (int j = 0; j < 2; j++) {
+            const uint64_t *xj = a + (size_t)(1 * 2 + j) * N; /* [sigma(c1)]_{q_j}, in [0, q_j) */
+            for (int l = 0; l < 3; l++) {
+                const uint64_t q = C->q[l];
+                for (int k = 0; k < N; k++) x[k] = xj[k] % q;
+                poly_mul(&C->R[l], x, gkr + ((size_t)(j * 2 + c) * 3 + l) * N, t);
+                poly_add(q, N, KS + (size_t)l * N, t, KS + (size_t)l * N);
+            }
+        }
+        moddown(C, 2, KS, ksd);
+        for (int l = 0; l < 2; l++) {
+            uint64_t *o = out + (size_t)(c * 2 + l) * N;
+            if (c == 0) poly_add(C->q[l], N, a + (size_t)l * N, ksd + (size_t)l * N, o);
+            else memcpy(o, ksd + (size_t)l * N, sizeof(uint64_t) * N);
+        }
+    }
+    free(a); free(x); free(t); free(KS); free(ksd);
+}
+void or_rotate1(int logN, const uint64_t *in, uint64_t r, const uint64_t *gkr, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); rotate1(&C, in, r, gkr, out); ctx_free(&C);
+}
+
+/* Algorithm 1 with SPEC.md:297's post-condition (reading R25): for each
+ * query ciphertext (level 2, tiled query) and part i < p:
+ *   C_i = Res(Mul(P)(C_in, mask_i)),  then for t = 0 .. log2(p)-1:  C_i = Add(C_i, Rot(C_i, s 2^t)).
+ * in [n][2][3][N], out [n][p][2][2][N] (level 1). */
+int or_expand(int logN, int d, int p, const int64_t *masks, const uint64_t *gk1, const uint64_t *in, int64_t n,
+              uint64_t *out)
+{
+    if (p <= 0 || d % p) return -1;
+    int log_p = 0;
+    while ((1 << log_p) < p) log_p++;
+    if ((1 << log_p) != p) return -1;
+    const int s = d / p;
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    const int N = X.c.N;
+    uint64_t *rot = malloc(sizeof(uint64_t) * 4 * N);
+    for (int64_t qi = 0; qi < n; qi++)
+        for (int i = 0; i < p; i++) {
+            uint64_t *Ci = out + ((size_t)qi * p + i) * 4 * N;
+            mul_plain_rescale_q2(&X, in + (size_t)qi * 6 * N, masks + (size_t)i * N, Ci);
+            for (int t = 0; t < log_p; t++) {
+                rotate1(&X.c, Ci, (uint64_t)s << t, gk1 + (size_t)t * 12 * N, rot);
+                for (int l = 0; l < 2; l++)
+                    for (int c = 0; c < 2; c++)
+                        poly_add(X.c.q[l], N, Ci + (size_t)(c * 2 + l) * N, rot + (size_t)(c * 2 + l) * N,
+                                 Ci + (size_t)(c * 2 + l) * N);
+            }
+        }
+    free(rot);
+    ctx2_free(&X);
+    return 0;
+}

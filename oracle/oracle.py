@@ -76,6 +76,20 @@ def lib():
         L.or_keygen_hoisted.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u64p]
         L.or_keygen_hoisted.restype = ctypes.c_int
         L.or_hoisted_rot_sum.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p]
+        # f3: server-side query expansion on the chain extended by q2
+        L.or_find_prime_below.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        L.or_find_prime_below.restype = ctypes.c_uint64
+        L.or_q2.restype = ctypes.c_uint64
+        L.or_keygen_exp.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p,
+                                    _u64p]
+        L.or_keygen_exp.restype = ctypes.c_int
+        L.or_encrypt_l2.argtypes = [ctypes.c_int, _u64p, _u64p, _i64p, ctypes.c_int64, ctypes.c_uint64,
+                                    ctypes.c_uint64, _u64p]
+        L.or_decrypt_l2.argtypes = [ctypes.c_int, _i8p, _u64p, _u64p]
+        L.or_mul_plain_rescale_q2.argtypes = [ctypes.c_int, _u64p, _i64p, _u64p]
+        L.or_rotate1.argtypes = [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p]
+        L.or_expand.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _u64p, _u64p, ctypes.c_int64, _u64p]
+        L.or_expand.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -331,3 +345,103 @@ def scores_from_output(logN, d, p, sk, out_ct, q0):
     P = primes()
     scale = DELTA * DELTA / P[1]
     return decode_slots(centred_i64(m, q0), logN, scale, slots=np.arange(B) * s)
+
+
+# ---------------------------------------------------------------------------- f3: query expansion
+# Algorithm 1 "Input Ciphertext Expansion" with SPEC.md:297's post-condition
+# on the chain extended by one 40-bit prime q2 (readings R24-R26): the client encrypts
+# the query tiled S/d times at level 2 = {q0, q1, q2}; the server multiplies by mask X_i (scale q2),
+# rescales by q2 (level 1, scale exactly 2^40) and adds log2(p) left rotations by s 2^t.
+def q2():
+    return int(lib().or_q2())
+
+
+def find_prime_below(below, m):
+    return int(lib().or_find_prime_below(below, m))
+
+
+def log2_exact(x):
+    k = x.bit_length() - 1
+    assert 1 << k == x
+    return k
+
+
+def keygen_exp(logN, seed, d, p, zero_error=False):
+    """Expansion keys of keygen(seed)'s secret: pk_q2 [2][N] (pk's q2 limb) and the level-1
+    Galois keys gk1 [log2 p][2 digits][2 comps][3 limbs q0,q1,P][N] of rotations s 2^t."""
+    N = 1 << logN
+    lp = log2_exact(p)
+    pk_q2 = np.zeros((2, N), np.uint64)
+    gk1 = np.zeros((max(lp, 1), 2, 2, 3, N), np.uint64)
+    rc = lib().or_keygen_exp(logN, seed, d, p, int(zero_error), _p(pk_q2, _u64p), _p(gk1, _u64p))
+    if rc:
+        raise ValueError(f"or_keygen_exp: {rc}")
+    return pk_q2, gk1[:lp]
+
+
+def encrypt_l2(logN, pk, pk_q2, pt, first_obj, seed):
+    """pt int64 [n][N] -> level-2 cts [n][2][3][N] (coefficient domain)."""
+    pt = np.ascontiguousarray(pt, np.int64)
+    n = pt.shape[0]
+    out = np.zeros((n, 2, 3, 1 << logN), np.uint64)
+    lib().or_encrypt_l2(logN, _p(np.ascontiguousarray(pk, np.uint64), _u64p),
+                        _p(np.ascontiguousarray(pk_q2, np.uint64), _u64p), _p(pt, _i64p), n, first_obj, seed,
+                        _p(out, _u64p))
+    return out
+
+
+def decrypt_l2(logN, sk, ct):
+    """ct [2][3][N] -> m residues [3][N] (limbs q0, q1, q2)."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    m = np.zeros((3, 1 << logN), np.uint64)
+    lib().or_decrypt_l2(logN, _p(np.ascontiguousarray(sk), _i8p), _p(ct, _u64p), _p(m, _u64p))
+    return m
+
+
+def mul_plain_rescale_q2(logN, ct, pt):
+    """Res(Mul(P)(ct, pt)): ct [2][3][N] level 2, pt int64 [N] -> [2][2][N] level 1."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    pt = np.ascontiguousarray(pt, np.int64)
+    out = np.zeros((2, 2, 1 << logN), np.uint64)
+    lib().or_mul_plain_rescale_q2(logN, _p(ct, _u64p), _p(pt, _i64p), _p(out, _u64p))
+    return out
+
+
+def rotate1(logN, ct, r, gkr):
+    """Rot at level 1 with a 2-digit Galois key gkr [2][2][3][N]: ct [2][2][N] -> [2][2][N]."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    out = np.zeros((2, 2, 1 << logN), np.uint64)
+    lib().or_rotate1(logN, _p(ct, _u64p), r, _p(np.ascontiguousarray(gkr, np.uint64), _u64p), _p(out, _u64p))
+    return out
+
+
+def expand_masks_slots(logN, d, p):
+    """X_i[x] = 1 if (x mod d) lies in [i s, (i+1) s), else 0, for x < S."""
+    S, s, _ = layout(logN, d, p)
+    x = np.arange(S) % d
+    return np.stack([((x >= i * s) & (x < (i + 1) * s)).astype(np.float64) for i in range(p)])
+
+
+def expand_masks(logN, d, p):
+    """The p mask plaintexts at scale q2 (so that Res by q2 leaves the query's scale at 2^40)."""
+    return encode(expand_masks_slots(logN, d, p), logN, scale=float(q2()))
+
+
+def tile_query(qv, logN, d):
+    """The client's single query vector: q_hat tiled S/d times."""
+    S = (1 << logN) // 2
+    qv = np.asarray(qv, np.float64).reshape(-1, d)
+    return np.tile(qv, (1, S // d))
+
+
+def expand(logN, d, p, masks, gk1, ct):
+    """Algorithm 1: level-2 cts [n][2][3][N] -> expanded level-1 parts [n][p][2][2][N]."""
+    ct = np.ascontiguousarray(ct, np.uint64).reshape(-1, 2, 3, 1 << logN)
+    n = ct.shape[0]
+    out = np.zeros((n, p, 2, 2, 1 << logN), np.uint64)
+    g = np.ascontiguousarray(gk1 if len(gk1) else np.zeros((1, 2, 2, 3, 1 << logN), np.uint64), np.uint64)
+    rc = lib().or_expand(logN, d, p, _p(np.ascontiguousarray(masks, np.int64), _i64p), _p(g, _u64p), _p(ct, _u64p),
+                         n, _p(out, _u64p))
+    if rc:
+        raise ValueError(f"or_expand: {rc}")
+    return out
