@@ -71,6 +71,7 @@ typedef struct bm_params {
     double scale;           /* 2^40                                    */
     double out_scale;       /* 2^80 / q1: scale of bm_match outputs    */
     uint8_t digest[32];     /* digest of (N, primes, scale, d, p)      */
+    uint64_t q2;            /* f3 only: the extra 40-bit prime of level 2 (2^40 - 45 2^14 + 1) */
 } bm_params;
 
 typedef struct bm_sk bm_sk;           /* host: ternary secret (client only)              */
@@ -141,7 +142,7 @@ int bm_encrypt_db(const bm_params *, const bm_pk_dev *, const double *tmpl, int6
 int bm_encrypt_query(const bm_params *, const bm_pk_dev *, const double *q, int64_t nq, int64_t first_query,
                      uint64_t seed, uint64_t *d_out, void *stream);
 
-/* Domain conversion of n_cts ciphertexts with n_limbs limbs (1 or 2; limbs q0[,q1]),
+/* Domain conversion of n_cts ciphertexts with n_limbs limbs (1, 2 or 3; limbs q0[,q1[,q2]]),
  * layout [n_cts][2][n_limbs][N], device in/out (may alias). */
 int bm_ct_to_coeff(const bm_params *, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
                    void *stream);
@@ -190,6 +191,50 @@ int bm_decrypt(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n
 int bm_decrypt_raw(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, int64_t *m);
 /* argmax with the lowest index winning ties. */
 int bm_top1(const double *scores, int64_t n, int64_t *idx, double *best);
+
+/* ---------------------------------------------------------------------------------------------
+ * f3: SERVER-SIDE QUERY EXPANSION, Algorithm 1 "Input Ciphertext Expansion"
+ * with SPEC.md:297's post-condition (readings R24-R26).  It needs one
+ * more level than BASELINE.json's chain, so it runs on the chain extended by q2 = prm->q2:
+ * level 2 = {q0, q1, q2}.  The client encrypts ONE ciphertext per query: the unit query tiled
+ * S/d times at level 2, scale 2^40.  The server computes, for every part i < p,
+ *   C_i = Res_q2(Mul(P)(C, X_i)),  X_i[x] = [(x mod d) in [i s, (i+1) s)] encoded at scale q2,
+ *   then for t < log2 p:  C_i = C_i + Rot(C_i, s 2^t)   (level-1 rotations, 2-digit key switch),
+ * so C_i is a level-1 ciphertext at scale exactly 2^40 with w_i[x] = q[i s + (x mod s)]: the
+ * d_q input of bm_match.  The rest of the scan is unchanged.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct bm_xk bm_xk;           /* host: pk limb q2 + level-1 Galois keys of strides s 2^t */
+typedef struct bm_xk_dev bm_xk_dev;   /* device: level-2 pk, Galois keys, masks (NTT domain)      */
+
+/* Expansion keys for keygen(seed)'s secret (pass the same seed).  pk limb q2 = (-a s + e, a)
+ * with pk's error e; gk1[t][j] (rotation r = s 2^t, digit j) over {q0,q1,P}:
+ * (-a s + e + [l = j](P mod q_l) sigma_{5^r}(s) [limb q_l], a).  Errors: BM_ERR_INVALID_ARG, BM_ERR_OOM. */
+int bm_xk_keygen(const bm_params *, uint64_t seed, bm_xk **out);
+void bm_xk_free(bm_xk *);
+/* pk_q2 [2][N]; gk1 [log2 p][2 digits][2 comps][3 limbs q0,q1,P][N] (canonical). */
+int bm_xk_export(const bm_xk *, uint64_t *pk_q2, uint64_t *gk1, int32_t *n_rot);
+int bm_xk_import(const bm_params *, const uint64_t *pk_q2, const uint64_t *gk1, int32_t n_rot, bm_xk **out);
+/* Upload (synchronous): the level-2 public key (pk's limbs + xk's q2 limb), the Galois keys and
+ * the p masks (h_masks [p][N] int64, e.g. from bm_encode_masks), all to the NTT domain.
+ * Errors: BM_ERR_KEY_MISMATCH, BM_ERR_CUDA, BM_ERR_OOM. */
+int bm_xk_to_device(const bm_params *, const bm_pk *, const bm_xk *, const int64_t *h_masks, bm_xk_dev **out);
+void bm_xk_dev_free(bm_xk_dev *);
+/* Client encoding (host): q[nq][d] -> pt[nq][N], the unit query tiled S/d times at scale 2^40;
+ * masks: pt[p][N], X_i at scale q2.  Errors: BM_ERR_ZERO_VECTOR, BM_ERR_MAGNITUDE. */
+int bm_encode_query_tiled(const bm_params *, const double *q, int64_t nq, int64_t *pt);
+int bm_encode_masks(const bm_params *, int64_t *pt);
+/* Level-2 public-key encryption (device): ct_o = (u b + e0 + pt, u a + e1) over {q0,q1,q2}, the
+ * streams of bm_encrypt (so limbs q0, q1 equal bm_encrypt's).  d_pt [n][N] int64 device;
+ * d_out [n][2][3][N] NTT domain. */
+int bm_encrypt_l2(const bm_params *, const bm_xk_dev *, const int64_t *d_pt, int64_t n_cts, uint64_t first_obj,
+                  uint64_t seed, uint64_t *d_out, void *stream);
+/* Algorithm 1 on the device: d_in [nq][2][3][N] level 2 (NTT) -> d_out [nq][p][2][2][N] level 1
+ * (NTT), the layout bm_match takes as d_q.  d_ws of at least bm_expand_ws_bytes(prm, nq) bytes.
+ * Asynchronous on `stream`, allocates nothing.  Errors: BM_ERR_INVALID_ARG, BM_ERR_KEY_MISMATCH,
+ * BM_ERR_WORKSPACE, BM_ERR_CUDA. */
+size_t bm_expand_ws_bytes(const bm_params *, int32_t nq);
+int bm_expand(const bm_params *, const bm_xk_dev *, const uint64_t *d_in, int32_t nq, uint64_t *d_out, void *d_ws,
+              size_t ws_bytes, void *stream);
 
 int bm_sync(void *stream);
 const char *bm_strerror(int status);

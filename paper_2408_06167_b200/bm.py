@@ -43,7 +43,7 @@ class bm_params(ctypes.Structure):
     _fields_ = [("logN", ctypes.c_int32), ("N", ctypes.c_int32), ("slots", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("p", ctypes.c_int32), ("s", ctypes.c_int32), ("B", ctypes.c_int32),
                 ("log_s", ctypes.c_int32), ("q", ctypes.c_uint64 * 3), ("scale", ctypes.c_double),
-                ("out_scale", ctypes.c_double), ("digest", ctypes.c_uint8 * 32)]
+                ("out_scale", ctypes.c_double), ("digest", ctypes.c_uint8 * 32), ("q2", ctypes.c_uint64)]
 
 
 _vp = ctypes.c_void_p
@@ -78,6 +78,16 @@ _SIGS = {
     "bm_decrypt": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_decrypt_raw": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_top1": (_i32, [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
+    # f3: server-side query expansion (Algorithm 1) on the chain extended by q2
+    "bm_xk_keygen": (_i32, [_P, _u64, _pp]), "bm_xk_free": (None, [_vp]),
+    "bm_xk_export": (_i32, [_vp, _vp, _vp, ctypes.POINTER(_i32)]),
+    "bm_xk_import": (_i32, [_P, _vp, _vp, _i32, _pp]),
+    "bm_xk_to_device": (_i32, [_P, _vp, _vp, _vp, _pp]), "bm_xk_dev_free": (None, [_vp]),
+    "bm_encode_query_tiled": (_i32, [_P, _vp, _i64, _vp]),
+    "bm_encode_masks": (_i32, [_P, _vp]),
+    "bm_encrypt_l2": (_i32, [_P, _vp, _vp, _i64, _u64, _u64, _vp, _vp]),
+    "bm_expand_ws_bytes": (_sz, [_P, _i32]),
+    "bm_expand": (_i32, [_P, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
     "bm_sync": (_i32, [_vp]),
     "bm_strerror": (ctypes.c_char_p, [_i32]),
     "bm_build_info": (ctypes.c_char_p, []),
@@ -143,6 +153,14 @@ class PublicKeyDev(_Handle):
 
 class EvalKeyDev(_Handle):
     _free = "bm_evk_dev_free"
+
+
+class ExpandKey(_Handle):
+    _free = "bm_xk_free"
+
+
+class ExpandKeyDev(_Handle):
+    _free = "bm_xk_dev_free"
 
 
 # --------------------------------------------------------------------------- API (same names as the C ABI)
@@ -346,3 +364,68 @@ def bm_strerror(code):
 
 def bm_build_info():
     return _lib.bm_build_info().decode()
+
+
+# --------------------------------------------------------------------------- f3: query expansion
+def bm_xk_keygen(prm, seed):
+    """f3 expansion keys (pk limb q2 + level-1 Galois keys) of bm_keygen(prm, seed)'s secret."""
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_xk_keygen(ctypes.byref(prm), seed, ctypes.byref(out)), "bm_xk_keygen")
+    return ExpandKey(out)
+
+
+def bm_xk_export(xk):
+    n = _i32()
+    _chk(_lib.bm_xk_export(xk.ptr, None, None, ctypes.byref(n)), "bm_xk_export")
+    pk_q2 = np.zeros((2, N), np.uint64)
+    gk1 = np.zeros((max(n.value, 1), 2, 2, 3, N), np.uint64)
+    _chk(_lib.bm_xk_export(xk.ptr, _np_ptr(pk_q2), _np_ptr(gk1), ctypes.byref(n)), "bm_xk_export")
+    return pk_q2, gk1[:n.value]
+
+
+def bm_xk_import(prm, pk_q2, gk1):
+    out = ctypes.c_void_p()
+    pk_q2 = np.ascontiguousarray(pk_q2, np.uint64)
+    gk1 = np.ascontiguousarray(gk1, np.uint64)
+    n = gk1.shape[0] if gk1.ndim == 5 else 0
+    _chk(_lib.bm_xk_import(ctypes.byref(prm), _np_ptr(pk_q2), _np_ptr(gk1) if n else None, n, ctypes.byref(out)),
+         "bm_xk_import")
+    return ExpandKey(out)
+
+
+def bm_encode_query_tiled(prm, q):
+    q = np.ascontiguousarray(q, np.float64)
+    out = np.zeros((q.shape[0], N), np.int64)
+    _chk(_lib.bm_encode_query_tiled(ctypes.byref(prm), _np_ptr(q), q.shape[0], _np_ptr(out)), "bm_encode_query_tiled")
+    return out
+
+
+def bm_encode_masks(prm):
+    out = np.zeros((prm.p, N), np.int64)
+    _chk(_lib.bm_encode_masks(ctypes.byref(prm), _np_ptr(out)), "bm_encode_masks")
+    return out
+
+
+def bm_xk_to_device(prm, pk, xk, masks=None):
+    """masks: int64 [p][N] plaintexts (default: bm_encode_masks(prm))."""
+    m = np.ascontiguousarray(bm_encode_masks(prm) if masks is None else masks, np.int64)
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_xk_to_device(ctypes.byref(prm), pk.ptr, xk.ptr, _np_ptr(m), ctypes.byref(out)), "bm_xk_to_device")
+    return ExpandKeyDev(out)
+
+
+def bm_encrypt_l2(prm, xk_dev, d_pt, first_obj, seed, d_out, stream=None):
+    """d_pt: CUDA int64 [n][N]; d_out: CUDA [n][2][3][N] (level 2, NTT domain)."""
+    _chk(_lib.bm_encrypt_l2(ctypes.byref(prm), xk_dev.ptr, _dptr(d_pt), d_pt.shape[0], first_obj, seed, _dptr(d_out),
+                            _stream(stream)), "bm_encrypt_l2")
+
+
+def bm_expand_ws_bytes(prm, nq):
+    return int(_lib.bm_expand_ws_bytes(ctypes.byref(prm), nq))
+
+
+def bm_expand(prm, xk_dev, d_in, nq, d_out, d_ws, stream=None):
+    """Algorithm 1: d_in [nq][2][3][N] level 2 -> d_out [nq][p][2][2][N] level 1 (NTT domain)."""
+    ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
+    _chk(_lib.bm_expand(ctypes.byref(prm), xk_dev.ptr, _dptr(d_in) if nq else None, nq, _dptr(d_out) if nq else None,
+                        _dptr(d_ws) if ws_bytes else None, ws_bytes, _stream(stream)), "bm_expand")

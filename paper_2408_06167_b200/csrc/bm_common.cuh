@@ -20,11 +20,15 @@ constexpr int SLOTS = BM_SLOTS;
 constexpr uint64_t Q0 = 288230376150876161ull;  // 2^58 - 835583
 constexpr uint64_t Q1 = 1099511480321ull;       // 2^40 - 147455
 constexpr uint64_t QP = 1152921504606830593ull; // 2^60 - 16383
+// f3 (server-side query expansion): the chain extended by one level,
+// q2 = the largest prime below q1 with q2 = 1 mod 2^14 (reading R24)
+constexpr uint64_t Q2 = 1099510890497ull;       // 2^40 - 737279 = 2^40 - 45 2^14 + 1
 
 // Purposes of the ChaCha20 random streams (reading R14).
 enum : uint32_t {
     P_SK = 1, P_PK_A = 2, P_PK_E = 3, P_RLK_A = 4, P_RLK_E = 5, P_GK_A = 6, P_GK_E = 7,
-    P_ENC_U = 8, P_ENC_E0 = 9, P_ENC_E1 = 10
+    P_ENC_U = 8, P_ENC_E0 = 9, P_ENC_E1 = 10,
+    P_GK1_A = 11, P_GK1_E = 12 // f3: level-1 Galois keys of the expansion strides
 };
 
 // ---------------------------------------------------------------- ChaCha20 (RFC 8439 sec. 2.3)

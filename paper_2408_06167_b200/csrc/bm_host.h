@@ -15,7 +15,7 @@ struct HostPrime {
     std::vector<uint64_t> inv;    // psi^-brev13(k)
     uint64_t ninv;                // N^-1 mod q
 };
-const HostPrime &host_prime(int i); // 0: q0, 1: q1, 2: P
+const HostPrime &host_prime(int i); // 0: q0, 1: q1, 2: P, 3: q2 (f3)
 const uint64_t *host_cdt();          // 19 Gaussian CDT thresholds
 
 uint64_t mulmod_h(uint64_t a, uint64_t b, uint64_t q);
@@ -42,4 +42,11 @@ struct bm_evk {
     std::vector<uint64_t> gk;  // [n_rot][2][2][N]
     int32_t n_hrot = 0;        // f2 hoisted rotation keys (s - 1 of them, 0 if not generated)
     std::vector<uint64_t> hgk; // [n_hrot][2][2][N], entry r-1 = rotation r
+};
+// f3 expansion keys: the q2 limb of pk and the level-1 Galois keys of rotations s 2^t, t < log2 p
+struct bm_xk {
+    uint8_t digest[32];
+    int32_t d, p, log_p;
+    std::vector<uint64_t> pk_q2; // [2][N]
+    std::vector<uint64_t> gk1;   // [log_p][2 digits][2 comps][3 limbs q0,q1,P][N]
 };

@@ -661,13 +661,216 @@ __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
     store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
 }
 
+// ================================================================== f3: server-side query expansion
+// Algorithm 1 "Input Ciphertext Expansion" on the chain
+// extended by q2 (readings R24-R26).  Per query ciphertext (level 2 = {q0, q1, q2}, NTT
+// domain) and part i < p -- a "ct" below is one (query, part) output:
+//   X1 k_exp_mask   (ct, c)  C_i = Res_q2(C (.) X_i): the mask product in all three limbs, y = INTT_q2
+//                            of the q2 limb, then per Q limb out = c X_i q2^-1 - NTT(q2^-1 y^) with
+//                            q2^-1 y^ = q2^-1 y - [y > q2/2] (q2^-1 is folded into the device masks'
+//                            Q limbs, like P^-1 into the key-switching keys): 3 transforms
+//   for t < log2 p, r = s 2^t, g = 5^r:  C_i <- C_i + Rot(C_i, r) at level 1 (2-digit key switch):
+//   X2 k_rot1_digits (ct, l) sigma_g(c1)[q_l] (an NTT-index gather), x_l = INTT_{q_l} of it, ModUp:
+//                            x0 -> NTT_{q1}, NTT_P; x1 -> NTT_{q0}, NTT_P: 3 transforms
+//   X3 k_rot1_ks    (ct, c)  KS_c over {q0, q1, P} with gk1 (P^-1 in its Q limbs), y = INTT_P(KS_c[P]),
+//                            c_c <- c_c + [c = 0] sigma_g(c0) + P^-1 KS_c - NTT(P^-1 y^) per Q limb: 3
+// XU per ct: [0] sigma(c1)[q0] (digit 0 in its own limb), [1] x0~[q1], [2] x0~[P], [3] x1~[q0],
+//            [4] sigma(c1)[q1] (digit 1 in its own limb), [5] x1~[P]   (all NTT domain)
+struct ExpK {
+    PrimeK pr[4];            // q0, q1, P, q2
+    ulonglong2 pinv[2];      // P^-1 mod q0, q1
+    ulonglong2 q2inv[2];     // q2^-1 mod q0, q1
+    const ulonglong2 *mask;  // [p][3 limbs q0,q1,q2][N]; the Q limbs carry q2^-1
+    const ulonglong2 *gk;    // this step's level-1 Galois key [2 digits][2 comps][3 limbs q0,q1,P][N]
+    const uint64_t *in;      // [n_q][2][3][N] level 2 (the chunk's first query)
+    uint64_t *out;           // [n_q][p][2][2][N] level 1 (the chunk's first query)
+    uint64_t *XU;            // [cts][6][N]
+    int p;
+    uint32_t g;              // Galois element of this step
+};
+constexpr int XU_POLYS = 6;
+constexpr size_t X1_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+constexpr size_t X2_SMEM_BYTES = 2 * SMEM_WORDS * sizeof(uint64_t);
+constexpr size_t X3_SMEM_BYTES = (2 * SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *ys = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t ct = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const int64_t jq = ct / K.p;
+    const int i = (int)(ct % K.p);
+    const uint64_t *cin = K.in + ((size_t)jq * 2 + c) * 3 * N; // [l][N]
+    const ulonglong2 *mk = K.mask + (size_t)i * 3 * N;
+    uint64_t *co = K.out + ((size_t)ct * 2 + c) * 2 * N;     // [l][N]
+    uint64_t a[E];
+    // q2 limb: y = INTT_q2(c[q2] X_i[q2]) (canonical)
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 v = ld2(cin + 2 * N + pos);
+        a[e] = shoup4<3>(v.x, ld2k(mk + 2 * N + pos));
+        a[e + 1] = shoup4<3>(v.y, ld2k(mk + 2 * N + pos + 1));
+    }
+    inv<3>(a, sm, K.pr[3]);
+#pragma unroll
+    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e];
+    // q1 limb (FP64-pipe transform): q2^-1 y^ mod q1 = q2^-1 y - [y > q2/2]
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = a[e];
+        a[e] = reduce_bnd<1>(shoup4<1>(y, K.q2inv[1]) + (y > (Q2 >> 1) ? Q1 - 1 : 0));
+    }
+    fwd_q1f(a, sm, K.pr[1].fwdf);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 v = ld2(cin + 1 * N + pos);
+        const uint64_t xa = shoup4<1>(v.x, ld2k(mk + 1 * N + pos)), xb = shoup4<1>(v.y, ld2k(mk + 1 * N + pos + 1));
+        st2(co + 1 * N + pos, reduce_bnd<1>(xa + Q1 - a[e]), reduce_bnd<1>(xb + Q1 - a[e + 1]));
+    }
+    // q0 limb
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = ys[tid + T * e];
+        a[e] = shoup4<0>(y, K.q2inv[0]) + (y > (Q2 >> 1) ? Q0 - 1 : 0); // < 5 q0
+    }
+    fwd<0>(a, sm, K.pr[0]); // canonical
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 v = ld2(cin + pos);
+        const uint64_t xa = shoup4<0>(v.x, ld2k(mk + pos)), xb = shoup4<0>(v.y, ld2k(mk + pos + 1));
+        st2(co + pos, reduce_bnd<0>(xa + Q0 - a[e]), reduce_bnd<0>(xb + Q0 - a[e + 1]));
+    }
+}
+
+// X2: digits of sigma_g(c1) and their ModUp (the rotation's half of k_digits)
+__global__ void __launch_bounds__(T, 1) k_rot1_digits(ExpK K)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *S = sm + SMEM_WORDS, *xs = S; // xs reuses S once the gather is done (the INTT's barriers)
+    const int tid = threadIdx.x;
+    const int64_t ct = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
+    const uint64_t *c1 = K.out + ((size_t)ct * 2 + 1) * 2 * N + (size_t)l * N;
+    uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
+    stage_by_j(S, c1);
+    __syncthreads();
+    uint64_t a[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = S[pidx(auto_perm(j_M4(tid, e), K.g))];
+    store_eval(xu + (size_t)(l == 0 ? 0 : 4) * N, a); // the digit in its own limb: sigma(c1)[q_l]
+    if (l == 0) {
+        inv<0>(a, sm, K.pr[0]);
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            xs[tid + T * e] = a[e];
+            a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
+        }
+        fwd_q1f(a, sm, K.pr[1].fwdf);
+        store_eval(xu + 1 * N, a);
+    } else {
+        inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
+#pragma unroll
+        for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
+        fwd<0, false>(a, sm, K.pr[0]); // x1 < q1 < q0; lazy [0, 2 q0): a Shoup operand only
+        store_eval(xu + 3 * N, a);
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = xs[tid + T * e];
+    fwd<2, false>(a, sm, K.pr[2]);
+    store_eval(xu + (size_t)(l == 0 ? 2 : 5) * N, a);
+}
+
+// X3: key switch + ModDown + add, one CTA per (ct, component), c_c updated in place
+__global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *S = sm + SMEM_WORDS, *ys = sm + 2 * SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t ct = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
+    uint64_t *cc = K.out + ((size_t)ct * 2 + c) * 2 * N; // [l][N]
+    const uint64_t *c0 = K.out + (size_t)ct * 4 * N;
+    const ulonglong2 *k0 = K.gk + (size_t)(0 * 2 + c) * 3 * N, *k1 = K.gk + (size_t)(1 * 2 + c) * 3 * N;
+    uint64_t a[E];
+    // P limb: y = INTT_P(x0~[P] gk[0][c][P] + x1~[P] gk[1][c][P])
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 u = ld2(xu + 2 * N + pos), v = ld2(xu + 5 * N + pos);
+        a[e] = red8to4<2>(shoup4<2>(u.x, ld2k(k0 + 2 * N + pos)) + shoup4<2>(v.x, ld2k(k1 + 2 * N + pos)));
+        a[e + 1] = red8to4<2>(shoup4<2>(u.y, ld2k(k0 + 2 * N + pos + 1)) + shoup4<2>(v.y, ld2k(k1 + 2 * N + pos + 1)));
+    }
+    inv<2>(a, sm, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e];
+#pragma unroll 1
+    for (int l = 1; l >= 0; l--) { // q1 (FP64-pipe transform), then q0
+        // P^-1 y^ mod q_l = P^-1 y - [y > P/2]
+        if (l == 1) {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint64_t y = ys[tid + T * e];
+                a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (y > (QP >> 1) ? Q1 - 1 : 0));
+            }
+            fwd_q1f(a, sm, K.pr[1].fwdf);
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint64_t y = ys[tid + T * e];
+                a[e] = shoup4<0>(y, K.pinv[0]) + (y > (QP >> 1) ? Q0 - 1 : 0); // < 5 q0
+            }
+            fwd<0>(a, sm, K.pr[0]);
+        }
+        if (c == 0) { // sigma_g(c0)[q_l] by an NTT-index gather (c0 is this CTA's to overwrite)
+            __syncthreads(); // previous limb's gathers from S are done
+            stage_by_j(S, c0 + (size_t)l * N);
+            __syncthreads();
+        }
+        const uint64_t q = l ? Q1 : Q0;
+        const ulonglong2 *kl0 = k0 + (size_t)l * N, *kl1 = k1 + (size_t)l * N;
+        const uint64_t *x0 = xu + (size_t)(l == 0 ? 0 : 1) * N, *x1 = xu + (size_t)(l == 0 ? 3 : 4) * N;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos);
+            const ulonglong2 cv = *reinterpret_cast<const ulonglong2 *>(cc + (size_t)l * N + pos);
+            uint64_t ka, kb;
+            if (l) {
+                ka = shoup4<1>(u.x, ld2k(kl0 + pos)) + shoup4<1>(v.x, ld2k(kl1 + pos));
+                kb = shoup4<1>(u.y, ld2k(kl0 + pos + 1)) + shoup4<1>(v.y, ld2k(kl1 + pos + 1));
+            } else {
+                ka = shoup4<0>(u.x, ld2k(kl0 + pos)) + shoup4<0>(v.x, ld2k(kl1 + pos));
+                kb = shoup4<0>(u.y, ld2k(kl0 + pos + 1)) + shoup4<0>(v.y, ld2k(kl1 + pos + 1));
+            }
+            uint64_t va = cv.x + ka + q - a[e], vb = cv.y + kb + q - a[e + 1]; // < 11 q
+            if (c == 0) {
+                va += S[pidx(auto_perm(j_M4(tid, e), K.g))];
+                vb += S[pidx(auto_perm(j_M4(tid, e + 1), K.g))];
+            }
+            a[e] = l ? reduce_bnd<1>(va) : reduce_bnd<0>(va);
+            a[e + 1] = l ? reduce_bnd<1>(vb) : reduce_bnd<0>(vb);
+        }
+        if (c == 0) __syncthreads(); // every gather of the old c0[q_l] is done before it is overwritten
+#pragma unroll
+        for (int e = 0; e < E; e += 2) st2(cc + (size_t)l * N + pos_M4(tid, e), a[e], a[e + 1]);
+    }
+}
+
 // ================================================================== encryption / conversion / keys
 struct EncK {
-    PrimeK pr[2];
-    const ulonglong2 *pk; // [2][2][N]
+    PrimeK pr[4];
+    const ulonglong2 *pk; // [2][n_limbs][N]
     const int64_t *pt;    // [n][N]
-    uint64_t *out;        // [n][2][2][N]
+    uint64_t *out;        // [n][2][n_limbs][N]
     uint64_t first_obj, seed;
+    int n_limbs;          // 2 (level 1: q0, q1) or 3 (f3 level 2: q0, q1, q2)
+    int lp[3];            // prime index of each limb
 };
 
 // sample a small polynomial of stream st into sm (residues mod q), adding pt if given
@@ -696,14 +899,15 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
 {
     extern __shared__ uint64_t sm[];
     const int tid = threadIdx.x;
-    const int64_t ct = blockIdx.x >> 1;
-    const int l = blockIdx.x & 1;
+    const int nl = Ek.n_limbs;
+    const int64_t ct = blockIdx.x / nl;
+    const int l = (int)(blockIdx.x % nl), pi = Ek.lp[l];
     const uint64_t o = Ek.first_obj + (uint64_t)ct;
-    const PrimeK P = l ? Ek.pr[1] : Ek.pr[0];
+    const PrimeK P = Ek.pr[pi];
     const uint64_t q = P.q;
-    uint64_t *c0 = Ek.out + ((size_t)ct * 4 + 0 + l) * N;
-    uint64_t *c1 = Ek.out + ((size_t)ct * 4 + 2 + l) * N;
-    const ulonglong2 *pb = Ek.pk + (size_t)(0 + l) * N, *pa = Ek.pk + (size_t)(2 + l) * N;
+    uint64_t *c0 = Ek.out + ((size_t)ct * 2 * nl + 0 + l) * N;
+    uint64_t *c1 = Ek.out + ((size_t)ct * 2 * nl + nl + l) * N;
+    const ulonglong2 *pb = Ek.pk + (size_t)(0 + l) * N, *pa = Ek.pk + (size_t)(nl + l) * N;
     uint64_t a[E];
     // phase 0: NTT(u) -> kept in c0 until phase 2;  phase 1: c1 = u a + e1;  phase 2: c0 = u b + e0 + pt
     for (int ph = 0; ph < 3; ph++) {
@@ -714,7 +918,7 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) a[e] = sm[pidx(j_M1(tid, e))];
-        fwd_rt(a, sm, P, l);
+        fwd_rt(a, sm, P, pi);
         if (ph == 0) {
             store_eval(c0, a);
             continue;
@@ -730,7 +934,7 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
 }
 
 struct ConvK {
-    PrimeK pr[3];
+    PrimeK pr[4];
     const uint64_t *in;
     uint64_t *out;
     int n_limbs;
@@ -745,7 +949,7 @@ __global__ void __launch_bounds__(T, 1) k_convert(ConvK C, int dir)
     const int64_t poly = blockIdx.x;
     const int li = (int)(poly % C.n_limbs);
     const int pidx_ = C.lp[li];
-    const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
+    const PrimeK P = C.pr[pidx_];
     const uint64_t *in = C.in + (size_t)poly * N;
     uint64_t *out = C.out + (size_t)poly * N;
     uint64_t a[E];
@@ -770,7 +974,7 @@ __global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
     const int64_t poly = blockIdx.x;
     const int li = (int)(poly % C.n_limbs);
     const int pidx_ = C.lp[li];
-    const PrimeK P = pidx_ == 0 ? C.pr[0] : pidx_ == 1 ? C.pr[1] : C.pr[2];
+    const PrimeK P = C.pr[pidx_];
     uint64_t a[E];
     load_coef(a, C.in + (size_t)poly * N);
     fwd_rt(a, sm, P, pidx_);
@@ -787,10 +991,11 @@ namespace {
 
 struct DevCtx {
     int dev = -1;
-    ulonglong2 *tw = nullptr;  // [3][2][N]
+    ulonglong2 *tw = nullptr;  // [4][2][N]: q0, q1, P, q2 (f3)
     ulonglong2 *twf = nullptr; // q1 [2][N], FP64 form
-    PrimeK pr[3] = {};
+    PrimeK pr[4] = {};
     ulonglong2 pinv[2], q1inv;
+    ulonglong2 q2inv[2];       // f3: q2^-1 mod q0, q1
     uint64_t pmod[2];
 };
 
@@ -826,8 +1031,8 @@ int ctx_get(DevCtx **out)
     }
     DevCtx *C = new DevCtx;
     C->dev = dev;
-    std::vector<ulonglong2> h(6 * (size_t)N);
-    for (int i = 0; i < 3; i++) {
+    std::vector<ulonglong2> h(8 * (size_t)N);
+    for (int i = 0; i < 4; i++) {
         const HostPrime &H = host_prime(i);
         for (int k = 0; k < N; k++) {
             h[(size_t)(2 * i) * N + k] = shoup_pair(H.fwd[k], H.q);
@@ -865,7 +1070,7 @@ int ctx_get(DevCtx **out)
         P.ninvf = fpair(H.ninv);
         P.ninv_w1f = fpair(mulmod_h(H.ninv, H.inv[1], H.q));
     }
-    for (int i = 0; i < 3; i++) {
+    for (int i = 0; i < 4; i++) {
         const HostPrime &H = host_prime(i);
         PrimeK &P = C->pr[i];
         P.q = H.q;
@@ -884,6 +1089,7 @@ int ctx_get(DevCtx **out)
         C->pinv[l] = shoup_pair(powmod_d(QP % q, q - 2, q), q);
     }
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
+    for (int l = 0; l < 2; l++) C->q2inv[l] = shoup_pair(powmod_d(Q2 % C->pr[l].q, C->pr[l].q - 2, C->pr[l].q), C->pr[l].q);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
     cudaFuncSetAttribute(k_tensor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
@@ -892,6 +1098,9 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
+    cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
+    cudaFuncSetAttribute(k_rot1_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
+    cudaFuncSetAttribute(k_rot1_ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X3_SMEM_BYTES);
     set_smem(k_convert);
     set_smem(k_key_ntt);
     if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -937,6 +1146,14 @@ struct bm_pk_dev {
     uint8_t digest[32];
     ulonglong2 *pk;
 };
+struct bm_xk_dev {
+    int dev;
+    uint8_t digest[32];
+    int32_t d, p, s, log_p;
+    ulonglong2 *pk2;  // [2][3 limbs q0,q1,q2][N] level-2 public key
+    ulonglong2 *gk1;  // [log_p][2][2][3 limbs q0,q1,P][N], P^-1 in the Q limbs
+    ulonglong2 *mask; // [p][3 limbs q0,q1,q2][N], q2^-1 in the Q limbs
+};
 struct bm_evk_dev {
     int dev;
     uint8_t digest[32];
@@ -961,7 +1178,7 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     }
     cudaMemcpy(tmp, h, (size_t)n_polys * N * 8, cudaMemcpyHostToDevice);
     ConvK K;
-    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    for (int i = 0; i < 4; i++) K.pr[i] = C->pr[i];
     K.in = tmp;
     K.out = nullptr;
     K.n_limbs = n_limbs;
@@ -1068,13 +1285,16 @@ int bm_encrypt(const bm_params *prm, const bm_pk_dev *pk, const int64_t *d_pt, i
     int rc = ctx_get(&C);
     if (rc) return rc;
     EncK Ek;
-    Ek.pr[0] = C->pr[0];
-    Ek.pr[1] = C->pr[1];
+    for (int i = 0; i < 4; i++) Ek.pr[i] = C->pr[i];
     Ek.pk = pk->pk;
     Ek.pt = d_pt;
     Ek.out = d_out;
     Ek.first_obj = first_obj;
     Ek.seed = seed;
+    Ek.n_limbs = 2;
+    Ek.lp[0] = 0;
+    Ek.lp[1] = 1;
+    Ek.lp[2] = 3;
     k_encrypt<<<(unsigned)(2 * n_cts), T, SMEM_BYTES, (cudaStream_t)stream>>>(Ek);
     return launch_check();
 }
@@ -1120,19 +1340,19 @@ int bm_encrypt_query(const bm_params *prm, const bm_pk_dev *pk, const double *q,
 static int convert(const bm_params *prm, const uint64_t *in, int64_t n_cts, int32_t n_limbs, uint64_t *out,
                    void *stream, int dir)
 {
-    if (!prm || n_cts < 0 || (n_limbs != 1 && n_limbs != 2) || (n_cts && (!in || !out))) return BM_ERR_INVALID_ARG;
+    if (!prm || n_cts < 0 || n_limbs < 1 || n_limbs > 3 || (n_cts && (!in || !out))) return BM_ERR_INVALID_ARG;
     if (n_cts == 0) return BM_OK;
     DevCtx *C;
     int rc = ctx_get(&C);
     if (rc) return rc;
     ConvK K;
-    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    for (int i = 0; i < 4; i++) K.pr[i] = C->pr[i];
     K.in = in;
     K.out = out;
     K.n_limbs = n_limbs;
     K.lp[0] = 0;
     K.lp[1] = 1;
-    K.lp[2] = 2;
+    K.lp[2] = 3; // level-2 limb q2 (f3)
     k_convert<<<(unsigned)(n_cts * 2 * n_limbs), T, SMEM_BYTES, (cudaStream_t)stream>>>(K, dir);
     return launch_check();
 }
@@ -1146,6 +1366,156 @@ int bm_ct_from_coeff(const bm_params *prm, const uint64_t *d_in, int64_t n_cts, 
                      void *stream)
 {
     return convert(prm, d_in, n_cts, n_limbs, d_out, stream, 0);
+}
+
+// ------------------------------------------------------------------ f3: query expansion
+int bm_xk_to_device(const bm_params *prm, const bm_pk *pk, const bm_xk *xk, const int64_t *h_masks, bm_xk_dev **out)
+{
+    if (!prm || !pk || !xk || !h_masks || !out) return BM_ERR_INVALID_ARG;
+    if (memcmp(pk->digest, prm->digest, 32) || memcmp(xk->digest, prm->digest, 32) || xk->d != prm->d ||
+        xk->p != prm->p)
+        return BM_ERR_KEY_MISMATCH;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    bm_xk_dev *d = new bm_xk_dev;
+    d->dev = C->dev;
+    memcpy(d->digest, prm->digest, 32);
+    d->d = prm->d;
+    d->p = prm->p;
+    d->s = prm->s;
+    d->log_p = xk->log_p;
+    d->pk2 = d->gk1 = d->mask = nullptr;
+    // level-2 pk: pk's limbs q0, q1 and xk's q2 limb
+    std::vector<uint64_t> h(6 * (size_t)N);
+    for (int c = 0; c < 2; c++) {
+        memcpy(&h[(size_t)(c * 3 + 0) * N], &pk->v[(size_t)(c * 2 + 0) * N], 8 * (size_t)N);
+        memcpy(&h[(size_t)(c * 3 + 1) * N], &pk->v[(size_t)(c * 2 + 1) * N], 8 * (size_t)N);
+        memcpy(&h[(size_t)(c * 3 + 2) * N], &xk->pk_q2[(size_t)c * N], 8 * (size_t)N);
+    }
+    const int l2[3] = {0, 1, 3}, lk[3] = {0, 1, 2};
+    rc = upload_key_polys(C, h.data(), 6, 3, l2, &d->pk2);
+    // Galois keys: P^-1 folded into the Q limbs (the ModDown multiplies by it anyway)
+    const uint64_t sk[3] = {C->pinv[0].x, C->pinv[1].x, 1};
+    if (!rc && xk->log_p > 0) rc = upload_key_polys(C, xk->gk1.data(), 12 * (int64_t)xk->log_p, 3, lk, &d->gk1, sk);
+    // masks: integer plaintexts -> residues per limb, q2^-1 folded into the Q limbs
+    if (!rc) {
+        std::vector<uint64_t> m(3 * (size_t)prm->p * N);
+        const uint64_t qs[3] = {Q0, Q1, Q2};
+        for (int i = 0; i < prm->p; i++)
+            for (int l = 0; l < 3; l++)
+                for (int k = 0; k < N; k++) {
+                    const int64_t x = h_masks[(size_t)i * N + k];
+                    const uint64_t q = qs[l];
+                    m[((size_t)i * 3 + l) * N + k] = x >= 0 ? (uint64_t)x % q : q - 1 - (uint64_t)(-(x + 1)) % q;
+                }
+        const uint64_t sm[3] = {C->q2inv[0].x, C->q2inv[1].x, 1};
+        rc = upload_key_polys(C, m.data(), 3 * (int64_t)prm->p, 3, l2, &d->mask, sm);
+    }
+    if (rc) {
+        cudaFree(d->pk2);
+        cudaFree(d->gk1);
+        cudaFree(d->mask);
+        cudaGetLastError();
+        delete d;
+        return rc;
+    }
+    *out = d;
+    return BM_OK;
+}
+
+void bm_xk_dev_free(bm_xk_dev *d)
+{
+    if (!d) return;
+    cudaFree(d->pk2);
+    cudaFree(d->gk1);
+    cudaFree(d->mask);
+    delete d;
+}
+
+int bm_encrypt_l2(const bm_params *prm, const bm_xk_dev *xk, const int64_t *d_pt, int64_t n_cts, uint64_t first_obj,
+                  uint64_t seed, uint64_t *d_out, void *stream)
+{
+    if (!prm || !xk || n_cts < 0 || (n_cts > 0 && (!d_pt || !d_out))) return BM_ERR_INVALID_ARG;
+    if (memcmp(xk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (n_cts == 0) return BM_OK;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    EncK Ek;
+    for (int i = 0; i < 4; i++) Ek.pr[i] = C->pr[i];
+    Ek.pk = xk->pk2;
+    Ek.pt = d_pt;
+    Ek.out = d_out;
+    Ek.first_obj = first_obj;
+    Ek.seed = seed;
+    Ek.n_limbs = 3;
+    Ek.lp[0] = 0;
+    Ek.lp[1] = 1;
+    Ek.lp[2] = 3;
+    k_encrypt<<<(unsigned)(3 * n_cts), T, SMEM_BYTES, (cudaStream_t)stream>>>(Ek);
+    return launch_check();
+}
+
+static int64_t expand_chunk_cts(const bm_params *prm, int32_t nq)
+{
+    int64_t ch = 2048; // (query, part) outputs per launch: 6 N u64 of workspace each (768 MiB)
+    if (const char *e = getenv("BM_EXPAND_CHUNK")) {
+        long v = atol(e);
+        if (v > 0) ch = v;
+    }
+    ch = ch / prm->p * prm->p; // whole queries
+    if (ch < prm->p) ch = prm->p;
+    const int64_t total = (int64_t)nq * prm->p;
+    return total < ch ? total : ch;
+}
+
+size_t bm_expand_ws_bytes(const bm_params *prm, int32_t nq)
+{
+    if (!prm || nq <= 0) return 0;
+    return (size_t)expand_chunk_cts(prm, nq) * XU_POLYS * N * sizeof(uint64_t);
+}
+
+int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, int32_t nq, uint64_t *d_out, void *d_ws,
+              size_t ws_bytes, void *stream)
+{
+    if (!prm || !xk || nq < 0) return BM_ERR_INVALID_ARG;
+    if (memcmp(xk->digest, prm->digest, 32) || xk->p != prm->p || xk->d != prm->d) return BM_ERR_KEY_MISMATCH;
+    if (nq == 0) return BM_OK;
+    if (!d_in || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
+    if (ws_bytes < bm_expand_ws_bytes(prm, nq)) return BM_ERR_WORKSPACE;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    ExpK K;
+    for (int i = 0; i < 4; i++) K.pr[i] = C->pr[i];
+    K.pinv[0] = C->pinv[0];
+    K.pinv[1] = C->pinv[1];
+    K.q2inv[0] = C->q2inv[0];
+    K.q2inv[1] = C->q2inv[1];
+    K.mask = xk->mask;
+    K.XU = (uint64_t *)d_ws;
+    K.p = prm->p;
+    const int64_t ch = expand_chunk_cts(prm, nq), qch = ch / prm->p;
+    for (int64_t j0 = 0; j0 < nq && !rc; j0 += qch) {
+        const int64_t nqc = nq - j0 < qch ? nq - j0 : qch;
+        const unsigned ncb = (unsigned)(2 * nqc * prm->p);
+        K.in = d_in + (size_t)j0 * 6 * N;
+        K.out = d_out + (size_t)j0 * prm->p * 4 * N;
+        K.gk = nullptr;
+        K.g = 1;
+        k_exp_mask<<<ncb, T, X1_SMEM_BYTES, s>>>(K);
+        rc = launch_check();
+        for (int t = 0; t < xk->log_p && !rc; t++) {
+            K.gk = xk->gk1 + (size_t)t * 12 * N;
+            K.g = (uint32_t)powmod_d(5, (uint64_t)prm->s << t, 2 * N);
+            k_rot1_digits<<<ncb, T, X2_SMEM_BYTES, s>>>(K);
+            k_rot1_ks<<<ncb, T, X3_SMEM_BYTES, s>>>(K);
+            rc = launch_check();
+        }
+    }
+    return rc;
 }
 
 // ------------------------------------------------------------------ the scan

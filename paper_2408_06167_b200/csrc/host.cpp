@@ -58,7 +58,7 @@ static unsigned brev13_h(unsigned x)
     return r;
 }
 
-static HostPrime g_primes[3];
+static HostPrime g_primes[4];
 static uint64_t g_cdt[19];
 static std::once_flag g_once;
 
@@ -78,8 +78,8 @@ static void make_cdt()
 
 static void init_tables()
 {
-    const uint64_t Qs[3] = {Q0, Q1, QP};
-    for (int i = 0; i < 3; i++) {
+    const uint64_t Qs[4] = {Q0, Q1, QP, Q2};
+    for (int i = 0; i < 4; i++) {
         HostPrime &H = g_primes[i];
         H.q = Qs[i];
         // psi: the first g^((q-1)/2N), g = 3, 5, 7, ..., with psi^N = -1 (order exactly 2N)
@@ -214,7 +214,7 @@ int bm_params_init(bm_params *o, int32_t d, int32_t p)
 {
     if (!o) return BM_ERR_INVALID_ARG;
     if (!pow2(d) || !pow2(p) || p > d || d > SLOTS) return BM_ERR_INVALID_LAYOUT;
-    const uint64_t Qs[3] = {Q0, Q1, QP};
+    const uint64_t Qs[4] = {Q0, Q1, QP, Q2};
     for (uint64_t q : Qs)
         if (!is_prime_h(q) || (q - 1) % (2 * N) != 0) return BM_ERR_INVALID_PRIME;
     // HE-standard 128-bit classical bound at N = 8192: log2(PQ) <= 218
@@ -235,6 +235,7 @@ int bm_params_init(bm_params *o, int32_t d, int32_t p)
     o->q[2] = QP;
     o->scale = std::ldexp(1.0, 40);
     o->out_scale = std::ldexp(1.0, 80) / (double)Q1;
+    o->q2 = Q2;
     make_digest(o->digest);
     host_prime(0); // build tables once
     return BM_OK;
@@ -348,6 +349,94 @@ int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **skp, bm_pk **pkp, bm_
     return BM_OK;
 }
 
+static bool canonical(const uint64_t *v, size_t n_polys, const int *limb_primes, int n_limbs);
+
+// f3 expansion keys (reading R26).  pk limb q2: (-a s + e, a) with pk's error (P_PK_E,
+// object 0) and a from (P_PK_A, object 0, sub-stream 3).  Level-1 Galois key of the left rotation
+// by r = s 2^t, digit j: over {q0, q1, P}, (-a s + e + [l = j] (P mod q_l) sigma_{5^r}(s), a) with
+// a from (P_GK1_A, object 2r + j, sub-stream l) and e from (P_GK1_E, object 2r + j).
+int bm_xk_keygen(const bm_params *prm, uint64_t seed, bm_xk **out)
+{
+    if (!prm || !out) return BM_ERR_INVALID_ARG;
+    const uint64_t Qs[3] = {Q0, Q1, QP};
+    bm_xk *x = new (std::nothrow) bm_xk;
+    if (!x) return BM_ERR_OOM;
+    memcpy(x->digest, prm->digest, 32);
+    x->d = prm->d;
+    x->p = prm->p;
+    x->log_p = 0;
+    while ((1 << x->log_p) < prm->p) x->log_p++;
+    std::vector<int64_t> sv(N), ev(N);
+    std::vector<uint64_t> s(N), e(N), a(N), t(N), sg(N);
+    sample_small(seed, P_SK, 0, 0, sv.data());
+    // pk limb q2
+    x->pk_q2.assign(2 * (size_t)N, 0);
+    sample_small(seed, P_PK_E, 0, 1, ev.data());
+    for (int k = 0; k < N; k++) s[k] = to_res(sv[k], Q2), e[k] = to_res(ev[k], Q2);
+    sample_uniform(seed, P_PK_A, 0, 3, Q2, a.data());
+    poly_mul_h(a.data(), s.data(), t.data(), 3);
+    for (int k = 0; k < N; k++) x->pk_q2[k] = (e[k] + Q2 - t[k]) % Q2, x->pk_q2[N + k] = a[k];
+    // level-1 Galois keys
+    x->gk1.assign((size_t)x->log_p * 12 * N, 0);
+    for (int tt = 0; tt < x->log_p; tt++) {
+        const uint64_t r = (uint64_t)prm->s << tt, g = powmod_h(5, r, 2 * N);
+        for (int j = 0; j < 2; j++) {
+            const uint64_t obj = 2 * r + (uint64_t)j;
+            sample_small(seed, P_GK1_E, obj, 1, ev.data());
+            for (int l = 0; l < 3; l++) {
+                const uint64_t q = Qs[l];
+                for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
+                sample_uniform(seed, P_GK1_A, obj, (uint32_t)l, q, a.data());
+                poly_mul_h(a.data(), s.data(), t.data(), l);
+                uint64_t *b = &x->gk1[((((size_t)tt * 2 + j) * 2 + 0) * 3 + l) * N];
+                uint64_t *aa = &x->gk1[((((size_t)tt * 2 + j) * 2 + 1) * 3 + l) * N];
+                for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
+                if (l == j) {
+                    std::fill(sg.begin(), sg.end(), 0);
+                    for (int k = 0; k < N; k++) {
+                        uint64_t y = (uint64_t)k * g % (2 * N);
+                        if (y < (uint64_t)N) sg[y] = s[k];
+                        else sg[y - N] = (q - s[k]) % q;
+                    }
+                    const uint64_t pm = QP % q;
+                    for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(sg[k], pm, q)) % q;
+                }
+            }
+        }
+    }
+    *out = x;
+    return BM_OK;
+}
+void bm_xk_free(bm_xk *x) { delete x; }
+int bm_xk_export(const bm_xk *x, uint64_t *pk_q2, uint64_t *gk1, int32_t *n_rot)
+{
+    if (!x) return BM_ERR_INVALID_ARG;
+    if (pk_q2) memcpy(pk_q2, x->pk_q2.data(), x->pk_q2.size() * 8);
+    if (gk1) memcpy(gk1, x->gk1.data(), x->gk1.size() * 8);
+    if (n_rot) *n_rot = x->log_p;
+    return BM_OK;
+}
+int bm_xk_import(const bm_params *prm, const uint64_t *pk_q2, const uint64_t *gk1, int32_t n_rot, bm_xk **out)
+{
+    if (!prm || !pk_q2 || (!gk1 && n_rot > 0) || !out) return BM_ERR_INVALID_ARG;
+    int log_p = 0;
+    while ((1 << log_p) < prm->p) log_p++;
+    if (n_rot != log_p) return BM_ERR_MISSING_ROTATION_KEY;
+    const int pq2[1] = {3}, pk3[3] = {0, 1, 2};
+    if (!canonical(pk_q2, 2, pq2, 1) || (n_rot && !canonical(gk1, (size_t)n_rot * 12, pk3, 3)))
+        return BM_ERR_INVALID_ARG;
+    bm_xk *x = new (std::nothrow) bm_xk;
+    if (!x) return BM_ERR_OOM;
+    memcpy(x->digest, prm->digest, 32);
+    x->d = prm->d;
+    x->p = prm->p;
+    x->log_p = log_p;
+    x->pk_q2.assign(pk_q2, pk_q2 + 2 * (size_t)N);
+    x->gk1.assign(gk1, gk1 + (size_t)n_rot * 12 * N);
+    *out = x;
+    return BM_OK;
+}
+
 void bm_sk_free(bm_sk *x) { delete x; }
 void bm_pk_free(bm_pk *x) { delete x; }
 void bm_evk_free(bm_evk *x) { delete x; }
@@ -458,13 +547,13 @@ static const std::vector<int> &slot_exp()
     return e;
 }
 
-static int encode_slots(const double *z, int64_t *pt)
+static int encode_slots(const double *z, int64_t *pt, double delta = 1099511627776.0 /* 2^40 */)
 {
     const std::vector<int> &e = slot_exp();
     std::vector<std::complex<double>> X(2 * N);
     for (int j = 0; j < SLOTS; j++) X[e[j]] = z[j];
     fft_pos(X);
-    const double scale = std::ldexp(1.0, 40) * 2.0 / N;
+    const double scale = delta * 2.0 / N;
     for (int k = 0; k < N; k++) {
         double v = scale * X[k].real();
         if (!std::isfinite(v) || std::fabs(v) > 9.0e18) return BM_ERR_MAGNITUDE;
@@ -532,6 +621,39 @@ int bm_encode_query(const bm_params *prm, const double *q, int64_t nq, int64_t *
             int rc = encode_slots(z.data(), pt + ((size_t)j * p + i) * N);
             if (rc) return rc;
         }
+    return BM_OK;
+}
+
+// f3: the client's single query ciphertext holds the unit query tiled S/d times,
+// encoded at 2^40; the expansion masks X_i[x] = [(x mod d) in [i s, (i+1) s)]
+// are encoded at scale q2, so that Res by q2 leaves the expanded parts at scale exactly 2^40.
+int bm_encode_query_tiled(const bm_params *prm, const double *q, int64_t nq, int64_t *pt)
+{
+    if (!prm || (!q && nq > 0) || !pt || nq < 0) return BM_ERR_INVALID_ARG;
+    const int d = prm->d;
+    std::vector<double> unit;
+    if (nq) {
+        int rc = unit_rows(q, nq, d, unit);
+        if (rc) return rc;
+    }
+    std::vector<double> z(SLOTS);
+    for (int64_t j = 0; j < nq; j++) {
+        for (int x = 0; x < SLOTS; x++) z[x] = unit[j * d + (x % d)];
+        int rc = encode_slots(z.data(), pt + (size_t)j * N);
+        if (rc) return rc;
+    }
+    return BM_OK;
+}
+int bm_encode_masks(const bm_params *prm, int64_t *pt)
+{
+    if (!prm || !pt) return BM_ERR_INVALID_ARG;
+    const int d = prm->d, s = prm->s;
+    std::vector<double> z(SLOTS);
+    for (int i = 0; i < prm->p; i++) {
+        for (int x = 0; x < SLOTS; x++) z[x] = ((x % d) >= i * s && (x % d) < (i + 1) * s) ? 1.0 : 0.0;
+        int rc = encode_slots(z.data(), pt + (size_t)i * N, (double)Q2);
+        if (rc) return rc;
+    }
     return BM_OK;
 }
 

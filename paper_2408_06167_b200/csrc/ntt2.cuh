@@ -19,6 +19,9 @@ template <int PI> struct PrimeC;
 template <> struct PrimeC<0> { static constexpr uint64_t q = Q0; };
 template <> struct PrimeC<1> { static constexpr uint64_t q = Q1; };
 template <> struct PrimeC<2> { static constexpr uint64_t q = QP; };
+template <> struct PrimeC<3> { static constexpr uint64_t q = Q2; }; // f3 only
+// the 40-bit primes (q1, q2) share the lazy-reduction schedule: never reduced inside a transform
+template <int PI> constexpr bool Q40 = (PI == 1 || PI == 3);
 
 // Q q mod 2^64
 template <int PI> BM_D uint64_t mul_q(uint64_t Q)
@@ -79,14 +82,14 @@ template <int PI> BM_D uint64_t reduce_full(uint64_t x, uint64_t one_p)
     return r >= q ? r - q : r;
 }
 
-// exact x mod q for the bounded x the NTT produces (any x < 2^64 for q0 and P, x < 2^62 for q1):
-// q = 2^k - c with 0 < c < 2^18, so Qe = x >> k under-estimates floor(x / q) by at most 1
-// (x / q - x / 2^k = x c / (2^k q) < 1 for these bounds) and x - Qe q lies in [0, 2q).
+// exact x mod q for the bounded x the NTT produces (any x < 2^64 for q0 and P, x < 2^62 for q1,
+// x < 2^60 for q2): q = 2^k - c with 0 < c < 2^20, so Qe = x >> k under-estimates floor(x / q) by
+// at most 1 (x / q - x / 2^k = x c / (2^k q) < 1 for these bounds) and x - Qe q lies in [0, 2q).
 template <int PI> BM_D uint64_t reduce_bnd(uint64_t x)
 {
-    constexpr int k = PI == 0 ? 58 : PI == 1 ? 40 : 60;
+    constexpr int k = PI == 0 ? 58 : Q40<PI> ? 40 : 60;
     constexpr uint64_t q = PrimeC<PI>::q;
-    constexpr uint64_t c = (1ull << k) - q; // 835583, 147455, 16383
+    constexpr uint64_t c = (1ull << k) - q; // 835583, 147455, 16383, 737279
     const uint64_t Qe = x >> k;
     const uint64_t r = x - (Qe << k) + Qe * c;
     return r >= q ? r - q : r;
@@ -96,7 +99,7 @@ template <int PI> BM_D uint64_t reduce_bnd(uint64_t x)
 // reduce_bnd without its final conditional subtraction (the lazy reductions of ntt3.cuh)
 template <int PI> BM_D uint64_t reduce_lazy(uint64_t x)
 {
-    static_assert(PI != 1, "q1 transforms never reduce inside");
+    static_assert(!Q40<PI>, "q1 / q2 transforms never reduce inside");
     constexpr int k = PI == 0 ? 58 : 60;
     constexpr uint32_t c = (uint32_t)((1ull << k) - PrimeC<PI>::q); // 835583, 16383
     const uint32_t Qe = (uint32_t)(x >> k);                         // <= 63 / 15
@@ -178,9 +181,9 @@ template <int PI> BM_D void ct4s(uint64_t &x, uint64_t &y, ulonglong2 w, int s)
 template <int PI, int ST> BM_D void gs4(uint64_t &x, uint64_t &y, ulonglong2 w)
 {
     constexpr uint64_t q = PrimeC<PI>::q;
-    constexpr uint64_t B = PI == 1 ? (4ull << ST) : 4ull;
+    constexpr uint64_t B = Q40<PI> ? (4ull << ST) : 4ull;
     uint64_t X = x + y;
-    if (PI != 1) X = X >= 4 * q ? X - 4 * q : X; // q0, P: keep [0, 4q)
+    if (!Q40<PI>) X = X >= 4 * q ? X - 4 * q : X; // q0, P: keep [0, 4q)
     const uint64_t T = x - y + (uint64_t)B * q;
     x = X;
     y = shoup4<PI>(T, w);
@@ -195,10 +198,10 @@ template <int PI, int ST> BM_D void gs4(uint64_t &x, uint64_t &y, ulonglong2 w)
 template <int PI, int ST> BM_D void gs4s(uint64_t &x, uint64_t &y, ulonglong2 w)
 {
     constexpr uint64_t q = PrimeC<PI>::q;
-    constexpr uint64_t B = PI == 1 ? (4ull << ST) : PI == 0 ? (4ull << (ST % 4)) : (4ull << (ST % 2));
+    constexpr uint64_t B = Q40<PI> ? (4ull << ST) : PI == 0 ? (4ull << (ST % 4)) : (4ull << (ST % 2));
     constexpr bool RED = PI == 0 ? (ST % 4 == 3) : PI == 2 ? (ST % 2 == 1) : false;
     uint64_t X = x + y;
-    if (RED) X = reduce_lazy<PI == 1 ? 0 : PI>(X);
+    if (RED) X = reduce_lazy<Q40<PI> ? 0 : PI>(X);
     const uint64_t T = x - y + B * q;
     x = X;
     y = shoup4<PI>(T, w);
@@ -264,7 +267,7 @@ template <int PI> BM_D void ntt_inv2(uint64_t a[32], uint64_t *sm, const PrimeK 
     }
     // last stage (s = 0) with N^-1 folded in; inputs < inv_bound(12) q
     constexpr uint64_t q = PrimeC<PI>::q;
-    constexpr uint64_t Bq = (PI == 1 ? (4ull << 12) : 4ull) * q;
+    constexpr uint64_t Bq = (Q40<PI> ? (4ull << 12) : 4ull) * q;
 #pragma unroll
     for (int k = 0; k < 16; k++) {
         const uint64_t x = a[k], y = a[k + 16];

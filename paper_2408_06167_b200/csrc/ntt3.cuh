@@ -107,12 +107,12 @@ template <int PI, bool CANON = true> BM_D void fwd(uint64_t a[E], uint64_t *sm, 
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
         ct4s<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd), 12);
-        if (CANON || PI == 1) {
+        if (CANON || Q40<PI>) {
             a[2 * m] = reduce_bnd<PI>(x);
             a[2 * m + 1] = reduce_bnd<PI>(y);
         } else {
-            a[2 * m] = reduce_lazy<PI == 1 ? 0 : PI>(x);
-            a[2 * m + 1] = reduce_lazy<PI == 1 ? 0 : PI>(y);
+            a[2 * m] = reduce_lazy<Q40<PI> ? 0 : PI>(x);
+            a[2 * m + 1] = reduce_lazy<Q40<PI> ? 0 : PI>(y);
         }
     }
 }
@@ -183,7 +183,7 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
         }
     }
     // s = 0 with N^-1 folded in; inputs < B q with B of stage 12
-    constexpr uint64_t Bq = (PI == 1 ? (4ull << 12) : 4ull) * PrimeC<PI>::q;
+    constexpr uint64_t Bq = (Q40<PI> ? (4ull << 12) : 4ull) * PrimeC<PI>::q;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const uint64_t x = a[k], y = a[k + 8];
@@ -196,13 +196,15 @@ BM_D void fwd_rt(uint64_t a[E], uint64_t *sm, const PrimeK &P, int pi)
 {
     if (pi == 0) fwd<0>(a, sm, P);
     else if (pi == 1) fwd<1>(a, sm, P);
-    else fwd<2>(a, sm, P);
+    else if (pi == 2) fwd<2>(a, sm, P);
+    else fwd<3>(a, sm, P);
 }
 BM_D void inv_rt(uint64_t a[E], uint64_t *sm, const PrimeK &P, int pi)
 {
     if (pi == 0) inv<0>(a, sm, P);
     else if (pi == 1) inv<1>(a, sm, P);
-    else inv<2>(a, sm, P);
+    else if (pi == 2) inv<2>(a, sm, P);
+    else inv<3>(a, sm, P);
 }
 
 // ------------------------------------------------------------------ global <-> register helpers

@@ -137,3 +137,37 @@ def test_device_calls_fail_loudly_without_gpu(B):
     with pytest.raises(B.BMError) as e:
         B.bm_evk_to_device(prm, evk)
     assert e.value.name == "BM_ERR_CUDA"
+
+
+# ----------------------------------------------------------------------------- f3 host side
+@pytest.mark.parametrize("d,p", [(128, 8), (16, 1)])
+def test_expansion_keys_match_oracle(B, O, d, p):
+    """f3: the product's expansion keys (pk limb q2, level-1 Galois keys of strides s 2^t) equal
+    the oracle's bit for bit (independent implementations of reading R26)."""
+    prm = B.bm_params_init(d, p)
+    assert prm.q2 == O.q2()
+    xk = B.bm_xk_keygen(prm, 4242)
+    pk_q2, gk1 = B.bm_xk_export(xk)
+    opk_q2, ogk1 = O.keygen_exp(13, 4242, d, p)
+    assert np.array_equal(pk_q2, opk_q2)
+    assert gk1.shape == ogk1.shape and np.array_equal(gk1, ogk1)
+    xk2 = B.bm_xk_import(prm, pk_q2, gk1)
+    a, b = B.bm_xk_export(xk2)
+    assert np.array_equal(a, pk_q2) and np.array_equal(b, gk1)
+    bad = pk_q2.copy()
+    bad[0, 0] = prm.q2
+    with pytest.raises(B.BMError):
+        B.bm_xk_import(prm, bad, gk1)
+
+
+def test_expansion_encoders_within_one_of_oracle(B, O):
+    """f3 client encoders: the tiled query (scale 2^40) and the masks X_i (scale q2) agree with the
+    oracle's encoder up to half-way FP roundings (reading R15)."""
+    prm = B.bm_params_init(128, 8)
+    Q, _ = I.queries(2, 6)
+    pq = B.bm_encode_query_tiled(prm, Q)
+    oq = O.encode(O.tile_query(Q, 13, 128), 13)
+    assert np.abs(pq - oq).max() <= 1 and (pq != oq).mean() < 1e-3
+    pm = B.bm_encode_masks(prm)
+    om = O.expand_masks(13, 128, 8)
+    assert np.abs(pm - om).max() <= 1 and (pm != om).mean() < 1e-3

@@ -1,0 +1,142 @@
+"""GPU parity of f3: server-side query expansion, Algorithm 1,
+on the chain extended by q2 (readings R24-R26).  The sm_100a path (bm_encrypt_l2,
+bm_expand, through the C ABI) against the CPU oracle, bit-exact on every RNS residue of the
+coefficient-domain outputs, given identical keys (tests/test_abi.py pins the host key generator
+to the oracle's), mask plaintexts (encoded by the oracle) and encryption randomness."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2408_06167_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+LOGN = 13
+NTH = max(1, min(16, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the GPU tests need a B200 (there is no CPU fallback)")
+    from paper_2408_06167_b200 import build
+    build.build(verbose=False)
+    from paper_2408_06167_b200 import bm
+    return torch, bm
+
+
+class XSetup:
+    def __init__(self, env, O, d, p, Q, key_seed=1, q_seed=3):
+        torch, B = env
+        self.torch, self.B, self.O, self.d, self.p = torch, B, O, d, p
+        self.prm = B.bm_params_init(d, p)
+        self.sk, self.pk, self.evk = B.bm_keygen(self.prm, key_seed)
+        self.xk = B.bm_xk_keygen(self.prm, key_seed)
+        self.osk, self.opk, self.orlk, self.ogk = O.keygen(LOGN, key_seed, O.n_rot_for(d, p))
+        self.opk_q2, self.ogk1 = O.keygen_exp(LOGN, key_seed, d, p)
+        self.masks = O.expand_masks(LOGN, d, p)
+        self.xk_dev = B.bm_xk_to_device(self.prm, self.pk, self.xk, self.masks)
+        self.q_pt = O.encode(O.tile_query(Q, LOGN, d), LOGN)
+        self.nq = Q.shape[0]
+        self.q_seed = q_seed
+        self.oct = O.encrypt_l2(LOGN, self.opk, self.opk_q2, self.q_pt, 0, q_seed)   # [nq][2][3][N]
+
+    def gpu_encrypt_l2(self):
+        torch, B = self.torch, self.B
+        out = torch.empty((self.nq, 2, 3, 8192), dtype=torch.int64, device="cuda")
+        B.bm_encrypt_l2(self.prm, self.xk_dev, torch.from_numpy(self.q_pt).cuda(), 0, self.q_seed, out)
+        return out
+
+    def gpu_expand(self, d_in):
+        torch, B = self.torch, self.B
+        out = torch.empty((self.nq, self.p, 2, 2, 8192), dtype=torch.int64, device="cuda")
+        ws = torch.empty(max(1, B.bm_expand_ws_bytes(self.prm, self.nq)), dtype=torch.uint8, device="cuda")
+        B.bm_expand(self.prm, self.xk_dev, d_in, self.nq, out, ws)
+        return out
+
+    def to_coeff(self, d, n_limbs):
+        c = self.torch.empty_like(d)
+        self.B.bm_ct_to_coeff(self.prm, d, n_limbs, c)
+        self.B.bm_sync()
+        return c.cpu().numpy().view(np.uint64)
+
+    def from_oracle(self, ct, n_limbs):
+        t = self.torch.from_numpy(np.ascontiguousarray(ct).view(np.int64)).cuda()
+        out = self.torch.empty_like(t)
+        self.B.bm_ct_from_coeff(self.prm, t, n_limbs, out)
+        return out
+
+
+def test_encrypt_l2_parity(env, O):
+    """Level-2 pk-encryption of the tiled query on the GPU == oracle (all three limbs); its q0, q1
+    limbs equal the level-1 encryption of the same plaintext (same streams)."""
+    torch, B = env
+    Q = I.random_unit(3, 128, 11)
+    st = XSetup(env, O, 128, 8, Q)
+    d2 = st.gpu_encrypt_l2()
+    got = st.to_coeff(d2, 3)
+    assert np.array_equal(got, st.oct)
+    back = torch.empty_like(d2)
+    B.bm_ct_from_coeff(st.prm, torch.from_numpy(got.view(np.int64)).cuda(), 3, back)
+    B.bm_sync()
+    assert torch.equal(back, d2)
+
+
+@pytest.mark.parametrize("d,p,nq", [(128, 8, 3), (16, 4, 2), (32, 2, 2), (64, 1, 2), (512, 16, 1)])
+def test_expand_parity(env, O, d, p, nq):
+    """bm_expand == or_expand bit for bit (every residue of every expanded part)."""
+    Q = I.random_unit(nq, d, 20 + p)
+    st = XSetup(env, O, d, p, Q)
+    got = st.to_coeff(st.gpu_expand(st.from_oracle(st.oct, 3)), 2)
+    exp = O.expand(LOGN, d, p, st.masks, st.ogk1, st.oct)
+    assert np.array_equal(got, exp)
+
+
+def test_expand_chunked_equals_unchunked(env, O):
+    """Several launches (BM_EXPAND_CHUNK = 8 parts = one query per chunk) give the same residues."""
+    Q = I.random_unit(3, 64, 5)
+    st = XSetup(env, O, 64, 8, Q)
+    d_in = st.from_oracle(st.oct, 3)
+    whole = st.to_coeff(st.gpu_expand(d_in), 2)
+    os.environ["BM_EXPAND_CHUNK"] = "8"
+    try:
+        parts = st.to_coeff(st.gpu_expand(d_in), 2)
+    finally:
+        del os.environ["BM_EXPAND_CHUNK"]
+    assert np.array_equal(whole, parts)
+    assert np.array_equal(whole[2], O.expand(LOGN, 64, 8, st.masks, st.ogk1, st.oct[2:3])[0])
+
+
+def test_expanded_query_scan_end_to_end(env, O):
+    """f3 + the hot path: Enc_l2(tiled query) on the GPU -> bm_expand -> bm_match gives, bit for bit,
+    the oracle's Algorithm 1 -> Algorithm 2 residues, decrypting to the plaintext cosines (1e-6) and
+    top-1 = 17 on configs[0]'s data at p = 4."""
+    torch, B = env
+    d, p = 16, 4
+    T = I.templates(1)
+    Q, _ = I.queries(1)
+    st = XSetup(env, O, d, p, Q)
+    S, s, Bk = O.layout(LOGN, d, p)
+    n_sets = -(-T.shape[0] // Bk)
+    db_pt = O.encode(O.pack_db(T, LOGN, d, p, 0, n_sets).reshape(-1, S), LOGN)
+    pk_dev = B.bm_pk_to_device(st.prm, st.pk)
+    evk_dev = B.bm_evk_to_device(st.prm, st.evk)
+    d_db = torch.empty((n_sets, p, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    B.bm_encrypt(st.prm, pk_dev, torch.from_numpy(db_pt).cuda(), 0, 2, d_db)
+    d_qx = st.gpu_expand(st.gpu_encrypt_l2())
+    out = torch.empty((1, n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_match_ws_bytes(st.prm, n_sets, 1, 0), dtype=torch.uint8, device="cuda")
+    B.bm_match(st.prm, evk_dev, d_db, n_sets, d_qx, 1, out, ws, 0)
+    B.bm_sync()
+    got = out.cpu().numpy().view(np.uint64)
+    # oracle: the same pipeline
+    odb = O.encrypt(LOGN, st.opk, db_pt, 0, 2).reshape(n_sets, p, 2, 2, -1)
+    oqx = O.expand(LOGN, d, p, st.masks, st.ogk1, st.oct)
+    ref, _ = O.match(LOGN, d, p, 0, st.orlk, st.ogk, odb, oqx, n_threads=NTH)
+    assert np.array_equal(got.reshape(-1, 2, 8192), ref.reshape(-1, 2, 8192))
+    sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(-1)[:T.shape[0]]
+    cos = T @ Q[0]
+    assert np.abs(sc - cos).max() < 1e-6
+    assert B.bm_top1(sc)[0] == 17 == int(np.argmax(cos))
