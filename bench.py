@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--order", type=int, default=0)
+    ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion leg")
     ap.add_argument("--nq", type=int, default=384)
     ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -313,6 +314,13 @@ def run_ours(args):
                "h2d_bytes_per_step": int(h_q.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
                "ms_per_step": round(e2e_ms, 3), "note": "per rank: query cts H2D + results D2H, wall clock"}
 
+    # f3: server-side query expansion (Algorithm 1) of the same batch -- the client
+    # uploads ONE level-2 ciphertext per query (the chain extended by q2) and bm_expand produces the p
+    # level-1 parts bm_match takes.  Device time of the expansion alone and of expansion + scan.
+    f3 = None
+    if world == 1 and not args.no_f3:
+        f3 = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_step, tq_per_step, stream)
+
     # CPU oracle on the host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -335,12 +343,71 @@ def run_ours(args):
                        "ring_N": N_RING, "parallelism": f"db-shard{world}",
                        "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
                            nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "f3_expand": f3,
+            "gpu_launches": int(launches * args.steps),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def f3_modmuls(p, s):
+    """Algorithmic modmuls of Algorithm 1 per expanded part (one (query, part) output): Mul(P) + Res
+    (2 comps x (INTT_q2, NTT_q0, NTT_q1) + 3 mask products + 2 q2^-1 folds per coefficient) and
+    log2(p) level-1 rotations (digits: 2 INTT + 4 ModUp NTT; per comp INTT_P + NTT_q0 + NTT_q1,
+    6 key products + 2 P^-1 folds per coefficient)."""
+    n = N_RING
+    log_p = p.bit_length() - 1
+    return 2 * (3 * BFLY + 5 * n) + log_p * (12 * BFLY + 16 * n)
+
+
+def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_scan, tq_per_step, stream):
+    from paper_2408_06167_b200 import inputs as I
+    p, nq = prm.p, d_q.shape[0]
+    dev = d_q.device
+    xk = B.bm_xk_keygen(prm, 1)
+    xk_dev = B.bm_xk_to_device(prm, pk, xk)
+    Q, _ = I.queries(CFG, nq)
+    d_pt = torch.from_numpy(B.bm_encode_query_tiled(prm, Q)).to(dev)
+    d_l2 = torch.empty((nq, 2, 3, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_l2(prm, xk_dev, d_pt, 0, 3, d_l2)
+    del d_pt
+    d_qx = torch.empty_like(d_q)
+    ws = torch.empty(B.bm_expand_ws_bytes(prm, nq), dtype=torch.uint8, device=dev)
+    for _ in range(max(2, args.warmup)):
+        B.bm_expand(prm, xk_dev, d_l2, nq, d_qx, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        B.bm_expand(prm, xk_dev, d_l2, nq, d_qx, ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    del ws
+    # sanity: the expanded queries scan to the same scores as the client-expanded ones (different noise)
+    k = min(4, nq)
+    out_x = torch.empty((k, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
+    ws2 = torch.empty(B.bm_match_ws_bytes(prm, n_sets, k, 0), dtype=torch.uint8, device=dev)
+    B.bm_match(prm, evk_dev, d_db, n_sets, d_qx[:k].contiguous(), k, out_x, ws2, 0)
+    B.bm_sync()
+    sa = B.bm_decrypt(prm, sk, out_x.cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
+    sb = B.bm_decrypt(prm, sk, d_out[:k].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
+    err = float(np.abs(sa - sb).max())
+    assert err < 1e-5, err
+    mm = f3_modmuls(p, prm.s) * nq * p
+    f_peak = 1965.0e6
+    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / IMAD_SLOTS_PER_MODMUL / 1e9
+    return {"queries": nq, "ms_per_batch": round(ms, 4), "queries_per_s": round(nq / (ms / 1e3), 1),
+            "gmodmul_s": round(mm / (ms / 1e3) / 1e9, 2), "alu_frac": round(mm / (ms / 1e3) / 1e9 / peak, 4),
+            "kernel_launches": 1 + 2 * (p.bit_length() - 1),
+            "upload_bytes_per_query": {"client_expanded": p * 4 * N_RING * 8, "server_expanded": 6 * N_RING * 8},
+            "expand_plus_scan": {"ms_per_step": round(ms + ms_scan, 4),
+                                 "value": round(tq_per_step / ((ms + ms_scan) / 1e3), 1),
+                                 "unit": "templates*queries/s"},
+            "score_check_max_abs_diff": err,
+            "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24)"}
 
 
 def run_reference(args):
