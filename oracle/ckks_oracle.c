@@ -813,8 +813,9 @@ int or_match(int logN, int d, int p, int order, const uint64_t *rlk, const uint6
 /* Layouts (coefficient domain):
  *   ct level 2   [2 comps][3 limbs q0,q1,q2][N]
  *   pk_q2        [2 comps (b,a)][N]: the q2 limb of the public key (its q0, q1 limbs are pk's)
- *   gk1          [log2 p][2 digits j][2 comps (b,a)][3 limbs q0,q1,P][N]; entry t is the
- *                level-1 Galois key of the left rotation by s 2^t
+ *   gk1          [n_rot][2 digits j][2 comps (b,a)][3 limbs q0,q1,P][N]; entry t is the
+ *                level-1 Galois key of the left rotation by s 2^t (n_rot = log2 p for the
+ *                expansion, log2 B for the enrollment, which uses the same family)
  *   masks        [p][N] int64 plaintexts of X_i at scale q2 (encoded by the caller)           */
 enum { P_GK1_A = 11, P_GK1_E = 12 };
 
@@ -860,9 +861,9 @@ static const ring_t *l2_R(const ctx2_t *x, int l) { return l == 2 ? &x->R2 : &x-
  * gk1 for rotation r = s 2^t, digit j in {0,1}: over {q0,q1,P},
  *   b = -a s + e + [l = j] (P mod q_l) sigma_{5^r}(s) in limb q_l,   b = -a s + e in limb P,
  * a from (P_GK1_A, object 2r + j, sub-stream l), e from (P_GK1_E, object 2r + j). */
-int or_keygen_exp(int logN, uint64_t seed, int d, int p, int zero_error, uint64_t *pk_q2, uint64_t *gk1)
+int or_keygen_exp(int logN, uint64_t seed, int d, int p, int n_rot, int zero_error, uint64_t *pk_q2, uint64_t *gk1)
 {
-    if (p <= 0 || d % p) return -1;
+    if (p <= 0 || d % p || n_rot < 0) return -1;
     ctx2_t X;
     ctx2_init(&X, logN);
     const ctx_t *C = &X.c;
@@ -882,10 +883,9 @@ int or_keygen_exp(int logN, uint64_t seed, int d, int p, int zero_error, uint64_
     poly_sub(X.q2, N, e, tmp, pk_q2);
     memcpy(pk_q2 + N, a, sizeof(uint64_t) * N);
 
-    /* level-1 Galois keys */
-    int log_p = 0;
-    while ((1 << log_p) < p) log_p++;
-    for (int t = 0; t < log_p; t++) {
+    /* level-1 Galois keys of the strides s 2^t, t < n_rot (expansion: t < log2 p; enrollment:
+     * t < log2 B, reading R27) */
+    for (int t = 0; t < n_rot; t++) {
         const uint64_t r = (uint64_t)s << t, g = galois_elt(N, r);
         for (int j = 0; j < 2; j++) {
             const uint64_t obj = 2 * r + (uint64_t)j;
@@ -1061,6 +1061,48 @@ int or_expand(int logN, int d, int p, const int64_t *masks, const uint64_t *gk1,
             }
         }
     free(rot);
+    ctx2_free(&X);
+    return 0;
+}
+
+/* ================================================================== */
+/* f4: server-side enrollment packing, Fig. 3 /    */
+/* PAPER.md:251-269, on the same extended chain      */
+/* ================================================================== */
+/* The client encrypts the unit template in slots [0, d) (zeros elsewhere) at level 2.  For each
+ * part i, with template index u = tB + k:
+ *   C = Res(Mul(P)(C_u, E_i)),  E_i[x] = [x in [i s, (i+1) s)] at scale q2,
+ *   C = Rot_right(C, (k - i) s) = Rot_left(C, m s), m = (i - k) mod B, done as the left rotations
+ *       by s 2^t for the set bits t of m, ascending (reading R27),
+ *   set[t][i] += C.
+ * in [n][2][3][N] (templates first_u .. first_u + n - 1), emasks [p][N], gk1 [log2 B] keys,
+ * db [n_sets][p][2][2][N] level 1 (accumulated; sets indexed from 0). */
+int or_enroll(int logN, int d, int p, const int64_t *emasks, const uint64_t *gk1, const uint64_t *in, int64_t n,
+              int64_t first_u, uint64_t *db, int64_t n_sets)
+{
+    if (p <= 0 || d % p) return -1;
+    const int N = 1 << logN, S = N / 2, s = d / p, B = S / s;
+    if (first_u < 0 || (first_u + n + B - 1) / B > n_sets) return -2;
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    uint64_t *C = malloc(sizeof(uint64_t) * 4 * N), *rot = malloc(sizeof(uint64_t) * 4 * N);
+    for (int64_t c = 0; c < n; c++) {
+        const int64_t u = first_u + c, t = u / B;
+        const int k = (int)(u % B);
+        for (int i = 0; i < p; i++) {
+            mul_plain_rescale_q2(&X, in + (size_t)c * 6 * N, emasks + (size_t)i * N, C);
+            const int m = ((i - k) % B + B) % B;
+            for (int b = 0; (1 << b) < B; b++) {
+                if (!((m >> b) & 1)) continue;
+                rotate1(&X.c, C, (uint64_t)s << b, gk1 + (size_t)b * 12 * N, rot);
+                memcpy(C, rot, sizeof(uint64_t) * 4 * N);
+            }
+            uint64_t *dst = db + ((size_t)t * p + i) * 4 * N;
+            for (int cl = 0; cl < 4; cl++)
+                poly_add(X.c.q[cl & 1], N, dst + (size_t)cl * N, C + (size_t)cl * N, dst + (size_t)cl * N);
+        }
+    }
+    free(C); free(rot);
     ctx2_free(&X);
     return 0;
 }

@@ -80,8 +80,8 @@ def lib():
         L.or_find_prime_below.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         L.or_find_prime_below.restype = ctypes.c_uint64
         L.or_q2.restype = ctypes.c_uint64
-        L.or_keygen_exp.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p,
-                                    _u64p]
+        L.or_keygen_exp.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, _u64p, _u64p]
         L.or_keygen_exp.restype = ctypes.c_int
         L.or_encrypt_l2.argtypes = [ctypes.c_int, _u64p, _u64p, _i64p, ctypes.c_int64, ctypes.c_uint64,
                                     ctypes.c_uint64, _u64p]
@@ -90,6 +90,9 @@ def lib():
         L.or_rotate1.argtypes = [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p]
         L.or_expand.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _u64p, _u64p, ctypes.c_int64, _u64p]
         L.or_expand.restype = ctypes.c_int
+        L.or_enroll.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _u64p, _u64p, ctypes.c_int64,
+                                ctypes.c_int64, _u64p, ctypes.c_int64]
+        L.or_enroll.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -366,14 +369,15 @@ def log2_exact(x):
     return k
 
 
-def keygen_exp(logN, seed, d, p, zero_error=False):
+def keygen_exp(logN, seed, d, p, zero_error=False, n_rot=None):
     """Expansion keys of keygen(seed)'s secret: pk_q2 [2][N] (pk's q2 limb) and the level-1
-    Galois keys gk1 [log2 p][2 digits][2 comps][3 limbs q0,q1,P][N] of rotations s 2^t."""
+    Galois keys gk1 [n_rot][2 digits][2 comps][3 limbs q0,q1,P][N] of rotations s 2^t
+    (n_rot: log2 p by default, the expansion's; log2 B covers the enrollment too)."""
     N = 1 << logN
-    lp = log2_exact(p)
+    lp = log2_exact(p) if n_rot is None else n_rot
     pk_q2 = np.zeros((2, N), np.uint64)
     gk1 = np.zeros((max(lp, 1), 2, 2, 3, N), np.uint64)
-    rc = lib().or_keygen_exp(logN, seed, d, p, int(zero_error), _p(pk_q2, _u64p), _p(gk1, _u64p))
+    rc = lib().or_keygen_exp(logN, seed, d, p, lp, int(zero_error), _p(pk_q2, _u64p), _p(gk1, _u64p))
     if rc:
         raise ValueError(f"or_keygen_exp: {rc}")
     return pk_q2, gk1[:lp]
@@ -445,3 +449,43 @@ def expand(logN, d, p, masks, gk1, ct):
     if rc:
         raise ValueError(f"or_expand: {rc}")
     return out
+
+
+# ---------------------------------------------------------------------------- f4: server-side enrollment
+# Fig. 3 / PAPER.md:251-269 with SPEC.md:282-293's semantics (reading R27), same chain as f3.
+def n_rot_enroll(logN, d, p):
+    """Galois keys the enrollment needs: strides s 2^t for t < log2 B."""
+    return log2_exact(layout(logN, d, p)[2])
+
+
+def enroll_masks_slots(logN, d, p):
+    """E_i[x] = 1 if x lies in [i s, (i+1) s), else 0."""
+    S, s, _ = layout(logN, d, p)
+    x = np.arange(S)
+    return np.stack([((x >= i * s) & (x < (i + 1) * s)).astype(np.float64) for i in range(p)])
+
+
+def enroll_masks(logN, d, p):
+    return encode(enroll_masks_slots(logN, d, p), logN, scale=float(q2()))
+
+
+def enroll_vector(v, logN, d):
+    """The client's enrollment slots: the template in slots [0, d), zeros elsewhere."""
+    S = (1 << logN) // 2
+    v = np.asarray(v, np.float64).reshape(-1, d)
+    z = np.zeros((v.shape[0], S))
+    z[:, :d] = v
+    return z
+
+
+def enroll(logN, d, p, emasks, gk1, ct, first_u, db):
+    """Accumulates the level-2 template cts ct [n][2][3][N] (templates first_u..) into db
+    [n_sets][p][2][2][N] (level 1, modified in place and returned)."""
+    ct = np.ascontiguousarray(ct, np.uint64).reshape(-1, 2, 3, 1 << logN)
+    assert db.flags["C_CONTIGUOUS"] and db.dtype == np.uint64
+    g = np.ascontiguousarray(gk1 if len(gk1) else np.zeros((1, 2, 2, 3, 1 << logN), np.uint64), np.uint64)
+    rc = lib().or_enroll(logN, d, p, _p(np.ascontiguousarray(emasks, np.int64), _i64p), _p(g, _u64p), _p(ct, _u64p),
+                         ct.shape[0], first_u, _p(db, _u64p), db.shape[0])
+    if rc:
+        raise ValueError(f"or_enroll: {rc}")
+    return db

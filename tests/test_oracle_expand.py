@@ -14,6 +14,12 @@ Pins used (each independent of the oracle code path it checks):
   * decryption of every expanded part equals SPEC.md:297's post-condition w_i[x] = q[i s + x mod s]
   * SPEC.md:300's worked example (S = 8, m = 4, N_in = 2) in real CKKS at N = 16
   * end to end: expanded queries through HE-C^3 give the plaintext cosines and top-1
+f4 (server-side enrollment packing, Fig. 3 / PAPER.md:251-269, same chain; reading R27):
+  * trivial ciphertexts: every set part equals a big-integer closed form (signed permutations
+    of round(E_i pt / q2) by the right rotations (k - i) s)
+  * SPEC.md:291's worked example at N = 16; decryption equals the client-side packing layout
+     for two sets covering every rotation amount; the enrolled DB scans to the
+    plaintext cosines and top-1
 """
 import json
 import os
@@ -331,3 +337,99 @@ def test_expanded_queries_through_he_c3(O):
     ref = (Q @ T.T)[0]
     assert np.abs(sc - ref).max() < 1e-6
     assert sc.argmax() == ref.argmax() == 17
+
+
+# ----------------------------------------------------------------------------- f4: server-side enrollment
+def test_enrollment_keys_extend_the_expansion_keys(O):
+    """The enrollment's log2 B strides s 2^t include the expansion's log2 p ones (same objects)."""
+    logN, d, p = 6, 16, 4
+    _, g_exp = O.keygen_exp(logN, 7, d, p)
+    nb = O.n_rot_enroll(logN, d, p)
+    _, g_enr = O.keygen_exp(logN, 7, d, p, n_rot=nb)
+    assert nb == 3 and g_enr.shape[0] == nb and np.array_equal(g_enr[:g_exp.shape[0]], g_exp)
+
+
+@pytest.mark.parametrize("first_u,n", [(0, 3), (5, 6)])
+def test_trivial_enrollment_closed_form(O, first_u, n):
+    """With c1 = 0 the key switches vanish: set[t][i] = sum over its templates u = tB + k of
+    sigma_{5^(s m)}(round(E_i pt_u / q2)), m = (i - k) mod B (a right rotation by (k - i) s)."""
+    logN, d, p = 5, 8, 2                  # N = 32, S = 16, s = 4, B = 4
+    N = 1 << logN
+    S, s, B = O.layout(logN, d, p)
+    q0, q1, P = O.primes()
+    q2 = O.q2()
+    _, gk1 = O.keygen_exp(logN, 8, d, p, n_rot=O.n_rot_enroll(logN, d, p))
+    rnd = random.Random(50 + first_u)
+    pts = [[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(n)]
+    em = np.array([[rnd.randrange(-2 ** 40, 2 ** 40) for _ in range(N)] for _ in range(p)], np.int64)
+    n_sets = -(-(first_u + n) // B)
+    db = np.zeros((n_sets, p, 2, 2, N), np.uint64)
+    ct = np.stack([_trivial_l2(pt, (q0, q1, q2), N) for pt in pts])
+    O.enroll(logN, d, p, em, gk1, ct, first_u, db)
+    for t in range(n_sets):
+        for i in range(p):
+            acc = [0] * N
+            for c in range(n):
+                u = first_u + c
+                if u // B != t:
+                    continue
+                m = (i - u % B) % B
+                C = [(v - _cent(v, q2)) // q2 for v in _negacyclic_big([int(x) for x in em[i]], pts[c])]
+                acc = [a + b for a, b in zip(acc, _sigma_int(C, pow(5, s * m, 2 * N)))]
+            assert [int(v) for v in db[t, i, 0, 0]] == [v % q0 for v in acc]
+            assert [int(v) for v in db[t, i, 0, 1]] == [v % q1 for v in acc]
+            assert not db[t, i, 1].any()
+
+
+def _enroll_and_decrypt(O, logN, d, p, T, first_u=0, key_seed=1):
+    S, s, B = O.layout(logN, d, p)
+    sk, pk, rlk, gk = O.keygen(logN, key_seed, O.n_rot_for(d, p))
+    pk_q2, gk1 = O.keygen_exp(logN, key_seed, d, p, n_rot=O.n_rot_enroll(logN, d, p))
+    ct = O.encrypt_l2(logN, pk, pk_q2, O.encode(O.enroll_vector(T, logN, d), logN), first_u, 5)
+    n_sets = -(-(first_u + len(T)) // B)
+    db = np.zeros((n_sets, p, 2, 2, 1 << logN), np.uint64)
+    O.enroll(logN, d, p, O.enroll_masks(logN, d, p), gk1, ct, first_u, db)
+    q0 = O.primes()[0]
+    z = np.zeros((n_sets, p, S))
+    for t in range(n_sets):
+        for i in range(p):
+            m = O.decrypt(logN, sk, db[t, i], 2)
+            z[t, i] = O.decode_slots(O.centred_i64(m[0], q0), logN, O.DELTA)
+    return z, db, (sk, pk, rlk, gk)
+
+
+def test_spec_enroll_example_N16(O):
+    """S = 8, m = 4, N_in = 2, enroll [a,b,c,d] at index 1 -> store ct 0 = [0,0,a,b,0,0,0,0],
+    ct 1 = [0,0,c,d,0,0,0,0], in real CKKS at N = 16."""
+    en = json.load(open(GOLD))["enroll"]
+    z, _, _ = _enroll_and_decrypt(O, 4, 4, 2, np.array([en["vector"]]), first_u=en["index"])
+    assert np.abs(z[0, 0] - en["ct0"]).max() < 1e-6
+    assert np.abs(z[0, 1] - en["ct1"]).max() < 1e-6
+
+
+def test_enrollment_meets_the_packing_layout(O):
+    """SPEC.md:282-289 post-condition: after enrolling templates 0..n-1, set t part i decrypts to the
+    client-side packing (template u = tB + k at slots k s .. k s + s - 1 of part i), two sets, the
+    second partial (N = 256, d = 16, p = 4: s = 4, B = 32, every rotation amount m < 32 occurs)."""
+    logN, d, p = 8, 16, 4
+    T = I.random_unit(45, d, 9)
+    z, _, _ = _enroll_and_decrypt(O, logN, d, p, T)
+    want = O.pack_db(T, logN, d, p, 0, z.shape[0])
+    assert np.abs(z - want).max() < 1e-6
+
+
+def test_server_enrolled_db_scans_to_cosines(O):
+    """f4 enrollment + Algorithm 2: the server-packed DB gives the plaintext cosines (1e-6) and top-1."""
+    logN, d, p = 9, 16, 4
+    T = I.random_unit(100, d, 12)
+    qv = T[37:38] + 0.05 * np.random.default_rng(3).standard_normal((1, d))
+    qv /= np.linalg.norm(qv)
+    z, db, (sk, pk, rlk, gk) = _enroll_and_decrypt(O, logN, d, p, T)
+    S, s, B = O.layout(logN, d, p)
+    qc = O.encrypt(logN, pk, O.encode(O.pack_query(qv, logN, d, p).reshape(-1, S), logN), 0, 3).reshape(1, p, 2, 2, -1)
+    out, pairs = O.match(logN, d, p, 0, rlk, gk, db, qc, n_threads=4)
+    q0 = O.primes()[0]
+    sc = np.concatenate([O.scores_from_output(logN, d, p, sk, out[i], q0) for i in range(len(pairs))])[:len(T)]
+    ref = (qv @ T.T)[0]
+    assert np.abs(sc - ref).max() < 1e-6
+    assert sc.argmax() == ref.argmax() == 37
