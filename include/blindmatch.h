@@ -206,23 +206,31 @@ int bm_top1(const double *scores, int64_t n, int64_t *idx, double *best);
 typedef struct bm_xk bm_xk;           /* host: pk limb q2 + level-1 Galois keys of strides s 2^t */
 typedef struct bm_xk_dev bm_xk_dev;   /* device: level-2 pk, Galois keys, masks (NTT domain)      */
 
-/* Expansion keys for keygen(seed)'s secret (pass the same seed).  pk limb q2 = (-a s + e, a)
- * with pk's error e; gk1[t][j] (rotation r = s 2^t, digit j) over {q0,q1,P}:
- * (-a s + e + [l = j](P mod q_l) sigma_{5^r}(s) [limb q_l], a).  Errors: BM_ERR_INVALID_ARG, BM_ERR_OOM. */
+/* Expansion / enrollment keys for keygen(seed)'s secret (pass the same seed).  pk limb q2 =
+ * (-a s + e, a) with pk's error e; gk1[t][j] (rotation r = s 2^t, t < log2 B, digit j) over
+ * {q0,q1,P}: (-a s + e + [l = j](P mod q_l) sigma_{5^r}(s) [limb q_l], a).  The expansion uses
+ * t < log2 p, the enrollment (f4) every t < log2 B.  Errors: BM_ERR_INVALID_ARG, BM_ERR_OOM. */
 int bm_xk_keygen(const bm_params *, uint64_t seed, bm_xk **out);
 void bm_xk_free(bm_xk *);
-/* pk_q2 [2][N]; gk1 [log2 p][2 digits][2 comps][3 limbs q0,q1,P][N] (canonical). */
+/* pk_q2 [2][N]; gk1 [n_rot][2 digits][2 comps][3 limbs q0,q1,P][N] (canonical).  Import accepts
+ * log2 p <= n_rot <= log2 B (BM_ERR_MISSING_ROTATION_KEY otherwise). */
 int bm_xk_export(const bm_xk *, uint64_t *pk_q2, uint64_t *gk1, int32_t *n_rot);
 int bm_xk_import(const bm_params *, const uint64_t *pk_q2, const uint64_t *gk1, int32_t n_rot, bm_xk **out);
-/* Upload (synchronous): the level-2 public key (pk's limbs + xk's q2 limb), the Galois keys and
- * the p masks (h_masks [p][N] int64, e.g. from bm_encode_masks), all to the NTT domain.
+/* Upload (synchronous): the level-2 public key (pk's limbs + xk's q2 limb), the Galois keys, the
+ * p expansion masks h_masks [p][N] and (optional, f4) the p enrollment masks h_emasks [p][N]
+ * (int64 plaintexts, e.g. from bm_encode_masks), all to the NTT domain.
  * Errors: BM_ERR_KEY_MISMATCH, BM_ERR_CUDA, BM_ERR_OOM. */
-int bm_xk_to_device(const bm_params *, const bm_pk *, const bm_xk *, const int64_t *h_masks, bm_xk_dev **out);
+int bm_xk_to_device(const bm_params *, const bm_pk *, const bm_xk *, const int64_t *h_masks, const int64_t *h_emasks,
+                    bm_xk_dev **out);
 void bm_xk_dev_free(bm_xk_dev *);
 /* Client encoding (host): q[nq][d] -> pt[nq][N], the unit query tiled S/d times at scale 2^40;
- * masks: pt[p][N], X_i at scale q2.  Errors: BM_ERR_ZERO_VECTOR, BM_ERR_MAGNITUDE. */
+ * bm_encode_enroll: v[n][d] -> pt[n][N], the unit template in slots [0, d), zeros elsewhere (f4);
+ * masks: pt[p][N] at scale q2, kind 0 the expansion masks X_i[x] = [(x mod d) in [i s, (i+1) s)],
+ * kind 1 the enrollment masks E_i[x] = [x in [i s, (i+1) s)].
+ * Errors: BM_ERR_ZERO_VECTOR, BM_ERR_MAGNITUDE, BM_ERR_INVALID_ARG. */
 int bm_encode_query_tiled(const bm_params *, const double *q, int64_t nq, int64_t *pt);
-int bm_encode_masks(const bm_params *, int64_t *pt);
+int bm_encode_enroll(const bm_params *, const double *v, int64_t n, int64_t *pt);
+int bm_encode_masks(const bm_params *, int32_t kind, int64_t *pt);
 /* Level-2 public-key encryption (device): ct_o = (u b + e0 + pt, u a + e1) over {q0,q1,q2}, the
  * streams of bm_encrypt (so limbs q0, q1 equal bm_encrypt's).  d_pt [n][N] int64 device;
  * d_out [n][2][3][N] NTT domain. */
@@ -235,6 +243,19 @@ int bm_encrypt_l2(const bm_params *, const bm_xk_dev *, const int64_t *d_pt, int
 size_t bm_expand_ws_bytes(const bm_params *, int32_t nq);
 int bm_expand(const bm_params *, const bm_xk_dev *, const uint64_t *d_in, int32_t nq, uint64_t *d_out, void *d_ws,
               size_t ws_bytes, void *stream);
+/* f4: SERVER-SIDE ENROLLMENT PACKING, Fig. 3 (SPEC.md:282-293,
+ * DESIGN.md reading R27), same extended chain.  d_in [n][2][3][N] (level 2, NTT): the level-2
+ * encryptions of bm_encode_enroll's templates first_template .. first_template + n - 1.  For template
+ * u = tB + k and part i:  set[t][i] += Rot_right(Res_q2(Mul(P)(C_u, E_i)), (k - i) s), the rotation
+ * done as left rotations by s 2^b for the set bits b of (i - k) mod B.  d_db [n_sets][p][2][2][N]
+ * (level 1, NTT; zero-filled for a fresh store) is accumulated in place -- the layout bm_encrypt_db
+ * writes and bm_match reads.  Asynchronous on `stream`, allocates nothing; d_ws of at least
+ * bm_enroll_ws_bytes(prm, n) bytes.  Errors: BM_ERR_INVALID_ARG (also: no enrollment masks
+ * uploaded), BM_ERR_KEY_MISMATCH, BM_ERR_MISSING_ROTATION_KEY, BM_ERR_CAPACITY (a template beyond
+ * n_sets), BM_ERR_WORKSPACE, BM_ERR_CUDA. */
+size_t bm_enroll_ws_bytes(const bm_params *, int64_t n);
+int bm_enroll(const bm_params *, const bm_xk_dev *, const uint64_t *d_in, int64_t n, int64_t first_template,
+              uint64_t *d_db, int64_t n_sets, void *d_ws, size_t ws_bytes, void *stream);
 
 int bm_sync(void *stream);
 const char *bm_strerror(int status);

@@ -82,9 +82,12 @@ _SIGS = {
     "bm_xk_keygen": (_i32, [_P, _u64, _pp]), "bm_xk_free": (None, [_vp]),
     "bm_xk_export": (_i32, [_vp, _vp, _vp, ctypes.POINTER(_i32)]),
     "bm_xk_import": (_i32, [_P, _vp, _vp, _i32, _pp]),
-    "bm_xk_to_device": (_i32, [_P, _vp, _vp, _vp, _pp]), "bm_xk_dev_free": (None, [_vp]),
+    "bm_xk_to_device": (_i32, [_P, _vp, _vp, _vp, _vp, _pp]), "bm_xk_dev_free": (None, [_vp]),
     "bm_encode_query_tiled": (_i32, [_P, _vp, _i64, _vp]),
-    "bm_encode_masks": (_i32, [_P, _vp]),
+    "bm_encode_enroll": (_i32, [_P, _vp, _i64, _vp]),
+    "bm_encode_masks": (_i32, [_P, _i32, _vp]),
+    "bm_enroll_ws_bytes": (_sz, [_P, _i64]),
+    "bm_enroll": (_i32, [_P, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp]),
     "bm_encrypt_l2": (_i32, [_P, _vp, _vp, _i64, _u64, _u64, _vp, _vp]),
     "bm_expand_ws_bytes": (_sz, [_P, _i32]),
     "bm_expand": (_i32, [_P, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
@@ -400,17 +403,32 @@ def bm_encode_query_tiled(prm, q):
     return out
 
 
-def bm_encode_masks(prm):
+MASK_EXPAND, MASK_ENROLL = 0, 1
+
+
+def bm_encode_masks(prm, kind=MASK_EXPAND):
     out = np.zeros((prm.p, N), np.int64)
-    _chk(_lib.bm_encode_masks(ctypes.byref(prm), _np_ptr(out)), "bm_encode_masks")
+    _chk(_lib.bm_encode_masks(ctypes.byref(prm), kind, _np_ptr(out)), "bm_encode_masks")
     return out
 
 
-def bm_xk_to_device(prm, pk, xk, masks=None):
-    """masks: int64 [p][N] plaintexts (default: bm_encode_masks(prm))."""
+def bm_encode_enroll(prm, v):
+    v = np.ascontiguousarray(v, np.float64)
+    out = np.zeros((v.shape[0], N), np.int64)
+    _chk(_lib.bm_encode_enroll(ctypes.byref(prm), _np_ptr(v), v.shape[0], _np_ptr(out)), "bm_encode_enroll")
+    return out
+
+
+def bm_xk_to_device(prm, pk, xk, masks=None, emasks=None, enroll=True):
+    """masks / emasks: int64 [p][N] expansion / enrollment plaintexts (defaults: bm_encode_masks;
+    enroll=False skips the enrollment masks)."""
     m = np.ascontiguousarray(bm_encode_masks(prm) if masks is None else masks, np.int64)
+    e = None
+    if enroll or emasks is not None:
+        e = np.ascontiguousarray(bm_encode_masks(prm, MASK_ENROLL) if emasks is None else emasks, np.int64)
     out = ctypes.c_void_p()
-    _chk(_lib.bm_xk_to_device(ctypes.byref(prm), pk.ptr, xk.ptr, _np_ptr(m), ctypes.byref(out)), "bm_xk_to_device")
+    _chk(_lib.bm_xk_to_device(ctypes.byref(prm), pk.ptr, xk.ptr, _np_ptr(m), _np_ptr(e) if e is not None else None,
+                              ctypes.byref(out)), "bm_xk_to_device")
     return ExpandKeyDev(out)
 
 
@@ -429,3 +447,15 @@ def bm_expand(prm, xk_dev, d_in, nq, d_out, d_ws, stream=None):
     ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
     _chk(_lib.bm_expand(ctypes.byref(prm), xk_dev.ptr, _dptr(d_in) if nq else None, nq, _dptr(d_out) if nq else None,
                         _dptr(d_ws) if ws_bytes else None, ws_bytes, _stream(stream)), "bm_expand")
+
+
+def bm_enroll_ws_bytes(prm, n):
+    return int(_lib.bm_enroll_ws_bytes(ctypes.byref(prm), n))
+
+
+def bm_enroll(prm, xk_dev, d_in, first_template, d_db, d_ws, stream=None):
+    """f4: accumulate the level-2 template cts d_in [n][2][3][N] into d_db [n_sets][p][2][2][N]."""
+    n = d_in.shape[0]
+    ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
+    _chk(_lib.bm_enroll(ctypes.byref(prm), xk_dev.ptr, _dptr(d_in) if n else None, n, first_template, _dptr(d_db),
+                        d_db.shape[0], _dptr(d_ws) if ws_bytes else None, ws_bytes, _stream(stream)), "bm_enroll")

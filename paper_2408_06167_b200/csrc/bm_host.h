@@ -43,10 +43,11 @@ struct bm_evk {
     int32_t n_hrot = 0;        // f2 hoisted rotation keys (s - 1 of them, 0 if not generated)
     std::vector<uint64_t> hgk; // [n_hrot][2][2][N], entry r-1 = rotation r
 };
-// f3 expansion keys: the q2 limb of pk and the level-1 Galois keys of rotations s 2^t, t < log2 p
+// f3/f4 keys: the q2 limb of pk and the level-1 Galois keys of rotations s 2^t, t < n_rot
+// (log2 p for the expansion; keygen makes log2 B, which the enrollment needs)
 struct bm_xk {
     uint8_t digest[32];
-    int32_t d, p, log_p;
+    int32_t d, p, n_rot;
     std::vector<uint64_t> pk_q2; // [2][N]
-    std::vector<uint64_t> gk1;   // [log_p][2 digits][2 comps][3 limbs q0,q1,P][N]
+    std::vector<uint64_t> gk1;   // [n_rot][2 digits][2 comps][3 limbs q0,q1,P][N]
 };

@@ -687,6 +687,18 @@ struct ExpK {
     uint64_t *XU;            // [cts][6][N]
     int p;
     uint32_t g;              // Galois element of this step
+    // f4 enrollment mode (enroll = 1): pure rotation C <- Rot(C) (no add), applied only to the parts
+    // whose amount m = (i - k) mod B has bit `bit` set (template u = u0 + ct / p, k = u mod B)
+    int enroll, Bk, bit;
+    int64_t u0;
+    BM_D bool skip(int64_t ct) const
+    {
+        if (!enroll) return false;
+        const int64_t u = u0 + ct / p;
+        const int i = (int)(ct % p), k = (int)(u % Bk);
+        const int m = ((i - k) % Bk + Bk) % Bk;
+        return !((m >> bit) & 1);
+    }
 };
 constexpr int XU_POLYS = 6;
 constexpr size_t X1_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
@@ -755,6 +767,7 @@ __global__ void __launch_bounds__(T, 1) k_rot1_digits(ExpK K)
     const int tid = threadIdx.x;
     const int64_t ct = blockIdx.x >> 1;
     const int l = blockIdx.x & 1;
+    if (K.skip(ct)) return;
     const uint64_t *c1 = K.out + ((size_t)ct * 2 + 1) * 2 * N + (size_t)l * N;
     uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
     stage_by_j(S, c1);
@@ -793,6 +806,7 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
     const int tid = threadIdx.x;
     const int64_t ct = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
+    if (K.skip(ct)) return;
     const uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
     uint64_t *cc = K.out + ((size_t)ct * 2 + c) * 2 * N; // [l][N]
     const uint64_t *c0 = K.out + (size_t)ct * 4 * N;
@@ -839,7 +853,9 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos);
-            const ulonglong2 cv = *reinterpret_cast<const ulonglong2 *>(cc + (size_t)l * N + pos);
+            // C + Rot(C) (expansion) or Rot(C) alone (enrollment)
+            const ulonglong2 cv = K.enroll ? make_ulonglong2(0, 0)
+                                           : *reinterpret_cast<const ulonglong2 *>(cc + (size_t)l * N + pos);
             uint64_t ka, kb;
             if (l) {
                 ka = shoup4<1>(u.x, ld2k(kl0 + pos)) + shoup4<1>(v.x, ld2k(kl1 + pos));
@@ -860,6 +876,26 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
 #pragma unroll
         for (int e = 0; e < E; e += 2) st2(cc + (size_t)l * N + pos_M4(tid, e), a[e], a[e + 1]);
     }
+}
+
+// f4: set[t][i] += the rotated parts of its templates (elementwise in the NTT domain, canonical)
+// grid: (local set, part, comp x limb, N / 256 slices); W [n][p][2][2][N] holds templates u0 .. u0+n-1
+__global__ void __launch_bounds__(256) k_enroll_add(const uint64_t *W, int64_t u0, int64_t n, int p, int Bk,
+                                                    int64_t t0, uint64_t *db)
+{
+    const int slice = blockIdx.x % (N / 256);
+    int64_t b = blockIdx.x / (N / 256);
+    const int cl = (int)(b % 4);
+    b /= 4;
+    const int i = (int)(b % p);
+    const int64_t t = t0 + b / p;
+    const uint64_t q = (cl & 1) ? Q1 : Q0;
+    const int k = slice * 256 + threadIdx.x;
+    const int64_t lo = t * Bk > u0 ? t * Bk : u0, hi = (t + 1) * Bk < u0 + n ? (t + 1) * Bk : u0 + n;
+    uint64_t *dst = db + (((size_t)t * p + i) * 4 + cl) * N + k;
+    uint64_t acc = *dst;
+    for (int64_t u = lo; u < hi; u++) acc = csub(acc + W[(((size_t)(u - u0) * p + i) * 4 + cl) * N + k], q);
+    *dst = acc;
 }
 
 // ================================================================== encryption / conversion / keys
@@ -1149,10 +1185,11 @@ struct bm_pk_dev {
 struct bm_xk_dev {
     int dev;
     uint8_t digest[32];
-    int32_t d, p, s, log_p;
-    ulonglong2 *pk2;  // [2][3 limbs q0,q1,q2][N] level-2 public key
-    ulonglong2 *gk1;  // [log_p][2][2][3 limbs q0,q1,P][N], P^-1 in the Q limbs
-    ulonglong2 *mask; // [p][3 limbs q0,q1,q2][N], q2^-1 in the Q limbs
+    int32_t d, p, s, n_rot;
+    ulonglong2 *pk2;   // [2][3 limbs q0,q1,q2][N] level-2 public key
+    ulonglong2 *gk1;   // [n_rot][2][2][3 limbs q0,q1,P][N], P^-1 in the Q limbs
+    ulonglong2 *mask;  // [p][3 limbs q0,q1,q2][N] expansion masks X_i, q2^-1 in the Q limbs
+    ulonglong2 *emask; // [p][3][N] enrollment masks E_i (f4; nullptr if not uploaded)
 };
 struct bm_evk_dev {
     int dev;
@@ -1369,7 +1406,25 @@ int bm_ct_from_coeff(const bm_params *prm, const uint64_t *d_in, int64_t n_cts, 
 }
 
 // ------------------------------------------------------------------ f3: query expansion
-int bm_xk_to_device(const bm_params *prm, const bm_pk *pk, const bm_xk *xk, const int64_t *h_masks, bm_xk_dev **out)
+static int upload_masks(DevCtx *C, const bm_params *prm, const int64_t *h_masks, ulonglong2 **out)
+{
+    // integer plaintexts -> residues per limb (q0, q1, q2), q2^-1 folded into the Q limbs
+    std::vector<uint64_t> m(3 * (size_t)prm->p * N);
+    const uint64_t qs[3] = {Q0, Q1, Q2};
+    for (int i = 0; i < prm->p; i++)
+        for (int l = 0; l < 3; l++)
+            for (int k = 0; k < N; k++) {
+                const int64_t x = h_masks[(size_t)i * N + k];
+                const uint64_t q = qs[l];
+                m[((size_t)i * 3 + l) * N + k] = x >= 0 ? (uint64_t)x % q : q - 1 - (uint64_t)(-(x + 1)) % q;
+            }
+    const uint64_t sm[3] = {C->q2inv[0].x, C->q2inv[1].x, 1};
+    const int l2[3] = {0, 1, 3};
+    return upload_key_polys(C, m.data(), 3 * (int64_t)prm->p, 3, l2, out, sm);
+}
+
+int bm_xk_to_device(const bm_params *prm, const bm_pk *pk, const bm_xk *xk, const int64_t *h_masks,
+                    const int64_t *h_emasks, bm_xk_dev **out)
 {
     if (!prm || !pk || !xk || !h_masks || !out) return BM_ERR_INVALID_ARG;
     if (memcmp(pk->digest, prm->digest, 32) || memcmp(xk->digest, prm->digest, 32) || xk->d != prm->d ||
@@ -1384,8 +1439,8 @@ int bm_xk_to_device(const bm_params *prm, const bm_pk *pk, const bm_xk *xk, cons
     d->d = prm->d;
     d->p = prm->p;
     d->s = prm->s;
-    d->log_p = xk->log_p;
-    d->pk2 = d->gk1 = d->mask = nullptr;
+    d->n_rot = xk->n_rot;
+    d->pk2 = d->gk1 = d->mask = d->emask = nullptr;
     // level-2 pk: pk's limbs q0, q1 and xk's q2 limb
     std::vector<uint64_t> h(6 * (size_t)N);
     for (int c = 0; c < 2; c++) {
@@ -1397,25 +1452,14 @@ int bm_xk_to_device(const bm_params *prm, const bm_pk *pk, const bm_xk *xk, cons
     rc = upload_key_polys(C, h.data(), 6, 3, l2, &d->pk2);
     // Galois keys: P^-1 folded into the Q limbs (the ModDown multiplies by it anyway)
     const uint64_t sk[3] = {C->pinv[0].x, C->pinv[1].x, 1};
-    if (!rc && xk->log_p > 0) rc = upload_key_polys(C, xk->gk1.data(), 12 * (int64_t)xk->log_p, 3, lk, &d->gk1, sk);
-    // masks: integer plaintexts -> residues per limb, q2^-1 folded into the Q limbs
-    if (!rc) {
-        std::vector<uint64_t> m(3 * (size_t)prm->p * N);
-        const uint64_t qs[3] = {Q0, Q1, Q2};
-        for (int i = 0; i < prm->p; i++)
-            for (int l = 0; l < 3; l++)
-                for (int k = 0; k < N; k++) {
-                    const int64_t x = h_masks[(size_t)i * N + k];
-                    const uint64_t q = qs[l];
-                    m[((size_t)i * 3 + l) * N + k] = x >= 0 ? (uint64_t)x % q : q - 1 - (uint64_t)(-(x + 1)) % q;
-                }
-        const uint64_t sm[3] = {C->q2inv[0].x, C->q2inv[1].x, 1};
-        rc = upload_key_polys(C, m.data(), 3 * (int64_t)prm->p, 3, l2, &d->mask, sm);
-    }
+    if (!rc && xk->n_rot > 0) rc = upload_key_polys(C, xk->gk1.data(), 12 * (int64_t)xk->n_rot, 3, lk, &d->gk1, sk);
+    if (!rc) rc = upload_masks(C, prm, h_masks, &d->mask);
+    if (!rc && h_emasks) rc = upload_masks(C, prm, h_emasks, &d->emask);
     if (rc) {
         cudaFree(d->pk2);
         cudaFree(d->gk1);
         cudaFree(d->mask);
+        cudaFree(d->emask);
         cudaGetLastError();
         delete d;
         return rc;
@@ -1430,6 +1474,7 @@ void bm_xk_dev_free(bm_xk_dev *d)
     cudaFree(d->pk2);
     cudaFree(d->gk1);
     cudaFree(d->mask);
+    cudaFree(d->emask);
     delete d;
 }
 
@@ -1481,6 +1526,9 @@ int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
 {
     if (!prm || !xk || nq < 0) return BM_ERR_INVALID_ARG;
     if (memcmp(xk->digest, prm->digest, 32) || xk->p != prm->p || xk->d != prm->d) return BM_ERR_KEY_MISMATCH;
+    int log_p = 0;
+    while ((1 << log_p) < prm->p) log_p++;
+    if (xk->n_rot < log_p) return BM_ERR_MISSING_ROTATION_KEY;
     if (nq == 0) return BM_OK;
     if (!d_in || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
     if (ws_bytes < bm_expand_ws_bytes(prm, nq)) return BM_ERR_WORKSPACE;
@@ -1497,6 +1545,10 @@ int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
     K.mask = xk->mask;
     K.XU = (uint64_t *)d_ws;
     K.p = prm->p;
+    K.enroll = 0;
+    K.Bk = prm->B;
+    K.bit = 0;
+    K.u0 = 0;
     const int64_t ch = expand_chunk_cts(prm, nq), qch = ch / prm->p;
     for (int64_t j0 = 0; j0 < nq && !rc; j0 += qch) {
         const int64_t nqc = nq - j0 < qch ? nq - j0 : qch;
@@ -1507,13 +1559,91 @@ int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
         K.g = 1;
         k_exp_mask<<<ncb, T, X1_SMEM_BYTES, s>>>(K);
         rc = launch_check();
-        for (int t = 0; t < xk->log_p && !rc; t++) {
+        for (int t = 0; t < log_p && !rc; t++) {
             K.gk = xk->gk1 + (size_t)t * 12 * N;
             K.g = (uint32_t)powmod_d(5, (uint64_t)prm->s << t, 2 * N);
             k_rot1_digits<<<ncb, T, X2_SMEM_BYTES, s>>>(K);
             k_rot1_ks<<<ncb, T, X3_SMEM_BYTES, s>>>(K);
             rc = launch_check();
         }
+    }
+    return rc;
+}
+
+// ------------------------------------------------------------------ f4: server-side enrollment
+static int64_t enroll_chunk_templates(const bm_params *prm, int64_t n)
+{
+    int64_t ch = 2048; // parts per launch: 10 N u64 of workspace each (W + XU, 1.25 GiB)
+    if (const char *e = getenv("BM_EXPAND_CHUNK")) {
+        long v = atol(e);
+        if (v > 0) ch = v;
+    }
+    int64_t t = ch / prm->p;
+    if (t < 1) t = 1;
+    return n < t ? n : t;
+}
+
+size_t bm_enroll_ws_bytes(const bm_params *prm, int64_t n)
+{
+    if (!prm || n <= 0) return 0;
+    return (size_t)enroll_chunk_templates(prm, n) * prm->p * (4 + XU_POLYS) * N * sizeof(uint64_t);
+}
+
+int bm_enroll(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, int64_t n, int64_t first_template,
+              uint64_t *d_db, int64_t n_sets, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!prm || !xk || n < 0 || first_template < 0 || n_sets < 0) return BM_ERR_INVALID_ARG;
+    if (memcmp(xk->digest, prm->digest, 32) || xk->p != prm->p || xk->d != prm->d) return BM_ERR_KEY_MISMATCH;
+    int log_b = 0;
+    while ((1 << log_b) < prm->B) log_b++;
+    if (xk->n_rot < log_b) return BM_ERR_MISSING_ROTATION_KEY;
+    if (!xk->emask) return BM_ERR_INVALID_ARG;
+    if (n == 0) return BM_OK;
+    if ((first_template + n + prm->B - 1) / prm->B > n_sets) return BM_ERR_CAPACITY;
+    if (!d_in || !d_db || !d_ws) return BM_ERR_INVALID_ARG;
+    if (ws_bytes < bm_enroll_ws_bytes(prm, n)) return BM_ERR_WORKSPACE;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t tch = enroll_chunk_templates(prm, n);
+    uint64_t *W = (uint64_t *)d_ws;
+    ExpK K;
+    for (int i = 0; i < 4; i++) K.pr[i] = C->pr[i];
+    K.pinv[0] = C->pinv[0];
+    K.pinv[1] = C->pinv[1];
+    K.q2inv[0] = C->q2inv[0];
+    K.q2inv[1] = C->q2inv[1];
+    K.mask = xk->emask;
+    K.XU = W + (size_t)tch * prm->p * 4 * N;
+    K.p = prm->p;
+    K.out = W;
+    K.Bk = prm->B;
+    for (int64_t c0 = 0; c0 < n && !rc; c0 += tch) {
+        const int64_t nc = n - c0 < tch ? n - c0 : tch;
+        const unsigned ncb = (unsigned)(2 * nc * prm->p);
+        K.in = d_in + (size_t)c0 * 6 * N;
+        K.u0 = first_template + c0;
+        K.enroll = 0;
+        K.g = 1;
+        K.gk = nullptr;
+        K.bit = 0;
+        k_exp_mask<<<ncb, T, X1_SMEM_BYTES, s>>>(K); // Res(Mul(P)(C_u, E_i)) for every part
+        rc = launch_check();
+        K.enroll = 1;
+        for (int b = 0; b < log_b && !rc; b++) {     // right rotation by (k - i) s = left by m s, bit by bit
+            K.bit = b;
+            K.gk = xk->gk1 + (size_t)b * 12 * N;
+            K.g = (uint32_t)powmod_d(5, (uint64_t)prm->s << b, 2 * N);
+            k_rot1_digits<<<ncb, T, X2_SMEM_BYTES, s>>>(K);
+            k_rot1_ks<<<ncb, T, X3_SMEM_BYTES, s>>>(K);
+            rc = launch_check();
+        }
+        if (rc) break;
+        const int64_t t0 = K.u0 / prm->B, t1 = (K.u0 + nc - 1) / prm->B;
+        k_enroll_add<<<(unsigned)((t1 - t0 + 1) * prm->p * 4 * (N / 256)), 256, 0, s>>>(W, K.u0, nc, prm->p, prm->B, t0,
+                                                                                         d_db);
+        rc = launch_check();
     }
     return rc;
 }

@@ -364,8 +364,9 @@ int bm_xk_keygen(const bm_params *prm, uint64_t seed, bm_xk **out)
     memcpy(x->digest, prm->digest, 32);
     x->d = prm->d;
     x->p = prm->p;
-    x->log_p = 0;
-    while ((1 << x->log_p) < prm->p) x->log_p++;
+    // strides s 2^t for t < log2 B: the expansion uses t < log2 p, the enrollment all of them
+    x->n_rot = 0;
+    while ((1 << x->n_rot) < prm->B) x->n_rot++;
     std::vector<int64_t> sv(N), ev(N);
     std::vector<uint64_t> s(N), e(N), a(N), t(N), sg(N);
     sample_small(seed, P_SK, 0, 0, sv.data());
@@ -377,8 +378,8 @@ int bm_xk_keygen(const bm_params *prm, uint64_t seed, bm_xk **out)
     poly_mul_h(a.data(), s.data(), t.data(), 3);
     for (int k = 0; k < N; k++) x->pk_q2[k] = (e[k] + Q2 - t[k]) % Q2, x->pk_q2[N + k] = a[k];
     // level-1 Galois keys
-    x->gk1.assign((size_t)x->log_p * 12 * N, 0);
-    for (int tt = 0; tt < x->log_p; tt++) {
+    x->gk1.assign((size_t)x->n_rot * 12 * N, 0);
+    for (int tt = 0; tt < x->n_rot; tt++) {
         const uint64_t r = (uint64_t)prm->s << tt, g = powmod_h(5, r, 2 * N);
         for (int j = 0; j < 2; j++) {
             const uint64_t obj = 2 * r + (uint64_t)j;
@@ -413,15 +414,16 @@ int bm_xk_export(const bm_xk *x, uint64_t *pk_q2, uint64_t *gk1, int32_t *n_rot)
     if (!x) return BM_ERR_INVALID_ARG;
     if (pk_q2) memcpy(pk_q2, x->pk_q2.data(), x->pk_q2.size() * 8);
     if (gk1) memcpy(gk1, x->gk1.data(), x->gk1.size() * 8);
-    if (n_rot) *n_rot = x->log_p;
+    if (n_rot) *n_rot = x->n_rot;
     return BM_OK;
 }
 int bm_xk_import(const bm_params *prm, const uint64_t *pk_q2, const uint64_t *gk1, int32_t n_rot, bm_xk **out)
 {
     if (!prm || !pk_q2 || (!gk1 && n_rot > 0) || !out) return BM_ERR_INVALID_ARG;
-    int log_p = 0;
+    int log_p = 0, log_b = 0;
     while ((1 << log_p) < prm->p) log_p++;
-    if (n_rot != log_p) return BM_ERR_MISSING_ROTATION_KEY;
+    while ((1 << log_b) < prm->B) log_b++;
+    if (n_rot < log_p || n_rot > log_b) return BM_ERR_MISSING_ROTATION_KEY;
     const int pq2[1] = {3}, pk3[3] = {0, 1, 2};
     if (!canonical(pk_q2, 2, pq2, 1) || (n_rot && !canonical(gk1, (size_t)n_rot * 12, pk3, 3)))
         return BM_ERR_INVALID_ARG;
@@ -430,7 +432,7 @@ int bm_xk_import(const bm_params *prm, const uint64_t *pk_q2, const uint64_t *gk
     memcpy(x->digest, prm->digest, 32);
     x->d = prm->d;
     x->p = prm->p;
-    x->log_p = log_p;
+    x->n_rot = n_rot;
     x->pk_q2.assign(pk_q2, pk_q2 + 2 * (size_t)N);
     x->gk1.assign(gk1, gk1 + (size_t)n_rot * 12 * N);
     *out = x;
@@ -644,14 +646,37 @@ int bm_encode_query_tiled(const bm_params *prm, const double *q, int64_t nq, int
     }
     return BM_OK;
 }
-int bm_encode_masks(const bm_params *prm, int64_t *pt)
+int bm_encode_masks(const bm_params *prm, int32_t kind, int64_t *pt)
 {
-    if (!prm || !pt) return BM_ERR_INVALID_ARG;
+    if (!prm || !pt || (kind != 0 && kind != 1)) return BM_ERR_INVALID_ARG;
     const int d = prm->d, s = prm->s;
     std::vector<double> z(SLOTS);
     for (int i = 0; i < prm->p; i++) {
-        for (int x = 0; x < SLOTS; x++) z[x] = ((x % d) >= i * s && (x % d) < (i + 1) * s) ? 1.0 : 0.0;
+        for (int x = 0; x < SLOTS; x++) {
+            const int y = kind == 0 ? x % d : x; // X_i is d-periodic, E_i is one block
+            z[x] = (y >= i * s && y < (i + 1) * s) ? 1.0 : 0.0;
+        }
         int rc = encode_slots(z.data(), pt + (size_t)i * N, (double)Q2);
+        if (rc) return rc;
+    }
+    return BM_OK;
+}
+
+// f4: the client's enrollment ciphertext holds the unit template in slots [0, d), zeros elsewhere
+// ("occupies the initial slots ... padded with zeros")
+int bm_encode_enroll(const bm_params *prm, const double *v, int64_t n, int64_t *pt)
+{
+    if (!prm || (!v && n > 0) || !pt || n < 0) return BM_ERR_INVALID_ARG;
+    const int d = prm->d;
+    std::vector<double> unit;
+    if (n) {
+        int rc = unit_rows(v, n, d, unit);
+        if (rc) return rc;
+    }
+    std::vector<double> z(SLOTS, 0.0);
+    for (int64_t j = 0; j < n; j++) {
+        for (int x = 0; x < d; x++) z[x] = unit[j * d + x];
+        int rc = encode_slots(z.data(), pt + (size_t)j * N);
         if (rc) return rc;
     }
     return BM_OK;

@@ -148,7 +148,7 @@ def test_expansion_keys_match_oracle(B, O, d, p):
     assert prm.q2 == O.q2()
     xk = B.bm_xk_keygen(prm, 4242)
     pk_q2, gk1 = B.bm_xk_export(xk)
-    opk_q2, ogk1 = O.keygen_exp(13, 4242, d, p)
+    opk_q2, ogk1 = O.keygen_exp(13, 4242, d, p, n_rot=O.n_rot_enroll(13, d, p))   # log2 B strides (f3 + f4)
     assert np.array_equal(pk_q2, opk_q2)
     assert gk1.shape == ogk1.shape and np.array_equal(gk1, ogk1)
     xk2 = B.bm_xk_import(prm, pk_q2, gk1)
@@ -171,3 +171,10 @@ def test_expansion_encoders_within_one_of_oracle(B, O):
     pm = B.bm_encode_masks(prm)
     om = O.expand_masks(13, 128, 8)
     assert np.abs(pm - om).max() <= 1 and (pm != om).mean() < 1e-3
+    pe = B.bm_encode_masks(prm, B.MASK_ENROLL)
+    oe = O.enroll_masks(13, 128, 8)
+    assert np.abs(pe - oe).max() <= 1 and (pe != oe).mean() < 1e-3
+    T = I.templates(2, 7)
+    pv = B.bm_encode_enroll(prm, T)
+    ov = O.encode(O.enroll_vector(T / np.linalg.norm(T, axis=1, keepdims=True), 13, 128), 13)
+    assert np.abs(pv - ov).max() <= 1 and (pv != ov).mean() < 1e-3

@@ -1,5 +1,6 @@
 """GPU parity of f3: server-side query expansion, Algorithm 1,
-on the chain extended by q2 (readings R24-R26).  The sm_100a path (bm_encrypt_l2,
+and of f4's server-side enrollment packing (Fig. 3), on the chain extended by q2
+(readings R24-R27).  The sm_100a path (bm_encrypt_l2,
 bm_expand, through the C ABI) against the CPU oracle, bit-exact on every RNS residue of the
 coefficient-domain outputs, given identical keys (tests/test_abi.py pins the host key generator
 to the oracle's), mask plaintexts (encoded by the oracle) and encryption randomness."""
@@ -28,7 +29,7 @@ def env():
 
 
 class XSetup:
-    def __init__(self, env, O, d, p, Q, key_seed=1, q_seed=3):
+    def __init__(self, env, O, d, p, Q, key_seed=1, q_seed=3, enroll_pt=None):
         torch, B = env
         self.torch, self.B, self.O, self.d, self.p = torch, B, O, d, p
         self.prm = B.bm_params_init(d, p)
@@ -37,7 +38,8 @@ class XSetup:
         self.osk, self.opk, self.orlk, self.ogk = O.keygen(LOGN, key_seed, O.n_rot_for(d, p))
         self.opk_q2, self.ogk1 = O.keygen_exp(LOGN, key_seed, d, p)
         self.masks = O.expand_masks(LOGN, d, p)
-        self.xk_dev = B.bm_xk_to_device(self.prm, self.pk, self.xk, self.masks)
+        self.emasks = O.enroll_masks(LOGN, d, p)
+        self.xk_dev = B.bm_xk_to_device(self.prm, self.pk, self.xk, self.masks, self.emasks)
         self.q_pt = O.encode(O.tile_query(Q, LOGN, d), LOGN)
         self.nq = Q.shape[0]
         self.q_seed = q_seed
@@ -140,3 +142,79 @@ def test_expanded_query_scan_end_to_end(env, O):
     cos = T @ Q[0]
     assert np.abs(sc - cos).max() < 1e-6
     assert B.bm_top1(sc)[0] == 17 == int(np.argmax(cos))
+
+
+
+# ----------------------------------------------------------------------------- f4: server-side enrollment
+def _enroll_gpu(st, T, first_u, d_db, enc_seed=5):
+    torch, B = st.torch, st.B
+    pt = st.O.encode(st.O.enroll_vector(T, LOGN, st.d), LOGN)
+    d_in = torch.empty((len(T), 2, 3, 8192), dtype=torch.int64, device="cuda")
+    B.bm_encrypt_l2(st.prm, st.xk_dev, torch.from_numpy(pt).cuda(), first_u, enc_seed, d_in)
+    ws = torch.empty(max(1, B.bm_enroll_ws_bytes(st.prm, len(T))), dtype=torch.uint8, device="cuda")
+    B.bm_enroll(st.prm, st.xk_dev, d_in, first_u, d_db, ws)
+    return pt
+
+
+def test_enroll_parity(env, O):
+    """bm_enroll == or_enroll bit for bit: templates 250..261 (across the set boundary of B = 256),
+    then 0..4 accumulated into the same store, at d = 128, p = 8."""
+    torch, B = env
+    d, p = 128, 8
+    st = XSetup(env, O, d, p, I.random_unit(1, d, 1))
+    _, gk1 = O.keygen_exp(LOGN, 1, d, p, n_rot=O.n_rot_enroll(LOGN, d, p))
+    d_db = torch.zeros((2, p, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    odb = np.zeros((2, p, 2, 2, 8192), np.uint64)
+    for first_u, n in ((250, 12), (0, 5)):
+        T = I.random_unit(n, d, 60 + first_u)
+        pt = _enroll_gpu(st, T, first_u, d_db)
+        oct_ = O.encrypt_l2(LOGN, st.opk, st.opk_q2, pt, first_u, 5)
+        O.enroll(LOGN, d, p, st.emasks, gk1, oct_, first_u, odb)
+    got = st.to_coeff(d_db, 2)
+    assert np.array_equal(got, odb)
+
+
+def test_server_enrolled_db_scan_end_to_end(env, O):
+    """configs[0]'s 256 templates enrolled one by one on the server (d = 16, p = 4), then scanned with
+    a client-expanded query: cosines within the guard and top-1 = 17 (decrypted on the client).
+    Guard 1e-5, not the client-packed path's 1e-6 (north_star: 1e-4): every enrolled template adds its
+    post-mask noise (Res rounding + up to log2 B = 10 level-1 key switches, ~1e-8 per slot) to ALL
+    slots of its set, so a set of 256 server-enrolled templates carries ~16x one template's noise
+    (measured max 1.6e-6 over the 256 scores; reading R27)."""
+    torch, B = env
+    d, p = 16, 4
+    T = I.templates(1)
+    Q, _ = I.queries(1)
+    st = XSetup(env, O, d, p, Q)
+    S, s, Bk = O.layout(LOGN, d, p)
+    n_sets = -(-T.shape[0] // Bk)
+    d_db = torch.zeros((n_sets, p, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    _enroll_gpu(st, T, 0, d_db)
+    pk_dev = B.bm_pk_to_device(st.prm, st.pk)
+    evk_dev = B.bm_evk_to_device(st.prm, st.evk)
+    d_q = torch.empty((1, p, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    B.bm_encrypt_query(st.prm, pk_dev, Q, 0, 3, d_q)
+    out = torch.empty((1, n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_match_ws_bytes(st.prm, n_sets, 1, 0), dtype=torch.uint8, device="cuda")
+    B.bm_match(st.prm, evk_dev, d_db, n_sets, d_q, 1, out, ws, 0)
+    B.bm_sync()
+    sc = B.bm_decrypt(st.prm, st.sk, out.cpu().numpy().view(np.uint64).reshape(-1, 2, 1, 8192)).reshape(-1)
+    cos = T @ Q[0]
+    assert np.abs(sc[:T.shape[0]] - cos).max() < 1e-5
+    assert np.abs(sc[T.shape[0]:]).max() < 1e-5          # unoccupied blocks stay empty
+    assert B.bm_top1(sc[:T.shape[0]])[0] == 17
+
+
+def test_enroll_errors(env, O):
+    torch, B = env
+    st = XSetup(env, O, 16, 4, I.random_unit(1, 16, 1))
+    d_in = torch.zeros((2, 2, 3, 8192), dtype=torch.int64, device="cuda")
+    d_db = torch.zeros((1, 4, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_enroll_ws_bytes(st.prm, 2), dtype=torch.uint8, device="cuda")
+    with pytest.raises(B.BMError) as e:       # templates 1023, 1024: the second is beyond one set (B = 1024)
+        B.bm_enroll(st.prm, st.xk_dev, d_in, 1023, d_db, ws)
+    assert e.value.name == "BM_ERR_CAPACITY"
+    xk_noenroll = B.bm_xk_to_device(st.prm, st.pk, st.xk, enroll=False)
+    with pytest.raises(B.BMError) as e:
+        B.bm_enroll(st.prm, xk_noenroll, d_in, 0, d_db, ws)
+    assert e.value.name == "BM_ERR_INVALID_ARG"
