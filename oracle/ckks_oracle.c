@@ -1106,3 +1106,260 @@ int or_enroll(int logN, int d, int p, const int64_t *emasks, const uint64_t *gk1
     ctx2_free(&X);
     return 0;
 }
+
+/* ================================================================== */
+/* f1: output compression (PAPER.md:273, 343-345;  */
+/* SPEC.md:321-329), on the same extended chain, so HE-C^3 runs one    */
+/* level higher: level 2 -> (tensor, relin, Res by q2) -> level 1 ->   */
+/* ladder at level 1 -> compression: Res_q1(Mul(P)(C_t, M)), right     */
+/* rotation by (t mod s) at level 0, add (reading R28).      */
+/* ================================================================== */
+/* Layouts (coefficient domain):
+ *   rlk2   [3 digits j][2 comps][4 limbs q0,q1,q2,P][N]
+ *   gkl    [log2 s][2 digits][2 comps][3 limbs q0,q1,P][N]: level-1 Galois keys of the ladder's
+ *          rotations 2^i (the gk1 family of f3, objects 2r + j)
+ *   gkc    [s-1][2 comps][2 limbs q0,P][N]: level-0 Galois keys of the left rotations by S - u
+ *          (right rotations by u), u = 1..s-1, PRNG objects CMP_OBJ + u
+ *   mask   int64 [N]: M[x] = [x mod s = 0] at scale q1 (encoded by the caller)              */
+enum { P_RLK2_A = 13, P_RLK2_E = 14 };
+#define CMP_OBJ 4096
+
+/* one level-1 Galois key (the f3 family): rotation r, digits j in {0,1}, over {q0,q1,P} */
+static void galois_key1(const ctx_t *C, uint64_t seed, uint64_t r, int zero_error, const int64_t *sv, uint64_t *out)
+{
+    const int N = C->N;
+    const uint64_t g = galois_elt(N, r);
+    uint64_t *tmp = malloc(sizeof(uint64_t) * N), *e = malloc(sizeof(uint64_t) * N);
+    uint64_t *sq = calloc((size_t)N, sizeof(uint64_t)), *a = malloc(sizeof(uint64_t) * N);
+    uint64_t *ss = malloc(sizeof(uint64_t) * N);
+    int64_t *ev = malloc(sizeof(int64_t) * N);
+    for (int j = 0; j < 2; j++) {
+        const uint64_t obj = 2 * r + (uint64_t)j;
+        or_sample(seed, P_GK1_E, obj, 0, 2, N, 0, (uint64_t *)ev);
+        if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = C->q[l];
+            for (int k = 0; k < N; k++) { sq[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+            or_sample(seed, P_GK1_A, obj, (uint32_t)l, 0, N, q, a);
+            uint64_t *b = out + (((size_t)j * 2 + 0) * 3 + l) * N, *aa = out + (((size_t)j * 2 + 1) * 3 + l) * N;
+            poly_mul(&C->R[l], a, sq, tmp);
+            poly_sub(q, N, e, tmp, b);
+            if (l == j) {
+                automorphism(q, N, sq, g, ss);
+                poly_scale(q, N, ss, C->P_mod[l], tmp);
+                poly_add(q, N, b, tmp, b);
+            }
+            memcpy(aa, a, sizeof(uint64_t) * N);
+        }
+    }
+    free(tmp); free(e); free(sq); free(a); free(ss); free(ev);
+}
+
+/* modulus / ring of a 4-limb key-switching limb (0 q0, 1 q1, 2 q2, 3 P) */
+static uint64_t l4_q(const ctx2_t *x, int l) { return l == 3 ? x->c.q[2] : l2_q(x, l); }
+static const ring_t *l4_R(const ctx2_t *x, int l) { return l == 3 ? &x->c.R[2] : l2_R(x, l); }
+
+/* Compression keys: rlk2 (3 digits over {q0,q1,q2,P}: b = -a s + e + [l = j](P mod q_l) s^2, a from
+ * (P_RLK2_A, object j, sub-stream l), e from (P_RLK2_E, object j)); the ladder's level-1 Galois keys;
+ * the level-0 keys of the right rotations by u = 1..s-1. */
+int or_keygen_cmp(int logN, uint64_t seed, int d, int p, int zero_error, uint64_t *rlk2, uint64_t *gkl, uint64_t *gkc)
+{
+    if (p <= 0 || d % p) return -1;
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    const ctx_t *C = &X.c;
+    const int N = C->N, S = N / 2, s = d / p;
+    uint64_t *tmp = malloc(sizeof(uint64_t) * N), *e = malloc(sizeof(uint64_t) * N);
+    uint64_t *sq = calloc((size_t)N, sizeof(uint64_t)), *a = malloc(sizeof(uint64_t) * N);
+    uint64_t *s2 = malloc(sizeof(uint64_t) * N);
+    int64_t *sv = malloc(sizeof(int64_t) * N), *ev = malloc(sizeof(int64_t) * N);
+    or_sample(seed, P_SK, 0, 0, 1, N, 0, (uint64_t *)sv);
+    for (int j = 0; j < 3; j++) {
+        or_sample(seed, P_RLK2_E, (uint64_t)j, 0, 2, N, 0, (uint64_t *)ev);
+        if (zero_error) memset(ev, 0, sizeof(int64_t) * N);
+        for (int l = 0; l < 4; l++) {
+            const uint64_t q = l4_q(&X, l);
+            for (int k = 0; k < N; k++) { sq[k] = from_signed(sv[k], q); e[k] = from_signed(ev[k], q); }
+            or_sample(seed, P_RLK2_A, (uint64_t)j, (uint32_t)l, 0, N, q, a);
+            uint64_t *b = rlk2 + (((size_t)j * 2 + 0) * 4 + l) * N, *aa = rlk2 + (((size_t)j * 2 + 1) * 4 + l) * N;
+            poly_mul(l4_R(&X, l), a, sq, tmp);
+            poly_sub(q, N, e, tmp, b);
+            if (l == j) {
+                poly_mul(l4_R(&X, l), sq, sq, s2);
+                poly_scale(q, N, s2, C->q[2] % q, tmp);
+                poly_add(q, N, b, tmp, b);
+            }
+            memcpy(aa, a, sizeof(uint64_t) * N);
+        }
+    }
+    int log_s = 0;
+    while ((1 << log_s) < s) log_s++;
+    for (int i = 0; i < log_s; i++) galois_key1(C, seed, (uint64_t)1 << i, zero_error, sv, gkl + (size_t)i * 12 * N);
+    for (int u = 1; u < s; u++)
+        galois_key(C, seed, (uint64_t)(S - u), (uint64_t)(CMP_OBJ + u), zero_error, sv, gkc + (size_t)(u - 1) * 4 * N);
+    free(tmp); free(e); free(sq); free(a); free(s2); free(sv); free(ev);
+    ctx2_free(&X);
+    return 0;
+}
+
+/* Relinearization at level 2 (3 digits) followed by Res by q2 (level 2 -> 1), the textbook way:
+ * x_j = [d2]_{q_j} in [0, q_j) lifted to {q0,q1,q2,P}; KS_c = sum_j x_j rlk2_j[c]; ModDown by P to
+ * {q0,q1,q2}; c_c = d_c + KS'_c; then (c_c[q_k] - centred_{q2}(c_c[q2])) q2^-1 mod q_k.
+ * d [3][3][N] -> out [2][2][N]. */
+static void relin_rescale_l2(const ctx2_t *X, const uint64_t *d, const uint64_t *rlk2, uint64_t *out)
+{
+    const int N = X->c.N;
+    const uint64_t P = X->c.q[2];
+    uint64_t *KS = malloc(sizeof(uint64_t) * 4 * N), *x = malloc(sizeof(uint64_t) * N);
+    uint64_t *t = malloc(sizeof(uint64_t) * N), *cc = malloc(sizeof(uint64_t) * 3 * N);
+    for (int c = 0; c < 2; c++) {
+        memset(KS, 0, sizeof(uint64_t) * 4 * N);
+        for (int j = 0; j < 3; j++) {
+            const uint64_t *xj = d + (size_t)(2 * 3 + j) * N; /* [d2]_{q_j}, in [0, q_j) */
+            for (int l = 0; l < 4; l++) {
+                const uint64_t q = l4_q(X, l);
+                for (int k = 0; k < N; k++) x[k] = xj[k] % q;
+                poly_mul(l4_R(X, l), x, rlk2 + (((size_t)j * 2 + c) * 4 + l) * N, t);
+                poly_add(q, N, KS + (size_t)l * N, t, KS + (size_t)l * N);
+            }
+        }
+        /* ModDown by P to the three Q limbs, added to d_c */
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = l2_q(X, l), pinv = invmod(P % q, q);
+            for (int k = 0; k < N; k++) {
+                uint64_t y = from_signed(centred(KS[(size_t)3 * N + k], P), q);
+                uint64_t ks = mulmod(submod(KS[(size_t)l * N + k], y, q), pinv, q);
+                cc[(size_t)l * N + k] = addmod(d[(size_t)(c * 3 + l) * N + k], ks, q);
+            }
+        }
+        /* Res by q2 */
+        for (int l = 0; l < 2; l++) {
+            const uint64_t q = X->c.q[l];
+            for (int k = 0; k < N; k++) {
+                uint64_t z = from_signed(centred(cc[(size_t)2 * N + k], X->q2), q);
+                out[(size_t)(c * 2 + l) * N + k] = mulmod(submod(cc[(size_t)l * N + k], z, q), X->q2_inv[l], q);
+            }
+        }
+    }
+    free(KS); free(x); free(t); free(cc);
+}
+void or_relin_rescale_l2(int logN, const uint64_t *d, const uint64_t *rlk2, uint64_t *out)
+{
+    ctx2_t X; ctx2_init(&X, logN); relin_rescale_l2(&X, d, rlk2, out); ctx2_free(&X);
+}
+
+/* HE-C^3 of one (query, set) pair one level up (hoisted order, reading R8): level-2 inputs
+ * qct, sct [p][2][3][N] -> tensor over 3 limbs -> relin_rescale_l2 -> log2(s) ladder steps
+ * C = C + Rot(C, 2^(i-1)) at level 1 (rotate1, keys gkl).  out [2][2][N] (level 1). */
+static void he_c3_pair_l2(const ctx2_t *X, int p, int log_s, const uint64_t *rlk2, const uint64_t *gkl,
+                          const uint64_t *qct, const uint64_t *sct, uint64_t *out)
+{
+    const int N = X->c.N;
+    uint64_t *d = calloc((size_t)9 * N, sizeof(uint64_t)), *t = malloc(sizeof(uint64_t) * N);
+    uint64_t *rot = malloc(sizeof(uint64_t) * 4 * N);
+    for (int i = 0; i < p; i++) {
+        const uint64_t *ca = qct + (size_t)i * 6 * N, *cb = sct + (size_t)i * 6 * N;
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = l2_q(X, l);
+            const ring_t *R = l2_R(X, l);
+            const uint64_t *a0 = ca + (size_t)l * N, *a1 = ca + (size_t)(3 + l) * N;
+            const uint64_t *b0 = cb + (size_t)l * N, *b1 = cb + (size_t)(3 + l) * N;
+            uint64_t *d0 = d + (size_t)l * N, *d1 = d + (size_t)(3 + l) * N, *d2 = d + (size_t)(6 + l) * N;
+            poly_mul(R, a0, b0, t); poly_add(q, N, d0, t, d0);
+            poly_mul(R, a0, b1, t); poly_add(q, N, d1, t, d1);
+            poly_mul(R, a1, b0, t); poly_add(q, N, d1, t, d1);
+            poly_mul(R, a1, b1, t); poly_add(q, N, d2, t, d2);
+        }
+    }
+    relin_rescale_l2(X, d, rlk2, out);
+    for (int i = 1; i <= log_s; i++) {
+        rotate1(&X->c, out, (uint64_t)1 << (i - 1), gkl + (size_t)(i - 1) * 12 * N, rot);
+        for (int cl = 0; cl < 4; cl++)
+            poly_add(X->c.q[cl & 1], N, out + (size_t)cl * N, rot + (size_t)cl * N, out + (size_t)cl * N);
+    }
+    free(d); free(t); free(rot);
+}
+
+/* Compression of one result: level 1 C_t -> Res_q1(Mul(P)(C_t, M)) (level 0), then the
+ * right rotation by u = t mod s (left rotation by S - u, key gkc[u-1]); out [2][1][N] */
+static void compress_one(const ctx2_t *X, int u, const int64_t *mask, const uint64_t *gkc, const uint64_t *in,
+                         uint64_t *out)
+{
+    const int N = X->c.N;
+    uint64_t *m = malloc(sizeof(uint64_t) * N), *t = malloc(sizeof(uint64_t) * 4 * N);
+    uint64_t *r0 = malloc(sizeof(uint64_t) * 2 * N);
+    for (int cl = 0; cl < 4; cl++) {
+        const uint64_t q = X->c.q[cl & 1];
+        for (int k = 0; k < N; k++) m[k] = from_signed(mask[k], q);
+        poly_mul(&X->c.R[cl & 1], in + (size_t)cl * N, m, t + (size_t)cl * N);
+    }
+    rescale(&X->c, t, u ? r0 : out);
+    if (u) rotate(&X->c, r0, (uint64_t)(N / 2 - u), gkc + (size_t)(u - 1) * 4 * N, out);
+    free(m); free(t); free(r0);
+}
+
+typedef struct {
+    const ctx2_t *X;
+    int p, log_s, s;
+    const uint64_t *rlk2, *gkl, *gkc, *db, *q;
+    const int64_t *mask;
+    int64_t n_sets, nq, n_groups;
+    uint64_t *out;
+    int64_t next;
+    pthread_mutex_t mu;
+} cjob_t;
+
+static void *cworker(void *arg)
+{
+    cjob_t *J = (cjob_t *)arg;
+    const int N = J->X->c.N, p = J->p, s = J->s;
+    const size_t st = (size_t)p * 6 * N;
+    uint64_t *C = malloc(sizeof(uint64_t) * 4 * N), *o = malloc(sizeof(uint64_t) * 2 * N);
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        int64_t w = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (w >= J->nq * J->n_groups) break;
+        const int64_t qi = w / J->n_groups, g = w % J->n_groups;
+        uint64_t *acc = J->out + (size_t)w * 2 * N;
+        memset(acc, 0, sizeof(uint64_t) * 2 * N);
+        for (int u = 0; u < s; u++) {
+            const int64_t t = g * s + u;
+            if (t >= J->n_sets) break;
+            he_c3_pair_l2(J->X, p, J->log_s, J->rlk2, J->gkl, J->q + (size_t)qi * st, J->db + (size_t)t * st, C);
+            compress_one(J->X, u, J->mask, J->gkc, C, o);
+            poly_add(J->X->c.q[0], 2 * N, acc, o, acc);
+        }
+    }
+    free(C); free(o);
+    return NULL;
+}
+
+/* The compressed scan: db [n_sets][p][2][3][N] and q [nq][p][2][3][N] at level 2 ->
+ * out [nq][ceil(n_sets / s)][2][1][N] (level 0): packed ciphertext g holds, at slot k s + u, the
+ * score of set g s + u's block k. */
+int or_match_cmp(int logN, int d, int p, const uint64_t *rlk2, const uint64_t *gkl, const uint64_t *gkc,
+                 const int64_t *mask, const uint64_t *db, int64_t n_sets, const uint64_t *q, int64_t nq, uint64_t *out,
+                 int n_threads)
+{
+    if (p <= 0 || d % p) return -1;
+    const int s = d / p;
+    int log_s = 0;
+    while ((1 << log_s) < s) log_s++;
+    if ((1 << log_s) != s) return -1;
+    ctx2_t X;
+    ctx2_init(&X, logN);
+    cjob_t J;
+    memset(&J, 0, sizeof J);
+    J.X = &X; J.p = p; J.log_s = log_s; J.s = s; J.rlk2 = rlk2; J.gkl = gkl; J.gkc = gkc; J.db = db; J.q = q;
+    J.mask = mask; J.n_sets = n_sets; J.nq = nq; J.n_groups = (n_sets + s - 1) / s; J.out = out;
+    pthread_mutex_init(&J.mu, NULL);
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int i = 0; i < n_threads; i++) pthread_create(&th[i], NULL, cworker, &J);
+    for (int i = 0; i < n_threads; i++) pthread_join(th[i], NULL);
+    free(th);
+    pthread_mutex_destroy(&J.mu);
+    ctx2_free(&X);
+    return 0;
+}

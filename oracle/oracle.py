@@ -93,6 +93,14 @@ def lib():
         L.or_enroll.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _u64p, _u64p, ctypes.c_int64,
                                 ctypes.c_int64, _u64p, ctypes.c_int64]
         L.or_enroll.restype = ctypes.c_int
+        # f1: compression, with HE-C^3 one level up
+        L.or_keygen_cmp.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p,
+                                    _u64p, _u64p]
+        L.or_keygen_cmp.restype = ctypes.c_int
+        L.or_relin_rescale_l2.argtypes = [ctypes.c_int, _u64p, _u64p, _u64p]
+        L.or_match_cmp.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p, _i64p, _u64p,
+                                   ctypes.c_int64, _u64p, ctypes.c_int64, _u64p, ctypes.c_int]
+        L.or_match_cmp.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -489,3 +497,72 @@ def enroll(logN, d, p, emasks, gk1, ct, first_u, db):
     if rc:
         raise ValueError(f"or_enroll: {rc}")
     return db
+
+
+# ---------------------------------------------------------------------------- f1: output compression
+# PAPER.md:273, 343-345 and SPEC.md:321-329 (reading R28), same extended chain: HE-C^3 runs at
+# level 2 (Res by q2), its ladder at level 1, and the compression's Mul(P) + Res by q1 ends at level 0.
+def keygen_cmp(logN, seed, d, p, zero_error=False):
+    """rlk2 [3][2][4 limbs q0,q1,q2,P][N]; gkl [log2 s][2][2][3][N] (level-1 ladder keys 2^i);
+    gkc [s-1][2][2 limbs q0,P][N] (level-0 right rotations by u = 1..s-1)."""
+    N = 1 << logN
+    S, s, _ = layout(logN, d, p)
+    ls = log2_exact(s)
+    rlk2 = np.zeros((3, 2, 4, N), np.uint64)
+    gkl = np.zeros((max(ls, 1), 2, 2, 3, N), np.uint64)
+    gkc = np.zeros((max(s - 1, 1), 2, 2, N), np.uint64)
+    rc = lib().or_keygen_cmp(logN, seed, d, p, int(zero_error), _p(rlk2, _u64p), _p(gkl, _u64p), _p(gkc, _u64p))
+    if rc:
+        raise ValueError(f"or_keygen_cmp: {rc}")
+    return rlk2, gkl[:ls], gkc[:s - 1]
+
+
+def relin_rescale_l2(logN, d3, rlk2):
+    """(d0, d1, d2) at level 2 [3][3][N] -> relinearized, Res by q2: [2][2][N] (level 1)."""
+    d3 = np.ascontiguousarray(d3, np.uint64)
+    out = np.zeros((2, 2, 1 << logN), np.uint64)
+    lib().or_relin_rescale_l2(logN, _p(d3, _u64p), _p(np.ascontiguousarray(rlk2, np.uint64), _u64p), _p(out, _u64p))
+    return out
+
+
+def cmp_mask(logN, d, p):
+    """M[x] = [x mod s = 0] at scale q1 (the compression's score mask)."""
+    S, s, _ = layout(logN, d, p)
+    z = (np.arange(S) % s == 0).astype(np.float64)
+    return encode(z, logN, scale=float(primes()[1]))
+
+
+def match_cmp(logN, d, p, rlk2, gkl, gkc, mask, db, q, n_threads=1):
+    """Compressed scan: db [T][p][2][3][N], q [Q][p][2][3][N] (level 2) -> [Q][ceil(T/s)][2][1][N]."""
+    N = 1 << logN
+    S, s, _ = layout(logN, d, p)
+    db = np.ascontiguousarray(db, np.uint64)
+    q = np.ascontiguousarray(q, np.uint64)
+    T, Q = db.shape[0], q.shape[0]
+    G = -(-T // s)
+    out = np.zeros((Q, G, 2, 1, N), np.uint64)
+    pad = lambda a, shape: np.ascontiguousarray(a if len(a) else np.zeros(shape, np.uint64), np.uint64)
+    rc = lib().or_match_cmp(logN, d, p, _p(np.ascontiguousarray(rlk2, np.uint64), _u64p),
+                            _p(pad(gkl, (1, 2, 2, 3, N)), _u64p), _p(pad(gkc, (1, 2, 2, N)), _u64p),
+                            _p(np.ascontiguousarray(mask, np.int64), _i64p), _p(db, _u64p), T, _p(q, _u64p), Q,
+                            _p(out, _u64p), n_threads)
+    if rc:
+        raise ValueError(f"or_match_cmp: {rc}")
+    return out
+
+
+def packed_scores(logN, d, p, sk, packed, n_sets):
+    """Decrypt packed results [G][2][1][N] -> scores [n_sets * B] (set t = g s + u, block k at slot
+    k s + u of packed g), scale 2^80 / q2."""
+    S, s, B = layout(logN, d, p)
+    q0, q1, P = primes()
+    scale = DELTA * DELTA / q2()
+    sc = np.zeros(n_sets * B)
+    for g in range(packed.shape[0]):
+        m = decrypt(logN, sk, packed[g], 1)[0]
+        z = decode_slots(centred_i64(m, q0), logN, scale)
+        for u in range(s):
+            t = g * s + u
+            if t < n_sets:
+                sc[t * B:(t + 1) * B] = z[u::s][:B]
+    return sc
