@@ -257,6 +257,41 @@ size_t bm_enroll_ws_bytes(const bm_params *, int64_t n);
 int bm_enroll(const bm_params *, const bm_xk_dev *, const uint64_t *d_in, int64_t n, int64_t first_template,
               uint64_t *d_db, int64_t n_sets, void *d_ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * f1: OUTPUT COMPRESSION (DESIGN.md
+ * reading R28), on the same extended chain: HE-C^3 runs one level higher -- level-2 DB and query
+ * parts (bm_encrypt_l2 of bm_encode_db / bm_encode_query plaintexts), tensor over three limbs,
+ * 3-digit relinearisation and Res by q2, the ladder at level 1 -- and then every set's result C_t
+ * is compressed: Res_q1(Mul(P)(C_t, M)), M[x] = [x mod s = 0] (the score slots), rotated right by
+ * t mod s at level 0 and added into packed ciphertext t / s.  Packed ciphertext g holds, at slot
+ * k s + u, the score of set g s + u's block k; every other slot of the uncompressed output (the
+ * partial sums) is masked away, and the output is s times smaller.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct bm_ck bm_ck;           /* host: rlk2 (3 digits), ladder keys at level 1, rotation keys */
+typedef struct bm_ck_dev bm_ck_dev;
+
+/* Keys for keygen(seed)'s secret: rlk2_j (j < 3) over {q0,q1,q2,P}: (-a s + e + [l = j](P mod q_l)
+ * s^2, a); the level-1 Galois keys of 2^i, i < log2 s (the f3 family); the level-0 Galois keys of the
+ * right rotations by u = 1..s-1 (left by S - u).  Export layouts: rlk2 [3][2][4 limbs q0,q1,q2,P][N],
+ * gkl [log2 s][2][2][3 limbs q0,q1,P][N], gkc [s-1][2][2 limbs q0,P][N]. */
+int bm_ck_keygen(const bm_params *, uint64_t seed, bm_ck **out);
+void bm_ck_free(bm_ck *);
+int bm_ck_export(const bm_ck *, uint64_t *rlk2, uint64_t *gkl, uint64_t *gkc);
+/* The score mask M at scale q1 (int64 [N]). */
+int bm_encode_cmp_mask(const bm_params *, int64_t *pt);
+/* Upload keys and mask (synchronous).  Errors: BM_ERR_KEY_MISMATCH, BM_ERR_CUDA, BM_ERR_OOM. */
+int bm_ck_to_device(const bm_params *, const bm_ck *, const int64_t *h_mask, bm_ck_dev **out);
+void bm_ck_dev_free(bm_ck_dev *);
+/* The compressed scan: d_db [n_sets][p][2][3][N], d_q [nq][p][2][3][N] (level 2, NTT) ->
+ * d_out [nq][ceil(n_sets / s)][2][N] (level 0, COEFFICIENT domain, scale 2^80 / q2; overwritten).
+ * Asynchronous, allocates nothing; d_ws of bm_match_cmp_ws_bytes(...) bytes.  Errors as bm_match. */
+size_t bm_match_cmp_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq);
+int bm_match_cmp(const bm_params *, const bm_ck_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+                 int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, void *stream);
+/* Client: decrypt n packed results h_ct [n][2][1][N] and decode ALL S slots into slots [n][S]
+ * (slot k s + u of packed ciphertext g = score of set g s + u, block k). */
+int bm_decrypt_packed(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, double *slots);
+
 int bm_sync(void *stream);
 const char *bm_strerror(int status);
 /* Library build information ("sm_100a", git hash...) */

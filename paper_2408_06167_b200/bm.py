@@ -91,6 +91,14 @@ _SIGS = {
     "bm_encrypt_l2": (_i32, [_P, _vp, _vp, _i64, _u64, _u64, _vp, _vp]),
     "bm_expand_ws_bytes": (_sz, [_P, _i32]),
     "bm_expand": (_i32, [_P, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    # f1: output compression (HE-C^3 one level up)
+    "bm_ck_keygen": (_i32, [_P, _u64, _pp]), "bm_ck_free": (None, [_vp]),
+    "bm_ck_export": (_i32, [_vp, _vp, _vp, _vp]),
+    "bm_encode_cmp_mask": (_i32, [_P, _vp]),
+    "bm_ck_to_device": (_i32, [_P, _vp, _vp, _pp]), "bm_ck_dev_free": (None, [_vp]),
+    "bm_match_cmp_ws_bytes": (_sz, [_P, _i64, _i32]),
+    "bm_match_cmp": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "bm_decrypt_packed": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_sync": (_i32, [_vp]),
     "bm_strerror": (ctypes.c_char_p, [_i32]),
     "bm_build_info": (ctypes.c_char_p, []),
@@ -156,6 +164,14 @@ class PublicKeyDev(_Handle):
 
 class EvalKeyDev(_Handle):
     _free = "bm_evk_dev_free"
+
+
+class CompressKey(_Handle):
+    _free = "bm_ck_free"
+
+
+class CompressKeyDev(_Handle):
+    _free = "bm_ck_dev_free"
 
 
 class ExpandKey(_Handle):
@@ -459,3 +475,52 @@ def bm_enroll(prm, xk_dev, d_in, first_template, d_db, d_ws, stream=None):
     ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
     _chk(_lib.bm_enroll(ctypes.byref(prm), xk_dev.ptr, _dptr(d_in) if n else None, n, first_template, _dptr(d_db),
                         d_db.shape[0], _dptr(d_ws) if ws_bytes else None, ws_bytes, _stream(stream)), "bm_enroll")
+
+
+# --------------------------------------------------------------------------- f1: output compression
+def bm_ck_keygen(prm, seed):
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_ck_keygen(ctypes.byref(prm), seed, ctypes.byref(out)), "bm_ck_keygen")
+    return CompressKey(out)
+
+
+def bm_ck_export(prm, ck):
+    rlk2 = np.zeros((3, 2, 4, N), np.uint64)
+    gkl = np.zeros((max(prm.log_s, 1), 2, 2, 3, N), np.uint64)
+    gkc = np.zeros((max(prm.s - 1, 1), 2, 2, N), np.uint64)
+    _chk(_lib.bm_ck_export(ck.ptr, _np_ptr(rlk2), _np_ptr(gkl), _np_ptr(gkc)), "bm_ck_export")
+    return rlk2, gkl[:prm.log_s], gkc[:prm.s - 1]
+
+
+def bm_encode_cmp_mask(prm):
+    out = np.zeros(N, np.int64)
+    _chk(_lib.bm_encode_cmp_mask(ctypes.byref(prm), _np_ptr(out)), "bm_encode_cmp_mask")
+    return out
+
+
+def bm_ck_to_device(prm, ck, mask=None):
+    m = np.ascontiguousarray(bm_encode_cmp_mask(prm) if mask is None else mask, np.int64)
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_ck_to_device(ctypes.byref(prm), ck.ptr, _np_ptr(m), ctypes.byref(out)), "bm_ck_to_device")
+    return CompressKeyDev(out)
+
+
+def bm_match_cmp_ws_bytes(prm, n_sets, nq):
+    return int(_lib.bm_match_cmp_ws_bytes(ctypes.byref(prm), n_sets, nq))
+
+
+def bm_match_cmp(prm, ck_dev, d_db, n_sets, d_q, nq, d_out, d_ws, stream=None):
+    """f1: level-2 DB / query parts -> packed level-0 results d_out [nq][ceil(n_sets/s)][2][N]."""
+    ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
+    _chk(_lib.bm_match_cmp(ctypes.byref(prm), ck_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
+                           _dptr(d_q) if nq else None, nq, _dptr(d_out) if nq * n_sets else None,
+                           _dptr(d_ws) if ws_bytes else None, ws_bytes, _stream(stream)), "bm_match_cmp")
+
+
+def bm_decrypt_packed(prm, sk, h_ct):
+    """h_ct: uint64 [n][2][1][N] packed results -> all S slots float64 [n][S]."""
+    h_ct = np.ascontiguousarray(h_ct, np.uint64)
+    n = h_ct.size // (2 * N)
+    out = np.zeros((n, SLOTS), np.float64)
+    _chk(_lib.bm_decrypt_packed(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt_packed")
+    return out

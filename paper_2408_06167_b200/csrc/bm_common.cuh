@@ -28,7 +28,8 @@ constexpr uint64_t Q2 = 1099510890497ull;       // 2^40 - 737279 = 2^40 - 45 2^1
 enum : uint32_t {
     P_SK = 1, P_PK_A = 2, P_PK_E = 3, P_RLK_A = 4, P_RLK_E = 5, P_GK_A = 6, P_GK_E = 7,
     P_ENC_U = 8, P_ENC_E0 = 9, P_ENC_E1 = 10,
-    P_GK1_A = 11, P_GK1_E = 12 // f3: level-1 Galois keys of the expansion strides
+    P_GK1_A = 11, P_GK1_E = 12, // f3/f4/f1: level-1 Galois keys
+    P_RLK2_A = 13, P_RLK2_E = 14 // f1: 3-digit relinearisation key at level 2
 };
 
 // ---------------------------------------------------------------- ChaCha20 (RFC 8439 sec. 2.3)

@@ -51,3 +51,11 @@ struct bm_xk {
     std::vector<uint64_t> pk_q2; // [2][N]
     std::vector<uint64_t> gk1;   // [n_rot][2 digits][2 comps][3 limbs q0,q1,P][N]
 };
+// f1 compression keys (reading R28)
+struct bm_ck {
+    uint8_t digest[32];
+    int32_t d, p, log_s;
+    std::vector<uint64_t> rlk2; // [3 digits][2 comps][4 limbs q0,q1,q2,P][N]
+    std::vector<uint64_t> gkl;  // [log_s][2 digits][2 comps][3 limbs q0,q1,P][N]
+    std::vector<uint64_t> gkc;  // [s-1][2 comps][2 limbs q0,P][N]
+};

@@ -37,7 +37,7 @@ __constant__ uint64_t c_cdt[19];
 //   XU  [4][N]     ModUp'd digits x0~[q1], x0~[P], x1~[q0], x1~[P] (NTT)   K2 -> K3
 // The paper order adds a level-0 accumulator ACC [2][N] (K3 sums into it across parts).
 struct MatchK {
-    PrimeK pr[3];
+    PrimeK pr[4];       // q0, q1, P, q2 (f1)
     ulonglong2 pinv[2]; // P^-1 mod q0, q1
     ulonglong2 q1inv;   // q1^-1 mod q0
     uint64_t pmod[2];   // P mod q0, q1
@@ -50,6 +50,7 @@ struct MatchK {
     int32_t p;
     BM_D int64_t out_row(int64_t pi) const { return (jq0 + pi / ct) * n_sets + t0 + pi % ct; }
     uint64_t *D01, *D2, *XC, *XU, *ACC;
+    uint64_t *XR, *XO;  // f1: level-0 masked results (NTT), rotated results (coefficients)
 };
 
 // a level-0 ciphertext buffer inside the workspace: pair pi, component c at base + pi*stride + c*N
@@ -92,7 +93,7 @@ BM_D uint64_t red128(u128 v, const PrimeK &P) { return reduce128((uint64_t)(v >>
 // x mod q for any x < 2^64, canonical (q1: fold 2^40 = c1 once so that reduce_bnd's x < 2^62 holds)
 template <int PI> BM_D uint64_t reduce_any(uint64_t x)
 {
-    if (PI == 1) x = (x & ((1ull << 40) - 1)) + (x >> 40) * ((1ull << 40) - Q1); // < 2^40 + 2^24 c1 < 2^43
+    if (Q40<PI>) x = (x & ((1ull << 40) - 1)) + (x >> 40) * ((1ull << 40) - PrimeC<PI>::q); // < 2^40 + 2^44
     return reduce_bnd<PI>(x);
 }
 // v mod q for a 128-bit v with the prime-specialised lazy Shoup product: hi (2^64 mod q) + lo
@@ -133,12 +134,16 @@ BM_D uint64_t f64_mod_q1(double x)
 // grid: ((qt * (N / CS) + slice) * nst + st) * 2 + l  (limbs alternate, so each SM holds one
 // q0-limb CTA on the integer pipe and one q1-limb CTA on the FP64 pipe; set tiles next: the CTAs
 // that share a query slice run together and the query data streams from HBM once)
-template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st, int part_lo,
+// NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
+// pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe
+template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st, int part_lo,
                                        int part_hi)
 {
     const int tid = threadIdx.x;
     const int c0 = sl * CS;
-    const PrimeK &P = K.pr[L];
+    constexpr int PI = L == 2 ? 3 : L;
+    constexpr bool INTL = L != 1;
+    const PrimeK &P = K.pr[PI];
     // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
     const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
     u128 a0[2][2], a1[2][2], a2[2][2];     // q0: 128-bit integer sums
@@ -147,7 +152,7 @@ template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *
     for (int u = 0; u < 2; u++)
 #pragma unroll
         for (int v = 0; v < 2; v++) {
-            if (L == 0) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+            if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
             else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
         }
 #pragma unroll 1
@@ -165,15 +170,15 @@ template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *
             if (tr < TQB) {
                 int64_t a = (int64_t)qt * TQB + tr;
                 a = a < K.cq ? a : K.cq - 1;
-                src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 4 * N;
+                src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 2 * NL * N;
                 dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
             } else {
                 int64_t bb = (int64_t)st * TSB + (tr - TQB);
                 bb = bb < K.ct ? bb : K.ct - 1;
-                src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 4 * N;
+                src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 2 * NL * N;
                 dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
             }
-            cp_async16(dst + 2 * ch, src + (size_t)(2 * comp + L) * N + c0 + 2 * ch);
+            cp_async16(dst + 2 * ch, src + (size_t)(NL * comp + L) * N + c0 + 2 * ch);
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
@@ -193,7 +198,7 @@ template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *
                 y0[v] = r[0];
                 y1[v] = r[CS];
             }
-            if (L == 0) {
+            if (INTL) {
 #pragma unroll
                 for (int u = 0; u < 2; u++)
 #pragma unroll
@@ -224,10 +229,10 @@ template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
-                    if (L == 0) {
-                        a0[u][v] = red128s<0>(a0[u][v], P.r64);
-                        a1[u][v] = red128s<0>(a1[u][v], P.r64);
-                        a2[u][v] = red128s<0>(a2[u][v], P.r64);
+                    if (INTL) {
+                        a0[u][v] = red128s<PI>(a0[u][v], P.r64);
+                        a1[u][v] = red128s<PI>(a1[u][v], P.r64);
+                        a2[u][v] = red128s<PI>(a2[u][v], P.r64);
                     } else {
                         f0[u][v] = (double)f64_mod_q1(f0[u][v]);
                         f1[u][v] = (double)f64_mod_q1(f1[u][v]);
@@ -247,35 +252,36 @@ template <int L> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *
             const int64_t pi = a * K.ct + bb;
             const int j = c0 + c;
             uint64_t d0, d2, kk;
-            if (L == 0) {
-                d0 = red128s<0>(a0[u][v], P.r64);
-                d2 = red128s<0>(a2[u][v], P.r64);
-                kk = red128s<0>(a1[u][v], P.r64);
+            if (INTL) {
+                d0 = red128s<PI>(a0[u][v], P.r64);
+                d2 = red128s<PI>(a2[u][v], P.r64);
+                kk = red128s<PI>(a1[u][v], P.r64);
             } else {
                 d0 = f64_mod_q1(f0[u][v]);
                 d2 = f64_mod_q1(f2[u][v]);
                 kk = f64_mod_q1(f1[u][v]);
             }
-            K.D01[((size_t)pi * 4 + 0 + L) * N + j] = d0;
-            K.D01[((size_t)pi * 4 + 2 + L) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
-            K.D2[((size_t)pi * 2 + L) * N + j] = d2;
+            K.D01[((size_t)pi * 2 * NL + 0 + L) * N + j] = d0;
+            K.D01[((size_t)pi * 2 * NL + NL + L) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
+            K.D2[((size_t)pi * NL + L) * N + j] = d2;
         }
 }
 
-__global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
+template <int NL> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
     uint64_t *Qs = sm, *Ss = sm + TQB * PCH * 2 * CS; // [tile row][part][comp][CS]
     const int nst = (int)((K.ct + TSB - 1) / TSB);
     int64_t b = blockIdx.x;
-    const int l = (int)(b & 1);
-    b >>= 1;
+    const int l = (int)(b % NL);
+    b /= NL;
     const int st = (int)(b % nst);
     b /= nst;
     const int sl = (int)(b % (N / CS));
     const int qt = (int)(b / (N / CS));
-    if (l == 0) tensor_tile<0>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
-    else tensor_tile<1>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
+    if (l == 0) tensor_tile<0, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
+    else if (l == 1) tensor_tile<1, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
+    else if (NL == 3) tensor_tile<2, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
 }
 
 // ================================================================== prime-specialised pointwise helpers
@@ -898,6 +904,295 @@ __global__ void __launch_bounds__(256) k_enroll_add(const uint64_t *W, int64_t u
     *dst = acc;
 }
 
+// ================================================================== f1: output compression
+// SURVEY.md sec. 8f row f1 (reading R28): HE-C^3 one
+// level up on the extended chain, then the compression.  Per chunk of (query, set) pairs:
+//   k_tensor<3>                        tensor + part sum over the three level-2 limbs
+//   C1 k_digits3   (pair, digit j)     x_j = INTT_{q_j}(d2[q_j]), ModUp to the other two Q primes and P
+//   C2 k_relin3    (pair, c)           KS_c over {q0,q1,q2,P} (rlk2, P^-1 in its Q limbs), ModDown fused
+//                                      with Res by q2 (the R22 rewriting with q2 in q1's role): level 1
+//   ladder at level 1: log2 s x (k_rot1_digits, k_rot1_ks) with the ladder's level-1 Galois keys
+//   C3 k_cmp_mask  (pair, c)           Res_q1(Mul(P)(C, M)): level 0 (q1^-1 folded into M's q0 limb)
+//   C4 k_cmp_rot   (pair)              right rotation by u = t mod s (left by S - u) at level 0 and the
+//                                      output INTT (u = 0: the INTT only); coefficient domain
+//   C5 k_cmp_add                        packed[g] += the s rotated results of group g
+constexpr int D2X_POLYS = 9; // XU at level 2: per digit j its 3 ModUp targets (other two Q limbs, P)
+constexpr size_t C1_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+constexpr size_t C2_SMEM_BYTES = (SMEM_WORDS + 2 * (size_t)N) * sizeof(uint64_t);
+constexpr size_t C4_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+
+BM_D uint32_t pow5_mod2n(uint32_t r) // 5^r mod 2N
+{
+    uint32_t x = 1, b = 5;
+    for (; r; r >>= 1, b = (b * b) & (2 * N - 1))
+        if (r & 1) x = (x * b) & (2 * N - 1);
+    return x;
+}
+
+struct CmpK {
+    MatchK m;                 // pr[4], pinv[2], q1inv, D01/D2/XU/XC/XR/XO, chunk geometry
+    ulonglong2 pinv2;         // P^-1 mod q2
+    ulonglong2 q2inv[2];      // q2^-1 mod q0, q1
+    const ulonglong2 *rlk2;   // [3 j][2 c][4 limbs q0,q1,q2,P][N]
+    const ulonglong2 *gkc;    // [s-1][2 c][2 limbs q0,P][N]
+    const ulonglong2 *mask;   // [2 limbs q0,q1][N], q1^-1 in the q0 limb
+    uint64_t *scr;            // [pairs][2][N] scratch of k_cmp_rot
+    int s;
+};
+
+__global__ void __launch_bounds__(T, 1) k_digits3(CmpK C)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *xs = sm + SMEM_WORDS;
+    const MatchK &K = C.m;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x / 3;
+    const int j = (int)(blockIdx.x % 3);
+    uint64_t a[E];
+    load_eval(a, K.D2 + ((size_t)pi * 3 + j) * N);
+    uint64_t *xu = K.XU + ((size_t)pi * D2X_POLYS + 3 * j) * N; // targets: other Q limbs ascending, then P
+    if (j == 0) inv<0>(a, sm, K.pr[0]);
+    else if (j == 1) inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
+    else inv<3>(a, sm, K.pr[3]);
+#pragma unroll
+    for (int e = 0; e < E; e++) xs[tid + T * e] = a[e]; // x_j in [0, q_j), non-centred (reading R4)
+#pragma unroll 1
+    for (int k = 0; k < 3; k++) {
+        // target k: the other two Q limbs ascending, then P (prime indices: 0 q0, 1 q1, 2 P, 3 q2)
+        const int tp = k == 2 ? 2 : j == 0 ? (k == 0 ? 1 : 3) : j == 1 ? (k == 0 ? 0 : 3) : (k == 0 ? 0 : 1);
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const uint64_t x = xs[tid + T * e];
+            if (tp == 1) a[e] = j == 0 ? reduce_bnd<1>(x) : x;                 // q1: x0 < 2^58; x2 < q2 < q1
+            else if (tp == 3) a[e] = j == 0 ? reduce_bnd<3>(x) : csub(x, Q2);  // q2: x0 < 2^58; x1 < q1 < 2 q2
+            else a[e] = x;                                                     // q0 (x1, x2 < q0), P (x < P)
+        }
+        if (tp == 2) fwd<2, false>(a, sm, K.pr[2]);       // lazy [0, 2P): a Shoup operand only
+        else if (tp == 1) fwd_q1f(a, sm, K.pr[1].fwdf);   // canonical (FP64 pipe)
+        else if (tp == 3) fwd<3>(a, sm, K.pr[3]);         // canonical
+        else fwd<0, false>(a, sm, K.pr[0]);               // lazy [0, 2 q0)
+        store_eval(xu + (size_t)k * N, a);
+    }
+}
+
+// the digit j's residue in limb tp (prime index) as stored by k_digits3 / k_tensor<3>
+BM_D const uint64_t *digit_poly(const MatchK &K, int64_t pi, int j, int tp)
+{
+    const int lj = j == 2 ? 3 : j; // prime index of digit j's own limb
+    if (tp == lj) return K.D2 + ((size_t)pi * 3 + j) * N;
+    const int k = tp == 2 ? 2 : j == 0 ? (tp == 1 ? 0 : 1) : j == 1 ? (tp == 0 ? 0 : 1) : (tp == 0 ? 0 : 1);
+    return K.XU + ((size_t)pi * D2X_POLYS + 3 * j + k) * N;
+}
+
+// C2: key switch with rlk2 + ModDown + Res by q2, per (pair, c) (reading R28; the R22 rewriting):
+//   y = INTT_P(KS_c[P]);  U = INTT_q2(d_c[q2] + P^-1 KS_c[q2]);  R = U - P^-1 y^ (mod q2);  z^ = c_q2(R)
+//   out_c[q_l] = q2^-1 (d_c[q_l] + P^-1 KS_c[q_l] - NTT_l(P^-1 y^ + z^)),  l = 0, 1
+__global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *ys = sm + SMEM_WORDS, *zs = ys + N;
+    const MatchK &K = C.m;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t *dc = K.D01 + ((size_t)pi * 6 + c * 3) * N; // d_c[q0], d_c[q1], d_c[q2]
+    // rlk2 [j][c][l][N], l: 0 q0, 1 q1, 2 q2, 3 P
+    auto key = [&](int j, int l) { return C.rlk2 + (((size_t)j * 2 + c) * 4 + l) * N; };
+    uint64_t a[E];
+    // ---- P limb
+    {
+        const uint64_t *x0 = digit_poly(K, pi, 0, 2), *x1 = digit_poly(K, pi, 1, 2), *x2 = digit_poly(K, pi, 2, 2);
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos);
+            a[e] = reduce_lazy<2>(shoup4<2>(u.x, ld2k(key(0, 3) + pos)) + shoup4<2>(v.x, ld2k(key(1, 3) + pos)) +
+                                  shoup4<2>(w.x, ld2k(key(2, 3) + pos)));
+            a[e + 1] = reduce_lazy<2>(shoup4<2>(u.y, ld2k(key(0, 3) + pos + 1)) + shoup4<2>(v.y, ld2k(key(1, 3) + pos + 1)) +
+                                      shoup4<2>(w.y, ld2k(key(2, 3) + pos + 1)));
+        }
+    }
+    inv<2>(a, sm, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // y, canonical
+    // ---- q2 limb
+    {
+        const uint64_t *x0 = digit_poly(K, pi, 0, 3), *x1 = digit_poly(K, pi, 1, 3), *x2 = digit_poly(K, pi, 2, 3);
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + 2 * N + pos);
+            a[e] = reduce_bnd<3>(dd.x + shoup4<3>(u.x, ld2k(key(0, 2) + pos)) + shoup4<3>(v.x, ld2k(key(1, 2) + pos)) +
+                                 shoup4<3>(w.x, ld2k(key(2, 2) + pos)));
+            a[e + 1] = reduce_bnd<3>(dd.y + shoup4<3>(u.y, ld2k(key(0, 2) + pos + 1)) +
+                                     shoup4<3>(v.y, ld2k(key(1, 2) + pos + 1)) + shoup4<3>(w.y, ld2k(key(2, 2) + pos + 1)));
+        }
+    }
+    inv<3>(a, sm, K.pr[3]); // U, canonical
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = ys[tid + T * e];
+        const uint64_t f = y > (QP >> 1) ? 1 : 0;
+        zs[tid + T * e] = reduce_bnd<3>(a[e] + f + 4 * Q2 - shoup4<3>(y, C.pinv2)); // R = U - P^-1 y^ (mod q2)
+    }
+    // ---- q1 (FP64-pipe transform), then q0
+#pragma unroll 1
+    for (int l = 1; l >= 0; l--) {
+        const uint64_t q = l ? Q1 : Q0;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const uint64_t y = ys[tid + T * e], R = zs[tid + T * e];
+            const uint64_t f = y > (QP >> 1) ? 1 : 0;
+            const uint64_t z = R > (Q2 >> 1) ? R + (q - Q2) : R; // z^ mod q_l
+            if (l) a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (f ? Q1 - 1 : 0) + z);
+            else a[e] = shoup4<0>(y, K.pinv[0]) + (f ? Q0 - 1 : 0) + z; // < 6 q0
+        }
+        if (l) fwd_q1f(a, sm, K.pr[1].fwdf); // canonical
+        else fwd<0, false>(a, sm, K.pr[0]);  // [0, 2 q0)
+        const uint64_t *x0 = digit_poly(K, pi, 0, l), *x1 = digit_poly(K, pi, 1, l), *x2 = digit_poly(K, pi, 2, l);
+        uint64_t *co = K.XC + ((size_t)pi * 2 + c) * 2 * N + (size_t)l * N;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int pos = pos_M4(tid, e);
+            const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + (size_t)l * N + pos);
+            uint64_t va, vb;
+            if (l) {
+                va = dd.x + shoup4<1>(u.x, ld2k(key(0, 1) + pos)) + shoup4<1>(v.x, ld2k(key(1, 1) + pos)) +
+                     shoup4<1>(w.x, ld2k(key(2, 1) + pos)) + Q1 - a[e];
+                vb = dd.y + shoup4<1>(u.y, ld2k(key(0, 1) + pos + 1)) + shoup4<1>(v.y, ld2k(key(1, 1) + pos + 1)) +
+                     shoup4<1>(w.y, ld2k(key(2, 1) + pos + 1)) + Q1 - a[e + 1];
+                st2(co + pos, reduce_bnd<1>(shoup4<1>(va, C.q2inv[1])), reduce_bnd<1>(shoup4<1>(vb, C.q2inv[1])));
+            } else {
+                va = dd.x + shoup4<0>(u.x, ld2k(key(0, 0) + pos)) + shoup4<0>(v.x, ld2k(key(1, 0) + pos)) +
+                     shoup4<0>(w.x, ld2k(key(2, 0) + pos)) + 2 * Q0 - a[e];
+                vb = dd.y + shoup4<0>(u.y, ld2k(key(0, 0) + pos + 1)) + shoup4<0>(v.y, ld2k(key(1, 0) + pos + 1)) +
+                     shoup4<0>(w.y, ld2k(key(2, 0) + pos + 1)) + 2 * Q0 - a[e + 1];
+                st2(co + pos, reduce_bnd<0>(shoup4<0>(va, C.q2inv[0])), reduce_bnd<0>(shoup4<0>(vb, C.q2inv[0])));
+            }
+        }
+    }
+}
+
+// C3: Res_q1(Mul(P)(C, M)) per (pair, c): y = INTT_q1(c[q1] M[q1]); out = c[q0] M'[q0] - NTT_q0(q1^-1 y^)
+__global__ void __launch_bounds__(T, 1) k_cmp_mask(CmpK C)
+{
+    extern __shared__ uint64_t sm[];
+    const MatchK &K = C.m;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    const uint64_t *ci = K.XC + ((size_t)pi * 2 + c) * 2 * N;
+    uint64_t a[E];
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 v = ld2(ci + N + pos);
+        a[e] = reduce_bnd<1>(shoup4<1>(v.x, ld2k(C.mask + N + pos)));
+        a[e + 1] = reduce_bnd<1>(shoup4<1>(v.y, ld2k(C.mask + N + pos + 1)));
+    }
+    inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // y, canonical
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], K.q1inv) + (a[e] > (Q1 >> 1) ? Q0 - 1 : 0); // < 5 q0
+    fwd<0>(a, sm, K.pr[0]); // canonical
+    uint64_t *co = K.XR + ((size_t)pi * 2 + c) * N;
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 v = ld2(ci + pos);
+        st2(co + pos, reduce_bnd<0>(shoup4<0>(v.x, ld2k(C.mask + pos)) + Q0 - a[e]),
+            reduce_bnd<0>(shoup4<0>(v.y, ld2k(C.mask + pos + 1)) + Q0 - a[e + 1]));
+    }
+}
+
+// C4: right rotation by u = t mod s of the level-0 ciphertext XR (left rotation by S - u with key gkc[u-1]),
+// straight to the coefficient domain:  out_0 = INTT_q0(sigma(c0) + sigma(c1) P^-1 gk[0][q0]) - P^-1 y^0,
+// out_1 = INTT_q0(sigma(c1) P^-1 gk[1][q0]) - P^-1 y^1;  u = 0: out_c = INTT_q0(c_c).
+__global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
+    const MatchK &K = C.m;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    const int u = (int)((K.t0 + pi % K.ct) % C.s);
+    const uint64_t *ci = K.XR + (size_t)pi * 2 * N;
+    uint64_t *co = K.XO + (size_t)pi * 2 * N;
+    uint64_t a[E];
+    if (u == 0) {
+#pragma unroll 1
+        for (int c = 0; c < 2; c++) {
+            load_eval(a, ci + (size_t)c * N);
+            inv<0>(a, XB, K.pr[0]);
+            store_coef(co + (size_t)c * N, a);
+        }
+        return;
+    }
+    const uint32_t g = (uint32_t)pow5_mod2n(SLOTS - u);
+    const ulonglong2 *gk = C.gkc + (size_t)(u - 1) * 4 * N; // [c][q0 | P][N]
+    uint64_t *ks1 = C.scr + (size_t)pi * 2 * N, *tsc = ks1 + N;
+    stage_by_j(S0, ci);
+    stage_by_j(S1, ci + N);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
+    inv<0>(a, XB, K.pr[0]);
+    fwd<2>(a, XB, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        st2(ks1 + pos, shoup4<2>(a[e], ld2k(gk + 3 * N + pos)), shoup4<2>(a[e + 1], ld2k(gk + 3 * N + pos + 1)));
+        a[e] = shoup4<2>(a[e], ld2k(gk + N + pos));
+        a[e + 1] = shoup4<2>(a[e + 1], ld2k(gk + N + pos + 1));
+    }
+#pragma unroll 1
+    for (int c = 0; c < 2; c++) {
+        if (c == 1) { // written by this thread above: coherent loads
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(ks1 + pos_M4(tid, e));
+                a[e] = v.x;
+                a[e + 1] = v.y;
+            }
+        }
+        inv<2>(a, XB, K.pr[2]);
+#pragma unroll
+        for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], K.pinv[0]) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+        const ulonglong2 *gq = gk + (size_t)(2 * c) * N;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int j = j_M4(tid, e), jp = auto_perm(j, g);
+            uint64_t v = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e))); // [0, 4 q0)
+            if (c == 0) v += S0[pidx(jp)];
+            a[e] = reduce_bnd<0>(v);
+        }
+        inv<0>(a, XB, K.pr[0]);
+        uint64_t *o = co + (size_t)c * N;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int j = j_M1(tid, e);
+            o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
+        }
+    }
+}
+
+// C5: d_out[query][group] += sum of its rotated results in this chunk (coefficient domain, canonical)
+__global__ void __launch_bounds__(256) k_cmp_add(CmpK C, uint64_t *out, int64_t n_groups, int64_t g0, int64_t ng)
+{
+    const MatchK &K = C.m;
+    const int slice = blockIdx.x % (N / 256);
+    int64_t b = blockIdx.x / (N / 256);
+    const int c = (int)(b & 1);
+    b >>= 1;
+    const int64_t g = g0 + b % ng, a = b / ng;
+    const int k = slice * 256 + threadIdx.x;
+    const int64_t tlo = g * C.s > K.t0 ? g * C.s : K.t0;
+    const int64_t thi = (g + 1) * C.s < K.t0 + K.ct ? (g + 1) * C.s : K.t0 + K.ct;
+    uint64_t *dst = out + (((size_t)(K.jq0 + a) * n_groups + g) * 2 + c) * N + k;
+    uint64_t acc = *dst;
+    for (int64_t t = tlo; t < thi; t++) acc = csub(acc + K.XO[(((size_t)a * K.ct + (t - K.t0)) * 2 + c) * N + k], Q0);
+    *dst = acc;
+}
+
 // ================================================================== encryption / conversion / keys
 struct EncK {
     PrimeK pr[4];
@@ -974,8 +1269,8 @@ struct ConvK {
     const uint64_t *in;
     uint64_t *out;
     int n_limbs;
-    int lp[3];          // prime index of each limb
-    uint64_t scale[3];  // k_key_ntt: constant folded into each limb (canonical, < q)
+    int lp[4];          // prime index of each limb
+    uint64_t scale[4];  // k_key_ntt: constant folded into each limb (canonical, < q)
 };
 
 // one block per polynomial; dir 0: coefficient -> NTT, 1: NTT -> coefficient
@@ -1032,6 +1327,7 @@ struct DevCtx {
     PrimeK pr[4] = {};
     ulonglong2 pinv[2], q1inv;
     ulonglong2 q2inv[2];       // f3: q2^-1 mod q0, q1
+    ulonglong2 pinv2;          // f1: P^-1 mod q2
     uint64_t pmod[2];
 };
 
@@ -1126,8 +1422,10 @@ int ctx_get(DevCtx **out)
     }
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
     for (int l = 0; l < 2; l++) C->q2inv[l] = shoup_pair(powmod_d(Q2 % C->pr[l].q, C->pr[l].q - 2, C->pr[l].q), C->pr[l].q);
+    C->pinv2 = shoup_pair(powmod_d(QP % Q2, Q2 - 2, Q2), Q2);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
-    cudaFuncSetAttribute(k_tensor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
@@ -1137,6 +1435,10 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
     cudaFuncSetAttribute(k_rot1_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
     cudaFuncSetAttribute(k_rot1_ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X3_SMEM_BYTES);
+    cudaFuncSetAttribute(k_digits3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1_SMEM_BYTES);
+    cudaFuncSetAttribute(k_relin3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2_SMEM_BYTES);
+    set_smem(k_cmp_mask);
+    cudaFuncSetAttribute(k_cmp_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C4_SMEM_BYTES);
     set_smem(k_convert);
     set_smem(k_key_ntt);
     if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -1191,6 +1493,15 @@ struct bm_xk_dev {
     ulonglong2 *mask;  // [p][3 limbs q0,q1,q2][N] expansion masks X_i, q2^-1 in the Q limbs
     ulonglong2 *emask; // [p][3][N] enrollment masks E_i (f4; nullptr if not uploaded)
 };
+struct bm_ck_dev {
+    int dev;
+    uint8_t digest[32];
+    int32_t d, p, s, log_s;
+    ulonglong2 *rlk2; // [3][2][4 limbs q0,q1,q2,P][N], P^-1 in the Q limbs
+    ulonglong2 *gkl;  // [log_s][2][2][3 limbs q0,q1,P][N], P^-1 in the Q limbs
+    ulonglong2 *gkc;  // [s-1][2][2 limbs q0,P][N], P^-1 in the q0 limb
+    ulonglong2 *mask; // [2 limbs q0,q1][N], q1^-1 in the q0 limb
+};
 struct bm_evk_dev {
     int dev;
     uint8_t digest[32];
@@ -1219,8 +1530,8 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     K.in = tmp;
     K.out = nullptr;
     K.n_limbs = n_limbs;
-    for (int i = 0; i < 3; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
-    for (int i = 0; i < 3; i++) K.scale[i] = scale && i < n_limbs ? scale[i] : 1;
+    for (int i = 0; i < 4; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
+    for (int i = 0; i < 4; i++) K.scale[i] = scale && i < n_limbs ? scale[i] : 1;
     k_key_ntt<<<(unsigned)n_polys, T, SMEM_BYTES>>>(K, dst);
     int rc = launch_check();
     if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
@@ -1648,6 +1959,172 @@ int bm_enroll(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
     return rc;
 }
 
+// ------------------------------------------------------------------ f1: compressed scan
+int bm_ck_to_device(const bm_params *prm, const bm_ck *ck, const int64_t *h_mask, bm_ck_dev **out)
+{
+    if (!prm || !ck || !h_mask || !out) return BM_ERR_INVALID_ARG;
+    if (memcmp(ck->digest, prm->digest, 32) || ck->d != prm->d || ck->p != prm->p) return BM_ERR_KEY_MISMATCH;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    bm_ck_dev *d = new bm_ck_dev;
+    d->dev = C->dev;
+    memcpy(d->digest, prm->digest, 32);
+    d->d = prm->d;
+    d->p = prm->p;
+    d->s = prm->s;
+    d->log_s = ck->log_s;
+    d->rlk2 = d->gkl = d->gkc = d->mask = nullptr;
+    const int l4[4] = {0, 1, 3, 2}, l3[3] = {0, 1, 2}, l0[2] = {0, 2}, lm[2] = {0, 1};
+    const uint64_t s4[4] = {C->pinv[0].x, C->pinv[1].x, C->pinv2.x, 1}, s3[3] = {C->pinv[0].x, C->pinv[1].x, 1};
+    const uint64_t s0[2] = {C->pinv[0].x, 1}, sm[2] = {C->q1inv.x, 1};
+    rc = upload_key_polys(C, ck->rlk2.data(), 24, 4, l4, &d->rlk2, s4);
+    if (!rc && ck->log_s > 0) rc = upload_key_polys(C, ck->gkl.data(), 12 * (int64_t)ck->log_s, 3, l3, &d->gkl, s3);
+    if (!rc && prm->s > 1) rc = upload_key_polys(C, ck->gkc.data(), 4 * (int64_t)(prm->s - 1), 2, l0, &d->gkc, s0);
+    if (!rc) {
+        std::vector<uint64_t> m(2 * (size_t)N);
+        for (int l = 0; l < 2; l++) {
+            const uint64_t q = l ? Q1 : Q0;
+            for (int k = 0; k < N; k++) {
+                const int64_t x = h_mask[k];
+                m[(size_t)l * N + k] = x >= 0 ? (uint64_t)x % q : q - 1 - (uint64_t)(-(x + 1)) % q;
+            }
+        }
+        rc = upload_key_polys(C, m.data(), 2, 2, lm, &d->mask, sm);
+    }
+    if (rc) {
+        cudaFree(d->rlk2);
+        cudaFree(d->gkl);
+        cudaFree(d->gkc);
+        cudaFree(d->mask);
+        cudaGetLastError();
+        delete d;
+        return rc;
+    }
+    *out = d;
+    return BM_OK;
+}
+
+void bm_ck_dev_free(bm_ck_dev *d)
+{
+    if (!d) return;
+    cudaFree(d->rlk2);
+    cudaFree(d->gkl);
+    cudaFree(d->gkc);
+    cudaFree(d->mask);
+    delete d;
+}
+
+// workspace per pair (u64 polynomials): D01 6, D2 3, XU 9, XC 4, XR 2, XO 2, scratch 2
+constexpr int CMP_WS_POLYS = 28;
+static int64_t cmp_chunk_pairs(int64_t total)
+{
+    int64_t ch = 4096;
+    if (const char *e = getenv("BM_CHUNK_PAIRS")) {
+        long v = atol(e);
+        if (v > 0) ch = v;
+    }
+    return total < ch ? total : ch;
+}
+
+size_t bm_match_cmp_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq)
+{
+    if (!prm || n_sets <= 0 || nq <= 0) return 0;
+    return (size_t)cmp_chunk_pairs(n_sets * (int64_t)nq) * CMP_WS_POLYS * N * sizeof(uint64_t);
+}
+
+int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+                 int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!prm || !ck || n_sets < 0 || nq < 0) return BM_ERR_INVALID_ARG;
+    if (memcmp(ck->digest, prm->digest, 32) || ck->p != prm->p || ck->d != prm->d) return BM_ERR_KEY_MISMATCH;
+    if (ck->log_s < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    const int64_t total = n_sets * (int64_t)nq;
+    if (total == 0) return BM_OK;
+    if (!d_db || !d_q || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
+    if (ws_bytes < bm_match_cmp_ws_bytes(prm, n_sets, nq)) return BM_ERR_WORKSPACE;
+    DevCtx *Cx;
+    int rc = ctx_get(&Cx);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ch = cmp_chunk_pairs(total), n_groups = (n_sets + prm->s - 1) / prm->s;
+    CmpK C;
+    MatchK &K = C.m;
+    for (int i = 0; i < 4; i++) K.pr[i] = Cx->pr[i];
+    K.pinv[0] = Cx->pinv[0];
+    K.pinv[1] = Cx->pinv[1];
+    K.q1inv = Cx->q1inv;
+    K.db = d_db;
+    K.qry = d_q;
+    K.out = nullptr;
+    K.n_sets = n_sets;
+    K.p = prm->p;
+
+    uint64_t *ws = (uint64_t *)d_ws;
+    const size_t P1 = (size_t)ch * N;
+    K.D01 = ws;
+    K.D2 = K.D01 + 6 * P1;
+    K.XU = K.D2 + 3 * P1;
+    K.XC = K.XU + 9 * P1;
+    K.XR = K.XC + 4 * P1;
+    K.XO = K.XR + 2 * P1;
+    K.ACC = nullptr;
+    C.scr = K.XO + 2 * P1;
+    C.pinv2 = Cx->pinv2;
+    C.q2inv[0] = Cx->q2inv[0];
+    C.q2inv[1] = Cx->q2inv[1];
+    C.rlk2 = ck->rlk2;
+    C.gkc = ck->gkc;
+    C.mask = ck->mask;
+    C.s = prm->s;
+    ExpK X; // the level-1 ladder reuses f3's rotation kernels (C <- C + Rot(C, 2^i))
+    for (int i = 0; i < 4; i++) X.pr[i] = Cx->pr[i];
+    X.pinv[0] = Cx->pinv[0];
+    X.pinv[1] = Cx->pinv[1];
+    X.q2inv[0] = Cx->q2inv[0];
+    X.q2inv[1] = Cx->q2inv[1];
+    X.mask = nullptr;
+    X.in = nullptr;
+    X.out = K.XC;
+    X.XU = K.XU;
+    X.p = 1;
+    X.enroll = 0;
+    X.Bk = 1;
+    X.bit = 0;
+    X.u0 = 0;
+    cudaMemsetAsync(d_out, 0, (size_t)nq * n_groups * 2 * N * sizeof(uint64_t), s);
+    const int64_t ct_full = n_sets < ch ? n_sets : ch;
+    const int64_t cq_full = ch / ct_full < nq ? ch / ct_full : nq;
+    for (int64_t jq0 = 0; jq0 < nq && !rc; jq0 += cq_full)
+        for (int64_t t0 = 0; t0 < n_sets && !rc; t0 += ct_full) {
+            K.jq0 = jq0;
+            K.t0 = t0;
+            K.cq = (int32_t)(nq - jq0 < cq_full ? nq - jq0 : cq_full);
+            K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
+            const int64_t np = K.cq * K.ct;
+            const unsigned npu = (unsigned)np;
+            const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS));
+            k_tensor<3><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
+            k_digits3<<<3 * npu, T, C1_SMEM_BYTES, s>>>(C);
+            k_relin3<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
+            rc = launch_check();
+            for (int i = 0; i < prm->log_s && !rc; i++) {
+                X.gk = ck->gkl + (size_t)i * 12 * N;
+                X.g = (uint32_t)powmod_d(5, (uint64_t)1 << i, 2 * N);
+                k_rot1_digits<<<2 * npu, T, X2_SMEM_BYTES, s>>>(X);
+                k_rot1_ks<<<2 * npu, T, X3_SMEM_BYTES, s>>>(X);
+                rc = launch_check();
+            }
+            if (rc) break;
+            k_cmp_mask<<<2 * npu, T, SMEM_BYTES, s>>>(C);
+            k_cmp_rot<<<npu, T, C4_SMEM_BYTES, s>>>(C);
+            const int64_t g0 = t0 / prm->s, g1 = (t0 + K.ct - 1) / prm->s, ng = g1 - g0 + 1;
+            k_cmp_add<<<(unsigned)(K.cq * ng * 2 * (N / 256)), 256, 0, s>>>(C, d_out, n_groups, g0, ng);
+            rc = launch_check();
+        }
+    return rc;
+}
+
 // ------------------------------------------------------------------ the scan
 static int64_t chunk_pairs(int64_t total)
 {
@@ -1709,7 +2186,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     const int64_t ch = chunk_pairs(total);
 
     MatchK K;
-    for (int i = 0; i < 3; i++) K.pr[i] = C->pr[i];
+    for (int i = 0; i < 4; i++) K.pr[i] = C->pr[i];
     K.pinv[0] = C->pinv[0];
     K.pinv[1] = C->pinv[1];
     K.q1inv = C->q1inv;
@@ -1769,7 +2246,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = per_part ? r : 0, hi = per_part ? r + 1 : prm->p;
             beg(0, 2 * np);
-            k_tensor<<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+            k_tensor<2><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             end();
             beg(1, 6 * np);
             k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);

@@ -351,6 +351,94 @@ int bm_keygen(const bm_params *prm, uint64_t seed, bm_sk **skp, bm_pk **pkp, bm_
 
 static bool canonical(const uint64_t *v, size_t n_polys, const int *limb_primes, int n_limbs);
 
+// Level-1 Galois key of the left rotation by r (f3/f4/f1), 2 digits j over {q0, q1, P}:
+// (-a s + e + [l = j] (P mod q_l) sigma_{5^r}(s), a), a from (P_GK1_A, object 2r + j, sub-stream l),
+// e from (P_GK1_E, object 2r + j); out [2 digits][2 comps][3 limbs][N]
+static void galois_key1(uint64_t seed, const std::vector<int64_t> &sv, uint64_t r, uint64_t *out)
+{
+    const uint64_t Qs[3] = {Q0, Q1, QP};
+    const uint64_t g = powmod_h(5, r, 2 * N);
+    std::vector<int64_t> ev(N);
+    std::vector<uint64_t> s(N), e(N), a(N), t(N), sg(N);
+    for (int j = 0; j < 2; j++) {
+        const uint64_t obj = 2 * r + (uint64_t)j;
+        sample_small(seed, P_GK1_E, obj, 1, ev.data());
+        for (int l = 0; l < 3; l++) {
+            const uint64_t q = Qs[l];
+            for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
+            sample_uniform(seed, P_GK1_A, obj, (uint32_t)l, q, a.data());
+            poly_mul_h(a.data(), s.data(), t.data(), l);
+            uint64_t *b = out + (((size_t)j * 2 + 0) * 3 + l) * N;
+            uint64_t *aa = out + (((size_t)j * 2 + 1) * 3 + l) * N;
+            for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
+            if (l == j) {
+                std::fill(sg.begin(), sg.end(), 0);
+                for (int k = 0; k < N; k++) {
+                    uint64_t y = (uint64_t)k * g % (2 * N);
+                    if (y < (uint64_t)N) sg[y] = s[k];
+                    else sg[y - N] = (q - s[k]) % q;
+                }
+                const uint64_t pm = QP % q;
+                for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(sg[k], pm, q)) % q;
+            }
+        }
+    }
+}
+
+// f1 (reading R28): 3-digit relinearisation key over {q0, q1, q2, P} (b = -a s + e + [l = j](P mod q_l) s^2,
+// a from (P_RLK2_A, object j, sub-stream l), e from (P_RLK2_E, object j)), the ladder's level-1 Galois keys
+// of 2^i (i < log2 s) and the level-0 keys of the right rotations by u = 1..s-1 (left by S - u, object
+// CMP_OBJ + u)
+constexpr uint64_t CMP_OBJ = 4096;
+int bm_ck_keygen(const bm_params *prm, uint64_t seed, bm_ck **out)
+{
+    if (!prm || !out) return BM_ERR_INVALID_ARG;
+    const uint64_t Q4[4] = {Q0, Q1, Q2, QP};
+    const int pi4[4] = {0, 1, 3, 2};
+    bm_ck *x = new (std::nothrow) bm_ck;
+    if (!x) return BM_ERR_OOM;
+    memcpy(x->digest, prm->digest, 32);
+    x->d = prm->d;
+    x->p = prm->p;
+    x->log_s = prm->log_s;
+    std::vector<int64_t> sv(N), ev(N);
+    std::vector<uint64_t> s(N), e(N), a(N), t(N), s2(N);
+    sample_small(seed, P_SK, 0, 0, sv.data());
+    x->rlk2.assign(24 * (size_t)N, 0);
+    for (int j = 0; j < 3; j++) {
+        sample_small(seed, P_RLK2_E, (uint64_t)j, 1, ev.data());
+        for (int l = 0; l < 4; l++) {
+            const uint64_t q = Q4[l];
+            for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
+            sample_uniform(seed, P_RLK2_A, (uint64_t)j, (uint32_t)l, q, a.data());
+            poly_mul_h(a.data(), s.data(), t.data(), pi4[l]);
+            uint64_t *b = &x->rlk2[(((size_t)j * 2 + 0) * 4 + l) * N], *aa = &x->rlk2[(((size_t)j * 2 + 1) * 4 + l) * N];
+            for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
+            if (l == j) {
+                poly_mul_h(s.data(), s.data(), s2.data(), pi4[l]);
+                const uint64_t pm = QP % q;
+                for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(s2[k], pm, q)) % q;
+            }
+        }
+    }
+    x->gkl.assign((size_t)x->log_s * 12 * N, 0);
+    for (int i = 0; i < x->log_s; i++) galois_key1(seed, sv, (uint64_t)1 << i, &x->gkl[(size_t)i * 12 * N]);
+    const int s_ = prm->s;
+    x->gkc.assign((size_t)(s_ - 1) * 4 * N, 0);
+    for (int u = 1; u < s_; u++) galois_key(seed, sv, (uint64_t)(SLOTS - u), CMP_OBJ + u, &x->gkc[(size_t)(u - 1) * 4 * N]);
+    *out = x;
+    return BM_OK;
+}
+void bm_ck_free(bm_ck *x) { delete x; }
+int bm_ck_export(const bm_ck *x, uint64_t *rlk2, uint64_t *gkl, uint64_t *gkc)
+{
+    if (!x) return BM_ERR_INVALID_ARG;
+    if (rlk2) memcpy(rlk2, x->rlk2.data(), x->rlk2.size() * 8);
+    if (gkl) memcpy(gkl, x->gkl.data(), x->gkl.size() * 8);
+    if (gkc) memcpy(gkc, x->gkc.data(), x->gkc.size() * 8);
+    return BM_OK;
+}
+
 // f3 expansion keys (reading R26).  pk limb q2: (-a s + e, a) with pk's error (P_PK_E,
 // object 0) and a from (P_PK_A, object 0, sub-stream 3).  Level-1 Galois key of the left rotation
 // by r = s 2^t, digit j: over {q0, q1, P}, (-a s + e + [l = j] (P mod q_l) sigma_{5^r}(s), a) with
@@ -379,32 +467,7 @@ int bm_xk_keygen(const bm_params *prm, uint64_t seed, bm_xk **out)
     for (int k = 0; k < N; k++) x->pk_q2[k] = (e[k] + Q2 - t[k]) % Q2, x->pk_q2[N + k] = a[k];
     // level-1 Galois keys
     x->gk1.assign((size_t)x->n_rot * 12 * N, 0);
-    for (int tt = 0; tt < x->n_rot; tt++) {
-        const uint64_t r = (uint64_t)prm->s << tt, g = powmod_h(5, r, 2 * N);
-        for (int j = 0; j < 2; j++) {
-            const uint64_t obj = 2 * r + (uint64_t)j;
-            sample_small(seed, P_GK1_E, obj, 1, ev.data());
-            for (int l = 0; l < 3; l++) {
-                const uint64_t q = Qs[l];
-                for (int k = 0; k < N; k++) s[k] = to_res(sv[k], q), e[k] = to_res(ev[k], q);
-                sample_uniform(seed, P_GK1_A, obj, (uint32_t)l, q, a.data());
-                poly_mul_h(a.data(), s.data(), t.data(), l);
-                uint64_t *b = &x->gk1[((((size_t)tt * 2 + j) * 2 + 0) * 3 + l) * N];
-                uint64_t *aa = &x->gk1[((((size_t)tt * 2 + j) * 2 + 1) * 3 + l) * N];
-                for (int k = 0; k < N; k++) b[k] = (e[k] + q - t[k]) % q, aa[k] = a[k];
-                if (l == j) {
-                    std::fill(sg.begin(), sg.end(), 0);
-                    for (int k = 0; k < N; k++) {
-                        uint64_t y = (uint64_t)k * g % (2 * N);
-                        if (y < (uint64_t)N) sg[y] = s[k];
-                        else sg[y - N] = (q - s[k]) % q;
-                    }
-                    const uint64_t pm = QP % q;
-                    for (int k = 0; k < N; k++) b[k] = (b[k] + mulmod_h(sg[k], pm, q)) % q;
-                }
-            }
-        }
-    }
+    for (int tt = 0; tt < x->n_rot; tt++) galois_key1(seed, sv, (uint64_t)prm->s << tt, &x->gk1[(size_t)tt * 12 * N]);
     *out = x;
     return BM_OK;
 }
@@ -662,6 +725,16 @@ int bm_encode_masks(const bm_params *prm, int32_t kind, int64_t *pt)
     return BM_OK;
 }
 
+// f1: the compression's score mask M[x] = [x mod s = 0] at scale q1 (Res by q1 restores the
+// input's scale)
+int bm_encode_cmp_mask(const bm_params *prm, int64_t *pt)
+{
+    if (!prm || !pt) return BM_ERR_INVALID_ARG;
+    std::vector<double> z(SLOTS);
+    for (int x = 0; x < SLOTS; x++) z[x] = (x % prm->s) == 0 ? 1.0 : 0.0;
+    return encode_slots(z.data(), pt, (double)Q1);
+}
+
 // f4: the client's enrollment ciphertext holds the unit template in slots [0, d), zeros elsewhere
 // ("occupies the initial slots ... padded with zeros")
 int bm_encode_enroll(const bm_params *prm, const double *v, int64_t n, int64_t *pt)
@@ -727,6 +800,29 @@ int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_
             const int64_t *mm = &m[(size_t)c * N];
             for (int t = 0; t < N; t++) acc += (double)mm[t] * cosT[(ex * t) % (2 * N)];
             scores[(size_t)c * prm->B + k] = acc / prm->out_scale;
+        }
+    return BM_OK;
+}
+
+// f1: packed (compressed) results: every slot is a score -- slot k s + u of packed ciphertext g is set
+// g s + u's block k; scale 2^80 / q2 (HE-C^3 one level up, reading R28)
+int bm_decrypt_packed(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, double *slots)
+{
+    if (!prm || !slots) return BM_ERR_INVALID_ARG;
+    std::vector<int64_t> m((size_t)std::max<int64_t>(n, 0) * N);
+    int rc = bm_decrypt_raw(prm, sk, ct, n, m.data());
+    if (rc) return rc;
+    std::vector<double> cosT(2 * N);
+    for (int i = 0; i < 2 * N; i++) cosT[i] = std::cos(M_PI * i / N);
+    const std::vector<int> &e = slot_exp();
+    const double scale = std::ldexp(1.0, 80) / (double)Q2;
+    for (int64_t c = 0; c < n; c++)
+        for (int j = 0; j < SLOTS; j++) {
+            const uint64_t ex = (uint64_t)e[j];
+            double acc = 0;
+            const int64_t *mm = &m[(size_t)c * N];
+            for (int t = 0; t < N; t++) acc += (double)mm[t] * cosT[(ex * t) % (2 * N)];
+            slots[(size_t)c * SLOTS + j] = acc / scale;
         }
     return BM_OK;
 }

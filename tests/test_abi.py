@@ -178,3 +178,20 @@ def test_expansion_encoders_within_one_of_oracle(B, O):
     pv = B.bm_encode_enroll(prm, T)
     ov = O.encode(O.enroll_vector(T / np.linalg.norm(T, axis=1, keepdims=True), 13, 128), 13)
     assert np.abs(pv - ov).max() <= 1 and (pv != ov).mean() < 1e-3
+
+
+
+# ----------------------------------------------------------------------------- f1 host side
+@pytest.mark.parametrize("d,p", [(16, 4), (128, 8)])
+def test_compression_keys_match_oracle(B, O, d, p):
+    """f1: the product's rlk2 / level-1 ladder keys / level-0 right-rotation keys equal the oracle's."""
+    prm = B.bm_params_init(d, p)
+    ck = B.bm_ck_keygen(prm, 99)
+    rlk2, gkl, gkc = B.bm_ck_export(prm, ck)
+    orlk2, ogkl, ogkc = O.keygen_cmp(13, 99, d, p)
+    assert np.array_equal(rlk2, orlk2)
+    assert gkl.shape == ogkl.shape and np.array_equal(gkl, ogkl)
+    assert gkc.shape == ogkc.shape and np.array_equal(gkc, ogkc)
+    m = B.bm_encode_cmp_mask(prm)
+    om = O.cmp_mask(13, d, p)
+    assert np.abs(m - om).max() <= 1 and (m != om).mean() < 1e-3
