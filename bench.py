@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--order", type=int, default=0)
-    ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion leg")
+    ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion / f4 enrollment leg")
+    ap.add_argument("--no-f1", action="store_true", help="skip the f1 compressed-scan leg")
     ap.add_argument("--nq", type=int, default=384)
     ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -320,6 +321,13 @@ def run_ours(args):
     f3 = None
     if world == 1 and not args.no_f3:
         f3 = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_step, tq_per_step, stream)
+    # f1: the compressed scan of the same workload one level up (level-2 DB and
+    # queries), packed outputs s times smaller with the partial sums masked away
+    f1 = None
+    if world == 1 and not args.no_f1:
+        del ws
+        torch.cuda.empty_cache()
+        f1 = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream)
 
     # CPU oracle on the host cores (rank 0, N = 1 only)
     cpu = None
@@ -343,7 +351,7 @@ def run_ours(args):
                        "ring_N": N_RING, "parallelism": f"db-shard{world}",
                        "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
                            nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "f3_expand": f3,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "f3_expand": f3, "f1_compressed": f1,
             "gpu_launches": int(launches * args.steps),
             "clocks": clocks,
         }
@@ -434,6 +442,51 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
             "score_check_max_abs_diff": err,
             "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24)",
             "f4_enroll": f4}
+
+
+def run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream):
+    from paper_2408_06167_b200 import inputs as I
+    dev = d_out.device
+    nq, p, s = d_out.shape[0], prm.p, prm.s
+    xk = B.bm_xk_keygen(prm, 1)
+    xk_dev = B.bm_xk_to_device(prm, pk, xk, enroll=False)       # the level-2 public key
+    ck_dev = B.bm_ck_to_device(prm, B.bm_ck_keygen(prm, 1))
+    T = I.templates(CFG, n_tmpl, 0)
+    Q, _ = I.queries(CFG, nq)
+    d_db = torch.empty((n_sets, p, 2, 3, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_l2(prm, xk_dev, torch.from_numpy(B.bm_encode_db(prm, T, 0, n_sets).reshape(-1, N_RING)).to(dev),
+                    0, 2, d_db)
+    d_q = torch.empty((nq, p, 2, 3, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_l2(prm, xk_dev, torch.from_numpy(B.bm_encode_query(prm, Q).reshape(-1, N_RING)).to(dev), 0, 3, d_q)
+    G = -(-n_sets // s)
+    out = torch.empty((nq, G, 2, N_RING), dtype=torch.int64, device=dev)
+    ws = torch.empty(B.bm_match_cmp_ws_bytes(prm, n_sets, nq), dtype=torch.uint8, device=dev)
+    B.bm_match_cmp(prm, ck_dev, d_db, n_sets, d_q, nq, out, ws)     # warm-up
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 3))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        B.bm_match_cmp(prm, ck_dev, d_db, n_sets, d_q, nq, out, ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    # the packed scores of two queries vs the uncompressed scan's
+    slots = B.bm_decrypt_packed(prm, sk, out[:2].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
+    ref = B.bm_decrypt(prm, sk, d_out[:2].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
+    ref = ref.reshape(2, n_sets, prm.B)
+    err = 0.0
+    for j in range(2):
+        for t in range(n_sets):
+            g, u = divmod(t, s)
+            err = max(err, float(np.abs(slots[j * G + g, u::s] - ref[j, t]).max()))
+    assert err < 1e-5, err
+    return {"ms_per_step": round(ms, 3), "value": round(tq_per_step / (ms / 1e3), 1), "unit": "templates*queries/s",
+            "packed_ciphertexts_per_query": G, "d2h_bytes_per_step": int(out.numel() * 8),
+            "d2h_bytes_uncompressed": int(d_out.numel() * 8), "score_check_max_abs_diff": err,
+            "note": "HE-C^3 one level up (level-2 DB and query parts: tensor over 3 limbs, 3-digit relin + Res q2, "
+                    "ladder at level 1) + compression (Res_q1(M * C_t), right rotation by t mod s, packing); "
+                    "chain extended by q2, DESIGN.md R28"}
 
 
 def run_reference(args):
