@@ -325,7 +325,7 @@ def run_ours(args):
     # queries), packed outputs s times smaller with the partial sums masked away
     f1 = None
     if world == 1 and not args.no_f1:
-        del ws
+        ws = None   # the scan's workspace (already released when the e2e leg ran)
         torch.cuda.empty_cache()
         f1 = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream)
 
