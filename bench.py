@@ -318,16 +318,26 @@ def run_ours(args):
     # f3: server-side query expansion (Algorithm 1) of the same batch -- the client
     # uploads ONE level-2 ciphertext per query (the chain extended by q2) and bm_expand produces the p
     # level-1 parts bm_match takes.  Device time of the expansion alone and of expansion + scan.
+    # (the NEXT-row legs never take the headline line down with them: a failure is recorded instead)
     f3 = None
     if world == 1 and not args.no_f3:
-        f3 = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_step, tq_per_step, stream)
+        try:
+            f3 = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_step, tq_per_step, stream)
+        except Exception as ex:  # noqa: BLE001
+            f3 = {"error": f"{type(ex).__name__}: {ex}"}
+            log(args, f"[rank {rank}] f3/f4 leg failed: {f3['error']}")
     # f1: the compressed scan of the same workload one level up (level-2 DB and
     # queries), packed outputs s times smaller with the partial sums masked away
     f1 = None
     if world == 1 and not args.no_f1:
         ws = None   # the scan's workspace (already released when the e2e leg ran)
         torch.cuda.empty_cache()
-        f1 = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream)
+        try:
+            f1 = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream)
+        except Exception as ex:  # noqa: BLE001
+            f1 = {"error": f"{type(ex).__name__}: {ex}"}
+            log(args, f"[rank {rank}] f1 leg failed: {f1['error']}")
+        torch.cuda.empty_cache()
 
     # CPU oracle on the host cores (rank 0, N = 1 only)
     cpu = None
