@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion / f4 enrollment leg")
     ap.add_argument("--no-f1", action="store_true", help="skip the f1 compressed-scan leg")
+    ap.add_argument("--no-f4", action="store_true", help="skip the f4 enrollment part of the f3 leg")
     ap.add_argument("--nq", type=int, default=384)
     ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -414,10 +415,27 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
     sb = B.bm_decrypt(prm, sk, d_out[:k].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
     err = float(np.abs(sa - sb).max())
     assert err < 1e-5, err
+    f4 = None
+    if not args.no_f4:
+        f4 = run_f4(B, torch, prm, xk_dev, sk, evk_dev, d_db, n_sets, d_q, out_x, ws2, sb, k, stream)
     mm = f3_modmuls(p, prm.s) * nq * p
-    f_peak = 1965.0e6
-    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / IMAD_SLOTS_PER_MODMUL / 1e9
-    # f4: server-side enrollment of the whole DB (the same templates), then the same spot check
+    peak = SM_COUNT * IMAD_PER_CLK_SM * 1965.0e6 / IMAD_SLOTS_PER_MODMUL / 1e9
+    return {"queries": nq, "ms_per_batch": round(ms, 4), "queries_per_s": round(nq / (ms / 1e3), 1),
+            "gmodmul_s": round(mm / (ms / 1e3) / 1e9, 2), "alu_frac": round(mm / (ms / 1e3) / 1e9 / peak, 4),
+            "kernel_launches": 1 + 2 * (p.bit_length() - 1),
+            "upload_bytes_per_query": {"client_expanded": p * 4 * N_RING * 8, "server_expanded": 6 * N_RING * 8},
+            "expand_plus_scan": {"ms_per_step": round(ms + ms_scan, 4),
+                                 "value": round(tq_per_step / ((ms + ms_scan) / 1e3), 1),
+                                 "unit": "templates*queries/s"},
+            "score_check_max_abs_diff": err,
+            "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24)",
+            "f4_enroll": f4}
+
+
+def run_f4(B, torch, prm, xk_dev, sk, evk_dev, d_db, n_sets, d_q, out_x, ws2, sb, k, stream):
+    """f4: server-side enrollment of the whole DB (the same templates), then the same spot check."""
+    from paper_2408_06167_b200 import inputs as I
+    dev = d_db.device
     T = I.templates(CFG, I.CONFIGS[CFG]["n"], 0)
     n_t = T.shape[0]
     d_pt = torch.from_numpy(B.bm_encode_enroll(prm, T)).to(dev)
@@ -426,6 +444,7 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
     del d_pt
     d_db2 = torch.zeros_like(d_db)
     ws3 = torch.empty(B.bm_enroll_ws_bytes(prm, n_t), dtype=torch.uint8, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
     B.bm_enroll(prm, xk_dev, d_tl2, 0, d_db2, ws3)
@@ -438,20 +457,10 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
     sc = B.bm_decrypt(prm, sk, out_x.cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
     err4 = float(np.abs(sc - sb).max())
     assert err4 < 1e-4, err4
-    f4 = {"templates": n_t, "ms": round(ms_enroll, 3), "templates_per_s": round(n_t / (ms_enroll / 1e3), 1),
-          "score_check_max_abs_diff": err4,
-          "note": "server-side enrollment (Fig. 3) of the configs[1] DB, one template ciphertext at a time semantics, "
-                  "all templates in one bm_enroll call; scores vs the client-packed DB"}
-    return {"queries": nq, "ms_per_batch": round(ms, 4), "queries_per_s": round(nq / (ms / 1e3), 1),
-            "gmodmul_s": round(mm / (ms / 1e3) / 1e9, 2), "alu_frac": round(mm / (ms / 1e3) / 1e9 / peak, 4),
-            "kernel_launches": 1 + 2 * (p.bit_length() - 1),
-            "upload_bytes_per_query": {"client_expanded": p * 4 * N_RING * 8, "server_expanded": 6 * N_RING * 8},
-            "expand_plus_scan": {"ms_per_step": round(ms + ms_scan, 4),
-                                 "value": round(tq_per_step / ((ms + ms_scan) / 1e3), 1),
-                                 "unit": "templates*queries/s"},
-            "score_check_max_abs_diff": err,
-            "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24)",
-            "f4_enroll": f4}
+    return {"templates": n_t, "ms": round(ms_enroll, 3), "templates_per_s": round(n_t / (ms_enroll / 1e3), 1),
+            "score_check_max_abs_diff": err4,
+            "note": "server-side enrollment (Fig. 3) of the configs[1] DB, one template ciphertext at a time "
+                    "semantics, all templates in one bm_enroll call; scores vs the client-packed DB"}
 
 
 def run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream):

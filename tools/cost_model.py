@@ -11,6 +11,13 @@ configs[1] (d = 128, 6,144 templates, 384 queries) for every p:
 and the model  T(p) = sets(p) x nq x (p t_tensor + t_relin + log2(s) t_rot)  is compared with the
 measured step time; p* = argmin T(p).
 
+With f3 built, the paper's actual trade-off (Propositions 1-2: "As N_in increases,
+the direct computation time for cosine similarity decreases. However, the time to generate N_in
+ciphertexts increases") is measured too: bench.py's f3 leg times the server-side expansion of the
+same 384 queries, calibrated as  T_exp(p) = nq x p x (t_xmask + log2(p) t_xrot)  (one Mul(P) + Res per
+part, log2 p level-1 Rot + Add per part; least squares over the sweep), and the recognition-path
+optimum is argmin T(p) + T_exp(p) for this database size.
+
     python tools/cost_model.py [--ps 1,2,4,8,16,32,64,128] [--out profiles/r01_cost_model.txt]
 (runs bench.py on the GPU for each p)."""
 import argparse
@@ -25,7 +32,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def run(p):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--p", str(p), "--steps", "3", "--warmup", "3",
-           "--no-cpu-baseline", "--no-e2e", "--quiet"]
+           "--no-cpu-baseline", "--no-e2e", "--no-f1", "--no-f4", "--quiet"]
     out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
     return json.loads(out)
 
@@ -48,8 +55,10 @@ def main():
         t_tensor = pc["tensor"]["ms_per_step"] / (pairs * p)
         t_relin = (pc["digits"]["ms_per_step"] + pc["relin"]["ms_per_step"]) / pairs
         t_rot = pc["ladder"]["ms_per_step"] / (pairs * ls) if ls else None
+        f3 = r.get("f3_expand") or {}
         rows.append(dict(p=p, s=s, B=B, sets=sets, pairs=pairs, log_s=ls, ms=r["ms_per_step"],
                          value=r["value"], t_tensor=t_tensor, t_relin=t_relin, t_rot=t_rot,
+                         exp_ms=f3.get("ms_per_batch"),
                          classes={k: v["ms_per_step"] for k, v in pc.items()}))
     # calibrated op costs: medians over the sweep (they should be nearly p-independent)
     med = lambda xs: sorted(xs)[len(xs) // 2]
@@ -70,6 +79,27 @@ def main():
         if best is None or model < best[1]:
             best = (r["p"], model)
     lines.append(f"# model optimum: p* = {best[0]} (paper, CPU, with expansion + compression: N_in = 4)")
+    # f3: the expansion stage, T_exp(p) = nq p (t_xmask + log2(p) t_xrot), least squares
+    ex = [r for r in rows if r["exp_ms"] is not None]
+    if ex:
+        import numpy as np
+        A = np.array([[nq * r["p"], nq * r["p"] * math.log2(r["p"])] for r in ex])
+        y = np.array([r["exp_ms"] for r in ex])
+        (t_xmask, t_xrot), *_ = np.linalg.lstsq(A, y, rcond=None)
+        lines.append(f"# f3 server-side expansion of the {nq} queries: t_xmask (Mul(P) + Res, one part) = "
+                     f"{t_xmask * 1e3:.3f} us, t_xrot (level-1 Rot + Add) = {t_xrot * 1e3:.3f} us")
+        lines.append(f"{'p':>4} {'scan_ms':>9} {'expand_ms':>10} {'exp_model':>10} {'total_ms':>9} {'tq_per_s':>12}")
+        best2 = None
+        for r in ex:
+            em = nq * r["p"] * (t_xmask + math.log2(r["p"]) * t_xrot)
+            tot = r["ms"] + r["exp_ms"]
+            lines.append(f"{r['p']:>4} {r['ms']:>9.3f} {r['exp_ms']:>10.3f} {em:>10.3f} {tot:>9.3f} "
+                         f"{n_tmpl * nq / (tot / 1e3):>12.4g}")
+            if best2 is None or tot < best2[1]:
+                best2 = (r["p"], tot)
+        lines.append(f"# measured optimum of expansion + scan (the paper's trade-off, {n_tmpl} templates): "
+                     f"p* = {best2[0]}; the expansion is per query, the scan per (query, set), so p* grows "
+                     f"with the database")
     text = "\n".join(lines) + "\n"
     print(text)
     with open(a.out, "w") as f:
