@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libblindmatch.so")
+LIB_PATH = os.environ.get("BM_LIB_PATH") or os.path.join(_PKG, "libblindmatch.so")   # override: A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2408_06167_b200.build` "

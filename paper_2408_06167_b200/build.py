@@ -14,7 +14,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES = ["host.cpp", "device.cu"]
-HEADERS = ["bm_common.cuh", "bm_host.h", "ntt.cuh", "ntt2.cuh", "ntt3.cuh"]
+HEADERS = ["bm_common.cuh", "bm_host.h", "ntt.cuh", "ntt2.cuh", "ntt3.cuh", "ntt3f.cuh"]
 
 
 def _newer(target, deps):
@@ -42,7 +42,7 @@ def build(force=False, verbose=True):
             continue
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                   "-I", INC, "-c", path, "-o", obj]
+                   *os.environ.get("BM_NVCC_FLAGS", "").split(), "-I", INC, "-c", path, "-o", obj]
         else:
             cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wno-unknown-pragmas",
                    "-I", os.path.join(CUDA, "include"), "-I", INC, "-c", path, "-o", obj]

@@ -1367,8 +1367,8 @@ int ctx_get(DevCtx **out)
     for (int i = 0; i < 4; i++) {
         const HostPrime &H = host_prime(i);
         for (int k = 0; k < N; k++) {
-            h[(size_t)(2 * i) * N + k] = shoup_pair(H.fwd[k], H.q);
-            h[(size_t)(2 * i + 1) * N + k] = shoup_pair(H.inv[k], H.q);
+            h[(size_t)(2 * i) * N + tw_pos(k)] = shoup_pair(H.fwd[k], H.q);     // load-order storage
+            h[(size_t)(2 * i + 1) * N + tw_pos(k)] = shoup_pair(H.inv[k], H.q);
         }
     }
     if (cudaMalloc(&C->tw, h.size() * sizeof(ulonglong2)) != cudaSuccess) {
@@ -1388,7 +1388,7 @@ int ctx_get(DevCtx **out)
     {
         const HostPrime &H = host_prime(1);
         std::vector<ulonglong2> hf(2 * (size_t)N);
-        for (int k = 0; k < N; k++) hf[k] = fpair(H.fwd[k]), hf[(size_t)N + k] = fpair(H.inv[k]);
+        for (int k = 0; k < N; k++) hf[tw_pos(k)] = fpair(H.fwd[k]), hf[(size_t)N + tw_pos(k)] = fpair(H.inv[k]);
         if (cudaMalloc(&C->twf, hf.size() * sizeof(ulonglong2)) != cudaSuccess) {
             cudaFree(C->tw);
             delete C;

@@ -446,7 +446,6 @@ int bm_ck_export(const bm_ck *x, uint64_t *rlk2, uint64_t *gkl, uint64_t *gkc)
 int bm_xk_keygen(const bm_params *prm, uint64_t seed, bm_xk **out)
 {
     if (!prm || !out) return BM_ERR_INVALID_ARG;
-    const uint64_t Qs[3] = {Q0, Q1, QP};
     bm_xk *x = new (std::nothrow) bm_xk;
     if (!x) return BM_ERR_OOM;
     memcpy(x->digest, prm->digest, 32);

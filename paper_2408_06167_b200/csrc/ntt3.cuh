@@ -28,6 +28,21 @@ BM_D int j_M3(int tid, int k) { return 32 * (tid >> 1) + 2 * k + (tid & 1); }
 BM_D int j_M4(int tid, int e) { return 32 * (tid >> 1) + 4 * (e >> 1) + 2 * (tid & 1) + (e & 1); }
 BM_D int pos_M4(int tid, int e) { return 1024 * (e >> 1) + 2 * tid + (e & 1); }
 
+// Storage position of twiddle index k (k = 2^s + r, stage s) in the device tables.  Stages 0..8 are
+// stored as indexed (their loads are warp-uniform or lane-contiguous); stages 9..11 (r = G 2^(s-8) + kk,
+// G = tid >> 1) and 12 (r = 16 G + 2 m + odd) are stored in the order the 512-thread CTA loads them,
+// kk-major / m-major, so every twiddle load of a warp is one contiguous 256-512 B run instead of 16
+// strided sectors.  A bijection on [2^s, 2^(s+1)) per stage.
+BM_HD int tw_pos(int k)
+{
+    int s = 0;
+    while ((2 << s) <= k) s++;
+    const int r = k - (1 << s);
+    if (s <= 8) return k;
+    if (s <= 11) return (1 << s) + (r & ((1 << (s - 8)) - 1)) * 256 + (r >> (s - 8));
+    return 4096 + 512 * ((r >> 1) & 7) + 2 * (r >> 4) + (r & 1);
+}
+
 // Layout exchange through shared memory.  M2 and M3 partition j into per-warp 512-point regions
 // (warp w owns j in [512 w, 512 w + 512)), so an M2 <-> M3 exchange stays inside one warp and only
 // needs __syncwarp; exchanges with M1 span the CTA.  Hazards on the shared buffer: a CTA-wide
@@ -90,7 +105,8 @@ template <int PI, bool CANON = true> BM_D void fwd(uint64_t a[E], uint64_t *sm, 
         }
     }
     xchg<2, 3>(a, sm);
-    // pass 3: s = 8..11; twiddle (1<<s) + (G << (s-8)) + (k >> (12-s)), G = tid >> 1
+    // pass 3: s = 8..11; twiddle index (1<<s) + (G << (s-8)) + (k >> (12-s)), G = tid >> 1, stored at
+    // (1<<s) + (k >> (12-s)) 256 + G (tw_pos)
     const int G = tid >> 1, odd = tid & 1;
 #pragma unroll
     for (int s = 8; s < 12; s++) {
@@ -98,7 +114,7 @@ template <int PI, bool CANON = true> BM_D void fwd(uint64_t a[E], uint64_t *sm, 
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct4s<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (G << (s - 8)) + (k >> (12 - s))), s);
+            ct4s<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + ((k >> (12 - s)) << 8) + G), s);
         }
     }
     // stage 12 (t = 1) on lane pairs: the even lane takes butterflies k = 2m, the odd lane k = 2m+1
@@ -106,7 +122,7 @@ template <int PI, bool CANON = true> BM_D void fwd(uint64_t a[E], uint64_t *sm, 
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
-        ct4s<PI>(x, y, ldtw(P.fwd + 4096 + 16 * G + 2 * m + odd), 12);
+        ct4s<PI>(x, y, ldtw(P.fwd + 4096 + 512 * m + tid), 12);
         if (CANON || Q40<PI>) {
             a[2 * m] = reduce_bnd<PI>(x);
             a[2 * m + 1] = reduce_bnd<PI>(y);
@@ -124,7 +140,7 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
     const int G = tid >> 1, odd = tid & 1;
     // stage 12 (first executed, st = 0): in-register pairs (j, j+1)
 #pragma unroll
-    for (int m = 0; m < 8; m++) gs4s<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(P.inv + 4096 + 16 * G + 2 * m + odd));
+    for (int m = 0; m < 8; m++) gs4s<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(P.inv + 4096 + 512 * m + tid));
     // back to M3: even lane keeps a[2m] and receives a[2m+1]; odd lane keeps a[2m+1]
 #pragma unroll
     for (int m = 0; m < 8; m++) {
@@ -139,7 +155,7 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            const ulonglong2 w = ldtw(P.inv + (1 << s) + (G << (s - 8)) + (k >> (12 - s)));
+            const ulonglong2 w = ldtw(P.inv + (1 << s) + ((k >> (12 - s)) << 8) + G);
             switch (12 - s) {
             case 1: gs4s<PI, 1>(a[k], a[k + half], w); break;
             case 2: gs4s<PI, 2>(a[k], a[k + half], w); break;

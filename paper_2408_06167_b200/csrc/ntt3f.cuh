@@ -96,14 +96,14 @@ BM_D void fwd_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct_f(a[k], a[k + half], ldtw(tw + (1 << s) + (G << (s - 8)) + (k >> (12 - s))));
+            ct_f(a[k], a[k + half], ldtw(tw + (1 << s) + ((k >> (12 - s)) << 8) + G));
         }
     }
 #pragma unroll
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
-        ct_f(x, y, ldtw(tw + 4096 + 16 * G + 2 * m + odd));
+        ct_f(x, y, ldtw(tw + 4096 + 512 * m + tid));
         a[2 * m] = canon_f(as_d(x));
         a[2 * m + 1] = canon_f(as_d(y));
     }
@@ -117,7 +117,7 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = as_u(from_u(a[e]));
 #pragma unroll
-    for (int m = 0; m < 8; m++) gs_f<0>(a[2 * m], a[2 * m + 1], ldtw(tw + 4096 + 16 * G + 2 * m + odd));
+    for (int m = 0; m < 8; m++) gs_f<0>(a[2 * m], a[2 * m + 1], ldtw(tw + 4096 + 512 * m + tid));
 #pragma unroll
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
@@ -130,7 +130,7 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            const ulonglong2 w = ldtw(tw + (1 << s) + (G << (s - 8)) + (k >> (12 - s)));
+            const ulonglong2 w = ldtw(tw + (1 << s) + ((k >> (12 - s)) << 8) + G);
             switch (12 - s) {
             case 1: gs_f<1>(a[k], a[k + half], w); break;
             case 2: gs_f<2>(a[k], a[k + half], w); break;

@@ -75,7 +75,11 @@ int main(int argc, char **argv)
         if (v == 3 && pi != 1) continue; // v4 = q1 on the FP64 pipe
         const HostPrime &H = host_prime(pi);
         std::vector<ulonglong2> tw(2 * N);
-        for (int k = 0; k < N; k++) tw[k] = sp(H.fwd[k], H.q), tw[N + k] = sp(H.inv[k], H.q);
+        // v1/v2 cores index the tables directly; the v3 cores (ntt3.cuh) read them in load order (tw_pos)
+        for (int k = 0; k < N; k++) {
+            const int pos = v >= 2 ? v3::tw_pos(k) : k;
+            tw[pos] = sp(H.fwd[k], H.q), tw[N + pos] = sp(H.inv[k], H.q);
+        }
         ulonglong2 *dtw;
         cudaMalloc(&dtw, tw.size() * 16);
         cudaMemcpy(dtw, tw.data(), tw.size() * 16, cudaMemcpyHostToDevice);
@@ -90,7 +94,7 @@ int main(int argc, char **argv)
             auto fp = [](uint64_t w) { double a = (double)w, b = a / (double)Q1; uint64_t x, y;
                                        memcpy(&x, &a, 8); memcpy(&y, &b, 8); return make_ulonglong2(x, y); };
             std::vector<ulonglong2> tf(2 * N);
-            for (int k = 0; k < N; k++) tf[k] = fp(H.fwd[k]), tf[N + k] = fp(H.inv[k]);
+            for (int k = 0; k < N; k++) tf[v3::tw_pos(k)] = fp(H.fwd[k]), tf[N + v3::tw_pos(k)] = fp(H.inv[k]);
             cudaMalloc(&dtwf, tf.size() * 16);
             cudaMemcpy(dtwf, tf.data(), tf.size() * 16, cudaMemcpyHostToDevice);
             P.fwdf = dtwf; P.invf = dtwf + N;
