@@ -41,7 +41,7 @@ struct MatchK {
     ulonglong2 pinv[2]; // P^-1 mod q0, q1
     ulonglong2 q1inv;   // q1^-1 mod q0
     uint64_t pmod[2];   // P mod q0, q1
-    const ulonglong2 *rlk, *gk;
+    const uint64_t *rlk, *gk; // PLANAR Shoup keys: poly k at [2k N, 2k N + N) = w, [2k N + N, 2k N + 2N) = w'
     const uint64_t *db, *qry;
     uint64_t *out;
     int64_t n_sets;       // sets in the DB (output row length)
@@ -68,6 +68,16 @@ BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
 BM_D void st2(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
 
 BM_D uint64_t submod_d(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// Planar Shoup keys (rlk, ladder gk): plane w at kp[0, N), plane w' at kp[N, 2N).  One 16-byte load per
+// plane gives positions pos, pos + 1 (pos even, lane-contiguous across a warp, like the twiddles' tw_pos):
+// ka = (w, w') of pos, kb = (w, w') of pos + 1.
+BM_D void ldkey2(const uint64_t *kp, int pos, ulonglong2 &ka, ulonglong2 &kb)
+{
+    const ulonglong2 w = ld2(kp + pos), wp = ld2(kp + N + pos);
+    ka = make_ulonglong2(w.x, wp.x);
+    kb = make_ulonglong2(w.y, wp.y);
+}
 
 // ================================================================== K1: tensor (a4)
 // d0 = sum_i x0_i y0_i, d2 = sum_i x1_i y1_i, d1 = sum_i (x0_i + x1_i)(y0_i + y1_i) - d0 - d2 per
@@ -348,8 +358,8 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
-    // rlk layout [j][c][l][N]
-    const ulonglong2 *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * N;
+    // rlk layout [j][c][l] planar polys of 2N u64
+    const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
     const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
     const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
     const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N; // d_c[q0], d_c[q1]
@@ -359,8 +369,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 1 * N + j), v = ld2(xu + 3 * N + j);
-        const ulonglong2 k0a = ld2k(r0 + 2 * N + j), k0b = ld2k(r0 + 2 * N + j + 1);
-        const ulonglong2 k1a = ld2k(r1 + 2 * N + j), k1b = ld2k(r1 + 2 * N + j + 1);
+        ulonglong2 k0a, k0b, k1a, k1b;
+        ldkey2(r0 + 2 * 2 * N, j, k0a, k0b);
+        ldkey2(r1 + 2 * 2 * N, j, k1a, k1b);
         a[e] = red8to4<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a));
         a[e + 1] = red8to4<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b));
     }
@@ -373,8 +384,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
-        const ulonglong2 k0a = ld2k(r0 + 1 * N + j), k0b = ld2k(r0 + 1 * N + j + 1);
-        const ulonglong2 k1a = ld2k(r1 + 1 * N + j), k1b = ld2k(r1 + 1 * N + j + 1);
+        ulonglong2 k0a, k0b, k1a, k1b;
+        ldkey2(r0 + 1 * 2 * N, j, k0a, k0b);
+        ldkey2(r1 + 1 * 2 * N, j, k1a, k1b);
         // P^-1 KS_c[q1] (P^-1 is folded into the device rlk Q limbs), < 8 q1
         const uint64_t ka = shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a);
         const uint64_t kb = shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b);
@@ -401,8 +413,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
-        const ulonglong2 k0a = ld2k(r0 + j), k0b = ld2k(r0 + j + 1);
-        const ulonglong2 k1a = ld2k(r1 + j), k1b = ld2k(r1 + j + 1);
+        ulonglong2 k0a, k0b, k1a, k1b;
+        ldkey2(r0, j, k0a, k0b);
+        ldkey2(r1, j, k1a, k1b);
         const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // P^-1 KS_c[q0], < 8 q0
         const uint64_t kb = shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b);
         // d + P^-1 KS - A + 2 q0 < 11 q0
@@ -447,8 +460,9 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 #pragma unroll 1
     for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
         const bool last = i == L - 1;
-        const ulonglong2 *gq0 = K.gk + (size_t)(i * 4 + 0) * N, *gp0 = gq0 + N; // [rot][c][q0|P][N]
-        const ulonglong2 *gq1 = K.gk + (size_t)(i * 4 + 2) * N, *gp1 = gq1 + N;
+        // [rot][c][q0|P] planar polys of 2N u64
+        const uint64_t *gq0 = K.gk + (size_t)(i * 4 + 0) * 2 * N, *gp0 = gq0 + 2 * N;
+        const uint64_t *gq1 = K.gk + (size_t)(i * 4 + 2) * 2 * N, *gp1 = gq1 + 2 * N;
         __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
         // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
 #pragma unroll
@@ -459,8 +473,9 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 #pragma unroll
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
-            const ulonglong2 w0 = ld2k(gp0 + pos), w0b = ld2k(gp0 + pos + 1);
-            const ulonglong2 w1 = ld2k(gp1 + pos), w1b = ld2k(gp1 + pos + 1);
+            ulonglong2 w0, w0b, w1, w1b;
+            ldkey2(gp0, pos, w0, w0b);
+            ldkey2(gp1, pos, w1, w1b);
             st2(ks1 + pos, shoup4<2>(a[e], w1), shoup4<2>(a[e + 1], w1b));
             a[e] = shoup4<2>(a[e], w0);
             a[e + 1] = shoup4<2>(a[e + 1], w0b);
@@ -480,14 +495,16 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 #pragma unroll
             for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
             uint64_t *S = c ? S1 : S0;
-            const ulonglong2 *gq = c ? gq1 : gq0;
+            const uint64_t *gq = c ? gq1 : gq0;
             if (!last) {
                 fwd<0>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), canonical
+                ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
                     // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
-                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e)));
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
                     uint64_t v = ks + Q0 - a[e] + S[pidx(j)]; // < 6 q0
                     if (c == 0) v += S0[pidx(jp)];           // < 7 q0
                     a[e] = reduce_bnd<0>(v);
@@ -498,10 +515,12 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
             } else {
 #pragma unroll
                 for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = a[e]; // P^-1 y^c (coefficients), < 5 q0
+                ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const int j = j_M4(tid, e), jp = auto_perm(j, g);
-                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e)));
+                    if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
                     uint64_t v = ks + S[pidx(j)]; // < 5 q0
                     if (c == 0) v += S0[pidx(jp)];
                     a[e] = reduce_bnd<0>(v);
@@ -1271,6 +1290,7 @@ struct ConvK {
     int n_limbs;
     int lp[4];          // prime index of each limb
     uint64_t scale[4];  // k_key_ntt: constant folded into each limb (canonical, < q)
+    int planar;         // k_key_ntt: write (w, w') as two planes per polynomial (ldkey2) instead of pairs
 };
 
 // one block per polynomial; dir 0: coefficient -> NTT, 1: NTT -> coefficient
@@ -1313,7 +1333,14 @@ __global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const uint64_t w = (uint64_t)((u128)a[e] * sc % P.q); // setup only: plain 128-bit remainder
-        dst[(size_t)poly * N + pos_M4(tid, e)] = make_ulonglong2(w, (uint64_t)(((u128)w << 64) / P.q));
+        const uint64_t wp = (uint64_t)(((u128)w << 64) / P.q);
+        if (C.planar) {
+            uint64_t *d = reinterpret_cast<uint64_t *>(dst) + (size_t)poly * 2 * N;
+            d[pos_M4(tid, e)] = w;
+            d[N + pos_M4(tid, e)] = wp;
+        } else {
+            dst[(size_t)poly * N + pos_M4(tid, e)] = make_ulonglong2(w, wp);
+        }
     }
 }
 
@@ -1506,15 +1533,15 @@ struct bm_evk_dev {
     int dev;
     uint8_t digest[32];
     int32_t n_rot;
-    ulonglong2 *rlk; // [2][2][3][N]
-    ulonglong2 *gk;  // [n_rot][2][2][N]
+    ulonglong2 *rlk; // [2][2][3] planar polys (ldkey2): 2N u64 each
+    ulonglong2 *gk;  // [n_rot][2][2] planar polys
     int32_t n_hrot;  // f2 hoisted rotation keys (0: none)
     uint64_t *hgk;   // [n_hrot][2][2][N], NTT domain, plain residues (no Shoup companion), P^-1 in q0
 };
 
 // keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1)
 static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out,
-                            const uint64_t *scale = nullptr)
+                            const uint64_t *scale = nullptr, bool planar = false)
 {
     uint64_t *tmp = nullptr;
     ulonglong2 *dst = nullptr;
@@ -1532,6 +1559,7 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     K.n_limbs = n_limbs;
     for (int i = 0; i < 4; i++) K.lp[i] = i < n_limbs ? lp[i] : 0;
     for (int i = 0; i < 4; i++) K.scale[i] = scale && i < n_limbs ? scale[i] : 1;
+    K.planar = planar ? 1 : 0;
     k_key_ntt<<<(unsigned)n_polys, T, SMEM_BYTES>>>(K, dst);
     int rc = launch_check();
     if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
@@ -1584,8 +1612,9 @@ int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
     // device convention: P^-1 is folded into the Q limbs of the key-switching keys (the ModDown
     // multiplies every Q-limb inner product by P^-1 anyway; exact mod q, saves one product)
     const uint64_t sr[3] = {C->pinv[0].x, C->pinv[1].x, 1}, sg[2] = {C->pinv[0].x, 1};
-    rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk, sr);
-    if (!rc && evk->n_rot > 0) rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk, sg);
+    rc = upload_key_polys(C, evk->rlk.data(), 12, 3, lr, &d->rlk, sr, true);
+    if (!rc && evk->n_rot > 0)
+        rc = upload_key_polys(C, evk->gk.data(), 4 * (int64_t)evk->n_rot, 2, lg, &d->gk, sg, true);
     if (!rc && evk->n_hrot > 0) { // f2 keys: keep only the residues (the hoisted sum accumulates in 128 bits)
         ulonglong2 *pairs = nullptr;
         const int64_t np = 4 * (int64_t)evk->n_hrot;
@@ -2192,8 +2221,8 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     K.q1inv = C->q1inv;
     K.pmod[0] = C->pmod[0];
     K.pmod[1] = C->pmod[1];
-    K.rlk = evk->rlk;
-    K.gk = evk->gk;
+    K.rlk = reinterpret_cast<const uint64_t *>(evk->rlk);
+    K.gk = reinterpret_cast<const uint64_t *>(evk->gk);
     K.db = d_db;
     K.qry = d_q;
     K.out = d_out;
