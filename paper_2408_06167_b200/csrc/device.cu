@@ -78,6 +78,17 @@ BM_D void ldkey2(const uint64_t *kp, int pos, ulonglong2 &ka, ulonglong2 &kb)
     ka = make_ulonglong2(w.x, wp.x);
     kb = make_ulonglong2(w.y, wp.y);
 }
+// the same for a poly addressed as ulonglong2 * (a planar poly occupies the bytes of N pairs)
+BM_D void ldkey2(const ulonglong2 *kp, int pos, ulonglong2 &ka, ulonglong2 &kb)
+{
+    ldkey2(reinterpret_cast<const uint64_t *>(kp), pos, ka, kb);
+}
+// one position of a planar key (pos of any parity: two 8-byte loads)
+BM_D ulonglong2 ldkey1(const ulonglong2 *kp, int pos)
+{
+    const uint64_t *p = reinterpret_cast<const uint64_t *>(kp);
+    return make_ulonglong2(__ldg(p + pos), __ldg(p + N + pos));
+}
 
 // ================================================================== K1: tensor (a4)
 // d0 = sum_i x0_i y0_i, d2 = sum_i x1_i y1_i, d1 = sum_i (x0_i + x1_i)(y0_i + y1_i) - d0 - d2 per
@@ -748,8 +759,10 @@ __global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 v = ld2(cin + 2 * N + pos);
-        a[e] = shoup4<3>(v.x, ld2k(mk + 2 * N + pos));
-        a[e + 1] = shoup4<3>(v.y, ld2k(mk + 2 * N + pos + 1));
+        ulonglong2 ma, mb;
+        ldkey2(mk + 2 * N, pos, ma, mb);
+        a[e] = shoup4<3>(v.x, ma);
+        a[e + 1] = shoup4<3>(v.y, mb);
     }
     inv<3>(a, sm, K.pr[3]);
 #pragma unroll
@@ -765,7 +778,9 @@ __global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 v = ld2(cin + 1 * N + pos);
-        const uint64_t xa = shoup4<1>(v.x, ld2k(mk + 1 * N + pos)), xb = shoup4<1>(v.y, ld2k(mk + 1 * N + pos + 1));
+        ulonglong2 ma, mb;
+        ldkey2(mk + 1 * N, pos, ma, mb);
+        const uint64_t xa = shoup4<1>(v.x, ma), xb = shoup4<1>(v.y, mb);
         st2(co + 1 * N + pos, reduce_bnd<1>(xa + Q1 - a[e]), reduce_bnd<1>(xb + Q1 - a[e + 1]));
     }
     // q0 limb
@@ -779,7 +794,9 @@ __global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 v = ld2(cin + pos);
-        const uint64_t xa = shoup4<0>(v.x, ld2k(mk + pos)), xb = shoup4<0>(v.y, ld2k(mk + pos + 1));
+        ulonglong2 ma, mb;
+        ldkey2(mk, pos, ma, mb);
+        const uint64_t xa = shoup4<0>(v.x, ma), xb = shoup4<0>(v.y, mb);
         st2(co + pos, reduce_bnd<0>(xa + Q0 - a[e]), reduce_bnd<0>(xb + Q0 - a[e + 1]));
     }
 }
@@ -842,8 +859,11 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 2 * N + pos), v = ld2(xu + 5 * N + pos);
-        a[e] = red8to4<2>(shoup4<2>(u.x, ld2k(k0 + 2 * N + pos)) + shoup4<2>(v.x, ld2k(k1 + 2 * N + pos)));
-        a[e + 1] = red8to4<2>(shoup4<2>(u.y, ld2k(k0 + 2 * N + pos + 1)) + shoup4<2>(v.y, ld2k(k1 + 2 * N + pos + 1)));
+        ulonglong2 k0a, k0b, k1a, k1b;
+        ldkey2(k0 + 2 * N, pos, k0a, k0b);
+        ldkey2(k1 + 2 * N, pos, k1a, k1b);
+        a[e] = red8to4<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a));
+        a[e + 1] = red8to4<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b));
     }
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
@@ -882,12 +902,15 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             const ulonglong2 cv = K.enroll ? make_ulonglong2(0, 0)
                                            : *reinterpret_cast<const ulonglong2 *>(cc + (size_t)l * N + pos);
             uint64_t ka, kb;
+            ulonglong2 w0a, w0b, w1a, w1b;
+            ldkey2(kl0, pos, w0a, w0b);
+            ldkey2(kl1, pos, w1a, w1b);
             if (l) {
-                ka = shoup4<1>(u.x, ld2k(kl0 + pos)) + shoup4<1>(v.x, ld2k(kl1 + pos));
-                kb = shoup4<1>(u.y, ld2k(kl0 + pos + 1)) + shoup4<1>(v.y, ld2k(kl1 + pos + 1));
+                ka = shoup4<1>(u.x, w0a) + shoup4<1>(v.x, w1a);
+                kb = shoup4<1>(u.y, w0b) + shoup4<1>(v.y, w1b);
             } else {
-                ka = shoup4<0>(u.x, ld2k(kl0 + pos)) + shoup4<0>(v.x, ld2k(kl1 + pos));
-                kb = shoup4<0>(u.y, ld2k(kl0 + pos + 1)) + shoup4<0>(v.y, ld2k(kl1 + pos + 1));
+                ka = shoup4<0>(u.x, w0a) + shoup4<0>(v.x, w1a);
+                kb = shoup4<0>(u.y, w0b) + shoup4<0>(v.y, w1b);
             }
             uint64_t va = cv.x + ka + q - a[e], vb = cv.y + kb + q - a[e + 1]; // < 11 q
             if (c == 0) {
@@ -1025,10 +1048,12 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos);
-            a[e] = reduce_lazy<2>(shoup4<2>(u.x, ld2k(key(0, 3) + pos)) + shoup4<2>(v.x, ld2k(key(1, 3) + pos)) +
-                                  shoup4<2>(w.x, ld2k(key(2, 3) + pos)));
-            a[e + 1] = reduce_lazy<2>(shoup4<2>(u.y, ld2k(key(0, 3) + pos + 1)) + shoup4<2>(v.y, ld2k(key(1, 3) + pos + 1)) +
-                                      shoup4<2>(w.y, ld2k(key(2, 3) + pos + 1)));
+            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
+            ldkey2(key(0, 3), pos, k0a, k0b);
+            ldkey2(key(1, 3), pos, k1a, k1b);
+            ldkey2(key(2, 3), pos, k2a, k2b);
+            a[e] = reduce_lazy<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a) + shoup4<2>(w.x, k2a));
+            a[e + 1] = reduce_lazy<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b) + shoup4<2>(w.y, k2b));
         }
     }
     inv<2>(a, sm, K.pr[2]);
@@ -1041,10 +1066,12 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + 2 * N + pos);
-            a[e] = reduce_bnd<3>(dd.x + shoup4<3>(u.x, ld2k(key(0, 2) + pos)) + shoup4<3>(v.x, ld2k(key(1, 2) + pos)) +
-                                 shoup4<3>(w.x, ld2k(key(2, 2) + pos)));
-            a[e + 1] = reduce_bnd<3>(dd.y + shoup4<3>(u.y, ld2k(key(0, 2) + pos + 1)) +
-                                     shoup4<3>(v.y, ld2k(key(1, 2) + pos + 1)) + shoup4<3>(w.y, ld2k(key(2, 2) + pos + 1)));
+            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
+            ldkey2(key(0, 2), pos, k0a, k0b);
+            ldkey2(key(1, 2), pos, k1a, k1b);
+            ldkey2(key(2, 2), pos, k2a, k2b);
+            a[e] = reduce_bnd<3>(dd.x + shoup4<3>(u.x, k0a) + shoup4<3>(v.x, k1a) + shoup4<3>(w.x, k2a));
+            a[e + 1] = reduce_bnd<3>(dd.y + shoup4<3>(u.y, k0b) + shoup4<3>(v.y, k1b) + shoup4<3>(w.y, k2b));
         }
     }
     inv<3>(a, sm, K.pr[3]); // U, canonical
@@ -1075,17 +1102,17 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + (size_t)l * N + pos);
             uint64_t va, vb;
+            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
+            ldkey2(key(0, l), pos, k0a, k0b);
+            ldkey2(key(1, l), pos, k1a, k1b);
+            ldkey2(key(2, l), pos, k2a, k2b);
             if (l) {
-                va = dd.x + shoup4<1>(u.x, ld2k(key(0, 1) + pos)) + shoup4<1>(v.x, ld2k(key(1, 1) + pos)) +
-                     shoup4<1>(w.x, ld2k(key(2, 1) + pos)) + Q1 - a[e];
-                vb = dd.y + shoup4<1>(u.y, ld2k(key(0, 1) + pos + 1)) + shoup4<1>(v.y, ld2k(key(1, 1) + pos + 1)) +
-                     shoup4<1>(w.y, ld2k(key(2, 1) + pos + 1)) + Q1 - a[e + 1];
+                va = dd.x + shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a) + shoup4<1>(w.x, k2a) + Q1 - a[e];
+                vb = dd.y + shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b) + shoup4<1>(w.y, k2b) + Q1 - a[e + 1];
                 st2(co + pos, reduce_bnd<1>(shoup4<1>(va, C.q2inv[1])), reduce_bnd<1>(shoup4<1>(vb, C.q2inv[1])));
             } else {
-                va = dd.x + shoup4<0>(u.x, ld2k(key(0, 0) + pos)) + shoup4<0>(v.x, ld2k(key(1, 0) + pos)) +
-                     shoup4<0>(w.x, ld2k(key(2, 0) + pos)) + 2 * Q0 - a[e];
-                vb = dd.y + shoup4<0>(u.y, ld2k(key(0, 0) + pos + 1)) + shoup4<0>(v.y, ld2k(key(1, 0) + pos + 1)) +
-                     shoup4<0>(w.y, ld2k(key(2, 0) + pos + 1)) + 2 * Q0 - a[e + 1];
+                va = dd.x + shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a) + shoup4<0>(w.x, k2a) + 2 * Q0 - a[e];
+                vb = dd.y + shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b) + shoup4<0>(w.y, k2b) + 2 * Q0 - a[e + 1];
                 st2(co + pos, reduce_bnd<0>(shoup4<0>(va, C.q2inv[0])), reduce_bnd<0>(shoup4<0>(vb, C.q2inv[0])));
             }
         }
@@ -1106,8 +1133,10 @@ __global__ void __launch_bounds__(T, 1) k_cmp_mask(CmpK C)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 v = ld2(ci + N + pos);
-        a[e] = reduce_bnd<1>(shoup4<1>(v.x, ld2k(C.mask + N + pos)));
-        a[e + 1] = reduce_bnd<1>(shoup4<1>(v.y, ld2k(C.mask + N + pos + 1)));
+        ulonglong2 ma, mb;
+        ldkey2(C.mask + N, pos, ma, mb);
+        a[e] = reduce_bnd<1>(shoup4<1>(v.x, ma));
+        a[e + 1] = reduce_bnd<1>(shoup4<1>(v.y, mb));
     }
     inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // y, canonical
 #pragma unroll
@@ -1118,8 +1147,9 @@ __global__ void __launch_bounds__(T, 1) k_cmp_mask(CmpK C)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 v = ld2(ci + pos);
-        st2(co + pos, reduce_bnd<0>(shoup4<0>(v.x, ld2k(C.mask + pos)) + Q0 - a[e]),
-            reduce_bnd<0>(shoup4<0>(v.y, ld2k(C.mask + pos + 1)) + Q0 - a[e + 1]));
+        ulonglong2 ma, mb;
+        ldkey2(C.mask, pos, ma, mb);
+        st2(co + pos, reduce_bnd<0>(shoup4<0>(v.x, ma) + Q0 - a[e]), reduce_bnd<0>(shoup4<0>(v.y, mb) + Q0 - a[e + 1]));
     }
 }
 
@@ -1159,9 +1189,12 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
-        st2(ks1 + pos, shoup4<2>(a[e], ld2k(gk + 3 * N + pos)), shoup4<2>(a[e + 1], ld2k(gk + 3 * N + pos + 1)));
-        a[e] = shoup4<2>(a[e], ld2k(gk + N + pos));
-        a[e + 1] = shoup4<2>(a[e + 1], ld2k(gk + N + pos + 1));
+        ulonglong2 w0, w0b, w1, w1b;
+        ldkey2(gk + N, pos, w0, w0b);
+        ldkey2(gk + 3 * N, pos, w1, w1b);
+        st2(ks1 + pos, shoup4<2>(a[e], w1), shoup4<2>(a[e + 1], w1b));
+        a[e] = shoup4<2>(a[e], w0);
+        a[e + 1] = shoup4<2>(a[e + 1], w0b);
     }
 #pragma unroll 1
     for (int c = 0; c < 2; c++) {
@@ -1180,7 +1213,7 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
 #pragma unroll
         for (int e = 0; e < E; e++) {
             const int j = j_M4(tid, e), jp = auto_perm(j, g);
-            uint64_t v = shoup4<0>(S1[pidx(jp)], ld2k(gq + pos_M4(tid, e))); // [0, 4 q0)
+            uint64_t v = shoup4<0>(S1[pidx(jp)], ldkey1(gq, pos_M4(tid, e))); // [0, 4 q0)
             if (c == 0) v += S0[pidx(jp)];
             a[e] = reduce_bnd<0>(v);
         }
@@ -1278,7 +1311,7 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
 #pragma unroll
         for (int e = 0; e < E; e++) {
             const int j = pos_M4(tid, e);
-            dst[j] = csub(csub(shoup(c0[j], ld2k(key + j), q) + a[e], 2 * q), q);
+            dst[j] = csub(csub(shoup(c0[j], ldkey1(key, j), q) + a[e], 2 * q), q);
         }
     }
 }
@@ -1539,9 +1572,10 @@ struct bm_evk_dev {
     uint64_t *hgk;   // [n_hrot][2][2][N], NTT domain, plain residues (no Shoup companion), P^-1 in q0
 };
 
-// keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1)
+// keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1); planar
+// (default): per polynomial the w plane then the w' plane (read with ldkey2 / ldkey1)
 static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out,
-                            const uint64_t *scale = nullptr, bool planar = false)
+                            const uint64_t *scale = nullptr, bool planar = true)
 {
     uint64_t *tmp = nullptr;
     ulonglong2 *dst = nullptr;
@@ -1618,7 +1652,7 @@ int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
     if (!rc && evk->n_hrot > 0) { // f2 keys: keep only the residues (the hoisted sum accumulates in 128 bits)
         ulonglong2 *pairs = nullptr;
         const int64_t np = 4 * (int64_t)evk->n_hrot;
-        rc = upload_key_polys(C, evk->hgk.data(), np, 2, lg, &pairs, sg);
+        rc = upload_key_polys(C, evk->hgk.data(), np, 2, lg, &pairs, sg, false); // interleaved: w at +0
         if (!rc && cudaMalloc(&d->hgk, (size_t)np * N * 8) != cudaSuccess) rc = BM_ERR_OOM;
         if (!rc && cudaMemcpy2D(d->hgk, 8, pairs, 16, 8, (size_t)np * N, cudaMemcpyDeviceToDevice) != cudaSuccess)
             rc = BM_ERR_CUDA;
