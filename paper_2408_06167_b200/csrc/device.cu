@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 #pragma unroll
         for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
         inv<0>(a, XB, K.pr[0]);
-        fwd<2>(a, XB, K.pr[2]);
+        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
         // P-limb key-switch products for both components; component 1's waits in the workspace
 #pragma unroll
         for (int e = 0; e < E; e += 2) {
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
             uint64_t *S = c ? S1 : S0;
             const uint64_t *gq = c ? gq1 : gq0;
             if (!last) {
-                fwd<0>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), canonical
+                fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), lazy [0, 2 q0)
                 ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                     if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
                     // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
                     const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
-                    uint64_t v = ks + Q0 - a[e] + S[pidx(j)]; // < 6 q0
+                    uint64_t v = ks + 2 * Q0 - a[e] + S[pidx(j)]; // < 7 q0
                     if (c == 0) v += S0[pidx(jp)];           // < 7 q0
                     a[e] = reduce_bnd<0>(v);
                 }
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
             continue;
         }
         // ---- digit: X~P = NTT_P(x), staged next to c1
-        fwd<2>(a, XB, K.pr[2]);
+        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup / 128-bit product operand
 #pragma unroll
         for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
         __syncthreads();
@@ -1185,7 +1185,7 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
     inv<0>(a, XB, K.pr[0]);
-    fwd<2>(a, XB, K.pr[2]);
+    fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
