@@ -218,3 +218,47 @@ def test_enroll_errors(env, O):
     with pytest.raises(B.BMError) as e:
         B.bm_enroll(st.prm, xk_noenroll, d_in, 0, d_db, ws)
     assert e.value.name == "BM_ERR_INVALID_ARG"
+
+
+def test_next_row_api_errors(env, O):
+    """f3/f4/f1 entry points: empty batches are no-ops; too-small workspaces, keys made for other
+    parameters and missing Galois keys fail with their documented codes."""
+    torch, B = env
+    st = XSetup(env, O, 16, 4, I.random_unit(1, 16, 1))
+    d_in = torch.zeros((1, 2, 3, 8192), dtype=torch.int64, device="cuda")
+    d_out = torch.zeros((1, 4, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_expand_ws_bytes(st.prm, 1), dtype=torch.uint8, device="cuda")
+    B.bm_expand(st.prm, st.xk_dev, d_in, 0, d_out, ws)                        # nq = 0: no-op
+    small = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(B.BMError) as e:
+        B.bm_expand(st.prm, st.xk_dev, d_in, 1, d_out, small)
+    assert e.value.name == "BM_ERR_WORKSPACE"
+    other = B.bm_params_init(32, 4)                                            # xk made for d = 16
+    with pytest.raises(B.BMError) as e:
+        B.bm_expand(other, st.xk_dev, d_in, 1, d_out, ws)
+    assert e.value.name == "BM_ERR_KEY_MISMATCH"
+    # an imported key set without the strides the layout needs
+    pk_q2, gk1 = B.bm_xk_export(st.xk)
+    with pytest.raises(B.BMError) as e:
+        B.bm_xk_import(st.prm, pk_q2, gk1[:1])                                 # log2 p = 2 strides needed
+    assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+    xk_p = B.bm_xk_import(st.prm, pk_q2, gk1[:2])                              # expansion only (not log2 B)
+    xk_p_dev = B.bm_xk_to_device(st.prm, st.pk, xk_p)
+    B.bm_expand(st.prm, xk_p_dev, d_in, 1, d_out, ws)                          # enough for f3
+    d_db = torch.zeros((1, 4, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    wse = torch.empty(B.bm_enroll_ws_bytes(st.prm, 1), dtype=torch.uint8, device="cuda")
+    with pytest.raises(B.BMError) as e:
+        B.bm_enroll(st.prm, xk_p_dev, d_in, 0, d_db, wse)                      # f4 needs log2 B strides
+    assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+    # f1
+    ck_dev = B.bm_ck_to_device(st.prm, B.bm_ck_keygen(st.prm, 1))
+    q = torch.zeros((1, 4, 2, 3, 8192), dtype=torch.int64, device="cuda")
+    db = torch.zeros((2, 4, 2, 3, 8192), dtype=torch.int64, device="cuda")
+    out = torch.zeros((1, 1, 2, 8192), dtype=torch.int64, device="cuda")
+    with pytest.raises(B.BMError) as e:
+        B.bm_match_cmp(st.prm, ck_dev, db, 2, q, 1, out, small)
+    assert e.value.name == "BM_ERR_WORKSPACE"
+    with pytest.raises(B.BMError) as e:
+        B.bm_match_cmp(other, ck_dev, db, 2, q, 1, out, small)
+    assert e.value.name == "BM_ERR_KEY_MISMATCH"
+    B.bm_sync()
