@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
-    // rlk layout [j][c][l] planar polys of 2N u64
+    // rlk layout [j][c][l] planar polys of 2N u64.  K3 reads only the w planes (8-byte keys): each limb's
+    // inner product x0 k0 + x1 k1 is formed exactly in 128 bits and reduced once (red128s), half the
+    // key bytes of two Shoup products (K3 is load-bound: 5.94 -> 5.63 ms)
     const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
     const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
     const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
@@ -380,11 +382,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 1 * N + j), v = ld2(xu + 3 * N + j);
-        ulonglong2 k0a, k0b, k1a, k1b;
-        ldkey2(r0 + 2 * 2 * N, j, k0a, k0b);
-        ldkey2(r1 + 2 * 2 * N, j, k1a, k1b);
-        a[e] = red8to4<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a));
-        a[e + 1] = red8to4<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b));
+        const ulonglong2 w0 = ld2(r0 + 2 * 2 * N + j), w1 = ld2(r1 + 2 * 2 * N + j);
+        a[e] = red128s<2>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[2].r64);
+        a[e + 1] = red128s<2>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[2].r64);
     }
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
@@ -395,12 +395,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
-        ulonglong2 k0a, k0b, k1a, k1b;
-        ldkey2(r0 + 1 * 2 * N, j, k0a, k0b);
-        ldkey2(r1 + 1 * 2 * N, j, k1a, k1b);
-        // P^-1 KS_c[q1] (P^-1 is folded into the device rlk Q limbs), < 8 q1
-        const uint64_t ka = shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a);
-        const uint64_t kb = shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b);
+        const ulonglong2 w0 = ld2(r0 + 1 * 2 * N + j), w1 = ld2(r1 + 1 * 2 * N + j);
+        const uint64_t ka = red128s<1>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[1].r64);
+        const uint64_t kb = red128s<1>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[1].r64);
         a[e] = reduce_bnd<1>(dd.x + ka);
         a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
@@ -424,11 +421,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
         const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
-        ulonglong2 k0a, k0b, k1a, k1b;
-        ldkey2(r0, j, k0a, k0b);
-        ldkey2(r1, j, k1a, k1b);
-        const uint64_t ka = shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a); // P^-1 KS_c[q0], < 8 q0
-        const uint64_t kb = shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b);
+        const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
+        const uint64_t ka = red128s<0>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[0].r64);
+        const uint64_t kb = red128s<0>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[0].r64);
         // d + P^-1 KS - A + 2 q0 < 11 q0
         uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + 2 * Q0 - a[e], q1inv));
         uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + 2 * Q0 - a[e + 1], q1inv));
@@ -859,11 +854,11 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
         const ulonglong2 u = ld2(xu + 2 * N + pos), v = ld2(xu + 5 * N + pos);
-        ulonglong2 k0a, k0b, k1a, k1b;
-        ldkey2(k0 + 2 * N, pos, k0a, k0b);
-        ldkey2(k1 + 2 * N, pos, k1a, k1b);
-        a[e] = red8to4<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a));
-        a[e + 1] = red8to4<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b));
+        // 8-byte keys (w planes), exact 128-bit inner products, one reduction (as K3)
+        const ulonglong2 w0 = ld2(reinterpret_cast<const uint64_t *>(k0 + 2 * N) + pos);
+        const ulonglong2 w1 = ld2(reinterpret_cast<const uint64_t *>(k1 + 2 * N) + pos);
+        a[e] = red128s<2>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[2].r64);
+        a[e + 1] = red128s<2>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[2].r64);
     }
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
@@ -902,15 +897,15 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             const ulonglong2 cv = K.enroll ? make_ulonglong2(0, 0)
                                            : *reinterpret_cast<const ulonglong2 *>(cc + (size_t)l * N + pos);
             uint64_t ka, kb;
-            ulonglong2 w0a, w0b, w1a, w1b;
-            ldkey2(kl0, pos, w0a, w0b);
-            ldkey2(kl1, pos, w1a, w1b);
+            const ulonglong2 w0 = ld2(reinterpret_cast<const uint64_t *>(kl0) + pos);
+            const ulonglong2 w1 = ld2(reinterpret_cast<const uint64_t *>(kl1) + pos);
+            const u128 sa = (u128)u.x * w0.x + (u128)v.x * w1.x, sb = (u128)u.y * w0.y + (u128)v.y * w1.y;
             if (l) {
-                ka = shoup4<1>(u.x, w0a) + shoup4<1>(v.x, w1a);
-                kb = shoup4<1>(u.y, w0b) + shoup4<1>(v.y, w1b);
+                ka = red128s<1>(sa, K.pr[1].r64);
+                kb = red128s<1>(sb, K.pr[1].r64);
             } else {
-                ka = shoup4<0>(u.x, w0a) + shoup4<0>(v.x, w1a);
-                kb = shoup4<0>(u.y, w0b) + shoup4<0>(v.y, w1b);
+                ka = red128s<0>(sa, K.pr[0].r64);
+                kb = red128s<0>(sb, K.pr[0].r64);
             }
             uint64_t va = cv.x + ka + q - a[e], vb = cv.y + kb + q - a[e + 1]; // < 11 q
             if (c == 0) {
@@ -1040,6 +1035,8 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
     const uint64_t *dc = K.D01 + ((size_t)pi * 6 + c * 3) * N; // d_c[q0], d_c[q1], d_c[q2]
     // rlk2 [j][c][l][N], l: 0 q0, 1 q1, 2 q2, 3 P
     auto key = [&](int j, int l) { return C.rlk2 + (((size_t)j * 2 + c) * 4 + l) * N; };
+    // 8-byte keys: the w plane of a planar poly (positions pos, pos + 1); exact 128-bit inner products
+    auto kw = [&](int j, int l, int pos) { return ld2(reinterpret_cast<const uint64_t *>(key(j, l)) + pos); };
     uint64_t a[E];
     // ---- P limb
     {
@@ -1048,12 +1045,9 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos);
-            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
-            ldkey2(key(0, 3), pos, k0a, k0b);
-            ldkey2(key(1, 3), pos, k1a, k1b);
-            ldkey2(key(2, 3), pos, k2a, k2b);
-            a[e] = reduce_lazy<2>(shoup4<2>(u.x, k0a) + shoup4<2>(v.x, k1a) + shoup4<2>(w.x, k2a));
-            a[e + 1] = reduce_lazy<2>(shoup4<2>(u.y, k0b) + shoup4<2>(v.y, k1b) + shoup4<2>(w.y, k2b));
+            const ulonglong2 k0 = kw(0, 3, pos), k1 = kw(1, 3, pos), k2 = kw(2, 3, pos);
+            a[e] = red128s<2>((u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x, K.pr[2].r64);
+            a[e + 1] = red128s<2>((u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y, K.pr[2].r64);
         }
     }
     inv<2>(a, sm, K.pr[2]);
@@ -1066,12 +1060,10 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + 2 * N + pos);
-            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
-            ldkey2(key(0, 2), pos, k0a, k0b);
-            ldkey2(key(1, 2), pos, k1a, k1b);
-            ldkey2(key(2, 2), pos, k2a, k2b);
-            a[e] = reduce_bnd<3>(dd.x + shoup4<3>(u.x, k0a) + shoup4<3>(v.x, k1a) + shoup4<3>(w.x, k2a));
-            a[e + 1] = reduce_bnd<3>(dd.y + shoup4<3>(u.y, k0b) + shoup4<3>(v.y, k1b) + shoup4<3>(w.y, k2b));
+            const ulonglong2 k0 = kw(0, 2, pos), k1 = kw(1, 2, pos), k2 = kw(2, 2, pos);
+            a[e] = reduce_bnd<3>(dd.x + red128s<3>((u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x, K.pr[3].r64));
+            a[e + 1] =
+                reduce_bnd<3>(dd.y + red128s<3>((u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y, K.pr[3].r64));
         }
     }
     inv<3>(a, sm, K.pr[3]); // U, canonical
@@ -1102,17 +1094,16 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + (size_t)l * N + pos);
             uint64_t va, vb;
-            ulonglong2 k0a, k0b, k1a, k1b, k2a, k2b;
-            ldkey2(key(0, l), pos, k0a, k0b);
-            ldkey2(key(1, l), pos, k1a, k1b);
-            ldkey2(key(2, l), pos, k2a, k2b);
+            const ulonglong2 k0 = kw(0, l, pos), k1 = kw(1, l, pos), k2 = kw(2, l, pos);
+            const u128 sa = (u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x;
+            const u128 sb = (u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y;
             if (l) {
-                va = dd.x + shoup4<1>(u.x, k0a) + shoup4<1>(v.x, k1a) + shoup4<1>(w.x, k2a) + Q1 - a[e];
-                vb = dd.y + shoup4<1>(u.y, k0b) + shoup4<1>(v.y, k1b) + shoup4<1>(w.y, k2b) + Q1 - a[e + 1];
+                va = dd.x + red128s<1>(sa, K.pr[1].r64) + Q1 - a[e];
+                vb = dd.y + red128s<1>(sb, K.pr[1].r64) + Q1 - a[e + 1];
                 st2(co + pos, reduce_bnd<1>(shoup4<1>(va, C.q2inv[1])), reduce_bnd<1>(shoup4<1>(vb, C.q2inv[1])));
             } else {
-                va = dd.x + shoup4<0>(u.x, k0a) + shoup4<0>(v.x, k1a) + shoup4<0>(w.x, k2a) + 2 * Q0 - a[e];
-                vb = dd.y + shoup4<0>(u.y, k0b) + shoup4<0>(v.y, k1b) + shoup4<0>(w.y, k2b) + 2 * Q0 - a[e + 1];
+                va = dd.x + red128s<0>(sa, K.pr[0].r64) + 2 * Q0 - a[e];
+                vb = dd.y + red128s<0>(sb, K.pr[0].r64) + 2 * Q0 - a[e + 1];
                 st2(co + pos, reduce_bnd<0>(shoup4<0>(va, C.q2inv[0])), reduce_bnd<0>(shoup4<0>(vb, C.q2inv[0])));
             }
         }
