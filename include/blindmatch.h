@@ -70,7 +70,7 @@ typedef struct bm_params {
     uint64_t q[3];          /* q0, q1, P                               */
     double scale;           /* 2^40                                    */
     double out_scale;       /* 2^80 / q1: scale of bm_match outputs    */
-    uint8_t digest[32];     /* digest of (N, primes, scale, d, p)      */
+    uint8_t digest[32];     /* digest of (N, q0, q1, P, scale); not of the layout (d, p) */
     uint64_t q2;            /* f3 only: the extra 40-bit prime of level 2 (2^40 - 45 2^14 + 1) */
 } bm_params;
 
@@ -148,6 +148,19 @@ int bm_ct_to_coeff(const bm_params *, const uint64_t *d_in, int64_t n_cts, int32
                    void *stream);
 int bm_ct_from_coeff(const bm_params *, const uint64_t *d_in, int64_t n_cts, int32_t n_limbs, uint64_t *d_out,
                      void *stream);
+
+/* Ciphertext (de)serialisation: a framed canonical byte form for
+ * storage and the network.  64-byte header {"BMCT", version 1, the params digest, level, limbs, scale,
+ * n_cts} + n_cts x [2][level+1 limbs][N] little-endian u64 residues in [0, q), COEFFICIENT domain
+ * (convert device NTT-domain ciphertexts with bm_ct_to_coeff first).  Levels 0, 1 and 2 (the f1/f3/f4
+ * chain, limbs q0, q1, q2).  bm_ct_export with buf = NULL returns the size in *len.  bm_ct_import with
+ * ct = NULL returns n_cts / level / scale only.  Host memory.  Errors: BM_ERR_INVALID_ARG (bad frame,
+ * short buffer, non-canonical residue), BM_ERR_KEY_MISMATCH (frame made for other params),
+ * BM_ERR_LEVEL. */
+int bm_ct_export(const bm_params *, const uint64_t *ct, int64_t n_cts, int32_t level, double scale, uint8_t *buf,
+                 size_t *len);
+int bm_ct_import(const bm_params *, const uint8_t *buf, size_t len, uint64_t *ct, int64_t *n_cts, int32_t *level,
+                 double *scale);
 
 /* THE HOT PATH: HE-C^3 scan of nq queries against n_sets sets.
  * d_db:  device [n_sets][p][2][2][N] level-1 NTT-domain DB (bm_encrypt output);

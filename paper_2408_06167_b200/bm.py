@@ -77,6 +77,9 @@ _SIGS = {
     "bm_profile_read": (_i32, [_vp, _vp, _vp]),
     "bm_decrypt": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_decrypt_raw": (_i32, [_P, _vp, _vp, _i64, _vp]),
+    "bm_ct_export": (_i32, [_P, _vp, _i64, _i32, ctypes.c_double, _vp, ctypes.POINTER(_sz)]),
+    "bm_ct_import": (_i32, [_P, _vp, _sz, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32),
+                            ctypes.POINTER(ctypes.c_double)]),
     "bm_top1": (_i32, [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
     # f3: server-side query expansion (Algorithm 1) on the chain extended by q2
     "bm_xk_keygen": (_i32, [_P, _u64, _pp]), "bm_xk_free": (None, [_vp]),
@@ -524,3 +527,28 @@ def bm_decrypt_packed(prm, sk, h_ct):
     out = np.zeros((n, SLOTS), np.float64)
     _chk(_lib.bm_decrypt_packed(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt_packed")
     return out
+
+
+# --------------------------------------------------------------------------- serialisation
+def bm_ct_export(prm, ct, level, scale):
+    """ct: uint64 [n][2][level+1][N] coefficient domain (host) -> framed bytes."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    n = ct.size // (2 * (level + 1) * N)
+    ln = _sz()
+    _chk(_lib.bm_ct_export(ctypes.byref(prm), _np_ptr(ct), n, level, scale, None, ctypes.byref(ln)), "bm_ct_export")
+    buf = np.zeros(ln.value, np.uint8)
+    _chk(_lib.bm_ct_export(ctypes.byref(prm), _np_ptr(ct), n, level, scale, _np_ptr(buf), ctypes.byref(ln)),
+         "bm_ct_export")
+    return buf.tobytes()
+
+
+def bm_ct_import(prm, data):
+    """framed bytes -> (ct uint64 [n][2][level+1][N], level, scale)."""
+    buf = np.frombuffer(data, np.uint8).copy()
+    n, lev, sc = _i64(), _i32(), ctypes.c_double()
+    _chk(_lib.bm_ct_import(ctypes.byref(prm), _np_ptr(buf), buf.size, None, ctypes.byref(n), ctypes.byref(lev),
+                           ctypes.byref(sc)), "bm_ct_import")
+    ct = np.zeros((n.value, 2, lev.value + 1, N), np.uint64)
+    _chk(_lib.bm_ct_import(ctypes.byref(prm), _np_ptr(buf), buf.size, _np_ptr(ct) if n.value else None,
+                           ctypes.byref(n), ctypes.byref(lev), ctypes.byref(sc)), "bm_ct_import")
+    return ct, lev.value, sc.value

@@ -754,6 +754,81 @@ int bm_encode_enroll(const bm_params *prm, const double *v, int64_t n, int64_t *
     return BM_OK;
 }
 
+// ------------------------------------------------------------------ serialisation
+// Frame: 64-byte header {char magic[4] = "BMCT", u32 version = 1, u8 digest[32], i32 level,
+// i32 n_limbs, f64 scale, i64 n_cts} followed by n_cts x [2][n_limbs][N] u64 little-endian residues in
+// [0, q) of the COEFFICIENT domain (device NTT-domain ciphertexts go through bm_ct_to_coeff first).
+// Level 2 (f1/f3/f4: limbs q0, q1, q2), level 1 (q0, q1), level 0 (q0).
+namespace {
+struct CtHeader {
+    char magic[4];
+    uint32_t version;
+    uint8_t digest[32];
+    int32_t level, n_limbs;
+    double scale;
+    int64_t n_cts;
+};
+static_assert(sizeof(CtHeader) == 64, "frame header is 64 bytes");
+const int LEVEL_PRIMES[3] = {0, 1, 3}; // host prime index of limb l
+bool ct_canonical(const uint64_t *ct, int64_t n_cts, int n_limbs)
+{
+    for (int64_t c = 0; c < n_cts * 2; c++)
+        for (int l = 0; l < n_limbs; l++) {
+            const uint64_t q = host_prime(LEVEL_PRIMES[l]).q;
+            const uint64_t *v = ct + ((size_t)c * n_limbs + l) * N;
+            for (int k = 0; k < N; k++)
+                if (v[k] >= q) return false;
+        }
+    return true;
+}
+} // namespace
+
+int bm_ct_export(const bm_params *prm, const uint64_t *ct, int64_t n_cts, int32_t level, double scale, uint8_t *buf,
+                 size_t *len)
+{
+    if (!prm || !len || n_cts < 0 || (n_cts > 0 && !ct)) return BM_ERR_INVALID_ARG;
+    if (level < 0 || level > 2) return BM_ERR_LEVEL;
+    const int nl = level + 1;
+    const size_t need = sizeof(CtHeader) + (size_t)n_cts * 2 * nl * N * sizeof(uint64_t);
+    if (!buf) {
+        *len = need;
+        return BM_OK;
+    }
+    if (*len < need) return BM_ERR_INVALID_ARG;
+    if (!ct_canonical(ct, n_cts, nl)) return BM_ERR_INVALID_ARG;
+    CtHeader h;
+    memcpy(h.magic, "BMCT", 4);
+    h.version = 1;
+    memcpy(h.digest, prm->digest, 32);
+    h.level = level;
+    h.n_limbs = nl;
+    h.scale = scale;
+    h.n_cts = n_cts;
+    memcpy(buf, &h, sizeof h); // the library runs on little-endian hosts only (x86-64 / aarch64)
+    memcpy(buf + sizeof h, ct, need - sizeof h);
+    *len = need;
+    return BM_OK;
+}
+
+int bm_ct_import(const bm_params *prm, const uint8_t *buf, size_t len, uint64_t *ct, int64_t *n_cts, int32_t *level,
+                 double *scale)
+{
+    if (!prm || !buf || len < sizeof(CtHeader)) return BM_ERR_INVALID_ARG;
+    CtHeader h;
+    memcpy(&h, buf, sizeof h);
+    if (memcmp(h.magic, "BMCT", 4) || h.version != 1) return BM_ERR_INVALID_ARG;
+    if (memcmp(h.digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (h.level < 0 || h.level > 2 || h.n_limbs != h.level + 1 || h.n_cts < 0) return BM_ERR_LEVEL;
+    const size_t need = sizeof h + (size_t)h.n_cts * 2 * h.n_limbs * N * sizeof(uint64_t);
+    if (len != need) return BM_ERR_INVALID_ARG;
+    if (n_cts) *n_cts = h.n_cts;
+    if (level) *level = h.level;
+    if (scale) *scale = h.scale;
+    if (!ct) return BM_OK; // size query
+    memcpy(ct, buf + sizeof h, need - sizeof h);
+    return ct_canonical(ct, h.n_cts, h.n_limbs) ? BM_OK : BM_ERR_INVALID_ARG;
+}
+
 // ------------------------------------------------------------------ decryption
 int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, int64_t *m)
 {

@@ -195,3 +195,37 @@ def test_compression_keys_match_oracle(B, O, d, p):
     m = B.bm_encode_cmp_mask(prm)
     om = O.cmp_mask(13, d, p)
     assert np.abs(m - om).max() <= 1 and (m != om).mean() < 1e-3
+
+
+
+# ----------------------------------------------------------------------------- serialisation
+def test_ciphertext_frame_roundtrip_and_errors(B, O):
+    """bm_ct_export / bm_ct_import: oracle ciphertexts of levels 0, 1, 2 survive the
+    frame bit for bit with level and scale; other params, a bad magic, a short buffer and a
+    non-canonical residue are rejected."""
+    prm = B.bm_params_init(16, 1)
+    sk, pk, rlk, gk = O.keygen(13, 1, 0)
+    pk_q2, _ = O.keygen_exp(13, 1, 16, 1)
+    pt = O.encode(np.random.default_rng(3).uniform(-1, 1, (2, 4096)), 13)
+    c1 = O.encrypt(13, pk, pt, 0, 9)
+    c2 = O.encrypt_l2(13, pk, pk_q2, pt, 0, 9)
+    c0 = np.ascontiguousarray(c1[:, :, :1, :])
+    for ct, lev, sc in ((c0, 0, 2.0 ** 80 / prm.q[1]), (c1, 1, 2.0 ** 40), (c2, 2, 2.0 ** 40)):
+        data = B.bm_ct_export(prm, ct, lev, sc)
+        assert len(data) == 64 + ct.size * 8 and data[:4] == b"BMCT"
+        back, lev2, sc2 = B.bm_ct_import(prm, data)
+        assert lev2 == lev and sc2 == sc and np.array_equal(back, ct)
+    data = B.bm_ct_export(prm, c1, 1, 2.0 ** 40)
+    other = bytearray(data)
+    other[8] ^= 1                                      # a frame made under another parameter digest
+    with pytest.raises(B.BMError) as e:
+        B.bm_ct_import(prm, bytes(other))
+    assert e.value.name == "BM_ERR_KEY_MISMATCH"
+    with pytest.raises(B.BMError):
+        B.bm_ct_import(prm, b"XXXX" + data[4:])
+    with pytest.raises(B.BMError):
+        B.bm_ct_import(prm, data[:-8])
+    bad = c1.copy()
+    bad[0, 1, 1, 5] = prm.q[1]
+    with pytest.raises(B.BMError):
+        B.bm_ct_export(prm, bad, 1, 2.0 ** 40)
