@@ -436,6 +436,89 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     }
 }
 
+// ================================================================== TMEM as thread-private scratch
+// The ladder's two per-thread scratch arrays (component 1's P-limb key-switch product, waiting for
+// component 0's INTT_P; the last step's t_1) live in tensor memory instead of global memory: 16 u64
+// per thread each, written and read back by the same thread.  With the 32x32b shape a warp reaches the
+// 32 TMEM lanes of its quarter (warp & 3); the four warps sharing a quarter use disjoint 64-column
+// ranges (warp >> 2), so the CTA allocates 256 of the SM's 512 columns (one CTA per SM).
+constexpr uint32_t TMEM_COLS = 256;
+BM_D uint32_t tmem_alloc(uint32_t *s_addr) // all threads; returns this thread's scratch base address
+{
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_addr)),
+                     "n"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    return *s_addr + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
+}
+BM_D void tmem_free(uint32_t base) // all threads, after every TMEM access of the CTA
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(TMEM_COLS) : "memory");
+}
+// 16 u64 of this thread <-> 32 TMEM columns of its lane
+BM_D void tmem_st16(uint32_t taddr, const uint64_t v[E])
+{
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 16; i++) r[2 * i] = (uint32_t)v[i], r[2 * i + 1] = (uint32_t)(v[i] >> 32);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
+                 "%32};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+                 "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+                 "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+BM_D void tmem_st8(uint32_t taddr, const uint64_t v[8]) // 8 u64 <-> 16 columns
+{
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 8; i++) r[2 * i] = (uint32_t)v[i], r[2 * i + 1] = (uint32_t)(v[i] >> 32);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+BM_D void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
+{
+    uint32_t r[32];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                 "[%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                   "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                   "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr)
+                 : "memory");
+    // the registers are valid only after wait::ld: make them operands of it so nothing reads them earlier
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = (uint64_t)r[2 * i] | ((uint64_t)r[2 * i + 1] << 32);
+}
+
 // ================================================================== fused ladder (a7 + a8)
 // One CTA runs the whole log2(s)-step rotate-and-add ladder of one pair with
 // the level-0 ciphertext C = (c0, c1) resident in shared memory (NTT domain, indexed by NTT index
@@ -457,7 +540,8 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
-    uint64_t *ks1 = K.D2 + (size_t)pi * 2 * N, *tsc = ks1 + N; // D2 is dead after K3
+    __shared__ uint32_t s_tmem;
+    const uint32_t tks1 = tmem_alloc(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
     stage_by_j(S0, cin.at(pi, 0));
     stage_by_j(S1, cin.at(pi, 1));
@@ -477,25 +561,25 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
         // P-limb key-switch products for both components; component 1's waits in the workspace
 #pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int pos = pos_M4(tid, e);
-            ulonglong2 w0, w0b, w1, w1b;
-            ldkey2(gp0, pos, w0, w0b);
-            ldkey2(gp1, pos, w1, w1b);
-            st2(ks1 + pos, shoup4<2>(a[e], w1), shoup4<2>(a[e + 1], w1b));
-            a[e] = shoup4<2>(a[e], w0);
-            a[e + 1] = shoup4<2>(a[e + 1], w0b);
+        for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live registers)
+            uint64_t k1[8];
+#pragma unroll
+            for (int e = 8 * h; e < 8 * h + 8; e += 2) {
+                const int pos = pos_M4(tid, e);
+                ulonglong2 w0, w0b, w1, w1b;
+                ldkey2(gp0, pos, w0, w0b);
+                ldkey2(gp1, pos, w1, w1b);
+                k1[e - 8 * h] = shoup4<2>(a[e], w1);
+                k1[e - 8 * h + 1] = shoup4<2>(a[e + 1], w1b);
+                a[e] = shoup4<2>(a[e], w0);
+                a[e + 1] = shoup4<2>(a[e + 1], w0b);
+            }
+            tmem_st8(tks1 + 16 * h, k1);
         }
+        tmem_wait_st();
 #pragma unroll 1
         for (int c = 0; c < 2; c++) {
-            if (c == 1) { // written by this thread above: coherent (not .nc) loads
-#pragma unroll
-                for (int e = 0; e < E; e += 2) {
-                    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(ks1 + pos_M4(tid, e));
-                    a[e] = v.x;
-                    a[e + 1] = v.y;
-                }
-            }
+            if (c == 1) tmem_ld16(tks1, a); // component 1's P-limb product, parked in TMEM above
             inv<2>(a, XB, K.pr[2]);
             // P^-1 y^c mod q0 with y^c = y - [y > P/2] P:  P^-1 y - [y > P/2], < 5 q0
 #pragma unroll
@@ -519,8 +603,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
 #pragma unroll
                 for (int e = 0; e < E; e++) S[pidx(j_M4(tid, e))] = a[e];
             } else {
-#pragma unroll
-                for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = a[e]; // P^-1 y^c (coefficients), < 5 q0
+                tmem_st16(ttsc, a); // P^-1 y^c (coefficient j_M1(tid, e)), < 5 q0
                 ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
@@ -533,14 +616,14 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                 }
                 inv<0>(a, XB, K.pr[0]);
                 uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+                uint64_t t[E];
+                tmem_ld16(ttsc, t);
 #pragma unroll
-                for (int e = 0; e < E; e++) {
-                    const int j = j_M1(tid, e);
-                    o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
-                }
+                for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
             }
         }
     }
+    tmem_free(s_tmem);
 }
 
 // ================================================================== f2: hoisted rotation sum
