@@ -442,28 +442,34 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
 // per thread each, written and read back by the same thread.  With the 32x32b shape a warp reaches the
 // 32 TMEM lanes of its quarter (warp & 3); the four warps sharing a quarter use disjoint 64-column
 // ranges (warp >> 2), so the CTA allocates 256 of the SM's 512 columns (one CTA per SM).
-constexpr uint32_t TMEM_COLS = 256;
-BM_D uint32_t tmem_alloc(uint32_t *s_addr) // all threads; returns this thread's scratch base address
+// COLS: the CTA's allocation (power of two, <= 512); each thread owns COLS / 4 columns of its lane
+template <uint32_t COLS> BM_D uint32_t tmem_alloc(uint32_t *s_addr) // all threads; this thread's base
 {
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(s_addr)),
-                     "n"(TMEM_COLS)
+                     "n"(COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    return *s_addr + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
+    return *s_addr + ((uint32_t)(32 * (warp & 3)) << 16) + (COLS / 4) * (uint32_t)(warp >> 2);
 }
-BM_D void tmem_free(uint32_t base) // all threads, after every TMEM access of the CTA
+template <uint32_t COLS> BM_D void tmem_free(uint32_t base) // all threads, after every TMEM access of the CTA
 {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if ((threadIdx.x >> 5) == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
+}
+BM_D void tmem_st2(uint32_t taddr, uint64_t x, uint64_t y) // 2 u64 <-> 4 columns (wait::st before reading)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"((uint32_t)x),
+                 "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32))
+                 : "memory");
 }
 // 16 u64 of this thread <-> 32 TMEM columns of its lane
 BM_D void tmem_st16(uint32_t taddr, const uint64_t v[E])
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
     __shared__ uint32_t s_tmem;
-    const uint32_t tks1 = tmem_alloc(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
+    const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
     stage_by_j(S0, cin.at(pi, 0));
     stage_by_j(S1, cin.at(pi, 1));
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
             }
         }
     }
-    tmem_free(s_tmem);
+    tmem_free<256>(s_tmem);
 }
 
 // ================================================================== f2: hoisted rotation sum
@@ -647,8 +653,11 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
     uint64_t *SP = sm + SMEM_WORDS; // reused for c0 after the rotation products
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x;
-    // scratch (dead after K3): A -> D01 [c][q0 | P], base_0 -> D2[0], P^-1 y^ -> D2[1]
-    uint64_t *Ab = K.D01 + (size_t)pi * 4 * N, *b0s = K.D2 + (size_t)pi * 2 * N, *tsc = b0s + N;
+    // A [c][q0 | P] (thread-private: 16 u64 per thread and polynomial) lives in TMEM, columns 32 v + 2 e,
+    // and P^-1 y^c reuses A[c][P]'s columns once consumed; base_0 waits in the D2 scratch (dead after K3)
+    __shared__ uint32_t s_tmem;
+    const uint32_t tA = tmem_alloc<512>(&s_tmem);
+    uint64_t *b0s = K.D2 + (size_t)pi * 2 * N;
     const ulonglong2 pinv = K.pinv[0];
     // Phases share one call site per transform (an instruction-cache concern: every unrolled
     // transform is ~40 KB of SASS): ph 0 = the digit, ph 1, 2 = the ModDown of component ph - 1.
@@ -661,33 +670,33 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
 #pragma unroll
             for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
         } else {       // y^c = INTT_P(A[c][P]); a = base_c + A[c][q0]
-#pragma unroll
-            for (int e = 0; e < E; e += 2) { // written by this thread: coherent loads
-                const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c + 1) * N + pos_M4(tid, e));
-                a[e] = v.x;
-                a[e + 1] = v.y;
-            }
+            tmem_ld16(tA + 32 * (2 * c + 1), a); // A[c][P]
             inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
 #pragma unroll
-            for (int e = 0; e < E; e++) tsc[j_M1(tid, e)] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            tmem_st16(tA + 32 * (2 * c + 1), a); // P^-1 y^c (coefficient j_M1(tid, e)) over A[c][P]
             const uint64_t *base = c ? cin.at(pi, 1) : b0s;
 #pragma unroll
             for (int e = 0; e < E; e += 2) {
                 const int pos = pos_M4(tid, e);
                 const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
-                const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Ab + (size_t)(2 * c) * N + pos);
-                a[e] = csub(bv.x + av.x, Q0);
-                a[e + 1] = csub(bv.y + av.y, Q0);
+                a[e] = bv.x;
+                a[e + 1] = bv.y;
+            }
+            {
+                uint64_t av[E];
+                tmem_ld16(tA + 32 * (2 * c), av); // A[c][q0]
+#pragma unroll
+                for (int e = 0; e < E; e++) a[e] = csub(a[e] + av[e], Q0);
             }
         }
         inv<0>(a, XB, K.pr[0]);
         if (ph > 0) { // out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c
             uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+            uint64_t t[E];
+            tmem_ld16(tA + 32 * (2 * c + 1), t);
 #pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int j = j_M1(tid, e);
-                o[j] = submod_d(a[e], reduce_bnd<0>(tsc[j]), Q0);
-            }
+            for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
             continue;
         }
         // ---- digit: X~P = NTT_P(x), staged next to c1
@@ -737,10 +746,11 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
             }
 #pragma unroll
             for (int v = 0; v < 4; v++) {
-                if (v & 1) st2(Ab + (size_t)v * N + pos, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
-                else st2(Ab + (size_t)v * N + pos, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
+                if (v & 1) tmem_st2(tA + 32 * v + 4 * g2, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
+                else tmem_st2(tA + 32 * v + 4 * g2, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
             }
         }
+        tmem_wait_st(); // the A stores above complete before phases 1, 2 read them back
         // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
         //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
         __syncthreads();
@@ -760,6 +770,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
+    tmem_free<512>(s_tmem);
 }
 }
 
