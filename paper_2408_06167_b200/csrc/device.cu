@@ -103,7 +103,11 @@ constexpr int TT = 256;                 // threads per tensor CTA
 constexpr int TQB = 8, TSB = 4;         // queries x sets per CTA
 constexpr int CS = 32;                  // coefficients per CTA
 constexpr int PCH = 8;                  // parts staged per round
-constexpr size_t TENSOR_SMEM_BYTES = (size_t)(TQB + TSB) * PCH * 2 * CS * sizeof(uint64_t); // 48 KiB
+#ifndef BM_TSL
+#define BM_TSL 8
+#endif
+constexpr int TSL = BM_TSL;             // coefficient slices per CTA (rounds double-buffered)
+constexpr size_t TENSOR_SMEM_BYTES = 2 * (size_t)(TQB + TSB) * PCH * 2 * CS * sizeof(uint64_t); // 2 x 48 KiB
 
 BM_D void cp_async16(void *smem, const void *gmem)
 {
@@ -157,67 +161,95 @@ BM_D uint64_t f64_mod_q1(double x)
 // that share a query slice run together and the query data streams from HBM once)
 // NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
 // pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe
-template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st, int part_lo,
-                                       int part_hi)
+// stage the operands of one round (coefficient slice sl, parts i0 .. i0 + pc - 1) with cp.async
+template <int L, int NL> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st,
+                                                int i0, int pc)
 {
     const int tid = threadIdx.x;
     const int c0 = sl * CS;
+    const int lpc = __ffs(pc) - 1;
+    // rows (tile row, part, comp) of CS u64 = 16 chunks of 16 B
+    const int rows = (TQB + TSB) * pc * 2;
+#pragma unroll 4
+    for (int k = tid; k < rows * (CS / 2); k += TT) {
+        const int row = k >> 4, ch = k & 15;
+        const int comp = row & 1, part = (row >> 1) & (pc - 1), tr = (row >> 1) >> lpc;
+        const uint64_t *src;
+        uint64_t *dst;
+        if (tr < TQB) {
+            int64_t a = (int64_t)qt * TQB + tr;
+            a = a < K.cq ? a : K.cq - 1;
+            src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 2 * NL * N;
+            dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
+        } else {
+            int64_t bb = (int64_t)st * TSB + (tr - TQB);
+            bb = bb < K.ct ? bb : K.ct - 1;
+            src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 2 * NL * N;
+            dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
+        }
+        cp_async16(dst + 2 * ch, src + (size_t)(NL * comp + L) * N + c0 + 2 * ch);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
+// pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe.  The CTA walks TSL consecutive
+// coefficient slices; the rounds (slice, chunk of PCH parts) are double-buffered: round r + 1's
+// operands are copied by cp.async while round r is computed.
+template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage, int qt, int sl0, int st, int part_lo,
+                                               int part_hi)
+{
+    const int tid = threadIdx.x;
     constexpr int PI = L == 2 ? 3 : L;
     constexpr bool INTL = L != 1;
     const PrimeK &P = K.pr[PI];
+    constexpr int BUF = (TQB + TSB) * PCH * 2 * CS; // u64 per buffer: Qs [TQB] then Ss [TSB]
     // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
     const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
-    u128 a0[2][2], a1[2][2], a2[2][2];     // q0: 128-bit integer sums
+    const int n_chunks = (part_hi - part_lo + PCH - 1) / PCH;
+    const int R = TSL * n_chunks;
+    auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
+    tensor_stage<L, NL>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
+    u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
     double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
-#pragma unroll
-    for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) {
-            if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
-            else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
-        }
 #pragma unroll 1
-    for (int i0 = part_lo; i0 < part_hi; i0 += PCH) {
-        const int pc = part_hi - i0 < PCH ? part_hi - i0 : PCH; // a power of two (p is)
-        const int lpc = __ffs(pc) - 1;
-        // stage: rows (tile row, part, comp) of CS u64 = 16 chunks of 16 B
-        const int rows = (TQB + TSB) * pc * 2;
-#pragma unroll 4
-        for (int k = tid; k < rows * (CS / 2); k += TT) {
-            const int row = k >> 4, ch = k & 15;
-            const int comp = row & 1, part = (row >> 1) & (pc - 1), tr = (row >> 1) >> lpc;
-            const uint64_t *src;
-            uint64_t *dst;
-            if (tr < TQB) {
-                int64_t a = (int64_t)qt * TQB + tr;
-                a = a < K.cq ? a : K.cq - 1;
-                src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 2 * NL * N;
-                dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
-            } else {
-                int64_t bb = (int64_t)st * TSB + (tr - TQB);
-                bb = bb < K.ct ? bb : K.ct - 1;
-                src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 2 * NL * N;
-                dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
-            }
-            cp_async16(dst + 2 * ch, src + (size_t)(NL * comp + L) * N + c0 + 2 * ch);
+    for (int r = 0; r < R; r++) {
+        const int sl = sl0 + r / n_chunks, j = r % n_chunks, i0 = part_lo + j * PCH, pc = chunk_pc(j);
+        if (r + 1 < R) {
+            const int r1 = r + 1, j1 = r1 % n_chunks;
+            uint64_t *b1 = stage + (size_t)(r1 & 1) * BUF;
+            tensor_stage<L, NL>(K, b1, b1 + TQB * PCH * 2 * CS, qt, sl0 + r1 / n_chunks, st, part_lo + j1 * PCH,
+                                chunk_pc(j1));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        const uint64_t *Qs = stage + (size_t)(r & 1) * BUF, *Ss = Qs + TQB * PCH * 2 * CS;
+        if (j == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+                    else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
+                }
+        }
 #pragma unroll
         for (int i = 0; i < PCH; i++) {
             if (i >= pc) break;
             uint64_t x0[2], x1[2], y0[2], y1[2];
 #pragma unroll
             for (int u = 0; u < 2; u++) {
-                const uint64_t *r = Qs + (((2 * su + u) * PCH + i) * 2) * CS + c;
-                x0[u] = r[0];
-                x1[u] = r[CS];
+                const uint64_t *rr = Qs + (((2 * su + u) * PCH + i) * 2) * CS + c;
+                x0[u] = rr[0];
+                x1[u] = rr[CS];
             }
 #pragma unroll
             for (int v = 0; v < 2; v++) {
-                const uint64_t *r = Ss + (((2 * sv + v) * PCH + i) * 2) * CS + c;
-                y0[v] = r[0];
-                y1[v] = r[CS];
+                const uint64_t *rr = Ss + (((2 * sv + v) * PCH + i) * 2) * CS + c;
+                y0[v] = rr[0];
+                y1[v] = rr[CS];
             }
             if (INTL) {
 #pragma unroll
@@ -261,48 +293,49 @@ template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *Qs, ui
                     }
                 }
         }
-        __syncthreads(); // before the next round overwrites the stage
-    }
-    const uint64_t q = P.q;
+        if (j == n_chunks - 1) { // the slice is complete: write its d0, d1, d2
+            const uint64_t q = P.q;
 #pragma unroll
-    for (int u = 0; u < 2; u++)
+            for (int u = 0; u < 2; u++)
 #pragma unroll
-        for (int v = 0; v < 2; v++) {
-            const int64_t a = (int64_t)qt * TQB + 2 * su + u, bb = (int64_t)st * TSB + 2 * sv + v;
-            if (a >= K.cq || bb >= K.ct) continue;
-            const int64_t pi = a * K.ct + bb;
-            const int j = c0 + c;
-            uint64_t d0, d2, kk;
-            if (INTL) {
-                d0 = red128s<PI>(a0[u][v], P.r64);
-                d2 = red128s<PI>(a2[u][v], P.r64);
-                kk = red128s<PI>(a1[u][v], P.r64);
-            } else {
-                d0 = f64_mod_q1(f0[u][v]);
-                d2 = f64_mod_q1(f2[u][v]);
-                kk = f64_mod_q1(f1[u][v]);
-            }
-            K.D01[((size_t)pi * 2 * NL + 0 + L) * N + j] = d0;
-            K.D01[((size_t)pi * 2 * NL + NL + L) * N + j] = submod_d(submod_d(kk, d0, q), d2, q);
-            K.D2[((size_t)pi * NL + L) * N + j] = d2;
+                for (int v = 0; v < 2; v++) {
+                    const int64_t a = (int64_t)qt * TQB + 2 * su + u, bb = (int64_t)st * TSB + 2 * sv + v;
+                    if (a >= K.cq || bb >= K.ct) continue;
+                    const int64_t pi = a * K.ct + bb;
+                    const int jj = sl * CS + c;
+                    uint64_t d0, d2, kk;
+                    if (INTL) {
+                        d0 = red128s<PI>(a0[u][v], P.r64);
+                        d2 = red128s<PI>(a2[u][v], P.r64);
+                        kk = red128s<PI>(a1[u][v], P.r64);
+                    } else {
+                        d0 = f64_mod_q1(f0[u][v]);
+                        d2 = f64_mod_q1(f2[u][v]);
+                        kk = f64_mod_q1(f1[u][v]);
+                    }
+                    K.D01[((size_t)pi * 2 * NL + 0 + L) * N + jj] = d0;
+                    K.D01[((size_t)pi * 2 * NL + NL + L) * N + jj] = submod_d(submod_d(kk, d0, q), d2, q);
+                    K.D2[((size_t)pi * NL + L) * N + jj] = d2;
+                }
         }
+        __syncthreads(); // every read of buffer r & 1 is done before round r + 2 overwrites it
+    }
 }
 
 template <int NL> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
-    uint64_t *Qs = sm, *Ss = sm + TQB * PCH * 2 * CS; // [tile row][part][comp][CS]
     const int nst = (int)((K.ct + TSB - 1) / TSB);
     int64_t b = blockIdx.x;
     const int l = (int)(b % NL);
     b /= NL;
     const int st = (int)(b % nst);
     b /= nst;
-    const int sl = (int)(b % (N / CS));
-    const int qt = (int)(b / (N / CS));
-    if (l == 0) tensor_tile<0, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
-    else if (l == 1) tensor_tile<1, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
-    else if (NL == 3) tensor_tile<2, NL>(K, Qs, Ss, qt, sl, st, part_lo, part_hi);
+    const int sg = (int)(b % (N / CS / TSL));
+    const int qt = (int)(b / (N / CS / TSL));
+    if (l == 0) tensor_tile<0, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (l == 1) tensor_tile<1, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (NL == 3) tensor_tile<2, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
 }
 
 // ================================================================== prime-specialised pointwise helpers
@@ -2251,7 +2284,7 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
             K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
             const int64_t np = K.cq * K.ct;
             const unsigned npu = (unsigned)np;
-            const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS));
+            const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
             k_tensor<3><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
             k_digits3<<<3 * npu, T, C1_SMEM_BYTES, s>>>(C);
             k_relin3<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
@@ -2388,7 +2421,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
         const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
-        const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS));
+        const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
         const bool per_part = order == BM_ORDER_PAPER;
         const int n_rounds = per_part ? prm->p : 1;
         for (int r = 0; r < n_rounds && !rc; r++) {
