@@ -10,8 +10,15 @@
 //                                        with the rescale by q1 (exact, R22):
 //                                        INTT_P, INTT_q1, NTT_q0 (3 transforms) -> C_c (level 0)
 //   K4 k_ladder  (pair)                  a7+a8: the log2(s) rotate-and-add steps with C resident in
-//                                        shared memory, 6 transforms per step, coefficient-domain output
+//                                        shared memory and per-thread scratch in TMEM, 6 transforms
+//                                        per step, coefficient-domain output
 //   K5 k_out_intt (pair, c)              a8 when s = 1 (no ladder): INTT_q0 of C
+// Also here: K6 k_hrot (f2, the hoisted rotation sum), the f3/f4 kernels (query expansion and
+// server-side enrollment: k_exp_mask, k_rot1_digits, k_rot1_ks, k_enroll_add) and the f1 kernels
+// (compressed scan one level up: k_tensor<3>, k_digits3, k_relin3, k_cmp_mask, k_cmp_rot,
+// k_cmp_add), encryption / conversion / key upload, and the host side of the device C ABI.
+// Memory-access conventions: NTT-domain data in the pair-coalesced M4 order,
+// twiddles in load order (tw_pos), Shoup keys planar (ldkey2).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
