@@ -377,9 +377,9 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
             xs[tid + T * e] = a[e];
             a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
         }
-        fwd_q1f(a, sm, K.pr[1].fwdf); // the FP64 pipe (ntt3f.cuh)
+        fwd_f<1>(a, sm, K.pr[1].fwdf); // the FP64 pipe (ntt3f.cuh)
     } else {
-        inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // the FP64 pipe
+        inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // the FP64 pipe
 #pragma unroll
         for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
         fwd<0, false>(a, sm, K.pr[0]); // lazy [0, 2 q0): only ever a Shoup-product operand
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         a[e] = reduce_bnd<1>(dd.x + ka);
         a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
-    inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
+    inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
     // ---- rescale in coefficient form
     const ulonglong2 pinv0 = K.pinv[0];
     // y^ = y - [y > P/2] P, so P^-1 y^ = P^-1 y - [y > P/2] in every q limb (no centring reduction)
@@ -890,10 +890,10 @@ __global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
         const ulonglong2 v = ld2(cin + 2 * N + pos);
         ulonglong2 ma, mb;
         ldkey2(mk + 2 * N, pos, ma, mb);
-        a[e] = shoup4<3>(v.x, ma);
-        a[e + 1] = shoup4<3>(v.y, mb);
+        a[e] = reduce_bnd<3>(shoup4<3>(v.x, ma));
+        a[e + 1] = reduce_bnd<3>(shoup4<3>(v.y, mb));
     }
-    inv<3>(a, sm, K.pr[3]);
+    inv_f<3>(a, sm, K.pr[3].invf, K.pr[3].ninvf, K.pr[3].ninv_w1f); // canonical (FP64 pipe)
 #pragma unroll
     for (int e = 0; e < E; e++) ys[tid + T * e] = a[e];
     // q1 limb (FP64-pipe transform): q2^-1 y^ mod q1 = q2^-1 y - [y > q2/2]
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(T, 1) k_exp_mask(ExpK K)
         const uint64_t y = a[e];
         a[e] = reduce_bnd<1>(shoup4<1>(y, K.q2inv[1]) + (y > (Q2 >> 1) ? Q1 - 1 : 0));
     }
-    fwd_q1f(a, sm, K.pr[1].fwdf);
+    fwd_f<1>(a, sm, K.pr[1].fwdf);
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int pos = pos_M4(tid, e);
@@ -954,10 +954,10 @@ __global__ void __launch_bounds__(T, 1) k_rot1_digits(ExpK K)
             xs[tid + T * e] = a[e];
             a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
         }
-        fwd_q1f(a, sm, K.pr[1].fwdf);
+        fwd_f<1>(a, sm, K.pr[1].fwdf);
         store_eval(xu + 1 * N, a);
     } else {
-        inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
+        inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
 #pragma unroll
         for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
         fwd<0, false>(a, sm, K.pr[0]); // x1 < q1 < q0; lazy [0, 2 q0): a Shoup operand only
@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
                 const uint64_t y = ys[tid + T * e];
                 a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (y > (QP >> 1) ? Q1 - 1 : 0));
             }
-            fwd_q1f(a, sm, K.pr[1].fwdf);
+            fwd_f<1>(a, sm, K.pr[1].fwdf);
         } else {
 #pragma unroll
             for (int e = 0; e < E; e++) {
@@ -1123,8 +1123,8 @@ __global__ void __launch_bounds__(T, 1) k_digits3(CmpK C)
     load_eval(a, K.D2 + ((size_t)pi * 3 + j) * N);
     uint64_t *xu = K.XU + ((size_t)pi * D2X_POLYS + 3 * j) * N; // targets: other Q limbs ascending, then P
     if (j == 0) inv<0>(a, sm, K.pr[0]);
-    else if (j == 1) inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
-    else inv<3>(a, sm, K.pr[3]);
+    else if (j == 1) inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f);
+    else inv_f<3>(a, sm, K.pr[3].invf, K.pr[3].ninvf, K.pr[3].ninv_w1f);
 #pragma unroll
     for (int e = 0; e < E; e++) xs[tid + T * e] = a[e]; // x_j in [0, q_j), non-centred (reading R4)
 #pragma unroll 1
@@ -1139,8 +1139,8 @@ __global__ void __launch_bounds__(T, 1) k_digits3(CmpK C)
             else a[e] = x;                                                     // q0 (x1, x2 < q0), P (x < P)
         }
         if (tp == 2) fwd<2, false>(a, sm, K.pr[2]);       // lazy [0, 2P): a Shoup operand only
-        else if (tp == 1) fwd_q1f(a, sm, K.pr[1].fwdf);   // canonical (FP64 pipe)
-        else if (tp == 3) fwd<3>(a, sm, K.pr[3]);         // canonical
+        else if (tp == 1) fwd_f<1>(a, sm, K.pr[1].fwdf);   // canonical (FP64 pipe)
+        else if (tp == 3) fwd_f<3>(a, sm, K.pr[3].fwdf);  // canonical (FP64 pipe)
         else fwd<0, false>(a, sm, K.pr[0]);               // lazy [0, 2 q0)
         store_eval(xu + (size_t)k * N, a);
     }
@@ -1200,7 +1200,7 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
                 reduce_bnd<3>(dd.y + red128s<3>((u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y, K.pr[3].r64));
         }
     }
-    inv<3>(a, sm, K.pr[3]); // U, canonical
+    inv_f<3>(a, sm, K.pr[3].invf, K.pr[3].ninvf, K.pr[3].ninv_w1f); // U, canonical (FP64 pipe)
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const uint64_t y = ys[tid + T * e];
@@ -1219,7 +1219,7 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
             if (l) a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (f ? Q1 - 1 : 0) + z);
             else a[e] = shoup4<0>(y, K.pinv[0]) + (f ? Q0 - 1 : 0) + z; // < 6 q0
         }
-        if (l) fwd_q1f(a, sm, K.pr[1].fwdf); // canonical
+        if (l) fwd_f<1>(a, sm, K.pr[1].fwdf); // canonical
         else fwd<0, false>(a, sm, K.pr[0]);  // [0, 2 q0)
         const uint64_t *x0 = digit_poly(K, pi, 0, l), *x1 = digit_poly(K, pi, 1, l), *x2 = digit_poly(K, pi, 2, l);
         uint64_t *co = K.XC + ((size_t)pi * 2 + c) * 2 * N + (size_t)l * N;
@@ -1263,7 +1263,7 @@ __global__ void __launch_bounds__(T, 1) k_cmp_mask(CmpK C)
         a[e] = reduce_bnd<1>(shoup4<1>(v.x, ma));
         a[e + 1] = reduce_bnd<1>(shoup4<1>(v.y, mb));
     }
-    inv_q1f(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // y, canonical
+    inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // y, canonical
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], K.q1inv) + (a[e] > (Q1 >> 1) ? Q0 - 1 : 0); // < 5 q0
     fwd<0>(a, sm, K.pr[0]); // canonical
@@ -1508,7 +1508,7 @@ namespace {
 struct DevCtx {
     int dev = -1;
     ulonglong2 *tw = nullptr;  // [4][2][N]: q0, q1, P, q2 (f3)
-    ulonglong2 *twf = nullptr; // q1 [2][N], FP64 form
+    ulonglong2 *twf = nullptr; // [q1, q2][fwd, inv][N], FP64 form
     PrimeK pr[4] = {};
     ulonglong2 pinv[2], q1inv;
     ulonglong2 q2inv[2];       // f3: q2^-1 mod q0, q1
@@ -1562,18 +1562,23 @@ int ctx_get(DevCtx **out)
         return BM_ERR_OOM;
     }
     cudaMemcpy(C->tw, h.data(), h.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
-    // q1 twiddles for the FP64-pipe transforms (ntt3f.cuh): (w, fl(w / q1)) as double bit patterns
-    auto fpair = [](uint64_t w) {
-        const double dw = (double)w, dq = dw / (double)Q1;
+    // q1 and q2 twiddles for the FP64-pipe transforms (ntt3f.cuh): (w, fl(w / q)) as double bit patterns
+    auto fpair = [](uint64_t w, uint64_t q) {
+        const double dw = (double)w, dq = dw / (double)q;
         uint64_t a, b;
         memcpy(&a, &dw, 8);
         memcpy(&b, &dq, 8);
         return make_ulonglong2(a, b);
     };
     {
-        const HostPrime &H = host_prime(1);
-        std::vector<ulonglong2> hf(2 * (size_t)N);
-        for (int k = 0; k < N; k++) hf[tw_pos(k)] = fpair(H.fwd[k]), hf[(size_t)N + tw_pos(k)] = fpair(H.inv[k]);
+        const int fp[2] = {1, 3};
+        std::vector<ulonglong2> hf(4 * (size_t)N);
+        for (int f = 0; f < 2; f++) {
+            const HostPrime &H = host_prime(fp[f]);
+            for (int k = 0; k < N; k++)
+                hf[(size_t)(2 * f) * N + tw_pos(k)] = fpair(H.fwd[k], H.q),
+                                       hf[(size_t)(2 * f + 1) * N + tw_pos(k)] = fpair(H.inv[k], H.q);
+        }
         if (cudaMalloc(&C->twf, hf.size() * sizeof(ulonglong2)) != cudaSuccess) {
             cudaFree(C->tw);
             delete C;
@@ -1581,11 +1586,14 @@ int ctx_get(DevCtx **out)
             return BM_ERR_OOM;
         }
         cudaMemcpy(C->twf, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
-        PrimeK &P = C->pr[1];
-        P.fwdf = C->twf;
-        P.invf = C->twf + N;
-        P.ninvf = fpair(H.ninv);
-        P.ninv_w1f = fpair(mulmod_h(H.ninv, H.inv[1], H.q));
+        for (int f = 0; f < 2; f++) {
+            const HostPrime &H = host_prime(fp[f]);
+            PrimeK &P = C->pr[fp[f]];
+            P.fwdf = C->twf + (size_t)(2 * f) * N;
+            P.invf = C->twf + (size_t)(2 * f + 1) * N;
+            P.ninvf = fpair(H.ninv, H.q);
+            P.ninv_w1f = fpair(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
+        }
     }
     for (int i = 0; i < 4; i++) {
         const HostPrime &H = host_prime(i);

@@ -1,4 +1,5 @@
-// ntt3f.cuh -- the q1 transforms on the FP64 pipe (exact).  q1 < 2^40, so every residue, lazy
+// ntt3f.cuh -- the q1 and q2 transforms on the FP64 pipe (exact), templated on the prime index
+// (PI = 1: q1, PI = 3: q2; the comments write q1 for either).  q1 < 2^40, so every residue, lazy
 // value and product piece fits a double exactly; the data stay in the registers and the shared-
 // memory exchanges of ntt3.cuh (same layouts M1..M4, same 512-thread CTA) as double bit patterns.
 // The Shoup product becomes (tools/pipe_bench.cu: DFMA issues at the IMAD rate on its own pipe):
@@ -16,8 +17,8 @@
 namespace bm {
 namespace v3 {
 
-constexpr double F_Q1 = (double)Q1;
-constexpr double F_Q1INV = 1.0 / (double)Q1;
+template <int PI> BM_HD constexpr double f_q() { return PI == 1 ? (double)Q1 : (double)Q2; }
+template <int PI> BM_HD constexpr double f_qinv() { return PI == 1 ? 1.0 / (double)Q1 : 1.0 / (double)Q2; }
 constexpr double F_MAGIC = 6755399441055744.0; // 1.5 2^52: x + M has ulp 1 for |x| < 2^51
 constexpr double F_2P52 = 4503599627370496.0;
 
@@ -25,43 +26,43 @@ BM_D double fl_floor(double x) { return __dadd_rd(x, F_MAGIC) - F_MAGIC; }
 BM_D double as_d(uint64_t x) { return __longlong_as_double((long long)x); }
 BM_D uint64_t as_u(double x) { return (uint64_t)__double_as_longlong(x); }
 // twiddle entry: (w, wq) as double bit patterns
-BM_D double mulw(double a, ulonglong2 t)
+template <int PI> BM_D double mulw(double a, ulonglong2 t)
 {
     const double w = as_d(t.x), wq = as_d(t.y);
     const double hi = a * w;
     const double lo = __fma_rn(a, w, -hi);
     const double qt = fl_floor(a * wq);
-    return __fma_rn(-qt, F_Q1, hi) + lo;
+    return __fma_rn(-qt, f_q<PI>(), hi) + lo;
 }
 // (-q1, 2 q1) for |x| < 2^51
-BM_D double red_f(double x) { return __fma_rn(-fl_floor(x * F_Q1INV), F_Q1, x); }
+template <int PI> BM_D double red_f(double x) { return __fma_rn(-fl_floor(x * f_qinv<PI>()), f_q<PI>(), x); }
 // canonical u64 residue of an integer-valued double |x| < 2^51
-BM_D uint64_t canon_f(double x)
+template <int PI> BM_D uint64_t canon_f(double x)
 {
-    double r = red_f(x);
-    r = r < 0 ? r + F_Q1 : r;
-    r = r >= F_Q1 ? r - F_Q1 : r;
+    double r = red_f<PI>(x);
+    r = r < 0 ? r + f_q<PI>() : r;
+    r = r >= f_q<PI>() ? r - f_q<PI>() : r;
     return as_u(r + F_2P52) & ((1ull << 52) - 1);
 }
 BM_D double from_u(uint64_t x) { return as_d(x | 0x4330000000000000ull) - F_2P52; } // x < 2^52
 
-BM_D void ct_f(uint64_t &x, uint64_t &y, ulonglong2 w)
+template <int PI> BM_D void ct_f(uint64_t &x, uint64_t &y, ulonglong2 w)
 {
-    const double X = as_d(x), T = mulw(as_d(y), w);
+    const double X = as_d(x), T = mulw<PI>(as_d(y), w);
     x = as_u(X + T);
     y = as_u(X - T);
 }
-template <int ST> BM_D void gs_f(uint64_t &x, uint64_t &y, ulonglong2 w)
+template <int PI, int ST> BM_D void gs_f(uint64_t &x, uint64_t &y, ulonglong2 w)
 {
     const double a = as_d(x), b = as_d(y);
     double X = a + b;
-    if (ST % 5 == 4) X = red_f(X);
+    if (ST % 5 == 4) X = red_f<PI>(X);
     x = as_u(X);
-    y = as_u(mulw(a - b, w));
+    y = as_u(mulw<PI>(a - b, w));
 }
 
 // forward, M1 -> M4 (twiddles fwdf), canonical u64 in and out
-BM_D void fwd_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
+template <int PI> BM_D void fwd_f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
 {
     const int tid = threadIdx.x;
 #pragma unroll
@@ -72,7 +73,7 @@ BM_D void fwd_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct_f(a[k], a[k + half], ldtw(tw + (1 << s) + (k >> (4 - s))));
+            ct_f<PI>(a[k], a[k + half], ldtw(tw + (1 << s) + (k >> (4 - s))));
         }
     }
     xchg<1, 2>(a, sm);
@@ -84,7 +85,7 @@ BM_D void fwd_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
 #pragma unroll
             for (int k = 0; k < E; k++) {
                 if (k & half) continue;
-                ct_f(a[k], a[k + half], ldtw(tw + (1 << s) + (B << (s - 4)) + (k >> (8 - s))));
+                ct_f<PI>(a[k], a[k + half], ldtw(tw + (1 << s) + (B << (s - 4)) + (k >> (8 - s))));
             }
         }
     }
@@ -96,28 +97,28 @@ BM_D void fwd_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw)
 #pragma unroll
         for (int k = 0; k < E; k++) {
             if (k & half) continue;
-            ct_f(a[k], a[k + half], ldtw(tw + (1 << s) + ((k >> (12 - s)) << 8) + G));
+            ct_f<PI>(a[k], a[k + half], ldtw(tw + (1 << s) + ((k >> (12 - s)) << 8) + G));
         }
     }
 #pragma unroll
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
         uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
-        ct_f(x, y, ldtw(tw + 4096 + 512 * m + tid));
-        a[2 * m] = canon_f(as_d(x));
-        a[2 * m + 1] = canon_f(as_d(y));
+        ct_f<PI>(x, y, ldtw(tw + 4096 + 512 * m + tid));
+        a[2 * m] = canon_f<PI>(as_d(x));
+        a[2 * m + 1] = canon_f<PI>(as_d(y));
     }
 }
 
 // inverse, M4 -> M1 (twiddles invf; N^-1 and N^-1 inv[1] as (w, wq) doubles), canonical in and out
-BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 ninv, ulonglong2 ninv_w1)
+template <int PI> BM_D void inv_f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 ninv, ulonglong2 ninv_w1)
 {
     const int tid = threadIdx.x;
     const int G = tid >> 1, odd = tid & 1;
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = as_u(from_u(a[e]));
 #pragma unroll
-    for (int m = 0; m < 8; m++) gs_f<0>(a[2 * m], a[2 * m + 1], ldtw(tw + 4096 + 512 * m + tid));
+    for (int m = 0; m < 8; m++) gs_f<PI, 0>(a[2 * m], a[2 * m + 1], ldtw(tw + 4096 + 512 * m + tid));
 #pragma unroll
     for (int m = 0; m < 8; m++) {
         const uint64_t r = shfl1(odd ? a[2 * m] : a[2 * m + 1]);
@@ -132,10 +133,10 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
             if (k & half) continue;
             const ulonglong2 w = ldtw(tw + (1 << s) + ((k >> (12 - s)) << 8) + G);
             switch (12 - s) {
-            case 1: gs_f<1>(a[k], a[k + half], w); break;
-            case 2: gs_f<2>(a[k], a[k + half], w); break;
-            case 3: gs_f<3>(a[k], a[k + half], w); break;
-            default: gs_f<4>(a[k], a[k + half], w); break;
+            case 1: gs_f<PI, 1>(a[k], a[k + half], w); break;
+            case 2: gs_f<PI, 2>(a[k], a[k + half], w); break;
+            case 3: gs_f<PI, 3>(a[k], a[k + half], w); break;
+            default: gs_f<PI, 4>(a[k], a[k + half], w); break;
             }
         }
     }
@@ -150,10 +151,10 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
                 if (k & half) continue;
                 const ulonglong2 w = ldtw(tw + (1 << s) + (B << (s - 4)) + (k >> (8 - s)));
                 switch (12 - s) {
-                case 5: gs_f<5>(a[k], a[k + half], w); break;
-                case 6: gs_f<6>(a[k], a[k + half], w); break;
-                case 7: gs_f<7>(a[k], a[k + half], w); break;
-                default: gs_f<8>(a[k], a[k + half], w); break;
+                case 5: gs_f<PI, 5>(a[k], a[k + half], w); break;
+                case 6: gs_f<PI, 6>(a[k], a[k + half], w); break;
+                case 7: gs_f<PI, 7>(a[k], a[k + half], w); break;
+                default: gs_f<PI, 8>(a[k], a[k + half], w); break;
                 }
             }
         }
@@ -167,9 +168,9 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
             if (k & half) continue;
             const ulonglong2 w = ldtw(tw + (1 << s) + (k >> (4 - s)));
             switch (12 - s) {
-            case 9: gs_f<9>(a[k], a[k + half], w); break;
-            case 10: gs_f<10>(a[k], a[k + half], w); break;
-            default: gs_f<11>(a[k], a[k + half], w); break;
+            case 9: gs_f<PI, 9>(a[k], a[k + half], w); break;
+            case 10: gs_f<PI, 10>(a[k], a[k + half], w); break;
+            default: gs_f<PI, 11>(a[k], a[k + half], w); break;
             }
         }
     }
@@ -177,8 +178,8 @@ BM_D void inv_q1f(uint64_t a[E], uint64_t *sm, const ulonglong2 *tw, ulonglong2 
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const double x = as_d(a[k]), y = as_d(a[k + 8]);
-        a[k] = canon_f(mulw(x + y, ninv));
-        a[k + 8] = canon_f(mulw(x - y, ninv_w1));
+        a[k] = canon_f<PI>(mulw<PI>(x + y, ninv));
+        a[k + 8] = canon_f<PI>(mulw<PI>(x - y, ninv_w1));
     }
 }
 

@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(512, MINB3) k_bench3(PrimeK P, uint64_t *data,
     v3::load_coef(a, d);
     for (int it = 0; it < iters; it++) {
         if constexpr (PI == 3) { // q1 on the FP64 pipe (ntt3f.cuh)
-            v3::fwd_q1f(a, sm, P.fwdf);
-            v3::inv_q1f(a, sm, P.invf, P.ninvf, P.ninv_w1f);
+            v3::fwd_f<1>(a, sm, P.fwdf);
+            v3::inv_f<1>(a, sm, P.invf, P.ninvf, P.ninv_w1f);
         } else {
             v3::fwd<PI>(a, sm, P);
             v3::inv<PI>(a, sm, P);
