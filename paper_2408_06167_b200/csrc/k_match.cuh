@@ -1,0 +1,796 @@
+// k_match.cuh -- the bm_match kernels: K1 k_tensor, K2 k_digits, K3 k_relin, K4 k_ladder (with the
+// TMEM scratch helpers), K5 k_out_intt, and f2's K6 k_hrot; the workspace layout MatchK / CtBuf.
+// Included once, by device.cu (one translation unit: the kernels are launched from its host side).
+#pragma once
+
+// ================================================================== device constants
+__constant__ uint64_t c_cdt[19];
+
+// Workspace per (query, set) pair, 12 N u64:
+//   D01 [c][l][N]  d_c[q_l] (NTT)                       K1 -> K3
+//   D2  [l][N]     d2[q_l] (NTT)                        K1 -> K2, K3; then the ladder's scratch
+//   XC  [2][N]     C = (c0, c1), level 0 (NTT)          K3 -> ladder
+//   XU  [4][N]     ModUp'd digits x0~[q1], x0~[P], x1~[q0], x1~[P] (NTT)   K2 -> K3
+// The paper order adds a level-0 accumulator ACC [2][N] (K3 sums into it across parts).
+struct MatchK {
+    PrimeK pr[4];       // q0, q1, P, q2 (f1)
+    ulonglong2 pinv[2]; // P^-1 mod q0, q1
+    ulonglong2 q1inv;   // q1^-1 mod q0
+    uint64_t pmod[2];   // P mod q0, q1
+    const uint64_t *rlk, *gk; // PLANAR Shoup keys: poly k at [2k N, 2k N + N) = w, [2k N + N, 2k N + 2N) = w'
+    const uint64_t *db, *qry;
+    uint64_t *out;
+    int64_t n_sets;       // sets in the DB (output row length)
+    int64_t jq0, t0, ct;  // chunk = queries [jq0, jq0+cq) x sets [t0, t0+ct); pair pi = a*ct + b
+    int32_t cq;
+    int32_t p;
+    BM_D int64_t out_row(int64_t pi) const { return (jq0 + pi / ct) * n_sets + t0 + pi % ct; }
+    uint64_t *D01, *D2, *XC, *XU, *ACC;
+    uint64_t *XR, *XO;  // f1: level-0 masked results (NTT), rotated results (coefficients)
+};
+
+// a level-0 ciphertext buffer inside the workspace: pair pi, component c at base + pi*stride + c*N
+struct CtBuf {
+    uint64_t *base;
+    int64_t stride;
+    BM_D uint64_t *at(int64_t pi, int c) const { return base + pi * stride + (int64_t)c * N; }
+};
+
+constexpr int WS_POLYS = 12;      // u64 polynomials of workspace per pair (hoisted order)
+constexpr int WS_POLYS_PAPER = 14;
+
+BM_D ulonglong2 ld2(const uint64_t *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
+BM_D void st2(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
+
+BM_D uint64_t submod_d(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// Planar Shoup keys (rlk, ladder gk): plane w at kp[0, N), plane w' at kp[N, 2N).  One 16-byte load per
+// plane gives positions pos, pos + 1 (pos even, lane-contiguous across a warp, like the twiddles' tw_pos):
+// ka = (w, w') of pos, kb = (w, w') of pos + 1.
+BM_D void ldkey2(const uint64_t *kp, int pos, ulonglong2 &ka, ulonglong2 &kb)
+{
+    const ulonglong2 w = ld2(kp + pos), wp = ld2(kp + N + pos);
+    ka = make_ulonglong2(w.x, wp.x);
+    kb = make_ulonglong2(w.y, wp.y);
+}
+// the same for a poly addressed as ulonglong2 * (a planar poly occupies the bytes of N pairs)
+BM_D void ldkey2(const ulonglong2 *kp, int pos, ulonglong2 &ka, ulonglong2 &kb)
+{
+    ldkey2(reinterpret_cast<const uint64_t *>(kp), pos, ka, kb);
+}
+// one position of a planar key (pos of any parity: two 8-byte loads)
+BM_D ulonglong2 ldkey1(const ulonglong2 *kp, int pos)
+{
+    const uint64_t *p = reinterpret_cast<const uint64_t *>(kp);
+    return make_ulonglong2(__ldg(p + pos), __ldg(p + N + pos));
+}
+
+// ================================================================== K1: tensor (a4)
+// d0 = sum_i x0_i y0_i, d2 = sum_i x1_i y1_i, d1 = sum_i (x0_i + x1_i)(y0_i + y1_i) - d0 - d2 per
+// (query x, set y) pair, limb and NTT-domain coefficient (Karatsuba over the ciphertext
+// components, exact mod q) -- for each coefficient a small "query tile x set tile" contraction
+// over the parts, tiled like one: a CTA owns TQB queries x TSB sets x CS coefficients of one limb
+// and stages the operands of up to PCH parts in shared memory with cp.async (each query / set
+// value is fetched from L2 once per CTA and reused TSB / TQB times); every thread then
+// accumulates a 2 x 2 block of pairs for one coefficient in 128-bit sums.  A product is
+// < (2q)^2 < 2^118, so the sums are folded mod q every 512 parts.
+constexpr int TT = 256;                 // threads per tensor CTA
+constexpr int TQB = 8, TSB = 4;         // queries x sets per CTA
+constexpr int CS = 32;                  // coefficients per CTA
+constexpr int PCH = 8;                  // parts staged per round
+#ifndef BM_TSL
+#define BM_TSL 8
+#endif
+constexpr int TSL = BM_TSL;             // coefficient slices per CTA (rounds double-buffered)
+constexpr size_t TENSOR_SMEM_BYTES = 2 * (size_t)(TQB + TSB) * PCH * 2 * CS * sizeof(uint64_t); // 2 x 48 KiB
+
+BM_D void cp_async16(void *smem, const void *gmem)
+{
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+BM_D uint64_t red128(u128 v, const PrimeK &P) { return reduce128((uint64_t)(v >> 64), (uint64_t)v, P.q, P.r64, P.one_p); }
+// x mod q for any x < 2^64, canonical (q1: fold 2^40 = c1 once so that reduce_bnd's x < 2^62 holds)
+template <int PI> BM_D uint64_t reduce_any(uint64_t x)
+{
+    if (Q40<PI>) x = (x & ((1ull << 40) - 1)) + (x >> 40) * ((1ull << 40) - PrimeC<PI>::q); // < 2^40 + 2^44
+    return reduce_bnd<PI>(x);
+}
+// v mod q for a 128-bit v with the prime-specialised lazy Shoup product: hi (2^64 mod q) + lo
+template <int PI> BM_D uint64_t red128s(u128 v, ulonglong2 r64)
+{
+    const uint64_t t = shoup4<PI>((uint64_t)(v >> 64), r64) + reduce_any<PI>((uint64_t)v); // < 5 q
+    return reduce_bnd<PI>(t);
+}
+
+// q1 limb on the FP64 pipe, exactly: for 0 <= a, b < 2^42 (integers held in doubles),
+// r = a b - floor(a b / q1) q1 up to +-q1: hi = fl(a b) and lo = a b - hi (one FMA, exact), the
+// quotient from fl(hi / q1) by a round-down add of 1.5 2^52, r = (hi - qt q1) + lo (the FMA's
+// exact result is an integer below 2^43, so nothing rounds).  |r| < 3 q1.  7 FP64 instructions,
+// which run on their own pipe: the q1-limb CTAs of k_tensor share each SM with q0-limb CTAs whose
+// 128-bit integer products load the FMA pipe.
+constexpr double MAGIC52 = 6755399441055744.0; // 1.5 2^52: x + M has ulp 1 for |x| < 2^51
+BM_D double f64_floor(double x) { return __dadd_rd(x, MAGIC52) - MAGIC52; }
+BM_D double mulmod_q1_f64(double a, double b)
+{
+    constexpr double q = (double)Q1, qinv = 1.0 / (double)Q1;
+    const double hi = a * b;
+    const double lo = __fma_rn(a, b, -hi);
+    const double qt = f64_floor(hi * qinv);
+    return __fma_rn(-qt, q, hi) + lo;
+}
+// exact u64 (< 2^52) <-> double through the 2^52 exponent pattern (one LOP3 + one DADD)
+BM_D double u2d(uint64_t x) { return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0; }
+// x mod q1 for an integer-valued double |x| < 2^51, as a canonical u64
+BM_D uint64_t f64_mod_q1(double x)
+{
+    constexpr double q = (double)Q1, qinv = 1.0 / (double)Q1;
+    double r = __fma_rn(-f64_floor(x * qinv), q, x); // in (-q1, 2 q1)
+    r = r < 0 ? r + q : r;
+    r = r >= q ? r - q : r;
+    return (uint64_t)__double_as_longlong(r + 4503599627370496.0) & ((1ull << 52) - 1);
+}
+
+// grid: ((qt * (N / CS) + slice) * nst + st) * 2 + l  (limbs alternate, so each SM holds one
+// q0-limb CTA on the integer pipe and one q1-limb CTA on the FP64 pipe; set tiles next: the CTAs
+// that share a query slice run together and the query data streams from HBM once)
+// NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
+// pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe
+// stage the operands of one round (coefficient slice sl, parts i0 .. i0 + pc - 1) with cp.async
+template <int L, int NL> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st,
+                                                int i0, int pc)
+{
+    const int tid = threadIdx.x;
+    const int c0 = sl * CS;
+    const int lpc = __ffs(pc) - 1;
+    // rows (tile row, part, comp) of CS u64 = 16 chunks of 16 B
+    const int rows = (TQB + TSB) * pc * 2;
+#pragma unroll 4
+    for (int k = tid; k < rows * (CS / 2); k += TT) {
+        const int row = k >> 4, ch = k & 15;
+        const int comp = row & 1, part = (row >> 1) & (pc - 1), tr = (row >> 1) >> lpc;
+        const uint64_t *src;
+        uint64_t *dst;
+        if (tr < TQB) {
+            int64_t a = (int64_t)qt * TQB + tr;
+            a = a < K.cq ? a : K.cq - 1;
+            src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 2 * NL * N;
+            dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
+        } else {
+            int64_t bb = (int64_t)st * TSB + (tr - TQB);
+            bb = bb < K.ct ? bb : K.ct - 1;
+            src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 2 * NL * N;
+            dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
+        }
+        cp_async16(dst + 2 * ch, src + (size_t)(NL * comp + L) * N + c0 + 2 * ch);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
+// pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe.  The CTA walks TSL consecutive
+// coefficient slices; the rounds (slice, chunk of PCH parts) are double-buffered: round r + 1's
+// operands are copied by cp.async while round r is computed.
+template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage, int qt, int sl0, int st, int part_lo,
+                                               int part_hi)
+{
+    const int tid = threadIdx.x;
+    constexpr int PI = L == 2 ? 3 : L;
+    constexpr bool INTL = L != 1;
+    const PrimeK &P = K.pr[PI];
+    constexpr int BUF = (TQB + TSB) * PCH * 2 * CS; // u64 per buffer: Qs [TQB] then Ss [TSB]
+    // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
+    const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
+    const int n_chunks = (part_hi - part_lo + PCH - 1) / PCH;
+    const int R = TSL * n_chunks;
+    auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
+    tensor_stage<L, NL>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
+    u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
+    double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
+#pragma unroll 1
+    for (int r = 0; r < R; r++) {
+        const int sl = sl0 + r / n_chunks, j = r % n_chunks, i0 = part_lo + j * PCH, pc = chunk_pc(j);
+        if (r + 1 < R) {
+            const int r1 = r + 1, j1 = r1 % n_chunks;
+            uint64_t *b1 = stage + (size_t)(r1 & 1) * BUF;
+            tensor_stage<L, NL>(K, b1, b1 + TQB * PCH * 2 * CS, qt, sl0 + r1 / n_chunks, st, part_lo + j1 * PCH,
+                                chunk_pc(j1));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const uint64_t *Qs = stage + (size_t)(r & 1) * BUF, *Ss = Qs + TQB * PCH * 2 * CS;
+        if (j == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+                    else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < PCH; i++) {
+            if (i >= pc) break;
+            uint64_t x0[2], x1[2], y0[2], y1[2];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const uint64_t *rr = Qs + (((2 * su + u) * PCH + i) * 2) * CS + c;
+                x0[u] = rr[0];
+                x1[u] = rr[CS];
+            }
+#pragma unroll
+            for (int v = 0; v < 2; v++) {
+                const uint64_t *rr = Ss + (((2 * sv + v) * PCH + i) * 2) * CS + c;
+                y0[v] = rr[0];
+                y1[v] = rr[CS];
+            }
+            if (INTL) {
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+#pragma unroll
+                    for (int v = 0; v < 2; v++) {
+                        a0[u][v] += (u128)x0[u] * y0[v];
+                        a2[u][v] += (u128)x1[u] * y1[v];
+                        a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
+                    }
+            } else {
+                double dx0[2], dx1[2], dxs[2], dy0[2], dy1[2], dys[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++) dx0[u] = u2d(x0[u]), dx1[u] = u2d(x1[u]), dxs[u] = dx0[u] + dx1[u];
+#pragma unroll
+                for (int v = 0; v < 2; v++) dy0[v] = u2d(y0[v]), dy1[v] = u2d(y1[v]), dys[v] = dy0[v] + dy1[v];
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+#pragma unroll
+                    for (int v = 0; v < 2; v++) {
+                        f0[u][v] += mulmod_q1_f64(dx0[u], dy0[v]);
+                        f2[u][v] += mulmod_q1_f64(dx1[u], dy1[v]);
+                        f1[u][v] += mulmod_q1_f64(dxs[u], dys[v]); // operands < 2 q1 < 2^41
+                    }
+            }
+        }
+        // folds: (2q)^2 < 2^118 in 128 bits (q0) / 3 q1 per part below 2^51 (q1): every 512 parts
+        if (((i0 + pc - part_lo) & 511) == 0 && i0 + pc < part_hi) {
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    if (INTL) {
+                        a0[u][v] = red128s<PI>(a0[u][v], P.r64);
+                        a1[u][v] = red128s<PI>(a1[u][v], P.r64);
+                        a2[u][v] = red128s<PI>(a2[u][v], P.r64);
+                    } else {
+                        f0[u][v] = (double)f64_mod_q1(f0[u][v]);
+                        f1[u][v] = (double)f64_mod_q1(f1[u][v]);
+                        f2[u][v] = (double)f64_mod_q1(f2[u][v]);
+                    }
+                }
+        }
+        if (j == n_chunks - 1) { // the slice is complete: write its d0, d1, d2
+            const uint64_t q = P.q;
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 2; v++) {
+                    const int64_t a = (int64_t)qt * TQB + 2 * su + u, bb = (int64_t)st * TSB + 2 * sv + v;
+                    if (a >= K.cq || bb >= K.ct) continue;
+                    const int64_t pi = a * K.ct + bb;
+                    const int jj = sl * CS + c;
+                    uint64_t d0, d2, kk;
+                    if (INTL) {
+                        d0 = red128s<PI>(a0[u][v], P.r64);
+                        d2 = red128s<PI>(a2[u][v], P.r64);
+                        kk = red128s<PI>(a1[u][v], P.r64);
+                    } else {
+                        d0 = f64_mod_q1(f0[u][v]);
+                        d2 = f64_mod_q1(f2[u][v]);
+                        kk = f64_mod_q1(f1[u][v]);
+                    }
+                    K.D01[((size_t)pi * 2 * NL + 0 + L) * N + jj] = d0;
+                    K.D01[((size_t)pi * 2 * NL + NL + L) * N + jj] = submod_d(submod_d(kk, d0, q), d2, q);
+                    K.D2[((size_t)pi * NL + L) * N + jj] = d2;
+                }
+        }
+        __syncthreads(); // every read of buffer r & 1 is done before round r + 2 overwrites it
+    }
+}
+
+template <int NL> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
+{
+    extern __shared__ uint64_t sm[];
+    const int nst = (int)((K.ct + TSB - 1) / TSB);
+    int64_t b = blockIdx.x;
+    const int l = (int)(b % NL);
+    b /= NL;
+    const int st = (int)(b % nst);
+    b /= nst;
+    const int sg = (int)(b % (N / CS / TSL));
+    const int qt = (int)(b / (N / CS / TSL));
+    if (l == 0) tensor_tile<0, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (l == 1) tensor_tile<1, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (NL == 3) tensor_tile<2, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+}
+
+// ================================================================== prime-specialised pointwise helpers
+// reduce_bnd<PI>: exact x mod q for x < 2^64 (q0, P) / x < 2^62 (q1), ntt2.cuh.
+// x < 8q -> [0, 4q)
+template <int PI> BM_D uint64_t red8to4(uint64_t x)
+{
+    constexpr uint64_t q4 = 4 * PrimeC<PI>::q;
+    return x >= q4 ? x - q4 : x;
+}
+
+// ================================================================== K2: digits + ModUp + NTT
+// CTA (pair, l): x_l = INTT_{q_l}(d2[q_l]) in [0, q_l) (non-centred digit, reading R4), kept in
+// shared memory (thread-private slots) between its two ModUp targets:
+//   l = 0: x0 mod q1 -> NTT_q1 -> XU[0],  x0 -> NTT_P -> XU[1]
+//   l = 1: x1 (< q1 < q0) -> NTT_q0 -> XU[2],  x1 -> NTT_P -> XU[3]
+constexpr size_t K2_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+__global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *xs = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
+    uint64_t a[E];
+    load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
+    uint64_t *xu = K.XU + ((size_t)pi * 4 + 2 * l) * N;
+    if (l == 0) {
+        inv<0>(a, sm, K.pr[0]);
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            xs[tid + T * e] = a[e];
+            a[e] = reduce_bnd<1>(a[e]); // x0 < q0 < 2^58: x0 mod q1
+        }
+        fwd_f<1>(a, sm, K.pr[1].fwdf); // the FP64 pipe (ntt3f.cuh)
+    } else {
+        inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // the FP64 pipe
+#pragma unroll
+        for (int e = 0; e < E; e++) xs[tid + T * e] = a[e];
+        fwd<0, false>(a, sm, K.pr[0]); // lazy [0, 2 q0): only ever a Shoup-product operand
+    }
+    store_eval(xu, a);
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = xs[tid + T * e];
+    fwd<2, false>(a, sm, K.pr[2]);
+    store_eval(xu + N, a);
+}
+
+// ================================================================== K3: key switch + ModDown + rescale
+// CTA (pair, c), R22 (exact rewriting of ModDown followed by the rescale by q1):
+// (the device rlk carries P^-1 in its Q limbs, so the Q-limb inner products below are P^-1 KS_c)
+//   KS_c[P]  = x0~[P] rlk0[c][P] + x1~[P] rlk1[c][P]          -> Y = INTT_P  (kept in shared memory)
+//   KS_c[q1] = x0~[q1] rlk0[c][q1] + d2[q1] rlk1[c][q1]        -> U = INTT_q1(d_c[q1] + P^-1 KS_c[q1])
+//   y^ = centred_P(Y);  R = U - P^-1 y^ (mod q1);  z^ = centred_q1(R)
+//   A  = NTT_q0(P^-1 y^ + z^)
+//   KS_c[q0] = d2[q0] rlk0[c][q0] + x1~[q0] rlk1[c][q0]
+//   C_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - A)   (level 0; accumulate: dst += C_c, paper order)
+// (the digit of limb j in its own limb is d2[q_j] itself: no transform needed there)
+constexpr size_t K3_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+__global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumulate)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *ys = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    // rlk layout [j][c][l] planar polys of 2N u64.  K3 reads only the w planes (8-byte keys): each limb's
+    // inner product x0 k0 + x1 k1 is formed exactly in 128 bits and reduced once (red128s), half the
+    // key bytes of two Shoup products (K3 is load-bound: 5.94 -> 5.63 ms)
+    const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
+    const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
+    const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
+    const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N; // d_c[q0], d_c[q1]
+    uint64_t a[E];
+    // ---- P limb
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(xu + 1 * N + j), v = ld2(xu + 3 * N + j);
+        const ulonglong2 w0 = ld2(r0 + 2 * 2 * N + j), w1 = ld2(r1 + 2 * 2 * N + j);
+        a[e] = red128s<2>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[2].r64);
+        a[e + 1] = red128s<2>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[2].r64);
+    }
+    inv<2>(a, sm, K.pr[2]);
+#pragma unroll
+    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // Y, canonical [0, P), coefficient j_M1(tid, e)
+    // ---- q1 limb
+    const ulonglong2 pinv1 = K.pinv[1];
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
+        const ulonglong2 w0 = ld2(r0 + 1 * 2 * N + j), w1 = ld2(r1 + 1 * 2 * N + j);
+        const uint64_t ka = red128s<1>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[1].r64);
+        const uint64_t kb = red128s<1>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[1].r64);
+        a[e] = reduce_bnd<1>(dd.x + ka);
+        a[e + 1] = reduce_bnd<1>(dd.y + kb);
+    }
+    inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
+    // ---- rescale in coefficient form
+    const ulonglong2 pinv0 = K.pinv[0];
+    // y^ = y - [y > P/2] P, so P^-1 y^ = P^-1 y - [y > P/2] in every q limb (no centring reduction)
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = ys[tid + T * e];
+        const uint64_t f = y > (QP >> 1) ? 1 : 0;
+        const uint64_t R = reduce_bnd<1>(a[e] + f + 4 * Q1 - shoup4<1>(y, pinv1)); // U - P^-1 y^
+        const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
+        a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
+    }
+    fwd<0, false>(a, sm, K.pr[0]); // A, in [0, 2 q0)
+    // ---- q0 limb and output
+    const ulonglong2 q1inv = K.q1inv;
+    uint64_t *co = dst.at(pi, c);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const int j = pos_M4(tid, e);
+        const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
+        const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
+        const uint64_t ka = red128s<0>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[0].r64);
+        const uint64_t kb = red128s<0>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[0].r64);
+        // d + P^-1 KS - A + 2 q0 < 11 q0
+        uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + 2 * Q0 - a[e], q1inv));
+        uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + 2 * Q0 - a[e + 1], q1inv));
+        if (accumulate) {
+            const ulonglong2 cc = *reinterpret_cast<const ulonglong2 *>(co + j);
+            oa = csub(oa + cc.x, Q0);
+            ob = csub(ob + cc.y, Q0);
+        }
+        st2(co + j, oa, ob);
+    }
+}
+
+// ================================================================== TMEM as thread-private scratch
+// The ladder's two per-thread scratch arrays (component 1's P-limb key-switch product, waiting for
+// component 0's INTT_P; the last step's t_1) live in tensor memory instead of global memory: 16 u64
+// per thread each, written and read back by the same thread.  With the 32x32b shape a warp reaches the
+// 32 TMEM lanes of its quarter (warp & 3); the four warps sharing a quarter use disjoint 64-column
+// ranges (warp >> 2), so the CTA allocates 256 of the SM's 512 columns (one CTA per SM).
+// COLS: the CTA's allocation (power of two, <= 512); each thread owns COLS / 4 columns of its lane
+template <uint32_t COLS> BM_D uint32_t tmem_alloc(uint32_t *s_addr) // all threads; this thread's base
+{
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_addr)),
+                     "n"(COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    return *s_addr + ((uint32_t)(32 * (warp & 3)) << 16) + (COLS / 4) * (uint32_t)(warp >> 2);
+}
+template <uint32_t COLS> BM_D void tmem_free(uint32_t base) // all threads, after every TMEM access of the CTA
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
+}
+BM_D void tmem_st2(uint32_t taddr, uint64_t x, uint64_t y) // 2 u64 <-> 4 columns (wait::st before reading)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"((uint32_t)x),
+                 "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32))
+                 : "memory");
+}
+// 16 u64 of this thread <-> 32 TMEM columns of its lane
+BM_D void tmem_st16(uint32_t taddr, const uint64_t v[E])
+{
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 16; i++) r[2 * i] = (uint32_t)v[i], r[2 * i + 1] = (uint32_t)(v[i] >> 32);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
+                 "%32};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+                 "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+                 "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+BM_D void tmem_st8(uint32_t taddr, const uint64_t v[8]) // 8 u64 <-> 16 columns
+{
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 8; i++) r[2 * i] = (uint32_t)v[i], r[2 * i + 1] = (uint32_t)(v[i] >> 32);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+BM_D void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
+{
+    uint32_t r[32];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                 "[%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                   "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                   "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr)
+                 : "memory");
+    // the registers are valid only after wait::ld: make them operands of it so nothing reads them earlier
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = (uint64_t)r[2 * i] | ((uint64_t)r[2 * i + 1] << 32);
+}
+
+// ================================================================== fused ladder (a7 + a8)
+// One CTA runs the whole log2(s)-step rotate-and-add ladder of one pair with
+// the level-0 ciphertext C = (c0, c1) resident in shared memory (NTT domain, indexed by NTT index
+// j, padded), so C never leaves the SM between steps.  Per step r = 2^i, g = 5^r mod 2N:
+//   digit   x   = INTT_q0(sigma_g(c1)) in [0, q0), lifted to P as is (reading R4); XP = NTT_P(x)
+//   comp c  y^c = centred_P(INTT_P(XP gk_r[c][P]))
+//           c_c <- c_c + [c = 0] sigma_g(c0) + sigma_g(c1) (P^-1 gk_r[c][q0]) - NTT_q0(P^-1 y^c)
+// (P^-1 is folded into the device Galois keys' q0 limb, and P^-1 y^c = P^-1 y - [y > P/2] needs
+// no centring reduction)
+// The last step leaves the NTT domain directly (INTT is linear, the rounding term y^c is already
+// in coefficient form): out_c = INTT_q0(c_c + [c = 0] sigma(c0) + P^-1 sigma(c1) gk[c][q0])
+// - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.
+constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+
+
+__global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    __shared__ uint32_t s_tmem;
+    const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
+    const ulonglong2 pinv = K.pinv[0];
+    stage_by_j(S0, cin.at(pi, 0));
+    stage_by_j(S1, cin.at(pi, 1));
+    uint64_t a[E];
+    uint32_t g = 5; // 5^(2^i) mod 2N
+#pragma unroll 1
+    for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
+        const bool last = i == L - 1;
+        // [rot][c][q0|P] planar polys of 2N u64
+        const uint64_t *gq0 = K.gk + (size_t)(i * 4 + 0) * 2 * N, *gp0 = gq0 + 2 * N;
+        const uint64_t *gq1 = K.gk + (size_t)(i * 4 + 2) * 2 * N, *gp1 = gq1 + 2 * N;
+        __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
+        // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
+#pragma unroll
+        for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
+        inv<0>(a, XB, K.pr[0]);
+        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
+        // P-limb key-switch products for both components; component 1's waits in the workspace
+#pragma unroll
+        for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live registers)
+            uint64_t k1[8];
+#pragma unroll
+            for (int e = 8 * h; e < 8 * h + 8; e += 2) {
+                const int pos = pos_M4(tid, e);
+                ulonglong2 w0, w0b, w1, w1b;
+                ldkey2(gp0, pos, w0, w0b);
+                ldkey2(gp1, pos, w1, w1b);
+                k1[e - 8 * h] = shoup4<2>(a[e], w1);
+                k1[e - 8 * h + 1] = shoup4<2>(a[e + 1], w1b);
+                a[e] = shoup4<2>(a[e], w0);
+                a[e + 1] = shoup4<2>(a[e + 1], w0b);
+            }
+            tmem_st8(tks1 + 16 * h, k1);
+        }
+        tmem_wait_st();
+#pragma unroll 1
+        for (int c = 0; c < 2; c++) {
+            if (c == 1) tmem_ld16(tks1, a); // component 1's P-limb product, parked in TMEM above
+            inv<2>(a, XB, K.pr[2]);
+            // P^-1 y^c mod q0 with y^c = y - [y > P/2] P:  P^-1 y - [y > P/2], < 5 q0
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            uint64_t *S = c ? S1 : S0;
+            const uint64_t *gq = c ? gq1 : gq0;
+            if (!last) {
+                fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), lazy [0, 2 q0)
+                ulonglong2 kk[2];
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                    // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
+                    uint64_t v = ks + 2 * Q0 - a[e] + S[pidx(j)]; // < 7 q0
+                    if (c == 0) v += S0[pidx(jp)];           // < 7 q0
+                    a[e] = reduce_bnd<0>(v);
+                }
+                __syncthreads(); // every read of the old c_c is done
+#pragma unroll
+                for (int e = 0; e < E; e++) S[pidx(j_M4(tid, e))] = a[e];
+            } else {
+                tmem_st16(ttsc, a); // P^-1 y^c (coefficient j_M1(tid, e)), < 5 q0
+                ulonglong2 kk[2];
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
+                    uint64_t v = ks + S[pidx(j)]; // < 5 q0
+                    if (c == 0) v += S0[pidx(jp)];
+                    a[e] = reduce_bnd<0>(v);
+                }
+                inv<0>(a, XB, K.pr[0]);
+                uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+                uint64_t t[E];
+                tmem_ld16(ttsc, t);
+#pragma unroll
+                for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
+            }
+        }
+    }
+    tmem_free<256>(s_tmem);
+}
+
+// ================================================================== f2: hoisted rotation sum
+// SURVEY.md sec. 8f, order BM_ORDER_HOISTED_ROT -- NOT the paper's ladder (oracle: hoisted_rot_sum).
+// One CTA per pair computes out = sum_{r<s} Rot(C, r) with ONE key switch (Halevi-Shoup hoisting):
+//   x = INTT_q0(c1) in [0, q0) (non-centred digit, R4), X~P = NTT_P(x); for r = 1..s-1 the
+//   automorphism acts on each NTT-domain digit limb as an index permutation, and
+//   A[c][q0] = sum_r sigma_r(c1) (P^-1 hgk_r[c][q0]),  A[c][P] = sum_r sigma_r(X~P) hgk_r[c][P]
+//   are accumulated exactly in 128 bits (8-byte keys, no Shoup companions; folded every 64 terms);
+//   then one ModDown per component straight to the coefficient-domain output:
+//   out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c,  y^c = centred_P(INTT_P(A[c][P])),
+//   base_0 = sum_{r<s} sigma_r(c0), base_1 = c1.   6 transforms per pair (the ladder: 6 log2 s).
+constexpr size_t HROT_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int s)
+{
+    extern __shared__ uint64_t sm[];
+    // XB: transform exchanges; SX: (c1, X~P) pairs by NTT index (one 16-byte gather per rotation)
+    uint64_t *XB = sm;
+    ulonglong2 *SX = reinterpret_cast<ulonglong2 *>(sm + SMEM_WORDS);
+    uint64_t *SP = sm + SMEM_WORDS; // reused for c0 after the rotation products
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x;
+    // A [c][q0 | P] (thread-private: 16 u64 per thread and polynomial) lives in TMEM, columns 32 v + 2 e,
+    // and P^-1 y^c reuses A[c][P]'s columns once consumed; base_0 waits in the D2 scratch (dead after K3)
+    __shared__ uint32_t s_tmem;
+    const uint32_t tA = tmem_alloc<512>(&s_tmem);
+    uint64_t *b0s = K.D2 + (size_t)pi * 2 * N;
+    const ulonglong2 pinv = K.pinv[0];
+    // Phases share one call site per transform (an instruction-cache concern: every unrolled
+    // transform is ~40 KB of SASS): ph 0 = the digit, ph 1, 2 = the ModDown of component ph - 1.
+    uint64_t a[E];
+#pragma unroll 1
+    for (int ph = 0; ph < 3; ph++) {
+        const int c = ph - 1;
+        if (ph == 0) { // (c1, .) staged by NTT index; a = c1
+            load_eval(a, cin.at(pi, 1));
+#pragma unroll
+            for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
+        } else {       // y^c = INTT_P(A[c][P]); a = base_c + A[c][q0]
+            tmem_ld16(tA + 32 * (2 * c + 1), a); // A[c][P]
+            inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            tmem_st16(tA + 32 * (2 * c + 1), a); // P^-1 y^c (coefficient j_M1(tid, e)) over A[c][P]
+            const uint64_t *base = c ? cin.at(pi, 1) : b0s;
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                const int pos = pos_M4(tid, e);
+                const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
+                a[e] = bv.x;
+                a[e + 1] = bv.y;
+            }
+            {
+                uint64_t av[E];
+                tmem_ld16(tA + 32 * (2 * c), av); // A[c][q0]
+#pragma unroll
+                for (int e = 0; e < E; e++) a[e] = csub(a[e] + av[e], Q0);
+            }
+        }
+        inv<0>(a, XB, K.pr[0]);
+        if (ph > 0) { // out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c
+            uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+            uint64_t t[E];
+            tmem_ld16(tA + 32 * (2 * c + 1), t);
+#pragma unroll
+            for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
+            continue;
+        }
+        // ---- digit: X~P = NTT_P(x), staged next to c1
+        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup / 128-bit product operand
+#pragma unroll
+        for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
+        __syncthreads();
+        // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
+        //      time, the next rotation's keys loaded while this one's are used
+#pragma unroll 1
+        for (int g2 = 0; g2 < E / 2; g2++) {
+            const int e0 = 2 * g2, pos = pos_M4(tid, e0);
+            const int j0 = j_M4(tid, e0), j1 = j_M4(tid, e0 + 1);
+            u128 A[2][4]; // [coefficient][c * 2 + limb (q0, P)]
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) A[u][v] = 0;
+            ulonglong2 kc[4], kn[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + (size_t)v * N + pos);
+            uint32_t gr = 1;
+#pragma unroll 1
+            for (int r = 1; r < s; r++) {
+                gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
+                if (r + 1 < s) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
+                }
+                const ulonglong2 x0 = SX[pidx(auto_perm(j0, gr))], x1 = SX[pidx(auto_perm(j1, gr))];
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    A[0][2 * c] += (u128)x0.x * kc[2 * c].x;
+                    A[1][2 * c] += (u128)x1.x * kc[2 * c].y;
+                    A[0][2 * c + 1] += (u128)x0.y * kc[2 * c + 1].x;
+                    A[1][2 * c + 1] += (u128)x1.y * kc[2 * c + 1].y;
+                }
+                if ((r & 63) == 0) { // 64 products of < 2^60 x 2^60 stay below 2^128
+#pragma unroll
+                    for (int u = 0; u < 2; u++)
+#pragma unroll
+                        for (int v = 0; v < 4; v++)
+                            A[u][v] = (v & 1) ? red128s<2>(A[u][v], K.pr[2].r64) : red128s<0>(A[u][v], K.pr[0].r64);
+                }
+#pragma unroll
+                for (int v = 0; v < 4; v++) kc[v] = kn[v];
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                if (v & 1) tmem_st2(tA + 32 * v + 4 * g2, red128s<2>(A[0][v], K.pr[2].r64), red128s<2>(A[1][v], K.pr[2].r64));
+                else tmem_st2(tA + 32 * v + 4 * g2, red128s<0>(A[0][v], K.pr[0].r64), red128s<0>(A[1][v], K.pr[0].r64));
+            }
+        }
+        tmem_wait_st(); // the A stores above complete before phases 1, 2 read them back
+        // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
+        //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
+        __syncthreads();
+        stage_by_j(SP, cin.at(pi, 0));
+#pragma unroll 1
+        for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = j_M4(tid, e);
+                a[e] = csub(SP[pidx(j)] + SP[pidx(auto_perm(j, g))], Q0);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
+    tmem_free<512>(s_tmem);
+}
+}
+
+// K7: output INTT when there is no ladder (s = 1)
+__global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
+{
+    extern __shared__ uint64_t sm[];
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
+    uint64_t a[E];
+    load_eval(a, cin.at(pi, c));
+    inv<0>(a, sm, K.pr[0]);
+    store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
+}
