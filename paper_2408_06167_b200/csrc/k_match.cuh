@@ -536,8 +536,9 @@ BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
 
 // ================================================================== fused ladder (a7 + a8)
 // One CTA runs the whole log2(s)-step rotate-and-add ladder of one pair with
-// the level-0 ciphertext C = (c0, c1) resident in shared memory (NTT domain, indexed by NTT index
-// j, padded), so C never leaves the SM between steps.  Per step r = 2^i, g = 5^r mod 2N:
+// the level-0 ciphertext C = (c0, c1) resident in shared memory (NTT domain, stored in natural
+// order, ntt3.cuh nat_at: conflict-free automorphism gathers), so C never leaves the SM between
+// steps.  Per step r = 2^i, g = 5^r mod 2N:
 //   digit   x   = INTT_q0(sigma_g(c1)) in [0, q0), lifted to P as is (reading R4); XP = NTT_P(x)
 //   comp c  y^c = centred_P(INTT_P(XP gk_r[c][P]))
 //           c_c <- c_c + [c = 0] sigma_g(c0) + sigma_g(c1) (P^-1 gk_r[c][q0]) - NTT_q0(P^-1 y^c)
@@ -558,8 +559,9 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     __shared__ uint32_t s_tmem;
     const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
-    stage_by_j(S0, cin.at(pi, 0));
-    stage_by_j(S1, cin.at(pi, 1));
+    const int nt = nat_tid(tid); // S0, S1 in natural order (nat_at / nat_auto: conflict-free)
+    stage_nat(S0, cin.at(pi, 0));
+    stage_nat(S1, cin.at(pi, 1));
     uint64_t a[E];
     uint32_t g = 5; // 5^(2^i) mod 2N
 #pragma unroll 1
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
         __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
         // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
 #pragma unroll
-        for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
+        for (int e = 0; e < E; e++) a[e] = S1[nat_auto(nt, e, g)];
         inv<0>(a, XB, K.pr[0]);
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
         // P-limb key-switch products for both components; component 1's waits in the workspace
@@ -606,27 +608,27 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                 ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
-                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
                     if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
                     // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
-                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
-                    uint64_t v = ks + 2 * Q0 - a[e] + S[pidx(j)]; // < 7 q0
-                    if (c == 0) v += S0[pidx(jp)];           // < 7 q0
+                    const uint64_t ks = shoup4<0>(S1[jp], kk[e & 1]);
+                    uint64_t v = ks + 2 * Q0 - a[e] + S[j]; // < 7 q0
+                    if (c == 0) v += S0[jp];           // < 7 q0
                     a[e] = reduce_bnd<0>(v);
                 }
                 __syncthreads(); // every read of the old c_c is done
 #pragma unroll
-                for (int e = 0; e < E; e++) S[pidx(j_M4(tid, e))] = a[e];
+                for (int e = 0; e < E; e++) S[nat_at(nt, e)] = a[e];
             } else {
                 tmem_st16(ttsc, a); // P^-1 y^c (coefficient j_M1(tid, e)), < 5 q0
                 ulonglong2 kk[2];
 #pragma unroll
                 for (int e = 0; e < E; e++) {
-                    const int j = j_M4(tid, e), jp = auto_perm(j, g);
+                    const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
                     if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
-                    const uint64_t ks = shoup4<0>(S1[pidx(jp)], kk[e & 1]);
-                    uint64_t v = ks + S[pidx(j)]; // < 5 q0
-                    if (c == 0) v += S0[pidx(jp)];
+                    const uint64_t ks = shoup4<0>(S1[jp], kk[e & 1]);
+                    uint64_t v = ks + S[j]; // < 5 q0
+                    if (c == 0) v += S0[jp];
                     a[e] = reduce_bnd<0>(v);
                 }
                 inv<0>(a, XB, K.pr[0]);

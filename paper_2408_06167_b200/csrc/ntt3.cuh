@@ -264,5 +264,40 @@ BM_D void stage_by_j(uint64_t *sm, const uint64_t *p)
     }
 }
 
+// Natural-order shared-memory storage of an NTT-domain polynomial (the resident operands of the
+// rotation kernels): NTT index j (bit-reversed evaluation order) is stored at word i + (i >> 4)
+// with i = brev13(j), the natural index of its evaluation point.  The automorphism sigma_g maps
+// natural index i to i g + (g - 1) / 2 mod N (odd g), so a warp's sigma_g gather of its M4 values
+// touches 16 consecutive (i >> 4) blocks with an odd stride: both the M4 accesses and every
+// gather are bank-conflict-free (2 wavefronts per 64-bit warp access; the j + (j >> 4) padding
+// of the exchange buffer gives 4 for M4 and 4-5 for the gathers).  j_M4's thread bits (1, 5..12)
+// and element bits (0, 2..4) are disjoint, so i = nat_tid | nat_e with nat_e a constant.
+BM_HD constexpr int brev13c(int x)
+{
+    int r = 0;
+    for (int b = 0; b < 13; b++) r |= ((x >> b) & 1) << (12 - b);
+    return r;
+}
+BM_D int nat_tid(int tid) { return brev13(32 * (tid >> 1) + 2 * (tid & 1)); }
+BM_HD constexpr int nat_e(int e) { return brev13c(4 * (e >> 1) + (e & 1)); }
+BM_HD constexpr int npad(int i) { return i + (i >> 4); }
+// word of this thread's element e (M4) / of the element sigma_g moves there
+BM_D int nat_at(int ntid, int e) { return npad(ntid) + npad(nat_e(e)); }
+BM_D int nat_auto(int ntid, int e, uint32_t g)
+{
+    const uint32_t i = (uint32_t)(ntid | nat_e(e));
+    return npad((int)((i * g + ((g - 1) >> 1)) & (N - 1)));
+}
+BM_D void stage_nat(uint64_t *sm, const uint64_t *p)
+{
+    const int nt = nat_tid(threadIdx.x);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        const ulonglong2 v = ldv(p + pos_M4(threadIdx.x, e));
+        sm[nat_at(nt, e)] = v.x;
+        sm[nat_at(nt, e + 1)] = v.y;
+    }
+}
+
 } // namespace v3
 } // namespace bm

@@ -28,7 +28,9 @@ def launches(path, out):
     for r in rows[1:]:
         if r[iM] != "gpu__time_duration.sum":
             continue
-        k = r[iK].split("(")[0].replace("void ", "").split("<")[0]
+        k = r[iK].split("(")[0].replace("void ", "")
+        if k.startswith("k_tensor<2"):  # bm_match's tensor; k_tensor<3> is f1's (level 2)
+            k = "k_tensor"
         tot[k] += float(r[iV].replace(",", ""))
         cnt[k] += 1
     match = {k: v for k, v in tot.items() if k in MATCH_KERNELS}
