@@ -658,7 +658,7 @@ constexpr size_t HROT_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int s)
 {
     extern __shared__ uint64_t sm[];
-    // XB: transform exchanges; SX: (c1, X~P) pairs by NTT index (one 16-byte gather per rotation)
+    // XB: transform exchanges; SX: (c1, X~P) pairs in natural order (one 16-byte gather per rotation)
     uint64_t *XB = sm;
     ulonglong2 *SX = reinterpret_cast<ulonglong2 *>(sm + SMEM_WORDS);
     uint64_t *SP = sm + SMEM_WORDS; // reused for c0 after the rotation products
@@ -672,14 +672,15 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
     const ulonglong2 pinv = K.pinv[0];
     // Phases share one call site per transform (an instruction-cache concern: every unrolled
     // transform is ~40 KB of SASS): ph 0 = the digit, ph 1, 2 = the ModDown of component ph - 1.
+    const int nt = nat_tid(tid); // SX, SP in natural order (ntt3.cuh nat_at: conflict-free gathers)
     uint64_t a[E];
 #pragma unroll 1
     for (int ph = 0; ph < 3; ph++) {
         const int c = ph - 1;
-        if (ph == 0) { // (c1, .) staged by NTT index; a = c1
+        if (ph == 0) { // (c1, .) staged in natural order; a = c1
             load_eval(a, cin.at(pi, 1));
 #pragma unroll
-            for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].x = a[e];
+            for (int e = 0; e < E; e++) SX[nat_at(nt, e)].x = a[e];
         } else {       // y^c = INTT_P(A[c][P]); a = base_c + A[c][q0]
             tmem_ld16(tA + 32 * (2 * c + 1), a); // A[c][P]
             inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
@@ -713,14 +714,14 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         // ---- digit: X~P = NTT_P(x), staged next to c1
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup / 128-bit product operand
 #pragma unroll
-        for (int e = 0; e < E; e++) SX[pidx(j_M4(tid, e))].y = a[e];
+        for (int e = 0; e < E; e++) SX[nat_at(nt, e)].y = a[e];
         __syncthreads();
         // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
         //      time, the next rotation's keys loaded while this one's are used
 #pragma unroll 1
         for (int g2 = 0; g2 < E / 2; g2++) {
             const int e0 = 2 * g2, pos = pos_M4(tid, e0);
-            const int j0 = j_M4(tid, e0), j1 = j_M4(tid, e0 + 1);
+            const uint32_t i0 = nat_i(nt, e0), i1 = nat_i(nt, e0 + 1);
             u128 A[2][4]; // [coefficient][c * 2 + limb (q0, P)]
 #pragma unroll
             for (int u = 0; u < 2; u++)
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
 #pragma unroll
                     for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
                 }
-                const ulonglong2 x0 = SX[pidx(auto_perm(j0, gr))], x1 = SX[pidx(auto_perm(j1, gr))];
+                const ulonglong2 x0 = SX[nat_auto_i(i0, gr)], x1 = SX[nat_auto_i(i1, gr)];
 #pragma unroll
                 for (int c = 0; c < 2; c++) {
                     A[0][2 * c] += (u128)x0.x * kc[2 * c].x;
@@ -763,24 +764,23 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         }
         tmem_wait_st(); // the A stores above complete before phases 1, 2 read them back
         // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
-        //      q0: the same residues as the term-by-term sum), c0 staged by NTT index over X~P
+        //      q0: the same residues as the term-by-term sum), c0 staged in natural order over X~P
         __syncthreads();
-        stage_by_j(SP, cin.at(pi, 0));
+        stage_nat(SP, cin.at(pi, 0));
 #pragma unroll 1
         for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; e++) {
-                const int j = j_M4(tid, e);
-                a[e] = csub(SP[pidx(j)] + SP[pidx(auto_perm(j, g))], Q0);
+                a[e] = csub(SP[nat_at(nt, e)] + SP[nat_auto(nt, e, g)], Q0);
             }
             __syncthreads();
 #pragma unroll
-            for (int e = 0; e < E; e++) SP[pidx(j_M4(tid, e))] = a[e];
+            for (int e = 0; e < E; e++) SP[nat_at(nt, e)] = a[e];
         }
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[pidx(j_M4(tid, e))];
+        for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[nat_at(nt, e)];
     tmem_free<512>(s_tmem);
 }
 }

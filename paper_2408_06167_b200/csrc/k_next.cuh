@@ -119,11 +119,12 @@ __global__ void __launch_bounds__(T, 1) k_rot1_digits(ExpK K)
     if (K.skip(ct)) return;
     const uint64_t *c1 = K.out + ((size_t)ct * 2 + 1) * 2 * N + (size_t)l * N;
     uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
-    stage_by_j(S, c1);
+    const int nt = nat_tid(tid);
+    stage_nat(S, c1); // natural order: conflict-free gather (ntt3.cuh nat_at)
     __syncthreads();
     uint64_t a[E];
 #pragma unroll
-    for (int e = 0; e < E; e++) a[e] = S[pidx(auto_perm(j_M4(tid, e), K.g))];
+    for (int e = 0; e < E; e++) a[e] = S[nat_auto(nt, e, K.g)];
     store_eval(xu + (size_t)(l == 0 ? 0 : 4) * N, a); // the digit in its own limb: sigma(c1)[q_l]
     if (l == 0) {
         inv<0>(a, sm, K.pr[0]);
@@ -193,9 +194,9 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             }
             fwd<0>(a, sm, K.pr[0]);
         }
-        if (c == 0) { // sigma_g(c0)[q_l] by an NTT-index gather (c0 is this CTA's to overwrite)
+        if (c == 0) { // sigma_g(c0)[q_l] by a gather (natural order; c0 is this CTA's to overwrite)
             __syncthreads(); // previous limb's gathers from S are done
-            stage_by_j(S, c0 + (size_t)l * N);
+            stage_nat(S, c0 + (size_t)l * N);
             __syncthreads();
         }
         const uint64_t q = l ? Q1 : Q0;
@@ -221,8 +222,8 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             }
             uint64_t va = cv.x + ka + q - a[e], vb = cv.y + kb + q - a[e + 1]; // < 11 q
             if (c == 0) {
-                va += S[pidx(auto_perm(j_M4(tid, e), K.g))];
-                vb += S[pidx(auto_perm(j_M4(tid, e + 1), K.g))];
+                va += S[nat_auto(nat_tid(tid), e, K.g)];
+                vb += S[nat_auto(nat_tid(tid), e + 1, K.g)];
             }
             a[e] = l ? reduce_bnd<1>(va) : reduce_bnd<0>(va);
             a[e + 1] = l ? reduce_bnd<1>(vb) : reduce_bnd<0>(vb);
@@ -482,11 +483,12 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
     const uint32_t g = (uint32_t)pow5_mod2n(SLOTS - u);
     const ulonglong2 *gk = C.gkc + (size_t)(u - 1) * 4 * N; // [c][q0 | P][N]
     uint64_t *ks1 = C.scr + (size_t)pi * 2 * N, *tsc = ks1 + N;
-    stage_by_j(S0, ci);
-    stage_by_j(S1, ci + N);
+    const int nt = nat_tid(tid);
+    stage_nat(S0, ci); // natural order: conflict-free gathers (ntt3.cuh nat_at)
+    stage_nat(S1, ci + N);
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < E; e++) a[e] = S1[pidx(auto_perm(j_M4(tid, e), g))];
+    for (int e = 0; e < E; e++) a[e] = S1[nat_auto(nt, e, g)];
     inv<0>(a, XB, K.pr[0]);
     fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
 #pragma unroll
@@ -515,9 +517,9 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
         const ulonglong2 *gq = gk + (size_t)(2 * c) * N;
 #pragma unroll
         for (int e = 0; e < E; e++) {
-            const int j = j_M4(tid, e), jp = auto_perm(j, g);
-            uint64_t v = shoup4<0>(S1[pidx(jp)], ldkey1(gq, pos_M4(tid, e))); // [0, 4 q0)
-            if (c == 0) v += S0[pidx(jp)];
+            const int jp = nat_auto(nt, e, g);
+            uint64_t v = shoup4<0>(S1[jp], ldkey1(gq, pos_M4(tid, e))); // [0, 4 q0)
+            if (c == 0) v += S0[jp];
             a[e] = reduce_bnd<0>(v);
         }
         inv<0>(a, XB, K.pr[0]);

@@ -283,11 +283,10 @@ BM_HD constexpr int nat_e(int e) { return brev13c(4 * (e >> 1) + (e & 1)); }
 BM_HD constexpr int npad(int i) { return i + (i >> 4); }
 // word of this thread's element e (M4) / of the element sigma_g moves there
 BM_D int nat_at(int ntid, int e) { return npad(ntid) + npad(nat_e(e)); }
-BM_D int nat_auto(int ntid, int e, uint32_t g)
-{
-    const uint32_t i = (uint32_t)(ntid | nat_e(e));
-    return npad((int)((i * g + ((g - 1) >> 1)) & (N - 1)));
-}
+BM_D int nat_auto_i(uint32_t i, uint32_t g) { return npad((int)((i * g + ((g - 1) >> 1)) & (N - 1))); }
+BM_D int nat_auto(int ntid, int e, uint32_t g) { return nat_auto_i((uint32_t)(ntid | nat_e(e)), g); }
+// natural index of element e when e is not a compile-time constant
+BM_D uint32_t nat_i(int ntid, int e) { return (uint32_t)(ntid | brev13(4 * (e >> 1) + (e & 1))); }
 BM_D void stage_nat(uint64_t *sm, const uint64_t *p)
 {
     const int nt = nat_tid(threadIdx.x);
