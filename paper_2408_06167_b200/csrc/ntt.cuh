@@ -22,11 +22,7 @@ constexpr int SMEM_WORDS = N + N / 16; // 8704 u64 = 69,632 B
 
 BM_D int pidx(int j) { return j + (j >> 4); }
 
-#ifdef BM_EXP_TW // timing experiment only (wrong results): every twiddle load hits the same 16 entries
-BM_D ulonglong2 ldtw(const ulonglong2 *p) { return __ldg((const ulonglong2 *)((uintptr_t)p & ~(uintptr_t)0xff0)); }
-#else
 BM_D ulonglong2 ldtw(const ulonglong2 *p) { return __ldg(p); }
-#endif
 
 // CT butterfly: x, y in [0,4q) -> x + w y, x - w y in [0,4q)
 BM_D void ct_bfly(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q, uint64_t q2)
