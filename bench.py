@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion / f4 enrollment leg")
     ap.add_argument("--no-f1", action="store_true", help="skip the f1 compressed-scan leg")
+    ap.add_argument("--no-single", action="store_true", help="skip the single-query latency leg")
     ap.add_argument("--no-f4", action="store_true", help="skip the f4 enrollment part of the f3 leg")
     ap.add_argument("--nq", type=int, default=384)
     ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
@@ -227,18 +228,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # events at every step boundary (recorded on the launching stream, no synchronisation between
+    # steps): the first and last bracket the timed region, the others give the per-step spread
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
+        ev[0].record(stream)
+        for i in range(args.steps):
             step()
-        e1.record(stream)
+            ev[i + 1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    ms = pdist.max_over_ranks(ev[0].elapsed_time(ev[-1]), dev)
     ms_step = ms / args.steps
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    ms_std = float(statistics.pstdev(per_step)) if len(per_step) > 1 else 0.0
     tq_per_step = world * n_tmpl * nq
     value = tq_per_step / (ms_step / 1e3)
 
@@ -291,6 +296,12 @@ def run_ours(args):
                 "hbm": {"achieved_gbs": round(hbm_achieved, 2), "peak_gbs": hbm_gbs,
                         "frac": round(hbm_achieved / hbm_gbs, 5)},
                 "per_class": {c: {k: round(v, 3) for k, v in d.items()} for c, d in per_class.items()}}
+
+    # single-query latency (the paper's shape: ONE query against the whole DB,
+    # PAPER.md:572-574): bm_match of query 0 over all sets, device time, 3 warm-ups + 10 timed runs
+    single = None
+    if world == 1 and not args.no_single:
+        single = run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, order, stream)
 
     # e2e through the C ABI with host buffers (query H2D + result D2H inside the timed region)
     e2e = None
@@ -357,7 +368,8 @@ def run_ours(args):
         line = {
             "metric": "encrypted templates matched/sec (d=128, N=8192)", "value": round(value, 1),
             "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": round(ms_step, 4), "ms_per_step_std": round(ms_std, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (seeded unit-norm Gaussian templates, genuine noisy queries)",
             "config": {"workload": f"BASELINE configs[1]: d=128, {n_tmpl} templates/GPU, {nq} queries, p={p}, "
                                    f"order={['hoisted', 'paper', 'hoisted-rotations (f2, not the paper ladder)'][order]}",
@@ -365,13 +377,37 @@ def run_ours(args):
                        "ring_N": N_RING, "parallelism": f"db-shard{world}",
                        "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
                            nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "f3_expand": f3, "f1_compressed": f1,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "single_query": single,
+            "f3_expand": f3, "f1_compressed": f1,
             "gpu_launches": int(launches * args.steps),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, order, stream):
+    """Latency of ONE query against the whole DB (the paper's measurement shape, PAPER.md:572-574:
+    6,144 templates at d = 128 in 0.45 s on 6 CPU cores): bm_match of query 0 over all n_sets sets,
+    CUDA events on the launching stream, 3 warm-ups then 10 timed runs (10 trials)."""
+    q1, o1 = d_q[:1], d_out[:1]
+    for _ in range(3):
+        B.bm_match(prm, evk_dev, d_db, n_sets, q1, 1, o1, ws, order)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        B.bm_match(prm, evk_dev, d_db, n_sets, q1, 1, o1, ws, order)
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = statistics.mean(times)
+    return {"ms": round(ms, 4), "ms_std": round(statistics.pstdev(times), 4), "runs": len(times),
+            "templates": n_tmpl, "templates_per_s": round(n_tmpl / (ms / 1e3), 1),
+            "note": "one query vs the whole configs[1] DB (24 (query, set) pairs: 24 CTAs per kernel on "
+                    "148 SMs, a latency-bound launch), device time of bm_match"}
 
 
 def f3_modmuls(p, s):
