@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-f4", action="store_true", help="skip the f4 enrollment part of the f3 leg")
     ap.add_argument("--nq", type=int, default=384)
     ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1 result gather (a8): p2p = fused into the output kernels (bm_match_rows storing "
+                         "to the roots over NVLink), nccl = all_to_all after each group's scan")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quiet", action="store_true")
@@ -204,21 +207,41 @@ def run_ours(args):
         Q, _ = I.queries(CFG, nq)
         B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
     d_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
-    # N > 1: broadcast (a3), scan and result all_to_all (a8) overlapped over query groups
+    # N > 1: broadcast (a3) and scan overlapped over query groups; the result gather (a8) either fused
+    # into the scan's output kernels (p2p: every result stored straight into its root's buffer over
+    # NVLink, dist.P2PGather) or an all_to_all after each group's scan (nccl)
     G = args.groups if world > 1 else 1
     gq = nq // G
     ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, gq, order), dtype=torch.uint8, device=dev)
-    recv = torch.empty((G, world, gq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev) if world > 1 else None
     comm_s, comp_s = (torch.cuda.Stream(), torch.cuda.Stream()) if world > 1 else (None, None)
+    gather, gat, recv, flag = "local", None, None, None
+    if world > 1 and args.gather == "p2p":
+        res = torch.empty((nq // world, n_sets * world, 2, N_RING), dtype=torch.int64, device=dev)
+        try:
+            gat = pdist.P2PGather(B, res, nq, G, n_sets * world)
+            flag = torch.zeros(1, dtype=torch.float64, device=dev)
+            gather = "p2p: fused into the output kernels (bm_match_rows, CUDA IPC peer stores over NVLink)"
+        except Exception as ex:  # noqa: BLE001 -- a transport fallback (NCCL), never a CPU one
+            del res
+            gather = f"nccl all_to_all (p2p unavailable: {type(ex).__name__}: {ex})"[:200]
+    if world > 1 and gat is None:
+        recv = torch.empty((G, world, gq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
+        if gather == "local":
+            gather = "nccl all_to_all per query group"
     B.bm_sync()
     stream = torch.cuda.current_stream()
 
     def match(g, q_g, out_g):
         B.bm_match(prm, evk_dev, d_db, n_sets, q_g, q_g.shape[0], out_g, ws, order)
 
+    def match_rows(g, q_g, rows_g):
+        B.bm_match_rows(prm, evk_dev, d_db, n_sets, q_g, q_g.shape[0], rows_g, rank * n_sets, ws, order)
+
     def step():
         if world == 1:
             B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+        elif gat is not None:
+            pdist.scan_p2p(match_rows, d_q, gat, G, comm_s, comp_s, flag)
         else:
             pdist.scan_pipelined(match, d_q, d_out, recv, G, comm_s, comp_s)
 
@@ -297,6 +320,12 @@ def run_ours(args):
                         "frac": round(hbm_achieved / hbm_gbs, 5)},
                 "per_class": {c: {k: round(v, 3) for k, v in d.items()} for c, d in per_class.items()}}
 
+    if gat is not None:   # fused gather: this rank's own sets in the rows it roots equal its local scan
+        torch.cuda.synchronize()
+        for j, (root, row) in enumerate(pdist.p2p_row_map(nq, G, world)):
+            if root == rank:
+                assert torch.equal(gat.res[row, rank * n_sets:(rank + 1) * n_sets], d_out[j]), "p2p gather"
+
     # single-query latency (the paper's shape: ONE query against the whole DB,
     # PAPER.md:572-574): bm_match of query 0 over all sets, device time, 3 warm-ups + 10 timed runs
     single = None
@@ -374,7 +403,7 @@ def run_ours(args):
             "config": {"workload": f"BASELINE configs[1]: d=128, {n_tmpl} templates/GPU, {nq} queries, p={p}, "
                                    f"order={['hoisted', 'paper', 'hoisted-rotations (f2, not the paper ladder)'][order]}",
                        "d": D, "p": p, "templates_per_gpu": n_tmpl, "sets_per_gpu": n_sets, "queries": nq,
-                       "ring_N": N_RING, "parallelism": f"db-shard{world}",
+                       "ring_N": N_RING, "parallelism": f"db-shard{world}", "gather": gather,
                        "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
                            nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "single_query": single,
@@ -383,6 +412,9 @@ def run_ours(args):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    if gat is not None:
+        dist.barrier()
+        gat.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -177,6 +177,30 @@ size_t bm_match_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t 
 int bm_match(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
              int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
 
+/* a8 fused into the scan ("the main server combines the returned
+ * outputs"): the same scan, but every result is stored by the output kernels themselves straight into
+ * its query's ROW on the query's root GPU -- over NVLink when the row lives on a peer (a pointer
+ * obtained with bm_ipc_open), so the gather overlaps the scan pair by pair and needs no collective.
+ * d_rows: DEVICE array of nq pointers; row j holds n_row_sets level-0 results [n_row_sets][2][N]
+ *         (coefficient domain, as d_out of bm_match), and (query j, local set t) is written at
+ *         d_rows[j] + ((set_offset + t) * 2 + c) * N, i.e. this rank's sets at their GLOBAL set
+ *         numbers.  Rows are caller-owned; they must not overlap.
+ * The caller orders the root's reads after every writer's scan (e.g. an NCCL all-reduce queued
+ * on each writer's stream after this call).  Errors as bm_match; BM_ERR_INVALID_ARG if d_rows is
+ * NULL or set_offset < 0. */
+int bm_match_rows(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+                  int32_t nq, uint64_t *const *d_rows, int64_t set_offset, void *d_ws, size_t ws_bytes, int32_t order,
+                  void *stream);
+
+/* CUDA IPC for bm_match_rows across processes (one process per GPU): bm_ipc_handle returns the
+ * 64-byte handle of the device allocation containing d_ptr and d_ptr's byte offset inside it;
+ * another process opens it with bm_ipc_open (peer access enabled lazily; *d_base = the allocation's
+ * base in this process, add the offset) and releases it with bm_ipc_close.  Errors: BM_ERR_CUDA,
+ * BM_ERR_INVALID_ARG. */
+int bm_ipc_handle(const void *d_ptr, uint8_t handle[64], uint64_t *offset);
+int bm_ipc_open(const uint8_t handle[64], void **d_base);
+int bm_ipc_close(void *d_base);
+
 /* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
  * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call.  The queries are
  * processed in groups of about 576 (query, set) pairs (or BM_HOST_GROUPS groups): group g's
@@ -191,7 +215,8 @@ int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, i
 
 /* Per-kernel-class device time of the last bm_match on this thread when profiling is
  * enabled (bm_set_profiling(1)); classes: 0 tensor, 1 digits + ModUp NTTs, 2 key switch +
- * ModDown + rescale, 3 unused, 4 rotate-and-add ladder (fused), 5 unused, 6 output INTT (s = 1).  ms[7] and
+ * ModDown + rescale, 3 unused, 4 rotate-and-add ladder (fused), 5 f2 hoisted rotation sum, 6 output
+ * INTT (s = 1).  ms[7] and
  * launches[7] accumulate until bm_profile_reset(). */
 void bm_set_profiling(int32_t on);
 void bm_profile_reset(void);

@@ -71,6 +71,9 @@ _SIGS = {
     "bm_ct_from_coeff": (_i32, [_P, _vp, _i64, _i32, _vp, _vp]),
     "bm_match_ws_bytes": (_sz, [_P, _i64, _i32, _i32]),
     "bm_match": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _i32, _vp]),
+    "bm_match_rows": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _i64, _vp, _sz, _i32, _vp]),
+    "bm_ipc_handle": (_i32, [_vp, _vp, ctypes.POINTER(_u64)]),
+    "bm_ipc_open": (_i32, [_vp, _pp]), "bm_ipc_close": (_i32, [_vp]),
     "bm_match_host_ws_bytes": (_sz, [_P, _i64, _i32, _i32]),
     "bm_match_host": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _i32, _vp]),
     "bm_set_profiling": (None, [_i32]), "bm_profile_reset": (None, []),
@@ -314,6 +317,38 @@ def bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, d_ws, order=ORDER_HOIST
     _chk(_lib.bm_match(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
                        _dptr(d_q) if nq else None, nq, _dptr(d_out) if nq * n_sets else None,
                        _dptr(d_ws) if ws_bytes else None, ws_bytes, order, _stream(stream)), "bm_match")
+
+
+def bm_match_rows(prm, evk_dev, d_db, n_sets, d_q, nq, d_rows, set_offset, d_ws, order=ORDER_HOISTED, stream=None):
+    """The scan with the gather fused into its output kernels: d_rows is a CUDA int64 tensor of nq
+    device addresses (local or peer, see bm_ipc_open); (query j, local set t) lands at row j, global
+    set set_offset + t (include/blindmatch.h)."""
+    import torch
+    assert d_rows.is_cuda and d_rows.dtype == torch.int64 and d_rows.numel() >= nq
+    ws_bytes = d_ws.numel() * d_ws.element_size()
+    _chk(_lib.bm_match_rows(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
+                            _dptr(d_q) if nq else None, nq, _dptr(d_rows), set_offset,
+                            _dptr(d_ws) if ws_bytes else None, ws_bytes, order, _stream(stream)), "bm_match_rows")
+
+
+def bm_ipc_handle(d_tensor):
+    """(64-byte CUDA IPC handle of the allocation holding d_tensor, byte offset of d_tensor in it)."""
+    h = (ctypes.c_uint8 * 64)()
+    off = _u64(0)
+    _chk(_lib.bm_ipc_handle(ctypes.c_void_p(d_tensor.data_ptr()), h, ctypes.byref(off)), "bm_ipc_handle")
+    return bytes(h), int(off.value)
+
+
+def bm_ipc_open(handle):
+    """Map a peer process's allocation: returns its base address in this process."""
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = ctypes.c_void_p()
+    _chk(_lib.bm_ipc_open(h, ctypes.byref(p)), "bm_ipc_open")
+    return int(p.value)
+
+
+def bm_ipc_close(base):
+    _chk(_lib.bm_ipc_close(ctypes.c_void_p(base)), "bm_ipc_close")
 
 
 def bm_match_host_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):

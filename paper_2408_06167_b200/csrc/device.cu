@@ -899,8 +899,9 @@ int bm_profile_read(double *ms, int64_t *launches, int64_t *units)
     return BM_OK;
 }
 
-int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
-             int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream)
+static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                      const uint64_t *d_q, int32_t nq, uint64_t *d_out, uint64_t *const *d_rows, int64_t set_offset,
+                      void *d_ws, size_t ws_bytes, int32_t order, void *stream)
 {
     if (!prm || !evk || n_sets < 0 || nq < 0 ||
         (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT))
@@ -910,7 +911,7 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     if (order == BM_ORDER_HOISTED_ROT && evk->n_hrot < prm->s - 1) return BM_ERR_MISSING_ROTATION_KEY;
     const int64_t total = n_sets * (int64_t)nq;
     if (total == 0) return BM_OK;
-    if (!d_db || !d_q || !d_out || !d_ws) return BM_ERR_INVALID_ARG;
+    if (!d_db || !d_q || (!d_out && !d_rows) || !d_ws || set_offset < 0) return BM_ERR_INVALID_ARG;
     if (ws_bytes < bm_match_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
     DevCtx *C;
     int rc = ctx_get(&C);
@@ -930,6 +931,8 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
     K.db = d_db;
     K.qry = d_q;
     K.out = d_out;
+    K.rows = d_rows;
+    K.set_off = set_offset;
     K.n_sets = n_sets;
     K.p = prm->p;
     uint64_t *ws = (uint64_t *)d_ws;
@@ -1021,6 +1024,73 @@ int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, 
         }
     }
     return rc;
+}
+
+int bm_match(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
+             int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream)
+{
+    if (!d_out && n_sets > 0 && nq > 0) return BM_ERR_INVALID_ARG;
+    return match_impl(prm, evk, d_db, n_sets, d_q, nq, d_out, nullptr, 0, d_ws, ws_bytes, order, stream);
+}
+
+int bm_match_rows(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                  const uint64_t *d_q, int32_t nq, uint64_t *const *d_rows, int64_t set_offset, void *d_ws,
+                  size_t ws_bytes, int32_t order, void *stream)
+{
+    if (!d_rows && n_sets > 0 && nq > 0) return BM_ERR_INVALID_ARG;
+    return match_impl(prm, evk, d_db, n_sets, d_q, nq, nullptr, d_rows, set_offset, d_ws, ws_bytes, order, stream);
+}
+
+int bm_ipc_handle(const void *d_ptr, uint8_t handle[64], uint64_t *offset)
+{
+    if (!d_ptr || !handle || !offset) return BM_ERR_INVALID_ARG;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, const_cast<void *>(d_ptr)) != cudaSuccess) {
+        cudaGetLastError();
+        return BM_ERR_CUDA;
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, 64);
+    // the handle names the whole allocation: d_ptr's offset inside it (driver cuMemGetAddressRange,
+    // reached through the runtime so the library does not link libcuda)
+    typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return BM_ERR_CUDA;
+        }
+        range = (range_fn)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0) return BM_ERR_CUDA;
+    *offset = (uint64_t)((uintptr_t)d_ptr - base);
+    return BM_OK;
+}
+
+int bm_ipc_open(const uint8_t handle[64], void **d_base)
+{
+    if (!handle || !d_base) return BM_ERR_INVALID_ARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    if (cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return BM_ERR_CUDA;
+    }
+    return BM_OK;
+}
+
+int bm_ipc_close(void *d_base)
+{
+    if (!d_base) return BM_ERR_INVALID_ARG;
+    if (cudaIpcCloseMemHandle(d_base) != cudaSuccess) {
+        cudaGetLastError();
+        return BM_ERR_CUDA;
+    }
+    return BM_OK;
 }
 
 // End-to-end scan from host buffers: the queries are processed in G groups.  Group g's query

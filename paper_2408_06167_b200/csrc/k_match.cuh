@@ -25,6 +25,15 @@ struct MatchK {
     int32_t cq;
     int32_t p;
     BM_D int64_t out_row(int64_t pi) const { return (jq0 + pi / ct) * n_sets + t0 + pi % ct; }
+    // bm_match_rows: query j's results go to rows[j] (possibly a peer GPU's memory) at global set
+    // set_off + t; otherwise to out [nq][n_sets][2][N]
+    uint64_t *const *rows = nullptr;
+    int64_t set_off = 0;
+    BM_D uint64_t *out_at(int64_t pi, int c) const
+    {
+        if (rows) return rows[jq0 + pi / ct] + ((set_off + t0 + pi % ct) * 2 + c) * (int64_t)N;
+        return out + (out_row(pi) * 2 + c) * (int64_t)N;
+    }
     uint64_t *D01, *D2, *XC, *XU, *ACC;
     uint64_t *XR, *XO;  // f1: level-0 masked results (NTT), rotated results (coefficients)
 };
@@ -632,7 +641,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                     a[e] = reduce_bnd<0>(v);
                 }
                 inv<0>(a, XB, K.pr[0]);
-                uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+                uint64_t *o = K.out_at(pi, c);
                 uint64_t t[E];
                 tmem_ld16(ttsc, t);
 #pragma unroll
@@ -704,7 +713,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         }
         inv<0>(a, XB, K.pr[0]);
         if (ph > 0) { // out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c
-            uint64_t *o = K.out + ((size_t)K.out_row(pi) * 2 + c) * N;
+            uint64_t *o = K.out_at(pi, c);
             uint64_t t[E];
             tmem_ld16(tA + 32 * (2 * c + 1), t);
 #pragma unroll
@@ -794,5 +803,5 @@ __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
     uint64_t a[E];
     load_eval(a, cin.at(pi, c));
     inv<0>(a, sm, K.pr[0]);
-    store_coef(K.out + ((size_t)K.out_row(pi) * 2 + c) * N, a);
+    store_coef(K.out_at(pi, c), a);
 }

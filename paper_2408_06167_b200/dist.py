@@ -7,6 +7,11 @@ Gather: query j's results go to a root rank; roots are assigned in contiguous qu
 (rank k owns queries [k nq/W, (k+1) nq/W)), so every rank is the root of the same number of
 queries and the exchange is one all_to_all over the [nq][local sets][2][N] result buffers.
 Collectives go through torch.distributed (NCCL on GPUs; gloo in the CPU tests).
+
+Fused gather (P2PGather / scan_p2p): the output kernels of the scan store every result directly
+into its root's buffer through CUDA IPC peer pointers (bm_match_rows over NVLink), so a8 overlaps
+the scan pair by pair and no result collective runs; one 8-byte all-reduce orders the roots' reads
+after every writer's scan.
 """
 import torch
 import torch.distributed as dist
@@ -122,6 +127,99 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
     cur.wait_stream(compute_stream)
     cur.wait_stream(comm_stream)
     return recv
+
+
+def p2p_row_map(nq, groups, world_size):
+    """[(root rank, row in the root's buffer)] for every query of a batch, with the roots of the
+    pipelined all_to_all (group g's queries split into W equal blocks, block k -> rank k): the root
+    holds its G nq/(G W) rows in (group, block position) order."""
+    assert nq % (groups * world_size) == 0, "nq must be a multiple of groups x world size"
+    gq = nq // groups
+    per = gq // world_size
+    out = []
+    for j in range(nq):
+        g, i = divmod(j, gq)
+        k, m = divmod(i, per)
+        out.append((k, g * per + m))
+    return out
+
+
+class P2PGather:
+    """a8 fused into the scan (bm_match_rows): `res` is this rank's root buffer
+    [nq/W][n_sets_global][2][N] (int64, CUDA, the rows of p2p_row_map); the ranks exchange CUDA IPC
+    handles of their buffers (all_gather_object) and open their peers', so `rows` holds, for every
+    query of the batch, the device address of its row on its root GPU (nq int64 on this device)."""
+
+    def __init__(self, B, res, nq, groups, n_sets_global):
+        w, r = world()
+        self.B = B
+        self.res = res
+        row_bytes = n_sets_global * 2 * B.N * 8
+        assert res.is_cuda and res.dtype == torch.int64 and res.is_contiguous()
+        assert res.numel() * 8 >= (nq // w) * row_bytes
+        self.opened = []
+        if w == 1:
+            bases = [res.data_ptr()]
+        else:
+            h, off = B.bm_ipc_handle(res)
+            allh = [None] * w
+            dist.all_gather_object(allh, (h, off))
+            bases = []
+            for k, (hk, ok) in enumerate(allh):
+                if k == r:
+                    bases.append(res.data_ptr())
+                else:
+                    b = B.bm_ipc_open(hk)
+                    self.opened.append(b)
+                    bases.append(b + ok)
+        addrs = [bases[k] + row * row_bytes for k, row in p2p_row_map(nq, groups, w)]
+        self.rows = torch.tensor(addrs, dtype=torch.int64, device=res.device)
+        self.gq = nq // groups
+
+    def rows_of(self, g):
+        return self.rows[g * self.gq:(g + 1) * self.gq]
+
+    def close(self):
+        for b in self.opened:
+            self.B.bm_ipc_close(b)
+        self.opened = []
+
+
+def scan_p2p(match_rows, d_q, gather, groups, comm_stream, compute_stream, flag):
+    """a3 + scan + fused a8: group g's broadcast runs on `comm_stream` two groups ahead while the
+    scans run on `compute_stream`; match_rows(g, q_slice, rows_slice) writes every result straight
+    to its root (gather.rows_of(g)).  `flag` (one float64 on this device) is all-reduced on the
+    compute stream after the last scan: NCCL completes it only when every rank has passed its
+    scans, so each root's buffer is complete once the call's work on the current stream is."""
+    w, _ = world()
+    nq = d_q.shape[0]
+    G = groups
+    gq = nq // G
+    qs = [d_q[g * gq:(g + 1) * gq] for g in range(G)]
+    bw = [None] * G
+
+    def bcast(g):
+        if w > 1:
+            with torch.cuda.stream(comm_stream):
+                bw[g] = dist.broadcast(qs[g], src=0, async_op=True)
+
+    compute_stream.wait_stream(torch.cuda.current_stream())
+    comm_stream.wait_stream(torch.cuda.current_stream())
+    for g in range(min(2, G)):
+        bcast(g)
+    for g in range(G):
+        with torch.cuda.stream(compute_stream):
+            if bw[g] is not None:
+                bw[g].wait()
+            match_rows(g, qs[g], gather.rows_of(g))
+        if g + 2 < G:
+            bcast(g + 2)
+    with torch.cuda.stream(compute_stream):
+        if w > 1:
+            dist.all_reduce(flag)
+    cur = torch.cuda.current_stream()
+    cur.wait_stream(compute_stream)
+    cur.wait_stream(comm_stream)
 
 
 def max_over_ranks(x, device):

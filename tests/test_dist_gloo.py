@@ -161,3 +161,65 @@ def test_two_rank_pipelined_scan_matches_single_process(tmp_path):
             for src in range(WORLD):
                 lo, cnt = pdist.shard_sets(n_sets, WORLD, src)
                 assert np.array_equal(recv[g, src, :, :cnt], ref[q0:q0 + nql, lo:lo + cnt])
+
+
+def _worker_p2p(rank, world, port, out_dir):
+    """The fused gather's data movement with the oracle as the local scan: every rank 'stores' each
+    local result at the address the output kernels use (row of p2p_row_map, global set lo + t,
+    component c: flat offset ((lo + t) * 2 + c) * N of the root's row), the stores travel to the
+    roots by all_gather_object (standing in for NVLink), and each root's buffer is saved."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    lo, cnt = pdist.shard_sets(n_sets, world, rank)
+    local_db = _encrypt_sets(O, T, pk, lo, cnt)
+    N = 1 << LOGN
+    q = torch.zeros((NQ, P_PARTS, 2, 2, N), dtype=torch.int64)
+    if rank == 0:
+        S = N // 2
+        qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+        q.copy_(torch.from_numpy(qc.reshape(q.shape).view(np.int64)))
+    pdist.broadcast_queries(q)
+    groups = 2
+    rmap = pdist.p2p_row_map(NQ, groups, world)
+    stores = []   # (root, row, flat offset in the row, values)
+    if cnt:
+        res, pairs = O.match(LOGN, D, P_PARTS, 0, rlk, gk, local_db, q.numpy().view(np.uint64))
+        for i, (j, t) in enumerate(pairs):
+            root, row = rmap[j]
+            for c in range(2):
+                stores.append((root, row, ((lo + t) * 2 + c) * N, res[i].reshape(2, N)[c].copy()))
+    allst = [None] * world
+    dist.all_gather_object(allst, stores)
+    mine = np.zeros((NQ // world, n_sets * 2 * N), np.uint64)
+    for st in allst:
+        for root, row, off, v in st:
+            if root == rank:
+                mine[row, off:off + N] = v
+    np.save(os.path.join(out_dir, f"p2p{rank}.npy"), mine)
+    dist.destroy_process_group()
+
+
+def test_two_rank_fused_gather_rows_match_single_process(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker_p2p, args=(WORLD, port, str(tmp_path)), nprocs=WORLD, join=True)
+    from paper_2408_06167_b200 import dist as pdist
+    O, T, Q, n_sets, (sk, pk, rlk, gk) = _setup()
+    N = 1 << LOGN
+    full_db = _encrypt_sets(O, T, pk, 0, n_sets)
+    S = N // 2
+    qc = O.encrypt(LOGN, pk, O.encode(O.pack_query(Q, LOGN, D, P_PARTS).reshape(-1, S), LOGN), 0, 3)
+    ref, _ = O.match(LOGN, D, P_PARTS, 0, rlk, gk, full_db, qc.reshape(NQ, P_PARTS, 2, 2, N))
+    ref = ref.reshape(NQ, n_sets * 2 * N)
+    rmap = pdist.p2p_row_map(NQ, 2, WORLD)
+    bufs = [np.load(tmp_path / f"p2p{r}.npy") for r in range(WORLD)]
+    for j, (root, row) in enumerate(rmap):
+        assert np.array_equal(bufs[root][row], ref[j])
+    # the roots are the pipelined all_to_all's: group g's block k lands on rank k
+    for g in range(2):
+        for k in range(WORLD):
+            q0, cnt = pdist.group_query_block(NQ, 2, WORLD, k, g)
+            assert all(rmap[j][0] == k for j in range(q0, q0 + cnt))
+    assert sorted(rmap) == sorted((k, i) for k in range(WORLD) for i in range(NQ // WORLD))

@@ -301,3 +301,38 @@ def test_hoisted_rotation_needs_its_keys(env, O):
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=2)
     assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+
+
+@pytest.mark.parametrize("order,chunk", [(0, None), (0, "5"), (2, None), (1, None)])
+def test_match_rows_fused_gather(env, O, monkeypatch, order, chunk):
+    """bm_match_rows (a8 fused into the output kernels, the multi-GPU gather path of dist.P2PGather):
+    results land in caller-given rows at global set numbers.  Rows in reversed order inside a wider
+    row buffer (n_sets + 3 global sets, this 'rank' at set offset 2) must hold exactly bm_match's
+    results, bit for bit, for every op order (ladder, paper order, f2's hoisted rotations; the
+    ladder, k_hrot and k_out_intt all store through the same row map), also when chunked; nothing
+    outside this rank's set range is touched."""
+    torch, B = env
+    if chunk:
+        monkeypatch.setenv("BM_CHUNK_PAIRS", chunk)
+    T = I.random_unit(700, 64, 21)
+    Q = I.random_unit(3, 64, 22)
+    st = Setup(env, O, 64, 4, T, Q, hoisted=(order == 2))   # s = 16, B = 256 -> 3 sets
+    ref = st.gpu_match(order)
+    n_glob, off = st.n_sets + 3, 2
+    res = torch.full((st.nq, n_glob, 2, 8192), -1, dtype=torch.int64, device="cuda")
+    base, row_bytes = res.data_ptr(), n_glob * 2 * 8192 * 8
+    rows = torch.tensor([base + (st.nq - 1 - j) * row_bytes for j in range(st.nq)], dtype=torch.int64,
+                        device="cuda")
+    ws = torch.empty(max(1, B.bm_match_ws_bytes(st.prm, st.n_sets, st.nq, order)), dtype=torch.uint8, device="cuda")
+    B.bm_match_rows(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q, st.nq, rows, off, ws, order)
+    B.bm_sync()
+    got = res.cpu().numpy()
+    for j in range(st.nq):
+        row = got[st.nq - 1 - j]
+        assert np.array_equal(row[off:off + st.n_sets].view(np.uint64), ref[j])
+        assert (row[:off] == -1).all() and (row[off + st.n_sets:] == -1).all()
+    # the IPC handle of the row buffer (what P2PGather exchanges) and its offset inside the allocation
+    h, o = B.bm_ipc_handle(res)
+    assert len(h) == 64 and 0 <= o < 1 << 40
+    with pytest.raises(B.BMError):
+        B.bm_match_rows(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q, st.nq, rows, -1, ws, order)
