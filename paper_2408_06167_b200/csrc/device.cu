@@ -154,8 +154,9 @@ int ctx_get(DevCtx **out)
     for (int l = 0; l < 2; l++) C->q2inv[l] = shoup_pair(powmod_d(Q2 % C->pr[l].q, C->pr[l].q - 2, C->pr[l].q), C->pr[l].q);
     C->pinv2 = shoup_pair(powmod_d(QP % Q2, Q2 - 2, Q2), Q2);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
-    cudaFuncSetAttribute(k_tensor<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
-    cudaFuncSetAttribute(k_tensor<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
@@ -837,7 +838,7 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
             const int64_t np = K.cq * K.ct;
             const unsigned npu = (unsigned)np;
             const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
-            k_tensor<3><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
+            k_tensor<3, false><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
             k_digits3<<<3 * npu, T, C1_SMEM_BYTES, s>>>(C);
             k_relin3<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
             rc = launch_check();
@@ -976,13 +977,18 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
         const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
-        const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
+        // few queries: k_tensor<2, true> puts the sets on the tile's wide (TQB) side and the queries
+        // on the TSB side -- less of the tile wasted, identical residues (the products are symmetric)
+        const bool tswap = K.cq < TQB && K.ct >= TQB;
+        const int64_t na = tswap ? K.ct : K.cq, nb = tswap ? K.cq : K.ct;
+        const unsigned ntiles = (unsigned)(((na + TQB - 1) / TQB) * ((nb + TSB - 1) / TSB) * (N / CS / TSL));
         const bool per_part = order == BM_ORDER_PAPER;
         const int n_rounds = per_part ? prm->p : 1;
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = per_part ? r : 0, hi = per_part ? r + 1 : prm->p;
             beg(0, 2 * np);
-            k_tensor<2><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+            if (tswap) k_tensor<2, true><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+            else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             end();
             beg(1, 6 * np);
             k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);

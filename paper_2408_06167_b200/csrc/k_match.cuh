@@ -147,7 +147,7 @@ BM_D uint64_t f64_mod_q1(double x)
 // NL = limbs per ciphertext (2: level 1; 3: level 2, f1), L = limb index; L = 1 (q1) runs on the FP64
 // pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe
 // stage the operands of one round (coefficient slice sl, parts i0 .. i0 + pc - 1) with cp.async
-template <int L, int NL> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st,
+template <int L, int NL, bool SW> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, uint64_t *Ss, int qt, int sl, int st,
                                                 int i0, int pc)
 {
     const int tid = threadIdx.x;
@@ -161,17 +161,17 @@ template <int L, int NL> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, u
         const int comp = row & 1, part = (row >> 1) & (pc - 1), tr = (row >> 1) >> lpc;
         const uint64_t *src;
         uint64_t *dst;
-        if (tr < TQB) {
-            int64_t a = (int64_t)qt * TQB + tr;
+        // tile row tr: a query (or, swapped, a set) on the TQB side, a set (a query) on the TSB side
+        const bool qside = (tr < TQB) != SW;
+        int64_t a = tr < TQB ? (int64_t)qt * TQB + tr : (int64_t)st * TSB + (tr - TQB);
+        if (qside) {
             a = a < K.cq ? a : K.cq - 1;
             src = K.qry + ((size_t)(K.jq0 + a) * K.p + i0 + part) * 2 * NL * N;
-            dst = Qs + ((tr * PCH + part) * 2 + comp) * CS;
         } else {
-            int64_t bb = (int64_t)st * TSB + (tr - TQB);
-            bb = bb < K.ct ? bb : K.ct - 1;
-            src = K.db + ((size_t)(K.t0 + bb) * K.p + i0 + part) * 2 * NL * N;
-            dst = Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
+            a = a < K.ct ? a : K.ct - 1;
+            src = K.db + ((size_t)(K.t0 + a) * K.p + i0 + part) * 2 * NL * N;
         }
+        dst = tr < TQB ? Qs + ((tr * PCH + part) * 2 + comp) * CS : Ss + (((tr - TQB) * PCH + part) * 2 + comp) * CS;
         cp_async16(dst + 2 * ch, src + (size_t)(NL * comp + L) * N + c0 + 2 * ch);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -181,7 +181,7 @@ template <int L, int NL> BM_D void tensor_stage(const MatchK &K, uint64_t *Qs, u
 // pipe, L = 0 (q0) and L = 2 (q2, prime index 3) on the integer pipe.  The CTA walks TSL consecutive
 // coefficient slices; the rounds (slice, chunk of PCH parts) are double-buffered: round r + 1's
 // operands are copied by cp.async while round r is computed.
-template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage, int qt, int sl0, int st, int part_lo,
+template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_t *stage, int qt, int sl0, int st, int part_lo,
                                                int part_hi)
 {
     const int tid = threadIdx.x;
@@ -194,7 +194,7 @@ template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage,
     const int n_chunks = (part_hi - part_lo + PCH - 1) / PCH;
     const int R = TSL * n_chunks;
     auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
-    tensor_stage<L, NL>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
+    tensor_stage<L, NL, SW>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
     u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
     double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
 #pragma unroll 1
@@ -203,7 +203,7 @@ template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage,
         if (r + 1 < R) {
             const int r1 = r + 1, j1 = r1 % n_chunks;
             uint64_t *b1 = stage + (size_t)(r1 & 1) * BUF;
-            tensor_stage<L, NL>(K, b1, b1 + TQB * PCH * 2 * CS, qt, sl0 + r1 / n_chunks, st, part_lo + j1 * PCH,
+            tensor_stage<L, NL, SW>(K, b1, b1 + TQB * PCH * 2 * CS, qt, sl0 + r1 / n_chunks, st, part_lo + j1 * PCH,
                                 chunk_pc(j1));
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
@@ -285,8 +285,8 @@ template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage,
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
                     const int64_t a = (int64_t)qt * TQB + 2 * su + u, bb = (int64_t)st * TSB + 2 * sv + v;
-                    if (a >= K.cq || bb >= K.ct) continue;
-                    const int64_t pi = a * K.ct + bb;
+                    if (a >= (SW ? K.ct : K.cq) || bb >= (SW ? K.cq : K.ct)) continue;
+                    const int64_t pi = SW ? bb * K.ct + a : a * K.ct + bb;
                     const int jj = sl * CS + c;
                     uint64_t d0, d2, kk;
                     if (INTL) {
@@ -307,10 +307,10 @@ template <int L, int NL> BM_D void tensor_tile(const MatchK &K, uint64_t *stage,
     }
 }
 
-template <int NL> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
+template <int NL, bool SW> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, int part_lo, int part_hi)
 {
     extern __shared__ uint64_t sm[];
-    const int nst = (int)((K.ct + TSB - 1) / TSB);
+    const int nst = (int)(((SW ? K.cq : K.ct) + TSB - 1) / TSB);
     int64_t b = blockIdx.x;
     const int l = (int)(b % NL);
     b /= NL;
@@ -318,9 +318,9 @@ template <int NL> __global__ void __launch_bounds__(TT, 2) k_tensor(MatchK K, in
     b /= nst;
     const int sg = (int)(b % (N / CS / TSL));
     const int qt = (int)(b / (N / CS / TSL));
-    if (l == 0) tensor_tile<0, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
-    else if (l == 1) tensor_tile<1, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
-    else if (NL == 3) tensor_tile<2, NL>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    if (l == 0) tensor_tile<0, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (l == 1) tensor_tile<1, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    else if (NL == 3) tensor_tile<2, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
 }
 
 // ================================================================== prime-specialised pointwise helpers

@@ -336,3 +336,25 @@ def test_match_rows_fused_gather(env, O, monkeypatch, order, chunk):
     assert len(h) == 64 and 0 <= o < 1 << 40
     with pytest.raises(B.BMError):
         B.bm_match_rows(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q, st.nq, rows, -1, ws, order)
+
+
+def test_small_query_batches_swapped_tensor_tiles(env, O):
+    """Fewer queries than the tensor tile's query side (cq < 8) with >= 8 sets run k_tensor with the
+    roles swapped (sets on the wide side; the Karatsuba products are symmetric): every query's
+    results equal those of the same query inside a full batch of 8 bit for bit, for batches of
+    1, 3 and 5 (ragged tiles on both sides), and one pair equals the oracle."""
+    torch, B = env
+    T = I.random_unit(5000, 16, 31)
+    Q = I.random_unit(8, 16, 32)
+    st = Setup(env, O, 16, 2, T, Q)          # s = 8, B = 512 -> 10 sets
+    assert st.n_sets >= 8
+    full = st.gpu_match(0)
+    for nq in (1, 3, 5):
+        for j0 in (0, 8 - nq):
+            out = torch.empty((nq, st.n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+            ws = torch.empty(B.bm_match_ws_bytes(st.prm, st.n_sets, nq, 0), dtype=torch.uint8, device="cuda")
+            B.bm_match(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q[j0:j0 + nq], nq, out, ws, 0)
+            B.bm_sync()
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), full[j0:j0 + nq]), (nq, j0)
+    ref = st.oracle_pairs([(7, 9)])
+    assert np.array_equal(full[7, 9], ref[0])
