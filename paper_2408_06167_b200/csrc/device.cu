@@ -51,6 +51,7 @@ struct DevCtx {
     ulonglong2 q2inv[2];       // f3: q2^-1 mod q0, q1
     ulonglong2 pinv2;          // f1: P^-1 mod q2
     uint64_t pmod[2];
+    int n_sm = 148;
 };
 
 std::mutex g_mu;
@@ -85,6 +86,7 @@ int ctx_get(DevCtx **out)
     }
     DevCtx *C = new DevCtx;
     C->dev = dev;
+    cudaDeviceGetAttribute(&C->n_sm, cudaDevAttrMultiProcessorCount, dev);
     std::vector<ulonglong2> h(8 * (size_t)N);
     for (int i = 0; i < 4; i++) {
         const HostPrime &H = host_prime(i);
@@ -161,6 +163,7 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_ladder_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
     cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
@@ -1005,7 +1008,11 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             rc = launch_check();
         } else if (log_s > 0 && !rc) {
             beg(4, 6 * log_s * np);
-            k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            // latency mode: fewer pairs than half the SMs -> one CTA pair (cluster) per pair
+            if (2 * np <= C->n_sm && !getenv("BM_NO_LADDER_C2"))
+                k_ladder_c2<<<2 * npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            else
+                k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
             end();
             rc = launch_check();
         }

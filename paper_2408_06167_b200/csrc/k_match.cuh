@@ -652,6 +652,121 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
     tmem_free<256>(s_tmem);
 }
 
+// ================================================================== latency mode: the ladder on a CTA pair
+// When a launch has fewer pairs than half the SMs (a single query against a small DB: the paper's
+// measurement shape), most SMs idle and the latency is one CTA's 6 transforms per step.  Here a
+// 2-CTA cluster runs one pair: cluster rank c owns component c (c_c resident in its shared memory,
+// natural order) and every step both ranks compute the digit (INTT_q0 + NTT_P of sigma_g(c1):
+// rank 0 copies c1 from rank 1's shared memory over DSMEM first) and then ONLY their own
+// component's INTT_P + NTT_q0 -- 4 transforms on the critical path per step instead of 6.
+// Same arithmetic as k_ladder (identical residues).  Cluster barriers per step: (1) c1 of the
+// previous step is complete before rank 0 copies it; (2) rank 0's copy is done before rank 1
+// overwrites c1 (split arrive / wait around the step's transforms).
+BM_D uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+BM_D void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+BM_D void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// generic address of the same shared-memory location in CTA `rank` of this cluster
+BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
+{
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    uint64_t g;
+    asm volatile("cvta.shared::cluster.u64 %0, %1;" : "=l"(g) : "l"((uint64_t)r));
+    return reinterpret_cast<const uint64_t *>(g);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T, 1) k_ladder_c2(MatchK K, CtBuf cin, int L)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *SC = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int c = (int)cluster_rank(); // this CTA's component
+    const int64_t pi = blockIdx.x >> 1;
+    __shared__ uint32_t s_tmem;
+    const uint32_t ttsc = tmem_alloc<128>(&s_tmem); // the last step's P^-1 y^c
+    const ulonglong2 pinv = K.pinv[0];
+    const int nt = nat_tid(tid);
+    stage_nat(SC, cin.at(pi, c));
+    const uint64_t *c1s = c ? SC : S1;                      // where this CTA gathers sigma(c1) from
+    const uint64_t *peer_c1 = c ? nullptr : cluster_peer(SC, 1); // rank 1's c1
+    uint64_t a[E];
+    uint32_t g = 5; // 5^(2^i) mod 2N
+#pragma unroll 1
+    for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
+        const bool last = i == L - 1;
+        const uint64_t *gq = K.gk + (size_t)(i * 4 + 2 * c) * 2 * N, *gp = gq + 2 * N; // gk[c][q0 | P]
+        cluster_arrive(); // (1) this CTA's c_c of the previous step (or its staging) is complete
+        cluster_wait();
+        if (c == 0) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(peer_c1);
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(S1);
+            for (int k = tid; k < SMEM_WORDS / 2; k += T) dst[k] = src[k];
+        }
+        cluster_arrive(); // (2) arrive: rank 0's copy of c1 is done (waited for before c1 is rewritten)
+        __syncthreads();
+        // digit: sigma_g(c1) -> INTT_q0 -> NTT_P, then this component's P-limb product
+#pragma unroll
+        for (int e = 0; e < E; e++) a[e] = c1s[nat_auto(nt, e, g)];
+        inv<0>(a, XB, K.pr[0]);
+        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P)
+#pragma unroll
+        for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live key registers)
+#pragma unroll
+            for (int e = 8 * h; e < 8 * h + 8; e += 2) {
+                ulonglong2 w, wb;
+                ldkey2(gp, pos_M4(tid, e), w, wb);
+                a[e] = shoup4<2>(a[e], w);
+                a[e + 1] = shoup4<2>(a[e + 1], wb);
+            }
+            asm volatile("" ::: "memory");
+        }
+        inv<2>(a, XB, K.pr[2]);
+#pragma unroll
+        for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0); // P^-1 y^c
+        ulonglong2 kk[2];
+        if (!last) {
+            fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), lazy [0, 2 q0)
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
+                if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                const uint64_t ks = shoup4<0>(c1s[jp], kk[e & 1]);
+                uint64_t v = ks + 2 * Q0 - a[e] + SC[j];
+                if (c == 0) v += SC[jp];
+                a[e] = reduce_bnd<0>(v);
+            }
+            cluster_wait(); // (2) wait: c1 may be rewritten now
+            __syncthreads(); // every local read of the old c_c is done
+#pragma unroll
+            for (int e = 0; e < E; e++) SC[nat_at(nt, e)] = a[e];
+        } else {
+            tmem_st16(ttsc, a);
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
+                if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                const uint64_t ks = shoup4<0>(c1s[jp], kk[e & 1]);
+                uint64_t v = ks + SC[j];
+                if (c == 0) v += SC[jp];
+                a[e] = reduce_bnd<0>(v);
+            }
+            inv<0>(a, XB, K.pr[0]);
+            uint64_t *o = K.out_at(pi, c);
+            uint64_t t[E];
+            tmem_ld16(ttsc, t);
+#pragma unroll
+            for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
+            cluster_wait(); // (2) wait: rank 1 stays resident until rank 0's last copy is done
+        }
+    }
+    tmem_free<128>(s_tmem);
+}
+
 // ================================================================== f2: hoisted rotation sum
 // SURVEY.md sec. 8f, order BM_ORDER_HOISTED_ROT -- NOT the paper's ladder (oracle: hoisted_rot_sum).
 // One CTA per pair computes out = sum_{r<s} Rot(C, r) with ONE key switch (Halevi-Shoup hoisting):

@@ -358,3 +358,24 @@ def test_small_query_batches_swapped_tensor_tiles(env, O):
             assert np.array_equal(out.cpu().numpy().view(np.uint64), full[j0:j0 + nq]), (nq, j0)
     ref = st.oracle_pairs([(7, 9)])
     assert np.array_equal(full[7, 9], ref[0])
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_latency_mode_cluster_ladder(env, O, monkeypatch, order):
+    """Launches with fewer pairs than half the SMs run the ladder on 2-CTA clusters (k_ladder_c2:
+    rank c owns component c, c1 copied over DSMEM each step): bit-identical to the one-CTA ladder
+    (BM_NO_LADDER_C2=1) and to the oracle, for the hoisted and the paper order, s = 16 (4 steps)
+    and s = 2 (the last step is the first)."""
+    torch, B = env
+    for d, p, n in ((64, 4, 600), (16, 8, 900)):
+        T = I.random_unit(n, d, 41)
+        Q = I.random_unit(2, d, 42)
+        st = Setup(env, O, d, p, T, Q)
+        assert 2 * st.nq * st.n_sets <= 148
+        got = st.gpu_match(order)
+        monkeypatch.setenv("BM_NO_LADDER_C2", "1")
+        ref_gpu = st.gpu_match(order)
+        monkeypatch.delenv("BM_NO_LADDER_C2")
+        assert np.array_equal(got, ref_gpu), (d, p)
+        ref = st.oracle_pairs([(1, st.n_sets - 1)], order)
+        assert np.array_equal(got[1, st.n_sets - 1], ref[0]), (d, p)
