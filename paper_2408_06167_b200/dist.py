@@ -161,17 +161,34 @@ class P2PGather:
         if w == 1:
             bases = [res.data_ptr()]
         else:
-            h, off = B.bm_ipc_handle(res)
+            # every step is collective and agreed on: a rank that fails still takes part, so all
+            # ranks raise together (and bench.py falls back to the NCCL gather) instead of hanging
+            try:
+                mine = B.bm_ipc_handle(res)
+            except Exception as ex:  # noqa: BLE001
+                mine = repr(ex)
             allh = [None] * w
-            dist.all_gather_object(allh, (h, off))
-            bases = []
+            dist.all_gather_object(allh, mine)
+            bad = [x for x in allh if not isinstance(x, tuple)]
+            if bad:
+                raise RuntimeError(f"CUDA IPC handle unavailable: {bad[0]}")
+            bases, err = [], None
             for k, (hk, ok) in enumerate(allh):
                 if k == r:
                     bases.append(res.data_ptr())
-                else:
+                    continue
+                try:
                     b = B.bm_ipc_open(hk)
                     self.opened.append(b)
                     bases.append(b + ok)
+                except Exception as ex:  # noqa: BLE001
+                    err = repr(ex)
+                    break
+            errs = [None] * w
+            dist.all_gather_object(errs, err)
+            if any(e is not None for e in errs):
+                self.close()
+                raise RuntimeError(f"CUDA IPC open failed: {next(e for e in errs if e is not None)}")
         addrs = [bases[k] + row * row_bytes for k, row in p2p_row_map(nq, groups, w)]
         self.rows = torch.tensor(addrs, dtype=torch.int64, device=res.device)
         self.gq = nq // groups
