@@ -144,6 +144,43 @@ def p2p_row_map(nq, groups, world_size):
     return out
 
 
+def exchange_ipc_bases(B, res, opened):
+    """CUDA IPC exchange of the ranks' root buffers: [base address of rank k's buffer in this
+    process] (this rank: res itself).  Opened peer mappings are appended to `opened`.  Every step is
+    collective and agreed on: a rank that fails still takes part, so all ranks raise together (and
+    bench.py falls back to the NCCL gather) instead of hanging in a collective."""
+    w, r = world()
+    try:
+        mine = B.bm_ipc_handle(res)
+    except Exception as ex:  # noqa: BLE001
+        mine = repr(ex)
+    allh = [None] * w
+    dist.all_gather_object(allh, mine)
+    bad = [x for x in allh if not isinstance(x, tuple)]
+    if bad:
+        raise RuntimeError(f"CUDA IPC handle unavailable: {bad[0]}")
+    bases, err = [], None
+    for k, (hk, ok) in enumerate(allh):
+        if k == r:
+            bases.append(res.data_ptr())
+            continue
+        try:
+            b = B.bm_ipc_open(hk)
+            opened.append(b)
+            bases.append(b + ok)
+        except Exception as ex:  # noqa: BLE001
+            err = repr(ex)
+            break
+    errs = [None] * w
+    dist.all_gather_object(errs, err)
+    if any(e is not None for e in errs):
+        for b in opened:
+            B.bm_ipc_close(b)
+        opened.clear()
+        raise RuntimeError(f"CUDA IPC open failed: {next(e for e in errs if e is not None)}")
+    return bases
+
+
 class P2PGather:
     """a8 fused into the scan (bm_match_rows): `res` is this rank's root buffer
     [nq/W][n_sets_global][2][N] (int64, CUDA, the rows of p2p_row_map); the ranks exchange CUDA IPC
@@ -161,34 +198,7 @@ class P2PGather:
         if w == 1:
             bases = [res.data_ptr()]
         else:
-            # every step is collective and agreed on: a rank that fails still takes part, so all
-            # ranks raise together (and bench.py falls back to the NCCL gather) instead of hanging
-            try:
-                mine = B.bm_ipc_handle(res)
-            except Exception as ex:  # noqa: BLE001
-                mine = repr(ex)
-            allh = [None] * w
-            dist.all_gather_object(allh, mine)
-            bad = [x for x in allh if not isinstance(x, tuple)]
-            if bad:
-                raise RuntimeError(f"CUDA IPC handle unavailable: {bad[0]}")
-            bases, err = [], None
-            for k, (hk, ok) in enumerate(allh):
-                if k == r:
-                    bases.append(res.data_ptr())
-                    continue
-                try:
-                    b = B.bm_ipc_open(hk)
-                    self.opened.append(b)
-                    bases.append(b + ok)
-                except Exception as ex:  # noqa: BLE001
-                    err = repr(ex)
-                    break
-            errs = [None] * w
-            dist.all_gather_object(errs, err)
-            if any(e is not None for e in errs):
-                self.close()
-                raise RuntimeError(f"CUDA IPC open failed: {next(e for e in errs if e is not None)}")
+            bases = exchange_ipc_bases(B, res, self.opened)
         addrs = [bases[k] + row * row_bytes for k, row in p2p_row_map(nq, groups, w)]
         self.rows = torch.tensor(addrs, dtype=torch.int64, device=res.device)
         self.gq = nq // groups

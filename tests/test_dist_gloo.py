@@ -223,3 +223,59 @@ def test_two_rank_fused_gather_rows_match_single_process(tmp_path):
             q0, cnt = pdist.group_query_block(NQ, 2, WORLD, k, g)
             assert all(rmap[j][0] == k for j in range(q0, q0 + cnt))
     assert sorted(rmap) == sorted((k, i) for k in range(WORLD) for i in range(NQ // WORLD))
+
+
+class _FakeIPC:
+    """Stands in for the CUDA IPC calls of the binding (no GPU here): handles name the rank's
+    buffer, opening maps rank k's buffer to a fake base 1000 (k + 1); `fail` makes one call raise."""
+
+    def __init__(self, rank, fail=None):
+        self.rank, self.fail, self.closed = rank, fail, []
+
+    def bm_ipc_handle(self, res):
+        if self.fail == ("handle", self.rank):
+            raise RuntimeError("no handle")
+        return bytes([self.rank]) * 64, 8 * self.rank
+
+    def bm_ipc_open(self, h):
+        if self.fail == ("open", self.rank):
+            raise RuntimeError("no open")
+        return 1000 * (h[0] + 1)
+
+    def bm_ipc_close(self, b):
+        self.closed.append(b)
+
+
+def _worker_ipc(rank, world, port, out_dir, fail):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_06167_b200 import dist as pdist
+    fake = _FakeIPC(rank, fail)
+    res = torch.zeros(4, dtype=torch.int64)
+    opened = []
+    try:
+        bases = pdist.exchange_ipc_bases(fake, res, opened)
+        out = ("ok", [b - (res.data_ptr() if k == rank else 0) for k, b in enumerate(bases)])
+    except RuntimeError as ex:
+        out = ("raised", str(ex), fake.closed)
+    np.save(os.path.join(out_dir, f"ipc{rank}.npy"), np.array([repr(out)]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail", [None, ("handle", 1), ("open", 0)])
+def test_ipc_exchange_agrees_across_ranks(tmp_path, fail):
+    """dist.exchange_ipc_bases: the peer bases are the opened handles plus each rank's offset, and a
+    failure on ANY rank (handle or open) makes EVERY rank raise (bench.py then falls back to the
+    NCCL gather on all ranks together) with the mappings already opened closed again."""
+    port = _free_port()
+    mp.spawn(_worker_ipc, args=(WORLD, port, str(tmp_path), fail), nprocs=WORLD, join=True)
+    outs = [eval(str(np.load(tmp_path / f"ipc{r}.npy")[0])) for r in range(WORLD)]
+    if fail is None:
+        for r, o in enumerate(outs):
+            assert o[0] == "ok"
+            assert o[1] == [0 if k == r else 1000 * (k + 1) + 8 * k for k in range(WORLD)]
+    else:
+        assert all(o[0] == "raised" for o in outs)
+        if fail[0] == "open":   # rank 1 had opened rank 0's buffer before rank 0 failed: closed again
+            assert outs[1][2] == [1000]
