@@ -16,7 +16,7 @@
 //   K5 k_out_intt (pair, c)              a8 when s = 1 (no ladder): INTT_q0 of C
 // Also here: K6 k_hrot (f2, the hoisted rotation sum), the f3/f4 kernels (query expansion and
 // server-side enrollment: k_exp_mask, k_rot1_digits, k_rot1_ks, k_enroll_add) and the f1 kernels
-// (compressed scan one level up: k_tensor<3>, k_digits3, k_relin3, k_cmp_mask, k_cmp_rot,
+// (compressed scan one level up: k_tensor<3>, k_digits3, k_relin3a/b, k_cmp_mask, k_cmp_rot,
 // k_cmp_add), encryption / conversion / key upload, and the host side of the device C ABI.
 // Memory-access conventions: NTT-domain data in the pair-coalesced M4 order,
 // twiddles in load order (tw_pos), Shoup keys planar (ldkey2).
@@ -170,7 +170,8 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_rot1_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
     cudaFuncSetAttribute(k_rot1_ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X3_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1_SMEM_BYTES);
-    cudaFuncSetAttribute(k_relin3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2_SMEM_BYTES);
+    cudaFuncSetAttribute(k_relin3a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2_SMEM_BYTES);
+    set_smem(k_relin3b);
     set_smem(k_cmp_mask);
     cudaFuncSetAttribute(k_cmp_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C4_SMEM_BYTES);
     set_smem(k_convert);
@@ -843,7 +844,8 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
             const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
             k_tensor<3, false><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
             k_digits3<<<3 * npu, T, C1_SMEM_BYTES, s>>>(C);
-            k_relin3<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
+            k_relin3a<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
+            k_relin3b<<<4 * npu, T, SMEM_BYTES, s>>>(C);
             rc = launch_check();
             for (int i = 0; i < prm->log_s && !rc; i++) {
                 X.gk = ck->gkl + (size_t)i * 12 * N;

@@ -1,6 +1,6 @@
 // k_next.cuh -- the NEXT-row kernels: f3 query expansion and f4 server-side
 // enrollment (ExpK: k_exp_mask, k_rot1_digits, k_rot1_ks, k_enroll_add), f1 compressed scan (CmpK:
-// k_digits3, k_relin3, k_cmp_mask, k_cmp_rot, k_cmp_add).
+// k_digits3, k_relin3a, k_relin3b, k_cmp_mask, k_cmp_rot, k_cmp_add).
 // Included once, by device.cu (one translation unit: the kernels are launched from its host side).
 #pragma once
 
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) k_enroll_add(const uint64_t *W, int64_t u
 // level up on the extended chain, then the compression.  Per chunk of (query, set) pairs:
 //   k_tensor<3>                        tensor + part sum over the three level-2 limbs
 //   C1 k_digits3   (pair, digit j)     x_j = INTT_{q_j}(d2[q_j]), ModUp to the other two Q primes and P
-//   C2 k_relin3    (pair, c)           KS_c over {q0,q1,q2,P} (rlk2, P^-1 in its Q limbs), ModDown fused
+//   C2 k_relin3a/b (pair, c[, l])      KS_c over {q0,q1,q2,P} (rlk2, P^-1 in its Q limbs), ModDown fused
 //                                      with Res by q2 (the R22 rewriting with q2 in q1's role): level 1
 //   ladder at level 1: log2 s x (k_rot1_digits, k_rot1_ks) with the ladder's level-1 Galois keys
 //   C3 k_cmp_mask  (pair, c)           Res_q1(Mul(P)(C, M)): level 0 (q1^-1 folded into M's q0 limb)
@@ -268,7 +268,6 @@ __global__ void __launch_bounds__(256) k_enroll_add(const uint64_t *W, int64_t u
 //   C5 k_cmp_add                        packed[g] += the s rotated results of group g
 constexpr int D2X_POLYS = 9; // XU at level 2: per digit j its 3 ModUp targets (other two Q limbs, P)
 constexpr size_t C1_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
-constexpr size_t C2_SMEM_BYTES = (SMEM_WORDS + 2 * (size_t)N) * sizeof(uint64_t);
 constexpr size_t C4_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 
 BM_D uint32_t pow5_mod2n(uint32_t r) // 5^r mod 2N
@@ -334,46 +333,57 @@ BM_D const uint64_t *digit_poly(const MatchK &K, int64_t pi, int j, int tp)
     return K.XU + ((size_t)pi * D2X_POLYS + 3 * j + k) * N;
 }
 
-// C2: key switch with rlk2 + ModDown + Res by q2, per (pair, c) (reading R28; the R22 rewriting):
-//   y = INTT_P(KS_c[P]);  U = INTT_q2(d_c[q2] + P^-1 KS_c[q2]);  R = U - P^-1 y^ (mod q2);  z^ = c_q2(R)
-//   out_c[q_l] = q2^-1 (d_c[q_l] + P^-1 KS_c[q_l] - NTT_l(P^-1 y^ + z^)),  l = 0, 1
-__global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
+// C2: key switch with rlk2 + ModDown + Res by q2 (reading R28; the R22 rewriting), in two kernels so
+// that each CTA runs at most two transform kinds (with all four in one kernel ncu's top stall was
+// no_instruction: 6.4 warps per issue -- the unrolled transforms, ~40 KB of SASS each, overflow the
+// instruction cache):
+//   C2a (pair, c):     y = INTT_P(KS_c[P]);  U = INTT_q2(d_c[q2] + P^-1 KS_c[q2]);  R = U - P^-1 y^ (mod q2)
+//                      -> y and R to the workspace (XR, XO: free until k_cmp_mask)
+//   C2b (pair, c, l):  out_c[q_l] = q2^-1 (d_c[q_l] + P^-1 KS_c[q_l] - NTT_l(P^-1 y^ + z^)), z^ = c_q2(R)
+constexpr size_t C2_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+BM_D const ulonglong2 *rlk2_key(const CmpK &C, int j, int c, int l) // rlk2 [j][c][l][N], l: 0 q0, 1 q1, 2 q2, 3 P
+{
+    return C.rlk2 + (((size_t)j * 2 + c) * 4 + l) * N;
+}
+// 8-byte keys: the w plane of a planar poly (positions pos, pos + 1); exact 128-bit inner products
+BM_D ulonglong2 rlk2_w(const ulonglong2 *k, int pos) { return ld2(reinterpret_cast<const uint64_t *>(k) + pos); }
+
+__global__ void __launch_bounds__(T, 1) k_relin3a(CmpK C)
 {
     extern __shared__ uint64_t sm[];
-    uint64_t *ys = sm + SMEM_WORDS, *zs = ys + N;
+    uint64_t *ys = sm + SMEM_WORDS;
     const MatchK &K = C.m;
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x >> 1;
     const int c = blockIdx.x & 1;
     const uint64_t *dc = K.D01 + ((size_t)pi * 6 + c * 3) * N; // d_c[q0], d_c[q1], d_c[q2]
-    // rlk2 [j][c][l][N], l: 0 q0, 1 q1, 2 q2, 3 P
-    auto key = [&](int j, int l) { return C.rlk2 + (((size_t)j * 2 + c) * 4 + l) * N; };
-    // 8-byte keys: the w plane of a planar poly (positions pos, pos + 1); exact 128-bit inner products
-    auto kw = [&](int j, int l, int pos) { return ld2(reinterpret_cast<const uint64_t *>(key(j, l)) + pos); };
+    uint64_t *yg = K.XR + ((size_t)pi * 2 + c) * N, *rg = K.XO + ((size_t)pi * 2 + c) * N; // thread-private order
     uint64_t a[E];
     // ---- P limb
     {
         const uint64_t *x0 = digit_poly(K, pi, 0, 2), *x1 = digit_poly(K, pi, 1, 2), *x2 = digit_poly(K, pi, 2, 2);
+        const ulonglong2 *r0 = rlk2_key(C, 0, c, 3), *r1 = rlk2_key(C, 1, c, 3), *r2 = rlk2_key(C, 2, c, 3);
 #pragma unroll
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos);
-            const ulonglong2 k0 = kw(0, 3, pos), k1 = kw(1, 3, pos), k2 = kw(2, 3, pos);
+            const ulonglong2 k0 = rlk2_w(r0, pos), k1 = rlk2_w(r1, pos), k2 = rlk2_w(r2, pos);
             a[e] = red128s<2>((u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x, K.pr[2].r64);
             a[e + 1] = red128s<2>((u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y, K.pr[2].r64);
         }
     }
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
-    for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // y, canonical
+    for (int e = 0; e < E; e++) ys[tid + T * e] = yg[tid + T * e] = a[e]; // y, canonical
     // ---- q2 limb
     {
         const uint64_t *x0 = digit_poly(K, pi, 0, 3), *x1 = digit_poly(K, pi, 1, 3), *x2 = digit_poly(K, pi, 2, 3);
+        const ulonglong2 *r0 = rlk2_key(C, 0, c, 2), *r1 = rlk2_key(C, 1, c, 2), *r2 = rlk2_key(C, 2, c, 2);
 #pragma unroll
         for (int e = 0; e < E; e += 2) {
             const int pos = pos_M4(tid, e);
             const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + 2 * N + pos);
-            const ulonglong2 k0 = kw(0, 2, pos), k1 = kw(1, 2, pos), k2 = kw(2, 2, pos);
+            const ulonglong2 k0 = rlk2_w(r0, pos), k1 = rlk2_w(r1, pos), k2 = rlk2_w(r2, pos);
             a[e] = reduce_bnd<3>(dd.x + red128s<3>((u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x, K.pr[3].r64));
             a[e + 1] =
                 reduce_bnd<3>(dd.y + red128s<3>((u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y, K.pr[3].r64));
@@ -384,41 +394,49 @@ __global__ void __launch_bounds__(T, 1) k_relin3(CmpK C)
     for (int e = 0; e < E; e++) {
         const uint64_t y = ys[tid + T * e];
         const uint64_t f = y > (QP >> 1) ? 1 : 0;
-        zs[tid + T * e] = reduce_bnd<3>(a[e] + f + 4 * Q2 - shoup4<3>(y, C.pinv2)); // R = U - P^-1 y^ (mod q2)
+        rg[tid + T * e] = reduce_bnd<3>(a[e] + f + 4 * Q2 - shoup4<3>(y, C.pinv2)); // R = U - P^-1 y^ (mod q2)
     }
-    // ---- q1 (FP64-pipe transform), then q0
-#pragma unroll 1
-    for (int l = 1; l >= 0; l--) {
-        const uint64_t q = l ? Q1 : Q0;
+}
+
+__global__ void __launch_bounds__(T, 1) k_relin3b(CmpK C)
+{
+    extern __shared__ uint64_t sm[];
+    const MatchK &K = C.m;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x >> 2;
+    const int c = (blockIdx.x >> 1) & 1, l = blockIdx.x & 1; // l = 1: q1 (FP64-pipe transform), 0: q0
+    const uint64_t *dc = K.D01 + ((size_t)pi * 6 + c * 3) * N;
+    const uint64_t *yg = K.XR + ((size_t)pi * 2 + c) * N, *rg = K.XO + ((size_t)pi * 2 + c) * N;
+    const uint64_t q = l ? Q1 : Q0;
+    uint64_t a[E];
 #pragma unroll
-        for (int e = 0; e < E; e++) {
-            const uint64_t y = ys[tid + T * e], R = zs[tid + T * e];
-            const uint64_t f = y > (QP >> 1) ? 1 : 0;
-            const uint64_t z = R > (Q2 >> 1) ? R + (q - Q2) : R; // z^ mod q_l
-            if (l) a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (f ? Q1 - 1 : 0) + z);
-            else a[e] = shoup4<0>(y, K.pinv[0]) + (f ? Q0 - 1 : 0) + z; // < 6 q0
-        }
-        if (l) fwd_f<1>(a, sm, K.pr[1].fwdf); // canonical
-        else fwd<0, false>(a, sm, K.pr[0]);  // [0, 2 q0)
-        const uint64_t *x0 = digit_poly(K, pi, 0, l), *x1 = digit_poly(K, pi, 1, l), *x2 = digit_poly(K, pi, 2, l);
-        uint64_t *co = K.XC + ((size_t)pi * 2 + c) * 2 * N + (size_t)l * N;
+    for (int e = 0; e < E; e++) {
+        const uint64_t y = yg[tid + T * e], R = rg[tid + T * e]; // written by the same thread index in C2a
+        const uint64_t f = y > (QP >> 1) ? 1 : 0;
+        const uint64_t z = R > (Q2 >> 1) ? R + (q - Q2) : R; // z^ mod q_l
+        if (l) a[e] = reduce_bnd<1>(shoup4<1>(y, K.pinv[1]) + (f ? Q1 - 1 : 0) + z);
+        else a[e] = shoup4<0>(y, K.pinv[0]) + (f ? Q0 - 1 : 0) + z; // < 6 q0
+    }
+    if (l) fwd_f<1>(a, sm, K.pr[1].fwdf); // canonical
+    else fwd<0, false>(a, sm, K.pr[0]);  // [0, 2 q0)
+    const uint64_t *x0 = digit_poly(K, pi, 0, l), *x1 = digit_poly(K, pi, 1, l), *x2 = digit_poly(K, pi, 2, l);
+    const ulonglong2 *r0 = rlk2_key(C, 0, c, l), *r1 = rlk2_key(C, 1, c, l), *r2 = rlk2_key(C, 2, c, l);
+    uint64_t *co = K.XC + ((size_t)pi * 2 + c) * 2 * N + (size_t)l * N;
 #pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int pos = pos_M4(tid, e);
-            const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + (size_t)l * N + pos);
-            uint64_t va, vb;
-            const ulonglong2 k0 = kw(0, l, pos), k1 = kw(1, l, pos), k2 = kw(2, l, pos);
-            const u128 sa = (u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x;
-            const u128 sb = (u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y;
-            if (l) {
-                va = dd.x + red128s<1>(sa, K.pr[1].r64) + Q1 - a[e];
-                vb = dd.y + red128s<1>(sb, K.pr[1].r64) + Q1 - a[e + 1];
-                st2(co + pos, reduce_bnd<1>(shoup4<1>(va, C.q2inv[1])), reduce_bnd<1>(shoup4<1>(vb, C.q2inv[1])));
-            } else {
-                va = dd.x + red128s<0>(sa, K.pr[0].r64) + 2 * Q0 - a[e];
-                vb = dd.y + red128s<0>(sb, K.pr[0].r64) + 2 * Q0 - a[e + 1];
-                st2(co + pos, reduce_bnd<0>(shoup4<0>(va, C.q2inv[0])), reduce_bnd<0>(shoup4<0>(vb, C.q2inv[0])));
-            }
+    for (int e = 0; e < E; e += 2) {
+        const int pos = pos_M4(tid, e);
+        const ulonglong2 u = ld2(x0 + pos), v = ld2(x1 + pos), w = ld2(x2 + pos), dd = ld2(dc + (size_t)l * N + pos);
+        const ulonglong2 k0 = rlk2_w(r0, pos), k1 = rlk2_w(r1, pos), k2 = rlk2_w(r2, pos);
+        const u128 sa = (u128)u.x * k0.x + (u128)v.x * k1.x + (u128)w.x * k2.x;
+        const u128 sb = (u128)u.y * k0.y + (u128)v.y * k1.y + (u128)w.y * k2.y;
+        if (l) {
+            const uint64_t va = dd.x + red128s<1>(sa, K.pr[1].r64) + Q1 - a[e];
+            const uint64_t vb = dd.y + red128s<1>(sb, K.pr[1].r64) + Q1 - a[e + 1];
+            st2(co + pos, reduce_bnd<1>(shoup4<1>(va, C.q2inv[1])), reduce_bnd<1>(shoup4<1>(vb, C.q2inv[1])));
+        } else {
+            const uint64_t va = dd.x + red128s<0>(sa, K.pr[0].r64) + 2 * Q0 - a[e];
+            const uint64_t vb = dd.y + red128s<0>(sb, K.pr[0].r64) + 2 * Q0 - a[e + 1];
+            st2(co + pos, reduce_bnd<0>(shoup4<0>(va, C.q2inv[0])), reduce_bnd<0>(shoup4<0>(vb, C.q2inv[0])));
         }
     }
 }
