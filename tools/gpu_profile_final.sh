@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 TAG=${TAG:-v13}
 timeout 900 python bench.py > gpurun_out/r01_bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo bench_rc=$?
-CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-f3 --no-f1 --quiet"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-f3 --no-f1 --no-single --quiet"
 $CMD > gpurun_out/plain.log 2>&1; echo plain_rc=$?
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file /tmp/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo ncu1_rc=$?
 python tools/ncu_summary.py /tmp/launches.csv gpurun_out/r01_${TAG} > /dev/null 2>&1
