@@ -139,6 +139,28 @@ def test_device_calls_fail_loudly_without_gpu(B):
     assert e.value.name == "BM_ERR_CUDA"
 
 
+def test_fused_gather_entry_points_validate_arguments(B):
+    """bm_match_rows / bm_ipc_*: argument errors are reported before any device work (callable
+    without a GPU), and the IPC calls fail with BM_ERR_CUDA, not a crash, when there is no device."""
+    import ctypes
+    import torch
+    lib = B._lib
+    prm = B.bm_params_init(16, 1)
+    P = ctypes.byref(prm)
+    one = ctypes.c_void_p(8)   # never dereferenced: the argument checks come first
+    # NULL evk, NULL row table (checked before the key digest is read)
+    assert lib.bm_match_rows(P, None, one, 1, one, 1, one, 0, one, 1, 0, None) == -1
+    assert lib.bm_match_rows(P, one, one, 1, one, 1, None, 0, one, 1, 0, None) == -1
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_uint64(0)
+    assert lib.bm_ipc_handle(None, h, ctypes.byref(off)) == -1
+    assert lib.bm_ipc_open(None, ctypes.byref(ctypes.c_void_p())) == -1
+    assert lib.bm_ipc_close(None) == -1
+    if not torch.cuda.is_available():
+        assert lib.bm_ipc_handle(one, h, ctypes.byref(off)) == -5          # BM_ERR_CUDA
+        assert lib.bm_ipc_open(h, ctypes.byref(ctypes.c_void_p())) == -5
+
+
 # ----------------------------------------------------------------------------- f3 host side
 @pytest.mark.parametrize("d,p", [(128, 8), (16, 1)])
 def test_expansion_keys_match_oracle(B, O, d, p):
