@@ -162,8 +162,8 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
-    cudaFuncSetAttribute(k_ladder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
-    cudaFuncSetAttribute(k_ladder_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
     cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
@@ -1011,10 +1011,23 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         } else if (log_s > 0 && !rc) {
             beg(4, 6 * log_s * np);
             // latency mode: fewer pairs than half the SMs -> one CTA pair (cluster) per pair
-            if (2 * np <= C->n_sm && !getenv("BM_NO_LADDER_C2"))
-                k_ladder_c2<<<2 * npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
-            else
-                k_ladder<<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            if (2 * np <= C->n_sm && !getenv("BM_NO_LADDER_C2")) {
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = 2;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3(2 * npu);
+                cfg.blockDim = dim3(T);
+                cfg.dynamicSmemBytes = LADDER_SMEM_BYTES;
+                cfg.stream = s;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                if (cudaLaunchKernelEx(&cfg, k_ladder_t<true>, K, bufC, (int)log_s) != cudaSuccess) rc = BM_ERR_CUDA;
+            } else {
+                k_ladder_t<false><<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            }
             end();
             rc = launch_check();
         }

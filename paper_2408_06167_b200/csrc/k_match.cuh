@@ -559,18 +559,48 @@ BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
 constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 
 
-__global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
+// Latency mode (k_ladder_t<true>): when a launch has fewer pairs than half the SMs (a single query
+// against a small DB: the paper's measurement shape), most SMs idle and the latency is one CTA's 6
+// transforms per step.  Launched as 2-CTA clusters, the ladder runs one pair per cluster: rank c
+// owns component c, both ranks compute the digit (INTT_q0 + NTT_P of sigma_g(c1); rank 0 copies c1
+// from rank 1's shared memory over DSMEM first) and then ONLY their own component's INTT_P +
+// NTT_q0 -- 4 transforms on the critical path per step instead of 6, identical residues.  Cluster
+// barriers per step: (1) c1 of the previous step is complete before rank 0 copies it; (2) rank 0's
+// copy is done before rank 1 overwrites c1 (split arrive / wait around the step's transforms).
+BM_D uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+BM_D void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+BM_D void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// generic address of the same shared-memory location in CTA `rank` of this cluster
+BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
+{
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    uint64_t g;
+    asm volatile("cvta.shared::cluster.u64 %0, %1;" : "=l"(g) : "l"((uint64_t)r));
+    return reinterpret_cast<const uint64_t *>(g);
+}
+
+template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, CtBuf cin, int L)
 {
     extern __shared__ uint64_t sm[];
     uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
     const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x;
+    // CL (latency mode, launched as 2-CTA clusters): rank r runs only component r; rank 0 keeps c0 in
+    // S0 and refreshes a copy of c1 in S1 from rank 1's S1 (DSMEM) every step
+    const int rank = CL ? (int)cluster_rank() : 0;
+    const int64_t pi = CL ? blockIdx.x >> 1 : blockIdx.x;
     __shared__ uint32_t s_tmem;
     const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
     const int nt = nat_tid(tid); // S0, S1 in natural order (nat_at / nat_auto: conflict-free)
-    stage_nat(S0, cin.at(pi, 0));
-    stage_nat(S1, cin.at(pi, 1));
+    if (!CL || rank == 0) stage_nat(S0, cin.at(pi, 0));
+    if (!CL || rank == 1) stage_nat(S1, cin.at(pi, 1));
+    const uint64_t *peer_c1 = CL && rank == 0 ? cluster_peer(S1, 1) : nullptr;
     uint64_t a[E];
     uint32_t g = 5; // 5^(2^i) mod 2N
 #pragma unroll 1
@@ -579,6 +609,16 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
         // [rot][c][q0|P] planar polys of 2N u64
         const uint64_t *gq0 = K.gk + (size_t)(i * 4 + 0) * 2 * N, *gp0 = gq0 + 2 * N;
         const uint64_t *gq1 = K.gk + (size_t)(i * 4 + 2) * 2 * N, *gp1 = gq1 + 2 * N;
+        if (CL) {
+            cluster_arrive(); // (1) both ranks' c_c of the previous step (or the staging) are complete
+            cluster_wait();
+            if (rank == 0) {
+                const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(peer_c1);
+                ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(S1);
+                for (int k = tid; k < SMEM_WORDS / 2; k += T) dst[k] = src[k];
+            }
+            cluster_arrive(); // (2) arrive: rank 0's copy of c1 is done (waited for before c1 is rewritten)
+        }
         __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
         // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
 #pragma unroll
@@ -586,26 +626,38 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
         inv<0>(a, XB, K.pr[0]);
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
         // P-limb key-switch products for both components; component 1's waits in the workspace
+        if (CL) { // this rank's component only
+            const uint64_t *gp = rank ? gp1 : gp0;
 #pragma unroll
-        for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live registers)
-            uint64_t k1[8];
-#pragma unroll
-            for (int e = 8 * h; e < 8 * h + 8; e += 2) {
-                const int pos = pos_M4(tid, e);
-                ulonglong2 w0, w0b, w1, w1b;
-                ldkey2(gp0, pos, w0, w0b);
-                ldkey2(gp1, pos, w1, w1b);
-                k1[e - 8 * h] = shoup4<2>(a[e], w1);
-                k1[e - 8 * h + 1] = shoup4<2>(a[e + 1], w1b);
-                a[e] = shoup4<2>(a[e], w0);
-                a[e + 1] = shoup4<2>(a[e + 1], w0b);
+            for (int e = 0; e < E; e += 2) {
+                ulonglong2 w, wb;
+                ldkey2(gp, pos_M4(tid, e), w, wb);
+                a[e] = shoup4<2>(a[e], w);
+                a[e + 1] = shoup4<2>(a[e + 1], wb);
             }
-            tmem_st8(tks1 + 16 * h, k1);
+        } else {
+#pragma unroll
+            for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live registers)
+                uint64_t k1[8];
+#pragma unroll
+                for (int e = 8 * h; e < 8 * h + 8; e += 2) {
+                    const int pos = pos_M4(tid, e);
+                    ulonglong2 w0, w0b, w1, w1b;
+                    ldkey2(gp0, pos, w0, w0b);
+                    ldkey2(gp1, pos, w1, w1b);
+                    k1[e - 8 * h] = shoup4<2>(a[e], w1);
+                    k1[e - 8 * h + 1] = shoup4<2>(a[e + 1], w1b);
+                    a[e] = shoup4<2>(a[e], w0);
+                    a[e + 1] = shoup4<2>(a[e + 1], w0b);
+                }
+                tmem_st8(tks1 + 16 * h, k1);
+            }
+            tmem_wait_st();
         }
-        tmem_wait_st();
 #pragma unroll 1
         for (int c = 0; c < 2; c++) {
-            if (c == 1) tmem_ld16(tks1, a); // component 1's P-limb product, parked in TMEM above
+            if (CL && c != rank) continue; // latency mode: this rank's component only
+            if (!CL && c == 1) tmem_ld16(tks1, a); // component 1's P-limb product, parked in TMEM above
             inv<2>(a, XB, K.pr[2]);
             // P^-1 y^c mod q0 with y^c = y - [y > P/2] P:  P^-1 y - [y > P/2], < 5 q0
 #pragma unroll
@@ -625,7 +677,8 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                     if (c == 0) v += S0[jp];           // < 7 q0
                     a[e] = reduce_bnd<0>(v);
                 }
-                __syncthreads(); // every read of the old c_c is done
+                if (CL) cluster_wait(); // (2) wait: c1 may be rewritten now
+                __syncthreads();        // every read of the old c_c is done
 #pragma unroll
                 for (int e = 0; e < E; e++) S[nat_at(nt, e)] = a[e];
             } else {
@@ -646,125 +699,11 @@ __global__ void __launch_bounds__(T, 1) k_ladder(MatchK K, CtBuf cin, int L)
                 tmem_ld16(ttsc, t);
 #pragma unroll
                 for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
+                if (CL) cluster_wait(); // (2) wait: rank 1 stays resident until rank 0's last copy is done
             }
         }
     }
     tmem_free<256>(s_tmem);
-}
-
-// ================================================================== latency mode: the ladder on a CTA pair
-// When a launch has fewer pairs than half the SMs (a single query against a small DB: the paper's
-// measurement shape), most SMs idle and the latency is one CTA's 6 transforms per step.  Here a
-// 2-CTA cluster runs one pair: cluster rank c owns component c (c_c resident in its shared memory,
-// natural order) and every step both ranks compute the digit (INTT_q0 + NTT_P of sigma_g(c1):
-// rank 0 copies c1 from rank 1's shared memory over DSMEM first) and then ONLY their own
-// component's INTT_P + NTT_q0 -- 4 transforms on the critical path per step instead of 6.
-// Same arithmetic as k_ladder (identical residues).  Cluster barriers per step: (1) c1 of the
-// previous step is complete before rank 0 copies it; (2) rank 0's copy is done before rank 1
-// overwrites c1 (split arrive / wait around the step's transforms).
-BM_D uint32_t cluster_rank()
-{
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-BM_D void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-BM_D void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-// generic address of the same shared-memory location in CTA `rank` of this cluster
-BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
-{
-    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    uint64_t g;
-    asm volatile("cvta.shared::cluster.u64 %0, %1;" : "=l"(g) : "l"((uint64_t)r));
-    return reinterpret_cast<const uint64_t *>(g);
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T, 1) k_ladder_c2(MatchK K, CtBuf cin, int L)
-{
-    extern __shared__ uint64_t sm[];
-    uint64_t *XB = sm, *SC = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
-    const int tid = threadIdx.x;
-    const int c = (int)cluster_rank(); // this CTA's component
-    const int64_t pi = blockIdx.x >> 1;
-    __shared__ uint32_t s_tmem;
-    const uint32_t ttsc = tmem_alloc<128>(&s_tmem); // the last step's P^-1 y^c
-    const ulonglong2 pinv = K.pinv[0];
-    const int nt = nat_tid(tid);
-    stage_nat(SC, cin.at(pi, c));
-    const uint64_t *c1s = c ? SC : S1;                      // where this CTA gathers sigma(c1) from
-    const uint64_t *peer_c1 = c ? nullptr : cluster_peer(SC, 1); // rank 1's c1
-    uint64_t a[E];
-    uint32_t g = 5; // 5^(2^i) mod 2N
-#pragma unroll 1
-    for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
-        const bool last = i == L - 1;
-        const uint64_t *gq = K.gk + (size_t)(i * 4 + 2 * c) * 2 * N, *gp = gq + 2 * N; // gk[c][q0 | P]
-        cluster_arrive(); // (1) this CTA's c_c of the previous step (or its staging) is complete
-        cluster_wait();
-        if (c == 0) {
-            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(peer_c1);
-            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(S1);
-            for (int k = tid; k < SMEM_WORDS / 2; k += T) dst[k] = src[k];
-        }
-        cluster_arrive(); // (2) arrive: rank 0's copy of c1 is done (waited for before c1 is rewritten)
-        __syncthreads();
-        // digit: sigma_g(c1) -> INTT_q0 -> NTT_P, then this component's P-limb product
-#pragma unroll
-        for (int e = 0; e < E; e++) a[e] = c1s[nat_auto(nt, e, g)];
-        inv<0>(a, XB, K.pr[0]);
-        fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P)
-#pragma unroll
-        for (int h = 0; h < 2; h++) { // two halves of 8 (fewer live key registers)
-#pragma unroll
-            for (int e = 8 * h; e < 8 * h + 8; e += 2) {
-                ulonglong2 w, wb;
-                ldkey2(gp, pos_M4(tid, e), w, wb);
-                a[e] = shoup4<2>(a[e], w);
-                a[e + 1] = shoup4<2>(a[e + 1], wb);
-            }
-            asm volatile("" ::: "memory");
-        }
-        inv<2>(a, XB, K.pr[2]);
-#pragma unroll
-        for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0); // P^-1 y^c
-        ulonglong2 kk[2];
-        if (!last) {
-            fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), lazy [0, 2 q0)
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
-                if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
-                const uint64_t ks = shoup4<0>(c1s[jp], kk[e & 1]);
-                uint64_t v = ks + 2 * Q0 - a[e] + SC[j];
-                if (c == 0) v += SC[jp];
-                a[e] = reduce_bnd<0>(v);
-            }
-            cluster_wait(); // (2) wait: c1 may be rewritten now
-            __syncthreads(); // every local read of the old c_c is done
-#pragma unroll
-            for (int e = 0; e < E; e++) SC[nat_at(nt, e)] = a[e];
-        } else {
-            tmem_st16(ttsc, a);
-#pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
-                if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
-                const uint64_t ks = shoup4<0>(c1s[jp], kk[e & 1]);
-                uint64_t v = ks + SC[j];
-                if (c == 0) v += SC[jp];
-                a[e] = reduce_bnd<0>(v);
-            }
-            inv<0>(a, XB, K.pr[0]);
-            uint64_t *o = K.out_at(pi, c);
-            uint64_t t[E];
-            tmem_ld16(ttsc, t);
-#pragma unroll
-            for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
-            cluster_wait(); // (2) wait: rank 1 stays resident until rank 0's last copy is done
-        }
-    }
-    tmem_free<128>(s_tmem);
 }
 
 // ================================================================== f2: hoisted rotation sum
