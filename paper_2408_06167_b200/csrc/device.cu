@@ -10,9 +10,11 @@
 //   K3 k_relin   (pair, component c)     a5+a6: KS_c = sum_j x_j rlk_j over {q0,q1,P}; ModDown fused
 //                                        with the rescale by q1 (exact, R22):
 //                                        INTT_P, INTT_q1, NTT_q0 (3 transforms) -> C_c (level 0)
-//   K4 k_ladder  (pair)                  a7+a8: the log2(s) rotate-and-add steps with C resident in
+//   K4 k_ladder_t<false> (pair)          a7+a8: the log2(s) rotate-and-add steps with C resident in
 //                                        shared memory and per-thread scratch in TMEM, 6 transforms
 //                                        per step, coefficient-domain output
+//      k_ladder_t<true> (2-CTA cluster per pair, latency mode: <= n_SM / 2 pairs): rank c runs
+//                                        component c, 4 transforms per step on the critical path
 //   K5 k_out_intt (pair, c)              a8 when s = 1 (no ladder): INTT_q0 of C
 // Also here: K6 k_hrot (f2, the hoisted rotation sum), the f3/f4 kernels (query expansion and
 // server-side enrollment: k_exp_mask, k_rot1_digits, k_rot1_ks, k_enroll_add) and the f1 kernels

@@ -1,4 +1,4 @@
-// k_match.cuh -- the bm_match kernels: K1 k_tensor, K2 k_digits, K3 k_relin, K4 k_ladder (with the
+// k_match.cuh -- the bm_match kernels: K1 k_tensor, K2 k_digits, K3 k_relin, K4 k_ladder_t (with the
 // TMEM scratch helpers), K5 k_out_intt, and f2's K6 k_hrot; the workspace layout MatchK / CtBuf.
 // Included once, by device.cu (one translation unit: the kernels are launched from its host side).
 #pragma once

@@ -362,7 +362,7 @@ def test_small_query_batches_swapped_tensor_tiles(env, O):
 
 @pytest.mark.parametrize("order", [0, 1])
 def test_latency_mode_cluster_ladder(env, O, monkeypatch, order):
-    """Launches with fewer pairs than half the SMs run the ladder on 2-CTA clusters (k_ladder_c2:
+    """Launches with fewer pairs than half the SMs run the ladder on 2-CTA clusters (k_ladder_t<true>:
     rank c owns component c, c1 copied over DSMEM each step): bit-identical to the one-CTA ladder
     (BM_NO_LADDER_C2=1) and to the oracle, for the hoisted and the paper order, s = 16 (4 steps)
     and s = 2 (the last step is the first)."""
