@@ -988,7 +988,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         // on the TSB side -- less of the tile wasted, identical residues (the products are symmetric)
         const bool tswap = K.cq < TQB && K.ct >= TQB;
         const int64_t na = tswap ? K.ct : K.cq, nb = tswap ? K.cq : K.ct;
-        const unsigned ntiles = (unsigned)(((na + TQB - 1) / TQB) * ((nb + TSB - 1) / TSB) * (N / CS / TSL));
+        const unsigned ntiles = (unsigned)(((na + TQB - 1) / TQB) * ((nb + TSB - 1) / TSB) * (N / CS / (tswap ? 1 : TSL)));
         const bool per_part = order == BM_ORDER_PAPER;
         const int n_rounds = per_part ? prm->p : 1;
         for (int r = 0; r < n_rounds && !rc; r++) {

@@ -192,7 +192,7 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
     // this thread: coefficient c, pairs (2 su + {0,1}) x (2 sv + {0,1}) of the tile
     const int c = tid & (CS - 1), su = tid >> 6, sv = (tid >> 5) & 1;
     const int n_chunks = (part_hi - part_lo + PCH - 1) / PCH;
-    const int R = TSL * n_chunks;
+    const int R = (SW ? 1 : TSL) * n_chunks; // the swapped (small-batch) tiles: one slice per CTA, more CTAs
     auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
     tensor_stage<L, NL, SW>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
     u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
@@ -316,11 +316,12 @@ template <int NL, bool SW> __global__ void __launch_bounds__(TT, 2) k_tensor(Mat
     b /= NL;
     const int st = (int)(b % nst);
     b /= nst;
-    const int sg = (int)(b % (N / CS / TSL));
-    const int qt = (int)(b / (N / CS / TSL));
-    if (l == 0) tensor_tile<0, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
-    else if (l == 1) tensor_tile<1, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
-    else if (NL == 3) tensor_tile<2, NL, SW>(K, sm, qt, sg * TSL, st, part_lo, part_hi);
+    constexpr int TS = SW ? 1 : TSL; // slices per CTA
+    const int sg = (int)(b % (N / CS / TS));
+    const int qt = (int)(b / (N / CS / TS));
+    if (l == 0) tensor_tile<0, NL, SW>(K, sm, qt, sg * TS, st, part_lo, part_hi);
+    else if (l == 1) tensor_tile<1, NL, SW>(K, sm, qt, sg * TS, st, part_lo, part_hi);
+    else if (NL == 3) tensor_tile<2, NL, SW>(K, sm, qt, sg * TS, st, part_lo, part_hi);
 }
 
 // ================================================================== prime-specialised pointwise helpers
