@@ -91,16 +91,33 @@ def hbm_bytes_per_step(p, n_sets, nq):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons DURING the timed region: NVML polled every 5 ms
+    from a thread (the timed region of a default run is ~0.15 s, shorter than one `nvidia-smi -lms`
+    start-up), falling back to `nvidia-smi -lms 100` where NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits (nvml.h): sw power cap 0x4, hw slowdown 0x8, sw thermal 0x20, hw thermal 0x40
+    REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
-        self.rows = []
+        self.rows = []          # (sm_mhz, max_mhz, set of reason names)
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -111,11 +128,38 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nvml
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = int(get_reasons(self.h))
+                self.rows.append((sm, mx, {k for k, v in self.REASON_BITS.items() if bits & v}))
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop.wait(0.005)
+
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            try:
+                self.rows.append((float(r[0]), float(r[1]),
+                                  {nm for k, nm in enumerate(names) if len(r) > 4 + k and r[4 + k].lower().startswith("active")}))
+            except (ValueError, IndexError):
+                continue
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -124,23 +168,12 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = []
-        mx = None
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            try:
-                s, m = float(r[0]), float(r[1])
-            except (ValueError, IndexError):
-                continue
-            mx = m
-            if s > 0.5 * m:          # under load
-                sm.append(s)
-            for k, nm in enumerate(names):
-                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(self.rows), "samples_under_load": len(sm)}
+        rows = list(self.rows)
+        sm = [s for s, m, _ in rows if s > 0.5 * m]    # under load
+        reasons = set().union(*[r for _, _, r in rows]) if rows else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": rows[-1][1] if rows else None,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(sm),
+                "source": "nvml (5 ms)" if self.nvml is not None else "nvidia-smi -lms 100"}
 
 
 # ----------------------------------------------------------------------------- oracle (cpu_baseline / reference)

@@ -32,7 +32,7 @@ def launches(path, out):
         if k.startswith("k_tensor<2"):  # bm_match's tensor; k_tensor<3> is f1's (level 2)
             k = "k_tensor"
         elif k.startswith("k_ladder_t<"):  # throughput ladder / latency-mode cluster ladder
-            k = "k_ladder" if "false" in k else "k_ladder_c2"
+            k = "k_ladder" if ("false" in k or "<0>" in k) else "k_ladder_c2"
         tot[k] += float(r[iV].replace(",", ""))
         cnt[k] += 1
     match = {k: v for k, v in tot.items() if k in MATCH_KERNELS}
