@@ -112,7 +112,7 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nvml = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.h = self._handle(pynvml)
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
             return self
@@ -127,6 +127,15 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
         return self
+
+    def _handle(self, nv):
+        # the CUDA device's PCI address (NVML indices ignore CUDA_VISIBLE_DEVICES), else the index
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.idx)
+            return nv.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(self.idx)
 
     def _poll(self):
         nv = self.nvml
