@@ -481,7 +481,8 @@ def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, ord
     return {"ms": round(ms, 4), "ms_std": round(statistics.pstdev(times), 4), "runs": len(times),
             "templates": n_tmpl, "templates_per_s": round(n_tmpl / (ms / 1e3), 1),
             "note": "one query vs the whole configs[1] DB: 24 (query, set) pairs, a latency-bound launch "
-                    "(latency mode: swapped tensor tiles, 2-CTA cluster ladder), device time of bm_match"}
+                    "(latency mode: small-batch tensor tiles, 3-CTA pipelined ladder), device time of bm_match, "
+                    "each run launched alone (launch latency included)"}
 
 
 def f3_modmuls(p, s):

@@ -173,9 +173,9 @@ int bm_ct_import(const bm_params *, const uint8_t *buf, size_t len, uint64_t *ct
  * Errors: BM_ERR_INVALID_ARG, BM_ERR_MISSING_ROTATION_KEY, BM_ERR_KEY_MISMATCH,
  * BM_ERR_WORKSPACE, BM_ERR_CUDA (launch errors; faults at bm_sync). nq = 0 or n_sets = 0
  * is a no-op.  Kernel choice depends only on the launch size, never on the results: chunks of
- * fewer than 8 queries use the swapped tensor tiles and launches of at most n_SM / 2 pairs run the
- * ladder on 2-CTA clusters (latency mode, e.g. one query against a small DB); the residues are
- * identical either way. */
+ * fewer than 8 queries use the swapped tensor tiles and launches of at most n_SM / 2 (n_SM / 3)
+ * pairs run the ladder on 2-CTA (3-CTA) clusters (latency mode, e.g. one query against a small DB);
+ * the residues are identical either way. */
 size_t bm_match_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);
 int bm_match(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *d_q,
              int32_t nq, uint64_t *d_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);

@@ -166,6 +166,7 @@ int ctx_get(DevCtx **out)
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_ladder_c3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
     cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
@@ -1012,21 +1013,25 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             rc = launch_check();
         } else if (log_s > 0 && !rc) {
             beg(4, 6 * log_s * np);
-            // latency mode: fewer pairs than half the SMs -> one CTA pair (cluster) per pair
+            // latency mode: at most n_SM / 2 pairs -> a 2-CTA cluster per pair (k_ladder_t<true>),
+            // at most n_SM / 3 -> the 3-rank pipelined ladder (k_ladder_c3)
+            const bool c3 = 3 * np <= C->n_sm && !getenv("BM_NO_LADDER_C3");
             if (2 * np <= C->n_sm && !getenv("BM_NO_LADDER_C2")) {
                 cudaLaunchConfig_t cfg = {};
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
-                attr[0].val.clusterDim.x = 2;
+                attr[0].val.clusterDim.x = c3 ? 3 : 2;
                 attr[0].val.clusterDim.y = 1;
                 attr[0].val.clusterDim.z = 1;
-                cfg.gridDim = dim3(2 * npu);
+                cfg.gridDim = dim3((c3 ? 3 : 2) * npu);
                 cfg.blockDim = dim3(T);
                 cfg.dynamicSmemBytes = LADDER_SMEM_BYTES;
                 cfg.stream = s;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                if (cudaLaunchKernelEx(&cfg, k_ladder_t<true>, K, bufC, (int)log_s) != cudaSuccess) rc = BM_ERR_CUDA;
+                const cudaError_t e = c3 ? cudaLaunchKernelEx(&cfg, k_ladder_c3, K, bufC, (int)log_s)
+                                         : cudaLaunchKernelEx(&cfg, k_ladder_t<true>, K, bufC, (int)log_s);
+                if (e != cudaSuccess) rc = BM_ERR_CUDA;
             } else {
                 k_ladder_t<false><<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
             }

@@ -707,6 +707,161 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
     tmem_free<256>(s_tmem);
 }
 
+// ================================================================== latency mode, 3 ranks: the pipelined ladder
+// For launches of at most n_SM / 3 pairs.  The c0 chain never feeds the c1 chain, and the c1 chain
+// can run in two domains at once (exact by linearity mod q0):
+//   c1coef_{i+1} = INTT_q0(c1_i + P^-1 sigma(c1_i) gk1[q0]) - P^-1 y^1_i,   digit_{i+1} = sigma_coef(c1coef_{i+1})
+// so a 3-CTA cluster runs one pair with two transform levels per step on the critical path (k_ladder_t:
+// 6 in one CTA, 4 on a pair):
+//   rank A: digit_i (coefficient-domain automorphism gather) -> NTT_P -> products with gk0 / gk1[P];
+//           INTT_P(XP gk1) -> t1 = P^-1 y^1 (to B)
+//   rank B: c1_i = NTT_q0(c1coef_i); w = INTT_q0(c1_i + P^-1 sigma(c1_i) gk1[q0]); c1coef_{i+1} = w - t1
+//           (to A's digit buffer; the last step's is output component 1)
+//   rank C: one level behind: INTT_P(XP gk0) -> P^-1 y^0, NTT_q0, the c0 update of k_ladder_t (sigma(c1_i)
+//           from a copy of B's c1_i); after the last step the output INTT of component 0.
+// Residues are identical to k_ladder_t (test_latency_mode_cluster_ladder).  Three cluster barriers per
+// step order the DSMEM traffic: XP gk0 (A -> C, read remotely), c1_i (B -> C copy), t1 (A -> B), c1coef (B -> A).
+__global__ void __launch_bounds__(T, 1) k_ladder_c3(MatchK K, CtBuf cin, int L)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *XB = sm, *R1 = sm + SMEM_WORDS, *R2 = sm + 2 * SMEM_WORDS; // two role buffers of SMEM_WORDS
+    const int tid = threadIdx.x;
+    const int rank = (int)cluster_rank();
+    const int64_t pi = blockIdx.x / 3;
+    const ulonglong2 pinv = K.pinv[0];
+    const int nt = nat_tid(tid);
+    __shared__ uint32_t s_tmem;
+    const uint32_t ttsc = tmem_alloc<128>(&s_tmem); // C: the last step's P^-1 y^0
+    auto csync = [] { cluster_arrive(); cluster_wait(); };
+    // A: R1 = SD (c1coef, plain coefficient order), R2 = U0 (XP gk0[P], thread-private order)
+    // B: R1 = S1 (c1_i, natural order), R2 = T1 (t1 from A, thread-private order)
+    // C: R1 = S0 (c0, natural order), R2 = S1c (copy of B's S1)
+    uint64_t a[E];
+    if (rank == 0) load_eval(a, cin.at(pi, 1)), inv<0>(a, XB, K.pr[0]);
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (rank == 0) R1[j_M1(tid, e)] = a[e];
+    if (rank == 1) stage_nat(R1, cin.at(pi, 1));
+    if (rank == 2) stage_nat(R1, cin.at(pi, 0));
+    uint64_t *peerU0 = rank == 2 ? const_cast<uint64_t *>(cluster_peer(R2, 0)) : nullptr; // A's U0
+    uint64_t *peerS1 = rank == 2 ? const_cast<uint64_t *>(cluster_peer(R1, 1)) : nullptr; // B's S1
+    uint64_t *peerT1 = rank == 0 ? const_cast<uint64_t *>(cluster_peer(R2, 1)) : nullptr; // B's T1
+    uint64_t *peerSD = rank == 1 ? const_cast<uint64_t *>(cluster_peer(R1, 0)) : nullptr; // A's SD
+    csync();
+    uint32_t g = 5, gi = 3277, gprev = 5; // 5^(2^i), its inverse mod 2N (5 * 3277 = 16385), the previous g
+#pragma unroll 1
+    for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1), gi = (gi * gi) & (2 * N - 1)) {
+        const bool last = i == L - 1;
+        const uint64_t *gq0 = K.gk + (size_t)(i * 4 + 0) * 2 * N, *gp0 = gq0 + 2 * N;
+        const uint64_t *gq1 = K.gk + (size_t)(i * 4 + 2) * 2 * N, *gp1 = gq1 + 2 * N;
+        // ---------------- level 1
+        if (rank == 0) { // digit_i = sigma_g(c1coef_i): coefficient k -> k g mod 2N, negated past N
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint32_t k0 = ((uint32_t)j_M1(tid, e) * gi) & (2 * N - 1);
+                const uint64_t x = R1[k0 & (N - 1)];
+                a[e] = k0 < (uint32_t)N ? x : (x ? Q0 - x : 0);
+            }
+            fwd<2, false>(a, XB, K.pr[2]); // XP, lazy [0, 2P)
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                const int pos = pos_M4(tid, e);
+                ulonglong2 w0, w0b, w1, w1b;
+                ldkey2(gp0, pos, w0, w0b);
+                ldkey2(gp1, pos, w1, w1b);
+                R2[tid + T * e] = shoup4<2>(a[e], w0);
+                R2[tid + T * (e + 1)] = shoup4<2>(a[e + 1], w0b);
+                a[e] = shoup4<2>(a[e], w1);
+                a[e + 1] = shoup4<2>(a[e + 1], w1b);
+            }
+        } else if (rank == 1) {
+            if (i > 0) { // c1_i = NTT_q0(c1coef_i), canonical, natural order
+                fwd<0>(a, XB, K.pr[0]);
+                __syncthreads(); // every read of the old S1 (this CTA's gathers) is done
+#pragma unroll
+                for (int e = 0; e < E; e++) R1[nat_at(nt, e)] = a[e];
+            }
+        } else if (i > 0) { // C: the c0 update of step i - 1 (a = P^-1 y^0_{i-1}, coefficient order)
+            const uint64_t *gqp = K.gk + (size_t)((i - 1) * 4 + 0) * 2 * N;
+            fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^0), lazy [0, 2 q0)
+            ulonglong2 kk[2];
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = nat_at(nt, e), jp = nat_auto(nt, e, gprev);
+                if (!(e & 1)) ldkey2(gqp, pos_M4(tid, e), kk[0], kk[1]);
+                const uint64_t ks = shoup4<0>(R2[jp], kk[e & 1]);
+                a[e] = reduce_bnd<0>(ks + 2 * Q0 - a[e] + R1[j] + R1[jp]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; e++) R1[nat_at(nt, e)] = a[e];
+        }
+        csync(); // (1) XP gk0 in A's U0, c1_i in B's S1, c0_i in C's S0
+        // ---------------- level 2
+        if (rank == 0) { // t1 = P^-1 y^1 -> B's T1
+            inv<2>(a, XB, K.pr[2]);
+#pragma unroll
+            for (int e = 0; e < E; e++)
+                peerT1[tid + T * e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0); // < 5 q0
+        } else if (rank == 1) { // w = INTT_q0(c1_i + P^-1 sigma(c1_i) gk1[q0])
+            ulonglong2 kk[2];
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
+                if (!(e & 1)) ldkey2(gq1, pos_M4(tid, e), kk[0], kk[1]);
+                a[e] = reduce_bnd<0>(shoup4<0>(R1[jp], kk[e & 1]) + R1[j]);
+            }
+            inv<0>(a, XB, K.pr[0]); // w, canonical
+        } else { // C: P^-1 y^0_i from A's XP gk0
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = peerU0[tid + T * e];
+            inv<2>(a, XB, K.pr[2]);
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0); // P^-1 y^0
+        }
+        csync(); // (2) t1 in B's T1
+        // ---------------- level 2b: c1coef_{i+1} = w - t1 (B); C copies c1_i before B overwrites it
+        if (rank == 2) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(peerS1);
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(R2);
+            for (int k = tid; k < SMEM_WORDS / 2; k += T) dst[k] = src[k];
+        }
+        if (rank == 1) {
+#pragma unroll
+            for (int e = 0; e < E; e++) a[e] = submod_d(a[e], reduce_bnd<0>(R2[tid + T * e]), Q0);
+            if (last) {
+                uint64_t *o = K.out_at(pi, 1);
+#pragma unroll
+                for (int e = 0; e < E; e++) o[j_M1(tid, e)] = a[e];
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) peerSD[j_M1(tid, e)] = a[e];
+            }
+        }
+        csync(); // (3) A's SD holds c1coef_{i+1}, C holds its copy of c1_i; every remote access is done
+        gprev = g;
+    }
+    if (rank == 2) { // output component 0: INTT_q0(c0 + sigma(c0) + P^-1 sigma(c1) gk0[q0]) - P^-1 y^0
+        const uint32_t gl = gprev;
+        const uint64_t *gq = K.gk + (size_t)((L - 1) * 4 + 0) * 2 * N;
+        tmem_st16(ttsc, a);
+        ulonglong2 kk[2];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int j = nat_at(nt, e), jp = nat_auto(nt, e, gl);
+            if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+            a[e] = reduce_bnd<0>(shoup4<0>(R2[jp], kk[e & 1]) + R1[j] + R1[jp]);
+        }
+        inv<0>(a, XB, K.pr[0]);
+        uint64_t *o = K.out_at(pi, 0);
+        uint64_t t[E];
+        tmem_ld16(ttsc, t);
+#pragma unroll
+        for (int e = 0; e < E; e++) o[j_M1(tid, e)] = submod_d(a[e], reduce_bnd<0>(t[e]), Q0);
+    }
+    tmem_free<128>(s_tmem);
+}
+
 // ================================================================== f2: hoisted rotation sum
 // SURVEY.md sec. 8f, order BM_ORDER_HOISTED_ROT -- NOT the paper's ladder (oracle: hoisted_rot_sum).
 // One CTA per pair computes out = sum_{r<s} Rot(C, r) with ONE key switch (Halevi-Shoup hoisting):

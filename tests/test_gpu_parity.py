@@ -360,13 +360,16 @@ def test_small_query_batches_swapped_tensor_tiles(env, O):
     assert np.array_equal(full[7, 9], ref[0])
 
 
-@pytest.mark.parametrize("order", [0, 1])
-def test_latency_mode_cluster_ladder(env, O, monkeypatch, order):
+@pytest.mark.parametrize("order,c3", [(0, False), (1, False), (0, True), (1, True)])
+def test_latency_mode_cluster_ladder(env, O, monkeypatch, order, c3):
     """Launches with fewer pairs than half the SMs run the ladder on 2-CTA clusters (k_ladder_t<true>:
     rank c owns component c, c1 copied over DSMEM each step): bit-identical to the one-CTA ladder
     (BM_NO_LADDER_C2=1) and to the oracle, for the hoisted and the paper order, s = 16 (4 steps)
-    and s = 2 (the last step is the first)."""
+    and s = 2 (the last step is the first); likewise the 3-rank pipelined ladder (k_ladder_c3,
+    the default at <= n_SM / 3 pairs: the c1 chain in two domains, sigma applied to coefficients)."""
     torch, B = env
+    if not c3:   # the 3-rank pipelined ladder (k_ladder_c3) is the default at <= n_SM / 3 pairs
+        monkeypatch.setenv("BM_NO_LADDER_C3", "1")
     for d, p, n in ((64, 4, 600), (16, 8, 900)):
         T = I.random_unit(n, d, 41)
         Q = I.random_unit(2, d, 42)
