@@ -319,6 +319,10 @@ def run_ours(args):
     n_chunks = G * math.ceil(n_sets * gq / min(chunk, n_sets * gq))
     rounds = p if order == 1 else 1
     launches = n_chunks * (3 * rounds + 1)
+    cp = min(chunk, n_sets * gq)                       # pairs per ladder launch
+    tail = cp % SM_COUNT
+    if prm.log_s > 0 and cp > SM_COUNT and 0 < 2 * tail <= SM_COUNT:
+        launches += n_chunks                           # the partial last wave runs on the cluster ladder
 
     # per-kernel-class device times (CUDA events on the launching stream), same step, profiled pass
     B.bm_set_profiling(True)

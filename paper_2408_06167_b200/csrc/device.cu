@@ -1014,24 +1014,36 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         } else if (log_s > 0 && !rc) {
             beg(4, 6 * log_s * np);
             // latency mode: at most n_SM / 2 pairs -> a 2-CTA cluster per pair (k_ladder_t<true>),
-            // at most n_SM / 3 -> the 3-rank pipelined ladder (k_ladder_c3)
-            const bool c3 = 3 * np <= C->n_sm && !getenv("BM_NO_LADDER_C3");
-            if (2 * np <= C->n_sm && !getenv("BM_NO_LADDER_C2")) {
+            // at most n_SM / 3 -> the 3-rank pipelined ladder (k_ladder_c3).  A large launch whose pair
+            // count is not a multiple of n_SM runs its partial last wave the same way: the one-CTA
+            // kernel takes floor(np / n_SM) full waves, the cluster kernels the remaining pairs.
+            auto cluster_ladder = [&](int64_t p0, int64_t n) {
+                const bool c3 = 3 * n <= C->n_sm && !getenv("BM_NO_LADDER_C3");
                 cudaLaunchConfig_t cfg = {};
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
                 attr[0].val.clusterDim.x = c3 ? 3 : 2;
                 attr[0].val.clusterDim.y = 1;
                 attr[0].val.clusterDim.z = 1;
-                cfg.gridDim = dim3((c3 ? 3 : 2) * npu);
+                cfg.gridDim = dim3((unsigned)((c3 ? 3 : 2) * n));
                 cfg.blockDim = dim3(T);
                 cfg.dynamicSmemBytes = LADDER_SMEM_BYTES;
                 cfg.stream = s;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                const cudaError_t e = c3 ? cudaLaunchKernelEx(&cfg, k_ladder_c3, K, bufC, (int)log_s)
-                                         : cudaLaunchKernelEx(&cfg, k_ladder_t<true>, K, bufC, (int)log_s);
+                MatchK Kt = K;
+                Kt.pair0 = p0;
+                const cudaError_t e = c3 ? cudaLaunchKernelEx(&cfg, k_ladder_c3, Kt, bufC, (int)log_s)
+                                         : cudaLaunchKernelEx(&cfg, k_ladder_t<true>, Kt, bufC, (int)log_s);
                 if (e != cudaSuccess) rc = BM_ERR_CUDA;
+            };
+            const bool use_c2 = !getenv("BM_NO_LADDER_C2");
+            const int64_t tail = np % C->n_sm;
+            if (2 * np <= C->n_sm && use_c2) {
+                cluster_ladder(0, np);
+            } else if (np > C->n_sm && 2 * tail <= C->n_sm && tail > 0 && use_c2 && !getenv("BM_NO_LADDER_TAIL")) {
+                k_ladder_t<false><<<(unsigned)(np - tail), T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+                cluster_ladder(np - tail, tail);
             } else {
                 k_ladder_t<false><<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
             }

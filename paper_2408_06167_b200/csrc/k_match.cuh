@@ -29,6 +29,7 @@ struct MatchK {
     // set_off + t; otherwise to out [nq][n_sets][2][N]
     uint64_t *const *rows = nullptr;
     int64_t set_off = 0;
+    int64_t pair0 = 0; // the ladder kernels' first pair (a launch may cover only the chunk's tail)
     BM_D uint64_t *out_at(int64_t pi, int c) const
     {
         if (rows) return rows[jq0 + pi / ct] + ((set_off + t0 + pi % ct) * 2 + c) * (int64_t)N;
@@ -594,7 +595,7 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
     // CL (latency mode, launched as 2-CTA clusters): rank r runs only component r; rank 0 keeps c0 in
     // S0 and refreshes a copy of c1 in S1 from rank 1's S1 (DSMEM) every step
     const int rank = CL ? (int)cluster_rank() : 0;
-    const int64_t pi = CL ? blockIdx.x >> 1 : blockIdx.x;
+    const int64_t pi = K.pair0 + (CL ? blockIdx.x >> 1 : blockIdx.x);
     __shared__ uint32_t s_tmem;
     const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder_c3(MatchK K, CtBuf cin, int L)
     uint64_t *XB = sm, *R1 = sm + SMEM_WORDS, *R2 = sm + 2 * SMEM_WORDS; // two role buffers of SMEM_WORDS
     const int tid = threadIdx.x;
     const int rank = (int)cluster_rank();
-    const int64_t pi = blockIdx.x / 3;
+    const int64_t pi = K.pair0 + blockIdx.x / 3;
     const ulonglong2 pinv = K.pinv[0];
     const int nt = nat_tid(tid);
     __shared__ uint32_t s_tmem;

@@ -382,3 +382,22 @@ def test_latency_mode_cluster_ladder(env, O, monkeypatch, order, c3):
         assert np.array_equal(got, ref_gpu), (d, p)
         ref = st.oracle_pairs([(1, st.n_sets - 1)], order)
         assert np.array_equal(got[1, st.n_sets - 1], ref[0]), (d, p)
+
+
+def test_ladder_tail_wave_on_clusters(env, O, monkeypatch):
+    """A launch of more than n_SM pairs whose last wave is at most half full runs that wave on the
+    cluster ladder (floor(np / n_SM) full waves on k_ladder_t<false>, the rest on k_ladder_c3 /
+    k_ladder_t<true> from pair offset MatchK::pair0): 160 pairs (tail 12) equal the one-kernel
+    launch (BM_NO_LADDER_TAIL=1) bit for bit, and a tail pair equals the oracle."""
+    torch, B = env
+    T = I.random_unit(40 * 2048, 16, 51)
+    Q = I.random_unit(4, 16, 52)
+    st = Setup(env, O, 16, 8, T, Q)          # s = 2, B = 2048 -> 40 sets x 4 queries = 160 pairs
+    assert st.n_sets * st.nq == 160
+    got = st.gpu_match(0)
+    monkeypatch.setenv("BM_NO_LADDER_TAIL", "1")
+    ref_gpu = st.gpu_match(0)
+    monkeypatch.delenv("BM_NO_LADDER_TAIL")
+    assert np.array_equal(got, ref_gpu)
+    ref = st.oracle_pairs([(3, 39)])
+    assert np.array_equal(got[3, 39], ref[0])
