@@ -302,6 +302,8 @@ def run_ours(args):
         for i in range(args.steps):
             step()
             ev[i + 1].record(stream)
+        while not ev[-1].query():   # wait without holding the GIL, so the clock sampler thread runs
+            time.sleep(0.0005)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
