@@ -265,13 +265,18 @@ BM_D void stage_by_j(uint64_t *sm, const uint64_t *p)
 }
 
 // Natural-order shared-memory storage of an NTT-domain polynomial (the resident operands of the
-// rotation kernels): NTT index j (bit-reversed evaluation order) is stored at word i + (i >> 4)
-// with i = brev13(j), the natural index of its evaluation point.  The automorphism sigma_g maps
-// natural index i to i g + (g - 1) / 2 mod N (odd g), so a warp's sigma_g gather of its M4 values
-// touches 16 consecutive (i >> 4) blocks with an odd stride: both the M4 accesses and every
-// gather are bank-conflict-free (2 wavefronts per 64-bit warp access; the j + (j >> 4) padding
-// of the exchange buffer gives 4 for M4 and 4-5 for the gathers).  j_M4's thread bits (1, 5..12)
-// and element bits (0, 2..4) are disjoint, so i = nat_tid | nat_e with nat_e a constant.
+// rotation kernels): NTT index j (bit-reversed evaluation order) is stored at word npad(i), i.e.
+// i + (i >> 4) with bank bit 0 toggled by bit 11, i = brev13(j) the natural index of its
+// evaluation point.  The
+// automorphism sigma_g maps natural index i to i g + (g - 1) / 2 mod N (odd g).  A 64-bit warp access
+// is served per half-warp (16 lanes x 8 B = one 128-byte wavefront when the lanes hit 16 distinct
+// 8-byte bank pairs): a half-warp's M4 elements differ in natural-index bits 5, 6, 7 and 11, and the
+// (i >> 4) padding spreads bits 5..7 over 8 bank pairs while the bit-11 toggle of the bank's low bit
+// separates the two halves -- so the M4 accesses AND every sigma_g gather take the minimum 2
+// wavefronts (a model over all 13 Galois elements 5^(2^k); the j + (j >> 4) padding of the exchange
+// buffer gives 4 and 6-7, plain i + (i >> 4) gives 4 and 4).  The map is a bijection onto
+// [0, N + N/16).  j_M4's thread bits (1, 5..12) and element bits (0, 2..4) are disjoint, so
+// i = nat_tid | nat_e with nat_e a constant (and bit 11 a thread bit).
 BM_HD constexpr int brev13c(int x)
 {
     int r = 0;
@@ -280,7 +285,14 @@ BM_HD constexpr int brev13c(int x)
 }
 BM_D int nat_tid(int tid) { return brev13(32 * (tid >> 1) + 2 * (tid & 1)); }
 BM_HD constexpr int nat_e(int e) { return brev13c(4 * (e >> 1) + (e & 1)); }
-BM_HD constexpr int npad(int i) { return i + (i >> 4); }
+// word(i) = pad(T) ^ bit11(T) + pad(E), T = the natural-index bits a thread owns (0..7, 11), E = the
+// element bits (8, 9, 10, 12): additive in the element part, so nat_at is a per-thread base plus
+// an immediate offset (an XOR after the sum cost the ladder 2% in address arithmetic)
+BM_HD constexpr int npad(int i)
+{
+    const int t = i & 0x8FF, e = i & 0x1700;
+    return ((t + (t >> 4)) ^ ((t >> 11) & 1)) + (e + (e >> 4));
+}
 // word of this thread's element e (M4) / of the element sigma_g moves there
 BM_D int nat_at(int ntid, int e) { return npad(ntid) + npad(nat_e(e)); }
 BM_D int nat_auto_i(uint32_t i, uint32_t g) { return npad((int)((i * g + ((g - 1) >> 1)) & (N - 1))); }
