@@ -1,22 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the encrypted 1:N cosine scan (HE-C^3) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--p P] [--order 0|1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C] [--p P]
 
-Workload (N = 1): BASELINE.json configs[1] -- d = 128, 6,144 unit-norm Gaussian templates
-(stand-ins for the paper's IJB-C ArcFace embeddings), 384 genuine queries
-(1 per 16 templates), p = 8 parts (best of the configs[1] sweep), CKKS N = 8192.
-One step = the whole hot path for the whole query batch: bm_match of 384 queries x 24 sets
-(tensor + part sum, relinearise, rescale, 4 rotate-and-add steps, coefficient-domain output);
-for N > 1 also the query broadcast and the result gather (NCCL).  N > 1 is weak scaling: every
-rank holds its own 6,144-template shard (global DB = 6,144 N templates).
-Metric: encrypted templates matched per second = templates x queries / s (BASELINE.json).
+Workloads (--config C = SURVEY.md sec. 8d C1..C5 = BASELINE.json configs[C-1]; default C = 4):
+  C4 (the metric's own configuration, BASELINE.json "d=128, N=8192 at 1/2/4/8 B200"): 1,048,576
+     unit-norm Gaussian templates (stand-ins for IJB-C ArcFace embeddings), d = 128,
+     p = 8 (the best of the C2 sweep), 256 queries (128 genuine + 128 impostor), the database
+     STRONG-scaled over the N GPUs (rank r owns the contiguous sets dist.shard_sets(4096, N, r),
+     encrypted with their global object numbers and one shared seed: a bit-exact partition of the
+     1-GPU database).  Results (128 KiB per (query, set) pair, 128 GiB per batch) stream through a
+     bounded device ring (--ring-gib, overwritten), the paper's cluster setting.
+  C2: 6,144 templates, 384 genuine queries, p in {1,2,4,8};  C3: d = 32, 65,536 clustered templates,
+  64 queries, p in {1,2,4};  C5: d = 512, 4,194,304 templates, 1,024 queries, p in {4,8,16} (at N < 8
+  --shard-of 8 runs rank 0's shard of the 8-GPU split: a labelled 1-GPU prefix);  C1: d = 16, one set.
+One step = the whole hot path for the whole query batch: bm_match of every (query, set) pair of
+this rank (tensor + part sum, relinearise, rescale, log2(s) rotate-and-add steps, coefficient-
+domain output) in query groups of ~16K pairs alternating two streams, plus for N > 1 the query
+broadcast (a3) and the result gather (a8, fused into the output kernels as NVLink peer stores).
+Metric: encrypted templates matched per second = templates x queries / s, all ranks (BASELINE.json).
+
+After the timed region the same step runs once more, untimed, with every result decrypted on the
+device (bm_decrypt_dev) and checked: max |score - float64 cosine|, top-1 agreement with the
+plaintext argmax, and a sample of >= 32 pairs (spread over query groups, sets and the last set)
+compared bit for bit with the CPU oracle (oracle/, which also re-encrypts those sets and queries).
 
 --impl reference runs the CPU oracle (oracle/, plain C) on the host cores on a bounded sample of
 the same workload (this tier has no reference implementation).
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -29,16 +43,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = 2
-D = 128
 N_RING = 8192
 BFLY = (N_RING // 2) * 13          # butterflies (= modmuls) per 8192-point transform
-SM_COUNT = 148
-IMAD_PER_CLK_SM = 64               # FMA pipe, 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
+IMAD_PER_CLK_SM = 64               # FMA-heavy pipe, 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
 # FMA-pipe issue slots (in IMAD units) of the cheapest 64-bit Shoup modmul a w mod q: 4 IMAD (low
 # words) + 3 IMAD.WIDE + 2 IMAD.HI, the wide / high forms at half the IMAD rate (measured 25-29 vs
 # 63 lanes/clk/SM, tools/pipe_bench.cu, profiles/r01_pipe_bench.txt): 4 + 2 x 5 = 14
 IMAD_SLOTS_PER_MODMUL = 14
+METRIC = "encrypted templates matched/sec (d=128, N=8192)"
 
 
 def parse():
@@ -47,19 +59,25 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--p", type=int, default=8)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="SURVEY.md sec. 8d C1..C5 = BASELINE.json configs[0..4]")
+    ap.add_argument("--p", type=int, default=None, help="parts (default: the config's)")
+    ap.add_argument("--nq", type=int, default=None, help="queries per batch (default: the config's)")
     ap.add_argument("--order", type=int, default=0)
-    ap.add_argument("--no-f3", action="store_true", help="skip the f3 query-expansion / f4 enrollment leg")
-    ap.add_argument("--no-f1", action="store_true", help="skip the f1 compressed-scan leg")
-    ap.add_argument("--no-single", action="store_true", help="skip the single-query latency leg")
-    ap.add_argument("--no-f4", action="store_true", help="skip the f4 enrollment part of the f3 leg")
-    ap.add_argument("--nq", type=int, default=384)
-    ap.add_argument("--groups", type=int, default=4, help="query groups overlapping comms and scans (N > 1)")
+    ap.add_argument("--shard-of", type=int, default=None,
+                    help="run rank r's shard of an S-way split (C5 default at N < 8: 8, a labelled prefix)")
+    ap.add_argument("--ring-gib", type=float, default=4.0, help="device result ring (bounded outputs)")
+    ap.add_argument("--chunk", type=int, default=16384, help="pairs per query group / bm_match chunk")
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1 result gather (a8): p2p = fused into the output kernels (bm_match_rows storing "
                          "to the roots over NVLink), nccl = all_to_all after each group's scan")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--oracle-pairs", type=int, default=48)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single", action="store_true", help="skip the single-query latency leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row legs (f1, f3, f4 on configs[1])")
     ap.add_argument("--quiet", action="store_true")
     return ap.parse_args()
 
@@ -89,11 +107,15 @@ def hbm_bytes_per_step(p, n_sets, nq):
     return n_sets * p * 4 * N_RING * 8 + nq * p * 4 * N_RING * 8 + nq * n_sets * 2 * N_RING * 8
 
 
+def int_peak_gmodmul(n_sm, f_hz):
+    """Derived integer roofline: n_SM x 64 IMAD/clk x f / 14 IMAD slots per modmul."""
+    return n_sm * IMAD_PER_CLK_SM * f_hz / IMAD_SLOTS_PER_MODMUL / 1e9
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons DURING the timed region: NVML polled every 5 ms
-    from a thread (the timed region of a default run is ~0.15 s, shorter than one `nvidia-smi -lms`
-    start-up), falling back to `nvidia-smi -lms 100` where NVML is unavailable."""
+    from a thread, falling back to `nvidia-smi -lms 100` where NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -185,27 +207,64 @@ class ClockSampler:
                 "source": "nvml (5 ms)" if self.nvml is not None else "nvidia-smi -lms 100"}
 
 
+# ----------------------------------------------------------------------------- workload
+class Workload:
+    """The (config, p) workload and this rank's share of it."""
+
+    def __init__(self, cfg, p, nq, world, rank, shard_of, chunk):
+        from paper_2408_06167_b200 import dist as pdist
+        from paper_2408_06167_b200 import inputs as I
+        c = I.CONFIGS[cfg]
+        self.cfg, self.d, self.n = cfg, c["d"], c["n"]
+        self.p = p or c["p"]
+        self.nq = nq or c["nq"]
+        s = self.d // self.p
+        self.B = 4096 // s
+        self.n_sets = -(-self.n // self.B)
+        self.split = shard_of or world                    # the DB split this run executes a share of
+        self.rank_in_split = rank
+        self.lo, self.n_local = pdist.shard_sets(self.n_sets, self.split, rank)
+        self.tmpl_lo = self.lo * self.B
+        self.n_tmpl_local = max(0, min(self.n, (self.lo + self.n_local) * self.B) - self.tmpl_lo)
+        # query groups: ~chunk pairs each; for N > 1 a group splits evenly over the ranks (roots)
+        want = max(1, chunk // max(1, self.n_local))
+        if world > 1:
+            cands = [g for g in range(world, self.nq + 1, world) if self.nq % g == 0]
+            assert cands, "nq must be a multiple of the world size"
+            self.gq = max([g for g in cands if g <= max(want, world)] or [cands[0]])
+        else:
+            self.gq = min(self.nq, want)
+        self.G = -(-self.nq // self.gq)
+
+    def label(self):
+        lab = f"BASELINE configs[{self.cfg - 1}]: d={self.d}, {self.n} templates, {self.nq} queries, p={self.p}"
+        if self.split > 1:
+            lab += f", DB split over {self.split} GPUs ({self.n_local} of {self.n_sets} sets on this rank)"
+        return lab
+
+
 # ----------------------------------------------------------------------------- oracle (cpu_baseline / reference)
-def oracle_sample(p, seconds_target, n_threads, log=None):
-    """Time the CPU oracle on a bounded sample of (query, set) pairs of the bench workload."""
+def oracle_sample(cfg, d, p, seconds_target, n_threads):
+    """Time the CPU oracle on a bounded sample of (query, set) pairs of the workload (two sets of the
+    config's templates, two of its queries, cycled)."""
     from oracle import oracle as O
     from paper_2408_06167_b200 import inputs as I
     logN = 13
-    S, s, B = O.layout(logN, D, p)
-    sk, pk, rlk, gk = O.keygen(logN, 1, O.n_rot_for(D, p))
-    T = I.templates(CFG, 2 * B)            # two full sets
-    Q, _ = I.queries(CFG, 2)
-    db = O.encrypt(logN, pk, O.encode(O.pack_db(T, logN, D, p, 0, 2).reshape(-1, S), logN), 0, 2).reshape(2, p, 2, 2, -1)
-    qc = O.encrypt(logN, pk, O.encode(O.pack_query(Q, logN, D, p).reshape(-1, S), logN), 0, 3).reshape(2, p, 2, 2, -1)
+    S, s, B = O.layout(logN, d, p)
+    sk, pk, rlk, gk = O.keygen(logN, 1, O.n_rot_for(d, p))
+    T = I.templates(cfg, 2 * B)            # two full sets
+    Q = I.random_unit(2, d, 7) if cfg != 2 else I.queries(cfg, 2)[0]
+    db = O.encrypt(logN, pk, O.encode(O.pack_db(T, logN, d, p, 0, 2).reshape(-1, S), logN), 0, 2).reshape(2, p, 2, 2, -1)
+    qc = O.encrypt(logN, pk, O.encode(O.pack_query(Q, logN, d, p).reshape(-1, S), logN), 0, 3).reshape(2, p, 2, 2, -1)
     t0 = time.perf_counter()
-    O.match(logN, D, p, 0, rlk, gk, db, qc, pairs=np.array([[0, 0]], np.int64), n_threads=1)
+    O.match(logN, d, p, 0, rlk, gk, db, qc, pairs=np.array([[0, 0]], np.int64), n_threads=1)
     t1 = time.perf_counter() - t0
     n_pairs = int(max(n_threads, min(4096, round(seconds_target * n_threads / max(t1, 1e-3)))))
     pairs = np.array([(k % 2, (k // 2) % 2) for k in range(n_pairs)], np.int64)
 
     def run():
         t = time.perf_counter()
-        O.match(logN, D, p, 0, rlk, gk, db, qc, pairs=pairs, n_threads=n_threads)
+        O.match(logN, d, p, 0, rlk, gk, db, qc, pairs=pairs, n_threads=n_threads)
         return time.perf_counter() - t
     return run, n_pairs, B, t1
 
@@ -233,232 +292,193 @@ def run_ours(args):
         dist.barrier()
     from paper_2408_06167_b200 import bm as B
 
-    p, nq, order = args.p, args.nq, args.order
-    prm = B.bm_params_init(D, p)
-    n_tmpl = I.CONFIGS[CFG]["n"]                     # per rank (weak scaling)
-    n_sets = -(-n_tmpl // prm.B)
+    shard_of = args.shard_of if args.shard_of else (8 if args.config == 5 and world < 8 else None)
+    if shard_of is not None and world > 1 and shard_of != world:
+        raise SystemExit("--shard-of applies to single-GPU prefix runs only")
+    W = Workload(args.config, args.p, args.nq, world, rank, shard_of, args.chunk)
+    p, nq, order, d = W.p, W.nq, args.order, W.d
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    prm = B.bm_params_init(d, p)
+    t_setup = time.perf_counter()
     sk, pk, evk = B.bm_keygen(prm, 1)                # deterministic: identical keys on every rank
     if order == 2:                                   # f2 hoisted rotation sum: keys of every rotation
         B.bm_evk_add_hoisted(prm, 1, evk)
     pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
-    T = I.templates(CFG, n_tmpl, rank * n_tmpl)
-    d_db = torch.empty((n_sets, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
-    B.bm_encrypt_db(prm, pk_dev, T, 0, n_sets, 2 + rank, d_db)
-    d_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    n_local = W.n_local
+    T_local = I.templates(W.cfg, W.n_tmpl_local, W.tmpl_lo)
+    d_db = torch.empty((n_local, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    # global set numbers and one seed: every rank's shard is a bit-exact slice of the 1-GPU database
+    B.bm_encrypt_db(prm, pk_dev, T_local, 0, n_local, 2, d_db) if n_local else None
+    Q, genuine = I.queries(W.cfg, nq)
+    d_q = torch.zeros((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
     if rank == 0:
-        Q, _ = I.queries(CFG, nq)
         B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
-    d_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
-    # N > 1: broadcast (a3) and scan overlapped over query groups; the result gather (a8) either fused
-    # into the scan's output kernels (p2p: every result stored straight into its root's buffer over
-    # NVLink, dist.P2PGather) or an all_to_all after each group's scan (nccl)
-    G = args.groups if world > 1 else 1
-    gq = nq // G
-    ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, gq, order), dtype=torch.uint8, device=dev)
-    comm_s, comp_s = (torch.cuda.Stream(), torch.cuda.Stream()) if world > 1 else (None, None)
-    gather, gat, recv, flag = "local", None, None, None
+    B.bm_sync()
+    t_setup = time.perf_counter() - t_setup
+    # bounded outputs: a ring of R group slots (R even: group g and g + R share a stream)
+    B.bm_set_option("chunk_pairs", max(1, min(args.chunk, W.gq * n_local)))
+    nstr = args.streams
+    row_bytes = n_local * 2 * N_RING * 8
+    slot_bytes = W.gq * row_bytes
+    R = max(2, int(args.ring_gib * 2**30 // max(1, slot_bytes)) // 2 * 2)
+    R = min(R, W.G + (W.G % 2))
+    ws = [torch.empty(max(1, B.bm_match_ws_bytes(prm, n_local, W.gq, order)), dtype=torch.uint8, device=dev)
+          for _ in range(nstr)]
+    streams = [torch.cuda.Stream() for _ in range(nstr)]
+    comm_s = torch.cuda.Stream() if world > 1 else None
+    gather, gat, flag, ring, recv = "local ring", None, None, None, None
     if world > 1 and args.gather == "p2p":
-        res = torch.empty((nq // world, n_sets * world, 2, N_RING), dtype=torch.int64, device=dev)
+        n_root = R * (W.gq // world)
+        res = torch.empty((n_root, W.n_sets, 2, N_RING), dtype=torch.int64, device=dev)
         try:
-            gat = pdist.P2PGather(B, res, nq, G, n_sets * world)
+            gat = pdist.P2PGather(B, res, nq, W.G, W.n_sets, ring=R)
             flag = torch.zeros(1, dtype=torch.float64, device=dev)
-            gather = "p2p: fused into the output kernels (bm_match_rows, CUDA IPC peer stores over NVLink)"
+            gather = "p2p: fused into the output kernels (bm_match_rows, CUDA IPC peer stores over NVLink), root ring"
         except Exception as ex:  # noqa: BLE001 -- a transport fallback (NCCL), never a CPU one
             del res
             gather = f"nccl all_to_all (p2p unavailable: {type(ex).__name__}: {ex})"[:200]
-    if world > 1 and gat is None:
-        recv = torch.empty((G, world, gq // world, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
-        if gather == "local":
-            gather = "nccl all_to_all per query group"
-    B.bm_sync()
-    stream = torch.cuda.current_stream()
+    if gat is None:
+        ring = [torch.empty((W.gq, n_local, 2, N_RING), dtype=torch.int64, device=dev) for _ in range(R)]
+        if world > 1:
+            recv = [torch.empty((world, W.gq // world, n_local, 2, N_RING), dtype=torch.int64, device=dev)
+                    for _ in range(R)]
+            if gather == "local ring":
+                gather = "nccl all_to_all per query group"
+    log(args, f"[rank {rank}] setup {t_setup:.1f} s: {W.label()}; {n_local} local sets x {nq} queries, "
+              f"{W.G} groups of {W.gq}, ring {R} x {slot_bytes / 2**30:.2f} GiB, ws {nstr} x {ws[0].numel() / 2**30:.2f} GiB")
+    main = torch.cuda.current_stream()
 
-    def match(g, q_g, out_g):
-        B.bm_match(prm, evk_dev, d_db, n_sets, q_g, q_g.shape[0], out_g, ws, order)
-
-    def match_rows(g, q_g, rows_g):
-        B.bm_match_rows(prm, evk_dev, d_db, n_sets, q_g, q_g.shape[0], rows_g, rank * n_sets, ws, order)
+    def groups():
+        for g in range(W.G):
+            q0 = g * W.gq
+            yield g, q0, min(W.gq, nq - q0)
 
     def step():
         if world == 1:
-            B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, order)
+            for s in streams:
+                s.wait_stream(main)
+            for g, q0, n in groups():
+                i = g % nstr
+                B.bm_match(prm, evk_dev, d_db, n_local, d_q[q0:q0 + n], n, ring[g % R][:n], ws[i], order,
+                           stream=streams[i])
+            for s in streams:
+                main.wait_stream(s)
         elif gat is not None:
-            pdist.scan_p2p(match_rows, d_q, gat, G, comm_s, comp_s, flag)
+            def match_rows(g, q_g, rows_g):
+                i = g % nstr
+                B.bm_match_rows(prm, evk_dev, d_db, n_local, q_g, q_g.shape[0], rows_g, W.lo, ws[i], order,
+                                stream=torch.cuda.current_stream())
+            pdist.scan_p2p(match_rows, d_q, gat, W.G, comm_s, streams, flag)
         else:
-            pdist.scan_pipelined(match, d_q, d_out, recv, G, comm_s, comp_s)
+            def match(g, q_g, out_g):
+                B.bm_match(prm, evk_dev, d_db, n_local, q_g, q_g.shape[0], out_g, ws[0], order,
+                           stream=torch.cuda.current_stream())
+            pdist.scan_pipelined(match, d_q, ring, recv, W.G, comm_s, streams[0])
 
-    log(args, f"[rank {rank}] setup done: {n_sets} sets x {nq} queries, p={p}, ws={ws.numel() / 2**30:.2f} GiB")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    B.bm_launch_count_reset()
     # events at every step boundary (recorded on the launching stream, no synchronisation between
     # steps): the first and last bracket the timed region, the others give the per-step spread
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        ev[0].record(stream)
+        ev[0].record(main)
         for i in range(args.steps):
             step()
-            ev[i + 1].record(stream)
+            ev[i + 1].record(main)
         while not ev[-1].query():   # wait without holding the GIL, so the clock sampler thread runs
             time.sleep(0.0005)
         torch.cuda.synchronize()
+    launches = B.bm_launch_count()
     if world > 1:
         dist.barrier()
     ms = pdist.max_over_ranks(ev[0].elapsed_time(ev[-1]), dev)
     ms_step = ms / args.steps
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     ms_std = float(statistics.pstdev(per_step)) if len(per_step) > 1 else 0.0
-    tq_per_step = world * n_tmpl * nq
+    n_tmpl_job = W.n if W.split == world else W.n_tmpl_local   # templates all ranks of THIS run scan
+    tq_per_step = n_tmpl_job * nq
     value = tq_per_step / (ms_step / 1e3)
-
-    # launches of our kernels per step: chunks x (3 per part-round + 1 fused ladder (or output INTT if s = 1))
-    import math
-    total_pairs = n_sets * nq
-    chunk = int(os.environ.get("BM_CHUNK_PAIRS", "16384"))
-    n_chunks = G * math.ceil(n_sets * gq / min(chunk, n_sets * gq))
-    rounds = p if order == 1 else 1
-    launches = n_chunks * (3 * rounds + 1)
-    cp = min(chunk, n_sets * gq)                       # pairs per ladder launch
-    tail = cp % SM_COUNT
-    if prm.log_s > 0 and cp > SM_COUNT and 0 < 2 * tail <= SM_COUNT:
-        launches += n_chunks                           # the partial last wave runs on the cluster ladder
-
-    # per-kernel-class device times (CUDA events on the launching stream), same step, profiled pass
-    B.bm_set_profiling(True)
-    B.bm_profile_reset()
-    for _ in range(args.steps):
-        for g in range(G):
-            B.bm_match(prm, evk_dev, d_db, n_sets, d_q[g * gq:(g + 1) * gq], gq, d_out[g * gq:(g + 1) * gq], ws, order)
-    B.bm_sync()
-    pms, pla, pun = B.bm_profile_read()
-    B.bm_set_profiling(False)
-    mm = class_modmuls(1 if order == 1 else p, prm.log_s)  # order 1 runs the part rounds one part each
-    classes = B.PROFILE_CLASSES
-    per_class = {}
-    step_work = 0.0   # algorithmic modmuls of one step: the classes that ran
-    for i, c in enumerate(classes):
-        if pla[i]:
-            work = mm[c] * total_pairs * args.steps * (rounds if i < 3 else 1)
-            step_work += work / args.steps
-            per_class[c] = {"ms_per_step": pms[i] / args.steps, "launches": int(pla[i]),
-                            "gmodmul_s": work / (pms[i] / 1e3) / 1e9}
-    dom = max(per_class, key=lambda c: per_class[c]["ms_per_step"])
     clocks = clk.summary()
-    f_peak = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = SM_COUNT * IMAD_PER_CLK_SM * f_peak / IMAD_SLOTS_PER_MODMUL / 1e9  # Gmodmul/s
-    ach = per_class[dom]["gmodmul_s"]
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(dom)
-    hbm_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6548.8
-    hbm_achieved = hbm_bytes_per_step(p, n_sets, nq) / (ms_step / 1e3) / 1e9
-    roofline = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2),
-                "unit": "Gmodmul/s", "frac": round(ach / peak, 4), "traffic": traffic,
-                "peak_basis": f"{SM_COUNT} SMs x {IMAD_PER_CLK_SM} IMAD/clk x {f_peak / 1e6:.0f} MHz / "
-                              f"{IMAD_SLOTS_PER_MODMUL} IMAD issue slots per 64-bit Shoup modmul "
-                              f"(4 IMAD + 3 IMAD.WIDE + 2 IMAD.HI at half rate)",
-                "step_gmodmul_s": round(step_work / (ms_step / 1e3) / 1e9, 2),
-                "step_frac": round(step_work / (ms_step / 1e3) / 1e9 / peak, 4),
-                "hbm": {"achieved_gbs": round(hbm_achieved, 2), "peak_gbs": hbm_gbs,
-                        "frac": round(hbm_achieved / hbm_gbs, 5)},
-                "per_class": {c: {k: round(v, 3) for k, v in d.items()} for c, d in per_class.items()}}
 
-    if gat is not None:   # fused gather: this rank's own sets in the rows it roots equal its local scan
-        torch.cuda.synchronize()
-        for j, (root, row) in enumerate(pdist.p2p_row_map(nq, G, world)):
-            if root == rank:
-                assert torch.equal(gat.res[row, rank * n_sets:(rank + 1) * n_sets], d_out[j]), "p2p gather"
+    # per-kernel-class device times (the library's CUDA events around every launch, on its launching
+    # stream), a separate profiled pass of the same step on one stream
+    roofline = profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws, W, order, n_sm, clocks,
+                            ms_step, groups)
 
-    # single-query latency (the paper's shape: ONE query against the whole DB,
-    # PAPER.md:572-574): bm_match of query 0 over all sets, device time, 3 warm-ups + 10 timed runs
+    verify = None
+    if not args.no_verify:
+        try:
+            verify = run_verify(args, B, torch, prm, sk, pk, evk_dev, d_db, d_q, Q, genuine, T_local, W, ring, gat,
+                                ws, order, world, rank, dev)
+        except Exception as ex:  # noqa: BLE001 -- recorded, and the line says parity failed
+            import traceback
+            traceback.print_exc()
+            verify = {"error": f"{type(ex).__name__}: {ex}"[:300], "parity": "error"}
+
     single = None
     if world == 1 and not args.no_single:
-        single = run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, order, stream)
+        single = run_single(B, torch, prm, evk_dev, d_db, n_local, W.n_tmpl_local, d_q, ring, ws[0], order, main)
 
-    # e2e through the C ABI with host buffers (query H2D + result D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        h_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64).pin_memory()
-        if world > 1:
-            pdist.broadcast_queries(d_q)
-        h_q.copy_(d_q)
-        h_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64).pin_memory()
-        del ws
-        torch.cuda.empty_cache()
-        ws2 = torch.empty(B.bm_match_host_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
-        B.bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, ws2, order)
-        k2 = max(1, args.steps)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(k2):
-            B.bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, ws2, order)
-        torch.cuda.synchronize()
-        e2e_ms = pdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / k2, dev)
-        # correctness spot check of the e2e output against the device path
-        assert torch.equal(h_out[0, 0], d_out[0, 0].cpu())
-        e2e = {"value": round(tq_per_step / (e2e_ms / 1e3), 1), "unit": "templates*queries/s",
-               "h2d_bytes_per_step": int(h_q.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
-               "ms_per_step": round(e2e_ms, 3), "note": "per rank: query cts H2D + results D2H, wall clock"}
+        e2e = run_e2e(args, B, torch, prm, evk_dev, d_db, n_local, d_q, W, order, dev, world, tq_per_step)
 
-    # f3: server-side query expansion (Algorithm 1) of the same batch -- the client
-    # uploads ONE level-2 ciphertext per query (the chain extended by q2) and bm_expand produces the p
-    # level-1 parts bm_match takes.  Device time of the expansion alone and of expansion + scan.
-    # (the NEXT-row legs never take the headline line down with them: a failure is recorded instead)
-    f3 = None
-    if world == 1 and not args.no_f3:
-        try:
-            f3 = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_step, tq_per_step, stream)
-        except Exception as ex:  # noqa: BLE001
-            f3 = {"error": f"{type(ex).__name__}: {ex}"}
-            log(args, f"[rank {rank}] f3/f4 leg failed: {f3['error']}")
-    # f1: the compressed scan of the same workload one level up (level-2 DB and
-    # queries), packed outputs s times smaller with the partial sums masked away
-    f1 = None
-    if world == 1 and not args.no_f1:
-        ws = None   # the scan's workspace (already released when the e2e leg ran)
+    extras = {}
+    if world == 1 and not args.no_extras and args.config in (2, 4) and order == 0:
+        del ring, ws
         torch.cuda.empty_cache()
         try:
-            f1 = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stream)
+            extras = run_extras(args, B, torch, dev, main)
         except Exception as ex:  # noqa: BLE001
-            f1 = {"error": f"{type(ex).__name__}: {ex}"}
-            log(args, f"[rank {rank}] f1 leg failed: {f1['error']}")
+            extras = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            log(args, f"[rank {rank}] extras failed: {extras['error']}")
         torch.cuda.empty_cache()
 
-    # CPU oracle on the host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
-        run, n_pairs, Bk, t1 = oracle_sample(p, 12.0, nth)
+        run, n_pairs, Bk, t1 = oracle_sample(W.cfg, d, p, 12.0, nth)
         secs = run()
         cpu = {"value": round(n_pairs * Bk / secs, 2), "unit": "templates*queries/s", "cores": nth, "kind": "oracle",
-               "sample": f"{n_pairs} (query, set) pairs of the bench workload (p={p}, {Bk} templates each), "
-                         f"{nth} threads, {secs:.1f} s wall; single pair {t1:.2f} s on 1 thread"}
+               "sample": f"{n_pairs} (query, set) pairs of the {W.label().split(':')[0]} workload (d={d}, p={p}, {Bk} "
+                         f"templates each), {nth} threads, {secs:.1f} s wall; single pair {t1:.2f} s on 1 thread"}
 
     if rank == 0:
+        hbm_bytes = hbm_bytes_per_step(p, W.n_sets if W.split == world else n_local, nq)
+        hbm_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6548.8
+        roofline["hbm"] = {"achieved_gbs": round(hbm_bytes / (ms_step / 1e3) / 1e9, 2), "peak_gbs": hbm_gbs,
+                           "frac": round(hbm_bytes / (ms_step / 1e3) / 1e9 / hbm_gbs, 5),
+                           "algorithmic_bytes_per_step": hbm_bytes}
+        scaling = "strong" if W.split == world and world > 1 else "weak"
         line = {
-            "metric": "encrypted templates matched/sec (d=128, N=8192)", "value": round(value, 1),
+            "metric": METRIC, "value": round(value, 1),
             "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "ms_per_step_std": round(ms_std, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u64", "data": "synthetic (seeded unit-norm Gaussian templates, genuine noisy queries)",
-            "config": {"workload": f"BASELINE configs[1]: d=128, {n_tmpl} templates/GPU, {nq} queries, p={p}, "
-                                   f"order={['hoisted', 'paper', 'hoisted-rotations (f2, not the paper ladder)'][order]}",
-                       "d": D, "p": p, "templates_per_gpu": n_tmpl, "sets_per_gpu": n_sets, "queries": nq,
-                       "ring_N": N_RING, "parallelism": f"db-shard{world}", "gather": gather,
-                       "l2": "inputs > L2: query cts %.0f MB + DB %.0f MB per step (126 MB L2), no flush" % (
-                           nq * p * 4 * N_RING * 8 / 1e6, n_sets * p * 4 * N_RING * 8 / 1e6)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "single_query": single,
-            "f3_expand": f3, "f1_compressed": f1,
-            "gpu_launches": int(launches * args.steps),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (seeded unit-norm Gaussian templates, genuine noisy queries + impostors)",
+            "config": {"workload": W.label() + (f"; 1-GPU prefix: rank 0's shard of the {W.split}-GPU split"
+                                                 if W.split > world else ""),
+                       "d": d, "p": p, "templates": W.n, "templates_this_run": n_tmpl_job, "queries": nq,
+                       "sets": W.n_sets, "sets_per_gpu": n_local, "ring_N": N_RING,
+                       "order": ["hoisted", "paper", "hoisted-rotations (f2, not the paper ladder)"][order],
+                       "parallelism": f"db-shard{world}", "gather": gather,
+                       "query_groups": W.G, "group_queries": W.gq, "streams": nstr,
+                       "output_ring": {"slots": R, "slot_bytes": slot_bytes},
+                       "l2": "inputs > L2: DB %.0f MB + queries %.0f MB per step, results %.0f MB written (126 MB L2), "
+                             "no flush" % (n_local * p * 4 * N_RING * 8 / 1e6, nq * p * 4 * N_RING * 8 / 1e6,
+                                           nq * n_local * 2 * N_RING * 8 / 1e6)},
+            "roofline": roofline, "verify": verify, "cpu_baseline": cpu, "e2e": e2e, "single_query": single,
+            "gpu_launches": int(launches),
             "clocks": clocks,
+            "setup_s": round(t_setup, 1),
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if gat is not None:
         dist.barrier()
@@ -467,11 +487,230 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, order, stream):
-    """Latency of ONE query against the whole DB (the paper's measurement shape, PAPER.md:572-574:
-    6,144 templates at d = 128 in 0.45 s on 6 CPU cores): bm_match of query 0 over all n_sets sets,
-    CUDA events on the launching stream, 3 warm-ups then 10 timed runs (10 trials)."""
-    q1, o1 = d_q[:1], d_out[:1]
+def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws, W, order, n_sm, clocks, ms_step,
+                 groups):
+    """Per-kernel-class device times: the library records CUDA events around each launch on its
+    launching stream (bm_set_profiling); one stream, min(steps, 2) steps of the same work."""
+    nsteps = max(1, min(args.steps, 2))
+    B.bm_set_profiling(True)
+    B.bm_profile_reset()
+    out = ring[0] if ring is not None else torch.empty((W.gq, n_local, 2, N_RING), dtype=torch.int64,
+                                                       device=d_db.device)
+    for _ in range(nsteps):
+        for g, q0, n in groups():
+            B.bm_match(prm, evk_dev, d_db, n_local, d_q[q0:q0 + n], n, out[:n], ws[0], order)
+    B.bm_sync()
+    pms, pla, pun = B.bm_profile_read()
+    B.bm_set_profiling(False)
+    p = W.p
+    mm = class_modmuls(1 if order == 1 else p, prm.log_s)  # order 1 runs the part rounds one part each
+    rounds = p if order == 1 else 1
+    pairs = n_local * W.nq
+    per_class, step_work = {}, 0.0
+    for i, c in enumerate(B.PROFILE_CLASSES):
+        if pla[i]:
+            work = mm[c] * pairs * nsteps * (rounds if i < 3 else 1)
+            step_work += work / nsteps
+            per_class[c] = {"ms_per_step": pms[i] / nsteps, "launches": int(pla[i]),
+                            "ms_per_launch": pms[i] / pla[i], "gmodmul_s": work / (pms[i] / 1e3) / 1e9,
+                            "modmul_per_launch": work / pla[i]}
+    dom = max(per_class, key=lambda c: per_class[c]["ms_per_step"])
+    f_peak = (clocks["sm_max_mhz"] or 1965.0) * 1e6
+    peak = int_peak_gmodmul(n_sm, f_peak)
+    ach = per_class[dom]["gmodmul_s"]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        traffic = tj.get(f"C{W.cfg}", {}).get(dom) if f"C{W.cfg}" in tj else tj.get(dom)
+    measured = None
+    mfile = os.path.join(ROOT, "profiles", "modmul_peak.json")
+    if os.path.exists(mfile):
+        mj = json.load(open(mfile))
+        measured = {"peak": mj["gmodmul_s"], "frac": round(ach / mj["gmodmul_s"], 4), "basis": mj["basis"]}
+    return {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2),
+            "unit": "Gmodmul/s", "frac": round(ach / peak, 4), "traffic": traffic,
+            "achieved_basis": f"{dom}: algorithmic modmuls per launch ({per_class[dom]['modmul_per_launch']:.4g}, "
+                              f"DESIGN.md sec. 3) / mean launch duration ({per_class[dom]['ms_per_launch']:.3f} ms, CUDA "
+                              f"events on the launching stream, profiled pass)",
+            "peak_basis": f"{n_sm} SMs x {IMAD_PER_CLK_SM} IMAD/clk x {f_peak / 1e6:.0f} MHz / "
+                          f"{IMAD_SLOTS_PER_MODMUL} IMAD issue slots per 64-bit Shoup modmul "
+                          f"(4 IMAD + 3 IMAD.WIDE + 2 IMAD.HI at half rate)",
+            "peak_measured": measured,
+            "step_gmodmul_s": round(step_work / (ms_step / 1e3) / 1e9, 2),
+            "step_frac": round(step_work / (ms_step / 1e3) / 1e9 / peak, 4),
+            "per_class": {c: {k: round(v, 4) for k, v in d.items()} for c, d in per_class.items()}}
+
+
+def pick_pairs(W, n, seed=5):
+    """>= n (query, GLOBAL set) pairs of this rank spread over query groups, sets, both ends and the
+    last set (ragged when the templates do not fill it)."""
+    rng = np.random.default_rng(seed)
+    lo, nl, nq = W.lo, W.n_local, W.nq
+    if nl == 0:
+        return []
+    pairs = {(0, lo), (nq - 1, lo + nl - 1), (min(W.gq, nq - 1), lo), (W.gq - 1, lo + nl - 1),
+             (nq // 2, lo + nl // 2)}
+    for g in range(W.G):                         # one pair per query group at least
+        pairs.add((min(nq - 1, g * W.gq + int(rng.integers(W.gq))), lo + int(rng.integers(nl))))
+        if len(pairs) >= n:
+            break
+    while len(pairs) < n:
+        pairs.add((int(rng.integers(nq)), lo + int(rng.integers(nl))))
+    return sorted(pairs)
+
+
+def run_verify(args, B, torch, prm, sk, pk, evk_dev, d_db, d_q, Q, genuine, T_local, W, ring, gat, ws, order, world,
+               rank, dev):
+    """One more (untimed) pass of the step with every result decrypted on the device and checked:
+    scores vs float64 cosine, top-1 vs the plaintext argmax, and sampled pairs bit for bit vs the
+    CPU oracle (which re-encrypts their sets and queries from the product's integer plaintexts)."""
+    from paper_2408_06167_b200 import dist as pdist
+    t0 = time.perf_counter()
+    n_local, nq, Bk = W.n_local, W.nq, W.B
+    nt = W.n_tmpl_local
+    if nt == 0:
+        return {"note": "no local sets"}
+    sk_dev = B.bm_sk_to_device(prm, sk)
+    Tt = torch.from_numpy(np.ascontiguousarray(T_local)).to(dev)
+    Qd = torch.from_numpy(np.ascontiguousarray(Q)).to(dev)
+    Qd = Qd / Qd.norm(dim=1, keepdim=True)
+    max_err = torch.zeros((), dtype=torch.float64, device=dev)
+    dec_top = torch.empty(nq, dtype=torch.int64, device=dev)
+    pt_top = torch.empty(nq, dtype=torch.int64, device=dev)
+    gap = torch.empty(nq, dtype=torch.float64, device=dev)
+    sample = pick_pairs(W, args.oracle_pairs)
+    got = {}
+    out = ring[0] if ring is not None else torch.empty((W.gq, n_local, 2, N_RING), dtype=torch.int64, device=dev)
+    scores = torch.empty((W.gq * n_local, Bk), dtype=torch.float64, device=dev)
+    for g in range(W.G):
+        q0 = g * W.gq
+        n = min(W.gq, nq - q0)
+        B.bm_match(prm, evk_dev, d_db, n_local, d_q[q0:q0 + n], n, out[:n], ws[0], order)
+        B.bm_decrypt_dev(prm, sk_dev, out[:n], scores[:n * n_local])
+        sc = scores[:n * n_local].view(n, n_local * Bk)[:, :nt]
+        cos = Qd[q0:q0 + n] @ Tt.T
+        max_err = torch.maximum(max_err, (sc - cos).abs().max())
+        dec_top[q0:q0 + n] = sc.argmax(dim=1)
+        top2 = cos.topk(min(2, nt), dim=1)
+        pt_top[q0:q0 + n] = top2.indices[:, 0]
+        gap[q0:q0 + n] = (top2.values[:, 0] - top2.values[:, -1]) if nt > 1 else 1.0
+        for j, t in sample:
+            if q0 <= j < q0 + n:
+                got[(j, t)] = out[j - q0, t - W.lo].cpu().numpy().view(np.uint64).copy()
+    torch.cuda.synchronize()
+    dec_top, pt_top, gap = dec_top.cpu().numpy(), pt_top.cpu().numpy(), gap.cpu().numpy()
+    gen = np.asarray(genuine)
+    is_gen = gen >= 0
+    in_shard = is_gen & (gen >= W.tmpl_lo) & (gen < W.tmpl_lo + nt)
+    ties = gap < 1e-5
+    agree = dec_top == pt_top
+    res = {
+        "max_abs_score_err": float(max_err.item()),
+        "scores_checked": int(nq * nt),
+        "top1_agree_all": float(agree.mean()),
+        "top1_agree_genuine": float(agree[is_gen].mean()) if is_gen.any() else None,
+        "genuine_queries": int(is_gen.sum()),
+        "genuine_top1_is_enrolled_template": (float((dec_top[in_shard] + W.tmpl_lo == gen[in_shard]).mean())
+                                              if in_shard.any() else None),
+        "near_ties_flagged": int(ties.sum()),
+        "tolerance": 1e-4,
+    }
+    # ---- oracle parity on the sampled pairs (rank-local sets)
+    from oracle import oracle as O
+    logN, d, p = 13, W.d, W.p
+    osk, opk, orlk, ogk = O.keygen(logN, 1, O.n_rot_for(d, p))
+    if order == 2:
+        ogk = O.keygen_hoisted(logN, 1, d // p)
+    sets = sorted({t for _, t in sample})
+    qs = sorted({j for j, _ in sample})
+    si = {t: k for k, t in enumerate(sets)}
+    qi = {j: k for k, j in enumerate(qs)}
+    db_c = torch.empty((len(sets), p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    for k, t in enumerate(sets):
+        db_c[k] = d_db[t - W.lo]
+    B.bm_ct_to_coeff(prm, db_c, 2, db_c)
+    q_c = torch.stack([d_q[j] for j in qs]).contiguous()
+    B.bm_ct_to_coeff(prm, q_c, 2, q_c)
+    torch.cuda.synchronize()
+    db_h = db_c.cpu().numpy().view(np.uint64)
+    q_h = q_c.cpu().numpy().view(np.uint64)
+    # a1 / a2: the oracle's encryption of the product's integer plaintexts == the device ciphertexts
+    enc_ok = True
+    for k, t in enumerate(sets):
+        pt = B.bm_encode_db(prm, T_local, t - W.lo, 1).reshape(p, N_RING)
+        enc_ok &= bool(np.array_equal(O.encrypt(logN, opk, pt, t * p, 2).reshape(p, 2, 2, -1), db_h[k]))
+    for k, j in enumerate(qs):
+        pt = B.bm_encode_query(prm, Q[j:j + 1]).reshape(p, N_RING)
+        enc_ok &= bool(np.array_equal(O.encrypt(logN, opk, pt, j * p, 3).reshape(p, 2, 2, -1), q_h[k]))
+    local = np.array([(qi[j], si[t]) for j, t in sample], np.int64)
+    ref, _ = O.match(logN, d, p, order, orlk, ogk, db_h, q_h, pairs=local, n_threads=os.cpu_count() or 1)
+    ref = ref.reshape(-1, 2, N_RING)
+    bad = [k for k, jt in enumerate(sample) if not np.array_equal(got[jt], ref[k])]
+    res.update({"parity": "bit-exact" if not bad and enc_ok else "MISMATCH",
+                "oracle_pairs": len(sample), "oracle_pairs_mismatched": len(bad),
+                "encrypt_parity": enc_ok,
+                "oracle_pairs_spread": f"{len(qs)} queries x {len(sets)} sets incl. (0, first), (last, last), every "
+                                       f"query group ({W.G}), the last set"})
+    if world > 1 and gat is not None:
+        res["gather_parity"] = gather_check(B, torch, prm, pk, evk_dev, d_db, d_q, W, gat, ws, order, world, rank, dev)
+    res["verify_s"] = round(time.perf_counter() - t0, 1)
+    ok = (res["parity"] == "bit-exact" and res["max_abs_score_err"] <= 1e-4
+          and (res["top1_agree_genuine"] in (None, 1.0)))
+    res["ok"] = bool(ok)
+    return res
+
+
+def gather_check(B, torch, prm, pk, evk_dev, d_db, d_q, W, gat, ws, order, world, rank, dev):
+    """N > 1: group 0's scan with the fused gather (peers store into the roots' rows); each root then
+    encrypts 2 sets owned by other ranks itself (global object numbers: identical ciphertexts),
+    scans them for its rows' queries and compares bit for bit with what the peers stored."""
+    import torch.distributed as dist
+    from paper_2408_06167_b200 import dist as pdist
+    from paper_2408_06167_b200 import inputs as I
+    B.bm_match_rows(prm, evk_dev, d_db, W.n_local, d_q[:W.gq], W.gq, gat.rows_of(0), W.lo, ws[0], order)
+    torch.cuda.synchronize()
+    dist.barrier()
+    rmap = pdist.p2p_row_map(W.nq, W.G, world, gat.ring)
+    mine = [(j, row) for j, (root, row) in enumerate(rmap[:W.gq]) if root == rank]
+    foreign = []
+    for src in range(world):
+        lo, cnt = pdist.shard_sets(W.n_sets, world, src)
+        if src != rank and cnt and len(foreign) < 2:
+            foreign.append(lo + cnt - 1)
+    pk_dev = B.bm_pk_to_device(prm, pk)
+    n_ok = n_all = 0
+    js = [j for j, _ in mine]
+    for t in foreign:
+        T = I.templates(W.cfg, min(W.B, W.n - t * W.B), t * W.B)
+        db1 = torch.empty((1, W.p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+        encrypt_set(B, prm, pk_dev, T, t, db1)
+        qq = torch.stack([d_q[j] for j in js]).contiguous()
+        out = torch.empty((len(js), 1, 2, N_RING), dtype=torch.int64, device=dev)
+        wsl = torch.empty(B.bm_match_ws_bytes(prm, 1, len(js), order), dtype=torch.uint8, device=dev)
+        B.bm_match(prm, evk_dev, db1, 1, qq, len(js), out, wsl, order)
+        torch.cuda.synchronize()
+        for k, (j, row) in enumerate(mine):
+            n_all += 1
+            n_ok += int(torch.equal(gat.res[row, t], out[k, 0]))
+    return {"pairs_checked": n_all, "pairs_equal": n_ok, "ok": n_all > 0 and n_ok == n_all}
+
+
+def encrypt_set(B, prm, pk_dev, T, t, out):
+    """encrypt global set t alone (object numbers t p + i, seed 2), as its owner did"""
+    import torch
+    pt = torch.from_numpy(B.bm_encode_db(prm, T, 0, 1).reshape(-1, N_RING)).to(out.device)
+    B.bm_encrypt(prm, pk_dev, pt, t * prm.p, 2, out)
+    B.bm_sync()
+
+
+def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, ring, ws, order, stream):
+    """Latency of ONE query against the whole (local) DB (the paper's measurement shape,
+    PAPER.md:572-574: 6,144 templates at d = 128 in 0.45 s on 6 CPU cores): bm_match of query 0
+    over all sets, CUDA events on the launching stream, 3 warm-ups then 10 timed runs."""
+    q1 = d_q[:1]
+    o1 = ring[0][:1] if ring is not None else torch.empty((1, n_sets, 2, N_RING), dtype=torch.int64,
+                                                          device=d_q.device)
     for _ in range(3):
         B.bm_match(prm, evk_dev, d_db, n_sets, q1, 1, o1, ws, order)
     torch.cuda.synchronize()
@@ -484,8 +723,6 @@ def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, ord
         b.synchronize()
         times.append(a.elapsed_time(b))
     ms = statistics.mean(times)
-    # the same call captured once in a CUDA graph and replayed alone (a server answering one query:
-    # the four launches become one graph launch)
     graph = None
     try:
         cg = torch.cuda.CUDAGraph()
@@ -506,9 +743,96 @@ def run_single(B, torch, prm, evk_dev, d_db, n_sets, n_tmpl, d_q, d_out, ws, ord
         graph = {"error": f"{type(ex).__name__}: {ex}"[:160]}
     return {"ms": round(ms, 4), "ms_std": round(statistics.pstdev(times), 4), "runs": len(times), "cuda_graph": graph,
             "templates": n_tmpl, "templates_per_s": round(n_tmpl / (ms / 1e3), 1),
-            "note": "one query vs the whole configs[1] DB: 24 (query, set) pairs, a latency-bound launch "
-                    "(latency mode: small-batch tensor tiles, 3-CTA pipelined ladder), device time of bm_match, "
-                    "each run launched alone (launch latency included)"}
+            "note": f"one query vs the whole local DB ({n_sets} (query, set) pairs), device time of bm_match, each "
+                    f"run launched alone (launch latency included)"}
+
+
+def run_e2e(args, B, torch, prm, evk_dev, d_db, n_local, d_q, W, order, dev, world, tq_per_step):
+    """The same scan end to end through the C ABI from HOST buffers: bm_match_host_ring (pinned query
+    upload and result download inside the call, results streamed through a bounded pinned host ring)."""
+    import torch.distributed as dist
+    from paper_2408_06167_b200 import dist as pdist
+    nq, p = W.nq, W.p
+    if world > 1:
+        pdist.broadcast_queries(d_q)
+    h_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64).pin_memory()
+    h_q.copy_(d_q)
+    row_bytes = n_local * 2 * N_RING * 8
+    ring_rows = int(max(1, min(nq, (args.ring_gib * 2**30) // max(1, row_bytes))))
+    h_ring = torch.empty((ring_rows, n_local, 2, N_RING), dtype=torch.int64).pin_memory()
+    torch.cuda.empty_cache()
+    ws2 = torch.empty(B.bm_match_host_ws_bytes(prm, n_local, nq, order), dtype=torch.uint8, device=dev)
+    B.bm_match_host_ring(prm, evk_dev, d_db, n_local, h_q, nq, h_ring, ring_rows, ws2, order)
+    k2 = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k2):
+        B.bm_match_host_ring(prm, evk_dev, d_db, n_local, h_q, nq, h_ring, ring_rows, ws2, order)
+    torch.cuda.synchronize()
+    e2e_ms = pdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / k2, dev)
+    # the last query's row (ring row (nq - 1) mod ring_rows) == a device scan of that query
+    chk = torch.empty((1, n_local, 2, N_RING), dtype=torch.int64, device=dev)
+    del ws2
+    wsc = torch.empty(B.bm_match_ws_bytes(prm, n_local, 1, order), dtype=torch.uint8, device=dev)
+    B.bm_match(prm, evk_dev, d_db, n_local, d_q[nq - 1:], 1, chk, wsc, order)
+    B.bm_sync()
+    same = bool(torch.equal(h_ring[(nq - 1) % ring_rows], chk[0].cpu()))
+    return {"value": round(tq_per_step / (e2e_ms / 1e3), 1), "unit": "templates*queries/s",
+            "h2d_bytes_per_step": int(h_q.numel() * 8), "d2h_bytes_per_step": int(nq * row_bytes),
+            "ms_per_step": round(e2e_ms, 3), "host_ring_rows": ring_rows, "last_row_equals_device_scan": same,
+            "note": "bm_match_host_ring per rank (its shard): pinned query cts H2D + every result D2H through a "
+                    "bounded pinned host ring, inside the timed region, wall clock, max over ranks"}
+
+
+# ----------------------------------------------------------------------------- NEXT-row legs (configs[1])
+def run_extras(args, B, torch, dev, stream):
+    """f3 (+ f4) and f1 measured on the configs[1] workload (d = 128, 6,144 templates, 384 queries,
+    p = 8), their own setup; the plain scan of that workload is timed as their reference."""
+    from paper_2408_06167_b200 import inputs as I
+    cfg, p, nq = 2, 8, 384
+    prm = B.bm_params_init(128, p)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
+    n_tmpl = I.CONFIGS[cfg]["n"]
+    n_sets = -(-n_tmpl // prm.B)
+    T = I.templates(cfg, n_tmpl)
+    d_db = torch.empty((n_sets, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_db(prm, pk_dev, T, 0, n_sets, 2, d_db)
+    Q, _ = I.queries(cfg, nq)
+    d_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
+    d_out = torch.empty((nq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
+    ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, nq, 0), dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    k = max(1, min(args.steps, 5))
+    for _ in range(k):
+        B.bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, ws, 0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_scan = e0.elapsed_time(e1) / k
+    tq = n_tmpl * nq
+    del ws
+    torch.cuda.empty_cache()
+    out = {"configs1_scan": {"ms_per_step": round(ms_scan, 4), "value": round(tq / (ms_scan / 1e3), 1),
+                             "unit": "templates*queries/s",
+                             "note": "BASELINE configs[1] (6,144 templates x 384 queries, p = 8), one bm_match, "
+                                     "device time: the reference point of the NEXT-row legs"}}
+    try:
+        out["f3_expand"] = run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_scan, tq, stream)
+    except Exception as ex:  # noqa: BLE001
+        out["f3_expand"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    torch.cuda.empty_cache()
+    try:
+        out["f1_compressed"] = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq, stream)
+    except Exception as ex:  # noqa: BLE001
+        out["f1_compressed"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    return out
 
 
 def f3_modmuls(p, s):
@@ -527,7 +851,7 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
     dev = d_q.device
     xk = B.bm_xk_keygen(prm, 1)
     xk_dev = B.bm_xk_to_device(prm, pk, xk)
-    Q, _ = I.queries(CFG, nq)
+    Q, _ = I.queries(2, nq)
     d_pt = torch.from_numpy(B.bm_encode_query_tiled(prm, Q)).to(dev)
     d_l2 = torch.empty((nq, 2, 3, N_RING), dtype=torch.int64, device=dev)
     B.bm_encrypt_l2(prm, xk_dev, d_pt, 0, 3, d_l2)
@@ -539,27 +863,30 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
+    k = max(1, min(args.steps, 5))
+    for _ in range(k):
         B.bm_expand(prm, xk_dev, d_l2, nq, d_qx, ws)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / k
     del ws
     # sanity: the expanded queries scan to the same scores as the client-expanded ones (different noise)
-    k = min(4, nq)
-    out_x = torch.empty((k, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
-    ws2 = torch.empty(B.bm_match_ws_bytes(prm, n_sets, k, 0), dtype=torch.uint8, device=dev)
-    B.bm_match(prm, evk_dev, d_db, n_sets, d_qx[:k].contiguous(), k, out_x, ws2, 0)
+    kq = min(4, nq)
+    out_x = torch.empty((kq, n_sets, 2, N_RING), dtype=torch.int64, device=dev)
+    ws2 = torch.empty(B.bm_match_ws_bytes(prm, n_sets, kq, 0), dtype=torch.uint8, device=dev)
+    B.bm_match(prm, evk_dev, d_db, n_sets, d_qx[:kq].contiguous(), kq, out_x, ws2, 0)
     B.bm_sync()
     sa = B.bm_decrypt(prm, sk, out_x.cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
-    sb = B.bm_decrypt(prm, sk, d_out[:k].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
+    sb = B.bm_decrypt(prm, sk, d_out[:kq].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
     err = float(np.abs(sa - sb).max())
     assert err < 1e-5, err
     f4 = None
-    if not args.no_f4:
-        f4 = run_f4(B, torch, prm, xk_dev, sk, evk_dev, d_db, n_sets, d_q, out_x, ws2, sb, k, stream)
+    try:
+        f4 = run_f4(B, torch, prm, xk_dev, sk, evk_dev, d_db, n_sets, d_q, out_x, ws2, sb, kq, stream)
+    except Exception as ex:  # noqa: BLE001
+        f4 = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     mm = f3_modmuls(p, prm.s) * nq * p
-    peak = SM_COUNT * IMAD_PER_CLK_SM * 1965.0e6 / IMAD_SLOTS_PER_MODMUL / 1e9
+    peak = int_peak_gmodmul(torch.cuda.get_device_properties(dev).multi_processor_count, 1965.0e6)
     return {"queries": nq, "ms_per_batch": round(ms, 4), "queries_per_s": round(nq / (ms / 1e3), 1),
             "gmodmul_s": round(mm / (ms / 1e3) / 1e9, 2), "alu_frac": round(mm / (ms / 1e3) / 1e9 / peak, 4),
             "kernel_launches": 1 + 2 * (p.bit_length() - 1),
@@ -568,15 +895,16 @@ def run_f3(args, B, torch, prm, pk, sk, evk_dev, d_db, n_sets, d_q, d_out, ms_sc
                                  "value": round(tq_per_step / ((ms + ms_scan) / 1e3), 1),
                                  "unit": "templates*queries/s"},
             "score_check_max_abs_diff": err,
-            "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24)",
+            "note": "Algorithm 1 on the chain extended by q2 (not BASELINE's parameter set; DESIGN.md R24), "
+                    "configs[1] batch",
             "f4_enroll": f4}
 
 
 def run_f4(B, torch, prm, xk_dev, sk, evk_dev, d_db, n_sets, d_q, out_x, ws2, sb, k, stream):
-    """f4: server-side enrollment of the whole DB (the same templates), then the same spot check."""
+    """f4: server-side enrollment of the whole configs[1] DB (the same templates), then the same spot check."""
     from paper_2408_06167_b200 import inputs as I
     dev = d_db.device
-    T = I.templates(CFG, I.CONFIGS[CFG]["n"], 0)
+    T = I.templates(2, I.CONFIGS[2]["n"], 0)
     n_t = T.shape[0]
     d_pt = torch.from_numpy(B.bm_encode_enroll(prm, T)).to(dev)
     d_tl2 = torch.empty((n_t, 2, 3, N_RING), dtype=torch.int64, device=dev)
@@ -610,8 +938,8 @@ def run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stre
     xk = B.bm_xk_keygen(prm, 1)
     xk_dev = B.bm_xk_to_device(prm, pk, xk, enroll=False)       # the level-2 public key
     ck_dev = B.bm_ck_to_device(prm, B.bm_ck_keygen(prm, 1))
-    T = I.templates(CFG, n_tmpl, 0)
-    Q, _ = I.queries(CFG, nq)
+    T = I.templates(2, n_tmpl, 0)
+    Q, _ = I.queries(2, nq)
     d_db = torch.empty((n_sets, p, 2, 3, N_RING), dtype=torch.int64, device=dev)
     B.bm_encrypt_l2(prm, xk_dev, torch.from_numpy(B.bm_encode_db(prm, T, 0, n_sets).reshape(-1, N_RING)).to(dev),
                     0, 2, d_db)
@@ -630,7 +958,6 @@ def run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stre
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / k
-    # the packed scores of two queries vs the uncompressed scan's
     slots = B.bm_decrypt_packed(prm, sk, out[:2].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
     ref = B.bm_decrypt(prm, sk, d_out[:2].cpu().numpy().view(np.uint64).reshape(-1, 2, 1, N_RING))
     ref = ref.reshape(2, n_sets, prm.B)
@@ -643,31 +970,34 @@ def run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq_per_step, stre
     return {"ms_per_step": round(ms, 3), "value": round(tq_per_step / (ms / 1e3), 1), "unit": "templates*queries/s",
             "packed_ciphertexts_per_query": G, "d2h_bytes_per_step": int(out.numel() * 8),
             "d2h_bytes_uncompressed": int(d_out.numel() * 8), "score_check_max_abs_diff": err,
-            "note": "HE-C^3 one level up (level-2 DB and query parts: tensor over 3 limbs, 3-digit relin + Res q2, "
-                    "ladder at level 1) + compression (Res_q1(M * C_t), right rotation by t mod s, packing); "
-                    "chain extended by q2, DESIGN.md R28"}
+            "note": "configs[1] workload: HE-C^3 one level up (level-2 DB and query parts: tensor over 3 limbs, "
+                    "3-digit relin + Res q2, ladder at level 1) + compression (Res_q1(M * C_t), right rotation by "
+                    "t mod s, packing); chain extended by q2, DESIGN.md R28"}
 
 
+# ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from paper_2408_06167_b200 import inputs as I
+    c = I.CONFIGS[args.config]
+    d, p = c["d"], args.p or c["p"]
     nth = os.cpu_count() or 1
-    p = args.p
-    run, n_pairs, Bk, t1 = oracle_sample(p, 8.0, nth)
+    run, n_pairs, Bk, t1 = oracle_sample(args.config, d, p, 8.0, nth)
     for _ in range(args.warmup):
         run()
     times = [run() for _ in range(args.steps)]
     secs = sum(times) / len(times)
     value = n_pairs * Bk / secs
     line = {
-        "impl": "reference", "metric": "encrypted templates matched/sec (d=128, N=8192)", "value": round(value, 2),
+        "impl": "reference", "metric": METRIC, "value": round(value, 2),
         "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"BASELINE configs[1]: d=128, p={p}, bounded sample of {n_pairs} (query, set) pairs "
-                               f"per step", "d": D, "p": p},
+        "config": {"workload": f"BASELINE configs[{args.config - 1}]: d={d}, p={p}, bounded sample of {n_pairs} "
+                               f"(query, set) pairs per step (the CPU oracle, oracle/)", "d": d, "p": p},
         "cpu_baseline": {"value": round(value, 2), "unit": "templates*queries/s", "cores": nth, "kind": "oracle",
                          "sample": f"{n_pairs} pairs x {Bk} templates per step on {nth} threads"},
         "e2e": {"value": round(value, 2), "unit": "templates*queries/s", "h2d_bytes_per_step": 0,

@@ -206,15 +206,47 @@ int bm_ipc_close(void *d_base);
 
 /* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
  * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call.  The queries are
- * processed in groups of about 576 (query, set) pairs (or BM_HOST_GROUPS groups): group g's
+ * processed in groups of about 576 (query, set) pairs (or BM_OPT_HOST_GROUPS groups): group g's
  * upload, scan and download overlap the neighbouring groups (four device slots, two internal
  * copy streams, the scans alternating between `stream` and an internal stream, all starting
- * after the work already queued on `stream`).
+ * after the work already queued on `stream`; the internal streams are created once per device and
+ * the calls on one device are serialised by the library).
  * Pinned host memory is required for the overlap.  d_ws must hold bm_match_host_ws_bytes(...)
  * bytes.  Synchronous (returns after h_out is written). */
 size_t bm_match_host_ws_bytes(const bm_params *, int64_t n_sets, int32_t nq, int32_t order);
 int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets, const uint64_t *h_q,
                   int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order, void *stream);
+
+/* Streaming variant for result sets larger than host memory (BASELINE.json configs[3]: 1,048,576
+ * templates x 256 queries = 128 GiB of level-0 results per batch): query j's results are written to
+ * host row (j mod ring_rows) of h_ring [ring_rows][n_sets][2][N], overwriting earlier queries' rows
+ * (the caller consumes rows between calls, or -- a benchmark -- not at all).  ring_rows >= 1;
+ * ring_rows >= nq is bm_match_host.  Same workspace, same scan, same errors. */
+int bm_match_host_ring(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, int64_t n_sets,
+                       const uint64_t *h_q, int32_t nq, uint64_t *h_ring, int32_t ring_rows, void *d_ws,
+                       size_t ws_bytes, int32_t order, void *stream);
+
+/* Library options (process-wide; the defaults are the product -- tests and tuning runs change them).
+ * Changing BM_OPT_CHUNK_PAIRS / BM_OPT_EXPAND_CHUNK / BM_OPT_CMP_CHUNK changes the workspace size the
+ * *_ws_bytes functions return: size the workspace after setting them.  Results never depend on them.
+ * bm_set_option returns BM_ERR_INVALID_ARG for an unknown key or a value out of range. */
+typedef enum {
+    BM_OPT_CHUNK_PAIRS = 0,  /* (query, set) pairs per bm_match chunk, >= 1 (default 16384)          */
+    BM_OPT_EXPAND_CHUNK = 1, /* (query, part) outputs per bm_expand / bm_enroll launch (2048)       */
+    BM_OPT_HOST_GROUPS = 2,  /* bm_match_host query groups, 0 = automatic (~576 pairs per group)   */
+    BM_OPT_LADDER_C2 = 3,    /* 0/1: latency-mode ladder on 2-CTA clusters (1)                      */
+    BM_OPT_LADDER_C3 = 4,    /* 0/1: latency-mode ladder on 3-CTA clusters (1)                      */
+    BM_OPT_LADDER_TAIL = 5,  /* 0/1: a large launch's partial last wave on the cluster ladders (1)  */
+    BM_OPT_CMP_CHUNK = 6,    /* pairs per bm_match_cmp chunk (4096)                                 */
+    BM_OPT_COUNT_ = 7
+} bm_option;
+int bm_set_option(int32_t key, int64_t value);
+int64_t bm_get_option(int32_t key);
+
+/* Number of kernels the library has launched in this process (every launch site counts itself;
+ * the bench's gpu_launches claim).  bm_launch_count_reset sets it to 0. */
+int64_t bm_launch_count(void);
+void bm_launch_count_reset(void);
 
 /* Per-kernel-class device time of the last bm_match on this thread when profiling is
  * enabled (bm_set_profiling(1)); classes: 0 tensor, 1 digits + ModUp NTTs, 2 key switch +
@@ -224,6 +256,20 @@ int bm_match_host(const bm_params *, const bm_evk_dev *, const uint64_t *d_db, i
 void bm_set_profiling(int32_t on);
 void bm_profile_reset(void);
 int bm_profile_read(double *ms, int64_t *launches, int64_t *units);
+
+/* Client side on the DEVICE (a9 at the scale of a 1:N batch).
+ * bm_sk_to_device uploads the secret (NTT domain mod q0; synchronous; a client-side handle -- the
+ * server never needs it).  bm_decrypt_dev decrypts n level-0 results d_ct [n][2][N] (device,
+ * COEFFICIENT domain: bm_match's d_out) and decodes the B score slots k*s into d_scores [n][B]
+ * (device float64): m = c0 + c1 s mod q0 (centred), slot j = Re m(zeta^(5^j)), zeta = exp(i pi / N),
+ * evaluated for all odd powers by one N-point FP64 FFT per ciphertext, divided by prm->out_scale.
+ * Same scores as bm_decrypt (the direct cosine sum) to ~1e-12.  Asynchronous on `stream`.
+ * Errors: BM_ERR_INVALID_ARG, BM_ERR_KEY_MISMATCH, BM_ERR_CUDA, BM_ERR_OOM. */
+typedef struct bm_sk_dev bm_sk_dev;
+int bm_sk_to_device(const bm_params *, const bm_sk *, bm_sk_dev **out);
+void bm_sk_dev_free(bm_sk_dev *);
+int bm_decrypt_dev(const bm_params *, const bm_sk_dev *, const uint64_t *d_ct, int64_t n, double *d_scores,
+                   void *stream);
 
 /* Client side (host): decrypt level-0 results h_ct [n][2][1][N] (canonical) and decode the
  * B scores at slots k*s into scores[n][B].  bm_decrypt_raw returns the

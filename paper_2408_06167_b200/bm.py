@@ -105,6 +105,11 @@ _SIGS = {
     "bm_match_cmp_ws_bytes": (_sz, [_P, _i64, _i32]),
     "bm_match_cmp": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _vp]),
     "bm_decrypt_packed": (_i32, [_P, _vp, _vp, _i64, _vp]),
+    "bm_sk_to_device": (_i32, [_P, _vp, _pp]), "bm_sk_dev_free": (None, [_vp]),
+    "bm_decrypt_dev": (_i32, [_P, _vp, _vp, _i64, _vp, _vp]),
+    "bm_match_host_ring": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp, _sz, _i32, _vp]),
+    "bm_set_option": (_i32, [_i32, _i64]), "bm_get_option": (_i64, [_i32]),
+    "bm_launch_count": (_i64, []), "bm_launch_count_reset": (None, []),
     "bm_sync": (_i32, [_vp]),
     "bm_strerror": (ctypes.c_char_p, [_i32]),
     "bm_build_info": (ctypes.c_char_p, []),
@@ -123,14 +128,29 @@ def _chk(rc, fn):
 
 
 def _np_ptr(a):
-    assert a.flags["C_CONTIGUOUS"]
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("expected a C-contiguous numpy array")
     return ctypes.c_void_p(a.ctypes.data)
 
 
 def _dptr(t):
     """device pointer of a contiguous CUDA tensor"""
-    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    if not (t.is_cuda and t.is_contiguous()):
+        raise ValueError("expected a contiguous CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t, n_u64, name):
+    """a CUDA tensor of 8-byte integers holding at least n_u64 elements (the C ABI trusts the sizes)."""
+    import torch
+    if t is None:
+        raise ValueError(f"{name}: missing")
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous CUDA tensor")
+    if t.dtype not in (torch.int64, torch.uint64):
+        raise ValueError(f"{name}: expected int64 / uint64, got {t.dtype}")
+    if t.numel() < n_u64:
+        raise ValueError(f"{name}: {t.numel()} elements, the call needs {n_u64}")
 
 
 def _stream(stream=None):
@@ -312,7 +332,18 @@ def bm_match_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):
     return int(_lib.bm_match_ws_bytes(ctypes.byref(prm), n_sets, nq, order))
 
 
+def _check_scan(prm, d_db, n_sets, d_q, nq, n_limbs=2):
+    if n_sets < 0 or nq < 0:
+        raise ValueError("n_sets and nq must be >= 0")
+    if n_sets and nq:
+        _need(d_db, n_sets * prm.p * 2 * n_limbs * N, "d_db")
+        _need(d_q, nq * prm.p * 2 * n_limbs * N, "d_q")
+
+
 def bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, d_ws, order=ORDER_HOISTED, stream=None):
+    _check_scan(prm, d_db, n_sets, d_q, nq)
+    if n_sets and nq:
+        _need(d_out, nq * n_sets * 2 * N, "d_out")
     ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
     _chk(_lib.bm_match(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
                        _dptr(d_q) if nq else None, nq, _dptr(d_out) if nq * n_sets else None,
@@ -323,8 +354,10 @@ def bm_match_rows(prm, evk_dev, d_db, n_sets, d_q, nq, d_rows, set_offset, d_ws,
     """The scan with the gather fused into its output kernels: d_rows is a CUDA int64 tensor of nq
     device addresses (local or peer, see bm_ipc_open); (query j, local set t) lands at row j, global
     set set_offset + t (include/blindmatch.h)."""
-    import torch
-    assert d_rows.is_cuda and d_rows.dtype == torch.int64 and d_rows.numel() >= nq
+    _check_scan(prm, d_db, n_sets, d_q, nq)
+    _need(d_rows, nq, "d_rows")
+    if set_offset < 0:
+        raise ValueError("set_offset must be >= 0")
     ws_bytes = d_ws.numel() * d_ws.element_size()
     _chk(_lib.bm_match_rows(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
                             _dptr(d_q) if nq else None, nq, _dptr(d_rows), set_offset,
@@ -355,16 +388,102 @@ def bm_match_host_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):
     return int(_lib.bm_match_host_ws_bytes(ctypes.byref(prm), n_sets, nq, order))
 
 
+def _hp(x, n_u64, name):
+    """host pointer of a contiguous CPU tensor / numpy array of at least n_u64 8-byte elements"""
+    if isinstance(x, np.ndarray):
+        if x.itemsize != 8 or x.size < n_u64:
+            raise ValueError(f"{name}: expected >= {n_u64} 8-byte elements")
+        return _np_ptr(x)
+    if x.is_cuda or not x.is_contiguous() or x.element_size() != 8 or x.numel() < n_u64:
+        raise ValueError(f"{name}: expected a contiguous CPU tensor of >= {n_u64} 8-byte elements")
+    return ctypes.c_void_p(x.data_ptr())
+
+
 def bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, d_ws, order=ORDER_HOISTED, stream=None):
     """h_q / h_out: (pinned) CPU tensors or numpy arrays."""
-    def hp(x):
-        if isinstance(x, np.ndarray):
-            return _np_ptr(x)
-        assert not x.is_cuda and x.is_contiguous()
-        return ctypes.c_void_p(x.data_ptr())
+    _need(d_db, n_sets * prm.p * 4 * N, "d_db")
     ws_bytes = d_ws.numel() * d_ws.element_size()
-    _chk(_lib.bm_match_host(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets, hp(h_q), nq, hp(h_out),
-                            _dptr(d_ws), ws_bytes, order, _stream(stream)), "bm_match_host")
+    _chk(_lib.bm_match_host(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets, _hp(h_q, nq * prm.p * 4 * N, "h_q"),
+                            nq, _hp(h_out, nq * n_sets * 2 * N, "h_out"), _dptr(d_ws), ws_bytes, order,
+                            _stream(stream)), "bm_match_host")
+
+
+def bm_match_host_ring(prm, evk_dev, d_db, n_sets, h_q, nq, h_ring, ring_rows, d_ws, order=ORDER_HOISTED,
+                       stream=None):
+    """bm_match_host with query j's results written to host row j mod ring_rows of h_ring
+    [ring_rows][n_sets][2][N] (bounded host memory for very large result sets)."""
+    _need(d_db, n_sets * prm.p * 4 * N, "d_db")
+    ws_bytes = d_ws.numel() * d_ws.element_size()
+    _chk(_lib.bm_match_host_ring(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets,
+                                 _hp(h_q, nq * prm.p * 4 * N, "h_q"), nq,
+                                 _hp(h_ring, ring_rows * n_sets * 2 * N, "h_ring"), ring_rows, _dptr(d_ws), ws_bytes,
+                                 order, _stream(stream)), "bm_match_host_ring")
+
+
+# --------------------------------------------------------------------------- options / counters
+OPTIONS = {"chunk_pairs": 0, "expand_chunk": 1, "host_groups": 2, "ladder_c2": 3, "ladder_c3": 4,
+           "ladder_tail": 5, "cmp_chunk": 6}
+
+
+def bm_set_option(name, value):
+    _chk(_lib.bm_set_option(OPTIONS[name], int(value)), "bm_set_option")
+
+
+def bm_get_option(name):
+    return int(_lib.bm_get_option(OPTIONS[name]))
+
+
+class options:
+    """with bm.options(chunk_pairs=7, ladder_c3=0): ...  -- library options set for the block and
+    restored afterwards (tests and tuning runs; the defaults are the product)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = bm_get_option(k)
+            bm_set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            bm_set_option(k, v)
+
+
+def bm_launch_count():
+    return int(_lib.bm_launch_count())
+
+
+def bm_launch_count_reset():
+    _lib.bm_launch_count_reset()
+
+
+# --------------------------------------------------------------------------- device-side client decryption
+class SecretKeyDev(_Handle):
+    _free = "bm_sk_dev_free"
+
+
+def bm_sk_to_device(prm, sk):
+    out = ctypes.c_void_p()
+    _chk(_lib.bm_sk_to_device(ctypes.byref(prm), sk.ptr, ctypes.byref(out)), "bm_sk_to_device")
+    return SecretKeyDev(out)
+
+
+def bm_decrypt_dev(prm, sk_dev, d_ct, d_scores=None, stream=None):
+    """d_ct: CUDA int64 [n][2][N] level-0 coefficient-domain results (bm_match's d_out, any leading
+    shape) -> d_scores CUDA float64 [n][B] (allocated if None)."""
+    import torch
+    n = d_ct.numel() // (2 * N)
+    _need(d_ct, n * 2 * N, "d_ct")
+    if d_scores is None:
+        d_scores = torch.empty((n, prm.B), dtype=torch.float64, device=d_ct.device)
+    if d_scores.dtype != torch.float64 or d_scores.numel() < n * prm.B or not d_scores.is_contiguous():
+        raise ValueError("d_scores: expected a contiguous float64 CUDA tensor of n x B")
+    _chk(_lib.bm_decrypt_dev(ctypes.byref(prm), sk_dev.ptr, _dptr(d_ct), n, _dptr(d_scores), _stream(stream)),
+         "bm_decrypt_dev")
+    return d_scores
 
 
 def bm_set_profiling(on):

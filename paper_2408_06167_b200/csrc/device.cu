@@ -25,6 +25,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -54,6 +57,12 @@ struct DevCtx {
     ulonglong2 pinv2;          // f1: P^-1 mod q2
     uint64_t pmod[2];
     int n_sm = 148;
+    double2 *zeta = nullptr;    // [N] exp(i pi k / N) (device decryption's canonical embedding)
+    int32_t *slot_t = nullptr;  // [S] (5^j mod 2N - 1) / 2
+    int max_cl[4] = {0, 0, 0, 0}; // cudaOccupancyMaxActiveClusters of the cluster ladders (index: cluster size)
+    // bm_match_host's extra streams (created once per device, reused by every call under host_mu)
+    std::mutex host_mu;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr}; // second compute stream, upload, download
 };
 
 std::mutex g_mu;
@@ -179,6 +188,44 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_cmp_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C4_SMEM_BYTES);
     set_smem(k_convert);
     set_smem(k_key_ntt);
+    cudaFuncSetAttribute(k_decrypt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DEC_SMEM_BYTES);
+    {   // device decryption tables: zeta^k = exp(i pi k / N) (long double, rounded once), slot -> FFT index
+        std::vector<double2> z(N);
+        for (int k = 0; k < N; k++) {
+            const long double a = 3.141592653589793238462643383279502884L * k / N;
+            z[k] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+        std::vector<int32_t> t(SLOTS);
+        uint64_t x = 1;
+        for (int j = 0; j < SLOTS; j++, x = x * 5 % (2 * N)) t[j] = (int32_t)((x - 1) / 2);
+        if (cudaMalloc(&C->zeta, N * sizeof(double2)) != cudaSuccess ||
+            cudaMalloc(&C->slot_t, SLOTS * sizeof(int32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return BM_ERR_OOM;
+        }
+        cudaMemcpy(C->zeta, z.data(), N * sizeof(double2), cudaMemcpyHostToDevice);
+        cudaMemcpy(C->slot_t, t.data(), SLOTS * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
+    // how many 2- / 3-CTA ladder clusters can be resident at once (MPS, green contexts or partitioned
+    // SMs can make this smaller than n_SM / size): the cluster ladders are used only within it
+    for (int cs = 2; cs <= 3; cs++) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)(cs * 16));
+        cfg.blockDim = dim3(T);
+        cfg.dynamicSmemBytes = LADDER_SMEM_BYTES;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        const cudaError_t e = cs == 3 ? cudaOccupancyMaxActiveClusters(&n, (void *)k_ladder_c3, &cfg)
+                                      : cudaOccupancyMaxActiveClusters(&n, (void *)k_ladder_t<true>, &cfg);
+        C->max_cl[cs] = e == cudaSuccess ? n : 0;
+        cudaGetLastError();
+    }
     if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         cudaFree(C->tw);
         delete C;
@@ -198,6 +245,28 @@ int launch_check()
     }
     return BM_OK;
 }
+
+// ------------------------------------------------------------------ options (bm_set_option)
+// Process-wide tuning / test switches of the library (explicit, no environment lookups on the hot
+// path); the defaults are the product.
+std::atomic<int64_t> g_opt[BM_OPT_COUNT_] = {};
+struct OptInit {
+    OptInit()
+    {
+        g_opt[BM_OPT_CHUNK_PAIRS] = 16384; // pairs per bm_match chunk (workspace 768 KiB per pair)
+        g_opt[BM_OPT_EXPAND_CHUNK] = 2048; // (query, part) outputs per bm_expand / bm_enroll launch
+        g_opt[BM_OPT_HOST_GROUPS] = 0;     // bm_match_host query groups (0: about 576 pairs each)
+        g_opt[BM_OPT_LADDER_C2] = 1;       // latency-mode ladder on 2-CTA clusters
+        g_opt[BM_OPT_LADDER_C3] = 1;       // latency-mode ladder on 3-CTA clusters
+        g_opt[BM_OPT_LADDER_TAIL] = 1;     // a large launch's partial last wave on the cluster ladders
+        g_opt[BM_OPT_CMP_CHUNK] = 4096;    // pairs per bm_match_cmp chunk
+    }
+} g_opt_init;
+int64_t opt(int k) { return g_opt[k].load(std::memory_order_relaxed); }
+
+// kernels launched by the library (bm_launch_count): the bench's gpu_launches claim
+std::atomic<int64_t> g_launches(0);
+inline void counted(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ profiling
 struct Prof {
@@ -250,6 +319,12 @@ struct bm_evk_dev {
     uint64_t *hgk;   // [n_hrot][2][2][N], NTT domain, plain residues (no Shoup companion), P^-1 in q0
 };
 
+struct bm_sk_dev {
+    int dev;
+    uint8_t digest[32];
+    ulonglong2 *s; // planar Shoup key of the secret mod q0 (NTT domain)
+};
+
 // keys -> device NTT-domain Shoup pairs; limb li is multiplied by scale[li] (nullptr: 1); planar
 // (default): per polynomial the w plane then the w' plane (read with ldkey2 / ldkey1)
 static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n_limbs, const int *lp, ulonglong2 **out,
@@ -273,6 +348,7 @@ static int upload_key_polys(DevCtx *C, const uint64_t *h, int64_t n_polys, int n
     for (int i = 0; i < 4; i++) K.scale[i] = scale && i < n_limbs ? scale[i] : 1;
     K.planar = planar ? 1 : 0;
     k_key_ntt<<<(unsigned)n_polys, T, SMEM_BYTES>>>(K, dst);
+    counted();
     int rc = launch_check();
     if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = BM_ERR_CUDA;
     cudaFree(tmp);
@@ -349,6 +425,67 @@ int bm_evk_to_device(const bm_params *prm, const bm_evk *evk, bm_evk_dev **out)
     return BM_OK;
 }
 
+int bm_sk_to_device(const bm_params *prm, const bm_sk *sk, bm_sk_dev **out)
+{
+    if (!prm || !sk || !out) return BM_ERR_INVALID_ARG;
+    if (memcmp(sk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    std::vector<uint64_t> h(N);
+    for (int k = 0; k < N; k++) h[k] = sk->s[k] >= 0 ? (uint64_t)sk->s[k] : Q0 - (uint64_t)(-sk->s[k]);
+    bm_sk_dev *d = new bm_sk_dev;
+    d->dev = C->dev;
+    memcpy(d->digest, prm->digest, 32);
+    const int lp[1] = {0};
+    rc = upload_key_polys(C, h.data(), 1, 1, lp, &d->s);
+    if (rc) {
+        delete d;
+        return rc;
+    }
+    *out = d;
+    return BM_OK;
+}
+
+void bm_sk_dev_free(bm_sk_dev *d)
+{
+    if (!d) return;
+    cudaFree(d->s);
+    delete d;
+}
+
+int bm_decrypt_dev(const bm_params *prm, const bm_sk_dev *sk, const uint64_t *d_ct, int64_t n, double *d_scores,
+                   void *stream)
+{
+    if (!prm || !sk || n < 0) return BM_ERR_INVALID_ARG;
+    if (memcmp(sk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (n == 0) return BM_OK;
+    if (!d_ct || !d_scores) return BM_ERR_INVALID_ARG;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    DecK K;
+    K.pr0 = C->pr[0];
+    K.s = reinterpret_cast<const uint64_t *>(sk->s);
+    K.ct = d_ct;
+    K.scores = d_scores;
+    K.zeta = C->zeta;
+    K.slot_t = C->slot_t;
+    K.B = prm->B;
+    K.s_len = prm->s;
+    K.inv_scale = 1.0 / prm->out_scale;
+    for (int64_t c0 = 0; c0 < n && !rc; c0 += 1 << 30) { // grid.x limit
+        DecK Kc = K;
+        const int64_t nc = n - c0 < (1 << 30) ? n - c0 : (1 << 30);
+        Kc.ct = d_ct + (size_t)c0 * 2 * N;
+        Kc.scores = d_scores + (size_t)c0 * prm->B;
+        k_decrypt<<<(unsigned)nc, T, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(Kc);
+        counted();
+        rc = launch_check();
+    }
+    return rc;
+}
+
 void bm_pk_dev_free(bm_pk_dev *d)
 {
     if (!d) return;
@@ -385,6 +522,7 @@ int bm_encrypt(const bm_params *prm, const bm_pk_dev *pk, const int64_t *d_pt, i
     Ek.lp[1] = 1;
     Ek.lp[2] = 3;
     k_encrypt<<<(unsigned)(2 * n_cts), T, SMEM_BYTES, (cudaStream_t)stream>>>(Ek);
+    counted();
     return launch_check();
 }
 
@@ -443,6 +581,7 @@ static int convert(const bm_params *prm, const uint64_t *in, int64_t n_cts, int3
     K.lp[1] = 1;
     K.lp[2] = 3; // level-2 limb q2 (f3)
     k_convert<<<(unsigned)(n_cts * 2 * n_limbs), T, SMEM_BYTES, (cudaStream_t)stream>>>(K, dir);
+    counted();
     return launch_check();
 }
 
@@ -551,16 +690,13 @@ int bm_encrypt_l2(const bm_params *prm, const bm_xk_dev *xk, const int64_t *d_pt
     Ek.lp[1] = 1;
     Ek.lp[2] = 3;
     k_encrypt<<<(unsigned)(3 * n_cts), T, SMEM_BYTES, (cudaStream_t)stream>>>(Ek);
+    counted();
     return launch_check();
 }
 
 static int64_t expand_chunk_cts(const bm_params *prm, int32_t nq)
 {
-    int64_t ch = 2048; // (query, part) outputs per launch: 6 N u64 of workspace each (768 MiB)
-    if (const char *e = getenv("BM_EXPAND_CHUNK")) {
-        long v = atol(e);
-        if (v > 0) ch = v;
-    }
+    int64_t ch = opt(BM_OPT_EXPAND_CHUNK); // (query, part) outputs per launch: 6 N u64 of workspace each
     ch = ch / prm->p * prm->p; // whole queries
     if (ch < prm->p) ch = prm->p;
     const int64_t total = (int64_t)nq * prm->p;
@@ -610,12 +746,15 @@ int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
         K.gk = nullptr;
         K.g = 1;
         k_exp_mask<<<ncb, T, X1_SMEM_BYTES, s>>>(K);
+        counted();
         rc = launch_check();
         for (int t = 0; t < log_p && !rc; t++) {
             K.gk = xk->gk1 + (size_t)t * 12 * N;
             K.g = (uint32_t)powmod_d(5, (uint64_t)prm->s << t, 2 * N);
             k_rot1_digits<<<ncb, T, X2_SMEM_BYTES, s>>>(K);
+            counted();
             k_rot1_ks<<<ncb, T, X3_SMEM_BYTES, s>>>(K);
+            counted();
             rc = launch_check();
         }
     }
@@ -625,11 +764,7 @@ int bm_expand(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
 // ------------------------------------------------------------------ f4: server-side enrollment
 static int64_t enroll_chunk_templates(const bm_params *prm, int64_t n)
 {
-    int64_t ch = 2048; // parts per launch: 10 N u64 of workspace each (W + XU, 1.25 GiB)
-    if (const char *e = getenv("BM_EXPAND_CHUNK")) {
-        long v = atol(e);
-        if (v > 0) ch = v;
-    }
+    int64_t ch = opt(BM_OPT_EXPAND_CHUNK); // parts per launch: 10 N u64 of workspace each (W + XU)
     int64_t t = ch / prm->p;
     if (t < 1) t = 1;
     return n < t ? n : t;
@@ -688,13 +823,16 @@ int bm_enroll(const bm_params *prm, const bm_xk_dev *xk, const uint64_t *d_in, i
             K.gk = xk->gk1 + (size_t)b * 12 * N;
             K.g = (uint32_t)powmod_d(5, (uint64_t)prm->s << b, 2 * N);
             k_rot1_digits<<<ncb, T, X2_SMEM_BYTES, s>>>(K);
+            counted();
             k_rot1_ks<<<ncb, T, X3_SMEM_BYTES, s>>>(K);
+            counted();
             rc = launch_check();
         }
         if (rc) break;
         const int64_t t0 = K.u0 / prm->B, t1 = (K.u0 + nc - 1) / prm->B;
         k_enroll_add<<<(unsigned)((t1 - t0 + 1) * prm->p * 4 * (N / 256)), 256, 0, s>>>(W, K.u0, nc, prm->p, prm->B, t0,
                                                                                          d_db);
+        counted();
         rc = launch_check();
     }
     return rc;
@@ -760,11 +898,7 @@ void bm_ck_dev_free(bm_ck_dev *d)
 constexpr int CMP_WS_POLYS = 28;
 static int64_t cmp_chunk_pairs(int64_t total)
 {
-    int64_t ch = 4096;
-    if (const char *e = getenv("BM_CHUNK_PAIRS")) {
-        long v = atol(e);
-        if (v > 0) ch = v;
-    }
+    int64_t ch = opt(BM_OPT_CMP_CHUNK);
     return total < ch ? total : ch;
 }
 
@@ -846,22 +980,31 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
             const unsigned npu = (unsigned)np;
             const unsigned ntiles = (unsigned)(((K.cq + TQB - 1) / TQB) * ((K.ct + TSB - 1) / TSB) * (N / CS / TSL));
             k_tensor<3, false><<<3 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, 0, prm->p);
+            counted();
             k_digits3<<<3 * npu, T, C1_SMEM_BYTES, s>>>(C);
+            counted();
             k_relin3a<<<2 * npu, T, C2_SMEM_BYTES, s>>>(C);
+            counted();
             k_relin3b<<<4 * npu, T, SMEM_BYTES, s>>>(C);
+            counted();
             rc = launch_check();
             for (int i = 0; i < prm->log_s && !rc; i++) {
                 X.gk = ck->gkl + (size_t)i * 12 * N;
                 X.g = (uint32_t)powmod_d(5, (uint64_t)1 << i, 2 * N);
                 k_rot1_digits<<<2 * npu, T, X2_SMEM_BYTES, s>>>(X);
+                counted();
                 k_rot1_ks<<<2 * npu, T, X3_SMEM_BYTES, s>>>(X);
+                counted();
                 rc = launch_check();
             }
             if (rc) break;
             k_cmp_mask<<<2 * npu, T, SMEM_BYTES, s>>>(C);
+            counted();
             k_cmp_rot<<<npu, T, C4_SMEM_BYTES, s>>>(C);
+            counted();
             const int64_t g0 = t0 / prm->s, g1 = (t0 + K.ct - 1) / prm->s, ng = g1 - g0 + 1;
             k_cmp_add<<<(unsigned)(K.cq * ng * 2 * (N / 256)), 256, 0, s>>>(C, d_out, n_groups, g0, ng);
+            counted();
             rc = launch_check();
         }
     return rc;
@@ -870,11 +1013,7 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
 // ------------------------------------------------------------------ the scan
 static int64_t chunk_pairs(int64_t total)
 {
-    int64_t ch = 16384; // large chunks: fewer launches and kernel tails (workspace 768 KiB per pair)
-    if (const char *e = getenv("BM_CHUNK_PAIRS")) {
-        long v = atol(e);
-        if (v > 0) ch = v;
-    }
+    int64_t ch = opt(BM_OPT_CHUNK_PAIRS); // large chunks: fewer launches and kernel tails (768 KiB of workspace per pair)
     return total < ch ? total : ch;
 }
 
@@ -997,18 +1136,22 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             beg(0, 2 * np);
             if (tswap) k_tensor<2, true><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+            counted();
             end();
             beg(1, 6 * np);
             k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
+            counted();
             end();
             beg(2, 6 * np);
             k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
+            counted();
             end();
             rc = launch_check();
         }
         if (log_s > 0 && !rc && order == BM_ORDER_HOISTED_ROT) {
             beg(5, 6 * np);
             k_hrot<<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufC, evk->hgk, prm->s);
+            counted();
             end();
             rc = launch_check();
         } else if (log_s > 0 && !rc) {
@@ -1017,15 +1160,25 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             // at most n_SM / 3 -> the 3-rank pipelined ladder (k_ladder_c3).  A large launch whose pair
             // count is not a multiple of n_SM runs its partial last wave the same way: the one-CTA
             // kernel takes floor(np / n_SM) full waves, the cluster kernels the remaining pairs.
+            // the cluster paths are used only while their clusters fit the device at once
+            // (DevCtx::max_cl, from cudaOccupancyMaxActiveClusters); a failed cluster launch falls
+            // back to the one-CTA ladder for the same pairs (identical residues)
+            const bool c2ok = opt(BM_OPT_LADDER_C2) != 0, c3ok = opt(BM_OPT_LADDER_C3) != 0;
+            auto one_cta = [&](int64_t p0, int64_t n) {
+                MatchK Kt = K;
+                Kt.pair0 = p0;
+                k_ladder_t<false><<<(unsigned)n, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
+                counted();
+            };
             auto cluster_ladder = [&](int64_t p0, int64_t n) {
-                const bool c3 = 3 * n <= C->n_sm && !getenv("BM_NO_LADDER_C3");
+                const int cs = (c3ok && n <= C->max_cl[3]) ? 3 : 2;
                 cudaLaunchConfig_t cfg = {};
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
-                attr[0].val.clusterDim.x = c3 ? 3 : 2;
+                attr[0].val.clusterDim.x = cs;
                 attr[0].val.clusterDim.y = 1;
                 attr[0].val.clusterDim.z = 1;
-                cfg.gridDim = dim3((unsigned)((c3 ? 3 : 2) * n));
+                cfg.gridDim = dim3((unsigned)(cs * n));
                 cfg.blockDim = dim3(T);
                 cfg.dynamicSmemBytes = LADDER_SMEM_BYTES;
                 cfg.stream = s;
@@ -1033,19 +1186,25 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
                 cfg.numAttrs = 1;
                 MatchK Kt = K;
                 Kt.pair0 = p0;
-                const cudaError_t e = c3 ? cudaLaunchKernelEx(&cfg, k_ladder_c3, Kt, bufC, (int)log_s)
-                                         : cudaLaunchKernelEx(&cfg, k_ladder_t<true>, Kt, bufC, (int)log_s);
-                if (e != cudaSuccess) rc = BM_ERR_CUDA;
+                const cudaError_t e = cs == 3 ? cudaLaunchKernelEx(&cfg, k_ladder_c3, Kt, bufC, (int)log_s)
+                                              : cudaLaunchKernelEx(&cfg, k_ladder_t<true>, Kt, bufC, (int)log_s);
+                if (e != cudaSuccess) {
+                    cudaGetLastError(); // not sticky: a launch-configuration error
+                    one_cta(p0, n);
+                } else {
+                    counted();
+                }
             };
-            const bool use_c2 = !getenv("BM_NO_LADDER_C2");
             const int64_t tail = np % C->n_sm;
-            if (2 * np <= C->n_sm && use_c2) {
+            const bool fits = c2ok && C->max_cl[2] > 0;
+            if (fits && np <= C->max_cl[2] && 2 * np <= C->n_sm) {
                 cluster_ladder(0, np);
-            } else if (np > C->n_sm && 2 * tail <= C->n_sm && tail > 0 && use_c2 && !getenv("BM_NO_LADDER_TAIL")) {
-                k_ladder_t<false><<<(unsigned)(np - tail), T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+            } else if (fits && opt(BM_OPT_LADDER_TAIL) && np > C->n_sm && tail > 0 && 2 * tail <= C->n_sm &&
+                       tail <= C->max_cl[2]) {
+                one_cta(0, np - tail);
                 cluster_ladder(np - tail, tail);
             } else {
-                k_ladder_t<false><<<npu, T, LADDER_SMEM_BYTES, s>>>(K, bufC, log_s);
+                one_cta(0, np);
             }
             end();
             rc = launch_check();
@@ -1053,6 +1212,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         if (log_s == 0 && !rc) {
             beg(6, 2 * np);
             k_out_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, bufC);
+            counted();
             end();
             rc = launch_check();
         }
@@ -1150,7 +1310,7 @@ static int host_groups(int64_t n_sets, int32_t nq)
     // about 576 (query, set) pairs per group (a few waves of the ladder kernel), at least 4 groups
     int64_t g = (n_sets * (int64_t)nq + 575) / 576;
     g = g < 4 ? 4 : g;
-    if (const char *e = getenv("BM_HOST_GROUPS")) g = atoi(e) > 0 ? atoi(e) : g;
+    if (opt(BM_OPT_HOST_GROUPS) > 0) g = opt(BM_OPT_HOST_GROUPS);
     return (int)(nq < g ? nq : g);
 }
 
@@ -1164,14 +1324,24 @@ size_t bm_match_host_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, 
     return HOST_SLOTS * (qbytes + obytes) + 2 * mws;
 }
 
-int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
-                  const uint64_t *h_q, int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order,
-                  void *stream)
+static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                           const uint64_t *h_q, int32_t nq, uint64_t *h_out, int32_t ring_rows, void *d_ws,
+                           size_t ws_bytes, int32_t order, void *stream)
 {
-    if (!prm || n_sets < 0 || nq < 0) return BM_ERR_INVALID_ARG;
+    if (!prm || n_sets < 0 || nq < 0 || ring_rows < 1) return BM_ERR_INVALID_ARG;
     if (n_sets == 0 || nq == 0) return BM_OK;
     if (!h_q || !h_out || !d_ws) return BM_ERR_INVALID_ARG;
     if (ws_bytes < bm_match_host_ws_bytes(prm, n_sets, nq, order)) return BM_ERR_WORKSPACE;
+    DevCtx *Cx;
+    int rc = ctx_get(&Cx);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(Cx->host_mu); // the internal streams are shared by the calls on this device
+    if (!Cx->hs[0])
+        for (int k = 0; k < 3; k++)
+            if (cudaStreamCreateWithFlags(&Cx->hs[k], cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                return BM_ERR_CUDA;
+            }
     const int G = host_groups(n_sets, nq);
     const int64_t gq = (nq + G - 1) / G;
     const size_t qrow = (size_t)prm->p * 4 * N, orow = (size_t)n_sets * 2 * N; // u64 per query
@@ -1183,11 +1353,7 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
     base += HOST_SLOTS * gq * orow;
     const size_t mws = (bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order) + 255) & ~(size_t)255;
     void *ws[2] = {base, (uint8_t *)base + mws};
-    cudaStream_t sc[2], su, sd;
-    sc[0] = (cudaStream_t)stream;
-    if (cudaStreamCreateWithFlags(&sc[1], cudaStreamNonBlocking) != cudaSuccess) return BM_ERR_CUDA;
-    cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+    cudaStream_t sc[2] = {(cudaStream_t)stream, Cx->hs[0]}, su = Cx->hs[1], sd = Cx->hs[2];
     // half-size first and last groups: the pipeline's unoverlapped head (first upload) and tail
     // (last download) shrink; the middle groups are gq queries
     std::vector<int64_t> g0, gn;
@@ -1203,52 +1369,83 @@ int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d
         if (tail) g0.push_back(q), gn.push_back(tail);
     }
     const int ngroups = (int)g0.size();
-    std::vector<cudaEvent_t> ev_up(ngroups), ev_done(ngroups), ev_down(ngroups);
-    for (int g = 0; g < ngroups; g++) {
-        cudaEventCreateWithFlags(&ev_up[g], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_down[g], cudaEventDisableTiming);
-    }
-    cudaEvent_t ev_start;
-    cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    // events: ev[g][0] upload done, [1] scan done, [2] download done (reusable after the call syncs)
+    std::vector<cudaEvent_t> ev(3 * (size_t)ngroups + 1);
+    for (auto &e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEvent_t ev_start = ev.back();
     cudaEventRecord(ev_start, sc[0]); // everything starts after the work already on the caller's stream
     cudaStreamWaitEvent(sc[1], ev_start, 0);
     cudaStreamWaitEvent(su, ev_start, 0);
-    int rc = BM_OK;
+    cudaStreamWaitEvent(sd, ev_start, 0);
     for (int g = 0; g < ngroups && !rc; g++) {
+        cudaEvent_t *E = &ev[3 * (size_t)g];
         const int slot = g % HOST_SLOTS;
         cudaStream_t cs = sc[g & 1];
         const int64_t q0 = g0[g], nqg = gn[g];
         // the query slot is free once the scan of group g - HOST_SLOTS has consumed it
-        if (g >= HOST_SLOTS) cudaStreamWaitEvent(su, ev_done[g - HOST_SLOTS], 0);
+        if (g >= HOST_SLOTS) cudaStreamWaitEvent(su, ev[3 * (size_t)(g - HOST_SLOTS) + 1], 0);
         if (cudaMemcpyAsync(dq[slot], h_q + q0 * qrow, nqg * qrow * 8, cudaMemcpyHostToDevice, su) != cudaSuccess)
             rc = BM_ERR_CUDA;
-        cudaEventRecord(ev_up[g], su);
-        cudaStreamWaitEvent(cs, ev_up[g], 0);
+        cudaEventRecord(E[0], su);
+        cudaStreamWaitEvent(cs, E[0], 0);
         // the output slot is free once group g - HOST_SLOTS's results are downloaded
-        if (g >= HOST_SLOTS) cudaStreamWaitEvent(cs, ev_down[g - HOST_SLOTS], 0);
+        if (g >= HOST_SLOTS) cudaStreamWaitEvent(cs, ev[3 * (size_t)(g - HOST_SLOTS) + 2], 0);
         if (!rc)
             rc = bm_match(prm, evk, d_db, n_sets, dq[slot], (int32_t)nqg, dout[slot], ws[g & 1], mws, order, cs);
-        cudaEventRecord(ev_done[g], cs);
-        cudaStreamWaitEvent(sd, ev_done[g], 0);
-        if (!rc && cudaMemcpyAsync(h_out + q0 * orow, dout[slot], nqg * orow * 8, cudaMemcpyDeviceToHost, sd) != cudaSuccess)
-            rc = BM_ERR_CUDA;
-        cudaEventRecord(ev_down[g], sd);
+        cudaEventRecord(E[1], cs);
+        cudaStreamWaitEvent(sd, E[1], 0);
+        // rows q0 .. q0 + nqg - 1 land at ring rows (q mod ring_rows): at most two contiguous runs
+        for (int64_t q = q0; q < q0 + nqg && !rc;) {
+            const int64_t r = q % ring_rows, run = std::min<int64_t>(q0 + nqg - q, ring_rows - r);
+            if (cudaMemcpyAsync(h_out + r * orow, dout[slot] + (q - q0) * orow, run * orow * 8, cudaMemcpyDeviceToHost,
+                                sd) != cudaSuccess)
+                rc = BM_ERR_CUDA;
+            q += run;
+        }
+        cudaEventRecord(E[2], sd);
     }
-    if (cudaStreamSynchronize(sd) != cudaSuccess || cudaStreamSynchronize(su) != cudaSuccess ||
-        cudaStreamSynchronize(sc[1]) != cudaSuccess || cudaStreamSynchronize(sc[0]) != cudaSuccess)
-        rc = rc ? rc : BM_ERR_CUDA;
-    for (int g = 0; g < ngroups; g++) {
-        cudaEventDestroy(ev_up[g]);
-        cudaEventDestroy(ev_done[g]);
-        cudaEventDestroy(ev_down[g]);
+    // the caller's stream waits for the internal streams (stream-ordered completion), then the call blocks
+    cudaEvent_t fin[3];
+    for (int k = 0; k < 3; k++) {
+        cudaEventCreateWithFlags(&fin[k], cudaEventDisableTiming);
+        cudaEventRecord(fin[k], k == 0 ? sc[1] : k == 1 ? su : sd);
+        cudaStreamWaitEvent(sc[0], fin[k], 0);
     }
-    cudaEventDestroy(ev_start);
-    cudaStreamDestroy(sc[1]);
-    cudaStreamDestroy(su);
-    cudaStreamDestroy(sd);
+    if (cudaStreamSynchronize(sc[0]) != cudaSuccess) rc = rc ? rc : BM_ERR_CUDA;
+    for (auto &e : ev) cudaEventDestroy(e);
+    for (auto &e : fin) cudaEventDestroy(e);
     return rc;
 }
+
+int bm_match_host(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                  const uint64_t *h_q, int32_t nq, uint64_t *h_out, void *d_ws, size_t ws_bytes, int32_t order,
+                  void *stream)
+{
+    return match_host_impl(prm, evk, d_db, n_sets, h_q, nq, h_out, nq > 0 ? nq : 1, d_ws, ws_bytes, order, stream);
+}
+
+int bm_match_host_ring(const bm_params *prm, const bm_evk_dev *evk, const uint64_t *d_db, int64_t n_sets,
+                       const uint64_t *h_q, int32_t nq, uint64_t *h_ring, int32_t ring_rows, void *d_ws,
+                       size_t ws_bytes, int32_t order, void *stream)
+{
+    return match_host_impl(prm, evk, d_db, n_sets, h_q, nq, h_ring, ring_rows, d_ws, ws_bytes, order, stream);
+}
+
+int bm_set_option(int32_t key, int64_t value)
+{
+    if (key < 0 || key >= BM_OPT_COUNT_) return BM_ERR_INVALID_ARG;
+    const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL;
+    if (flag ? (value != 0 && value != 1) : key == BM_OPT_HOST_GROUPS ? value < 0 : value < 1) return BM_ERR_INVALID_ARG;
+    g_opt[key].store(value);
+    return BM_OK;
+}
+int64_t bm_get_option(int32_t key)
+{
+    if (key < 0 || key >= BM_OPT_COUNT_) return BM_ERR_INVALID_ARG;
+    return opt(key);
+}
+int64_t bm_launch_count(void) { return g_launches.load(); }
+void bm_launch_count_reset(void) { g_launches.store(0); }
 
 int bm_sync(void *stream)
 {

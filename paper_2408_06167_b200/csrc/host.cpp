@@ -1,11 +1,14 @@
 // host.cpp -- host (client-side) part of libblindmatch: parameters, key generation,
 // packing + encoding, decryption, argmax.  Compiled by g++ (needs libquadmath for the
 // exact Gaussian CDT).  Device work lives in device.cu.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 #include <quadmath.h>
 
@@ -577,10 +580,27 @@ int bm_evk_import(const bm_params *prm, const uint64_t *rlk, const uint64_t *gk,
 
 // ------------------------------------------------------------------ encoding
 // pt_k = round(Delta * (2/N) Re(sum_t X[t] w^(k t))), X[5^j mod 2N] = z_j, w = exp(i pi / N):
-// one 2N-point complex FFT (positive exponent) per plaintext.
+// one 2N-point complex FFT (positive exponent) per plaintext.  The twiddles w^m, m < N, come from
+// one table computed in long double (a configs[3] database is 32,768 plaintexts: per-butterfly
+// cos / sin calls made the encoder the setup's bottleneck).
+static const std::vector<std::complex<double>> &fft_twiddles()
+{
+    static std::vector<std::complex<double>> w;
+    static std::once_flag f;
+    std::call_once(f, [] {
+        w.resize(N);
+        for (int m = 0; m < N; m++) {
+            const long double a = 3.141592653589793238462643383279502884L * m / N; // 2 pi m / 2N
+            w[m] = std::complex<double>((double)cosl(a), (double)sinl(a));
+        }
+    });
+    return w;
+}
+
 static void fft_pos(std::vector<std::complex<double>> &a)
 {
-    const int n = (int)a.size();
+    const int n = (int)a.size(); // 2N
+    const std::vector<std::complex<double>> &W = fft_twiddles();
     for (int i = 1, j = 0; i < n; i++) {
         int bit = n >> 1;
         for (; j & bit; bit >>= 1) j ^= bit;
@@ -588,16 +608,39 @@ static void fft_pos(std::vector<std::complex<double>> &a)
         if (i < j) std::swap(a[i], a[j]);
     }
     for (int len = 2; len <= n; len <<= 1) {
-        double ang = 2 * M_PI / len;
+        const int step = n / len; // w_len^k = exp(2 pi i k / len) = W[k n / len]
         for (int i = 0; i < n; i += len)
             for (int k = 0; k < len / 2; k++) {
-                std::complex<double> w(std::cos(ang * k), std::sin(ang * k));
-                std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * W[k * step];
                 a[i + k] = u + v;
                 a[i + k + len / 2] = u - v;
             }
     }
 }
+
+// run f(i) for i < n on up to hardware_concurrency threads (encoding is per plaintext independent);
+// returns the first nonzero status
+extern "C++" {
+template <typename F> static int parallel_for(int64_t n, F f)
+{
+    int nt = (int)std::min<int64_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; i++)
+            if (int rc = f(i)) return rc;
+        return BM_OK;
+    }
+    std::atomic<int64_t> next(0);
+    std::atomic<int> status(BM_OK);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; t++)
+        th.emplace_back([&] {
+            for (int64_t i; (i = next.fetch_add(1)) < n && status.load() == BM_OK;)
+                if (int rc = f(i)) status.store(rc);
+        });
+    for (auto &x : th) x.join();
+    return status.load();
+}
+} // extern "C++"
 
 static const std::vector<int> &slot_exp()
 {
@@ -653,20 +696,18 @@ int bm_encode_db(const bm_params *prm, const double *tmpl, int64_t n, int64_t fi
         int rc = unit_rows(tmpl + lo * d, hi - lo, d, unit);
         if (rc) return rc;
     }
-    std::vector<double> z(SLOTS);
-    for (int64_t t = 0; t < n_sets; t++)
-        for (int i = 0; i < p; i++) {
-            std::fill(z.begin(), z.end(), 0.0);
-            for (int k = 0; k < B; k++) {
-                int64_t u = (first_set + t) * B + k;
-                if (u >= n) break;
-                const double *v = &unit[(u - lo) * d];
-                for (int j = 0; j < s; j++) z[k * s + j] = v[i * s + j];
-            }
-            int rc = encode_slots(z.data(), pt + ((size_t)t * p + i) * N);
-            if (rc) return rc;
+    return parallel_for(n_sets * p, [&](int64_t ti) {
+        const int64_t t = ti / p;
+        const int i = (int)(ti % p);
+        std::vector<double> z(SLOTS, 0.0);
+        for (int k = 0; k < B; k++) {
+            int64_t u = (first_set + t) * B + k;
+            if (u >= n) break;
+            const double *v = &unit[(u - lo) * d];
+            for (int j = 0; j < s; j++) z[k * s + j] = v[i * s + j];
         }
-    return BM_OK;
+        return encode_slots(z.data(), pt + ((size_t)t * p + i) * N);
+    });
 }
 
 int bm_encode_query(const bm_params *prm, const double *q, int64_t nq, int64_t *pt)
@@ -678,14 +719,13 @@ int bm_encode_query(const bm_params *prm, const double *q, int64_t nq, int64_t *
         int rc = unit_rows(q, nq, d, unit);
         if (rc) return rc;
     }
-    std::vector<double> z(SLOTS);
-    for (int64_t j = 0; j < nq; j++)
-        for (int i = 0; i < p; i++) {
-            for (int x = 0; x < SLOTS; x++) z[x] = unit[j * d + i * s + (x % s)];
-            int rc = encode_slots(z.data(), pt + ((size_t)j * p + i) * N);
-            if (rc) return rc;
-        }
-    return BM_OK;
+    return parallel_for(nq * p, [&](int64_t ji) {
+        const int64_t j = ji / p;
+        const int i = (int)(ji % p);
+        std::vector<double> z(SLOTS);
+        for (int x = 0; x < SLOTS; x++) z[x] = unit[j * d + i * s + (x % s)];
+        return encode_slots(z.data(), pt + ((size_t)j * p + i) * N);
+    });
 }
 
 // f3: the client's single query ciphertext holds the unit query tiled S/d times,
@@ -834,13 +874,14 @@ int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, in
 {
     if (!prm || !sk || (!ct && n) || (!m && n) || n < 0) return BM_ERR_INVALID_ARG;
     if (memcmp(sk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
-    std::vector<uint64_t> s(N), t(N);
+    std::vector<uint64_t> s(N);
     for (int k = 0; k < N; k++) s[k] = to_res(sk->s[k], Q0);
     host_ntt_fwd(s.data(), 0);
-    for (int64_t c = 0; c < n; c++) {
+    return parallel_for(n, [&](int64_t c) {
+        std::vector<uint64_t> t(N);
         const uint64_t *c0 = ct + (size_t)c * 2 * N, *c1 = c0 + N;
         for (int k = 0; k < N; k++)
-            if (c0[k] >= Q0 || c1[k] >= Q0) return BM_ERR_INVALID_ARG;
+            if (c0[k] >= Q0 || c1[k] >= Q0) return (int)BM_ERR_INVALID_ARG;
         memcpy(t.data(), c1, 8 * N);
         host_ntt_fwd(t.data(), 0);
         for (int k = 0; k < N; k++) t[k] = mulmod_h(t[k], s[k], Q0);
@@ -849,8 +890,8 @@ int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, in
             uint64_t v = (c0[k] + t[k]) % Q0;
             m[(size_t)c * N + k] = v > Q0 / 2 ? (int64_t)v - (int64_t)Q0 : (int64_t)v;
         }
-    }
-    return BM_OK;
+        return (int)BM_OK;
+    });
 }
 
 int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, double *scores)
@@ -867,7 +908,7 @@ int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_
         for (int i = 0; i < 2 * N; i++) cosT[i] = std::cos(M_PI * i / N);
     });
     const std::vector<int> &e = slot_exp();
-    for (int64_t c = 0; c < n; c++)
+    return parallel_for(n, [&](int64_t c) {
         for (int k = 0; k < prm->B; k++) {
             uint64_t ex = (uint64_t)e[(size_t)k * prm->s];
             double acc = 0;
@@ -875,7 +916,8 @@ int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_
             for (int t = 0; t < N; t++) acc += (double)mm[t] * cosT[(ex * t) % (2 * N)];
             scores[(size_t)c * prm->B + k] = acc / prm->out_scale;
         }
-    return BM_OK;
+        return (int)BM_OK;
+    });
 }
 
 // f1: packed (compressed) results: every slot is a score -- slot k s + u of packed ciphertext g is set

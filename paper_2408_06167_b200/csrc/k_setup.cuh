@@ -134,3 +134,72 @@ __global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
         }
     }
 }
+
+// ================================================================== client-side decryption on the device (a9)
+// PAPER.md:347-349 (the client decrypts the returned ciphertexts and reads the score slots), at the
+// scale of a 1:N identification batch: one CTA per level-0 ciphertext (c0, c1) in the canonical
+// coefficient domain (bm_match's output):
+//   m = c0 + INTT_q0(NTT_q0(c1) * NTT_q0(s))  (mod q0), centred      -- 2 transforms
+//   X[t] = sum_k m_k zeta^(k (2t + 1)), zeta = exp(i pi / N)          -- the canonical embedding at
+//          the odd powers: y_k = m_k zeta^k, then an N-point FP64 FFT (positive exponent) in shared memory
+//   score[b] = Re X[t(b s)] / out_scale, t(j) = (5^j mod 2N - 1) / 2   (slot j = b s holds template b)
+// The host bm_decrypt evaluates the same slots by the direct O(N) cosine sum (the reference the GPU
+// test compares against).
+struct DecK {
+    PrimeK pr0;
+    const uint64_t *s;      // planar Shoup key of the secret, NTT domain mod q0 (2N u64)
+    const uint64_t *ct;     // [n][2][N] level 0, coefficient domain
+    double *scores;         // [n][B]
+    const double2 *zeta;    // [N]: exp(i pi k / N)
+    const int32_t *slot_t;  // [S]: t(j)
+    int32_t B, s_len;
+    double inv_scale;
+};
+constexpr size_t DEC_SMEM_BYTES = (size_t)N * sizeof(double2); // 128 KiB (also holds the NTT exchanges)
+
+__global__ void __launch_bounds__(T, 1) k_decrypt(DecK K)
+{
+    extern __shared__ uint64_t sm[];
+    double2 *X = reinterpret_cast<double2 *>(sm);
+    const int tid = threadIdx.x;
+    const int64_t c = blockIdx.x;
+    const uint64_t *c0 = K.ct + (size_t)c * 2 * N, *c1 = c0 + N;
+    uint64_t a[E];
+    load_coef(a, c1);
+    fwd<0, false>(a, sm, K.pr0); // [0, 2 q0)
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+        ulonglong2 w, wb;
+        ldkey2(K.s, pos_M4(tid, e), w, wb);
+        a[e] = shoup4<0>(a[e], w);       // [0, 4 q0): the inverse transform's input bound
+        a[e + 1] = shoup4<0>(a[e + 1], wb);
+    }
+    inv<0>(a, sm, K.pr0); // c1 s, canonical, coefficient j_M1(tid, e)
+    __syncthreads();      // the exchange buffer becomes X
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int k = j_M1(tid, e);
+        uint64_t v = a[e] + c0[k];
+        v = v >= Q0 ? v - Q0 : v;
+        const double m = v > (Q0 >> 1) ? -(double)(Q0 - v) : (double)v; // centred, exact (< 2^53 in practice)
+        const double2 z = K.zeta[k];
+        X[brev13(k)] = make_double2(m * z.x, m * z.y);
+    }
+    __syncthreads();
+    // iterative radix-2 DIT over bit-reversed input: block length len, twiddle exp(2 pi i k / len) = zeta[2 k N / len]
+#pragma unroll 1
+    for (int lg = 1; lg <= LOGN; lg++) {
+        const int half = 1 << (lg - 1);
+        for (int b = tid; b < N / 2; b += T) {
+            const int k = b & (half - 1);
+            const int i = ((b >> (lg - 1)) << lg) + k, j = i + half;
+            const double2 w = K.zeta[(2 * k) << (LOGN - lg)];
+            const double2 u = X[i], v = X[j];
+            const double vr = v.x * w.x - v.y * w.y, vi = v.x * w.y + v.y * w.x;
+            X[i] = make_double2(u.x + vr, u.y + vi);
+            X[j] = make_double2(u.x - vr, u.y - vi);
+        }
+        __syncthreads();
+    }
+    for (int b = tid; b < K.B; b += T) K.scores[(size_t)c * K.B + b] = X[K.slot_t[b * K.s_len]].x * K.inv_scale;
+}

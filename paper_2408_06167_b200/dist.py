@@ -77,14 +77,24 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
     [G][W][nq/(G W)][n_local][2][N].  Group g's broadcast and result all_to_all run on
     `comm_stream` while other groups are scanned on `compute_stream`: the collectives are issued in
     the same order on every rank (b0, b1, then a_g, b_{g+2}, ...), broadcasts two groups ahead.
-    With one rank, or without CUDA streams (gloo), the same sequence runs in order."""
+    With one rank, or without CUDA streams (gloo), the same sequence runs in order.
+
+    Bounded outputs (result sets larger than memory, BASELINE.json configs[3]): d_out and recv may
+    instead be LISTS of R slots ([nq/G][n_local][2][N] and [W][nq/(G W)][n_local][2][N]); group g
+    uses slot g mod R, overwriting group g - R's results (a slot is rewritten only after its
+    previous all_to_all has completed)."""
     w, _ = world()
     nq = d_q.shape[0]
     G = groups
     assert nq % G == 0
     gq = nq // G
     qs = [d_q[g * gq:(g + 1) * gq] for g in range(G)]
-    outs = [d_out[g * gq:(g + 1) * gq] for g in range(G)]
+    ring = isinstance(d_out, (list, tuple))
+    if ring:
+        outs = [d_out[g % len(d_out)] for g in range(G)]
+        recv = [recv[g % len(recv)] for g in range(G)] if recv is not None else None
+    else:
+        outs = [d_out[g * gq:(g + 1) * gq] for g in range(G)]
     cuda = comm_stream is not None and compute_stream is not None
     if not cuda:
         for g in range(G):
@@ -95,6 +105,8 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
         return recv
     bw = [None] * G
     done = [None] * G
+    sent = [None] * G
+    R = len(d_out) if ring else G
 
     def bcast(g):
         if w > 1:
@@ -106,6 +118,8 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
             with torch.cuda.stream(comm_stream):
                 comm_stream.wait_event(done[g])
                 dist.all_to_all_single(recv[g].view(-1), outs[g].view(-1), async_op=True).wait()
+                sent[g] = torch.cuda.Event()
+                sent[g].record(comm_stream)
 
     compute_stream.wait_stream(torch.cuda.current_stream())
     comm_stream.wait_stream(torch.cuda.current_stream())
@@ -115,6 +129,8 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
         with torch.cuda.stream(compute_stream):
             if bw[g] is not None:
                 bw[g].wait()
+            if g >= R and sent[g - R] is not None:   # the slot's previous results have left
+                compute_stream.wait_event(sent[g - R])
             match(g, qs[g], outs[g])
             done[g] = torch.cuda.Event()
             done[g].record(compute_stream)
@@ -129,10 +145,11 @@ def scan_pipelined(match, d_q, d_out, recv, groups, comm_stream=None, compute_st
     return recv
 
 
-def p2p_row_map(nq, groups, world_size):
+def p2p_row_map(nq, groups, world_size, ring=None):
     """[(root rank, row in the root's buffer)] for every query of a batch, with the roots of the
     pipelined all_to_all (group g's queries split into W equal blocks, block k -> rank k): the root
-    holds its G nq/(G W) rows in (group, block position) order."""
+    holds its G nq/(G W) rows in (group, block position) order.  With ring = R the root holds only R
+    groups' rows: group g's rows are slot g mod R (bounded outputs; later groups overwrite)."""
     assert nq % (groups * world_size) == 0, "nq must be a multiple of groups x world size"
     gq = nq // groups
     per = gq // world_size
@@ -140,7 +157,7 @@ def p2p_row_map(nq, groups, world_size):
     for j in range(nq):
         g, i = divmod(j, gq)
         k, m = divmod(i, per)
-        out.append((k, g * per + m))
+        out.append((k, (g if ring is None else g % ring) * per + m))
     return out
 
 
@@ -187,19 +204,23 @@ class P2PGather:
     handles of their buffers (all_gather_object) and open their peers', so `rows` holds, for every
     query of the batch, the device address of its row on its root GPU (nq int64 on this device)."""
 
-    def __init__(self, B, res, nq, groups, n_sets_global):
+    def __init__(self, B, res, nq, groups, n_sets_global, ring=None):
         w, r = world()
         self.B = B
         self.res = res
+        self.ring = ring
         row_bytes = n_sets_global * 2 * B.N * 8
-        assert res.is_cuda and res.dtype == torch.int64 and res.is_contiguous()
-        assert res.numel() * 8 >= (nq // w) * row_bytes
+        if not (res.is_cuda and res.dtype == torch.int64 and res.is_contiguous()):
+            raise ValueError("P2PGather: res must be a contiguous int64 CUDA tensor")
+        n_rows = nq // w if ring is None else ring * (nq // groups // w)
+        if res.numel() * 8 < n_rows * row_bytes:
+            raise ValueError(f"P2PGather: res holds {res.numel() * 8} bytes, the rows need {n_rows * row_bytes}")
         self.opened = []
         if w == 1:
             bases = [res.data_ptr()]
         else:
             bases = exchange_ipc_bases(B, res, self.opened)
-        addrs = [bases[k] + row * row_bytes for k, row in p2p_row_map(nq, groups, w)]
+        addrs = [bases[k] + row * row_bytes for k, row in p2p_row_map(nq, groups, w, ring)]
         self.rows = torch.tensor(addrs, dtype=torch.int64, device=res.device)
         self.gq = nq // groups
 
@@ -214,38 +235,45 @@ class P2PGather:
 
 def scan_p2p(match_rows, d_q, gather, groups, comm_stream, compute_stream, flag):
     """a3 + scan + fused a8: group g's broadcast runs on `comm_stream` two groups ahead while the
-    scans run on `compute_stream`; match_rows(g, q_slice, rows_slice) writes every result straight
-    to its root (gather.rows_of(g)).  `flag` (one float64 on this device) is all-reduced on the
-    compute stream after the last scan: NCCL completes it only when every rank has passed its
-    scans, so each root's buffer is complete once the call's work on the current stream is."""
+    scans run on `compute_stream` (or, given a list of streams, group g on stream g mod len: one
+    group's kernels fill the tails of the previous group's); match_rows(g, q_slice, rows_slice)
+    writes every result straight to its root (gather.rows_of(g)).  `flag` (one float64 on this
+    device) is all-reduced after the last scan of every stream: NCCL completes it only when every
+    rank has passed its scans, so each root's buffer is complete once the call's work on the current
+    stream is."""
     w, _ = world()
     nq = d_q.shape[0]
     G = groups
     gq = nq // G
     qs = [d_q[g * gq:(g + 1) * gq] for g in range(G)]
     bw = [None] * G
+    cs = list(compute_stream) if isinstance(compute_stream, (list, tuple)) else [compute_stream]
 
     def bcast(g):
         if w > 1:
             with torch.cuda.stream(comm_stream):
                 bw[g] = dist.broadcast(qs[g], src=0, async_op=True)
 
-    compute_stream.wait_stream(torch.cuda.current_stream())
+    for s in cs:
+        s.wait_stream(torch.cuda.current_stream())
     comm_stream.wait_stream(torch.cuda.current_stream())
     for g in range(min(2, G)):
         bcast(g)
     for g in range(G):
-        with torch.cuda.stream(compute_stream):
+        s = cs[g % len(cs)]
+        with torch.cuda.stream(s):
             if bw[g] is not None:
                 bw[g].wait()
             match_rows(g, qs[g], gather.rows_of(g))
         if g + 2 < G:
             bcast(g + 2)
-    with torch.cuda.stream(compute_stream):
+    for s in cs[1:]:
+        cs[0].wait_stream(s)
+    with torch.cuda.stream(cs[0]):
         if w > 1:
             dist.all_reduce(flag)
     cur = torch.cuda.current_stream()
-    cur.wait_stream(compute_stream)
+    cur.wait_stream(cs[0])
     cur.wait_stream(comm_stream)
 
 

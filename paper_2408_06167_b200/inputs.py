@@ -56,6 +56,22 @@ def templates(cfg, n=None, first=0):
     return out
 
 
+def template_rows(cfg, rows):
+    """templates(cfg, 1, u)[0] for every u in rows (the same values), drawing each 65,536-row chunk
+    once up to the last row needed from it."""
+    d = CONFIGS[cfg]["d"]
+    rows = np.asarray(rows, np.int64)
+    out = np.empty((rows.size, d))
+    CH = 65536
+    for ch in np.unique(rows // CH):
+        sel = np.nonzero(rows // CH == ch)[0]
+        hi = int((rows[sel] - ch * CH).max()) + 1
+        rng = np.random.default_rng([DATA_SEED_BASE + cfg, int(ch)])
+        block = _unit(rng.standard_normal((hi, d)))
+        out[sel] = block[rows[sel] - ch * CH]
+    return out
+
+
 def queries(cfg, nq=None):
     """Queries [nq][d] float64 unit norm, and the expected genuine template index (-1 = impostor).
 
@@ -87,7 +103,7 @@ def queries(cfg, nq=None):
         u = rng.choice(c["n"], size=n_gen, replace=False)
     else:
         u = 4 * rng.choice(c["n"] // 4, size=n_gen, replace=False)
-    gen = np.stack([templates(cfg, 1, int(x))[0] for x in u]) if n_gen else np.zeros((0, d))
+    gen = template_rows(cfg, u) if n_gen else np.zeros((0, d))
     gen = _unit(gen + rng.standard_normal((n_gen, d)) * 0.05)
     imp = _unit(rng.standard_normal((nq - n_gen, d)))
     return np.concatenate([gen, imp]), np.concatenate([u, np.full(nq - n_gen, -1)])

@@ -84,7 +84,7 @@ def test_compressed_scan_parity(env, O, d, p, n_tmpl, nq):
 
 
 def test_compressed_scan_chunked_and_scores(env, O):
-    """Chunks that split the sets of a packed group (BM_CHUNK_PAIRS = 5) give the same residues; the
+    """Chunks that split the sets of a packed group (option cmp_chunk = 5) give the same residues; the
     packed slots decrypt to the plaintext cosines (1e-6) with the genuine template on top."""
     torch, B = env
     d, p = 16, 4
@@ -93,11 +93,8 @@ def test_compressed_scan_chunked_and_scores(env, O):
     Q /= np.linalg.norm(Q)
     st = CSetup(env, O, d, p, T, Q)
     whole = st.gpu()
-    os.environ["BM_CHUNK_PAIRS"] = "5"
-    try:
+    with B.options(cmp_chunk=5):
         parts = st.gpu()
-    finally:
-        del os.environ["BM_CHUNK_PAIRS"]
     assert np.array_equal(whole, parts)
     S, s, Bk = O.layout(LOGN, d, p)
     slots = B.bm_decrypt_packed(st.prm, st.sk, whole.reshape(-1, 2, 1, 8192))

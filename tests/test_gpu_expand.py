@@ -97,16 +97,13 @@ def test_expand_parity(env, O, d, p, nq):
 
 
 def test_expand_chunked_equals_unchunked(env, O):
-    """Several launches (BM_EXPAND_CHUNK = 8 parts = one query per chunk) give the same residues."""
+    """Several launches (option expand_chunk = 8 parts = one query per chunk) give the same residues."""
     Q = I.random_unit(3, 64, 5)
     st = XSetup(env, O, 64, 8, Q)
     d_in = st.from_oracle(st.oct, 3)
     whole = st.to_coeff(st.gpu_expand(d_in), 2)
-    os.environ["BM_EXPAND_CHUNK"] = "8"
-    try:
+    with st.B.options(expand_chunk=8):
         parts = st.to_coeff(st.gpu_expand(d_in), 2)
-    finally:
-        del os.environ["BM_EXPAND_CHUNK"]
     assert np.array_equal(whole, parts)
     assert np.array_equal(whole[2], O.expand(LOGN, 64, 8, st.masks, st.ogk1, st.oct[2:3])[0])
 

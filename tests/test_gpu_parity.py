@@ -153,20 +153,20 @@ def test_paper_order_parity(env, O):
     assert not np.array_equal(hoisted[1, 3], got[1, 3])  # reading R8: orders differ in residues
 
 
-@pytest.mark.parametrize("chunk", ["7", "1"])
-def test_chunking_ragged(env, O, monkeypatch, chunk):
-    """Pairs processed in small chunks (BM_CHUNK_PAIRS): 5 queries x 2 sets; chunk 7 gives query
+@pytest.mark.parametrize("chunk", [7, 1])
+def test_chunking_ragged(env, O, chunk):
+    """Pairs processed in small chunks (option chunk_pairs): 5 queries x 2 sets; chunk 7 gives query
     blocks of 3 + 2 (ragged 2x2 tensor tiles), chunk 1 splits the set range too."""
-    monkeypatch.setenv("BM_CHUNK_PAIRS", chunk)
+    torch, B = env
     T = I.random_unit(300, 32, 5)
     Q = I.random_unit(5, 32, 6)
     st = Setup(env, O, 32, 2, T, Q)       # s = 16, B = 256 -> 2 sets; last set ragged (44 templates)
-    got = st.gpu_match(0)
+    with B.options(chunk_pairs=chunk):
+        got = st.gpu_match(0)
     pairs = [(4, 1), (3, 0), (0, 1)]
     ref = st.oracle_pairs(pairs)
     for k, (j, t) in enumerate(pairs):
         assert np.array_equal(got[j, t], ref[k])
-    monkeypatch.delenv("BM_CHUNK_PAIRS")
     again = st.gpu_match(0)
     assert np.array_equal(got, again)
 
@@ -207,20 +207,25 @@ def test_edge_cases_and_errors(env, O):
     assert e.value.name == "BM_ERR_INVALID_ARG"
 
 
-@pytest.mark.parametrize("groups", ["3", "8"])
-def test_match_host_pipelined_equals_device(env, O, monkeypatch, groups):
-    """bm_match_host (host buffers, grouped + overlapped copies) == bm_match on device buffers."""
+@pytest.mark.parametrize("groups", [3, 8])
+def test_match_host_pipelined_equals_device(env, O, groups):
+    """bm_match_host (host buffers, grouped + overlapped copies) == bm_match on device buffers;
+    bm_match_host_ring with a 3-row host ring holds the last 3 queries' rows (query j at row j mod 3)."""
     torch, B = env
-    monkeypatch.setenv("BM_HOST_GROUPS", groups)
     T = I.templates(2, 700)
     Q, _ = I.queries(2, 7)
     st = Setup(env, O, 128, 8, T, Q)
     dev_out = st.gpu_match(0)
     h_q = st.d_q.cpu().pin_memory()
     h_out = torch.empty((st.nq, st.n_sets, 2, 8192), dtype=torch.int64).pin_memory()
-    ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq), dtype=torch.uint8, device="cuda")
-    B.bm_match_host(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, h_out, ws)
-    assert np.array_equal(h_out.numpy().view(np.uint64), dev_out)
+    with B.options(host_groups=groups):
+        ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq), dtype=torch.uint8, device="cuda")
+        B.bm_match_host(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, h_out, ws)
+        assert np.array_equal(h_out.numpy().view(np.uint64), dev_out)
+        ring = torch.zeros((3, st.n_sets, 2, 8192), dtype=torch.int64).pin_memory()
+        B.bm_match_host_ring(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, ring, 3, ws)
+        for j in range(st.nq - 3, st.nq):
+            assert np.array_equal(ring[j % 3].numpy().view(np.uint64), dev_out[j]), j
 
 
 def test_scan_pipelined_streams_equal_device(env, O):
@@ -303,8 +308,8 @@ def test_hoisted_rotation_needs_its_keys(env, O):
     assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
 
 
-@pytest.mark.parametrize("order,chunk", [(0, None), (0, "5"), (2, None), (1, None)])
-def test_match_rows_fused_gather(env, O, monkeypatch, order, chunk):
+@pytest.mark.parametrize("order,chunk", [(0, None), (0, 5), (2, None), (1, None)])
+def test_match_rows_fused_gather(env, O, order, chunk):
     """bm_match_rows (a8 fused into the output kernels, the multi-GPU gather path of dist.P2PGather):
     results land in caller-given rows at global set numbers.  Rows in reversed order inside a wider
     row buffer (n_sets + 3 global sets, this 'rank' at set offset 2) must hold exactly bm_match's
@@ -313,7 +318,7 @@ def test_match_rows_fused_gather(env, O, monkeypatch, order, chunk):
     outside this rank's set range is touched."""
     torch, B = env
     if chunk:
-        monkeypatch.setenv("BM_CHUNK_PAIRS", chunk)
+        B.bm_set_option("chunk_pairs", chunk)
     T = I.random_unit(700, 64, 21)
     Q = I.random_unit(3, 64, 22)
     st = Setup(env, O, 64, 4, T, Q, hoisted=(order == 2))   # s = 16, B = 256 -> 3 sets
@@ -334,8 +339,9 @@ def test_match_rows_fused_gather(env, O, monkeypatch, order, chunk):
     # the IPC handle of the row buffer (what P2PGather exchanges) and its offset inside the allocation
     h, o = B.bm_ipc_handle(res)
     assert len(h) == 64 and 0 <= o < 1 << 40
-    with pytest.raises(B.BMError):
+    with pytest.raises(ValueError):
         B.bm_match_rows(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q, st.nq, rows, -1, ws, order)
+    B.bm_set_option("chunk_pairs", 16384)
 
 
 def test_small_query_batches_swapped_tensor_tiles(env, O):
@@ -361,43 +367,94 @@ def test_small_query_batches_swapped_tensor_tiles(env, O):
 
 
 @pytest.mark.parametrize("order,c3", [(0, False), (1, False), (0, True), (1, True)])
-def test_latency_mode_cluster_ladder(env, O, monkeypatch, order, c3):
+def test_latency_mode_cluster_ladder(env, O, order, c3):
     """Launches with fewer pairs than half the SMs run the ladder on 2-CTA clusters (k_ladder_t<true>:
     rank c owns component c, c1 copied over DSMEM each step): bit-identical to the one-CTA ladder
-    (BM_NO_LADDER_C2=1) and to the oracle, for the hoisted and the paper order, s = 16 (4 steps)
+    (option ladder_c2 = 0) and to the oracle, for the hoisted and the paper order, s = 16 (4 steps)
     and s = 2 (the last step is the first); likewise the 3-rank pipelined ladder (k_ladder_c3,
     the default at <= n_SM / 3 pairs: the c1 chain in two domains, sigma applied to coefficients)."""
     torch, B = env
-    if not c3:   # the 3-rank pipelined ladder (k_ladder_c3) is the default at <= n_SM / 3 pairs
-        monkeypatch.setenv("BM_NO_LADDER_C3", "1")
     for d, p, n in ((64, 4, 600), (16, 8, 900)):
         T = I.random_unit(n, d, 41)
         Q = I.random_unit(2, d, 42)
         st = Setup(env, O, d, p, T, Q)
         assert 2 * st.nq * st.n_sets <= 148
-        got = st.gpu_match(order)
-        monkeypatch.setenv("BM_NO_LADDER_C2", "1")
-        ref_gpu = st.gpu_match(order)
-        monkeypatch.delenv("BM_NO_LADDER_C2")
+        # the 3-rank pipelined ladder (k_ladder_c3) is the default at <= n_SM / 3 pairs
+        with B.options(ladder_c3=int(c3)):
+            got = st.gpu_match(order)
+        with B.options(ladder_c2=0):
+            ref_gpu = st.gpu_match(order)
         assert np.array_equal(got, ref_gpu), (d, p)
         ref = st.oracle_pairs([(1, st.n_sets - 1)], order)
         assert np.array_equal(got[1, st.n_sets - 1], ref[0]), (d, p)
 
 
-def test_ladder_tail_wave_on_clusters(env, O, monkeypatch):
+@pytest.mark.parametrize("extra", [12, 60])
+def test_ladder_tail_wave_on_clusters(env, O, extra):
     """A launch of more than n_SM pairs whose last wave is at most half full runs that wave on the
-    cluster ladder (floor(np / n_SM) full waves on k_ladder_t<false>, the rest on k_ladder_c3 /
-    k_ladder_t<true> from pair offset MatchK::pair0): 160 pairs (tail 12) equal the one-kernel
-    launch (BM_NO_LADDER_TAIL=1) bit for bit, and a tail pair equals the oracle."""
+    cluster ladder (floor(np / n_SM) full waves on k_ladder_t<false>, the rest from pair offset
+    MatchK::pair0 on k_ladder_c3 when tail <= n_SM / 3, else on k_ladder_t<true>): n_SM + extra pairs
+    (extra = 12: the 3-CTA tail; extra = 60: n_SM / 3 < tail <= n_SM / 2, the 2-CTA tail) equal the
+    one-kernel launch (option ladder_tail = 0) bit for bit, and a tail pair equals the oracle.  The
+    pair count comes from the device's SM count."""
     torch, B = env
-    T = I.random_unit(40 * 2048, 16, 51)
-    Q = I.random_unit(4, 16, 52)
-    st = Setup(env, O, 16, 8, T, Q)          # s = 2, B = 2048 -> 40 sets x 4 queries = 160 pairs
-    assert st.n_sets * st.nq == 160
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    np_ = n_sm + extra
+    assert 0 < extra and 2 * extra <= n_sm and (extra > n_sm // 3) == (extra == 60)
+    nq = 1
+    n_sets = np_                              # 1 query x n_SM + extra sets of B = 2048 templates
+    T = I.random_unit(n_sets * 2048 - 100, 16, 51)
+    Q = I.random_unit(nq, 16, 52)
+    st = Setup(env, O, 16, 8, T, Q)          # s = 2
+    assert st.n_sets * st.nq == np_
     got = st.gpu_match(0)
-    monkeypatch.setenv("BM_NO_LADDER_TAIL", "1")
-    ref_gpu = st.gpu_match(0)
-    monkeypatch.delenv("BM_NO_LADDER_TAIL")
+    with B.options(ladder_tail=0):
+        ref_gpu = st.gpu_match(0)
     assert np.array_equal(got, ref_gpu)
-    ref = st.oracle_pairs([(3, 39)])
-    assert np.array_equal(got[3, 39], ref[0])
+    ref = st.oracle_pairs([(0, np_ - 1), (0, np_ - extra)])
+    assert np.array_equal(got[0, np_ - 1], ref[0]) and np.array_equal(got[0, np_ - extra], ref[1])
+
+
+def test_decrypt_dev_equals_host_decrypt(env, O):
+    """bm_decrypt_dev (client-side decryption on the device: c0 + c1 s by NTT, FP64 FFT decode) gives
+    the scores of the host bm_decrypt (the direct O(N) cosine sum of PAPER.md:347-349's decode) to
+    1e-9, and both the float64 cosines to 1e-6; the launch counter sees the kernel."""
+    torch, B = env
+    T = I.templates(2, 700)
+    Q, _ = I.queries(2, 3)
+    st = Setup(env, O, 128, 8, T, Q)
+    got = st.gpu_match(0)
+    host = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192))
+    sk_dev = B.bm_sk_to_device(st.prm, st.sk)
+    n0 = B.bm_launch_count()
+    dev = B.bm_decrypt_dev(st.prm, sk_dev, torch.from_numpy(got.view(np.int64)).cuda())
+    B.bm_sync()
+    assert B.bm_launch_count() == n0 + 1
+    dev = dev.cpu().numpy()
+    assert dev.shape == host.shape
+    assert np.abs(dev - host).max() < 1e-9
+    sc = dev.reshape(st.nq, -1)[:, :T.shape[0]]
+    assert np.abs(sc - Q @ T.T).max() < 1e-6
+    # the layout (d, p) only selects the score slots: the same ciphertexts decode to S / s scores each
+    prm2 = B.bm_params_init(64, 4)
+    assert B.bm_decrypt_dev(prm2, sk_dev, torch.from_numpy(got.view(np.int64)).cuda()).shape[1] == prm2.B
+
+
+def test_binding_validates_sizes(env, O):
+    """The binding refuses tensors too small for the scan it describes (the C ABI trusts sizes)."""
+    torch, B = env
+    prm = B.bm_params_init(128, 8)
+    sk, pk, evk = B.bm_keygen(prm, 9)
+    evk_dev = B.bm_evk_to_device(prm, evk)
+    db = torch.zeros((2, 8, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    q = torch.zeros((3, 8, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    out = torch.zeros((3, 2, 2, 8192), dtype=torch.int64, device="cuda")
+    ws = torch.empty(B.bm_match_ws_bytes(prm, 2, 3), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        B.bm_match(prm, evk_dev, db, 3, q, 3, out, ws)            # 3 sets, 2 present
+    with pytest.raises(ValueError):
+        B.bm_match(prm, evk_dev, db, 2, q, 4, out, ws)            # 4 queries, 3 present
+    with pytest.raises(ValueError):
+        B.bm_match(prm, evk_dev, db, 2, q, 3, out[:2], ws)        # output too small
+    with pytest.raises(ValueError):
+        B.bm_match(prm, evk_dev, db.float(), 2, q, 3, out, ws)    # wrong dtype
