@@ -206,7 +206,7 @@ int bm_ipc_close(void *d_base);
 
 /* The same scan end to end from HOST buffers: h_q (host [nq][p][2][2][N], NTT domain) is
  * copied in and h_out (host [nq][n_sets][2][N]) copied out inside the call.  The queries are
- * processed in groups of about 576 (query, set) pairs (or BM_OPT_HOST_GROUPS groups): group g's
+ * processed in groups of max(576, min(16384, 4 n_sets)) (query, set) pairs (or BM_OPT_HOST_GROUPS groups): group g's
  * upload, scan and download overlap the neighbouring groups (four device slots, two internal
  * copy streams, the scans alternating between `stream` and an internal stream, all starting
  * after the work already queued on `stream`; the internal streams are created once per device and
@@ -233,7 +233,7 @@ int bm_match_host_ring(const bm_params *, const bm_evk_dev *, const uint64_t *d_
 typedef enum {
     BM_OPT_CHUNK_PAIRS = 0,  /* (query, set) pairs per bm_match chunk, >= 1 (default 16384)          */
     BM_OPT_EXPAND_CHUNK = 1, /* (query, part) outputs per bm_expand / bm_enroll launch (2048)       */
-    BM_OPT_HOST_GROUPS = 2,  /* bm_match_host query groups, 0 = automatic (~576 pairs per group)   */
+    BM_OPT_HOST_GROUPS = 2,  /* bm_match_host query groups, 0 = automatic (see bm_match_host)      */
     BM_OPT_LADDER_C2 = 3,    /* 0/1: latency-mode ladder on 2-CTA clusters (1)                      */
     BM_OPT_LADDER_C3 = 4,    /* 0/1: latency-mode ladder on 3-CTA clusters (1)                      */
     BM_OPT_LADDER_TAIL = 5,  /* 0/1: a large launch's partial last wave on the cluster ladders (1)  */

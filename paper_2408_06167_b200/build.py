@@ -14,7 +14,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES = ["host.cpp", "device.cu"]
-HEADERS = ["bm_common.cuh", "bm_host.h", "ntt.cuh", "ntt2.cuh", "ntt3.cuh", "ntt3f.cuh",
+HEADERS = ["bm_common.cuh", "bm_host.h", "ntt_base.cuh", "ntt2.cuh", "ntt3.cuh", "ntt3f.cuh",
            "k_match.cuh", "k_next.cuh", "k_setup.cuh"]
 
 

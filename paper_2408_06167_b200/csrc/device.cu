@@ -1307,8 +1307,11 @@ int bm_ipc_close(void *d_base)
 constexpr int HOST_SLOTS = 4;
 static int host_groups(int64_t n_sets, int32_t nq)
 {
-    // about 576 (query, set) pairs per group (a few waves of the ladder kernel), at least 4 groups
-    int64_t g = (n_sets * (int64_t)nq + 575) / 576;
+    // about max(576, min(16384, 4 n_sets)) (query, set) pairs per group (a few waves of the ladder for
+    // small databases; whole chunks of several queries for large ones, where one query's group would
+    // stream the whole DB through the tensor per query), at least 4 groups
+    const int64_t target = std::max<int64_t>(576, std::min<int64_t>(16384, 4 * n_sets));
+    int64_t g = (n_sets * (int64_t)nq + target - 1) / target;
     g = g < 4 ? 4 : g;
     if (opt(BM_OPT_HOST_GROUPS) > 0) g = opt(BM_OPT_HOST_GROUPS);
     return (int)(nq < g ? nq : g);

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(T, 1) k_convert(ConvK C, int dir)
     }
 }
 
-// keys: canonical coefficients -> NTT domain Shoup pairs (storage order pos_L3)
+// keys: canonical coefficients -> NTT domain Shoup pairs (storage order pos_M4)
 __global__ void __launch_bounds__(T, 1) k_key_ntt(ConvK C, ulonglong2 *dst)
 {
     extern __shared__ uint64_t sm[];

@@ -190,7 +190,7 @@ def test_edge_cases_and_errors(env, O):
     prm = B.bm_params_init(128, 8)
     sk, pk, evk = B.bm_keygen(prm, 9)
     evk_dev = B.bm_evk_to_device(prm, evk)
-    dummy = torch.zeros(8, dtype=torch.int64, device="cuda")
+    dummy = torch.zeros(8 * 4 * 8192, dtype=torch.int64, device="cuda")   # one set / query / result of any p <= 8
     # empty scans are no-ops
     B.bm_match(prm, evk_dev, dummy, 0, dummy, 3, dummy, None)
     B.bm_match(prm, evk_dev, dummy, 5, dummy, 0, dummy, None)
@@ -302,7 +302,7 @@ def test_hoisted_rotation_needs_its_keys(env, O):
     prm = B.bm_params_init(128, 8)
     sk, pk, evk = B.bm_keygen(prm, 9)
     evk_dev = B.bm_evk_to_device(prm, evk)
-    dummy = torch.zeros(8, dtype=torch.int64, device="cuda")
+    dummy = torch.zeros(8 * 4 * 8192, dtype=torch.int64, device="cuda")
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=2)
     assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"

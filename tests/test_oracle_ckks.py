@@ -207,6 +207,100 @@ def test_rotation_keyswitch_decrypts_to_rotated_slots(O):
         assert np.abs(back - _rot_left(z, r)).max() < 1e-6
 
 
+# ----------------------------------------------------------------------------- exact level-0 key-switch identities
+def _sigma_signed(a, g):
+    """sigma_g on integer coefficients: X^k -> X^(k g mod 2N), negated past N (direct substitution)."""
+    n = len(a)
+    out = [0] * n
+    for k, v in enumerate(a):
+        t = k * g % (2 * n)
+        if t < n:
+            out[t] += v
+        else:
+            out[t - n] -= v
+    return out
+
+
+def _moddown_round(x_P, key_P, P):
+    """y^ = centred_P(x key mod P): the ModDown rounding term, recomputed with big integers from the
+    digit lifted to P and the key's P limb (SURVEY.md sec. 8c "Key switch" pin)."""
+    return [_cent(v % P, P) for v in _negacyclic_big(x_P, key_P)]
+
+
+@pytest.mark.parametrize("r", [1, 2, 4])
+def test_rotate_level0_keyswitch_identity(O, r):
+    """Level-0 rotation (reading R3: one digit x = sigma_g(c1) in [0, q0), lifted to P as is; Galois key
+    over {q0, P}): with error-free keys, EXACTLY
+        c0' + c1' s = sigma(c0) + sigma(c1) sigma(s) - P^-1 (y^_0 + y^_1 s)   (mod q0),
+    y^_c = centred_P(x gk[c][P]) recomputed here from the key's P limb (big integers); |e| <= (N+1)/2.
+    A dropped term, a wrong sign, the wrong Galois element or a centred lift all break the equality."""
+    logN = 5
+    N = 1 << logN
+    q0, q1, P = O.primes()
+    sk, pk, rlk, gk = O.keygen(logN, 3, 3, zero_error=True)
+    g = pow(5, r, 2 * N)
+    rnd = random.Random(31 + r)
+    ct = np.array([[[rnd.randrange(q0) for _ in range(N)]] for _ in range(2)], np.uint64)
+    out = O.rotate(logN, ct, r, gk[r.bit_length() - 1])
+    s = [int(v) for v in sk]
+    c0, c1 = [int(v) for v in ct[0, 0]], [int(v) for v in ct[1, 0]]
+    x = [v % q0 for v in _sigma_signed(c1, g)]                    # the digit, canonical mod q0
+    y0 = _moddown_round(x, [int(v) for v in gk[r.bit_length() - 1][0][1]], P)
+    y1 = _moddown_round(x, [int(v) for v in gk[r.bit_length() - 1][1][1]], P)
+    Pinv = pow(P, -1, q0)
+    lhs = [(int(out[0, 0, k]) + v) % q0 for k, v in enumerate(_negacyclic_big([int(v) for v in out[1, 0]], s))]
+    xs = _negacyclic_big(x, _sigma_signed(s, g))
+    corr = [y0[k] + v for k, v in enumerate(_negacyclic_big(y1, s))]
+    sc0 = _sigma_signed(c0, g)
+    rhs = [(sc0[k] + xs[k] - Pinv * corr[k]) % q0 for k in range(N)]
+    assert lhs == rhs
+    e = [_cent((lhs[k] - sc0[k] - xs[k]) % q0, q0) for k in range(N)]
+    assert max(abs(v) for v in e) <= (N + 1) // 2 and any(v != 0 for v in e)
+
+
+@pytest.mark.parametrize("s_len", [2, 4, 8])
+def test_hoisted_rot_sum_keyswitch_identity(O, s_len):
+    """f2's hoisted rotation sum (reading R23): with error-free keys, EXACTLY
+        o0 + o1 s = sum_{r<s} sigma_r(c0) + c1 s + sum_{0<r<s} sigma_r(c1) sigma_r(s)
+                    - P^-1 (Y_0 + Y_1 s)   (mod q0),
+    Y_c = centred_P(sum_{0<r<s} sigma_r(x~)_P hgk_r[c][P]) with the digit x = c1 in [0, q0) lifted to P
+    ONCE and permuted in the P limb as a signed permutation (negation mod P), big integers."""
+    logN = 5
+    N = 1 << logN
+    q0, q1, P = O.primes()
+    sk, pk, rlk, gk = O.keygen(logN, 5, 0, zero_error=True)
+    hgk = O.keygen_hoisted(logN, 5, s_len, zero_error=True)
+    rnd = random.Random(40 + s_len)
+    ct = np.array([[[rnd.randrange(q0) for _ in range(N)]] for _ in range(2)], np.uint64)
+    out = O.hoisted_rot_sum(logN, s_len, hgk, ct)
+    s = [int(v) for v in sk]
+    c0, c1 = [int(v) for v in ct[0, 0]], [int(v) for v in ct[1, 0]]
+    acc = [0] * N   # the Q-limb message part
+    Y = [[0] * N, [0] * N]
+    for r in range(s_len):
+        g = pow(5, r, 2 * N)
+        sc0 = _sigma_signed(c0, g)
+        acc = [acc[k] + sc0[k] for k in range(N)]
+        if r == 0:
+            acc = [acc[k] + v for k, v in enumerate(_negacyclic_big(c1, s))]
+            continue
+        xg = _sigma_signed(c1, g)                           # sigma_r of the lifted digit (integers)
+        ss = _negacyclic_big(xg, _sigma_signed(s, g))
+        acc = [acc[k] + ss[k] for k in range(N)]
+        for c in range(2):
+            kp = [int(v) for v in hgk[r - 1][c][1]]
+            prod = _negacyclic_big([v % P for v in xg], kp)
+            Y[c] = [Y[c][k] + prod[k] for k in range(N)]
+    Yc = [[_cent(v % P, P) for v in Y[c]] for c in range(2)]
+    Pinv = pow(P, -1, q0)
+    corr = [Yc[0][k] + v for k, v in enumerate(_negacyclic_big(Yc[1], s))]
+    lhs = [(int(out[0, 0, k]) + v) % q0 for k, v in enumerate(_negacyclic_big([int(v) for v in out[1, 0]], s))]
+    rhs = [(acc[k] - Pinv * corr[k]) % q0 for k in range(N)]
+    assert lhs == rhs
+    e = [_cent((lhs[k] - acc[k]) % q0, q0) for k in range(N)]
+    assert max(abs(v) for v in e) <= (N + 1) // 2 and any(v != 0 for v in e)
+
+
 # ----------------------------------------------------------------------------- trivial-ciphertext closed form
 def _trivial(pt_list, q0, q1, N):
     """(pt, 0) as a level-1 ciphertext."""

@@ -9,6 +9,7 @@
 #include "../paper_2408_06167_b200/csrc/bm_host.h"
 #include "../paper_2408_06167_b200/csrc/ntt3.cuh"
 #include "../paper_2408_06167_b200/csrc/ntt3f.cuh"
+#include "ntt_legacy.cuh"
 using namespace bm;
 typedef unsigned __int128 u128;
 

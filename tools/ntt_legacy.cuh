@@ -1,4 +1,7 @@
-// ntt.cuh -- register-blocked negacyclic NTT / INTT of one 8192-coefficient u64 polynomial
+// ntt_legacy.cuh -- DIAGNOSTIC ONLY (tools/ntt_bench.cu), not part of the library: the superseded
+// v1 core (below) and v2 transforms (end of file) the library's ntt3.cuh replaced.
+//
+// v1: register-blocked negacyclic NTT / INTT of one 8192-coefficient u64 polynomial
 // per 256-thread CTA (K1 in SURVEY.md sec. 2.2).
 //
 // Transform: forward = Cooley-Tukey with psi^brev twiddles (Harvey lazy butterflies in
@@ -13,16 +16,11 @@
 // Forward maps L1 -> L3, inverse L3 -> L1.  Shared memory is padded (one word per 16) so
 // every transpose is bank-conflict free.
 #pragma once
-#include "bm_common.cuh"
+#include "../paper_2408_06167_b200/csrc/ntt2.cuh"
 
 namespace bm {
 
 constexpr int NTT_THREADS = 256;
-constexpr int SMEM_WORDS = N + N / 16; // 8704 u64 = 69,632 B
-
-BM_D int pidx(int j) { return j + (j >> 4); }
-
-BM_D ulonglong2 ldtw(const ulonglong2 *p) { return __ldg(p); }
 
 // CT butterfly: x, y in [0,4q) -> x + w y, x - w y in [0,4q)
 BM_D void ct_bfly(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q, uint64_t q2)
@@ -202,12 +200,176 @@ BM_D void ntt_inv(uint64_t a[32], uint64_t *sm, const PrimeK &P)
 
 // NTT-domain automorphism sigma_g as an index map: NTT(sigma_g a)[j] = NTT(a)[perm_g(j)],
 // perm_g(j) = brev13(((2 brev13(j) + 1) g mod 2N - 1) / 2).
-BM_D int brev13(int x) { return (int)(__brev((unsigned)x) >> 19); }
 BM_D int auto_perm(int j, uint32_t g)
 {
     uint32_t e = 2u * (uint32_t)brev13(j) + 1u;
     e = (e * g) & (2u * N - 1u);
     return brev13((int)((e - 1u) >> 1));
 }
+
+// ================================================================== v2 (prime-specialised, 256 threads)
+// exact x mod q for any x < 2^64 (Shoup with w = 1 and a final correction)
+template <int PI> BM_D uint64_t reduce_full(uint64_t x, uint64_t one_p)
+{
+    constexpr uint64_t q = PrimeC<PI>::q;
+    uint64_t r = x - mul_q<PI>(__umul64hi(x, one_p)); // [0, 2q)
+    return r >= q ? r - q : r;
+}
+
+
+// ------------------------------------------------------------------ forward (L1 -> L3)
+template <int PI> BM_D void ct4(uint64_t &x, uint64_t &y, ulonglong2 w)
+{
+    constexpr uint64_t q = PrimeC<PI>::q;
+    uint64_t X = x;
+    if (PI == 2) X = X >= 4 * q ? X - 4 * q : X; // P: keep [0, 8q)
+    const uint64_t T = shoup4<PI>(y, w);         // [0, 4q)
+    x = X + T;
+    y = X - T + 4 * q;
+}
+
+template <int PI> BM_D void ntt_fwd2(uint64_t a[32], uint64_t *sm, const PrimeK &P)
+{
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int s = 0; s < 5; s++) {
+        const int half = 16 >> s;
+#pragma unroll
+        for (int k = 0; k < 32; k++) {
+            if (k & half) continue;
+            ct4<PI>(a[k], a[k + half], ldtw(P.fwd + (1 << s) + (k >> (5 - s))));
+        }
+    }
+    exchange<1, 2>(a, sm);
+#pragma unroll
+    for (int s = 5; s < 9; s++) {
+        const int half = 8 >> (s - 5);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int B = (tid + 256 * h) >> 4;
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                if (k & half) continue;
+                ct4<PI>(a[16 * h + k], a[16 * h + k + half], ldtw(P.fwd + (1 << s) + (B << (s - 5)) + (k >> (9 - s))));
+            }
+        }
+    }
+    exchange<2, 3>(a, sm);
+#pragma unroll
+    for (int s = 9; s < 13; s++) {
+        const int half = 8 >> (s - 9);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int G = tid + 256 * h;
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                if (k & half) continue;
+                ct4<PI>(a[16 * h + k], a[16 * h + k + half], ldtw(P.fwd + (1 << s) + (G << (s - 9)) + (k >> (13 - s))));
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 32; e++) a[e] = reduce_full<PI>(a[e], P.one_p);
+}
+
+
+// ------------------------------------------------------------------ inverse (L3 -> L1)
+// GS butterfly of inverse stage number ST (0 = first executed) whose inputs are < B q with
+// B = 4 (q0, P: reduced every stage) or 4 * 2^ST (q1: never reduced): x + y, (x - y + Bq) w
+template <int PI, int ST> BM_D void gs4(uint64_t &x, uint64_t &y, ulonglong2 w)
+{
+    constexpr uint64_t q = PrimeC<PI>::q;
+    constexpr uint64_t B = Q40<PI> ? (4ull << ST) : 4ull;
+    uint64_t X = x + y;
+    if (!Q40<PI>) X = X >= 4 * q ? X - 4 * q : X; // q0, P: keep [0, 4q)
+    const uint64_t T = x - y + (uint64_t)B * q;
+    x = X;
+    y = shoup4<PI>(T, w);
+}
+
+
+template <int PI> BM_D void ntt_inv2(uint64_t a[32], uint64_t *sm, const PrimeK &P)
+{
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int s = 12; s >= 9; s--) {
+        const int half = 8 >> (s - 9);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int G = tid + 256 * h;
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                if (k & half) continue;
+                const ulonglong2 w = ldtw(P.inv + (1 << s) + (G << (s - 9)) + (k >> (13 - s)));
+                switch (12 - s) {
+                case 0: gs4<PI, 0>(a[16 * h + k], a[16 * h + k + half], w); break;
+                case 1: gs4<PI, 1>(a[16 * h + k], a[16 * h + k + half], w); break;
+                case 2: gs4<PI, 2>(a[16 * h + k], a[16 * h + k + half], w); break;
+                default: gs4<PI, 3>(a[16 * h + k], a[16 * h + k + half], w); break;
+                }
+            }
+        }
+    }
+    exchange<3, 2>(a, sm);
+#pragma unroll
+    for (int s = 8; s >= 5; s--) {
+        const int half = 8 >> (s - 5);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int B = (tid + 256 * h) >> 4;
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                if (k & half) continue;
+                const ulonglong2 w = ldtw(P.inv + (1 << s) + (B << (s - 5)) + (k >> (9 - s)));
+                switch (12 - s) {
+                case 4: gs4<PI, 4>(a[16 * h + k], a[16 * h + k + half], w); break;
+                case 5: gs4<PI, 5>(a[16 * h + k], a[16 * h + k + half], w); break;
+                case 6: gs4<PI, 6>(a[16 * h + k], a[16 * h + k + half], w); break;
+                default: gs4<PI, 7>(a[16 * h + k], a[16 * h + k + half], w); break;
+                }
+            }
+        }
+    }
+    exchange<2, 1>(a, sm);
+#pragma unroll
+    for (int s = 4; s >= 1; s--) {
+        const int half = 16 >> s;
+#pragma unroll
+        for (int k = 0; k < 32; k++) {
+            if (k & half) continue;
+            const ulonglong2 w = ldtw(P.inv + (1 << s) + (k >> (5 - s)));
+            switch (12 - s) {
+            case 8: gs4<PI, 8>(a[k], a[k + half], w); break;
+            case 9: gs4<PI, 9>(a[k], a[k + half], w); break;
+            case 10: gs4<PI, 10>(a[k], a[k + half], w); break;
+            default: gs4<PI, 11>(a[k], a[k + half], w); break;
+            }
+        }
+    }
+    // last stage (s = 0) with N^-1 folded in; inputs < inv_bound(12) q
+    constexpr uint64_t q = PrimeC<PI>::q;
+    constexpr uint64_t Bq = (Q40<PI> ? (4ull << 12) : 4ull) * q;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const uint64_t x = a[k], y = a[k + 16];
+        a[k] = reduce_full<PI>(shoup4<PI>(x + y, P.ninv), P.one_p);
+        a[k + 16] = reduce_full<PI>(shoup4<PI>(x - y + Bq, P.ninv_w1), P.one_p);
+    }
+}
+
+// runtime prime dispatch (one code copy per prime at each call site)
+BM_D void ntt_fwd_rt(uint64_t a[32], uint64_t *sm, const PrimeK &P, int pi)
+{
+    if (pi == 0) ntt_fwd2<0>(a, sm, P);
+    else if (pi == 1) ntt_fwd2<1>(a, sm, P);
+    else ntt_fwd2<2>(a, sm, P);
+}
+BM_D void ntt_inv_rt(uint64_t a[32], uint64_t *sm, const PrimeK &P, int pi)
+{
+    if (pi == 0) ntt_inv2<0>(a, sm, P);
+    else if (pi == 1) ntt_inv2<1>(a, sm, P);
+    else ntt_inv2<2>(a, sm, P);
+}
+
 
 } // namespace bm
