@@ -291,6 +291,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     from paper_2408_06167_b200 import bm as B
+    # seeded streams (BM_RNG_SEEDED): the DB shards must be bit-exact slices of one database across
+    # ranks and the in-bench oracle check re-encrypts with the same streams (the library default is
+    # OS entropy)
+    B.bm_rng_mode(B.RNG_SEEDED)
 
     shard_of = args.shard_of if args.shard_of else (8 if args.config == 5 and world < 8 else None)
     if shard_of is not None and world > 1 and shard_of != world:

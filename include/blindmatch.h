@@ -80,6 +80,23 @@ typedef struct bm_evk bm_evk;         /* host: relinearization key + Galois keys
 typedef struct bm_pk_dev bm_pk_dev;   /* device copy of pk (NTT domain)                   */
 typedef struct bm_evk_dev bm_evk_dev; /* device copy of evk (NTT domain)                  */
 
+/* Randomness (a seeded generator as a test mode, a cryptographic one otherwise).
+ * Every draw comes from ChaCha20 (RFC 8439) keyed by the call's 64-bit seed, the draw's purpose and a
+ * 160-bit key extension; objects / components / limbs are nonces (reading R14).
+ *   BM_RNG_OS (the default): the keygen family (bm_keygen, bm_evk_add_hoisted, bm_xk_keygen,
+ *     bm_ck_keygen) uses a 160-bit process key drawn once from getrandom() -- 224 bits of key entropy,
+ *     and the same seed gives the same secret within the process, so the family stays consistent;
+ *     keys outlive the process through bm_*_export / import -- and EVERY encryption call (bm_encrypt,
+ *     bm_encrypt_db, bm_encrypt_query, bm_encrypt_l2) draws a fresh 160-bit extension, so two batches
+ *     encrypted with the same seed and object numbers share no randomness.
+ *   BM_RNG_SEEDED: all extensions zero -- deterministic in the seed (tests, benchmarks, the oracle's
+ *     streams).  Never reuse a seed across encryptions in this mode.
+ * bm_rng_mode returns BM_ERR_INVALID_ARG for another value.  Process-wide. */
+#define BM_RNG_SEEDED 0
+#define BM_RNG_OS 1
+int bm_rng_mode(int32_t mode);
+int32_t bm_get_rng_mode(void);
+
 /* Fill *out for feature size d and part count p (both powers of two, 1 <= p <= d <= 4096).
  * Errors: BM_ERR_INVALID_ARG (out null), BM_ERR_INVALID_LAYOUT, BM_ERR_INVALID_PRIME,
  * BM_ERR_INSECURE_PARAMS. */

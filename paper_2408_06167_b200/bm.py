@@ -53,6 +53,7 @@ _pp = ctypes.POINTER(ctypes.c_void_p)
 
 _SIGS = {
     "bm_params_init": (_i32, [_P, _i32, _i32]),
+    "bm_rng_mode": (_i32, [_i32]), "bm_get_rng_mode": (_i32, []),
     "bm_keygen": (_i32, [_P, _u64, _pp, _pp, _pp]),
     "bm_evk_add_hoisted": (_i32, [_P, _u64, _vp]),
     "bm_sk_free": (None, [_vp]), "bm_pk_free": (None, [_vp]), "bm_evk_free": (None, [_vp]),
@@ -209,6 +210,19 @@ class ExpandKeyDev(_Handle):
 
 
 # --------------------------------------------------------------------------- API (same names as the C ABI)
+RNG_SEEDED, RNG_OS = 0, 1
+
+
+def bm_rng_mode(mode):
+    """RNG_OS (the library default): getrandom()-keyed streams (224-bit keys, fresh per encryption);
+    RNG_SEEDED: deterministic in the seed (tests, benchmarks, oracle parity)."""
+    _chk(_lib.bm_rng_mode(mode), "bm_rng_mode")
+
+
+def bm_get_rng_mode():
+    return int(_lib.bm_get_rng_mode())
+
+
 def bm_params_init(d, p):
     prm = bm_params()
     _chk(_lib.bm_params_init(ctypes.byref(prm), d, p), "bm_params_init")

@@ -7,8 +7,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INC = os.path.join(ROOT, "include")
-BUILD = os.path.join(ROOT, "build")
-LIB = os.path.join(PKG, "libblindmatch.so")
+# BM_VARIANT=name (A/B builds only, tools/ab.sh): objects in build/var_<name>, the library at
+# paper_2408_06167_b200/variants/libblindmatch_<name>.so (loaded with BM_LIB_PATH); the product is the default
+_VAR = os.environ.get("BM_VARIANT")
+BUILD = os.path.join(ROOT, "build", f"var_{_VAR}") if _VAR else os.path.join(ROOT, "build")
+LIB = os.path.join(PKG, "variants", f"libblindmatch_{_VAR}.so") if _VAR else os.path.join(PKG, "libblindmatch.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -33,6 +36,7 @@ def _run(cmd, verbose):
 
 def build(force=False, verbose=True):
     os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INC, "blindmatch.h")]
     objs = []
     for src in SOURCES:

@@ -41,16 +41,22 @@ BM_HD uint32_t rotl32(uint32_t x, int n) { return (x << n) | (x >> (32 - n)); }
     a += b; d ^= a; d = rotl32(d, 8);          \
     c += d; b ^= c; b = rotl32(b, 7);
 
-// Stream key/nonce of (seed, purpose, object, sub): key = {seed lo, seed hi, purpose, 0...},
+// Stream key/nonce of (seed, purpose, object, sub): key = {seed lo, seed hi, purpose, kx[0..4]},
 // nonce = {obj lo, obj hi, sub}; the 32-bit block counter indexes 8 u64 draws per block.
+// kx: 160 bits of key extension -- zero in the seeded (test / reproducibility) mode, where the
+// streams are those of DESIGN.md reading R14 and the oracle; getrandom() output in the default
+// OS-entropy mode (bm_rng_mode), so keys carry 224 bits of entropy and every encryption call is
+// keyed afresh.
 struct Stream {
     uint32_t k0, k1, k2, n0, n1, n2;
+    uint32_t kx[5];
 };
-BM_HD Stream make_stream(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t sub)
+BM_HD Stream make_stream(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t sub, const uint32_t *kx = nullptr)
 {
     Stream s;
     s.k0 = (uint32_t)seed; s.k1 = (uint32_t)(seed >> 32); s.k2 = purpose;
     s.n0 = (uint32_t)obj; s.n1 = (uint32_t)(obj >> 32); s.n2 = sub;
+    for (int i = 0; i < 5; i++) s.kx[i] = kx ? kx[i] : 0u;
     return s;
 }
 
@@ -58,7 +64,8 @@ BM_HD Stream make_stream(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t
 BM_HD void chacha_draws(const Stream &st, uint32_t ctr, uint64_t out[8])
 {
     uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
-    uint32_t x4 = st.k0, x5 = st.k1, x6 = st.k2, x7 = 0, x8 = 0, x9 = 0, x10 = 0, x11 = 0;
+    uint32_t x4 = st.k0, x5 = st.k1, x6 = st.k2, x7 = st.kx[0], x8 = st.kx[1], x9 = st.kx[2], x10 = st.kx[3],
+             x11 = st.kx[4];
     uint32_t x12 = ctr, x13 = st.n0, x14 = st.n1, x15 = st.n2;
 #pragma unroll
     for (int r = 0; r < 10; r++) {
@@ -67,6 +74,7 @@ BM_HD void chacha_draws(const Stream &st, uint32_t ctr, uint64_t out[8])
     }
     x0 += 0x61707865u; x1 += 0x3320646eu; x2 += 0x79622d32u; x3 += 0x6b206574u;
     x4 += st.k0; x5 += st.k1; x6 += st.k2;
+    x7 += st.kx[0]; x8 += st.kx[1]; x9 += st.kx[2]; x10 += st.kx[3]; x11 += st.kx[4];
     x12 += ctr; x13 += st.n0; x14 += st.n1; x15 += st.n2;
     out[0] = (uint64_t)x0 | ((uint64_t)x1 << 32);
     out[1] = (uint64_t)x2 | ((uint64_t)x3 << 32);

@@ -21,6 +21,11 @@ const uint64_t *host_cdt();          // 19 Gaussian CDT thresholds
 uint64_t mulmod_h(uint64_t a, uint64_t b, uint64_t q);
 uint64_t shoup_companion(uint64_t w, uint64_t q); // floor(w 2^64 / q)
 
+// randomness mode (bm_rng_mode): the key extension of the keygen family (the process key in the
+// OS-entropy mode, zeros when seeded) and a fresh one for an encryption call
+const uint32_t *rng_keygen_kx();
+void rng_encrypt_kx(uint32_t out[5]);
+
 // host negacyclic NTT (same ordering as the device kernels)
 void host_ntt_fwd(uint64_t *a, int prime);
 void host_ntt_inv(uint64_t *a, int prime);

@@ -517,6 +517,7 @@ int bm_encrypt(const bm_params *prm, const bm_pk_dev *pk, const int64_t *d_pt, i
     Ek.out = d_out;
     Ek.first_obj = first_obj;
     Ek.seed = seed;
+    rng_encrypt_kx(Ek.kx); // fresh per call unless seeded (bm_rng_mode)
     Ek.n_limbs = 2;
     Ek.lp[0] = 0;
     Ek.lp[1] = 1;
@@ -685,6 +686,7 @@ int bm_encrypt_l2(const bm_params *prm, const bm_xk_dev *xk, const int64_t *d_pt
     Ek.out = d_out;
     Ek.first_obj = first_obj;
     Ek.seed = seed;
+    rng_encrypt_kx(Ek.kx); // fresh per call unless seeded (bm_rng_mode)
     Ek.n_limbs = 3;
     Ek.lp[0] = 0;
     Ek.lp[1] = 1;

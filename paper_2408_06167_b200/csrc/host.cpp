@@ -11,6 +11,9 @@
 #include <thread>
 #include <vector>
 #include <quadmath.h>
+#include <cerrno>
+#include <cstdlib>
+#include <sys/random.h>
 
 #include "bm_common.cuh"
 #include "bm_host.h"
@@ -169,10 +172,53 @@ static void poly_mul_h(const uint64_t *a, const uint64_t *b, uint64_t *c, int pi
     memcpy(c, A.data(), sizeof(uint64_t) * N);
 }
 
+// ------------------------------------------------------------------ randomness mode
+// BM_RNG_OS (default): the keygen family keys its ChaCha20 streams with the seed AND a 160-bit process
+// key drawn once from getrandom() (224 bits of key entropy; the same seed gives the same secret within
+// the process, so bm_evk_add_hoisted / bm_xk_keygen / bm_ck_keygen still match bm_keygen), and every
+// encryption call draws a fresh 160-bit extension (two batches encrypted with the same seed and object
+// numbers share no randomness).  BM_RNG_SEEDED: all-zero extensions, the reproducible streams of
+// DESIGN.md reading R14 that the oracle implements (tests, bench).
+static std::atomic<int> g_rng_mode(BM_RNG_OS);
+static uint32_t g_proc_kx[5];
+static std::once_flag g_proc_once;
+static const uint32_t g_zero_kx[5] = {0, 0, 0, 0, 0};
+
+static void os_random(void *buf, size_t n)
+{
+    uint8_t *p = (uint8_t *)buf;
+    while (n) {
+        const ssize_t r = getrandom(p, n, 0);
+        if (r < 0) {
+            if (errno == EINTR) continue;
+            abort(); // no entropy source: refuse to produce keys or ciphertexts
+        }
+        p += r;
+        n -= (size_t)r;
+    }
+}
+
+namespace bm {
+const uint32_t *rng_keygen_kx()
+{
+    if (g_rng_mode.load() == BM_RNG_SEEDED) return g_zero_kx;
+    std::call_once(g_proc_once, [] { os_random(g_proc_kx, sizeof(g_proc_kx)); });
+    return g_proc_kx;
+}
+void rng_encrypt_kx(uint32_t out[5])
+{
+    if (g_rng_mode.load() == BM_RNG_SEEDED) {
+        memset(out, 0, 5 * sizeof(uint32_t));
+        return;
+    }
+    os_random(out, 5 * sizeof(uint32_t));
+}
+} // namespace bm
+
 // draws n u64 values of a stream, in order
 static void stream_draws(uint64_t seed, uint32_t purpose, uint64_t obj, uint32_t sub, int n, uint64_t *out)
 {
-    Stream st = make_stream(seed, purpose, obj, sub);
+    Stream st = make_stream(seed, purpose, obj, sub, rng_keygen_kx());
     uint64_t d[8];
     for (int b = 0; b * 8 < n; b++) {
         chacha_draws(st, (uint32_t)b, d);
@@ -212,6 +258,14 @@ static bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
 // ================================================================== C ABI (host part)
 extern "C" {
+
+int bm_rng_mode(int32_t mode)
+{
+    if (mode != BM_RNG_SEEDED && mode != BM_RNG_OS) return BM_ERR_INVALID_ARG;
+    g_rng_mode.store(mode);
+    return BM_OK;
+}
+int32_t bm_get_rng_mode(void) { return g_rng_mode.load(); }
 
 int bm_params_init(bm_params *o, int32_t d, int32_t p)
 {

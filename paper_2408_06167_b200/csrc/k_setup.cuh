@@ -10,6 +10,7 @@ struct EncK {
     const int64_t *pt;    // [n][N]
     uint64_t *out;        // [n][2][n_limbs][N]
     uint64_t first_obj, seed;
+    uint32_t kx[5];       // ChaCha20 key extension of this call (zeros when seeded, bm_rng_mode)
     int n_limbs;          // 2 (level 1: q0, q1) or 3 (f3 level 2: q0, q1, q2)
     int lp[3];            // prime index of each limb
 };
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
     for (int ph = 0; ph < 3; ph++) {
         __syncthreads();
         const uint32_t purpose = ph == 0 ? P_ENC_U : ph == 1 ? P_ENC_E1 : P_ENC_E0;
-        sample_to_smem(sm, make_stream(Ek.seed, purpose, o, 0), ph != 0, q, P.one_p,
+        sample_to_smem(sm, make_stream(Ek.seed, purpose, o, 0, Ek.kx), ph != 0, q, P.one_p,
                        ph == 2 ? Ek.pt + (size_t)ct * N : nullptr);
         __syncthreads();
 #pragma unroll

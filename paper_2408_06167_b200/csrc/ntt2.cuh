@@ -46,6 +46,40 @@ template <int PI> BM_D uint64_t shoup4(uint64_t a, uint64_t w, uint64_t wp)
 #else
     constexpr uint64_t nq = 0ull - PrimeC<PI>::q;
     uint64_t r;
+#ifndef BM_NO_SHOUP_PSHIFT
+    if (PI == 2) {
+        // P = 2^60 - 2^14 + 1: -Q P = (Q << 14) - Q - (Q << 60) mod 2^64 from shifts and adds (LEA /
+        // SHF / IADD3 on the ALU pipes) instead of 1 IMAD.WIDE + 2 IMAD: 11 FMA-pipe slots instead of 14
+        asm("{\n\t"
+            ".reg .u32 a0, a1, w0, w1, p0, p1, h, c, t0, t1, r0, r1, u, s0, s1;\n\t"
+            ".reg .u64 Q, R, S;\n\t"
+            "mov.b64 {a0, a1}, %1;\n\t"
+            "mov.b64 {w0, w1}, %2;\n\t"
+            "mov.b64 {p0, p1}, %3;\n\t"
+            "mul.hi.u32 h, a0, p1;\n\t"
+            "mad.hi.cc.u32 h, a1, p0, h;\n\t"
+            "addc.u32 c, 0, 0;\n\t"
+            "mov.b64 Q, {h, c};\n\t"
+            "mad.wide.u32 Q, a1, p1, Q;\n\t"
+            "mov.b64 {t0, t1}, Q;\n\t"
+            "mul.wide.u32 R, a0, w0;\n\t"
+            "mov.b64 {r0, r1}, R;\n\t"
+            "mad.lo.u32 r1, a0, w1, r1;\n\t"
+            "mad.lo.u32 r1, a1, w0, r1;\n\t"
+            "shl.b64 S, Q, 14;\n\t"
+            "sub.u64 S, S, Q;\n\t"
+            "shl.b32 u, t0, 28;\n\t"
+            "mov.b64 {s0, s1}, S;\n\t"
+            "sub.u32 s1, s1, u;\n\t"
+            "add.cc.u32 r0, r0, s0;\n\t"
+            "addc.u32 r1, r1, s1;\n\t"
+            "mov.b64 %0, {r0, r1};\n\t"
+            "}"
+            : "=l"(r)
+            : "l"(a), "l"(w), "l"(wp));
+        return r;
+    }
+#endif
     asm("{\n\t"
         ".reg .u32 a0, a1, w0, w1, p0, p1, h, c, t0, t1, r0, r1;\n\t"
         ".reg .u64 Q, R;\n\t"
@@ -82,8 +116,19 @@ template <int PI> BM_D uint64_t reduce_bnd(uint64_t x)
     constexpr int k = PI == 0 ? 58 : Q40<PI> ? 40 : 60;
     constexpr uint64_t q = PrimeC<PI>::q;
     constexpr uint64_t c = (1ull << k) - q; // 835583, 147455, 16383, 737279
-    const uint64_t Qe = x >> k;
-    const uint64_t r = x - (Qe << k) + Qe * c;
+    uint64_t r;
+#ifdef BM_RB64
+    if (true) {
+#else
+    if (Q40<PI>) {
+#endif
+        const uint64_t Qe = x >> k; // < 2^22: Qe c needs 64 bits
+        r = x - (Qe << k) + Qe * c;
+    } else {
+        // Qe < 64 and c < 2^20: one 32-bit IMAD (a 64-bit Qe c costs an IMAD.WIDE + a move)
+        const uint32_t Qe = (uint32_t)(x >> k);
+        r = (x & ((1ull << k) - 1)) + (uint64_t)(Qe * (uint32_t)c);
+    }
     return r >= q ? r - q : r;
 }
 

@@ -251,3 +251,34 @@ def test_ciphertext_frame_roundtrip_and_errors(B, O):
     bad[0, 1, 1, 5] = prm.q[1]
     with pytest.raises(B.BMError):
         B.bm_ct_export(prm, bad, 1, 2.0 ** 40)
+
+
+def test_rng_modes(B):
+    """BM_RNG_OS (the library default): the keygen family draws a 160-bit process key from getrandom()
+    -- the same seed gives the same secret within the process (so bm_xk_keygen / bm_ck_keygen /
+    bm_evk_add_hoisted stay consistent with bm_keygen) but not the seeded-mode (oracle) secret;
+    BM_RNG_SEEDED restores the deterministic streams.  Unknown modes are refused; the options and the
+    launch counter are process-wide and validated."""
+    prm = B.bm_params_init(16, 1)
+    assert B.bm_get_rng_mode() == B.RNG_SEEDED          # conftest selects the test mode
+    seeded = B.bm_sk_export(B.bm_keygen(prm, 7)[0])
+    try:
+        B.bm_rng_mode(B.RNG_OS)
+        a = B.bm_sk_export(B.bm_keygen(prm, 7)[0])
+        b = B.bm_sk_export(B.bm_keygen(prm, 7)[0])
+        assert np.array_equal(a, b)                      # one process key
+        assert not np.array_equal(a, seeded)             # 224-bit key, not the 64-bit seed alone
+        assert set(np.unique(a)) <= {-1, 0, 1}
+    finally:
+        B.bm_rng_mode(B.RNG_SEEDED)
+    assert np.array_equal(B.bm_sk_export(B.bm_keygen(prm, 7)[0]), seeded)
+    with pytest.raises(B.BMError):
+        B.bm_rng_mode(5)
+    with pytest.raises(B.BMError):
+        B.bm_set_option("chunk_pairs", 0)
+    with pytest.raises(B.BMError):
+        B.bm_set_option("ladder_c2", 2)
+    with B.options(chunk_pairs=33):
+        assert B.bm_get_option("chunk_pairs") == 33
+    assert B.bm_get_option("chunk_pairs") == 16384
+    assert B.bm_launch_count() >= 0

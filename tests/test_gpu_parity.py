@@ -199,8 +199,9 @@ def test_edge_cases_and_errors(env, O):
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm4, evk_dev, dummy, 1, dummy, 1, dummy, dummy)
     assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+    tiny = torch.zeros(64, dtype=torch.uint8, device="cuda")
     with pytest.raises(B.BMError) as e:
-        B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy)
+        B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, tiny)
     assert e.value.name == "BM_ERR_WORKSPACE"
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=7)
@@ -458,3 +459,31 @@ def test_binding_validates_sizes(env, O):
         B.bm_match(prm, evk_dev, db, 2, q, 3, out[:2], ws)        # output too small
     with pytest.raises(ValueError):
         B.bm_match(prm, evk_dev, db.float(), 2, q, 3, out, ws)    # wrong dtype
+
+
+def test_rng_os_mode_fresh_encryption_randomness(env, O):
+    """BM_RNG_OS: two encryptions of the same plaintext with the same seed and object numbers differ
+    (a fresh 160-bit key extension per call) yet both decrypt to it; BM_RNG_SEEDED repeats exactly."""
+    torch, B = env
+    prm = B.bm_params_init(16, 1)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    pk_dev = B.bm_pk_to_device(prm, pk)
+    pt = torch.from_numpy(O.encode(O.pack_query(I.random_unit(1, 16, 3), 13, 16, 1).reshape(-1, 4096), 13)).cuda()
+    outs = []
+    try:
+        for mode in (B.RNG_OS, B.RNG_OS, B.RNG_SEEDED, B.RNG_SEEDED):
+            B.bm_rng_mode(mode)
+            o = torch.empty((1, 2, 2, 8192), dtype=torch.int64, device="cuda")
+            B.bm_encrypt(prm, pk_dev, pt, 0, 3, o)
+            B.bm_sync()
+            outs.append(o)
+    finally:
+        B.bm_rng_mode(B.RNG_SEEDED)
+    assert not torch.equal(outs[0], outs[1]) and torch.equal(outs[2], outs[3])
+    for o in (outs[0], outs[1]):
+        c = torch.empty_like(o)
+        B.bm_ct_to_coeff(prm, o, 2, c)
+        B.bm_sync()
+        m = O.decrypt(13, B.bm_sk_export(sk), c.cpu().numpy().view(np.uint64)[0], 2)[0]
+        err = O.centred_i64(m, prm.q[0]) - pt.cpu().numpy()[0]
+        assert np.abs(err).max() < 2 ** 20                 # the encryption noise only
