@@ -34,7 +34,9 @@ template <int PI> BM_D uint64_t mul_q(uint64_t Q)
 // most 2; the remainder a w - Q q is formed mod 2^64 as a w + Q (2^64 - q) in one multiply-add
 // chain: 2 IMAD.HI + 3 IMAD.WIDE + 4 IMAD on the FMA-heavy pipe, one carry on the ALU pipe.
 // (IMAD.WIDE / IMAD.HI issue at half the IMAD rate, tools/pipe_bench.cu.  Tried and dropped:
-// forming Q q from shifts for q = 2^k - c (ptxas re-balances it back onto IMAD.X, slower), and
+// forming Q q from shifts for q = 2^k - c (ptxas re-balances it back onto IMAD.X, slower; for
+// P = 2^60 - 2^14 + 1 the shift form takes 11 instead of 14 FMA-pipe slots but adds 5 ALU
+// instructions, and the ladder ran 16.52 -> 16.56 ms: issue, not the FMA pipe alone, binds), and
 // the quotient's cross terms on the idle FP64 pipe (exact, but the u32 <-> f64 conversions cost
 // more FMA/ALU issue than the two IMAD.HI they replace: 2.36 vs 2.75 butterflies/clk/SM).)
 template <int PI> BM_D uint64_t shoup4(uint64_t a, uint64_t w, uint64_t wp)
@@ -46,40 +48,6 @@ template <int PI> BM_D uint64_t shoup4(uint64_t a, uint64_t w, uint64_t wp)
 #else
     constexpr uint64_t nq = 0ull - PrimeC<PI>::q;
     uint64_t r;
-#ifndef BM_NO_SHOUP_PSHIFT
-    if (PI == 2) {
-        // P = 2^60 - 2^14 + 1: -Q P = (Q << 14) - Q - (Q << 60) mod 2^64 from shifts and adds (LEA /
-        // SHF / IADD3 on the ALU pipes) instead of 1 IMAD.WIDE + 2 IMAD: 11 FMA-pipe slots instead of 14
-        asm("{\n\t"
-            ".reg .u32 a0, a1, w0, w1, p0, p1, h, c, t0, t1, r0, r1, u, s0, s1;\n\t"
-            ".reg .u64 Q, R, S;\n\t"
-            "mov.b64 {a0, a1}, %1;\n\t"
-            "mov.b64 {w0, w1}, %2;\n\t"
-            "mov.b64 {p0, p1}, %3;\n\t"
-            "mul.hi.u32 h, a0, p1;\n\t"
-            "mad.hi.cc.u32 h, a1, p0, h;\n\t"
-            "addc.u32 c, 0, 0;\n\t"
-            "mov.b64 Q, {h, c};\n\t"
-            "mad.wide.u32 Q, a1, p1, Q;\n\t"
-            "mov.b64 {t0, t1}, Q;\n\t"
-            "mul.wide.u32 R, a0, w0;\n\t"
-            "mov.b64 {r0, r1}, R;\n\t"
-            "mad.lo.u32 r1, a0, w1, r1;\n\t"
-            "mad.lo.u32 r1, a1, w0, r1;\n\t"
-            "shl.b64 S, Q, 14;\n\t"
-            "sub.u64 S, S, Q;\n\t"
-            "shl.b32 u, t0, 28;\n\t"
-            "mov.b64 {s0, s1}, S;\n\t"
-            "sub.u32 s1, s1, u;\n\t"
-            "add.cc.u32 r0, r0, s0;\n\t"
-            "addc.u32 r1, r1, s1;\n\t"
-            "mov.b64 %0, {r0, r1};\n\t"
-            "}"
-            : "=l"(r)
-            : "l"(a), "l"(w), "l"(wp));
-        return r;
-    }
-#endif
     asm("{\n\t"
         ".reg .u32 a0, a1, w0, w1, p0, p1, h, c, t0, t1, r0, r1;\n\t"
         ".reg .u64 Q, R;\n\t"

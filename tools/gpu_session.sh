@@ -9,7 +9,7 @@ for st in $STAGES; do
 case $st in
 build) python -m paper_2408_06167_b200.build > gpurun_out/build.log 2>&1 ;;
 micro) bash tools/build_micro.sh > gpurun_out/micro_build.log 2>&1; timeout 120 tools/modmul_bench > gpurun_out/modmul_bench.txt 2>&1 ;;
-pytest) timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
+pytest) timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu ${PYTEST_K:+-k "$PYTEST_K"} ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
 sanitize)
   timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize.py all > gpurun_out/san_memcheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_memcheck.log
   timeout 1200 compute-sanitizer --tool racecheck --racecheck-report all --print-limit 20 python tools/sanitize.py small > gpurun_out/san_racecheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_racecheck.log
