@@ -311,8 +311,12 @@ def run_ours(args):
     n_local = W.n_local
     T_local = I.templates(W.cfg, W.n_tmpl_local, W.tmpl_lo)
     d_db = torch.empty((n_local, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
-    # global set numbers and one seed: every rank's shard is a bit-exact slice of the 1-GPU database
-    B.bm_encrypt_db(prm, pk_dev, T_local, 0, n_local, 2, d_db) if n_local else None
+    # global object numbers (set t, part i -> t p + i) and one seed: every rank's shard is a bit-exact
+    # slice of the 1-GPU database (packing is position-independent, so the local templates suffice)
+    if n_local:
+        pt = torch.from_numpy(B.bm_encode_db(prm, T_local, 0, n_local).reshape(-1, N_RING)).to(dev)
+        B.bm_encrypt(prm, pk_dev, pt, W.lo * p, 2, d_db)
+        del pt
     Q, genuine = I.queries(W.cfg, nq)
     d_q = torch.zeros((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
     if rank == 0:

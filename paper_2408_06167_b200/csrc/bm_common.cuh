@@ -9,6 +9,57 @@
 #define BM_HD __host__ __device__ __forceinline__
 #define BM_D __device__ __forceinline__
 
+// Debug builds (the sanitizer substitute; never the product):
+//  BM_DEBUG_CHECKS: device-side bounds checks (shared-memory words, output rows, tables) that trap;
+//  BM_DEBUG_JITTER: every CTA / warp barrier and cluster barrier is surrounded by a per-thread
+//    pseudo-random spin of up to ~2000 cycles, so warps, lanes and cluster ranks reach each phase in
+//    shuffled orders -- a missing barrier then shows up as a result that differs from the oracle.
+#ifdef BM_DEBUG_CHECKS
+#include <cstdio>
+#define BM_CHECK(c)                                                                                   \
+    do {                                                                                             \
+        if (!(c)) {                                                                                  \
+            printf("BM_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                   (int)threadIdx.x, #c);                                                            \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define BM_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+#ifdef BM_DEBUG_JITTER
+__device__ __forceinline__ void bm_jitter()
+{
+    unsigned x = (unsigned)clock64() ^ (threadIdx.x * 2654435761u) ^ (blockIdx.x * 40503u);
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    const long long t0 = clock64(), n = (long long)(x & 2047u);
+    while (clock64() - t0 < n) {
+    }
+}
+#define BM_SYNCTHREADS()  \
+    do {                  \
+        bm_jitter();      \
+        __syncthreads();  \
+        bm_jitter();      \
+    } while (0)
+#define BM_SYNCWARP()    \
+    do {                 \
+        bm_jitter();     \
+        __syncwarp();    \
+        bm_jitter();     \
+    } while (0)
+#else
+#define bm_jitter() \
+    do {            \
+    } while (0)
+#define BM_SYNCTHREADS() __syncthreads()
+#define BM_SYNCWARP() __syncwarp()
+#endif
+
 namespace bm {
 
 constexpr int N = BM_N;        // ring degree ("N = 8,192")

@@ -934,6 +934,7 @@ int bm_match_cmp(const bm_params *prm, const bm_ck_dev *ck, const uint64_t *d_db
     K.db = d_db;
     K.qry = d_q;
     K.out = nullptr;
+    K.nq_total = nq;
     K.n_sets = n_sets;
     K.p = prm->p;
 
@@ -1082,6 +1083,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     K.qry = d_q;
     K.out = d_out;
     K.rows = d_rows;
+    K.nq_total = nq;
     K.set_off = set_offset;
     K.n_sets = n_sets;
     K.p = prm->p;

@@ -30,8 +30,10 @@ struct MatchK {
     uint64_t *const *rows = nullptr;
     int64_t set_off = 0;
     int64_t pair0 = 0; // the ladder kernels' first pair (a launch may cover only the chunk's tail)
+    int64_t nq_total = 0; // queries of the whole call (debug bounds checks)
     BM_D uint64_t *out_at(int64_t pi, int c) const
     {
+        BM_CHECK(pi >= 0 && pi < (int64_t)cq * ct && jq0 + pi / ct < nq_total && t0 + pi % ct < n_sets);
         if (rows) return rows[jq0 + pi / ct] + ((set_off + t0 + pi % ct) * 2 + c) * (int64_t)N;
         return out + (out_row(pi) * 2 + c) * (int64_t)N;
     }
@@ -142,6 +144,26 @@ BM_D uint64_t f64_mod_q1(double x)
     return (uint64_t)__double_as_longlong(r + 4503599627370496.0) & ((1ull << 52) - 1);
 }
 
+// Integer-limb accumulator of the tensor (q0, q2): operands split into 29-bit limbs,
+// x y = xl yl + (xl yh + xh yl) 2^29 + xh yh 2^58, every partial product ONE IMAD.WIDE into its own
+// 64-bit sum -- no carry chains (a 128-bit multiply-accumulate costs ~13 instructions, a third of
+// them IMAD.X carries on the FMA pipe).  Exact for up to 15 products of operands < 2^59 (the
+// Karatsuba sums: xh < 2^30, so M grows by < 2^60 per product): the tile folds every PCH = 8 parts.
+struct Acc29 {
+    uint64_t L, M, H;
+    BM_D void zero() { L = M = H = 0; }
+    BM_D void set(uint64_t r) { L = r, M = 0, H = 0; }            // r < 2^60: L stays < 2^63
+    BM_D void mac(uint32_t xl, uint32_t xh, uint32_t yl, uint32_t yh)
+    {
+        L += (uint64_t)xl * yl;
+        M += (uint64_t)xl * yh;
+        M += (uint64_t)xh * yl;
+        H += (uint64_t)xh * yh;
+    }
+    BM_D u128 value() const { return (u128)L + ((u128)M << 29) + ((u128)H << 58); }
+};
+constexpr uint32_t M29 = (1u << 29) - 1;
+
 // grid: ((qt * (N / CS) + slice) * nst + st) * 2 + l  (limbs alternate, so each SM holds one
 // q0-limb CTA on the integer pipe and one q1-limb CTA on the FP64 pipe; set tiles next: the CTAs
 // that share a query slice run together and the query data streams from HBM once)
@@ -196,7 +218,7 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
     const int R = (SW ? 1 : TSL) * n_chunks; // the swapped (small-batch) tiles: one slice per CTA, more CTAs
     auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
     tensor_stage<L, NL, SW>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
-    u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
+    Acc29 a0[2][2], a1[2][2], a2[2][2];    // q0, q2: split-limb integer sums (Acc29)
     double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
 #pragma unroll 1
     for (int r = 0; r < R; r++) {
@@ -210,14 +232,14 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        __syncthreads();
+        BM_SYNCTHREADS();
         const uint64_t *Qs = stage + (size_t)(r & 1) * BUF, *Ss = Qs + TQB * PCH * 2 * CS;
         if (j == 0) {
 #pragma unroll
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
-                    if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+                    if (INTL) a0[u][v].zero(), a1[u][v].zero(), a2[u][v].zero();
                     else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
                 }
         }
@@ -238,13 +260,23 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                 y1[v] = rr[CS];
             }
             if (INTL) {
+                uint32_t xl[3][2], xh[3][2], yl[3][2], yh[3][2]; // [x0, x1, x0 + x1] split at bit 29
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const uint64_t xv[3] = {x0[u], x1[u], x0[u] + x1[u]}, yv[3] = {y0[u], y1[u], y0[u] + y1[u]};
+#pragma unroll
+                    for (int t = 0; t < 3; t++) {
+                        xl[t][u] = (uint32_t)xv[t] & M29, xh[t][u] = (uint32_t)(xv[t] >> 29);
+                        yl[t][u] = (uint32_t)yv[t] & M29, yh[t][u] = (uint32_t)(yv[t] >> 29);
+                    }
+                }
 #pragma unroll
                 for (int u = 0; u < 2; u++)
 #pragma unroll
                     for (int v = 0; v < 2; v++) {
-                        a0[u][v] += (u128)x0[u] * y0[v];
-                        a2[u][v] += (u128)x1[u] * y1[v];
-                        a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
+                        a0[u][v].mac(xl[0][u], xh[0][u], yl[0][v], yh[0][v]);
+                        a2[u][v].mac(xl[1][u], xh[1][u], yl[1][v], yh[1][v]);
+                        a1[u][v].mac(xl[2][u], xh[2][u], yl[2][v], yh[2][v]);
                     }
             } else {
                 double dx0[2], dx1[2], dxs[2], dy0[2], dy1[2], dys[2];
@@ -262,16 +294,17 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                     }
             }
         }
-        // folds: (2q)^2 < 2^118 in 128 bits (q0) / 3 q1 per part below 2^51 (q1): every 512 parts
-        if (((i0 + pc - part_lo) & 511) == 0 && i0 + pc < part_hi) {
+        // folds: Acc29 every PCH = 8 parts (q0, q2: at most 15 products per sum) / 3 q1 per part below
+        // 2^51 (q1): every 512 parts
+        if ((INTL || ((i0 + pc - part_lo) & 511) == 0) && i0 + pc < part_hi) {
 #pragma unroll
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
                     if (INTL) {
-                        a0[u][v] = red128s<PI>(a0[u][v], P.r64);
-                        a1[u][v] = red128s<PI>(a1[u][v], P.r64);
-                        a2[u][v] = red128s<PI>(a2[u][v], P.r64);
+                        a0[u][v].set(red128s<PI>(a0[u][v].value(), P.r64));
+                        a1[u][v].set(red128s<PI>(a1[u][v].value(), P.r64));
+                        a2[u][v].set(red128s<PI>(a2[u][v].value(), P.r64));
                     } else {
                         f0[u][v] = (double)f64_mod_q1(f0[u][v]);
                         f1[u][v] = (double)f64_mod_q1(f1[u][v]);
@@ -291,9 +324,9 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                     const int jj = sl * CS + c;
                     uint64_t d0, d2, kk;
                     if (INTL) {
-                        d0 = red128s<PI>(a0[u][v], P.r64);
-                        d2 = red128s<PI>(a2[u][v], P.r64);
-                        kk = red128s<PI>(a1[u][v], P.r64);
+                        d0 = red128s<PI>(a0[u][v].value(), P.r64);
+                        d2 = red128s<PI>(a2[u][v].value(), P.r64);
+                        kk = red128s<PI>(a1[u][v].value(), P.r64);
                     } else {
                         d0 = f64_mod_q1(f0[u][v]);
                         d2 = f64_mod_q1(f2[u][v]);
@@ -304,7 +337,7 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                     K.D2[((size_t)pi * NL + L) * N + jj] = d2;
                 }
         }
-        __syncthreads(); // every read of buffer r & 1 is done before round r + 2 overwrites it
+        BM_SYNCTHREADS(); // every read of buffer r & 1 is done before round r + 2 overwrites it
     }
 }
 
@@ -474,14 +507,14 @@ template <uint32_t COLS> BM_D uint32_t tmem_alloc(uint32_t *s_addr) // all threa
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    BM_SYNCTHREADS();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     return *s_addr + ((uint32_t)(32 * (warp & 3)) << 16) + (COLS / 4) * (uint32_t)(warp >> 2);
 }
 template <uint32_t COLS> BM_D void tmem_free(uint32_t base) // all threads, after every TMEM access of the CTA
 {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    BM_SYNCTHREADS();
     if ((threadIdx.x >> 5) == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
 }
@@ -575,8 +608,16 @@ BM_D uint32_t cluster_rank()
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
-BM_D void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-BM_D void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+BM_D void cluster_arrive()
+{
+    bm_jitter();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+BM_D void cluster_wait()
+{
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    bm_jitter();
+}
 // generic address of the same shared-memory location in CTA `rank` of this cluster
 BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
 {
@@ -621,7 +662,7 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
             }
             cluster_arrive(); // (2) arrive: rank 0's copy of c1 is done (waited for before c1 is rewritten)
         }
-        __syncthreads(); // S0 / S1 of the previous step (or the initial staging) are complete
+        BM_SYNCTHREADS(); // S0 / S1 of the previous step (or the initial staging) are complete
         // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
 #pragma unroll
         for (int e = 0; e < E; e++) a[e] = S1[nat_auto(nt, e, g)];
@@ -680,7 +721,7 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
                     a[e] = reduce_bnd<0>(v);
                 }
                 if (CL) cluster_wait(); // (2) wait: c1 may be rewritten now
-                __syncthreads();        // every read of the old c_c is done
+                BM_SYNCTHREADS();        // every read of the old c_c is done
 #pragma unroll
                 for (int e = 0; e < E; e++) S[nat_at(nt, e)] = a[e];
             } else {
@@ -778,7 +819,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder_c3(MatchK K, CtBuf cin, int L)
         } else if (rank == 1) {
             if (i > 0) { // c1_i = NTT_q0(c1coef_i), canonical, natural order
                 fwd<0>(a, XB, K.pr[0]);
-                __syncthreads(); // every read of the old S1 (this CTA's gathers) is done
+                BM_SYNCTHREADS(); // every read of the old S1 (this CTA's gathers) is done
 #pragma unroll
                 for (int e = 0; e < E; e++) R1[nat_at(nt, e)] = a[e];
             }
@@ -793,7 +834,7 @@ __global__ void __launch_bounds__(T, 1) k_ladder_c3(MatchK K, CtBuf cin, int L)
                 const uint64_t ks = shoup4<0>(R2[jp], kk[e & 1]);
                 a[e] = reduce_bnd<0>(ks + 2 * Q0 - a[e] + R1[j] + R1[jp]);
             }
-            __syncthreads();
+            BM_SYNCTHREADS();
 #pragma unroll
             for (int e = 0; e < E; e++) R1[nat_at(nt, e)] = a[e];
         }
@@ -935,7 +976,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup / 128-bit product operand
 #pragma unroll
         for (int e = 0; e < E; e++) SX[nat_at(nt, e)].y = a[e];
-        __syncthreads();
+        BM_SYNCTHREADS();
         // ---- the s-1 rotations' key-switch products, two coefficients (one 16-byte key position) at a
         //      time, the next rotation's keys loaded while this one's are used
 #pragma unroll 1
@@ -985,20 +1026,20 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         tmem_wait_st(); // the A stores above complete before phases 1, 2 read them back
         // ---- base_0 = sum_{r<s} sigma_r(c0) by log2(s) doublings t <- t + sigma_{2^i}(t) (exact sums mod
         //      q0: the same residues as the term-by-term sum), c0 staged in natural order over X~P
-        __syncthreads();
+        BM_SYNCTHREADS();
         stage_nat(SP, cin.at(pi, 0));
 #pragma unroll 1
         for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
-            __syncthreads();
+            BM_SYNCTHREADS();
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 a[e] = csub(SP[nat_at(nt, e)] + SP[nat_auto(nt, e, g)], Q0);
             }
-            __syncthreads();
+            BM_SYNCTHREADS();
 #pragma unroll
             for (int e = 0; e < E; e++) SP[nat_at(nt, e)] = a[e];
         }
-        __syncthreads();
+        BM_SYNCTHREADS();
 #pragma unroll
         for (int e = 0; e < E; e++) b0s[pos_M4(tid, e)] = SP[nat_at(nt, e)];
     tmem_free<512>(s_tmem);

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(T, 1) k_rot1_digits(ExpK K)
     uint64_t *xu = K.XU + (size_t)ct * XU_POLYS * N;
     const int nt = nat_tid(tid);
     stage_nat(S, c1); // natural order: conflict-free gather (ntt3.cuh nat_at)
-    __syncthreads();
+    BM_SYNCTHREADS();
     uint64_t a[E];
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = S[nat_auto(nt, e, K.g)];
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             fwd<0>(a, sm, K.pr[0]);
         }
         if (c == 0) { // sigma_g(c0)[q_l] by a gather (natural order; c0 is this CTA's to overwrite)
-            __syncthreads(); // previous limb's gathers from S are done
+            BM_SYNCTHREADS(); // previous limb's gathers from S are done
             stage_nat(S, c0 + (size_t)l * N);
-            __syncthreads();
+            BM_SYNCTHREADS();
         }
         const uint64_t q = l ? Q1 : Q0;
         const ulonglong2 *kl0 = k0 + (size_t)l * N, *kl1 = k1 + (size_t)l * N;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
             a[e] = l ? reduce_bnd<1>(va) : reduce_bnd<0>(va);
             a[e + 1] = l ? reduce_bnd<1>(vb) : reduce_bnd<0>(vb);
         }
-        if (c == 0) __syncthreads(); // every gather of the old c0[q_l] is done before it is overwritten
+        if (c == 0) BM_SYNCTHREADS(); // every gather of the old c0[q_l] is done before it is overwritten
 #pragma unroll
         for (int e = 0; e < E; e += 2) st2(cc + (size_t)l * N + pos_M4(tid, e), a[e], a[e + 1]);
     }
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(T, 1) k_cmp_rot(CmpK C)
     const int nt = nat_tid(tid);
     stage_nat(S0, ci); // natural order: conflict-free gathers (ntt3.cuh nat_at)
     stage_nat(S1, ci + N);
-    __syncthreads();
+    BM_SYNCTHREADS();
 #pragma unroll
     for (int e = 0; e < E; e++) a[e] = S1[nat_auto(nt, e, g)];
     inv<0>(a, XB, K.pr[0]);

@@ -53,11 +53,11 @@ __global__ void __launch_bounds__(T, 1) k_encrypt(EncK Ek)
     uint64_t a[E];
     // phase 0: NTT(u) -> kept in c0 until phase 2;  phase 1: c1 = u a + e1;  phase 2: c0 = u b + e0 + pt
     for (int ph = 0; ph < 3; ph++) {
-        __syncthreads();
+        BM_SYNCTHREADS();
         const uint32_t purpose = ph == 0 ? P_ENC_U : ph == 1 ? P_ENC_E1 : P_ENC_E0;
         sample_to_smem(sm, make_stream(Ek.seed, purpose, o, 0, Ek.kx), ph != 0, q, P.one_p,
                        ph == 2 ? Ek.pt + (size_t)ct * N : nullptr);
-        __syncthreads();
+        BM_SYNCTHREADS();
 #pragma unroll
         for (int e = 0; e < E; e++) a[e] = sm[pidx(j_M1(tid, e))];
         fwd_rt(a, sm, P, pi);
@@ -99,12 +99,12 @@ __global__ void __launch_bounds__(T, 1) k_convert(ConvK C, int dir)
     if (dir == 0) {
         load_coef(a, in);
         fwd_rt(a, sm, P, pidx_);
-        __syncthreads(); // in may alias out
+        BM_SYNCTHREADS(); // in may alias out
         store_eval(out, a);
     } else {
         load_eval(a, in);
         inv_rt(a, sm, P, pidx_);
-        __syncthreads();
+        BM_SYNCTHREADS();
         store_coef(out, a);
     }
 }
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(T, 1) k_decrypt(DecK K)
         a[e + 1] = shoup4<0>(a[e + 1], wb);
     }
     inv<0>(a, sm, K.pr0); // c1 s, canonical, coefficient j_M1(tid, e)
-    __syncthreads();      // the exchange buffer becomes X
+    BM_SYNCTHREADS();      // the exchange buffer becomes X
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const int k = j_M1(tid, e);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(T, 1) k_decrypt(DecK K)
         const double2 z = K.zeta[k];
         X[brev13(k)] = make_double2(m * z.x, m * z.y);
     }
-    __syncthreads();
+    BM_SYNCTHREADS();
     // iterative radix-2 DIT over bit-reversed input: block length len, twiddle exp(2 pi i k / len) = zeta[2 k N / len]
 #pragma unroll 1
     for (int lg = 1; lg <= LOGN; lg++) {
@@ -200,7 +200,10 @@ __global__ void __launch_bounds__(T, 1) k_decrypt(DecK K)
             X[i] = make_double2(u.x + vr, u.y + vi);
             X[j] = make_double2(u.x - vr, u.y - vi);
         }
-        __syncthreads();
+        BM_SYNCTHREADS();
     }
-    for (int b = tid; b < K.B; b += T) K.scores[(size_t)c * K.B + b] = X[K.slot_t[b * K.s_len]].x * K.inv_scale;
+    for (int b = tid; b < K.B; b += T) {
+        BM_CHECK(b * K.s_len < SLOTS && K.slot_t[b * K.s_len] < N);
+        K.scores[(size_t)c * K.B + b] = X[K.slot_t[b * K.s_len]].x * K.inv_scale;
+    }
 }

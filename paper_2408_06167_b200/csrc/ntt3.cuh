@@ -56,15 +56,16 @@ BM_D void xchg(uint64_t a[E], uint64_t *sm)
     const int tid = threadIdx.x;
     constexpr bool local_w = (FROM != 1);          // writes stay in the warp's region
     constexpr bool local_r = (TO != 1);            // reads stay in the warp's region
-    if (FROM == 1 || (FROM == 3 && TO == 2)) __syncthreads();
-    else __syncwarp();
+    if (FROM == 1 || (FROM == 3 && TO == 2)) BM_SYNCTHREADS();
+    else BM_SYNCWARP();
 #pragma unroll
     for (int k = 0; k < E; k++) {
         const int j = FROM == 1 ? j_M1(tid, k) : FROM == 2 ? j_M2(tid, k) : j_M3(tid, k);
+        BM_CHECK(pidx(j) < SMEM_WORDS);
         sm[pidx(j)] = a[k];
     }
-    if (local_w && local_r) __syncwarp();
-    else __syncthreads();
+    if (local_w && local_r) BM_SYNCWARP();
+    else BM_SYNCTHREADS();
 #pragma unroll
     for (int k = 0; k < E; k++) {
         const int j = TO == 1 ? j_M1(tid, k) : TO == 2 ? j_M2(tid, k) : j_M3(tid, k);
@@ -295,7 +296,12 @@ BM_HD constexpr int npad(int i)
 }
 // word of this thread's element e (M4) / of the element sigma_g moves there
 BM_D int nat_at(int ntid, int e) { return npad(ntid) + npad(nat_e(e)); }
-BM_D int nat_auto_i(uint32_t i, uint32_t g) { return npad((int)((i * g + ((g - 1) >> 1)) & (N - 1))); }
+BM_D int nat_auto_i(uint32_t i, uint32_t g)
+{
+    const int w = npad((int)((i * g + ((g - 1) >> 1)) & (N - 1)));
+    BM_CHECK(w >= 0 && w < SMEM_WORDS && (g & 1));
+    return w;
+}
 BM_D int nat_auto(int ntid, int e, uint32_t g) { return nat_auto_i((uint32_t)(ntid | nat_e(e)), g); }
 // natural index of element e when e is not a compile-time constant
 BM_D uint32_t nat_i(int ntid, int e) { return (uint32_t)(ntid | brev13(4 * (e >> 1) + (e & 1))); }

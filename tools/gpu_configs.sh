@@ -7,7 +7,8 @@ run() {  # label, args
   echo "rc=$?" >> gpurun_out/cfg_$1.err
   tail -1 gpurun_out/cfg_$1.json >> gpurun_out/configs.jsonl
 }
-for spec in ${SPECS:-"1:1 2:1 2:2 2:4 2:8 3:1 3:2 3:4 5:16 5:8 5:4"}; do
+SPECS=${SPECS:-"1:1 2:1 2:2 2:4 2:8 3:1 3:2 3:4 5:16 5:8 5:4"}
+for spec in $SPECS; do
   c=${spec%%:*}; p=${spec#*:}
   case $c in
     5) run c${c}p$p --config $c --p $p --steps 2 --warmup 1 --no-e2e ;;
