@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-single", action="store_true", help="skip the single-query latency leg")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row legs (f1, f3, f4 on configs[1])")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library option NAME=VALUE (bm.OPTIONS; A/B runs only, the defaults are the product)")
     ap.add_argument("--quiet", action="store_true")
     return ap.parse_args()
 
@@ -295,6 +297,9 @@ def run_ours(args):
     # ranks and the in-bench oracle check re-encrypts with the same streams (the library default is
     # OS entropy)
     B.bm_rng_mode(B.RNG_SEEDED)
+    for o in args.opt:
+        k, v = o.split("=")
+        B.bm_set_option(k, int(v))
 
     shard_of = args.shard_of if args.shard_of else (8 if args.config == 5 and world < 8 else None)
     if shard_of is not None and world > 1 and shard_of != world:
@@ -486,6 +491,8 @@ def run_ours(args):
             "clocks": clocks,
             "setup_s": round(t_setup, 1),
         }
+        if args.opt:
+            line["config"]["options"] = args.opt
         line.update(extras)
         print(json.dumps(line), flush=True)
     if gat is not None:
@@ -1016,6 +1023,9 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if os.environ.get("BM_BENCH_WATCHDOG"):   # debugging aid: dump every thread's stack and exit after N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["BM_BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(T, 1) k_rot1_ks(ExpK K)
         // 8-byte keys (w planes), exact 128-bit inner products, one reduction (as K3)
         const ulonglong2 w0 = ld2(reinterpret_cast<const uint64_t *>(k0 + 2 * N) + pos);
         const ulonglong2 w1 = ld2(reinterpret_cast<const uint64_t *>(k1 + 2 * N) + pos);
-        a[e] = red128s<2>((u128)u.x * w0.x + (u128)v.x * w1.x, K.pr[2].r64);
-        a[e + 1] = red128s<2>((u128)u.y * w0.y + (u128)v.y * w1.y, K.pr[2].r64);
+        a[e] = red128s<2>(dot2(u.x, w0.x, v.x, w1.x), K.pr[2].r64);
+        a[e + 1] = red128s<2>(dot2(u.y, w0.y, v.y, w1.y), K.pr[2].r64);
     }
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll

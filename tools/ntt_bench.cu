@@ -59,6 +59,41 @@ __global__ void __launch_bounds__(512, MINB3) k_bench3(PrimeK P, uint64_t *data,
     v3::store_coef(d, a);
 }
 
+// two polynomials per CTA through the dual transforms (ntt3.cuh fwd2x / inv2x); the butterfly count
+// of one launch is 2x that of k_bench3 with the same grid
+template <int PI>
+__global__ void __launch_bounds__(512, 1) k_bench3x2(PrimeK P, uint64_t *data, int iters)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t a[16], b[16];
+    uint64_t *d = data + (size_t)blockIdx.x * 2 * N;
+    v3::load_coef(a, d);
+    v3::load_coef(b, d + N);
+    for (int it = 0; it < iters; it++) {
+        v3::fwd2x<PI>(a, b, sm, sm + SMEM_WORDS, P);
+        v3::inv2x<PI>(a, b, sm, sm + SMEM_WORDS, P);
+    }
+    v3::store_coef(d, a);
+    v3::store_coef(d + N, b);
+}
+
+// hybrid: one integer-prime polynomial (PI) and one q1 polynomial on the FP64 pipe per CTA (fwd_h / inv_h)
+template <int PI>
+__global__ void __launch_bounds__(512, 1) k_bench3h(PrimeK P, PrimeK P1, uint64_t *data, int iters)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t a[16], b[16];
+    uint64_t *d = data + (size_t)blockIdx.x * 2 * N;
+    v3::load_coef(a, d);
+    v3::load_coef(b, d + N);
+    for (int it = 0; it < iters; it++) {
+        v3::fwd_h<PI, true, 1>(a, b, sm, sm + SMEM_WORDS, P, P1.fwdf);
+        v3::inv_h<PI, 1>(a, b, sm, sm + SMEM_WORDS, P, P1.invf, P1.ninvf, P1.ninv_w1f);
+    }
+    v3::store_coef(d, a);
+    v3::store_coef(d + N, b);
+}
+
 static ulonglong2 sp(uint64_t w, uint64_t q) { return make_ulonglong2(w, shoup_companion(w, q)); }
 
 int main(int argc, char **argv)
@@ -71,9 +106,12 @@ int main(int argc, char **argv)
                    {k_bench3<0>, k_bench3<1>, k_bench3<2>}, {k_bench3<3>, k_bench3<3>, k_bench3<3>}};
     for (int v = 0; v < 4; v++)
         for (int i = 0; i < 3; i++) cudaFuncSetAttribute(kf[v][i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BYTES);
-    for (int v = 1; v < 4; v++)
+    KF kx2[3] = {k_bench3x2<0>, k_bench3x2<1>, k_bench3x2<2>};
+    for (int i = 0; i < 3; i++) cudaFuncSetAttribute(kx2[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SMEM_WORDS * 8));
+    for (int v = 1; v < 5; v++)
     for (int pi = 0; pi < 3; pi++) {
         if (v == 3 && pi != 1) continue; // v4 = q1 on the FP64 pipe
+        if (v == 4 && pi == 1) continue; // v5 = dual transforms (q0, P)
         const HostPrime &H = host_prime(pi);
         std::vector<ulonglong2> tw(2 * N);
         // v1/v2 cores index the tables directly; the v3 cores (ntt3.cuh) read them in load order (tw_pos)
@@ -101,30 +139,92 @@ int main(int argc, char **argv)
             P.fwdf = dtwf; P.invf = dtwf + N;
             P.ninvf = fp(H.ninv); P.ninv_w1f = fp(mulmod_h(H.ninv, H.inv[1], H.q));
         }
-        std::vector<uint64_t> h((size_t)blocks * N);
+        const int per = v == 4 ? 2 : 1;                  // polynomials per CTA
+        std::vector<uint64_t> h((size_t)blocks * N * per);
         srand(pi + 1);
         for (auto &x : h) x = (((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ rand()) % H.q;
         uint64_t *dd;
         cudaMalloc(&dd, h.size() * 8);
         cudaMemcpy(dd, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-        KF k = kf[v][pi];
+        KF k = v == 4 ? kx2[pi] : kf[v][pi];
         const int thr = v >= 2 ? 512 : 256;
-        k<<<blocks, thr, SM_BYTES>>>(P, dd, 1); // warm-up (+ round trip)
+        const size_t smb = v == 4 ? 2 * SMEM_WORDS * 8 : SM_BYTES;
+        k<<<blocks, thr, smb>>>(P, dd, 1); // warm-up (+ round trip)
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        k<<<blocks, thr, SM_BYTES>>>(P, dd, iters);
+        k<<<blocks, thr, smb>>>(P, dd, iters);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         std::vector<uint64_t> back(h.size());
         cudaMemcpy(back.data(), dd, h.size() * 8, cudaMemcpyDeviceToHost);
         bool ok = back == h;
-        double bfly = (double)blocks * iters * 2 * (N / 2) * LOGN;
+        double bfly = (double)blocks * per * iters * 2 * (N / 2) * LOGN;
         int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
         printf("v%d prime %d: %s  %.3f ms  %.1f Gbfly/s  %.2f bfly/clk/SM (at %d MHz)  err=%s\n", v + 1, pi, ok ? "ok" : "MISMATCH", ms,
                bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
         cudaFree(dd); cudaFree(dtw); cudaFree(dtwf);
+    }
+    // v6: hybrid pairs (an integer-prime transform interleaved with a q1 transform on the FP64 pipe)
+    auto mk = [&](int pi, bool fp) {
+        const HostPrime &H = host_prime(pi);
+        std::vector<ulonglong2> tw(2 * N);
+        for (int k = 0; k < N; k++) tw[v3::tw_pos(k)] = sp(H.fwd[k], H.q), tw[N + v3::tw_pos(k)] = sp(H.inv[k], H.q);
+        ulonglong2 *dtw;
+        cudaMalloc(&dtw, tw.size() * 16);
+        cudaMemcpy(dtw, tw.data(), tw.size() * 16, cudaMemcpyHostToDevice);
+        PrimeK P;
+        P.q = H.q; P.q2 = 2 * H.q; P.fwd = dtw; P.inv = dtw + N;
+        P.ninv = sp(H.ninv, H.q);
+        P.ninv_w1 = sp(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
+        P.r64 = sp((uint64_t)(((u128)1 << 64) % H.q), H.q);
+        P.one_p = (uint64_t)(((u128)1 << 64) / H.q);
+        if (fp) {
+            auto fpp = [&](uint64_t w) { double a = (double)w, b = a / (double)H.q; uint64_t x, y;
+                                         memcpy(&x, &a, 8); memcpy(&y, &b, 8); return make_ulonglong2(x, y); };
+            std::vector<ulonglong2> tf(2 * N);
+            for (int k = 0; k < N; k++) tf[v3::tw_pos(k)] = fpp(H.fwd[k]), tf[N + v3::tw_pos(k)] = fpp(H.inv[k]);
+            ulonglong2 *dtwf;
+            cudaMalloc(&dtwf, tf.size() * 16);
+            cudaMemcpy(dtwf, tf.data(), tf.size() * 16, cudaMemcpyHostToDevice);
+            P.fwdf = dtwf; P.invf = dtwf + N;
+            P.ninvf = fpp(H.ninv); P.ninv_w1f = fpp(mulmod_h(H.ninv, H.inv[1], H.q));
+        }
+        return P;
+    };
+    const PrimeK P1 = mk(1, true);
+    typedef void (*KH)(PrimeK, PrimeK, uint64_t *, int);
+    KH kh[2] = {k_bench3h<0>, k_bench3h<2>};
+    for (int i = 0; i < 2; i++) {
+        cudaFuncSetAttribute(kh[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SMEM_WORDS * 8));
+        const int pi = i ? 2 : 0;
+        const PrimeK P = mk(pi, false);
+        std::vector<uint64_t> h((size_t)blocks * 2 * N);
+        srand(pi + 7);
+        for (size_t b = 0; b < (size_t)blocks; b++)
+            for (int k = 0; k < 2 * N; k++)
+                h[b * 2 * N + k] = (((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ rand()) % (k < N ? P.q : Q1);
+        uint64_t *dd;
+        cudaMalloc(&dd, h.size() * 8);
+        cudaMemcpy(dd, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        kh[i]<<<blocks, 512, 2 * SMEM_WORDS * 8>>>(P, P1, dd, 1);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        kh[i]<<<blocks, 512, 2 * SMEM_WORDS * 8>>>(P, P1, dd, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        std::vector<uint64_t> back(h.size());
+        cudaMemcpy(back.data(), dd, h.size() * 8, cudaMemcpyDeviceToHost);
+        const bool ok = back == h;
+        const double bfly = (double)blocks * 2 * iters * 2 * (N / 2) * LOGN;
+        int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+        printf("v6 hybrid prime %d + q1 fp64: %s  %.3f ms  %.1f Gbfly/s  %.2f bfly/clk/SM (at %d MHz)  err=%s\n", pi,
+               ok ? "ok" : "MISMATCH", ms, bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000,
+               cudaGetErrorString(cudaGetLastError()));
+        cudaFree(dd);
     }
     return 0;
 }
