@@ -564,6 +564,7 @@ def pick_pairs(W, n, seed=5):
     lo, nl, nq = W.lo, W.n_local, W.nq
     if nl == 0:
         return []
+    n = min(n, nq * nl)                          # configs[0]: one pair in all
     pairs = {(0, lo), (nq - 1, lo + nl - 1), (min(W.gq, nq - 1), lo), (W.gq - 1, lo + nl - 1),
              (nq // 2, lo + nl // 2)}
     for g in range(W.G):                         # one pair per query group at least

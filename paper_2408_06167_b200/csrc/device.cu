@@ -172,8 +172,6 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_tensor<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
-    cudaFuncSetAttribute(k_digits_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM_BYTES);
-    cudaFuncSetAttribute(k_relin_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
@@ -262,7 +260,6 @@ struct OptInit {
         g_opt[BM_OPT_LADDER_C3] = 1;       // latency-mode ladder on 3-CTA clusters
         g_opt[BM_OPT_LADDER_TAIL] = 1;     // a large launch's partial last wave on the cluster ladders
         g_opt[BM_OPT_CMP_CHUNK] = 4096;    // pairs per bm_match_cmp chunk
-        g_opt[BM_OPT_PAIR_KERNELS] = 0;    // K2 / K3 as one CTA per pair with paired transforms
     }
 } g_opt_init;
 int64_t opt(int k) { return g_opt[k].load(std::memory_order_relaxed); }
@@ -1145,15 +1142,12 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             counted();
             end();
-            const bool pairk = opt(BM_OPT_PAIR_KERNELS) != 0;
             beg(1, 6 * np);
-            if (pairk) k_digits_h<<<npu, T, PAIR_SMEM_BYTES, s>>>(K);
-            else k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
+            k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
             counted();
             end();
             beg(2, 6 * np);
-            if (pairk) k_relin_h<<<npu, T, PAIR_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
-            else k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
+            k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             counted();
             end();
             rc = launch_check();
@@ -1447,8 +1441,7 @@ int bm_match_host_ring(const bm_params *prm, const bm_evk_dev *evk, const uint64
 int bm_set_option(int32_t key, int64_t value)
 {
     if (key < 0 || key >= BM_OPT_COUNT_) return BM_ERR_INVALID_ARG;
-    const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL ||
-                      key == BM_OPT_PAIR_KERNELS;
+    const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL;
     if (flag ? (value != 0 && value != 1) : key == BM_OPT_HOST_GROUPS ? value < 0 : value < 1) return BM_ERR_INVALID_ARG;
     g_opt[key].store(value);
     return BM_OK;

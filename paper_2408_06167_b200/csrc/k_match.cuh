@@ -116,14 +116,14 @@ template <int PI> BM_D uint64_t red128s(u128 v, ulonglong2 r64)
     return reduce_bnd<PI>(t);
 }
 
-// u0 w0 + u1 w1 as a 128-bit value for u < 2^61, w < 2^60 (the key-switch inner products: lazy
-// [0, 2q) digits times canonical key residues) from 30-bit limbs: every partial product one IMAD.WIDE
-// into a carry-free 64-bit sum (L < 2^61, M < 2^63, H < 2^62), then L + M 2^30 + H 2^60 -- instead of
-// two 128-bit multiply-adds with their carry chains
+// u0 w0 + u1 w1 as a 128-bit value (the key-switch inner products: lazy [0, 2q) digits times canonical
+// key residues, u < 2^61, w < 2^60).  BM_DOT_SPLIT (A/B variant): from 30-bit limbs,
+// every partial product one IMAD.WIDE into a carry-free 64-bit sum (L < 2^61, M < 2^63, H < 2^62),
+// then L + M 2^30 + H 2^60 -- fewer FMA-pipe slots, but K3 ran 3% slower than with the 128-bit form
 BM_D u128 dot2(uint64_t u0, uint64_t w0, uint64_t u1, uint64_t w1)
 {
-#ifdef BM_DOT_U128
-    return (u128)u0 * w0 + (u128)u1 * w1;
+#ifndef BM_DOT_SPLIT
+    return (u128)u0 * w0 + (u128)u1 * w1; // the product default: the split form measured 3% slower in K3
 #else
     constexpr uint32_t M30 = (1u << 30) - 1;
     const uint32_t a0 = (uint32_t)u0 & M30, b0 = (uint32_t)(u0 >> 30), c0 = (uint32_t)w0 & M30, d0 = (uint32_t)(w0 >> 30);
@@ -163,7 +163,8 @@ BM_D uint64_t f64_mod_q1(double x)
     return (uint64_t)__double_as_longlong(r + 4503599627370496.0) & ((1ull << 52) - 1);
 }
 
-// Integer-limb accumulator of the tensor (q0, q2): operands split into 29-bit limbs,
+// A/B variant (BM_TENSOR_ACC29; the tensor ran 7% SLOWER with it, so the product
+// keeps the 128-bit multiply-accumulate): integer-limb accumulator with operands split into 29-bit limbs,
 // x y = xl yl + (xl yh + xh yl) 2^29 + xh yh 2^58, every partial product ONE IMAD.WIDE into its own
 // 64-bit sum -- no carry chains (a 128-bit multiply-accumulate costs ~13 instructions, a third of
 // them IMAD.X carries on the FMA pipe).  Exact for up to 15 products of operands < 2^59 (the
@@ -182,19 +183,6 @@ struct Acc29 {
     BM_D u128 value() const { return (u128)L + ((u128)M << 29) + ((u128)H << 58); }
 };
 constexpr uint32_t M29 = (1u << 29) - 1;
-// the plain 128-bit multiply-accumulate with the same interface (the product default: measured faster,
-// DESIGN.md sec. 12; operands are rebuilt from the limbs, which the compiler folds away)
-struct Acc128 {
-    u128 v;
-    BM_D void zero() { v = 0; }
-    BM_D void set(uint64_t r) { v = r; }
-    BM_D void mac(uint32_t xl, uint32_t xh, uint32_t yl, uint32_t yh)
-    {
-        v += (u128)(((uint64_t)xh << 29) | xl) * (((uint64_t)yh << 29) | yl);
-    }
-    BM_D u128 value() const { return v; }
-};
-
 // grid: ((qt * (N / CS) + slice) * nst + st) * 2 + l  (limbs alternate, so each SM holds one
 // q0-limb CTA on the integer pipe and one q1-limb CTA on the FP64 pipe; set tiles next: the CTAs
 // that share a query slice run together and the query data streams from HBM once)
@@ -250,9 +238,9 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
     auto chunk_pc = [&](int j) { const int i0 = part_lo + j * PCH; return part_hi - i0 < PCH ? part_hi - i0 : PCH; };
     tensor_stage<L, NL, SW>(K, stage, stage + TQB * PCH * 2 * CS, qt, sl0, st, part_lo, chunk_pc(0));
 #ifdef BM_TENSOR_ACC29
-    Acc29 a0[2][2], a1[2][2], a2[2][2];    // q0, q2: split-limb integer sums (Acc29)
+    Acc29 a0[2][2], a1[2][2], a2[2][2];    // q0, q2: split-limb integer sums (A/B variant)
 #else
-    Acc128 a0[2][2], a1[2][2], a2[2][2];   // q0, q2: 128-bit integer sums
+    u128 a0[2][2], a1[2][2], a2[2][2];     // q0, q2: 128-bit integer sums
 #endif
     double f0[2][2], f1[2][2], f2[2][2];   // q1: exact FP64 sums of signed residues
 #pragma unroll 1
@@ -274,7 +262,11 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
+#ifdef BM_TENSOR_ACC29
                     if (INTL) a0[u][v].zero(), a1[u][v].zero(), a2[u][v].zero();
+#else
+                    if (INTL) a0[u][v] = a1[u][v] = a2[u][v] = 0;
+#endif
                     else f0[u][v] = f1[u][v] = f2[u][v] = 0.0;
                 }
         }
@@ -294,6 +286,18 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                 y0[v] = rr[0];
                 y1[v] = rr[CS];
             }
+#ifndef BM_TENSOR_ACC29
+            if (INTL) {
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+#pragma unroll
+                    for (int v = 0; v < 2; v++) {
+                        a0[u][v] += (u128)x0[u] * y0[v];
+                        a2[u][v] += (u128)x1[u] * y1[v];
+                        a1[u][v] += (u128)(x0[u] + x1[u]) * (y0[v] + y1[v]);
+                    }
+            } else {
+#else
             if (INTL) {
                 uint32_t xl[3][2], xh[3][2], yl[3][2], yh[3][2]; // [x0, x1, x0 + x1] split at bit 29
 #pragma unroll
@@ -314,6 +318,7 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                         a1[u][v].mac(xl[2][u], xh[2][u], yl[2][v], yh[2][v]);
                     }
             } else {
+#endif
                 double dx0[2], dx1[2], dxs[2], dy0[2], dy1[2], dys[2];
 #pragma unroll
                 for (int u = 0; u < 2; u++) dx0[u] = u2d(x0[u]), dx1[u] = u2d(x1[u]), dxs[u] = dx0[u] + dx1[u];
@@ -342,9 +347,15 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
 #pragma unroll
                 for (int v = 0; v < 2; v++) {
                     if (INTL) {
+#ifdef BM_TENSOR_ACC29
                         a0[u][v].set(red128s<PI>(a0[u][v].value(), P.r64));
                         a1[u][v].set(red128s<PI>(a1[u][v].value(), P.r64));
                         a2[u][v].set(red128s<PI>(a2[u][v].value(), P.r64));
+#else
+                        a0[u][v] = red128s<PI>(a0[u][v], P.r64);
+                        a1[u][v] = red128s<PI>(a1[u][v], P.r64);
+                        a2[u][v] = red128s<PI>(a2[u][v], P.r64);
+#endif
                     } else {
                         f0[u][v] = (double)f64_mod_q1(f0[u][v]);
                         f1[u][v] = (double)f64_mod_q1(f1[u][v]);
@@ -364,9 +375,15 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                     const int jj = sl * CS + c;
                     uint64_t d0, d2, kk;
                     if (INTL) {
+#ifdef BM_TENSOR_ACC29
                         d0 = red128s<PI>(a0[u][v].value(), P.r64);
                         d2 = red128s<PI>(a2[u][v].value(), P.r64);
                         kk = red128s<PI>(a1[u][v].value(), P.r64);
+#else
+                        d0 = red128s<PI>(a0[u][v], P.r64);
+                        d2 = red128s<PI>(a2[u][v], P.r64);
+                        kk = red128s<PI>(a1[u][v], P.r64);
+#endif
                     } else {
                         d0 = f64_mod_q1(f0[u][v]);
                         d2 = f64_mod_q1(f2[u][v]);
@@ -616,117 +633,6 @@ BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
                  : "memory");
 #pragma unroll
     for (int i = 0; i < 16; i++) v[i] = (uint64_t)r[2 * i] | ((uint64_t)r[2 * i + 1] << 32);
-}
-
-// ================================================================== K2 / K3 as pair kernels (two transforms at a time)
-// One CTA per (query, set) pair runs the work of K2's two CTAs (or K3's two), with the independent
-// transforms paired: an integer-prime transform interleaved stage by stage with a q1 transform on the
-// FP64 pipe (ntt3f.cuh fwd_h / inv_h), or two integer transforms sharing twiddle loads and exchange
-// barriers (ntt3.cuh fwd2x / inv2x).  Two exchange buffers; the values a phase parks for later live in
-// tensor memory.  Same residues as k_digits / k_relin (the arithmetic is the same, only interleaved).
-constexpr size_t PAIR_SMEM_BYTES = 2 * SMEM_WORDS * sizeof(uint64_t);
-
-// K2h: x0 = INTT_q0(d2[q0]) || x1 = INTT_q1(d2[q1]);  NTT_q0(x1) || NTT_q1(x0 mod q1);  NTT_P(x0) || NTT_P(x1)
-__global__ void __launch_bounds__(T, 1) k_digits_h(MatchK K)
-{
-    extern __shared__ uint64_t sm[];
-    uint64_t *XA = sm, *XB = sm + SMEM_WORDS;
-    const int64_t pi = blockIdx.x;
-    __shared__ uint32_t s_tmem;
-    const uint32_t tx = tmem_alloc<256>(&s_tmem); // x0 at +0, x1 at +32 columns
-    uint64_t a[E], b[E];
-    load_eval(a, K.D2 + ((size_t)pi * 2 + 0) * N);
-    load_eval(b, K.D2 + ((size_t)pi * 2 + 1) * N);
-    inv_h<0, 1>(a, b, XA, XB, K.pr[0], K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // x0, x1 canonical
-    tmem_st16(tx, a);
-    tmem_st16(tx + 32, b);
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const uint64_t x0 = a[e];
-        a[e] = b[e];                  // x1 (< q1 < q0) -> q0
-        b[e] = reduce_bnd<1>(x0);     // x0 mod q1
-    }
-    fwd_h<0, false, 1>(a, b, XA, XB, K.pr[0], K.pr[1].fwdf);
-    uint64_t *xu = K.XU + (size_t)pi * 4 * N;
-    store_eval(xu + 2 * N, a); // x1~[q0] (lazy [0, 2 q0): a Shoup operand only)
-    store_eval(xu + 0 * N, b); // x0~[q1]
-    tmem_ld16(tx, a);
-    tmem_ld16(tx + 32, b);
-    fwd2x<2, false>(a, b, XA, XB, K.pr[2]);
-    store_eval(xu + 1 * N, a); // x0~[P]
-    store_eval(xu + 3 * N, b); // x1~[P]
-    tmem_free<256>(s_tmem);
-}
-
-// K3h, both components of a pair: per component c, INTT_P(KS_c[P]) || INTT_q1(d_c[q1] + P^-1 KS_c[q1])
-// (hybrid), the rescale terms, parked; then NTT_q0 of both at once, and the q0-limb outputs (k_relin's
-// arithmetic, R22).
-__global__ void __launch_bounds__(T, 1) k_relin_h(MatchK K, CtBuf dst, int accumulate)
-{
-    extern __shared__ uint64_t sm[];
-    uint64_t *XA = sm, *XB = sm + SMEM_WORDS;
-    const int tid = threadIdx.x;
-    const int64_t pi = blockIdx.x;
-    __shared__ uint32_t s_tmem;
-    const uint32_t tt = tmem_alloc<256>(&s_tmem); // component 0's rescale term at +0
-    const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
-    const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
-    const ulonglong2 pinv0 = K.pinv[0], pinv1 = K.pinv[1];
-    uint64_t a[E], b[E];
-#pragma unroll 1
-    for (int c = 0; c < 2; c++) {
-        const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
-        const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N;
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int j = pos_M4(tid, e);
-            const ulonglong2 u = ld2(xu + 1 * N + j), v = ld2(xu + 3 * N + j);
-            const ulonglong2 w0 = ld2(r0 + 2 * 2 * N + j), w1 = ld2(r1 + 2 * 2 * N + j);
-            a[e] = red128s<2>(dot2(u.x, w0.x, v.x, w1.x), K.pr[2].r64);
-            a[e + 1] = red128s<2>(dot2(u.y, w0.y, v.y, w1.y), K.pr[2].r64);
-            const ulonglong2 u1 = ld2(xu + 0 * N + j), v1 = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
-            const ulonglong2 k0 = ld2(r0 + 1 * 2 * N + j), k1 = ld2(r1 + 1 * 2 * N + j);
-            b[e] = reduce_bnd<1>(dd.x + red128s<1>(dot2(u1.x, k0.x, v1.x, k1.x), K.pr[1].r64));
-            b[e + 1] = reduce_bnd<1>(dd.y + red128s<1>(dot2(u1.y, k0.y, v1.y, k1.y), K.pr[1].r64));
-        }
-        inv_h<2, 1>(a, b, XA, XB, K.pr[2], K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // Y, U canonical
-#pragma unroll
-        for (int e = 0; e < E; e++) {
-            const uint64_t y = a[e];
-            const uint64_t f = y > (QP >> 1) ? 1 : 0;
-            const uint64_t R = reduce_bnd<1>(b[e] + f + 4 * Q1 - shoup4<1>(y, pinv1)); // U - P^-1 y^
-            const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
-            a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
-        }
-        if (c == 0) tmem_st16(tt, a);
-    }
-    tmem_ld16(tt, b); // b = component 0's term, a = component 1's
-    fwd2x<0, false>(b, a, XA, XB, K.pr[0]);
-    const ulonglong2 q1inv = K.q1inv;
-#pragma unroll 1
-    for (int c = 0; c < 2; c++) {
-        const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
-        const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N;
-        uint64_t *co = dst.at(pi, c);
-        const uint64_t *A = c ? a : b;
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-            const int j = pos_M4(tid, e);
-            const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
-            const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
-            const uint64_t ka = red128s<0>(dot2(u.x, w0.x, v.x, w1.x), K.pr[0].r64);
-            const uint64_t kb = red128s<0>(dot2(u.y, w0.y, v.y, w1.y), K.pr[0].r64);
-            uint64_t oa = reduce_bnd<0>(shoup4<0>(dd.x + ka + 2 * Q0 - A[e], q1inv));
-            uint64_t ob = reduce_bnd<0>(shoup4<0>(dd.y + kb + 2 * Q0 - A[e + 1], q1inv));
-            if (accumulate) {
-                const ulonglong2 cc = *reinterpret_cast<const ulonglong2 *>(co + j);
-                oa = csub(oa + cc.x, Q0);
-                ob = csub(ob + cc.y, Q0);
-            }
-            st2(co + j, oa, ob);
-        }
-    }
-    tmem_free<256>(s_tmem);
 }
 
 // ================================================================== fused ladder (a7 + a8)

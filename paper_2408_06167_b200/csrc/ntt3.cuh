@@ -209,171 +209,6 @@ template <int PI> BM_D void inv(uint64_t a[E], uint64_t *sm, const PrimeK &P)
     }
 }
 
-// ------------------------------------------------------------------ two polynomials at once
-// The same transforms on two independent polynomials a, b of one prime (e.g. the ladder's two
-// key-switch components): each twiddle is loaded once for both, each exchange writes both before one
-// barrier, and the two butterfly streams interleave (one poly's shared-memory traffic overlaps the
-// other's arithmetic).  Exchange buffers smA, smB (SMEM_WORDS each).
-template <int FROM, int TO>
-BM_D void xchg2(uint64_t a[E], uint64_t b[E], uint64_t *smA, uint64_t *smB)
-{
-    const int tid = threadIdx.x;
-    constexpr bool local_w = (FROM != 1), local_r = (TO != 1);
-    if (FROM == 1 || (FROM == 3 && TO == 2)) BM_SYNCTHREADS();
-    else BM_SYNCWARP();
-#pragma unroll
-    for (int k = 0; k < E; k++) {
-        const int j = FROM == 1 ? j_M1(tid, k) : FROM == 2 ? j_M2(tid, k) : j_M3(tid, k);
-        smA[pidx(j)] = a[k];
-        smB[pidx(j)] = b[k];
-    }
-    if (local_w && local_r) BM_SYNCWARP();
-    else BM_SYNCTHREADS();
-#pragma unroll
-    for (int k = 0; k < E; k++) {
-        const int j = TO == 1 ? j_M1(tid, k) : TO == 2 ? j_M2(tid, k) : j_M3(tid, k);
-        a[k] = smA[pidx(j)];
-        b[k] = smB[pidx(j)];
-    }
-}
-
-template <int PI, bool CANON = true>
-BM_D void fwd2x(uint64_t a[E], uint64_t b[E], uint64_t *smA, uint64_t *smB, const PrimeK &P)
-{
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int s = 0; s < 4; s++) {
-        const int half = 8 >> s;
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            if (k & half) continue;
-            const ulonglong2 w = ldtw(P.fwd + (1 << s) + (k >> (4 - s)));
-            ct4s<PI>(a[k], a[k + half], w, s);
-            ct4s<PI>(b[k], b[k + half], w, s);
-        }
-    }
-    xchg2<1, 2>(a, b, smA, smB);
-    {
-        const int B = tid >> 5;
-#pragma unroll
-        for (int s = 4; s < 8; s++) {
-            const int half = 8 >> (s - 4);
-#pragma unroll
-            for (int k = 0; k < E; k++) {
-                if (k & half) continue;
-                const ulonglong2 w = ldtw(P.fwd + (1 << s) + (B << (s - 4)) + (k >> (8 - s)));
-                ct4s<PI>(a[k], a[k + half], w, s);
-                ct4s<PI>(b[k], b[k + half], w, s);
-            }
-        }
-    }
-    xchg2<2, 3>(a, b, smA, smB);
-    const int G = tid >> 1, odd = tid & 1;
-#pragma unroll
-    for (int s = 8; s < 12; s++) {
-        const int half = 8 >> (s - 8);
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            if (k & half) continue;
-            const ulonglong2 w = ldtw(P.fwd + (1 << s) + ((k >> (12 - s)) << 8) + G);
-            ct4s<PI>(a[k], a[k + half], w, s);
-            ct4s<PI>(b[k], b[k + half], w, s);
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < 8; m++) {
-        const ulonglong2 w = ldtw(P.fwd + 4096 + 512 * m + tid);
-        const uint64_t ra = shfl1(odd ? a[2 * m] : a[2 * m + 1]), rb = shfl1(odd ? b[2 * m] : b[2 * m + 1]);
-        uint64_t xa = odd ? ra : a[2 * m], ya = odd ? a[2 * m + 1] : ra;
-        uint64_t xb = odd ? rb : b[2 * m], yb = odd ? b[2 * m + 1] : rb;
-        ct4s<PI>(xa, ya, w, 12);
-        ct4s<PI>(xb, yb, w, 12);
-        if (CANON || Q40<PI>) {
-            a[2 * m] = reduce_bnd<PI>(xa), a[2 * m + 1] = reduce_bnd<PI>(ya);
-            b[2 * m] = reduce_bnd<PI>(xb), b[2 * m + 1] = reduce_bnd<PI>(yb);
-        } else {
-            a[2 * m] = reduce_lazy<Q40<PI> ? 0 : PI>(xa), a[2 * m + 1] = reduce_lazy<Q40<PI> ? 0 : PI>(ya);
-            b[2 * m] = reduce_lazy<Q40<PI> ? 0 : PI>(xb), b[2 * m + 1] = reduce_lazy<Q40<PI> ? 0 : PI>(yb);
-        }
-    }
-}
-
-template <int PI> BM_D void inv2x(uint64_t a[E], uint64_t b[E], uint64_t *smA, uint64_t *smB, const PrimeK &P)
-{
-    const int tid = threadIdx.x;
-    const int G = tid >> 1, odd = tid & 1;
-#pragma unroll
-    for (int m = 0; m < 8; m++) {
-        const ulonglong2 w = ldtw(P.inv + 4096 + 512 * m + tid);
-        gs4s<PI, 0>(a[2 * m], a[2 * m + 1], w);
-        gs4s<PI, 0>(b[2 * m], b[2 * m + 1], w);
-    }
-#pragma unroll
-    for (int m = 0; m < 8; m++) {
-        const uint64_t ra = shfl1(odd ? a[2 * m] : a[2 * m + 1]), rb = shfl1(odd ? b[2 * m] : b[2 * m + 1]);
-        if (odd) a[2 * m] = ra, b[2 * m] = rb;
-        else a[2 * m + 1] = ra, b[2 * m + 1] = rb;
-    }
-#pragma unroll
-    for (int s = 11; s >= 8; s--) {
-        const int half = 8 >> (s - 8);
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            if (k & half) continue;
-            const ulonglong2 w = ldtw(P.inv + (1 << s) + ((k >> (12 - s)) << 8) + G);
-            switch (12 - s) {
-            case 1: gs4s<PI, 1>(a[k], a[k + half], w); gs4s<PI, 1>(b[k], b[k + half], w); break;
-            case 2: gs4s<PI, 2>(a[k], a[k + half], w); gs4s<PI, 2>(b[k], b[k + half], w); break;
-            case 3: gs4s<PI, 3>(a[k], a[k + half], w); gs4s<PI, 3>(b[k], b[k + half], w); break;
-            default: gs4s<PI, 4>(a[k], a[k + half], w); gs4s<PI, 4>(b[k], b[k + half], w); break;
-            }
-        }
-    }
-    xchg2<3, 2>(a, b, smA, smB);
-    {
-        const int B = tid >> 5;
-#pragma unroll
-        for (int s = 7; s >= 4; s--) {
-            const int half = 8 >> (s - 4);
-#pragma unroll
-            for (int k = 0; k < E; k++) {
-                if (k & half) continue;
-                const ulonglong2 w = ldtw(P.inv + (1 << s) + (B << (s - 4)) + (k >> (8 - s)));
-                switch (12 - s) {
-                case 5: gs4s<PI, 5>(a[k], a[k + half], w); gs4s<PI, 5>(b[k], b[k + half], w); break;
-                case 6: gs4s<PI, 6>(a[k], a[k + half], w); gs4s<PI, 6>(b[k], b[k + half], w); break;
-                case 7: gs4s<PI, 7>(a[k], a[k + half], w); gs4s<PI, 7>(b[k], b[k + half], w); break;
-                default: gs4s<PI, 8>(a[k], a[k + half], w); gs4s<PI, 8>(b[k], b[k + half], w); break;
-                }
-            }
-        }
-    }
-    xchg2<2, 1>(a, b, smA, smB);
-#pragma unroll
-    for (int s = 3; s >= 1; s--) {
-        const int half = 8 >> s;
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            if (k & half) continue;
-            const ulonglong2 w = ldtw(P.inv + (1 << s) + (k >> (4 - s)));
-            switch (12 - s) {
-            case 9: gs4s<PI, 9>(a[k], a[k + half], w); gs4s<PI, 9>(b[k], b[k + half], w); break;
-            case 10: gs4s<PI, 10>(a[k], a[k + half], w); gs4s<PI, 10>(b[k], b[k + half], w); break;
-            default: gs4s<PI, 11>(a[k], a[k + half], w); gs4s<PI, 11>(b[k], b[k + half], w); break;
-            }
-        }
-    }
-    constexpr uint64_t Bq = (Q40<PI> ? (4ull << 12) : 4ull) * PrimeC<PI>::q;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        const uint64_t xa = a[k], ya = a[k + 8], xb = b[k], yb = b[k + 8];
-        a[k] = reduce_bnd<PI>(shoup4<PI>(xa + ya, P.ninv));
-        a[k + 8] = reduce_bnd<PI>(shoup4<PI>(xa - ya + Bq, P.ninv_w1));
-        b[k] = reduce_bnd<PI>(shoup4<PI>(xb + yb, P.ninv));
-        b[k + 8] = reduce_bnd<PI>(shoup4<PI>(xb - yb + Bq, P.ninv_w1));
-    }
-}
-
 BM_D void fwd_rt(uint64_t a[E], uint64_t *sm, const PrimeK &P, int pi)
 {
     if (pi == 0) fwd<0>(a, sm, P);

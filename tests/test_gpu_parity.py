@@ -487,20 +487,3 @@ def test_rng_os_mode_fresh_encryption_randomness(env, O):
         m = O.decrypt(13, B.bm_sk_export(sk), c.cpu().numpy().view(np.uint64)[0], 2)[0]
         err = O.centred_i64(m, prm.q[0]) - pt.cpu().numpy()[0]
         assert np.abs(err).max() < 2 ** 20                 # the encryption noise only
-
-
-@pytest.mark.parametrize("order", [0, 1, 2])
-def test_pair_kernels_equal_split_kernels(env, O, order):
-    """Relinearisation as one CTA per pair with paired transforms (option pair_kernels: k_digits_h /
-    k_relin_h, hybrid integer + FP64-pipe transforms) gives the residues of the two-CTA kernels bit for
-    bit (hoisted, paper order with its accumulation, f2's order), and a pair equals the oracle."""
-    torch, B = env
-    T = I.templates(2, 900)
-    Q, _ = I.queries(2, 5)
-    st = Setup(env, O, 128, 8, T, Q, hoisted=(order == 2))
-    ref_gpu = st.gpu_match(order)
-    with B.options(pair_kernels=1):
-        got = st.gpu_match(order)
-    assert np.array_equal(got, ref_gpu)
-    ref = st.oracle_pairs([(4, st.n_sets - 1)], order)
-    assert np.array_equal(got[4, st.n_sets - 1], ref[0])

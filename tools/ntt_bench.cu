@@ -10,6 +10,7 @@
 #include "../paper_2408_06167_b200/csrc/ntt3.cuh"
 #include "../paper_2408_06167_b200/csrc/ntt3f.cuh"
 #include "ntt_legacy.cuh"
+#include "ntt_experiments.cuh"
 using namespace bm;
 typedef unsigned __int128 u128;
 
