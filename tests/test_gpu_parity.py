@@ -487,3 +487,35 @@ def test_rng_os_mode_fresh_encryption_randomness(env, O):
         m = O.decrypt(13, B.bm_sk_export(sk), c.cpu().numpy().view(np.uint64)[0], 2)[0]
         err = O.centred_i64(m, prm.q[0]) - pt.cpu().numpy()[0]
         assert np.abs(err).max() < 2 ** 20                 # the encryption noise only
+
+
+def test_bench_ring_wraparound_equals_bm_match(env, O):
+    """bench.py's bounded outputs: query groups written round-robin into R = 2 ring slots on two
+    alternating streams (each slot reused every R groups) leave in every slot exactly bm_match's
+    results of the last group that used it, bit for bit; sampled pairs equal the oracle."""
+    torch, B = env
+    T = I.templates(2, 3 * 256 + 40)          # p = 8: B = 256 -> 4 sets (the last ragged)
+    Q, _ = I.queries(2, 7)
+    st = Setup(env, O, 128, 8, T, Q)
+    full = st.gpu_match(0)
+    gq, R = 2, 2                              # groups {0,1}, {2,3}, {4,5}, {6}: slot 0 <- groups 0, 2; slot 1 <- 1, 3
+    ring = [torch.full((gq, st.n_sets, 2, 8192), -1, dtype=torch.int64, device="cuda") for _ in range(R)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ws = [torch.empty(B.bm_match_ws_bytes(st.prm, st.n_sets, gq), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    last = {}
+    main = torch.cuda.current_stream()
+    for s in streams:
+        s.wait_stream(main)
+    for g in range(-(-st.nq // gq)):
+        q0, n = g * gq, min(gq, st.nq - g * gq)
+        B.bm_match(st.prm, st.evk_dev, st.d_db, st.n_sets, st.d_q[q0:q0 + n], n, ring[g % R][:n], ws[g % 2], 0,
+                   stream=streams[g % 2])
+        last[g % R] = (q0, n)
+    for s in streams:
+        main.wait_stream(s)
+    torch.cuda.synchronize()
+    for slot, (q0, n) in last.items():
+        got = ring[slot][:n].cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, full[q0:q0 + n]), slot
+    ref = st.oracle_pairs([(6, st.n_sets - 1), (5, 0)])
+    assert np.array_equal(full[6, st.n_sets - 1], ref[0]) and np.array_equal(full[5, 0], ref[1])
