@@ -1010,7 +1010,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 2),
         "unit": "templates*queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True,
+        "scaling": "strong" if world > 1 and args.config in (4, 5) else "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"BASELINE configs[{args.config - 1}]: d={d}, p={p}, bounded sample of {n_pairs} "
                                f"(query, set) pairs per step (the CPU oracle, oracle/)", "d": d, "p": p},

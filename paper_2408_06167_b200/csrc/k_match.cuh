@@ -773,9 +773,14 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
                     if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
                     // sigma(c1) P^-1 gk[c][q0] (P^-1 folded into the device key), [0, 4 q0)
                     const uint64_t ks = shoup4<0>(S1[jp], kk[e & 1]);
-                    uint64_t v = ks + 2 * Q0 - a[e] + S[j]; // < 7 q0
-                    if (c == 0) v += S0[jp];           // < 7 q0
+                    uint64_t v = ks + 2 * Q0 - a[e] + S[j]; // < 8 q0 (S in [0, 2 q0))
+                    if (c == 0) v += S0[jp];           // < 10 q0
+#ifdef BM_LADDER_CANON_S
                     a[e] = reduce_bnd<0>(v);
+#else
+                    a[e] = reduce_lazy<0>(v);          // [0, 2 q0): the resident C stays lazy (its readers:
+                                                       // Shoup operands and inv<0>, which takes < 4 q0)
+#endif
                 }
                 if (CL) cluster_wait(); // (2) wait: c1 may be rewritten now
                 BM_SYNCTHREADS();        // every read of the old c_c is done
@@ -789,9 +794,13 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
                     const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
                     if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
                     const uint64_t ks = shoup4<0>(S1[jp], kk[e & 1]);
-                    uint64_t v = ks + S[j]; // < 5 q0
-                    if (c == 0) v += S0[jp];
+                    uint64_t v = ks + S[j]; // < 6 q0
+                    if (c == 0) v += S0[jp]; // < 8 q0
+#ifdef BM_LADDER_CANON_S
                     a[e] = reduce_bnd<0>(v);
+#else
+                    a[e] = reduce_lazy<0>(v); // [0, 2 q0) < 4 q0: inv<0>'s input bound; its output is canonical
+#endif
                 }
                 inv<0>(a, XB, K.pr[0]);
                 uint64_t *o = K.out_at(pi, c);
