@@ -296,9 +296,17 @@ BM_HD constexpr int npad(int i)
 }
 // word of this thread's element e (M4) / of the element sigma_g moves there
 BM_D int nat_at(int ntid, int e) { return npad(ntid) + npad(nat_e(e)); }
+// npad for a runtime index: the thread / element split of npad is only for immediates, and
+// ((t + (t >> 4)) ^ b) + (e + (e >> 4)) = (i + (i >> 4)) ^ b with b = bit 11 of i, because e + (e >> 4)
+// has bit 0 clear (so the bank-bit toggle commutes with adding it): 5 instructions per gather
+BM_D int npad_rt(uint32_t i) { return (int)((i + (i >> 4)) ^ ((i >> 11) & 1u)); }
 BM_D int nat_auto_i(uint32_t i, uint32_t g)
 {
+#ifdef BM_NPAD_SPLIT
     const int w = npad((int)((i * g + ((g - 1) >> 1)) & (N - 1)));
+#else
+    const int w = npad_rt((i * g + ((g - 1) >> 1)) & (N - 1));
+#endif
     BM_CHECK(w >= 0 && w < SMEM_WORDS && (g & 1));
     return w;
 }
