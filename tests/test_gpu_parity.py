@@ -519,3 +519,28 @@ def test_bench_ring_wraparound_equals_bm_match(env, O):
         assert np.array_equal(got, full[q0:q0 + n]), slot
     ref = st.oracle_pairs([(6, st.n_sets - 1), (5, 0)])
     assert np.array_equal(full[6, st.n_sets - 1], ref[0]) and np.array_equal(full[5, 0], ref[1])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_random_layouts_fuzz(env, O, seed):
+    """Seeded random layouts (d a power of two in [4, 2048], p | d), template counts (ragged last
+    sets) and batch sizes, both op orders: two random pairs per case equal the oracle bit for bit and
+    the decrypted scores match the float64 cosines."""
+    torch, B = env
+    rng = np.random.default_rng(1000 + seed)
+    d = int(2 ** rng.integers(2, 12))
+    p = int(2 ** rng.integers(0, int(np.log2(d)) + 1))
+    Bk = 4096 * p // d
+    n_tmpl = int(rng.integers(1, 3 * Bk + 1))
+    nq = int(rng.integers(1, 6))
+    order = int(rng.integers(0, 2))
+    T = I.random_unit(n_tmpl, d, 70 + seed)
+    Q = I.random_unit(nq, d, 80 + seed)
+    st = Setup(env, O, d, p, T, Q)
+    got = st.gpu_match(order)
+    pairs = sorted({(int(rng.integers(nq)), int(rng.integers(st.n_sets))) for _ in range(2)})
+    ref = st.oracle_pairs(pairs, order)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k]), (d, p, n_tmpl, nq, order, j, t)
+    sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(nq, -1)[:, :n_tmpl]
+    assert np.abs(sc - Q @ T.T).max() < 1e-6, (d, p)
