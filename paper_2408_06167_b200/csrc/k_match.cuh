@@ -472,6 +472,18 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
 //   C_c = q1^-1 (d_c[q0] + P^-1 KS_c[q0] - A)   (level 0; accumulate: dst += C_c, paper order)
 // (the digit of limb j in its own limb is d2[q_j] itself: no transform needed there)
 constexpr size_t K3_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+// L2 prefetch of a polynomial's 128-byte lines that this thread's later ld2 (pos_M4) reads: one lane in
+// eight issues each line (16-byte vectors, eight lanes per line); the data move DRAM -> L2 while the
+// CTA computes the current phase's transform
+BM_D void prefetch_poly_l2(const uint64_t *p)
+{
+#ifdef BM_K3_PREFETCH
+    if ((threadIdx.x & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < E; e += 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + pos_M4(threadIdx.x, e)));
+    }
+#endif
+}
 __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumulate)
 {
     extern __shared__ uint64_t sm[];
@@ -496,6 +508,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         a[e] = red128s<2>(dot2(u.x, w0.x, v.x, w1.x), K.pr[2].r64);
         a[e + 1] = red128s<2>(dot2(u.y, w0.y, v.y, w1.y), K.pr[2].r64);
     }
+    prefetch_poly_l2(xu + 0 * N); // the q1 phase's DRAM operands, during INTT_P
+    prefetch_poly_l2(d2 + 1 * N);
+    prefetch_poly_l2(dc + 1 * N);
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
     for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // Y, canonical [0, P), coefficient j_M1(tid, e)
@@ -511,6 +526,9 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         a[e] = reduce_bnd<1>(dd.x + ka);
         a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
+    prefetch_poly_l2(d2 + 0 * N); // the q0 phase's DRAM operands, during INTT_q1 and NTT_q0
+    prefetch_poly_l2(xu + 2 * N);
+    prefetch_poly_l2(dc);
     inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
     // ---- rescale in coefficient form
     const ulonglong2 pinv0 = K.pinv[0];
