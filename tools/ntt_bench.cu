@@ -95,6 +95,23 @@ __global__ void __launch_bounds__(512, 1) k_bench3h(PrimeK P, PrimeK P1, uint64_
     v3::store_coef(d + N, b);
 }
 
+// v7: 1,024 threads x 8 coefficients (tools/ntt_experiments.cuh x10), natural-order twiddle tables
+template <int PI>
+__global__ void __launch_bounds__(1024, 1) k_bench10(PrimeK P, uint64_t *data, int iters)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t a[8];
+    uint64_t *d = data + (size_t)blockIdx.x * N;
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = d[threadIdx.x + 1024 * k];
+    for (int it = 0; it < iters; it++) {
+        v3::x10::fwd10<PI>(a, sm, P.fwd);
+        v3::x10::inv10<PI>(a, sm, P.inv, P.ninv, P.ninv_w1);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) d[threadIdx.x + 1024 * k] = a[k];
+}
+
 static ulonglong2 sp(uint64_t w, uint64_t q) { return make_ulonglong2(w, shoup_companion(w, q)); }
 
 int main(int argc, char **argv)
@@ -226,6 +243,45 @@ int main(int argc, char **argv)
                ok ? "ok" : "MISMATCH", ms, bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000,
                cudaGetErrorString(cudaGetLastError()));
         cudaFree(dd);
+    }
+    // v7: 1,024-thread core, natural-order twiddles
+    typedef void (*KT)(PrimeK, uint64_t *, int);
+    KT k10[3] = {k_bench10<0>, k_bench10<1>, k_bench10<2>};
+    for (int pi = 0; pi < 3; pi++) {
+        cudaFuncSetAttribute(k10[pi], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM_WORDS * 8));
+        const HostPrime &H = host_prime(pi);
+        std::vector<ulonglong2> tw(2 * N);
+        for (int k = 0; k < N; k++) tw[k] = sp(H.fwd[k], H.q), tw[N + k] = sp(H.inv[k], H.q);
+        ulonglong2 *dtw;
+        cudaMalloc(&dtw, tw.size() * 16);
+        cudaMemcpy(dtw, tw.data(), tw.size() * 16, cudaMemcpyHostToDevice);
+        PrimeK P;
+        P.q = H.q; P.q2 = 2 * H.q; P.fwd = dtw; P.inv = dtw + N;
+        P.ninv = sp(H.ninv, H.q);
+        P.ninv_w1 = sp(mulmod_h(H.ninv, H.inv[1], H.q), H.q);
+        std::vector<uint64_t> h((size_t)blocks * N);
+        srand(pi + 11);
+        for (auto &x : h) x = (((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ rand()) % H.q;
+        uint64_t *dd;
+        cudaMalloc(&dd, h.size() * 8);
+        cudaMemcpy(dd, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        k10[pi]<<<blocks, 1024, SMEM_WORDS * 8>>>(P, dd, 1);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        k10[pi]<<<blocks, 1024, SMEM_WORDS * 8>>>(P, dd, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        std::vector<uint64_t> back(h.size());
+        cudaMemcpy(back.data(), dd, h.size() * 8, cudaMemcpyDeviceToHost);
+        const bool ok = back == h;
+        const double bfly = (double)blocks * iters * 2 * (N / 2) * LOGN;
+        int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+        printf("v7 1024x8 prime %d: %s  %.3f ms  %.1f Gbfly/s  %.2f bfly/clk/SM (at %d MHz)  err=%s\n", pi,
+               ok ? "ok" : "MISMATCH", ms, bfly / ms / 1e6, bfly / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000,
+               cudaGetErrorString(cudaGetLastError()));
+        cudaFree(dd); cudaFree(dtw);
     }
     return 0;
 }

@@ -324,5 +324,150 @@ BM_D void inv_h(uint64_t a[E], uint64_t b[E], uint64_t *smA, uint64_t *smB, cons
     }
 }
 
+
+// ================================================================== v7: 1,024 threads x 8 coefficients (experiment)
+// More warps per SM (32 instead of 16) at 8 coefficients per thread (fits 64 registers), for latency
+// hiding; 3 register passes of 3 stages + one lane-pair shuffle stage, 3 exchanges per transform (two
+// CTA-wide, one warp-local) against v3's 2.  Twiddles from NATURAL-order tables (index k at k).
+// Layouts (w = warp, l = lane, k < 8):
+//   J1: j = tid + 1024 k                                   (k <-> bits 10..12)
+//   J2: j = (w & 3) | l << 2 | k << 7 | (w >> 2) << 10     (k <-> bits 7..9; warp region: bits 2..9)
+//   J3: j = (w & 3) | (l & 3) << 2 | k << 4 | (l >> 2) << 7 | (w >> 2) << 10   (k <-> bits 4..6; same region)
+//   J4: j = (l & 1) | k << 1 | (l >> 1) << 4 | w << 8      (k <-> bits 1..3)
+//   J5 (after stage 12): a[2m + b] <-> j = b | (2m + (l & 1)) << 1 | (l >> 1) << 4 | w << 8
+namespace x10 {
+constexpr int T10 = 1024, E8 = 8;
+BM_D int J1(int t, int k) { return t + 1024 * k; }
+BM_D int J2(int t, int k) { const int w = t >> 5, l = t & 31; return (w & 3) | (l << 2) | (k << 7) | ((w >> 2) << 10); }
+BM_D int J3(int t, int k)
+{
+    const int w = t >> 5, l = t & 31;
+    return (w & 3) | ((l & 3) << 2) | (k << 4) | ((l >> 2) << 7) | ((w >> 2) << 10);
+}
+BM_D int J4(int t, int k) { const int w = t >> 5, l = t & 31; return (l & 1) | (k << 1) | ((l >> 1) << 4) | (w << 8); }
+BM_D int J5(int t, int e)
+{
+    const int w = t >> 5, l = t & 31;
+    return (e & 1) | ((2 * (e >> 1) + (l & 1)) << 1) | ((l >> 1) << 4) | (w << 8);
+}
+template <int L> BM_D int J(int t, int k) { return L == 1 ? J1(t, k) : L == 2 ? J2(t, k) : L == 3 ? J3(t, k) : J4(t, k); }
+
+template <int FROM, int TO, bool WARP> BM_D void xch(uint64_t a[E8], uint64_t *sm)
+{
+    const int t = threadIdx.x;
+    if (WARP) __syncwarp();
+    else __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E8; k++) sm[pidx(J<FROM>(t, k))] = a[k];
+    if (WARP) __syncwarp();
+    else __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E8; k++) a[k] = sm[pidx(J<TO>(t, k))];
+}
+
+// one register pass of 3 forward stages s0, s0+1, s0+2 in layout L (stage s pairs bit 12 - s <-> k bit 2 - (s - s0))
+template <int PI, int L, int S0> BM_D void fpass(uint64_t a[E8], const ulonglong2 *tw)
+{
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int s = S0; s < S0 + 3; s++) {
+        const int half = 4 >> (s - S0);
+#pragma unroll
+        for (int k = 0; k < E8; k++) {
+            if (k & half) continue;
+            const int jl = J<L>(t, k);
+            ct4s<PI>(a[k], a[k + half], __ldg(tw + (1 << s) + (jl >> (13 - s))), s);
+        }
+    }
+}
+template <int PI, int L, int S0, int ST0> BM_D void ipass(uint64_t a[E8], const ulonglong2 *tw)
+{
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int s = S0 + 2; s >= S0; s--) {
+        const int half = 4 >> (s - S0);
+#pragma unroll
+        for (int k = 0; k < E8; k++) {
+            if (k & half) continue;
+            const int jl = J<L>(t, k);
+            const ulonglong2 w = __ldg(tw + (1 << s) + (jl >> (13 - s)));
+            constexpr int dummy = 0;
+            (void)dummy;
+            switch (12 - s) {
+            case 1: gs4s<PI, 1>(a[k], a[k + half], w); break;
+            case 2: gs4s<PI, 2>(a[k], a[k + half], w); break;
+            case 3: gs4s<PI, 3>(a[k], a[k + half], w); break;
+            case 4: gs4s<PI, 4>(a[k], a[k + half], w); break;
+            case 5: gs4s<PI, 5>(a[k], a[k + half], w); break;
+            case 6: gs4s<PI, 6>(a[k], a[k + half], w); break;
+            case 7: gs4s<PI, 7>(a[k], a[k + half], w); break;
+            case 8: gs4s<PI, 8>(a[k], a[k + half], w); break;
+            case 9: gs4s<PI, 9>(a[k], a[k + half], w); break;
+            case 10: gs4s<PI, 10>(a[k], a[k + half], w); break;
+            default: gs4s<PI, 11>(a[k], a[k + half], w); break;
+            }
+        }
+    }
+}
+
+template <int PI> BM_D void fwd10(uint64_t a[E8], uint64_t *sm, const ulonglong2 *tw)
+{
+    const int t = threadIdx.x, odd = t & 1;
+    fpass<PI, 1, 0>(a, tw);
+    xch<1, 2, false>(a, sm);
+    fpass<PI, 2, 3>(a, tw);
+    xch<2, 3, true>(a, sm);
+    fpass<PI, 3, 6>(a, tw);
+    xch<3, 4, false>(a, sm);
+    fpass<PI, 4, 9>(a, tw);
+#pragma unroll
+    for (int m = 0; m < 4; m++) { // stage 12 on lane pairs: even lane k = 2m, odd lane k = 2m + 1
+        const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? a[2 * m] : a[2 * m + 1], 1);
+        uint64_t x = odd ? r : a[2 * m], y = odd ? a[2 * m + 1] : r;
+        const int jl = J4(t, 2 * m + odd) & ~1;
+        ct4s<PI>(x, y, __ldg(tw + 4096 + (jl >> 1)), 12);
+        a[2 * m] = reduce_bnd<PI>(x);
+        a[2 * m + 1] = reduce_bnd<PI>(y);
+    }
+}
+
+template <int PI> BM_D void inv10(uint64_t a[E8], uint64_t *sm, const ulonglong2 *tw, ulonglong2 ninv, ulonglong2 ninv_w1)
+{
+    const int t = threadIdx.x, odd = t & 1;
+#pragma unroll
+    for (int m = 0; m < 4; m++) gs4s<PI, 0>(a[2 * m], a[2 * m + 1], __ldg(tw + 4096 + (J5(t, 2 * m) >> 1)));
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+        const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? a[2 * m] : a[2 * m + 1], 1);
+        if (odd) a[2 * m] = r;
+        else a[2 * m + 1] = r;
+    }
+    ipass<PI, 4, 9, 1>(a, tw);
+    xch<4, 3, false>(a, sm);
+    ipass<PI, 3, 6, 4>(a, tw);
+    xch<3, 2, true>(a, sm);
+    ipass<PI, 2, 3, 7>(a, tw);
+    xch<2, 1, false>(a, sm);
+    // stages 2, 1 in J1 (k bits 1, 0), then stage 0 (k bit 2) with N^-1 folded in
+#pragma unroll
+    for (int s = 2; s >= 1; s--) {
+        const int half = 4 >> s;
+#pragma unroll
+        for (int k = 0; k < E8; k++) {
+            if (k & half) continue;
+            const ulonglong2 w = __ldg(tw + (1 << s) + (J1(t, k) >> (13 - s)));
+            if (s == 2) gs4s<PI, 10>(a[k], a[k + half], w);
+            else gs4s<PI, 11>(a[k], a[k + half], w);
+        }
+    }
+    constexpr uint64_t Bq = (Q40<PI> ? (4ull << 12) : 4ull) * PrimeC<PI>::q;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint64_t x = a[k], y = a[k + 4];
+        a[k] = reduce_bnd<PI>(shoup4<PI>(x + y, ninv));
+        a[k + 4] = reduce_bnd<PI>(shoup4<PI>(x - y + Bq, ninv_w1));
+    }
+}
+} // namespace x10
 } // namespace v3
 } // namespace bm
