@@ -66,6 +66,7 @@ def to_dev(torch, B, prm, ct, n_limbs):
     (128, 8, 0, "qm1"), (128, 8, 0, "alt"), (128, 8, 0, "ntt"),
     (128, 8, 1, "qm1"), (128, 8, 1, "ntt"),
     (128, 8, 2, "qm1"), (128, 8, 2, "ntt"),          # k_hrot: 15 rotations accumulated in 128 bits
+    (128, 1, 2, "qm1"), (128, 1, 2, "alt"),          # k_hrot: 127 rotations, its 64-rotation folds
     (4096, 1, 0, "qm1"), (4096, 1, 0, "alt"),        # s = 4096: the 12-step ladder
     (1024, 1024, 0, "ntt"), (1024, 1024, 0, "qm1"),  # p = 1024: the tensor's 512-part folds
 ])
