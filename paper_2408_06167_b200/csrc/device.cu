@@ -31,6 +31,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h> // header-only NVTX v3: named ranges for Nsight timelines (no-ops without a tool)
+
 #include "bm_common.cuh"
 #include "bm_host.h"
 #include "ntt3.cuh"
@@ -245,6 +247,12 @@ int launch_check()
     }
     return BM_OK;
 }
+
+// NVTX range for the life of a scope (Nsight Systems timelines; a no-op without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *m) { nvtxRangePushA(m); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ options (bm_set_option)
 // Process-wide tuning / test switches of the library (explicit, no environment lookups on the hot
@@ -1117,6 +1125,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     };
 
     const int log_s = prm->log_s;
+    NvtxRange nvtx_call(d_rows ? "bm_match_rows" : "bm_match");
     // chunks are rectangles of cq queries x ct sets (cq * ct <= ch pairs)
     const int64_t ct_full = n_sets < ch ? n_sets : ch;
     const int64_t cq_full = ch / ct_full < nq ? ch / ct_full : nq;
@@ -1128,6 +1137,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         K.ct = n_sets - t0 < ct_full ? n_sets - t0 : ct_full;
         const int64_t np = K.cq * K.ct;
         const unsigned npu = (unsigned)np;
+        NvtxRange nvtx_chunk("bm_match chunk (tensor, digits, relin, ladder)");
         // few queries: k_tensor<2, true> puts the sets on the tile's wide (TQB) side and the queries
         // on the TSB side -- less of the tile wasted, identical residues (the products are symmetric)
         const bool tswap = K.cq < TQB && K.ct >= TQB;
@@ -1343,6 +1353,7 @@ static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const ui
     int rc = ctx_get(&Cx);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(Cx->host_mu); // the internal streams are shared by the calls on this device
+    NvtxRange nvtx_call("bm_match_host");
     if (!Cx->hs[0])
         for (int k = 0; k < 3; k++)
             if (cudaStreamCreateWithFlags(&Cx->hs[k], cudaStreamNonBlocking) != cudaSuccess) {
