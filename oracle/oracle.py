@@ -21,7 +21,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liboracle.so")
+LIB_PATH = os.path.join(HERE, "liboracle_san.so" if os.environ.get("ORACLE_SANITIZE") else "liboracle.so")
 
 DELTA = 2.0 ** 40          # encoding scale (BASELINE.json configs[0]: "scale 2^40")
 ORDER_HOISTED = 0
@@ -34,10 +34,13 @@ _u32p = ctypes.POINTER(ctypes.c_uint32)
 
 
 def build(force=False):
-    """Compile liboracle.so (plain C, no optimisation flags beyond -O2)."""
+    """Compile liboracle.so (plain C, no optimisation flags beyond -O2).  ORACLE_SANITIZE=1 builds an
+    ASan + UBSan instrumented copy instead (tools/oracle_sanitize.sh)."""
     src = os.path.join(HERE, "ckks_oracle.c")
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-Wall", "-fPIC", "-shared", "-o", LIB_PATH, src, "-lpthread"])
+        san = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-g"] if os.environ.get(
+            "ORACLE_SANITIZE") else []
+        subprocess.check_call(["gcc", "-O2", "-Wall", "-fPIC", "-shared", *san, "-o", LIB_PATH, src, "-lpthread"])
     return LIB_PATH
 
 
