@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--ring-gib", type=float, default=4.0, help="device result ring (bounded outputs)")
     ap.add_argument("--chunk", type=int, default=16384, help="pairs per query group / bm_match chunk")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--group-queries", type=int, default=None,
+                    help="queries per bm_match call (default: ~--chunk pairs, at least 8 when the batch has them)")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1 result gather (a8): p2p = fused into the output kernels (bm_match_rows storing "
                          "to the roots over NVLink), nccl = all_to_all after each group's scan")
@@ -213,7 +215,7 @@ class ClockSampler:
 class Workload:
     """The (config, p) workload and this rank's share of it."""
 
-    def __init__(self, cfg, p, nq, world, rank, shard_of, chunk):
+    def __init__(self, cfg, p, nq, world, rank, shard_of, chunk, group_queries=None):
         from paper_2408_06167_b200 import dist as pdist
         from paper_2408_06167_b200 import inputs as I
         c = I.CONFIGS[cfg]
@@ -228,8 +230,9 @@ class Workload:
         self.lo, self.n_local = pdist.shard_sets(self.n_sets, self.split, rank)
         self.tmpl_lo = self.lo * self.B
         self.n_tmpl_local = max(0, min(self.n, (self.lo + self.n_local) * self.B) - self.tmpl_lo)
-        # query groups: ~chunk pairs each; for N > 1 a group splits evenly over the ranks (roots)
-        want = max(1, chunk // max(1, self.n_local))
+        # query groups: ~chunk pairs each, at least 8 queries when the batch has them (bm_match then cuts
+        # 8-query chunks: the tensor's full tiles); for N > 1 a group splits evenly over the ranks (roots)
+        want = group_queries or max(1, chunk // max(1, self.n_local), min(8, self.nq))
         if world > 1:
             cands = [g for g in range(world, self.nq + 1, world) if self.nq % g == 0]
             assert cands, "nq must be a multiple of the world size"
@@ -304,7 +307,7 @@ def run_ours(args):
     shard_of = args.shard_of if args.shard_of else (8 if args.config == 5 and world < 8 else None)
     if shard_of is not None and world > 1 and shard_of != world:
         raise SystemExit("--shard-of applies to single-GPU prefix runs only")
-    W = Workload(args.config, args.p, args.nq, world, rank, shard_of, args.chunk)
+    W = Workload(args.config, args.p, args.nq, world, rank, shard_of, args.chunk, args.group_queries)
     p, nq, order, d = W.p, W.nq, args.order, W.d
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     prm = B.bm_params_init(d, p)
@@ -329,7 +332,7 @@ def run_ours(args):
     B.bm_sync()
     t_setup = time.perf_counter() - t_setup
     # bounded outputs: a ring of R group slots (R even: group g and g + R share a stream)
-    B.bm_set_option("chunk_pairs", max(1, min(args.chunk, W.gq * n_local)))
+    B.bm_set_option("chunk_pairs", max(1, min(args.chunk, W.gq * n_local)))   # pairs per bm_match chunk
     nstr = args.streams
     row_bytes = n_local * 2 * N_RING * 8
     slot_bytes = W.gq * row_bytes

@@ -1126,9 +1126,10 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
 
     const int log_s = prm->log_s;
     NvtxRange nvtx_call(d_rows ? "bm_match_rows" : "bm_match");
-    // chunks are rectangles of cq queries x ct sets (cq * ct <= ch pairs)
-    const int64_t ct_full = n_sets < ch ? n_sets : ch;
-    const int64_t cq_full = ch / ct_full < nq ? ch / ct_full : nq;
+    // chunks are rectangles of cq queries x ct sets (cq * ct <= ch pairs); at least TQB queries per chunk
+    // when the call has them (the tensor's full, double-buffered tiles instead of the swapped ones)
+    const int64_t cq_full = std::min<int64_t>(nq, std::max<int64_t>(ch / n_sets, std::min<int64_t>(TQB, ch)));
+    const int64_t ct_full = std::min<int64_t>(n_sets, std::max<int64_t>(1, ch / cq_full));
     for (int64_t jq0 = 0; jq0 < nq && !rc; jq0 += cq_full)
     for (int64_t t0 = 0; t0 < n_sets && !rc; t0 += ct_full) {
         K.jq0 = jq0;
