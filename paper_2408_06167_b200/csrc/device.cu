@@ -65,6 +65,7 @@ struct DevCtx {
     // bm_match_host's extra streams (created once per device, reused by every call under host_mu)
     std::mutex host_mu;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr}; // second compute stream, upload, download
+    std::vector<cudaEvent_t> hev;                      // bm_match_host's events, grown on demand, reused
 };
 
 std::mutex g_mu;
@@ -1388,16 +1389,26 @@ static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const ui
         if (tail) g0.push_back(q), gn.push_back(tail);
     }
     const int ngroups = (int)g0.size();
-    // events: ev[g][0] upload done, [1] scan done, [2] download done (reusable after the call syncs)
-    std::vector<cudaEvent_t> ev(3 * (size_t)ngroups + 1);
-    for (auto &e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    cudaEvent_t ev_start = ev.back();
+    // events: ev[g][0] upload done, [1] scan done, [2] download done, then the start event and the three
+    // completion events; owned by the device context (created once, reused: the call synchronises before
+    // returning, so every event is idle again)
+    const size_t n_ev = 3 * (size_t)ngroups + 4;
+    while (Cx->hev.size() < n_ev) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return BM_ERR_CUDA;
+        }
+        Cx->hev.push_back(e);
+    }
+    cudaEvent_t *ev = Cx->hev.data();
+    cudaEvent_t ev_start = ev[3 * (size_t)ngroups];
     cudaEventRecord(ev_start, sc[0]); // everything starts after the work already on the caller's stream
     cudaStreamWaitEvent(sc[1], ev_start, 0);
     cudaStreamWaitEvent(su, ev_start, 0);
     cudaStreamWaitEvent(sd, ev_start, 0);
     for (int g = 0; g < ngroups && !rc; g++) {
-        cudaEvent_t *E = &ev[3 * (size_t)g];
+        cudaEvent_t *E = ev + 3 * (size_t)g;
         const int slot = g % HOST_SLOTS;
         cudaStream_t cs = sc[g & 1];
         const int64_t q0 = g0[g], nqg = gn[g];
@@ -1424,15 +1435,12 @@ static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const ui
         cudaEventRecord(E[2], sd);
     }
     // the caller's stream waits for the internal streams (stream-ordered completion), then the call blocks
-    cudaEvent_t fin[3];
+    cudaEvent_t *fin = ev + 3 * (size_t)ngroups + 1;
     for (int k = 0; k < 3; k++) {
-        cudaEventCreateWithFlags(&fin[k], cudaEventDisableTiming);
         cudaEventRecord(fin[k], k == 0 ? sc[1] : k == 1 ? su : sd);
         cudaStreamWaitEvent(sc[0], fin[k], 0);
     }
     if (cudaStreamSynchronize(sc[0]) != cudaSuccess) rc = rc ? rc : BM_ERR_CUDA;
-    for (auto &e : ev) cudaEventDestroy(e);
-    for (auto &e : fin) cudaEventDestroy(e);
     return rc;
 }
 
