@@ -255,8 +255,7 @@ typedef enum {
     BM_OPT_LADDER_C3 = 4,    /* 0/1: latency-mode ladder on 3-CTA clusters (1)                      */
     BM_OPT_LADDER_TAIL = 5,  /* 0/1: a large launch's partial last wave on the cluster ladders (1)  */
     BM_OPT_CMP_CHUNK = 6,    /* pairs per bm_match_cmp chunk (4096)                                 */
-    BM_OPT_GRID_LIMIT = 7,   /* K2 / K3 / ladder as persistent grids of <= this many CTAs (0: off)   */
-    BM_OPT_COUNT_ = 8
+    BM_OPT_COUNT_ = 7
 } bm_option;
 int bm_set_option(int32_t key, int64_t value);
 int64_t bm_get_option(int32_t key);

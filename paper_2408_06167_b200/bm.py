@@ -436,7 +436,7 @@ def bm_match_host_ring(prm, evk_dev, d_db, n_sets, h_q, nq, h_ring, ring_rows, d
 
 # --------------------------------------------------------------------------- options / counters
 OPTIONS = {"chunk_pairs": 0, "expand_chunk": 1, "host_groups": 2, "ladder_c2": 3, "ladder_c3": 4,
-           "ladder_tail": 5, "cmp_chunk": 6, "grid_limit": 7}
+           "ladder_tail": 5, "cmp_chunk": 6}
 
 
 def bm_set_option(name, value):

@@ -173,11 +173,8 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_tensor<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_tensor<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_tensor<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
-    cudaFuncSetAttribute(k_digits<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
-    cudaFuncSetAttribute(k_relin<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
-    cudaFuncSetAttribute(k_digits<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
-    cudaFuncSetAttribute(k_relin<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
-    cudaFuncSetAttribute(k_ladder_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
+    cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
@@ -272,7 +269,6 @@ struct OptInit {
         g_opt[BM_OPT_LADDER_C3] = 1;       // latency-mode ladder on 3-CTA clusters
         g_opt[BM_OPT_LADDER_TAIL] = 1;     // a large launch's partial last wave on the cluster ladders
         g_opt[BM_OPT_CMP_CHUNK] = 4096;    // pairs per bm_match_cmp chunk
-        g_opt[BM_OPT_GRID_LIMIT] = 0;      // persistent grids of at most this many CTAs (0: one CTA per unit)
     }
 } g_opt_init;
 int64_t opt(int k) { return g_opt[k].load(std::memory_order_relaxed); }
@@ -1158,20 +1154,12 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             counted();
             end();
-            // BM_OPT_GRID_LIMIT > 0: persistent grids of at most that many CTAs striding over the work
-            // (co-scheduling experiments: two streams' kernels then share the SMs)
-            const int64_t glim = opt(BM_OPT_GRID_LIMIT);
-            MatchK Kg = K;
-            Kg.n_units = glim > 0 ? 2 * np : 0;
-            const unsigned g2 = (unsigned)(glim > 0 ? std::min<int64_t>(2 * np, glim) : 2 * np);
             beg(1, 6 * np);
-            if (glim > 0) k_digits<true><<<g2, T, K2_SMEM_BYTES, s>>>(Kg);
-            else k_digits<false><<<g2, T, K2_SMEM_BYTES, s>>>(Kg);
+            k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
             counted();
             end();
             beg(2, 6 * np);
-            if (glim > 0) k_relin<true><<<g2, T, K3_SMEM_BYTES, s>>>(Kg, bufC, r > 0 ? 1 : 0);
-            else k_relin<false><<<g2, T, K3_SMEM_BYTES, s>>>(Kg, bufC, r > 0 ? 1 : 0);
+            k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             counted();
             end();
             rc = launch_check();
@@ -1192,14 +1180,10 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             // (DevCtx::max_cl, from cudaOccupancyMaxActiveClusters); a failed cluster launch falls
             // back to the one-CTA ladder for the same pairs (identical residues)
             const bool c2ok = opt(BM_OPT_LADDER_C2) != 0, c3ok = opt(BM_OPT_LADDER_C3) != 0;
-            const int64_t glim_l = opt(BM_OPT_GRID_LIMIT);
             auto one_cta = [&](int64_t p0, int64_t n) {
                 MatchK Kt = K;
                 Kt.pair0 = p0;
-                Kt.n_units = glim_l > 0 ? n : 0;
-                const unsigned grid = (unsigned)(glim_l > 0 ? std::min<int64_t>(n, glim_l) : n);
-                if (glim_l > 0) k_ladder_t<false, true><<<grid, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
-                else k_ladder_t<false><<<grid, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
+                k_ladder_t<false><<<(unsigned)n, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
                 counted();
             };
             auto cluster_ladder = [&](int64_t p0, int64_t n) {
@@ -1228,7 +1212,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
                 }
             };
             const int64_t tail = np % C->n_sm;
-            const bool fits = c2ok && C->max_cl[2] > 0 && glim_l == 0;
+            const bool fits = c2ok && C->max_cl[2] > 0;
             if (fits && np <= C->max_cl[2] && 2 * np <= C->n_sm) {
                 cluster_ladder(0, np);
             } else if (fits && opt(BM_OPT_LADDER_TAIL) && np > C->n_sm && tail > 0 && 2 * tail <= C->n_sm &&
@@ -1478,9 +1462,7 @@ int bm_set_option(int32_t key, int64_t value)
 {
     if (key < 0 || key >= BM_OPT_COUNT_) return BM_ERR_INVALID_ARG;
     const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL;
-    if (flag ? (value != 0 && value != 1)
-             : (key == BM_OPT_HOST_GROUPS || key == BM_OPT_GRID_LIMIT) ? value < 0 : value < 1)
-        return BM_ERR_INVALID_ARG;
+    if (flag ? (value != 0 && value != 1) : key == BM_OPT_HOST_GROUPS ? value < 0 : value < 1) return BM_ERR_INVALID_ARG;
     g_opt[key].store(value);
     return BM_OK;
 }

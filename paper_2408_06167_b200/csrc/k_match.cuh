@@ -30,7 +30,6 @@ struct MatchK {
     uint64_t *const *rows = nullptr;
     int64_t set_off = 0;
     int64_t pair0 = 0; // the ladder kernels' first pair (a launch may cover only the chunk's tail)
-    int64_t n_units = 0; // CTA work units of a grid-stride launch (0: one unit per CTA, blockIdx.x)
     int64_t nq_total = 0; // queries of the whole call (debug bounds checks)
     BM_D uint64_t *out_at(int64_t pi, int c) const
     {
@@ -431,12 +430,13 @@ template <int PI> BM_D uint64_t red8to4(uint64_t x)
 //   l = 0: x0 mod q1 -> NTT_q1 -> XU[0],  x0 -> NTT_P -> XU[1]
 //   l = 1: x1 (< q1 < q0) -> NTT_q0 -> XU[2],  x1 -> NTT_P -> XU[3]
 constexpr size_t K2_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
-BM_D void k_digits_unit(const MatchK &K, uint64_t *sm, int64_t u)
+__global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
 {
+    extern __shared__ uint64_t sm[];
     uint64_t *xs = sm + SMEM_WORDS;
     const int tid = threadIdx.x;
-    const int64_t pi = u >> 1;
-    const int l = (int)(u & 1);
+    const int64_t pi = blockIdx.x >> 1;
+    const int l = blockIdx.x & 1;
     uint64_t a[E];
     load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
     uint64_t *xu = K.XU + ((size_t)pi * 4 + 2 * l) * N;
@@ -459,20 +459,6 @@ BM_D void k_digits_unit(const MatchK &K, uint64_t *sm, int64_t u)
     for (int e = 0; e < E; e++) a[e] = xs[tid + T * e];
     fwd<2, false>(a, sm, K.pr[2]);
     store_eval(xu + N, a);
-}
-// GS (BM_OPT_GRID_LIMIT): a persistent grid striding over the K.n_units (pair, digit) units
-template <bool GS> __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
-{
-    extern __shared__ uint64_t sm[];
-    if (!GS) {
-        k_digits_unit(K, sm, blockIdx.x);
-        return;
-    }
-#pragma unroll 1
-    for (int64_t u = blockIdx.x; u < K.n_units; u += gridDim.x) {
-        k_digits_unit(K, sm, u);
-        BM_SYNCTHREADS(); // the exchange buffer is rewritten by the next unit
-    }
 }
 
 // ================================================================== K3: key switch + ModDown + rescale
@@ -498,12 +484,13 @@ BM_D void prefetch_poly_l2(const uint64_t *p)
     }
 #endif
 }
-BM_D void k_relin_unit(const MatchK &K, const CtBuf &dst, int accumulate, uint64_t *sm, int64_t u)
+__global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumulate)
 {
+    extern __shared__ uint64_t sm[];
     uint64_t *ys = sm + SMEM_WORDS;
     const int tid = threadIdx.x;
-    const int64_t pi = u >> 1;
-    const int c = (int)(u & 1);
+    const int64_t pi = blockIdx.x >> 1;
+    const int c = blockIdx.x & 1;
     // rlk layout [j][c][l] planar polys of 2N u64.  K3 reads only the w planes (8-byte keys): each limb's
     // inner product x0 k0 + x1 k1 is formed exactly in 128 bits and reduced once (red128s), half the
     // key bytes of two Shoup products (K3 is load-bound: 5.94 -> 5.63 ms)
@@ -574,19 +561,6 @@ BM_D void k_relin_unit(const MatchK &K, const CtBuf &dst, int accumulate, uint64
             ob = csub(ob + cc.y, Q0);
         }
         st2(co + j, oa, ob);
-    }
-}
-template <bool GS> __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumulate)
-{
-    extern __shared__ uint64_t sm[];
-    if (!GS) {
-        k_relin_unit(K, dst, accumulate, sm, blockIdx.x);
-        return;
-    }
-#pragma unroll 1
-    for (int64_t u = blockIdx.x; u < K.n_units; u += gridDim.x) {
-        k_relin_unit(K, dst, accumulate, sm, u);
-        BM_SYNCTHREADS(); // the exchange buffer and Y are rewritten by the next unit
     }
 }
 
@@ -729,7 +703,7 @@ BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
     return reinterpret_cast<const uint64_t *>(g);
 }
 
-template <bool CL, bool GS = false> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, CtBuf cin, int L)
+template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, CtBuf cin, int L)
 {
     extern __shared__ uint64_t sm[];
     uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
@@ -737,15 +711,11 @@ template <bool CL, bool GS = false> __global__ void __launch_bounds__(T, 1) k_la
     // CL (latency mode, launched as 2-CTA clusters): rank r runs only component r; rank 0 keeps c0 in
     // S0 and refreshes a copy of c1 in S1 from rank 1's S1 (DSMEM) every step
     const int rank = CL ? (int)cluster_rank() : 0;
+    const int64_t pi = K.pair0 + (CL ? blockIdx.x >> 1 : blockIdx.x);
     __shared__ uint32_t s_tmem;
     const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
     const ulonglong2 pinv = K.pinv[0];
     const int nt = nat_tid(tid); // S0, S1 in natural order (nat_at / nat_auto: conflict-free)
-    // the one-CTA kernel may stride over the launch's pairs (K.n_units); a cluster handles one pair
-    const int64_t nu = GS ? K.n_units : 1;
-#pragma unroll 1
-    for (int64_t u = GS ? blockIdx.x : 0; u < nu; u += GS ? gridDim.x : 1) {
-    const int64_t pi = K.pair0 + (CL ? blockIdx.x >> 1 : GS ? u : blockIdx.x);
     if (!CL || rank == 0) stage_nat(S0, cin.at(pi, 0));
     if (!CL || rank == 1) stage_nat(S1, cin.at(pi, 1));
     const uint64_t *peer_c1 = CL && rank == 0 ? cluster_peer(S1, 1) : nullptr;
@@ -859,8 +829,6 @@ template <bool CL, bool GS = false> __global__ void __launch_bounds__(T, 1) k_la
                 if (CL) cluster_wait(); // (2) wait: rank 1 stays resident until rank 0's last copy is done
             }
         }
-    }
-    if (GS) BM_SYNCTHREADS(); // S0 / S1 are restaged by the next pair
     }
     tmem_free<256>(s_tmem);
 }

@@ -544,17 +544,3 @@ def test_random_layouts_fuzz(env, O, seed):
         assert np.array_equal(got[j, t], ref[k]), (d, p, n_tmpl, nq, order, j, t)
     sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(nq, -1)[:, :n_tmpl]
     assert np.abs(sc - Q @ T.T).max() < 1e-6, (d, p)
-
-
-@pytest.mark.parametrize("order", [0, 1])
-def test_grid_limited_persistent_kernels_equal(env, O, order):
-    """Option grid_limit: K2, K3 and the one-CTA ladder as persistent grids of at most 37 CTAs striding
-    over their units give the default launch's residues bit for bit (hoisted and paper order)."""
-    torch, B = env
-    T = I.templates(2, 900)
-    Q, _ = I.queries(2, 40)
-    st = Setup(env, O, 128, 8, T, Q)           # 4 sets x 40 queries = 160 pairs: a ladder tail too
-    ref = st.gpu_match(order)
-    with B.options(grid_limit=37):
-        got = st.gpu_match(order)
-    assert np.array_equal(got, ref)
