@@ -804,6 +804,96 @@ int or_match(int logN, int d, int p, int order, const uint64_t *rlk, const uint6
     return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* f2: the relin-free degree-2 output for p = d      */
+/* (s = 1: no rotation, so no key switch needs a degree-1 ciphertext).  */
+/* ------------------------------------------------------------------ */
+/* C = sum_i tensor(C_u,i, C_s,i) = (d0, d1, d2) at level 1 (PAPER.md:328 without the relinearisation
+ * inside Mul(C)), then Res of EACH component by q1 (the rescale formula above applied to
+ * three polynomials); the client decrypts with (1, s, s^2).  qct, sct [p][2][2][N]; out [3][1][N]. */
+static void deg2_pair(const ctx_t *C, int p, const uint64_t *qct, const uint64_t *sct, uint64_t *out)
+{
+    const int N = C->N;
+    const size_t ct1 = (size_t)4 * N;
+    const uint64_t q0 = C->q[0], q1 = C->q[1];
+    uint64_t *d = calloc((size_t)6 * N, sizeof(uint64_t));
+    for (int i = 0; i < p; i++) tensor_acc(C, qct + i * ct1, sct + i * ct1, d);
+    for (int c = 0; c < 3; c++)
+        for (int k = 0; k < N; k++) {
+            uint64_t z = from_signed(centred(d[(size_t)(c * 2 + 1) * N + k], q1), q0);
+            out[(size_t)c * N + k] = mulmod(submod(d[(size_t)(c * 2 + 0) * N + k], z, q0), C->q1_inv_q0, q0);
+        }
+    free(d);
+}
+
+typedef struct {
+    const ctx_t *C;
+    int p;
+    const uint64_t *db, *q;
+    const int64_t *pairs;
+    int64_t n_pairs, next;
+    uint64_t *out; /* [n_pairs][3][N] */
+    pthread_mutex_t mu;
+} job2_t;
+
+static void *worker2(void *arg)
+{
+    job2_t *J = (job2_t *)arg;
+    const int N = J->C->N;
+    const size_t set_stride = (size_t)J->p * 4 * N;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        int64_t i = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (i >= J->n_pairs) break;
+        deg2_pair(J->C, J->p, J->q + (size_t)J->pairs[2 * i] * set_stride, J->db + (size_t)J->pairs[2 * i + 1] * set_stride,
+                  J->out + (size_t)i * 3 * N);
+    }
+    return NULL;
+}
+
+/* the degree-2 scan over listed pairs; requires d == p (s = 1).  out [n_pairs][3][1][N] */
+int or_match_deg2(int logN, int d, int p, const uint64_t *db, int64_t n_sets, const uint64_t *q, int64_t nq,
+                  const int64_t *pairs, int64_t n_pairs, uint64_t *out, int n_threads)
+{
+    if (p <= 0 || d != p) return -1;
+    for (int64_t i = 0; i < n_pairs; i++)
+        if (pairs[2 * i] < 0 || pairs[2 * i] >= nq || pairs[2 * i + 1] < 0 || pairs[2 * i + 1] >= n_sets) return -2;
+    ctx_t C;
+    ctx_init(&C, logN);
+    job2_t J;
+    memset(&J, 0, sizeof J);
+    J.C = &C; J.p = p; J.db = db; J.q = q; J.pairs = pairs; J.n_pairs = n_pairs; J.out = out;
+    pthread_mutex_init(&J.mu, NULL);
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, worker2, &J);
+    for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
+    free(th);
+    pthread_mutex_destroy(&J.mu);
+    ctx_free(&C);
+    return 0;
+}
+
+/* m = c0 + c1 s + c2 s^2 (mod q0) of a level-0 degree-2 ciphertext ct [3][N] */
+void or_decrypt_deg2(int logN, const int8_t *sk, const uint64_t *ct, uint64_t *m)
+{
+    ctx_t C;
+    ctx_init(&C, logN);
+    const int N = C.N;
+    const uint64_t q0 = C.q[0];
+    uint64_t *s = calloc((size_t)N, sizeof(uint64_t)), *s2 = calloc((size_t)N, sizeof(uint64_t)), *t = calloc((size_t)N, sizeof(uint64_t));
+    for (int k = 0; k < N; k++) s[k] = from_signed(sk[k], q0);
+    poly_mul(&C.R[0], s, s, s2);
+    memcpy(m, ct, sizeof(uint64_t) * N);
+    poly_mul(&C.R[0], ct + N, s, t);
+    poly_add(q0, N, m, t, m);
+    poly_mul(&C.R[0], ct + 2 * (size_t)N, s2, t);
+    poly_add(q0, N, m, t, m);
+    free(s); free(s2); free(t);
+    ctx_free(&C);
+}
+
 /* ================================================================== */
 /* f3: server-side query expansion, Algorithm 1    */
 /* "Input Ciphertext Expansion", on the chain        */

@@ -75,6 +75,10 @@ def lib():
         L.or_moddown.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p]
         L.or_match.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p,
                                ctypes.c_int64, _u64p, ctypes.c_int64, _i64p, ctypes.c_int64, _u64p, ctypes.c_int]
+        L.or_match_deg2.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_int64, _u64p,
+                                    ctypes.c_int64, _i64p, ctypes.c_int64, _u64p, ctypes.c_int]
+        L.or_match_deg2.restype = ctypes.c_int
+        L.or_decrypt_deg2.argtypes = [ctypes.c_int, _i8p, _u64p, _u64p]
         L.or_match.restype = ctypes.c_int
         L.or_keygen_hoisted.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u64p]
         L.or_keygen_hoisted.restype = ctypes.c_int
@@ -237,6 +241,31 @@ def moddown(logN, n_q, KS):
     out = np.zeros((n_q, 1 << logN), np.uint64)
     lib().or_moddown(logN, n_q, _p(KS, _u64p), _p(out, _u64p))
     return out
+
+
+def match_deg2(logN, d, p, db, q, pairs=None, n_threads=1):
+    """f2: the relin-free degree-2 scan for p = d (no rotations): per pair sum_i tensor, then Res of
+    each of the three components.  db [T][p][2][2][N], q [Q][p][2][2][N] -> out [n_pairs][3][1][N]."""
+    N = 1 << logN
+    db = np.ascontiguousarray(db, np.uint64)
+    q = np.ascontiguousarray(q, np.uint64)
+    T, Q = db.shape[0], q.shape[0]
+    if pairs is None:
+        pairs = np.array([(j, t) for j in range(Q) for t in range(T)], np.int64).reshape(-1, 2)
+    pairs = np.ascontiguousarray(pairs, np.int64)
+    out = np.zeros((pairs.shape[0], 3, 1, N), np.uint64)
+    rc = lib().or_match_deg2(logN, d, p, _p(db, _u64p), T, _p(q, _u64p), Q, _p(pairs, _i64p), pairs.shape[0],
+                             _p(out, _u64p), n_threads)
+    assert rc == 0, rc
+    return out, pairs
+
+
+def decrypt_deg2(logN, sk, ct):
+    """m = c0 + c1 s + c2 s^2 mod q0 of a level-0 degree-2 ciphertext [3][N] (residues)."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    m = np.zeros(1 << logN, np.uint64)
+    lib().or_decrypt_deg2(logN, _p(np.ascontiguousarray(sk), _i8p), _p(ct, _u64p), _p(m, _u64p))
+    return m
 
 
 def match(logN, d, p, order, rlk, gk, db, q, pairs=None, n_threads=1):

@@ -491,3 +491,57 @@ def test_spec_match_example_N16(O):
     sc, out = _run_scan(O, 4, 4, 2, T, Q)
     # slot 0 = block 0 (template 0), slot 2 = block 1 (template 1)
     assert abs(sc[0, 0] - g["slot0"]) < 1e-6 and abs(sc[0, 1] - g["slot2"]) < 1e-6
+
+
+# ----------------------------------------------------------------------------- f2: relin-free degree-2 output
+def test_deg2_scan_big_integer_closed_form(O):
+    """f2's relin-free output for p = d: per pair, every component of
+    sum_i tensor(C_u,i, C_s,i) rescaled by q1.  Recomputed here with big integers on random (not
+    trivial) ciphertexts: per limb the negacyclic products summed over the parts (Karatsuba-free
+    schoolbook d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1), the CRT lift of the two limbs,
+    and (X - centred_q1(X)) / q1 mod q0."""
+    logN, d = 4, 4
+    p = d
+    N = 1 << logN
+    q0, q1, P = O.primes()
+    rnd = random.Random(71)
+    ct = lambda: np.array([[[[rnd.randrange(m) for _ in range(N)] for m in (q0, q1)] for _ in range(2)]
+                           for _ in range(p)], np.uint64)
+    qct, sct = ct()[None], ct()[None]
+    out, _ = O.match_deg2(logN, d, p, sct, qct)
+    for comp, terms in ((0, [(0, 0)]), (1, [(0, 1), (1, 0)]), (2, [(1, 1)])):
+        lim = []
+        for li, m in enumerate((q0, q1)):
+            acc = [0] * N
+            for i in range(p):
+                for a, b in terms:
+                    pr = _negacyclic_big([int(v) for v in qct[0, i, a, li]], [int(v) for v in sct[0, i, b, li]])
+                    acc = [x + y for x, y in zip(acc, pr)]
+            lim.append([v % m for v in acc])
+        X = [_crt([lim[0][k], lim[1][k]], [q0, q1]) for k in range(N)]
+        exp = [((x - _cent(x, q1)) // q1) % q0 for x in X]
+        assert [int(v) for v in out[0, comp, 0]] == exp, comp
+
+
+def test_deg2_scan_decrypts_with_s_squared(O):
+    """The degree-2 output decrypts with (1, s, s^2) to the cosines of every template (s = 1: every
+    slot is a score, B = 4096) at N = 8192; top-1 is the genuine template.  Tolerance 1e-5 (north_star
+    contract 1e-4): unlike the relinearised output, the rounding of the third component's rescale is
+    multiplied by s^2 (dense ternary s: coefficients of s^2 ~ sqrt(2N/3) ~ 74), a slot error of
+    sigma ~ sqrt(N) 0.29 74 sqrt(N) / 2^40 ~ 1.6e-7 (f2 degree-2 output)."""
+    logN, d = 13, 16
+    p = d
+    T = I.random_unit(300, d, 72)
+    q = T[123] + 0.05 * np.random.default_rng(73).standard_normal(d)
+    Q = (q / np.linalg.norm(q))[None]
+    S, s, B = O.layout(logN, d, p)
+    sk, pk, rlk, gk = O.keygen(logN, 1, 0)
+    db = O.encrypt(logN, pk, O.encode(O.pack_db(T, logN, d, p, 0, 1).reshape(-1, S), logN), 0, 2).reshape(1, p, 2, 2, -1)
+    qc = O.encrypt(logN, pk, O.encode(O.pack_query(Q, logN, d, p).reshape(-1, S), logN), 0, 3).reshape(1, p, 2, 2, -1)
+    out, _ = O.match_deg2(logN, d, p, db, qc)
+    q0, q1, P = O.primes()
+    m = O.decrypt_deg2(logN, sk, out[0].reshape(3, -1))
+    slots = O.decode_slots(O.centred_i64(m, q0), logN, 2.0 ** 80 / q1)
+    sc = slots[:T.shape[0]]
+    assert np.abs(sc - T @ Q[0]).max() < 1e-5
+    assert int(np.argmax(sc)) == 123
