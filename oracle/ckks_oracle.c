@@ -626,7 +626,10 @@ static void rotate(const ctx_t *C, const uint64_t *in, uint64_t r, const uint64_
  *   out_0 = sum_{r<s} sigma_r(c0) + ModDown(sum_{r>=1} KS_r[0]),  out_1 = c1 + ModDown(sum_{r>=1} KS_r[1]).
  * Slot k s of the result holds the same block sum as the ladder's (decrypts to the same scores up to
  * noise), but the residues differ: it has its own parity (order 2).  in/out [2][1][N]. */
-static void hoisted_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+/* (generalised for the baby-step giant-step variant below: the n rotations by i * step, i < n; the
+ *  key of rotation r is hgk[r - 1]; step = 1, n = s is the sum above) */
+static void hoisted_rot_sum_step(const ctx_t *C, int n, int step, const uint64_t *hgk, const uint64_t *in,
+                                 uint64_t *out)
 {
     const int N = C->N;
     const uint64_t q0 = C->q[0], P = C->q[2];
@@ -637,7 +640,8 @@ static void hoisted_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const ui
     uint64_t *c0sum = malloc(sizeof(uint64_t) * N), *ksd = malloc(sizeof(uint64_t) * N);
     for (int k = 0; k < N; k++) xP[k] = c1[k] % P; /* non-centred lift (reading R4): x < q0 < P */
     memcpy(c0sum, c0, sizeof(uint64_t) * N);
-    for (int r = 1; r < s; r++) {
+    for (int i = 1; i < n; i++) {
+        const int r = i * step;
         const uint64_t g = galois_elt(N, (uint64_t)r);
         const uint64_t *key = hgk + (size_t)(r - 1) * 4 * N;
         automorphism(q0, N, c1, g, xr0);
@@ -658,9 +662,35 @@ static void hoisted_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const ui
     free(xr0); free(xrP); free(t); free(xP); free(acc); free(c0sum); free(ksd);
 }
 
+static void hoisted_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+{
+    hoisted_rot_sum_step(C, s, 1, hgk, in, out);
+}
+
+/* f2 baby-step giant-step rotation sum (NOT the paper's ladder): with
+ * s = b g, b = 2^ceil(log2(s) / 2), g = s / b,
+ *   sum_{r<s} Rot(C, r) = sum_{j<g} Rot( sum_{i<b} Rot(C, i), j b )
+ * each of the two sums by one hoisted key switch (b - 1 and g - 1 key products, two ModDowns per
+ * component instead of one): the baby steps use the keys of rotations 1..b-1, the giant steps those of
+ * b, 2b, .., (g-1) b -- all among hgk[s-1].  Same decrypted scores as the ladder, its own residues. */
+static void bsgs_rot_sum(const ctx_t *C, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+{
+    int log_s = 0;
+    while ((1 << log_s) < s) log_s++;
+    const int b = 1 << ((log_s + 1) / 2), g = s / b;
+    uint64_t *baby = malloc(sizeof(uint64_t) * 2 * C->N);
+    hoisted_rot_sum_step(C, b, 1, hgk, in, baby);
+    hoisted_rot_sum_step(C, g, b, hgk, baby, out);
+    free(baby);
+}
+
 void or_hoisted_rot_sum(int logN, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
 {
     ctx_t C; ctx_init(&C, logN); hoisted_rot_sum(&C, s, hgk, in, out); ctx_free(&C);
+}
+void or_bsgs_rot_sum(int logN, int s, const uint64_t *hgk, const uint64_t *in, uint64_t *out)
+{
+    ctx_t C; ctx_init(&C, logN); bsgs_rot_sum(&C, s, hgk, in, out); ctx_free(&C);
 }
 
 /* exported single-op entry points for the pins */
@@ -708,6 +738,7 @@ static void tensor_acc(const ctx_t *C, const uint64_t *ca, const uint64_t *cb, u
  *                    trivial zero ciphertext (line 3; reading R9).
  * then for i = 1..log2(s): C = Add(Rot(C, 2^(i-1)), C)   (lines 7-9, reading R7).
  * order 2 (f2, not the paper's ladder): order 0's C, then hoisted_rot_sum (gk = hgk).
+ * order 4 (f2, not the paper's ladder): order 0's C, then bsgs_rot_sum (gk = hgk).
  * qct, sct: [p][2][2][N]; out: [2][1][N]. */
 static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64_t *rlk, const uint64_t *gk,
                        const uint64_t *qct, const uint64_t *sct, uint64_t *out)
@@ -720,7 +751,7 @@ static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64
     uint64_t *rot = malloc(sizeof(uint64_t) * 2 * N);
     const uint64_t q0 = C->q[0];
     memset(out, 0, sizeof(uint64_t) * 2 * N);
-    if (order == 0 || order == 2) {
+    if (order == 0 || order == 2 || order == 4) {
         for (int i = 0; i < p; i++) tensor_acc(C, qct + i * ct1, sct + i * ct1, d);
         relinearize(C, d, rlk, r1);
         rescale(C, r1, out);
@@ -733,9 +764,10 @@ static void he_c3_pair(const ctx_t *C, int p, int log_s, int order, const uint64
             poly_add(q0, 2 * N, out, r0, out); /* Add at level 0, both components */
         }
     }
-    if (order == 2) { /* f2: gk holds the hoisted keys hgk[s-1] */
+    if (order == 2 || order == 4) { /* f2: gk holds the hoisted keys hgk[s-1] */
         memcpy(r0, out, sizeof(uint64_t) * 2 * N);
-        hoisted_rot_sum(C, 1 << log_s, gk, r0, out);
+        if (order == 2) hoisted_rot_sum(C, 1 << log_s, gk, r0, out);
+        else bsgs_rot_sum(C, 1 << log_s, gk, r0, out);
     } else {
         for (int i = 1; i <= log_s; i++) {
             rotate(C, out, (uint64_t)1 << (i - 1), gk + (size_t)(i - 1) * 4 * N, rot);

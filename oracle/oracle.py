@@ -83,6 +83,7 @@ def lib():
         L.or_keygen_hoisted.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u64p]
         L.or_keygen_hoisted.restype = ctypes.c_int
         L.or_hoisted_rot_sum.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p]
+        L.or_bsgs_rot_sum.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p, _u64p]
         # f3: server-side query expansion on the chain extended by q2
         L.or_find_prime_below.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         L.or_find_prime_below.restype = ctypes.c_uint64
@@ -198,6 +199,16 @@ def hoisted_rot_sum(logN, s, hgk, ct):
     return out
 
 
+def bsgs_rot_sum(logN, s, hgk, ct):
+    """f2: sum_{r<s} Rot(ct, r) as baby steps (b = 2^ceil(log2(s)/2)) then giant steps (g = s / b), each
+    one hoisted key switch; ct [2][1][N] level 0."""
+    ct = np.ascontiguousarray(ct, np.uint64)
+    out = np.zeros((2, 1, 1 << logN), np.uint64)
+    h = np.ascontiguousarray(hgk if len(hgk) else np.zeros((1, 2, 2, 1 << logN), np.uint64), np.uint64)
+    lib().or_bsgs_rot_sum(logN, s, _p(h, _u64p), _p(ct, _u64p), _p(out, _u64p))
+    return out
+
+
 def encrypt(logN, pk, pt, first_obj, seed):
     """pt int64 [n][N] -> level-1 cts [n][2][2][N] (coefficient domain)."""
     pt = np.ascontiguousarray(pt, np.int64)
@@ -270,7 +281,8 @@ def decrypt_deg2(logN, sk, ct):
 
 def match(logN, d, p, order, rlk, gk, db, q, pairs=None, n_threads=1):
     """Algorithm 2 over (query, set) pairs. db [T][p][2][2][N], q [Q][p][2][2][N].
-    order 0 hoisted relin, 1 paper order, 2 f2 hoisted rotation sum (gk = keygen_hoisted keys).
+    order 0 hoisted relin, 1 paper order, 2 f2 hoisted rotation sum, 4 f2 baby-step giant-step rotation
+    sum (2 and 4: gk = keygen_hoisted keys).
     Returns out [n_pairs][2][1][N] and the pairs array."""
     N = 1 << logN
     db = np.ascontiguousarray(db, np.uint64)

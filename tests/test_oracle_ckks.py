@@ -384,6 +384,57 @@ def test_hoisted_rotation_sum_decrypts_to_window_sums(O):
         assert np.array_equal(O.hoisted_rot_sum(logN, 1, O.keygen_hoisted(logN, 4, 1), ct0), ct0)
 
 
+def test_bsgs_rotation_sum_decrypts_to_window_sums(O):
+    """f2 baby-step giant-step sum (b = 2^ceil(log2 s / 2) baby rotations, g = s / b giant ones, each a
+    hoisted key switch) decrypts to the sum of the s left rotations of the slots, s = 2..32
+    (s = 2: b = 2, g = 1 -- the plain hoisted sum, bit for bit)."""
+    logN = 6
+    S = 32
+    q0 = O.primes()[0]
+    sk, pk, rlk, gk = O.keygen(logN, 4, 3)
+    z = np.random.default_rng(8).uniform(-1, 1, S)
+    ct = O.encrypt(logN, pk, O.encode(z[None], logN), 0, 1)[0]
+    ct0 = np.ascontiguousarray(ct[:, :1, :])
+    for s in (2, 4, 8, 16, 32):
+        hgk = O.keygen_hoisted(logN, 4, s)
+        out = O.bsgs_rot_sum(logN, s, hgk, ct0)
+        m = O.decrypt(logN, sk, out, 1)[0]
+        back = O.decode_slots(O.centred_i64(m, q0), logN, O.DELTA)
+        want = sum(_rot_left(z, r) for r in range(s))
+        assert np.abs(back - want).max() < 1e-6, s
+        if s == 2:
+            assert np.array_equal(out, O.hoisted_rot_sum(logN, s, hgk, ct0))
+        else:
+            assert not np.array_equal(out, O.hoisted_rot_sum(logN, s, hgk, ct0))
+
+
+@pytest.mark.parametrize("s_len", [4, 8, 16])
+def test_bsgs_rotation_sum_exact_error_bound(O, s_len):
+    """With error-free keys the baby-step giant-step sum is the window sum of the decryption up to the
+    two ModDowns' rounding: o0 + o1 s - sum_{r<s} sigma_r(c0 + c1 s) = g e_b' + e_g with every
+    |coefficient| <= (g + 1)(N + 1)/2 (each hoisted ModDown adds |e| <= (N + 1)/2, the baby one is
+    rotated g times), big integers, random level-0 ciphertext.  A wrong key (amount, index) or a wrong
+    giant stride leaves an error of order q0."""
+    logN = 5
+    N = 1 << logN
+    q0 = O.primes()[0]
+    sk, pk, rlk, gk = O.keygen(logN, 6, 0, zero_error=True)
+    hgk = O.keygen_hoisted(logN, 6, s_len, zero_error=True)
+    rnd = random.Random(90 + s_len)
+    ct = np.array([[[rnd.randrange(q0) for _ in range(N)]] for _ in range(2)], np.uint64)
+    out = O.bsgs_rot_sum(logN, s_len, hgk, ct)
+    sv = [int(v) for v in sk]
+    m = [int(a) + b for a, b in zip(ct[0, 0], _negacyclic_big([int(v) for v in ct[1, 0]], sv))]
+    want = [0] * N
+    for r in range(s_len):
+        want = [a + b for a, b in zip(want, _sigma_signed(m, pow(5, r, 2 * N)))]
+    got = [int(a) + b for a, b in zip(out[0, 0], _negacyclic_big([int(v) for v in out[1, 0]], sv))]
+    e = [_cent((x - y) % q0, q0) for x, y in zip(got, want)]
+    log_s = s_len.bit_length() - 1
+    g = s_len // (1 << ((log_s + 1) // 2))
+    assert max(abs(v) for v in e) <= (g + 1) * (N + 1) // 2 and any(v != 0 for v in e)
+
+
 def test_hoisted_keys_are_galois_keys_of_their_rotation(O):
     """hgk[r-1] satisfies the Galois-key relation of rotation r: with zero-error keys,
     b + a s = (P mod q0) sigma_{5^r}(s) in q0 and 0 in P -- an independent big-integer check of the
