@@ -851,7 +851,64 @@ def run_extras(args, B, torch, dev, stream):
         out["f1_compressed"] = run_f1(args, B, torch, prm, pk, sk, d_out, n_sets, n_tmpl, tq, stream)
     except Exception as ex:  # noqa: BLE001
         out["f1_compressed"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    del d_db, d_q, d_out
+    torch.cuda.empty_cache()
+    try:
+        out["f2_degree2"] = run_f2_deg2(args, B, torch, dev, stream)
+    except Exception as ex:  # noqa: BLE001
+        out["f2_degree2"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     return out
+
+
+def run_f2_deg2(args, B, torch, dev, stream):
+    """f2 relin-free degree-2 output (BM_ORDER_DEG2) against the relinearised scan of the SAME
+    workload: configs[1]'s 6,144 templates at p = d = 128 (s = 1: no ladder either way), 96 queries.
+    Device time of one bm_match per order; the degree-2 results are 1.5x the bytes and decrypt with
+    s^2 (client cost); scores of 2 queries checked against float64 cosines."""
+    from paper_2408_06167_b200 import inputs as I
+    d = p = 128
+    nq = 96
+    prm = B.bm_params_init(d, p)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
+    n_tmpl = I.CONFIGS[2]["n"]
+    n_sets = -(-n_tmpl // prm.B)
+    T = I.templates(2, n_tmpl)
+    Q, _ = I.queries(2, nq)
+    d_db = torch.empty((n_sets, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_db(prm, pk_dev, T, 0, n_sets, 2, d_db)
+    d_q = torch.empty((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
+    B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
+    res = {}
+    k = max(1, min(args.steps, 5))
+    for order, name in ((0, "relinearised"), (B.ORDER_DEG2, "degree2")):
+        out = torch.empty((nq, n_sets, B.n_components(order), N_RING), dtype=torch.int64, device=dev)
+        ws = torch.empty(B.bm_match_ws_bytes(prm, n_sets, nq, order), dtype=torch.uint8, device=dev)
+        ek = None if order == B.ORDER_DEG2 else evk_dev
+        for _ in range(2):
+            B.bm_match(prm, ek, d_db, n_sets, d_q, nq, out, ws, order)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            B.bm_match(prm, ek, d_db, n_sets, d_q, nq, out, ws, order)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        h = out[:2].cpu().numpy().view(np.uint64)
+        t0 = time.perf_counter()
+        sc = (B.bm_decrypt_deg2 if order == B.ORDER_DEG2 else B.bm_decrypt)(prm, sk, h.reshape(2 * n_sets, -1))
+        dec_ms = (time.perf_counter() - t0) * 1e3 / (2 * n_sets)
+        err = float(np.abs(sc.reshape(2, -1)[:, :n_tmpl] - Q[:2] @ T.T).max())
+        res[name] = {"ms_per_step": round(ms, 4), "value": round(n_tmpl * nq / (ms / 1e3), 1),
+                     "unit": "templates*queries/s", "result_bytes_per_pair": int(B.n_components(order) * N_RING * 8),
+                     "client_decrypt_ms_per_result": round(dec_ms, 3), "max_abs_score_err_2q": err}
+        del out, ws
+        torch.cuda.empty_cache()
+    res["speedup_device"] = round(res["relinearised"]["ms_per_step"] / res["degree2"]["ms_per_step"], 3)
+    res["note"] = ("configs[1] templates at p = d = 128, 96 queries: relin-free degree-2 output vs the "
+                   "relinearised scan (both s = 1, no ladder); device time of one bm_match")
+    return res
 
 
 def f3_modmuls(p, s):

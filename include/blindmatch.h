@@ -56,9 +56,14 @@ typedef enum {
 typedef enum {
     BM_ORDER_HOISTED = 0,     /* sum_i tensor_i, then one relin + one rescale (reading R8) */
     BM_ORDER_PAPER = 1,       /* per part Res(Mul(C_u,i, C_s,i)), then Add at level 0 */
-    BM_ORDER_HOISTED_ROT = 2  /* f2, NOT the paper's ladder: BM_ORDER_HOISTED's C,
+    BM_ORDER_HOISTED_ROT = 2, /* f2, NOT the paper's ladder: BM_ORDER_HOISTED's C,
                                  then sum_{r<s} Rot(C, r) with ONE hoisted key switch (Halevi-Shoup):
                                  same decrypted scores, different residues; needs bm_evk_add_hoisted */
+    BM_ORDER_DEG2 = 3         /* f2, relin-free, p = d only (s = 1, no ladder):
+                                 sum_i tensor_i rescaled by q1 component by component; the result is
+                                 the DEGREE-2 ciphertext (d0, d1, d2) [nq][n_sets][3][N] (coefficients,
+                                 scale out_scale), decrypted with (1, s, s^2) by bm_decrypt_deg2;
+                                 evk unused (may be NULL); BM_ERR_INVALID_LAYOUT when p != d */
 } bm_order;
 
 /* Scheme parameters and the packing layout:
@@ -187,6 +192,7 @@ int bm_ct_import(const bm_params *, const uint8_t *buf, size_t len, uint64_t *ct
  * d_ws:  device workspace of at least bm_match_ws_bytes(prm, n_sets, nq, order) bytes.
  * Per (query, set): tensor + sum over parts (a4), relinearize (a5), rescale (a6), log2(s)
  * rotate-and-add steps (a7), all in sm_100a kernels on `stream`; allocates nothing.
+ * BM_ORDER_DEG2 instead writes d_out [nq][n_sets][3][N] (the degree-2 result; see bm_order).
  * Errors: BM_ERR_INVALID_ARG, BM_ERR_MISSING_ROTATION_KEY, BM_ERR_KEY_MISMATCH,
  * BM_ERR_WORKSPACE, BM_ERR_CUDA (launch errors; faults at bm_sync). nq = 0 or n_sets = 0
  * is a no-op.  Kernel choice depends only on the launch size, never on the results: chunks of
@@ -293,6 +299,10 @@ int bm_decrypt_dev(const bm_params *, const bm_sk_dev *, const uint64_t *d_ct, i
  * centred message coefficients m = c0 + c1 s mod q0 as int64 [n][N]. */
 int bm_decrypt(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, double *scores);
 int bm_decrypt_raw(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, int64_t *m);
+/* f2 degree-2 results (BM_ORDER_DEG2): h_ct [n][3][N] coefficient-domain (d0, d1, d2) over q0;
+ * m = d0 + d1 s + d2 s^2 mod q0 (the decryption of a degree-2 ciphertext, PAPER.md:155-157 extended
+ * to the tensor's third component), then scores[n][B] as bm_decrypt (s = 1: every slot).  Same errors. */
+int bm_decrypt_deg2(const bm_params *, const bm_sk *, const uint64_t *h_ct, int64_t n, double *scores);
 /* argmax with the lowest index winning ties. */
 int bm_top1(const double *scores, int64_t n, int64_t *idx, double *best);
 

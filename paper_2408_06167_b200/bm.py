@@ -23,6 +23,7 @@ SLOTS = 4096
 ORDER_HOISTED = 0
 ORDER_PAPER = 1
 ORDER_HOISTED_ROT = 2   # f2: hoisted rotation sum, not the paper's ladder
+ORDER_DEG2 = 3          # f2: relin-free degree-2 output (p = d), [nq][n_sets][3][N]; bm_decrypt_deg2
 
 BM_OK = 0
 ERRORS = {
@@ -81,6 +82,7 @@ _SIGS = {
     "bm_profile_read": (_i32, [_vp, _vp, _vp]),
     "bm_decrypt": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_decrypt_raw": (_i32, [_P, _vp, _vp, _i64, _vp]),
+    "bm_decrypt_deg2": (_i32, [_P, _vp, _vp, _i64, _vp]),
     "bm_ct_export": (_i32, [_P, _vp, _i64, _i32, ctypes.c_double, _vp, ctypes.POINTER(_sz)]),
     "bm_ct_import": (_i32, [_P, _vp, _sz, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32),
                             ctypes.POINTER(ctypes.c_double)]),
@@ -354,12 +356,18 @@ def _check_scan(prm, d_db, n_sets, d_q, nq, n_limbs=2):
         _need(d_q, nq * prm.p * 2 * n_limbs * N, "d_q")
 
 
+def n_components(order):
+    """Result polynomials per (query, set): 3 for the degree-2 output, else 2."""
+    return 3 if order == ORDER_DEG2 else 2
+
+
 def bm_match(prm, evk_dev, d_db, n_sets, d_q, nq, d_out, d_ws, order=ORDER_HOISTED, stream=None):
+    """evk_dev may be None for ORDER_DEG2 (no key switch)."""
     _check_scan(prm, d_db, n_sets, d_q, nq)
     if n_sets and nq:
-        _need(d_out, nq * n_sets * 2 * N, "d_out")
+        _need(d_out, nq * n_sets * n_components(order) * N, "d_out")
     ws_bytes = d_ws.numel() * d_ws.element_size() if d_ws is not None else 0
-    _chk(_lib.bm_match(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
+    _chk(_lib.bm_match(ctypes.byref(prm), evk_dev.ptr if evk_dev is not None else None, _dptr(d_db) if n_sets else None, n_sets,
                        _dptr(d_q) if nq else None, nq, _dptr(d_out) if nq * n_sets else None,
                        _dptr(d_ws) if ws_bytes else None, ws_bytes, order, _stream(stream)), "bm_match")
 
@@ -373,7 +381,7 @@ def bm_match_rows(prm, evk_dev, d_db, n_sets, d_q, nq, d_rows, set_offset, d_ws,
     if set_offset < 0:
         raise ValueError("set_offset must be >= 0")
     ws_bytes = d_ws.numel() * d_ws.element_size()
-    _chk(_lib.bm_match_rows(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db) if n_sets else None, n_sets,
+    _chk(_lib.bm_match_rows(ctypes.byref(prm), evk_dev.ptr if evk_dev is not None else None, _dptr(d_db) if n_sets else None, n_sets,
                             _dptr(d_q) if nq else None, nq, _dptr(d_rows), set_offset,
                             _dptr(d_ws) if ws_bytes else None, ws_bytes, order, _stream(stream)), "bm_match_rows")
 
@@ -417,8 +425,8 @@ def bm_match_host(prm, evk_dev, d_db, n_sets, h_q, nq, h_out, d_ws, order=ORDER_
     """h_q / h_out: (pinned) CPU tensors or numpy arrays."""
     _need(d_db, n_sets * prm.p * 4 * N, "d_db")
     ws_bytes = d_ws.numel() * d_ws.element_size()
-    _chk(_lib.bm_match_host(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets, _hp(h_q, nq * prm.p * 4 * N, "h_q"),
-                            nq, _hp(h_out, nq * n_sets * 2 * N, "h_out"), _dptr(d_ws), ws_bytes, order,
+    _chk(_lib.bm_match_host(ctypes.byref(prm), evk_dev.ptr if evk_dev is not None else None, _dptr(d_db), n_sets, _hp(h_q, nq * prm.p * 4 * N, "h_q"),
+                            nq, _hp(h_out, nq * n_sets * n_components(order) * N, "h_out"), _dptr(d_ws), ws_bytes, order,
                             _stream(stream)), "bm_match_host")
 
 
@@ -428,9 +436,9 @@ def bm_match_host_ring(prm, evk_dev, d_db, n_sets, h_q, nq, h_ring, ring_rows, d
     [ring_rows][n_sets][2][N] (bounded host memory for very large result sets)."""
     _need(d_db, n_sets * prm.p * 4 * N, "d_db")
     ws_bytes = d_ws.numel() * d_ws.element_size()
-    _chk(_lib.bm_match_host_ring(ctypes.byref(prm), evk_dev.ptr, _dptr(d_db), n_sets,
+    _chk(_lib.bm_match_host_ring(ctypes.byref(prm), evk_dev.ptr if evk_dev is not None else None, _dptr(d_db), n_sets,
                                  _hp(h_q, nq * prm.p * 4 * N, "h_q"), nq,
-                                 _hp(h_ring, ring_rows * n_sets * 2 * N, "h_ring"), ring_rows, _dptr(d_ws), ws_bytes,
+                                 _hp(h_ring, ring_rows * n_sets * n_components(order) * N, "h_ring"), ring_rows, _dptr(d_ws), ws_bytes,
                                  order, _stream(stream)), "bm_match_host_ring")
 
 
@@ -533,6 +541,15 @@ def bm_decrypt_raw(prm, sk, h_ct):
     n = h_ct.size // (2 * N)
     out = np.zeros((n, N), np.int64)
     _chk(_lib.bm_decrypt_raw(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt_raw")
+    return out
+
+
+def bm_decrypt_deg2(prm, sk, h_ct):
+    """f2 degree-2 results: h_ct uint64 [n][3][N] canonical (BM_ORDER_DEG2) -> scores float64 [n][B]."""
+    h_ct = np.ascontiguousarray(h_ct, np.uint64)
+    n = h_ct.size // (3 * N)
+    out = np.zeros((n, prm.B), np.float64)
+    _chk(_lib.bm_decrypt_deg2(ctypes.byref(prm), sk.ptr, _np_ptr(h_ct), n, _np_ptr(out)), "bm_decrypt_deg2")
     return out
 
 

@@ -176,6 +176,7 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
+    cudaFuncSetAttribute(k_rescale_deg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K7_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_c3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
@@ -1063,11 +1064,13 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
                       const uint64_t *d_q, int32_t nq, uint64_t *d_out, uint64_t *const *d_rows, int64_t set_offset,
                       void *d_ws, size_t ws_bytes, int32_t order, void *stream)
 {
-    if (!prm || !evk || n_sets < 0 || nq < 0 ||
-        (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT))
+    const bool deg2 = order == BM_ORDER_DEG2;
+    if (!prm || (!evk && !deg2) || n_sets < 0 || nq < 0 ||
+        (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT && !deg2))
         return BM_ERR_INVALID_ARG;
-    if (memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
-    if (order != BM_ORDER_HOISTED_ROT && evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    if (deg2 && prm->s != 1) return BM_ERR_INVALID_LAYOUT; // the degree-2 output has no ladder: p = d only
+    if (evk && memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
+    if (!deg2 && order != BM_ORDER_HOISTED_ROT && evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
     if (order == BM_ORDER_HOISTED_ROT && evk->n_hrot < prm->s - 1) return BM_ERR_MISSING_ROTATION_KEY;
     const int64_t total = n_sets * (int64_t)nq;
     if (total == 0) return BM_OK;
@@ -1086,8 +1089,8 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     K.q1inv = C->q1inv;
     K.pmod[0] = C->pmod[0];
     K.pmod[1] = C->pmod[1];
-    K.rlk = reinterpret_cast<const uint64_t *>(evk->rlk);
-    K.gk = reinterpret_cast<const uint64_t *>(evk->gk);
+    K.rlk = evk ? reinterpret_cast<const uint64_t *>(evk->rlk) : nullptr;
+    K.gk = evk ? reinterpret_cast<const uint64_t *>(evk->gk) : nullptr;
     K.db = d_db;
     K.qry = d_q;
     K.out = d_out;
@@ -1154,6 +1157,14 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
             counted();
             end();
+            if (deg2) {
+                beg(6, 3 * np);
+                k_rescale_deg2<<<3 * npu, T, K7_SMEM_BYTES, s>>>(K);
+                counted();
+                end();
+                rc = launch_check();
+                break;
+            }
             beg(1, 6 * np);
             k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
             counted();
@@ -1225,7 +1236,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             end();
             rc = launch_check();
         }
-        if (log_s == 0 && !rc) {
+        if (log_s == 0 && !rc && !deg2) {
             beg(6, 2 * np);
             k_out_intt<<<2 * npu, T, SMEM_BYTES, s>>>(K, bufC);
             counted();
@@ -1338,7 +1349,8 @@ size_t bm_match_host_ws_bytes(const bm_params *prm, int64_t n_sets, int32_t nq, 
     if (!prm || n_sets <= 0 || nq <= 0) return 0;
     const int G = host_groups(n_sets, nq);
     const int64_t gq = (nq + G - 1) / G;
-    const size_t qbytes = (size_t)gq * prm->p * 4 * N * 8, obytes = (size_t)gq * n_sets * 2 * N * 8;
+    const int nc = order == BM_ORDER_DEG2 ? 3 : 2; // result components
+    const size_t qbytes = (size_t)gq * prm->p * 4 * N * 8, obytes = (size_t)gq * n_sets * nc * N * 8;
     const size_t mws = (bm_match_ws_bytes(prm, n_sets, (int32_t)gq, order) + 255) & ~(size_t)255;
     return HOST_SLOTS * (qbytes + obytes) + 2 * mws;
 }
@@ -1364,7 +1376,7 @@ static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const ui
             }
     const int G = host_groups(n_sets, nq);
     const int64_t gq = (nq + G - 1) / G;
-    const size_t qrow = (size_t)prm->p * 4 * N, orow = (size_t)n_sets * 2 * N; // u64 per query
+    const size_t qrow = (size_t)prm->p * 4 * N, orow = (size_t)n_sets * (order == BM_ORDER_DEG2 ? 3 : 2) * N; // u64 per query
     uint64_t *dq[HOST_SLOTS], *dout[HOST_SLOTS];
     uint64_t *base = (uint64_t *)d_ws;
     for (int k = 0; k < HOST_SLOTS; k++) dq[k] = base + k * gq * qrow;
@@ -1378,7 +1390,7 @@ static int match_host_impl(const bm_params *prm, const bm_evk_dev *evk, const ui
     // (last download) shrink; the middle groups are gq queries
     std::vector<int64_t> g0, gn;
     {
-        const int64_t h = nq >= 4 ? (gq + 1) / 2 : nq;
+        const int64_t h = nq >= 4 ? (gq + 1) / 2 : gq; // (fewer queries: groups of gq, the slot size)
         int64_t q = 0;
         g0.push_back(0), gn.push_back(h), q = h;
         const int64_t tail = nq - q > h ? h : 0;

@@ -924,21 +924,28 @@ int bm_ct_import(const bm_params *prm, const uint8_t *buf, size_t len, uint64_t 
 }
 
 // ------------------------------------------------------------------ decryption
-int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, int64_t *m)
+// m = c0 + c1 s (+ c2 s^2 when deg == 2) mod q0, centred
+static int decrypt_m(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, int deg, int64_t *m)
 {
     if (!prm || !sk || (!ct && n) || (!m && n) || n < 0) return BM_ERR_INVALID_ARG;
     if (memcmp(sk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
-    std::vector<uint64_t> s(N);
+    std::vector<uint64_t> s(N), s2(N);
     for (int k = 0; k < N; k++) s[k] = to_res(sk->s[k], Q0);
     host_ntt_fwd(s.data(), 0);
+    for (int k = 0; k < N; k++) s2[k] = mulmod_h(s[k], s[k], Q0);
     return parallel_for(n, [&](int64_t c) {
-        std::vector<uint64_t> t(N);
-        const uint64_t *c0 = ct + (size_t)c * 2 * N, *c1 = c0 + N;
+        std::vector<uint64_t> t(N), t2(N);
+        const uint64_t *c0 = ct + (size_t)c * (deg + 1) * N, *c1 = c0 + N, *c2 = c1 + N;
         for (int k = 0; k < N; k++)
-            if (c0[k] >= Q0 || c1[k] >= Q0) return (int)BM_ERR_INVALID_ARG;
+            if (c0[k] >= Q0 || c1[k] >= Q0 || (deg == 2 && c2[k] >= Q0)) return (int)BM_ERR_INVALID_ARG;
         memcpy(t.data(), c1, 8 * N);
         host_ntt_fwd(t.data(), 0);
         for (int k = 0; k < N; k++) t[k] = mulmod_h(t[k], s[k], Q0);
+        if (deg == 2) {
+            memcpy(t2.data(), c2, 8 * N);
+            host_ntt_fwd(t2.data(), 0);
+            for (int k = 0; k < N; k++) t[k] = (t[k] + mulmod_h(t2[k], s2[k], Q0)) % Q0;
+        }
         host_ntt_inv(t.data(), 0);
         for (int k = 0; k < N; k++) {
             uint64_t v = (c0[k] + t[k]) % Q0;
@@ -948,11 +955,17 @@ int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, in
     });
 }
 
-int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, double *scores)
+int bm_decrypt_raw(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, int64_t *m)
+{
+    return decrypt_m(prm, sk, ct, n, 1, m);
+}
+
+static int decrypt_scores(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, int deg,
+                          double *scores)
 {
     if (!prm || !scores) return BM_ERR_INVALID_ARG;
     std::vector<int64_t> m((size_t)std::max<int64_t>(n, 0) * N);
-    int rc = bm_decrypt_raw(prm, sk, ct, n, m.data());
+    int rc = decrypt_m(prm, sk, ct, n, deg, m.data());
     if (rc) return rc;
     // score of block k = slot k*s:  z = sum_t m_t cos(pi t e / N) / out_scale, e = 5^(k s) mod 2N
     static std::vector<double> cosT;
@@ -972,6 +985,16 @@ int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_
         }
         return (int)BM_OK;
     });
+}
+
+int bm_decrypt(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, double *scores)
+{
+    return decrypt_scores(prm, sk, ct, n, 1, scores);
+}
+
+int bm_decrypt_deg2(const bm_params *prm, const bm_sk *sk, const uint64_t *ct, int64_t n, double *scores)
+{
+    return decrypt_scores(prm, sk, ct, n, 2, scores);
 }
 
 // f1: packed (compressed) results: every slot is a score -- slot k s + u of packed ciphertext g is set

@@ -1141,3 +1141,36 @@ __global__ void __launch_bounds__(T, 1) k_out_intt(MatchK K, CtBuf cin)
     inv<0>(a, sm, K.pr[0]);
     store_coef(K.out_at(pi, c), a);
 }
+
+// ================================================================== f2 K7: relin-free degree-2 output
+// BM_ORDER_DEG2 (p = d, s = 1, reading R32): the scan stops after the
+// tensor, the result is the degree-2 ciphertext (d0, d1, d2) = sum_i tensor(C_u,i, C_s,i) rescaled by q1
+// component by component -- no key switch, no rotations (s = 1: every slot is a score).  CTA (pair, c):
+//   U = INTT_q1(d_c[q1]) (canonical);  z^ = centred_q1(U);  out_c = q1^-1 (INTT_q0(d_c[q0]) - z^) mod q0
+// (PAPER.md:329 Res at level 1 -> 0 on each component; the same rescale K3 applies after its ModDown).
+// Output [nq][n_sets][3][N] (coefficients, [0, q0)) or rows[j] + (set * 3 + c) N.
+constexpr size_t K7_SMEM_BYTES = (SMEM_WORDS + (size_t)N) * sizeof(uint64_t);
+__global__ void __launch_bounds__(T, 1) k_rescale_deg2(MatchK K)
+{
+    extern __shared__ uint64_t sm[];
+    uint64_t *zs = sm + SMEM_WORDS;
+    const int tid = threadIdx.x;
+    const int64_t pi = blockIdx.x / 3;
+    const int c = (int)(blockIdx.x - 3 * pi);
+    const uint64_t *src = c < 2 ? K.D01 + ((size_t)pi * 4 + c * 2) * N : K.D2 + (size_t)pi * 2 * N; // [q0], [q1]
+    uint64_t a[E];
+    load_eval(a, src + N);
+    inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // canonical [0, q1)
+#pragma unroll
+    for (int e = 0; e < E; e++) zs[tid + T * e] = a[e] > (Q1 >> 1) ? a[e] + (Q0 - Q1) : a[e]; // z^ mod q0
+    load_eval(a, src);
+    inv<0>(a, sm, K.pr[0]); // canonical [0, q0)
+    const ulonglong2 q1inv = K.q1inv;
+#pragma unroll
+    for (int e = 0; e < E; e++) a[e] = reduce_bnd<0>(shoup4<0>(a[e] + Q0 - zs[tid + T * e], q1inv));
+    BM_CHECK(pi >= 0 && pi < (int64_t)K.cq * K.ct && K.jq0 + pi / K.ct < K.nq_total);
+    const int64_t set = K.t0 + pi % K.ct;
+    uint64_t *o = K.rows ? K.rows[K.jq0 + pi / K.ct] + ((K.set_off + set) * 3 + c) * (int64_t)N
+                         : K.out + ((K.out_row(pi)) * 3 + c) * (int64_t)N;
+    store_coef(o, a);
+}

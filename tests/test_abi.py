@@ -113,6 +113,27 @@ def test_decrypt_matches_oracle(B, O):
     assert B.bm_top1(np.array([0.5, 0.7, 0.7, 0.1]))[0] == 1   # lowest index wins ties
 
 
+def test_decrypt_deg2_matches_oracle(B, O):
+    """Client-side decryption (1, s, s^2) of an oracle-made degree-2 result (f2 BM_ORDER_DEG2, p = d)."""
+    d = p = 16
+    prm = B.bm_params_init(d, p)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    osk, opk, orlk, ogk = O.keygen(13, 1, 0)
+    T = I.random_unit(200, d, 5)
+    Q = I.random_unit(1, d, 6)
+    db = O.encrypt(13, opk, O.encode(O.pack_db(T, 13, d, p, 0, 1).reshape(-1, 4096), 13), 0, 2).reshape(1, p, 2, 2, -1)
+    qc = O.encrypt(13, opk, O.encode(O.pack_query(Q, 13, d, p).reshape(-1, 4096), 13), 0, 3).reshape(1, p, 2, 2, -1)
+    out, _ = O.match_deg2(13, d, p, db, qc)
+    sc = B.bm_decrypt_deg2(prm, sk, out.reshape(1, 3, -1))[0]
+    q0 = prm.q[0]
+    om = O.decrypt_deg2(13, osk, out[0].reshape(3, -1))
+    osc = O.decode_slots(O.centred_i64(om, q0), 13, prm.out_scale)
+    assert np.abs(sc - osc[:prm.B]).max() < 1e-9
+    assert np.abs(sc[:200] - T @ Q[0]).max() < 1e-5
+    with pytest.raises(B.BMError):                     # residues must be canonical
+        B.bm_decrypt_deg2(prm, sk, np.full((1, 3, 8192), q0, np.uint64))
+
+
 def test_key_import_roundtrip(B):
     prm = B.bm_params_init(32, 2)
     sk, pk, evk = B.bm_keygen(prm, 77)

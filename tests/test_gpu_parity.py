@@ -69,10 +69,11 @@ class Setup:
 
     def gpu_match(self, order=0):
         torch, B = self.torch, self.B
-        out = torch.empty((self.nq, self.n_sets, 2, 8192), dtype=torch.int64, device="cuda")
+        out = torch.empty((self.nq, self.n_sets, B.n_components(order), 8192), dtype=torch.int64, device="cuda")
         ws = torch.empty(max(1, B.bm_match_ws_bytes(self.prm, self.n_sets, self.nq, order)), dtype=torch.uint8,
                          device="cuda")
-        B.bm_match(self.prm, self.evk_dev, self.d_db, self.n_sets, self.d_q, self.nq, out, ws, order)
+        evk = None if order == B.ORDER_DEG2 else self.evk_dev      # the degree-2 output needs no keys
+        B.bm_match(self.prm, evk, self.d_db, self.n_sets, self.d_q, self.nq, out, ws, order)
         B.bm_sync()
         return out.cpu().numpy().view(np.uint64)
 
@@ -82,6 +83,10 @@ class Setup:
         qi = {j: k for k, j in enumerate(qs)}
         ti = {t: k for k, t in enumerate(ts)}
         local = np.array([(qi[j], ti[t]) for j, t in pairs], np.int64).reshape(-1, 2)
+        if order == 3:
+            out, _ = self.O.match_deg2(LOGN, self.d, self.p, self.oracle_db(ts), self.oracle_q(qs), pairs=local,
+                                       n_threads=NTH)
+            return out.reshape(-1, 3, 8192)
         gk = self.ohgk if order == 2 else self.ogk
         out, _ = self.O.match(LOGN, self.d, self.p, order, self.orlk, gk, self.oracle_db(ts), self.oracle_q(qs),
                               pairs=local, n_threads=NTH)
@@ -229,6 +234,22 @@ def test_match_host_pipelined_equals_device(env, O, groups):
             assert np.array_equal(ring[j % 3].numpy().view(np.uint64), dev_out[j]), j
 
 
+@pytest.mark.parametrize("nq", [1, 2, 3, 5])
+def test_match_host_few_queries(env, O, nq):
+    """bm_match_host with fewer queries than its default 4 groups (one query per group; regression: the
+    first group used to take all nq < 4 queries into a one-query slot -> BM_ERR_WORKSPACE)."""
+    torch, B = env
+    T = I.templates(2, 700)
+    Q, _ = I.queries(2, nq)
+    st = Setup(env, O, 128, 8, T, Q)
+    dev_out = st.gpu_match(0)
+    h_q = st.d_q.cpu().pin_memory()
+    h_out = torch.empty((st.nq, st.n_sets, 2, 8192), dtype=torch.int64).pin_memory()
+    ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq), dtype=torch.uint8, device="cuda")
+    B.bm_match_host(st.prm, st.evk_dev, st.d_db, st.n_sets, h_q, st.nq, h_out, ws)
+    assert np.array_equal(h_out.numpy().view(np.uint64), dev_out)
+
+
 def test_scan_pipelined_streams_equal_device(env, O):
     """bench.py's N > 1 step structure (dist.scan_pipelined: per-group scans on a compute stream,
     collectives on a comm stream) at world size 1 on the GPU == one bm_match over all queries."""
@@ -307,6 +328,55 @@ def test_hoisted_rotation_needs_its_keys(env, O):
     with pytest.raises(B.BMError) as e:
         B.bm_match(prm, evk_dev, dummy, 1, dummy, 1, dummy, dummy, order=2)
     assert e.value.name == "BM_ERR_MISSING_ROTATION_KEY"
+
+
+@pytest.mark.parametrize("d,nt,nq,chunk", [(16, 9000, 3, None), (16, 9000, 3, 4), (128, 300, 2, None),
+                                            (1024, 20, 1, None)])
+def test_degree2_output_parity(env, O, d, nt, nq, chunk):
+    """f2's relin-free degree-2 output (BM_ORDER_DEG2, p = d; R32): every
+    (query, set) result (d0, d1, d2) equals the oracle's match_deg2 bit for bit (3 sets with a ragged
+    last one at d = 16; chunked into 4-pair rectangles), decrypts with (1, s, s^2) to the float64 cosines
+    within 1e-5 (tests/test_oracle_ckks.py::test_deg2_scan_decrypts_with_s_squared derives it), with the
+    same top-1; the host-buffer pipeline returns the same rows."""
+    torch, B = env
+    with B.options(chunk_pairs=chunk or B.bm_get_option("chunk_pairs")):
+        _degree2_case(env, O, d, nt, nq)
+
+
+def _degree2_case(env, O, d, nt, nq):
+    torch, B = env
+    T = I.random_unit(nt, d, 81)
+    Q = T[[5, nt // 2, nt - 1][:nq]] + 0.01 * np.random.default_rng(82).standard_normal((nq, d))
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    st = Setup(env, O, d, d, T, Q)
+    got = st.gpu_match(B.ORDER_DEG2)
+    pairs = [(j, t) for j in range(st.nq) for t in range(st.n_sets)]
+    if len(pairs) > 6:
+        pairs = [pairs[0], pairs[len(pairs) // 2], pairs[-1]]
+    ref = st.oracle_pairs(pairs, 3)
+    for k, (j, t) in enumerate(pairs):
+        assert np.array_equal(got[j, t], ref[k]), (j, t)
+    sc = B.bm_decrypt_deg2(st.prm, st.sk, got).reshape(st.nq, -1)[:, :nt]
+    cos = Q @ T.T
+    assert np.abs(sc - cos).max() < 1e-5
+    assert np.array_equal(sc.argmax(1), cos.argmax(1))
+    h_q = st.d_q.cpu().numpy().view(np.uint64)
+    h_out = np.zeros((st.nq, st.n_sets, 3, 8192), np.uint64)
+    ws = torch.empty(B.bm_match_host_ws_bytes(st.prm, st.n_sets, st.nq, 3), dtype=torch.uint8, device="cuda")
+    B.bm_match_host(st.prm, None, st.d_db, st.n_sets, h_q, st.nq, h_out, ws, order=3)
+    assert np.array_equal(h_out, got)
+
+
+def test_degree2_output_needs_p_equal_d(env, O):
+    torch, B = env
+    prm = B.bm_params_init(128, 8)
+    dummy = torch.zeros(8 * 4 * 8192, dtype=torch.int64, device="cuda")
+    with pytest.raises(B.BMError) as e:
+        B.bm_match(prm, None, dummy, 1, dummy, 1, dummy, dummy, order=3)
+    assert e.value.name == "BM_ERR_INVALID_LAYOUT"
+    with pytest.raises(B.BMError) as e:          # the other orders still need their keys
+        B.bm_match(prm, None, dummy, 1, dummy, 1, dummy, dummy, order=0)
+    assert e.value.name == "BM_ERR_INVALID_ARG"
 
 
 @pytest.mark.parametrize("order,chunk", [(0, None), (0, 5), (2, None), (1, None)])
