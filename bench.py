@@ -63,7 +63,8 @@ def parse():
                     help="SURVEY.md sec. 8d C1..C5 = BASELINE.json configs[0..4]")
     ap.add_argument("--p", type=int, default=None, help="parts (default: the config's)")
     ap.add_argument("--nq", type=int, default=None, help="queries per batch (default: the config's)")
-    ap.add_argument("--order", type=int, default=0)
+    ap.add_argument("--order", type=int, default=0, choices=[0, 1, 2, 4],
+                    help="0 hoisted (product), 1 paper order, 2 f2 hoisted rotations, 4 f2 baby-step giant-step")
     ap.add_argument("--shard-of", type=int, default=None,
                     help="run rank r's shard of an S-way split (C5 default at N < 8: 8, a labelled prefix)")
     ap.add_argument("--ring-gib", type=float, default=4.0, help="device result ring (bounded outputs)")
@@ -92,16 +93,23 @@ def log(args, *a):
 
 
 # ----------------------------------------------------------------------------- algorithmic work
-def class_modmuls(p, log_s):
+def class_modmuls(p, log_s, order=0):
     """Algorithmic 64-bit modular multiplications per (query, set) pair, per kernel class
     (DESIGN.md "Algorithmic work"): butterflies of every transform + pointwise products."""
     n = N_RING
+    s = 1 << log_s
+    if order == 4 and log_s:    # f2 BSGS: two hoisted passes of b - 1 and g - 1 rotations (g = 1: one pass)
+        b = 1 << ((log_s + 1) // 2)
+        g = s // b
+        hrot = 6 * BFLY + 4 * n * (b - 1) + ((6 * BFLY + 4 * n * (g - 1)) if g > 1 else 0)
+    else:
+        hrot = (6 * BFLY + 4 * n * (s - 1)) if log_s else 0  # f2: 6 transforms + 4 products per rotation
     return {
         "tensor": 8 * n * p,                                       # a0b0, a1b1, (a0+a1)(b0+b1) per limb (+ adds)
         "digits": 6 * BFLY + n,                                    # INTT_q0, INTT_q1, NTT_q1, NTT_P x2, NTT_q0
         "relin": 6 * BFLY + 12 * n + 8 * n,                        # INTT_P, INTT_q1, NTT_q0 x 2 comps; rlk + scalings
         "ladder": (6 * BFLY + 6 * n) * log_s,                      # digit INTT_q0 + NTT_P, 2 x (INTT_P + NTT_q0)
-        "hrot": (6 * BFLY + 4 * n * ((1 << log_s) - 1)) if log_s else 0,  # f2: 6 transforms + 4 products per rotation
+        "hrot": hrot,
         "out_intt": 0 if log_s else 2 * BFLY,
     }
 
@@ -313,7 +321,7 @@ def run_ours(args):
     prm = B.bm_params_init(d, p)
     t_setup = time.perf_counter()
     sk, pk, evk = B.bm_keygen(prm, 1)                # deterministic: identical keys on every rank
-    if order == 2:                                   # f2 hoisted rotation sum: keys of every rotation
+    if order in (2, 4):                              # f2 hoisted / BSGS rotation sums: keys of every rotation
         B.bm_evk_add_hoisted(prm, 1, evk)
     pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
     n_local = W.n_local
@@ -482,7 +490,8 @@ def run_ours(args):
                                                  if W.split > world else ""),
                        "d": d, "p": p, "templates": W.n, "templates_this_run": n_tmpl_job, "queries": nq,
                        "sets": W.n_sets, "sets_per_gpu": n_local, "ring_N": N_RING,
-                       "order": ["hoisted", "paper", "hoisted-rotations (f2, not the paper ladder)"][order],
+                       "order": ["hoisted", "paper", "hoisted-rotations (f2, not the paper ladder)", "degree-2 (f2)",
+                                 "baby-step giant-step rotations (f2, not the paper ladder)"][order],
                        "parallelism": f"db-shard{world}", "gather": gather,
                        "query_groups": W.G, "group_queries": W.gq, "streams": nstr,
                        "output_ring": {"slots": R, "slot_bytes": slot_bytes},
@@ -521,7 +530,7 @@ def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws
     pms, pla, pun = B.bm_profile_read()
     B.bm_set_profiling(False)
     p = W.p
-    mm = class_modmuls(1 if order == 1 else p, prm.log_s)  # order 1 runs the part rounds one part each
+    mm = class_modmuls(1 if order == 1 else p, prm.log_s, order)  # order 1 runs the part rounds one part each
     rounds = p if order == 1 else 1
     pairs = n_local * W.nq
     per_class, step_work = {}, 0.0
@@ -639,7 +648,7 @@ def run_verify(args, B, torch, prm, sk, pk, evk_dev, d_db, d_q, Q, genuine, T_lo
     from oracle import oracle as O
     logN, d, p = 13, W.d, W.p
     osk, opk, orlk, ogk = O.keygen(logN, 1, O.n_rot_for(d, p))
-    if order == 2:
+    if order in (2, 4):
         ogk = O.keygen_hoisted(logN, 1, d // p)
     sets = sorted({t for _, t in sample})
     qs = sorted({j for j, _ in sample})

@@ -59,11 +59,15 @@ typedef enum {
     BM_ORDER_HOISTED_ROT = 2, /* f2, NOT the paper's ladder: BM_ORDER_HOISTED's C,
                                  then sum_{r<s} Rot(C, r) with ONE hoisted key switch (Halevi-Shoup):
                                  same decrypted scores, different residues; needs bm_evk_add_hoisted */
-    BM_ORDER_DEG2 = 3         /* f2, relin-free, p = d only (s = 1, no ladder):
+    BM_ORDER_DEG2 = 3,        /* f2, relin-free, p = d only (s = 1, no ladder):
                                  sum_i tensor_i rescaled by q1 component by component; the result is
                                  the DEGREE-2 ciphertext (d0, d1, d2) [nq][n_sets][3][N] (coefficients,
                                  scale out_scale), decrypted with (1, s, s^2) by bm_decrypt_deg2;
                                  evk unused (may be NULL); BM_ERR_INVALID_LAYOUT when p != d */
+    BM_ORDER_BSGS = 4         /* f2, NOT the paper's ladder: BM_ORDER_HOISTED's C,
+                                 then baby-step giant-step: sum_{j<g} Rot(sum_{i<b} Rot(C, i), j b),
+                                 b = 2^ceil(log2(s)/2), g = s/b, each sum one hoisted key switch; same
+                                 decrypted scores, its own residues; needs bm_evk_add_hoisted */
 } bm_order;
 
 /* Scheme parameters and the packing layout:

@@ -24,6 +24,7 @@ ORDER_HOISTED = 0
 ORDER_PAPER = 1
 ORDER_HOISTED_ROT = 2   # f2: hoisted rotation sum, not the paper's ladder
 ORDER_DEG2 = 3          # f2: relin-free degree-2 output (p = d), [nq][n_sets][3][N]; bm_decrypt_deg2
+ORDER_BSGS = 4          # f2: baby-step giant-step rotation sum (hoisted keys), not the paper's ladder
 
 BM_OK = 0
 ERRORS = {

@@ -180,7 +180,8 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_c3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
-    cudaFuncSetAttribute(k_hrot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
+    cudaFuncSetAttribute(k_hrot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
+    cudaFuncSetAttribute(k_hrot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
     set_smem(k_encrypt);
     cudaFuncSetAttribute(k_exp_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X1_SMEM_BYTES);
     cudaFuncSetAttribute(k_rot1_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
@@ -1066,12 +1067,14 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
 {
     const bool deg2 = order == BM_ORDER_DEG2;
     if (!prm || (!evk && !deg2) || n_sets < 0 || nq < 0 ||
-        (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT && !deg2))
+        (order != BM_ORDER_HOISTED && order != BM_ORDER_PAPER && order != BM_ORDER_HOISTED_ROT &&
+         order != BM_ORDER_BSGS && !deg2))
         return BM_ERR_INVALID_ARG;
     if (deg2 && prm->s != 1) return BM_ERR_INVALID_LAYOUT; // the degree-2 output has no ladder: p = d only
     if (evk && memcmp(evk->digest, prm->digest, 32)) return BM_ERR_KEY_MISMATCH;
-    if (!deg2 && order != BM_ORDER_HOISTED_ROT && evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
-    if (order == BM_ORDER_HOISTED_ROT && evk->n_hrot < prm->s - 1) return BM_ERR_MISSING_ROTATION_KEY;
+    const bool hoisted_rot = order == BM_ORDER_HOISTED_ROT || order == BM_ORDER_BSGS;
+    if (!deg2 && !hoisted_rot && evk->n_rot < prm->log_s) return BM_ERR_MISSING_ROTATION_KEY;
+    if (hoisted_rot && evk->n_hrot < prm->s - 1) return BM_ERR_MISSING_ROTATION_KEY;
     const int64_t total = n_sets * (int64_t)nq;
     if (total == 0) return BM_OK;
     if (!d_db || !d_q || (!d_out && !d_rows) || !d_ws || set_offset < 0) return BM_ERR_INVALID_ARG;
@@ -1175,9 +1178,22 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             end();
             rc = launch_check();
         }
-        if (log_s > 0 && !rc && order == BM_ORDER_HOISTED_ROT) {
-            beg(5, 6 * np);
-            k_hrot<<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufC, evk->hgk, prm->s);
+        if (log_s > 0 && !rc && hoisted_rot) {
+            // BM_ORDER_HOISTED_ROT: one hoisted sum of s rotations; BM_ORDER_BSGS: b = 2^ceil(log2(s)/2)
+            // baby rotations (NTT-domain result in XU) then g = s / b giant ones by b (the oracle's
+            // bsgs_rot_sum; g = 1 is the plain hoisted sum)
+            const int b = order == BM_ORDER_BSGS ? 1 << ((log_s + 1) / 2) : prm->s, g = prm->s / b;
+            const CtBuf bufU{K.XU, 4 * N};
+            uint32_t gb = 1;
+            for (int i = 0; i < b; i++) gb = (gb * 5u) & (2 * N - 1);
+            beg(5, 6 * np * (g > 1 ? 2 : 1));
+            if (g > 1) {
+                k_hrot<true><<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufC, evk->hgk, b, 1, 5u, bufU);
+                counted();
+                k_hrot<false><<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufU, evk->hgk, g, b, gb, bufC);
+            } else {
+                k_hrot<false><<<npu, T, HROT_SMEM_BYTES, s>>>(K, bufC, evk->hgk, b, 1, 5u, bufC);
+            }
             counted();
             end();
             rc = launch_check();

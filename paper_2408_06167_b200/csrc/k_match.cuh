@@ -998,9 +998,16 @@ __global__ void __launch_bounds__(T, 1) k_ladder_c3(MatchK K, CtBuf cin, int L)
 //   then one ModDown per component straight to the coefficient-domain output:
 //   out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c,  y^c = centred_P(INTT_P(A[c][P])),
 //   base_0 = sum_{r<s} sigma_r(c0), base_1 = c1.   6 transforms per pair (the ladder: 6 log2 s).
+// Generalised for the baby-step giant-step variant (BM_ORDER_BSGS): the n rotations by i * step,
+// i < n (key of rotation r at hgk[r - 1]; g_step = 5^step mod 2N); NTT_OUT: the result stays in the
+// NTT domain, canonical, in nout (the giant pass's input) -- per component
+//   out_c = base_c + A[c][q0] - NTT_q0(P^-1 y^c)   (= NTT_q0 of the coefficient form, exactly)
+// with the same transform count (NTT_q0 of P^-1 y^c in place of INTT_q0 of the sum).
 constexpr size_t HROT_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
 
-__global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int s)
+template <bool NTT_OUT>
+__global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64_t *hgk, int n, int step,
+                                               uint32_t g_step, CtBuf nout)
 {
     extern __shared__ uint64_t sm[];
     // XB: transform exchanges; SX: (c1, X~P) pairs in natural order (one 16-byte gather per rotation)
@@ -1031,21 +1038,36 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
             inv<2>(a, XB, K.pr[2]); // y^c (canonical [0, P))
 #pragma unroll
             for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
-            tmem_st16(tA + 32 * (2 * c + 1), a); // P^-1 y^c (coefficient j_M1(tid, e)) over A[c][P]
-            const uint64_t *base = c ? cin.at(pi, 1) : b0s;
+            if (!NTT_OUT) {
+                tmem_st16(tA + 32 * (2 * c + 1), a); // P^-1 y^c (coefficient j_M1(tid, e)) over A[c][P]
+                const uint64_t *base = c ? cin.at(pi, 1) : b0s;
 #pragma unroll
-            for (int e = 0; e < E; e += 2) {
-                const int pos = pos_M4(tid, e);
-                const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
-                a[e] = bv.x;
-                a[e + 1] = bv.y;
-            }
-            {
+                for (int e = 0; e < E; e += 2) {
+                    const int pos = pos_M4(tid, e);
+                    const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
+                    a[e] = bv.x;
+                    a[e + 1] = bv.y;
+                }
                 uint64_t av[E];
                 tmem_ld16(tA + 32 * (2 * c), av); // A[c][q0]
 #pragma unroll
                 for (int e = 0; e < E; e++) a[e] = csub(a[e] + av[e], Q0);
             }
+        }
+        if (NTT_OUT && ph > 0) { // out_c = base_c + A[c][q0] - NTT_q0(P^-1 y^c), NTT domain, canonical
+            fwd<0, false>(a, XB, K.pr[0]); // lazy [0, 2 q0)
+            const uint64_t *base = c ? cin.at(pi, 1) : b0s;
+            uint64_t *o = nout.at(pi, c);
+            uint64_t av[E];
+            tmem_ld16(tA + 32 * (2 * c), av); // A[c][q0]
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                const int pos = pos_M4(tid, e);
+                const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(base + pos);
+                const uint64_t x0 = csub(bv.x + av[e], Q0), x1 = csub(bv.y + av[e + 1], Q0);
+                st2(o + pos, submod_d(x0, csub(a[e], Q0), Q0), submod_d(x1, csub(a[e + 1], Q0), Q0));
+            }
+            continue;
         }
         inv<0>(a, XB, K.pr[0]);
         if (ph > 0) { // out_c = INTT_q0(base_c + A[c][q0]) - P^-1 y^c
@@ -1074,14 +1096,14 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
                 for (int v = 0; v < 4; v++) A[u][v] = 0;
             ulonglong2 kc[4], kn[4];
 #pragma unroll
-            for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + (size_t)v * N + pos);
+            for (int v = 0; v < 4; v++) kc[v] = ld2(hgk + ((size_t)(step - 1) * 4 + v) * N + pos);
             uint32_t gr = 1;
 #pragma unroll 1
-            for (int r = 1; r < s; r++) {
-                gr = (gr * 5u) & (2 * N - 1); // 5^r mod 2N
-                if (r + 1 < s) {
+            for (int r = 1; r < n; r++) {
+                gr = (gr * g_step) & (2 * N - 1); // 5^(r step) mod 2N
+                if (r + 1 < n) {
 #pragma unroll
-                    for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)r * 4 + v) * N + pos);
+                    for (int v = 0; v < 4; v++) kn[v] = ld2(hgk + ((size_t)((r + 1) * step - 1) * 4 + v) * N + pos);
                 }
                 const ulonglong2 x0 = SX[nat_auto_i(i0, gr)], x1 = SX[nat_auto_i(i1, gr)];
 #pragma unroll
@@ -1113,7 +1135,7 @@ __global__ void __launch_bounds__(T, 1) k_hrot(MatchK K, CtBuf cin, const uint64
         BM_SYNCTHREADS();
         stage_nat(SP, cin.at(pi, 0));
 #pragma unroll 1
-        for (uint32_t g = 5, w = 1; w < (uint32_t)s; w <<= 1, g = (g * g) & (2 * N - 1)) {
+        for (uint32_t g = g_step, w = 1; w < (uint32_t)n; w <<= 1, g = (g * g) & (2 * N - 1)) {
             BM_SYNCTHREADS();
 #pragma unroll
             for (int e = 0; e < E; e++) {

@@ -87,7 +87,7 @@ class Setup:
             out, _ = self.O.match_deg2(LOGN, self.d, self.p, self.oracle_db(ts), self.oracle_q(qs), pairs=local,
                                        n_threads=NTH)
             return out.reshape(-1, 3, 8192)
-        gk = self.ohgk if order == 2 else self.ogk
+        gk = self.ohgk if order in (2, 4) else self.ogk
         out, _ = self.O.match(LOGN, self.d, self.p, order, self.orlk, gk, self.oracle_db(ts), self.oracle_q(qs),
                               pairs=local, n_threads=NTH)
         return out.reshape(-1, 2, 8192)
@@ -296,18 +296,21 @@ def test_config2_full_size_bench_launch(env, O):
 
 
 # ----------------------------------------------------------------------------- f2: hoisted rotation sum
-@pytest.mark.parametrize("d,p,nt", [(16, 1, 256), (128, 8, 6144), (128, 1, 700), (4096, 8, 20)])
-def test_hoisted_rotation_order_parity(env, O, d, p, nt):
-    """BM_ORDER_HOISTED_ROT (f2; not the paper's ladder): bit-exact vs the oracle's
-    hoisted_rot_sum on sampled pairs, scores vs float64 cosine, and the same top-1 as the ladder.
-    s = 16, 16, 128 and 512 (the 128-bit sums are folded every 64 rotations)."""
+@pytest.mark.parametrize("order", [2, 4])
+@pytest.mark.parametrize("d,p,nt", [(16, 1, 256), (128, 8, 6144), (128, 1, 700), (4096, 8, 20), (64, 32, 300),
+                                    (64, 16, 300)])
+def test_hoisted_rotation_order_parity(env, O, d, p, nt, order):
+    """BM_ORDER_HOISTED_ROT / BM_ORDER_BSGS (f2; not the paper's ladder): bit-exact
+    vs the oracle's hoisted_rot_sum / bsgs_rot_sum on sampled pairs, scores vs float64 cosine, and the
+    same top-1 as the ladder.  s = 16, 16, 128, 512 (the 128-bit sums are folded every 64 rotations),
+    2 (BSGS: b = 2, g = 1, one pass) and 4 (b = g = 2)."""
     torch, B = env
     T = I.templates(1) if d == 16 else (I.templates(2, nt) if d == 128 else I.random_unit(nt, d, 3))
     Q = I.queries(1)[0] if d == 16 else (I.queries(2, 3)[0] if d == 128 else I.random_unit(1, d, 4))
     st = Setup(env, O, d, p, T, Q, hoisted=True)
-    got = st.gpu_match(2)
+    got = st.gpu_match(order)
     pairs = [(0, st.n_sets - 1)] + ([(Q.shape[0] - 1, 0)] if st.n_sets > 1 or Q.shape[0] > 1 else [])
-    ref = st.oracle_pairs(pairs, 2)
+    ref = st.oracle_pairs(pairs, order)
     for k, (j, t) in enumerate(pairs):
         assert np.array_equal(got[j, t], ref[k]), (j, t)
     sc = B.bm_decrypt(st.prm, st.sk, got.reshape(-1, 2, 1, 8192)).reshape(Q.shape[0], -1)[:, :T.shape[0]]
@@ -379,7 +382,7 @@ def test_degree2_output_needs_p_equal_d(env, O):
     assert e.value.name == "BM_ERR_INVALID_ARG"
 
 
-@pytest.mark.parametrize("order,chunk", [(0, None), (0, 5), (2, None), (1, None)])
+@pytest.mark.parametrize("order,chunk", [(0, None), (0, 5), (2, None), (4, None), (1, None)])
 def test_match_rows_fused_gather(env, O, order, chunk):
     """bm_match_rows (a8 fused into the output kernels, the multi-GPU gather path of dist.P2PGather):
     results land in caller-given rows at global set numbers.  Rows in reversed order inside a wider
@@ -392,7 +395,7 @@ def test_match_rows_fused_gather(env, O, order, chunk):
         B.bm_set_option("chunk_pairs", chunk)
     T = I.random_unit(700, 64, 21)
     Q = I.random_unit(3, 64, 22)
-    st = Setup(env, O, 64, 4, T, Q, hoisted=(order == 2))   # s = 16, B = 256 -> 3 sets
+    st = Setup(env, O, 64, 4, T, Q, hoisted=(order in (2, 4)))   # s = 16, B = 256 -> 3 sets
     ref = st.gpu_match(order)
     n_glob, off = st.n_sets + 3, 2
     res = torch.full((st.nq, n_glob, 2, 8192), -1, dtype=torch.int64, device="cuda")

@@ -7,7 +7,8 @@ sanitizers"; diagnostic, not a test).  Usage on the GPU box:
 
 Legs: configs[0] (1 pair: the 3-CTA pipelined latency ladder k_ladder_c3 + swapped tensor tiles),
 the 2-CTA latency ladder (k_ladder_t<true>), a launch of n_SM + 12 pairs (full waves on
-k_ladder_t<false> + the cluster tail from MatchK::pair0), f2's k_hrot, the paper order (k_relin
+k_ladder_t<false> + the cluster tail from MatchK::pair0), f2's k_hrot (hoisted and BSGS), f2's
+degree-2 output (k_rescale_deg2), the paper order (k_relin
 accumulating), s = 1 (k_out_intt), f3 bm_expand, f4 bm_enroll, f1 bm_match_cmp, device decryption.
 """
 import os
@@ -28,7 +29,7 @@ dev = torch.device("cuda")
 def scan(d, p, n_tmpl, nq, order=0, **opts):
     prm = B.bm_params_init(d, p)
     sk, pk, evk = B.bm_keygen(prm, 1)
-    if order == 2:
+    if order in (2, 4):
         B.bm_evk_add_hoisted(prm, 1, evk)
     pk_dev, evk_dev = B.bm_pk_to_device(prm, pk), B.bm_evk_to_device(prm, evk)
     n_sets = -(-n_tmpl // prm.B)
@@ -48,6 +49,25 @@ def scan(d, p, n_tmpl, nq, order=0, **opts):
     err = float((sc.view(nq, -1)[:, :n_tmpl].cpu() - torch.from_numpy(Q @ T.T)).abs().max())
     print(f"scan d={d} p={p} pairs={n_sets * nq} order={order} {opts}: max err {err:.2e}", flush=True)
     return prm, sk, pk, evk_dev
+
+
+def deg2():
+    d = p = 32
+    prm = B.bm_params_init(d, p)
+    sk, pk, evk = B.bm_keygen(prm, 1)
+    pk_dev = B.bm_pk_to_device(prm, pk)
+    T = I.random_unit(5000, d, 8)
+    Q = I.random_unit(2, d, 9)
+    d_db = torch.empty((2, p, 2, 2, N), dtype=torch.int64, device=dev)
+    d_q = torch.empty((2, p, 2, 2, N), dtype=torch.int64, device=dev)
+    B.bm_encrypt_db(prm, pk_dev, T, 0, 2, 2, d_db)
+    B.bm_encrypt_query(prm, pk_dev, Q, 0, 3, d_q)
+    out = torch.empty((2, 2, 3, N), dtype=torch.int64, device=dev)
+    ws = torch.empty(B.bm_match_ws_bytes(prm, 2, 2, B.ORDER_DEG2), dtype=torch.uint8, device=dev)
+    B.bm_match(prm, None, d_db, 2, d_q, 2, out, ws, B.ORDER_DEG2)
+    B.bm_sync()
+    sc = B.bm_decrypt_deg2(prm, sk, out.cpu().numpy().view(np.uint64)).reshape(2, -1)[:, :5000]
+    print(f"f2 degree-2 output: max err {np.abs(sc - Q @ T.T).max():.2e}", flush=True)
 
 
 def next_rows():
@@ -99,6 +119,8 @@ def main():
         return
     scan(16, 8, (n_sm + 12) * 2048 - 100, 1)             # one-CTA waves + the cluster tail
     scan(128, 8, 700, 3, order=2)                        # k_hrot
+    scan(128, 8, 700, 3, order=4)                        # k_hrot<true> + k_hrot<false> (BSGS)
+    deg2()                                               # k_rescale_deg2
     scan(128, 8, 700, 3, order=1)                        # paper order (k_relin accumulates)
     scan(16, 16, 300, 2)                                 # s = 1: k_out_intt
     next_rows()
