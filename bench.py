@@ -534,9 +534,15 @@ def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws
     rounds = p if order == 1 else 1
     pairs = n_local * W.nq
     per_class, step_work = {}, 0.0
+    # relin and ladder: the library counts the transforms it ran (component 0 split for the one-CTA
+    # ladder: one transform fewer in K3 and in every ladder step but the last)
+    pointwise = {"relin": 20 * N_RING, "ladder": 6 * N_RING * prm.log_s}
     for i, c in enumerate(B.PROFILE_CLASSES):
         if pla[i]:
-            work = mm[c] * pairs * nsteps * (rounds if i < 3 else 1)
+            if c in pointwise and order in (0, 1):
+                work = pun[i] * BFLY + pointwise[c] * pairs * nsteps * (rounds if i < 3 else 1)
+            else:
+                work = mm[c] * pairs * nsteps * (rounds if i < 3 else 1)
             step_work += work / nsteps
             per_class[c] = {"ms_per_step": pms[i] / nsteps, "launches": int(pla[i]),
                             "ms_per_launch": pms[i] / pla[i], "gmodmul_s": work / (pms[i] / 1e3) / 1e9,

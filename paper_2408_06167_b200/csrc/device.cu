@@ -178,6 +178,7 @@ int ctx_get(DevCtx **out)
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_rescale_deg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K7_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
+    cudaFuncSetAttribute(k_ladder_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_ladder_c3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LADDER_SMEM_BYTES);
     cudaFuncSetAttribute(k_hrot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HROT_SMEM_BYTES);
@@ -1153,6 +1154,20 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         const unsigned ntiles = (unsigned)(((na + TQB - 1) / TQB) * ((nb + TSB - 1) / TSB) * (N / CS / (tswap ? 1 : TSL)));
         const bool per_part = order == BM_ORDER_PAPER;
         const int n_rounds = per_part ? prm->p : 1;
+        // the ladder's launch plan (see below): pairs [0, n_one) on the one-CTA kernel, the rest on clusters
+        const bool c2ok = opt(BM_OPT_LADDER_C2) != 0, c3ok = opt(BM_OPT_LADDER_C3) != 0;
+        const int64_t tail = np % C->n_sm;
+        const bool fits = c2ok && C->max_cl[2] > 0;
+        const bool all_cl = fits && np <= C->max_cl[2] && 2 * np <= C->n_sm;
+        const bool tail_cl = !all_cl && fits && opt(BM_OPT_LADDER_TAIL) && np > C->n_sm && tail > 0 &&
+                             2 * tail <= C->n_sm && tail <= C->max_cl[2];
+        const int64_t n_one = all_cl ? 0 : tail_cl ? np - tail : np;
+        // K3 leaves component 0 split (two accumulators) for the pairs the one-CTA ladder takes
+#ifdef BM_K3_NO_SPLIT
+        K.split_lim = 0;
+#else
+        K.split_lim = (LADDER_SPLIT_C0 && log_s > 0 && !hoisted_rot && !per_part && !deg2) ? n_one : 0;
+#endif
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = per_part ? r : 0, hi = per_part ? r + 1 : prm->p;
             beg(0, 2 * np);
@@ -1172,7 +1187,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             k_digits<<<2 * npu, T, K2_SMEM_BYTES, s>>>(K);
             counted();
             end();
-            beg(2, 6 * np);
+            beg(2, 6 * np - K.split_lim); // transforms: one fewer for each split component 0
             k_relin<<<2 * npu, T, K3_SMEM_BYTES, s>>>(K, bufC, r > 0 ? 1 : 0);
             counted();
             end();
@@ -1198,7 +1213,8 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             end();
             rc = launch_check();
         } else if (log_s > 0 && !rc) {
-            beg(4, 6 * log_s * np);
+            // transforms: 6 per step, 5 in the one-CTA kernel's steps but the last (component 0 split)
+            beg(4, 6 * log_s * np - (LADDER_SPLIT_C0 ? (log_s - 1) * n_one : 0));
             // latency mode: at most n_SM / 2 pairs -> a 2-CTA cluster per pair (k_ladder_t<true>),
             // at most n_SM / 3 -> the 3-rank pipelined ladder (k_ladder_c3).  A large launch whose pair
             // count is not a multiple of n_SM runs its partial last wave the same way: the one-CTA
@@ -1206,11 +1222,11 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
             // the cluster paths are used only while their clusters fit the device at once
             // (DevCtx::max_cl, from cudaOccupancyMaxActiveClusters); a failed cluster launch falls
             // back to the one-CTA ladder for the same pairs (identical residues)
-            const bool c2ok = opt(BM_OPT_LADDER_C2) != 0, c3ok = opt(BM_OPT_LADDER_C3) != 0;
             auto one_cta = [&](int64_t p0, int64_t n) {
                 MatchK Kt = K;
                 Kt.pair0 = p0;
-                k_ladder_t<false><<<(unsigned)n, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
+                if (p0 + n <= K.split_lim) k_ladder_t<false, true><<<(unsigned)n, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
+                else k_ladder_t<false><<<(unsigned)n, T, LADDER_SMEM_BYTES, s>>>(Kt, bufC, log_s);
                 counted();
             };
             auto cluster_ladder = [&](int64_t p0, int64_t n) {
@@ -1234,18 +1250,16 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
                 if (e != cudaSuccess) {
                     cudaGetLastError(); // not sticky: a launch-configuration error
                     one_cta(p0, n);
+                    if (prof && LADDER_SPLIT_C0) recs.back().units -= (log_s - 1) * n;
                 } else {
                     counted();
                 }
             };
-            const int64_t tail = np % C->n_sm;
-            const bool fits = c2ok && C->max_cl[2] > 0;
-            if (fits && np <= C->max_cl[2] && 2 * np <= C->n_sm) {
+            if (all_cl) {
                 cluster_ladder(0, np);
-            } else if (fits && opt(BM_OPT_LADDER_TAIL) && np > C->n_sm && tail > 0 && 2 * tail <= C->n_sm &&
-                       tail <= C->max_cl[2]) {
-                one_cta(0, np - tail);
-                cluster_ladder(np - tail, tail);
+            } else if (tail_cl) {
+                one_cta(0, n_one);
+                cluster_ladder(n_one, tail);
             } else {
                 one_cta(0, np);
             }

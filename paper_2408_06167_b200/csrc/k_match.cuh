@@ -31,6 +31,9 @@ struct MatchK {
     int64_t set_off = 0;
     int64_t pair0 = 0; // the ladder kernels' first pair (a launch may cover only the chunk's tail)
     int64_t nq_total = 0; // queries of the whole call (debug bounds checks)
+    // pairs pi < split_lim leave K3 with component 0 split for the throughput ladder (coef_acc_update):
+    // the NTT-domain part in the ciphertext buffer, the coefficient-domain part over D01[pi][0][q1]
+    int64_t split_lim = 0;
     BM_D uint64_t *out_at(int64_t pi, int c) const
     {
         BM_CHECK(pi >= 0 && pi < (int64_t)cq * ct && jq0 + pi / ct < nq_total && t0 + pi % ct < n_sets);
@@ -541,10 +544,29 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
         a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
     }
-    fwd<0, false>(a, sm, K.pr[0]); // A, in [0, 2 q0)
-    // ---- q0 limb and output
     const ulonglong2 q1inv = K.q1inv;
     uint64_t *co = dst.at(pi, c);
+    if (c == 0 && pi < K.split_lim) {
+        // component 0 for the throughput ladder, split (k_ladder_t<false>, coef_acc_update): the NTT_q0 of
+        // A is not needed -- C0 = q1^-1 (d0 + P^-1 KS0[q0]) (NTT domain) + q1^-1 (-A) (coefficient domain,
+        // M1 order, lazily in [0, 2 q0)), the latter written over d_0[q1] (read only by this CTA, and
+        // only before inv_f's barriers)
+        uint64_t *ai = K.D01 + ((size_t)pi * 4 + 1) * N;
+#pragma unroll
+        for (int e = 0; e < E; e++) ai[j_M1(tid, e)] = reduce_lazy<0>(shoup4<0>(6 * Q0 - a[e], q1inv));
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            const int j = pos_M4(tid, e);
+            const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
+            const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
+            const uint64_t ka = red128s<0>(dot2(u.x, w0.x, v.x, w1.x), K.pr[0].r64);
+            const uint64_t kb = red128s<0>(dot2(u.y, w0.y, v.y, w1.y), K.pr[0].r64);
+            st2(co + j, reduce_bnd<0>(shoup4<0>(dd.x + ka, q1inv)), reduce_bnd<0>(shoup4<0>(dd.y + kb, q1inv)));
+        }
+        return;
+    }
+    fwd<0, false>(a, sm, K.pr[0]); // A, in [0, 2 q0)
+    // ---- q0 limb and output
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
@@ -665,8 +687,15 @@ BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
 // no centring reduction)
 // The last step leaves the NTT domain directly (INTT is linear, the rounding term y^c is already
 // in coefficient form): out_c = INTT_q0(c_c + [c = 0] sigma(c0) + P^-1 sigma(c1) gk[c][q0])
-// - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.
+// - P^-1 y^c, i.e. 6 transforms per step and none for the output conversion.  The throughput mode
+// (k_ladder_t<false>) keeps c0 as two accumulators (coef_acc_update): 5 transforms per step, 6 in the
+// last one.
 constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
+#ifdef BM_LADDER_NO_SPLIT_C0
+constexpr bool LADDER_SPLIT_C0 = false;
+#else
+constexpr bool LADDER_SPLIT_C0 = true;
+#endif
 
 
 // Latency mode (k_ladder_t<true>): when a launch has fewer pairs than half the SMs (a single query
@@ -703,7 +732,66 @@ BM_D const uint64_t *cluster_peer(const uint64_t *p, uint32_t rank)
     return reinterpret_cast<const uint64_t *>(g);
 }
 
-template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, CtBuf cin, int L)
+BM_D void tmem_ld8(uint32_t taddr, uint64_t v[8]) // 16 columns -> 8 u64 (waits)
+{
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15])
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15])
+                 :
+                 : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; i++) v[i] = (uint64_t)r[2 * i] | ((uint64_t)r[2 * i + 1] << 32);
+}
+
+// Component 0's coefficient-domain accumulator of the throughput ladder (k_ladder_t<false>).  c0 never
+// feeds the digit, and every operation on it is linear mod q0 and commutes with the NTT (sigma_g is a
+// permutation of the evaluations and a signed permutation X^j -> +-X^(j g mod N) of the coefficients), so
+//   c0_L = INTT_q0(S0) + A,  S0 <- S0 + sigma(S0) + sigma(c1) P^-1 gk0[q0]   (NTT domain, pointwise)
+//                            A  <- A + sigma(A) - P^-1 y^0                  (coefficient domain)
+// gives the same residues as c0 <- c0 + sigma(c0) + sigma(c1) P^-1 gk0[q0] - NTT_q0(P^-1 y^0) with
+// one transform less per step (the NTT_q0 of P^-1 y^0; the output's INTT_q0 is needed anyway).
+// A lives in TMEM (this thread's coefficients j_M1(tid, e), lazily in [0, 2 q0)); sigma(A) is a scatter
+// through the exchange buffer.  py: P^-1 y^0 (< 5 q0) in M1 order; first: A = 0 before this step.
+BM_D void coef_acc_update(const uint64_t py[E], uint64_t *XB, uint32_t tacc, uint32_t g, bool first)
+{
+    const int tid = threadIdx.x;
+    uint64_t t[E];
+    if (first) {
+#pragma unroll
+        for (int e = 0; e < E; e++) t[e] = reduce_lazy<0>(5 * Q0 - py[e]);
+    } else {
+        BM_SYNCTHREADS(); // the transform's last reads of XB are done
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            uint64_t v[8];
+            tmem_ld8(tacc + 16 * h, v);
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const uint32_t j = (uint32_t)j_M1(tid, 8 * h + e);
+                const uint32_t u = (j * g) & (2 * N - 1); // X^j -> X^(j g mod 2N) = -X^(u - N) for u >= N
+                BM_CHECK(pidx((int)(u & (N - 1))) < SMEM_WORDS);
+                XB[pidx((int)(u & (N - 1)))] = (u & N) ? 2 * Q0 - v[e] : v[e]; // (0, 2 q0]
+                t[8 * h + e] = v[e] + 5 * Q0 - py[8 * h + e];                  // < 7 q0
+            }
+        }
+        BM_SYNCTHREADS();
+#pragma unroll
+        for (int e = 0; e < E; e++) t[e] = reduce_lazy<0>(t[e] + XB[pidx(j_M1(tid, e))]); // < 9 q0
+    }
+    tmem_st16(tacc, t);
+}
+
+// ACC (throughput mode only): every pair of the launch comes from K3 with component 0 split (pi < split_lim)
+template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, CtBuf cin, int L)
 {
     extern __shared__ uint64_t sm[];
     uint64_t *XB = sm, *S0 = sm + SMEM_WORDS, *S1 = sm + 2 * SMEM_WORDS;
@@ -714,12 +802,23 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
     const int64_t pi = K.pair0 + (CL ? blockIdx.x >> 1 : blockIdx.x);
     __shared__ uint32_t s_tmem;
     const uint32_t tks1 = tmem_alloc<256>(&s_tmem), ttsc = tks1 + 32; // TMEM scratch (see tmem_alloc)
+    // component 0's coefficient-domain accumulator (throughput mode); it shares ttsc's columns: ttsc is
+    // written only by component 1 of the last step, after component 0 has read the accumulator
+    const uint32_t tacc = ttsc;
     const ulonglong2 pinv = K.pinv[0];
     const int nt = nat_tid(tid); // S0, S1 in natural order (nat_at / nat_auto: conflict-free)
     if (!CL || rank == 0) stage_nat(S0, cin.at(pi, 0));
     if (!CL || rank == 1) stage_nat(S1, cin.at(pi, 1));
     const uint64_t *peer_c1 = CL && rank == 0 ? cluster_peer(S1, 1) : nullptr;
     uint64_t a[E];
+    // component 0 split by K3 (coef_acc_update): its coefficient-domain part starts the accumulator
+    static_assert(!(CL && ACC), "the cluster ladders take component 0 unsplit");
+    constexpr bool have_acc = ACC;
+    BM_CHECK(!ACC || pi < K.split_lim);
+    if (have_acc) {
+        load_coef(a, K.D01 + ((size_t)pi * 4 + 1) * N);
+        tmem_st16(tacc, a);
+    }
     uint32_t g = 5; // 5^(2^i) mod 2N
 #pragma unroll 1
     for (int i = 0; i < L; i++, g = (g * g) & (2 * N - 1)) {
@@ -782,6 +881,34 @@ template <bool CL> __global__ void __launch_bounds__(T, 1) k_ladder_t(MatchK K, 
             for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
             uint64_t *S = c ? S1 : S0;
             const uint64_t *gq = c ? gq1 : gq0;
+#ifndef BM_LADDER_NO_SPLIT_C0
+            if (!CL && c == 0) {
+                // component 0 in two accumulators (coef_acc_update): the coefficient-domain part takes
+                // (1 + sigma_g) and - P^-1 y^0; the NTT-domain part S0 takes only the pointwise terms
+                coef_acc_update(a, XB, tacc, g, i == 0 && !have_acc);
+                ulonglong2 kk[2];
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int j = nat_at(nt, e), jp = nat_auto(nt, e, g);
+                    if (!(e & 1)) ldkey2(gq, pos_M4(tid, e), kk[0], kk[1]);
+                    const uint64_t ks = shoup4<0>(S1[jp], kk[e & 1]); // [0, 4 q0)
+                    a[e] = reduce_lazy<0>(ks + S0[j] + S0[jp]);       // < 8 q0 -> [0, 2 q0)
+                }
+                if (!last) {
+                    BM_SYNCTHREADS(); // every read of the old c0 is done
+#pragma unroll
+                    for (int e = 0; e < E; e++) S0[nat_at(nt, e)] = a[e];
+                } else {
+                    inv<0>(a, XB, K.pr[0]); // canonical
+                    uint64_t *o = K.out_at(pi, 0);
+                    uint64_t t[E];
+                    tmem_ld16(tacc, t); // [0, 2 q0)
+#pragma unroll
+                    for (int e = 0; e < E; e++) o[j_M1(tid, e)] = reduce_bnd<0>(a[e] + t[e]);
+                }
+                continue;
+            }
+#endif
             if (!last) {
                 fwd<0, false>(a, XB, K.pr[0]); // NTT_q0(P^-1 y^c), lazy [0, 2 q0)
                 ulonglong2 kk[2];
