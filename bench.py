@@ -83,6 +83,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row legs (f1, f3, f4 on configs[1])")
     ap.add_argument("--opt", action="append", default=[],
                     help="library option NAME=VALUE (bm.OPTIONS; A/B runs only, the defaults are the product)")
+    ap.add_argument("--no-tc", action="store_true",
+                    help="do not register the DB in the tensor-core layout (K1 on the CUDA cores; A/B runs)")
     ap.add_argument("--quiet", action="store_true")
     return ap.parse_args()
 
@@ -333,6 +335,12 @@ def run_ours(args):
         pt = torch.from_numpy(B.bm_encode_db(prm, T_local, 0, n_local).reshape(-1, N_RING)).to(dev)
         B.bm_encrypt(prm, pk_dev, pt, W.lo * p, 2, d_db)
         del pt
+    # server-side enrollment of the DB into the tensor-core layout (K1 on tcgen05):
+    # part of the DB's setup like its encryption, outside the timed region
+    d_dbp = None
+    if n_local and not args.no_tc and B.bm_db_tc_bytes(prm, n_local):
+        d_dbp = torch.empty(B.bm_db_tc_bytes(prm, n_local), dtype=torch.uint8, device=dev)
+        B.bm_db_tc_register(prm, d_db, n_local, d_dbp)
     Q, genuine = I.queries(W.cfg, nq)
     d_q = torch.zeros((nq, p, 2, 2, N_RING), dtype=torch.int64, device=dev)
     if rank == 0:
@@ -503,6 +511,8 @@ def run_ours(args):
             "clocks": clocks,
             "setup_s": round(t_setup, 1),
         }
+        line["config"]["k1"] = ("tensor cores (tcgen05.mma kind::i8, DB registered in the tensor-core layout)"
+                                if d_dbp is not None and "tensor_mma=0" not in args.opt else "CUDA cores")
         if args.opt:
             line["config"]["options"] = args.opt
         line.update(extras)

@@ -253,6 +253,21 @@ int bm_match_host_ring(const bm_params *, const bm_evk_dev *, const uint64_t *d_
                        const uint64_t *h_q, int32_t nq, uint64_t *h_ring, int32_t ring_rows, void *d_ws,
                        size_t ws_bytes, int32_t order, void *stream);
 
+/* The DB in the tensor-core layout (server-side enrollment step for K1 on the tcgen05 tensor cores,
+ * DESIGN.md sec. 3 "K1 on the tensor cores"; the tensor of PAPER.md:327-328 as a u8 x u8 -> s32 GEMM per
+ * coefficient).  bm_db_tc_register packs d_db [n_sets][p][2][2][N] (device storage order) into the
+ * caller-owned device buffer d_packed (>= bm_db_tc_bytes bytes; 128-set tiles, per limb and coefficient one
+ * contiguous 128 x 16 p-byte block) on `stream` and records the pair: from then on bm_match / bm_match_rows /
+ * bm_match_host* calls with this d_db (same n_sets and p) compute the tensor on the tensor cores (results
+ * identical).  The caller keeps d_db unchanged and d_packed allocated while registered (register again
+ * after changing d_db; registering a d_db again replaces its entry); bm_db_tc_unregister forgets it
+ * (BM_ERR_INVALID_ARG if it was not registered).  p must be 4 or 8 (BM_ERR_INVALID_ARG otherwise;
+ * bm_db_tc_bytes returns 0); BM_ERR_WORKSPACE if bytes is too small. */
+size_t bm_db_tc_bytes(const bm_params *, int64_t n_sets);
+int bm_db_tc_register(const bm_params *, const uint64_t *d_db, int64_t n_sets, void *d_packed, size_t bytes,
+                      void *stream);
+int bm_db_tc_unregister(const uint64_t *d_db);
+
 /* Library options (process-wide; the defaults are the product -- tests and tuning runs change them).
  * Changing BM_OPT_CHUNK_PAIRS / BM_OPT_EXPAND_CHUNK / BM_OPT_CMP_CHUNK changes the workspace size the
  * *_ws_bytes functions return: size the workspace after setting them.  Results never depend on them.
@@ -265,7 +280,8 @@ typedef enum {
     BM_OPT_LADDER_C3 = 4,    /* 0/1: latency-mode ladder on 3-CTA clusters (1)                      */
     BM_OPT_LADDER_TAIL = 5,  /* 0/1: a large launch's partial last wave on the cluster ladders (1)  */
     BM_OPT_CMP_CHUNK = 6,    /* pairs per bm_match_cmp chunk (4096)                                 */
-    BM_OPT_COUNT_ = 7
+    BM_OPT_TENSOR_MMA = 7,   /* 0/1: K1 on the tensor cores for registered DBs (bm_db_tc_*) (1)      */
+    BM_OPT_COUNT_ = 8
 } bm_option;
 int bm_set_option(int32_t key, int64_t value);
 int64_t bm_get_option(int32_t key);

@@ -73,6 +73,9 @@ _SIGS = {
     "bm_ct_to_coeff": (_i32, [_P, _vp, _i64, _i32, _vp, _vp]),
     "bm_ct_from_coeff": (_i32, [_P, _vp, _i64, _i32, _vp, _vp]),
     "bm_match_ws_bytes": (_sz, [_P, _i64, _i32, _i32]),
+    "bm_db_tc_bytes": (_sz, [_P, _i64]),
+    "bm_db_tc_register": (_i32, [_P, _vp, _i64, _vp, _sz, _vp]),
+    "bm_db_tc_unregister": (_i32, [_vp]),
     "bm_match": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _vp, _sz, _i32, _vp]),
     "bm_match_rows": (_i32, [_P, _vp, _vp, _i64, _vp, _i32, _vp, _i64, _vp, _sz, _i32, _vp]),
     "bm_ipc_handle": (_i32, [_vp, _vp, ctypes.POINTER(_u64)]),
@@ -349,6 +352,24 @@ def bm_match_ws_bytes(prm, n_sets, nq, order=ORDER_HOISTED):
     return int(_lib.bm_match_ws_bytes(ctypes.byref(prm), n_sets, nq, order))
 
 
+def bm_db_tc_bytes(prm, n_sets):
+    return int(_lib.bm_db_tc_bytes(ctypes.byref(prm), n_sets))
+
+
+def bm_db_tc_register(prm, d_db, n_sets, d_packed, stream=None):
+    """Pack the DB into the tensor-core layout (d_packed: a CUDA uint8 tensor of >= bm_db_tc_bytes bytes,
+    kept alive by the caller) and register it: bm_match then runs K1 on the tensor cores for d_db."""
+    if d_packed.numel() * d_packed.element_size() < bm_db_tc_bytes(prm, n_sets):
+        raise ValueError("d_packed: smaller than bm_db_tc_bytes")
+    _need(d_db, n_sets * prm.p * 4 * N, "d_db")
+    _chk(_lib.bm_db_tc_register(ctypes.byref(prm), _dptr(d_db), n_sets, _dptr(d_packed),
+                                d_packed.numel() * d_packed.element_size(), _stream(stream)), "bm_db_tc_register")
+
+
+def bm_db_tc_unregister(d_db):
+    _chk(_lib.bm_db_tc_unregister(_dptr(d_db)), "bm_db_tc_unregister")
+
+
 def _check_scan(prm, d_db, n_sets, d_q, nq, n_limbs=2):
     if n_sets < 0 or nq < 0:
         raise ValueError("n_sets and nq must be >= 0")
@@ -445,7 +466,7 @@ def bm_match_host_ring(prm, evk_dev, d_db, n_sets, h_q, nq, h_ring, ring_rows, d
 
 # --------------------------------------------------------------------------- options / counters
 OPTIONS = {"chunk_pairs": 0, "expand_chunk": 1, "host_groups": 2, "ladder_c2": 3, "ladder_c3": 4,
-           "ladder_tail": 5, "cmp_chunk": 6}
+           "ladder_tail": 5, "cmp_chunk": 6, "tensor_mma": 7}
 
 
 def bm_set_option(name, value):

@@ -18,7 +18,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES = ["host.cpp", "device.cu"]
 HEADERS = ["bm_common.cuh", "bm_host.h", "ntt_base.cuh", "ntt2.cuh", "ntt3.cuh", "ntt3f.cuh",
-           "k_match.cuh", "k_next.cuh", "k_setup.cuh"]
+           "k_match.cuh", "k_tensor_mma.cuh", "k_next.cuh", "k_setup.cuh"]
 
 
 def _newer(target, deps):

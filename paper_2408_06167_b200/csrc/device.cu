@@ -43,6 +43,7 @@ using namespace bm;
 typedef unsigned __int128 u128;
 
 #include "k_match.cuh"
+#include "k_tensor_mma.cuh"
 #include "k_next.cuh"
 #include "k_setup.cuh"
 
@@ -62,6 +63,7 @@ struct DevCtx {
     double2 *zeta = nullptr;    // [N] exp(i pi k / N) (device decryption's canonical embedding)
     int32_t *slot_t = nullptr;  // [S] (5^j mod 2N - 1) / 2
     int max_cl[4] = {0, 0, 0, 0}; // cudaOccupancyMaxActiveClusters of the cluster ladders (index: cluster size)
+    TmConst tmc;                  // k_tensor_mma: 2^(8v) mod q0, q1 and 2^40 mod q0 (Shoup pairs)
     // bm_match_host's extra streams (created once per device, reused by every call under host_mu)
     std::mutex host_mu;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr}; // second compute stream, upload, download
@@ -70,6 +72,24 @@ struct DevCtx {
 
 std::mutex g_mu;
 std::vector<DevCtx *> g_ctx;
+
+// DBs registered in the tensor-core layout (bm_db_tc_register): bm_match runs K1 on the tensor cores
+// for them (k_tensor_mma)
+struct TcDb {
+    const uint64_t *db;
+    int64_t n_sets;
+    int32_t p;
+    const uint8_t *packed;
+};
+std::mutex g_tc_mu;
+std::vector<TcDb> g_tc;
+const uint8_t *tc_lookup(const uint64_t *db, int64_t n_sets, int32_t p)
+{
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    for (const TcDb &e : g_tc)
+        if (e.db == db && e.n_sets == n_sets && e.p == p) return e.packed;
+    return nullptr;
+}
 
 ulonglong2 shoup_pair(uint64_t w, uint64_t q) { return make_ulonglong2(w, shoup_companion(w, q)); }
 uint64_t powmod_d(uint64_t a, uint64_t e, uint64_t q)
@@ -167,6 +187,11 @@ int ctx_get(DevCtx **out)
         C->pinv[l] = shoup_pair(powmod_d(QP % q, q - 2, q), q);
     }
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
+    for (int v = 0; v < 8; v++) {
+        C->tmc.w[0][v] = shoup_pair(powmod_d(2, 8 * v, Q0), Q0);
+        C->tmc.w[1][v] = shoup_pair(powmod_d(2, 8 * v, Q1), Q1);
+    }
+    C->tmc.c40 = shoup_pair(powmod_d(2, 40, Q0), Q0);
     for (int l = 0; l < 2; l++) C->q2inv[l] = shoup_pair(powmod_d(Q2 % C->pr[l].q, C->pr[l].q - 2, C->pr[l].q), C->pr[l].q);
     C->pinv2 = shoup_pair(powmod_d(QP % Q2, Q2 - 2, Q2), Q2);
     cudaMemcpyToSymbol(c_cdt, host_cdt(), sizeof(uint64_t) * 19);
@@ -174,6 +199,8 @@ int ctx_get(DevCtx **out)
     cudaFuncSetAttribute(k_tensor<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_tensor<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TENSOR_SMEM_BYTES);
     cudaFuncSetAttribute(k_digits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM_BYTES);
+    cudaFuncSetAttribute(k_tensor_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tm_smem_bytes<4>());
+    cudaFuncSetAttribute(k_tensor_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tm_smem_bytes<8>());
     cudaFuncSetAttribute(k_relin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM_BYTES);
     set_smem(k_out_intt);
     cudaFuncSetAttribute(k_rescale_deg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K7_SMEM_BYTES);
@@ -272,6 +299,7 @@ struct OptInit {
         g_opt[BM_OPT_LADDER_C3] = 1;       // latency-mode ladder on 3-CTA clusters
         g_opt[BM_OPT_LADDER_TAIL] = 1;     // a large launch's partial last wave on the cluster ladders
         g_opt[BM_OPT_CMP_CHUNK] = 4096;    // pairs per bm_match_cmp chunk
+        g_opt[BM_OPT_TENSOR_MMA] = 1;      // K1 on the tensor cores where it applies (k_tensor_mma)
     }
 } g_opt_init;
 int64_t opt(int k) { return g_opt[k].load(std::memory_order_relaxed); }
@@ -1111,6 +1139,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     K.XU = K.XC + 2 * P1;
     K.ACC = order == BM_ORDER_PAPER ? K.XU + 4 * P1 : nullptr;
     const CtBuf bufC = order == BM_ORDER_PAPER ? CtBuf{K.ACC, 2 * N} : CtBuf{K.XC, 2 * N};
+    const uint8_t *dbp = tc_lookup(d_db, n_sets, prm->p); // the DB in the tensor-core layout, if registered
 
     bool prof;
     {
@@ -1154,6 +1183,13 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         const unsigned ntiles = (unsigned)(((na + TQB - 1) / TQB) * ((nb + TSB - 1) / TSB) * (N / CS / (tswap ? 1 : TSL)));
         const bool per_part = order == BM_ORDER_PAPER;
         const int n_rounds = per_part ? prm->p : 1;
+        // K1 on the tensor cores (k_tensor_mma): all parts at once (p = 4 or 8), at least half a 128-set
+        // tile, and the query operand (16 p MiB per query tile) inside the XC / XU region (6 N u64 per pair
+        // of the chunk capacity), which K1 does not otherwise use
+        const int64_t n_qt = (K.cq + TM_Q - 1) / TM_Q, n_st = (K.ct + TM_M - 1) / TM_M;
+        const bool use_mma = dbp && opt(BM_OPT_TENSOR_MMA) && !per_part && (prm->p == 4 || prm->p == 8) &&
+                             K.t0 % TM_M == 0 && K.ct >= TM_M / 2 && K.cq >= TM_Q / 2 &&
+                             (size_t)2 * n_qt * N * tm_b_bytes(prm->p) <= (size_t)6 * ch * N * sizeof(uint64_t);
         // the ladder's launch plan (see below): pairs [0, n_one) on the one-CTA kernel, the rest on clusters
         const bool c2ok = opt(BM_OPT_LADDER_C2) != 0, c3ok = opt(BM_OPT_LADDER_C3) != 0;
         const int64_t tail = np % C->n_sm;
@@ -1171,9 +1207,27 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
         for (int r = 0; r < n_rounds && !rc; r++) {
             const int lo = per_part ? r : 0, hi = per_part ? r + 1 : prm->p;
             beg(0, 2 * np);
-            if (tswap) k_tensor<2, true><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
-            else k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
-            counted();
+            if (use_mma) {
+                // K1 on the tensor cores: the query operand (B) into the XC / XU region (free until K3)
+                uint8_t *XB = reinterpret_cast<uint8_t *>(K.XC);
+                const int64_t nthr = 2 * n_qt * (int64_t)N * 2 * TM_Q * (prm->p / 2);
+                const unsigned nblk = (unsigned)((nthr + 255) / 256);
+                const unsigned nmma = (unsigned)(2 * n_qt * n_st * (N / TM_CB));
+                if (prm->p == 8) {
+                    k_tm_qexp<8><<<nblk, 256, 0, s>>>(K, XB, (int)n_qt, C->tmc);
+                    k_tensor_mma<8><<<nmma, TM_T, tm_smem_bytes<8>(), s>>>(K, dbp, XB, (int)n_qt, (int)n_st, C->tmc);
+                } else {
+                    k_tm_qexp<4><<<nblk, 256, 0, s>>>(K, XB, (int)n_qt, C->tmc);
+                    k_tensor_mma<4><<<nmma, TM_T, tm_smem_bytes<4>(), s>>>(K, dbp, XB, (int)n_qt, (int)n_st, C->tmc);
+                }
+                counted(2);
+            } else if (tswap) {
+                k_tensor<2, true><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+                counted();
+            } else {
+                k_tensor<2, false><<<2 * ntiles, TT, TENSOR_SMEM_BYTES, s>>>(K, lo, hi);
+                counted();
+            }
             end();
             if (deg2) {
                 beg(6, 3 * np);
@@ -1500,10 +1554,55 @@ int bm_match_host_ring(const bm_params *prm, const bm_evk_dev *evk, const uint64
     return match_host_impl(prm, evk, d_db, n_sets, h_q, nq, h_ring, ring_rows, d_ws, ws_bytes, order, stream);
 }
 
+size_t bm_db_tc_bytes(const bm_params *prm, int64_t n_sets)
+{
+    if (!prm || n_sets <= 0 || (prm->p != 4 && prm->p != 8)) return 0;
+    return (size_t)((n_sets + TM_M - 1) / TM_M) * 2 * N * tm_a_bytes(prm->p);
+}
+int bm_db_tc_register(const bm_params *prm, const uint64_t *d_db, int64_t n_sets, void *d_packed, size_t bytes,
+                      void *stream)
+{
+    if (!prm || !d_db || !d_packed || n_sets <= 0) return BM_ERR_INVALID_ARG;
+    if (prm->p != 4 && prm->p != 8) return BM_ERR_INVALID_ARG;
+    if (bytes < bm_db_tc_bytes(prm, n_sets)) return BM_ERR_WORKSPACE;
+    DevCtx *C;
+    int rc = ctx_get(&C);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n_st = (n_sets + TM_M - 1) / TM_M;
+    const int64_t nthr = n_st * 2 * 16 * prm->p * (int64_t)N;
+    const unsigned nblk = (unsigned)((nthr + 255) / 256);
+    uint8_t *pk = reinterpret_cast<uint8_t *>(d_packed);
+    if (prm->p == 8) k_tm_dbpack<8><<<nblk, 256, 0, s>>>(d_db, n_sets, n_st, pk);
+    else k_tm_dbpack<4><<<nblk, 256, 0, s>>>(d_db, n_sets, n_st, pk);
+    counted();
+    rc = launch_check();
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    for (TcDb &e : g_tc)
+        if (e.db == d_db) {
+            e = TcDb{d_db, n_sets, prm->p, pk};
+            return BM_OK;
+        }
+    g_tc.push_back(TcDb{d_db, n_sets, prm->p, pk});
+    return BM_OK;
+}
+int bm_db_tc_unregister(const uint64_t *d_db)
+{
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    for (size_t i = 0; i < g_tc.size(); i++)
+        if (g_tc[i].db == d_db) {
+            g_tc.erase(g_tc.begin() + (long)i);
+            return BM_OK;
+        }
+    return BM_ERR_INVALID_ARG;
+}
+
 int bm_set_option(int32_t key, int64_t value)
 {
     if (key < 0 || key >= BM_OPT_COUNT_) return BM_ERR_INVALID_ARG;
-    const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL;
+    const bool flag = key == BM_OPT_LADDER_C2 || key == BM_OPT_LADDER_C3 || key == BM_OPT_LADDER_TAIL ||
+                      key == BM_OPT_TENSOR_MMA;
     if (flag ? (value != 0 && value != 1) : key == BM_OPT_HOST_GROUPS ? value < 0 : value < 1) return BM_ERR_INVALID_ARG;
     g_opt[key].store(value);
     return BM_OK;
