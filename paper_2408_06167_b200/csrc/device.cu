@@ -1135,6 +1135,7 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     const size_t P1 = (size_t)ch * N;
     K.D01 = ws;
     K.D2 = K.D01 + 4 * P1;
+    K.cap = ch; // the D01 / D2 piece layout's pair stride (dofs)
     K.XC = K.D2 + 2 * P1;
     K.XU = K.XC + 2 * P1;
     K.ACC = order == BM_ORDER_PAPER ? K.XU + 4 * P1 : nullptr;

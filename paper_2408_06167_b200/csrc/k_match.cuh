@@ -34,6 +34,7 @@ struct MatchK {
     // pairs pi < split_lim leave K3 with component 0 split for the throughput ladder (coef_acc_update):
     // the NTT-domain part in the ciphertext buffer, the coefficient-domain part over D01[pi][0][q1]
     int64_t split_lim = 0;
+    int64_t cap = 0; // pairs of the workspace (the chunk capacity): the D01 / D2 piece stride (dofs)
     BM_D uint64_t *out_at(int64_t pi, int c) const
     {
         BM_CHECK(pi >= 0 && pi < (int64_t)cq * ct && jq0 + pi / ct < nq_total && t0 + pi % ct < n_sets);
@@ -43,6 +44,19 @@ struct MatchK {
     uint64_t *D01, *D2, *XC, *XU, *ACC;
     uint64_t *XR, *XO;  // f1: level-0 masked results (NTT), rotated results (coefficients)
 };
+
+// D01 (poly P = 2 c + l: d_c[q_l]) and D2 (P = l) of the level-1 scan: 16-coefficient pieces with the
+// pairs interleaved -- piece stride cap * 16 u64, pair stride 16 u64 -- so the K1 epilogues' per-pair
+// pieces of consecutive pairs are adjacent in HBM, while one pair's NTT-domain warp access (512 bytes,
+// 64 coefficients) is still four whole 128-byte lines
+#ifndef BM_DPIECE
+#define BM_DPIECE 64
+#endif
+constexpr int DPIECE = BM_DPIECE; // coefficients per piece (16, 32, 64: A/B)
+BM_D size_t dofs(const MatchK &K, int P, int64_t pi, int j)
+{
+    return ((size_t)(P * (N / DPIECE) + j / DPIECE) * (size_t)K.cap + (size_t)pi) * DPIECE + (j % DPIECE);
+}
 
 // a level-0 ciphertext buffer inside the workspace: pair pi, component c at base + pi*stride + c*N
 struct CtBuf {
@@ -59,6 +73,18 @@ BM_D ulonglong2 ld2k(const ulonglong2 *p) { return __ldg(p); }
 BM_D void st2(uint64_t *p, uint64_t x, uint64_t y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
 
 BM_D uint64_t submod_d(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// an NTT-domain polynomial of the D01 / D2 piece layout into registers (M4, like load_eval)
+BM_D void load_eval_d(uint64_t a[16], const uint64_t *base, const MatchK &K, int P, int64_t pi)
+{
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) {
+        const int j = 1024 * (e >> 1) + 2 * (int)threadIdx.x; // pos_M4(tid, e)
+        const ulonglong2 v = ld2(base + dofs(K, P, pi, j));
+        a[e] = v.x;
+        a[e + 1] = v.y;
+    }
+}
 
 // Planar Shoup keys (rlk, ladder gk): plane w at kp[0, N), plane w' at kp[N, 2N).  One 16-byte load per
 // plane gives positions pos, pos + 1 (pos even, lane-contiguous across a warp, like the twiddles' tw_pos):
@@ -392,9 +418,16 @@ template <int L, int NL, bool SW> BM_D void tensor_tile(const MatchK &K, uint64_
                         d2 = f64_mod_q1(f2[u][v]);
                         kk = f64_mod_q1(f1[u][v]);
                     }
-                    K.D01[((size_t)pi * 2 * NL + 0 + L) * N + jj] = d0;
-                    K.D01[((size_t)pi * 2 * NL + NL + L) * N + jj] = submod_d(submod_d(kk, d0, q), d2, q);
-                    K.D2[((size_t)pi * NL + L) * N + jj] = d2;
+                    const uint64_t d1 = submod_d(submod_d(kk, d0, q), d2, q);
+                    if (NL == 2) { // the level-1 scan's piece layout (dofs)
+                        K.D01[dofs(K, L, pi, jj)] = d0;
+                        K.D01[dofs(K, 2 + L, pi, jj)] = d1;
+                        K.D2[dofs(K, L, pi, jj)] = d2;
+                    } else {
+                        K.D01[((size_t)pi * 2 * NL + 0 + L) * N + jj] = d0;
+                        K.D01[((size_t)pi * 2 * NL + NL + L) * N + jj] = d1;
+                        K.D2[((size_t)pi * NL + L) * N + jj] = d2;
+                    }
                 }
         }
         BM_SYNCTHREADS(); // every read of buffer r & 1 is done before round r + 2 overwrites it
@@ -441,7 +474,7 @@ __global__ void __launch_bounds__(T, 1) k_digits(MatchK K)
     const int64_t pi = blockIdx.x >> 1;
     const int l = blockIdx.x & 1;
     uint64_t a[E];
-    load_eval(a, K.D2 + ((size_t)pi * 2 + l) * N);
+    load_eval_d(a, K.D2, K, l, pi);
     uint64_t *xu = K.XU + ((size_t)pi * 4 + 2 * l) * N;
     if (l == 0) {
         inv<0>(a, sm, K.pr[0]);
@@ -499,8 +532,7 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
     // key bytes of two Shoup products (K3 is load-bound: 5.94 -> 5.63 ms)
     const uint64_t *r0 = K.rlk + (size_t)(0 * 2 + c) * 3 * 2 * N, *r1 = K.rlk + (size_t)(1 * 2 + c) * 3 * 2 * N;
     const uint64_t *xu = K.XU + (size_t)pi * 4 * N;
-    const uint64_t *d2 = K.D2 + (size_t)pi * 2 * N;
-    const uint64_t *dc = K.D01 + ((size_t)pi * 4 + c * 2) * N; // d_c[q0], d_c[q1]
+    // d2[q_l] = D2 poly l, d_c[q_l] = D01 poly 2 c + l (dofs)
     uint64_t a[E];
     // ---- P limb
 #pragma unroll
@@ -512,8 +544,6 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         a[e + 1] = red128s<2>(dot2(u.y, w0.y, v.y, w1.y), K.pr[2].r64);
     }
     prefetch_poly_l2(xu + 0 * N); // the q1 phase's DRAM operands, during INTT_P
-    prefetch_poly_l2(d2 + 1 * N);
-    prefetch_poly_l2(dc + 1 * N);
     inv<2>(a, sm, K.pr[2]);
 #pragma unroll
     for (int e = 0; e < E; e++) ys[tid + T * e] = a[e]; // Y, canonical [0, P), coefficient j_M1(tid, e)
@@ -522,16 +552,14 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
-        const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(d2 + 1 * N + j), dd = ld2(dc + 1 * N + j);
+        const ulonglong2 u = ld2(xu + 0 * N + j), v = ld2(K.D2 + dofs(K, 1, pi, j)), dd = ld2(K.D01 + dofs(K, 2 * c + 1, pi, j));
         const ulonglong2 w0 = ld2(r0 + 1 * 2 * N + j), w1 = ld2(r1 + 1 * 2 * N + j);
         const uint64_t ka = red128s<1>(dot2(u.x, w0.x, v.x, w1.x), K.pr[1].r64);
         const uint64_t kb = red128s<1>(dot2(u.y, w0.y, v.y, w1.y), K.pr[1].r64);
         a[e] = reduce_bnd<1>(dd.x + ka);
         a[e + 1] = reduce_bnd<1>(dd.y + kb);
     }
-    prefetch_poly_l2(d2 + 0 * N); // the q0 phase's DRAM operands, during INTT_q1 and NTT_q0
-    prefetch_poly_l2(xu + 2 * N);
-    prefetch_poly_l2(dc);
+    prefetch_poly_l2(xu + 2 * N); // the q0 phase's DRAM operands, during INTT_q1 and NTT_q0
     inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // U, canonical (FP64 pipe)
     // ---- rescale in coefficient form
     const ulonglong2 pinv0 = K.pinv[0];
@@ -551,13 +579,12 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         // A is not needed -- C0 = q1^-1 (d0 + P^-1 KS0[q0]) (NTT domain) + q1^-1 (-A) (coefficient domain,
         // M1 order, lazily in [0, 2 q0)), the latter written over d_0[q1] (read only by this CTA, and
         // only before inv_f's barriers)
-        uint64_t *ai = K.D01 + ((size_t)pi * 4 + 1) * N;
 #pragma unroll
-        for (int e = 0; e < E; e++) ai[j_M1(tid, e)] = reduce_lazy<0>(shoup4<0>(6 * Q0 - a[e], q1inv));
+        for (int e = 0; e < E; e++) K.D01[dofs(K, 1, pi, j_M1(tid, e))] = reduce_lazy<0>(shoup4<0>(6 * Q0 - a[e], q1inv));
 #pragma unroll
         for (int e = 0; e < E; e += 2) {
             const int j = pos_M4(tid, e);
-            const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
+            const ulonglong2 u = ld2(K.D2 + dofs(K, 0, pi, j)), v = ld2(xu + 2 * N + j), dd = ld2(K.D01 + dofs(K, 2 * c, pi, j));
             const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
             const uint64_t ka = red128s<0>(dot2(u.x, w0.x, v.x, w1.x), K.pr[0].r64);
             const uint64_t kb = red128s<0>(dot2(u.y, w0.y, v.y, w1.y), K.pr[0].r64);
@@ -570,7 +597,7 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
         const int j = pos_M4(tid, e);
-        const ulonglong2 u = ld2(d2 + 0 * N + j), v = ld2(xu + 2 * N + j), dd = ld2(dc + j);
+        const ulonglong2 u = ld2(K.D2 + dofs(K, 0, pi, j)), v = ld2(xu + 2 * N + j), dd = ld2(K.D01 + dofs(K, 2 * c, pi, j));
         const ulonglong2 w0 = ld2(r0 + j), w1 = ld2(r1 + j);
         const uint64_t ka = red128s<0>(dot2(u.x, w0.x, v.x, w1.x), K.pr[0].r64);
         const uint64_t kb = red128s<0>(dot2(u.y, w0.y, v.y, w1.y), K.pr[0].r64);
@@ -816,7 +843,8 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
     constexpr bool have_acc = ACC;
     BM_CHECK(!ACC || pi < K.split_lim);
     if (have_acc) {
-        load_coef(a, K.D01 + ((size_t)pi * 4 + 1) * N);
+#pragma unroll
+        for (int e = 0; e < E; e++) a[e] = K.D01[dofs(K, 1, pi, j_M1(tid, e))];
         tmem_st16(tacc, a);
     }
     uint32_t g = 5; // 5^(2^i) mod 2N
@@ -1306,13 +1334,14 @@ __global__ void __launch_bounds__(T, 1) k_rescale_deg2(MatchK K)
     const int tid = threadIdx.x;
     const int64_t pi = blockIdx.x / 3;
     const int c = (int)(blockIdx.x - 3 * pi);
-    const uint64_t *src = c < 2 ? K.D01 + ((size_t)pi * 4 + c * 2) * N : K.D2 + (size_t)pi * 2 * N; // [q0], [q1]
+    const uint64_t *src = c < 2 ? K.D01 : K.D2; // poly P0 = [q0], P0 + 1 = [q1] (dofs)
+    const int P0 = c < 2 ? 2 * c : 0;
     uint64_t a[E];
-    load_eval(a, src + N);
+    load_eval_d(a, src, K, P0 + 1, pi);
     inv_f<1>(a, sm, K.pr[1].invf, K.pr[1].ninvf, K.pr[1].ninv_w1f); // canonical [0, q1)
 #pragma unroll
     for (int e = 0; e < E; e++) zs[tid + T * e] = a[e] > (Q1 >> 1) ? a[e] + (Q0 - Q1) : a[e]; // z^ mod q0
-    load_eval(a, src);
+    load_eval_d(a, src, K, P0, pi);
     inv<0>(a, sm, K.pr[0]); // canonical [0, q0)
     const ulonglong2 q1inv = K.q1inv;
 #pragma unroll

@@ -287,17 +287,16 @@ template <int P, int L> BM_D void tm_tile(const MatchK &K, const uint8_t *DBP, c
     const int s_ep = 32 * (warp & 3) + lane, g = warp >> 2;
     const int64_t set_ep = (int64_t)st * TM_M + s_ep;
     const uint32_t t_ep = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 16 * g;
-    // output rows of this thread: pair (query 8 qt + 2 g + j, set), outputs d0, d2, d1
-    uint64_t *dst[6];
+    // outputs of this thread: pairs (query 8 qt + 2 g + j, set), d0, d2, d1 at D01 poly L, D2 poly L,
+    // D01 poly 2 + L (dofs: the 4 coefficients of an iteration are one 32-byte piece, and the warp's 32
+    // consecutive sets write 32 adjacent pieces)
+    int64_t pij[2];
     bool ok[2];
 #pragma unroll
     for (int j = 0; j < 2; j++) {
         const int64_t q = (int64_t)qt * TM_Q + 2 * g + j;
         ok[j] = q < K.cq && set_ep < K.ct;
-        const int64_t pi = ok[j] ? q * K.ct + set_ep : 0;
-        dst[0 + j] = K.D01 + ((size_t)pi * 4 + L) * N;
-        dst[2 + j] = K.D2 + ((size_t)pi * 2 + L) * N;
-        dst[4 + j] = K.D01 + ((size_t)pi * 4 + 2 + L) * N;
+        pij[j] = ok[j] ? q * K.ct + set_ep : 0;
     }
     uint32_t ph0 = 0, ph1 = 0;
     load(c_lo, 0);
@@ -339,7 +338,7 @@ template <int P, int L> BM_D void tm_tile(const MatchK &K, const uint8_t *DBP, c
 #pragma unroll
             for (int j = 0; j < 2; j++)
                 if (ok[j]) {
-                    uint64_t *d = dst[2 * o + j] + c;
+                    uint64_t *d = (o == 1 ? K.D2 : K.D01) + dofs(K, o == 2 ? 2 + L : L, pij[j], c);
                     tm_st4(d, val[0][2 * o + j], val[1][2 * o + j], val[2][2 * o + j], val[3][2 * o + j]);
                 }
     }
