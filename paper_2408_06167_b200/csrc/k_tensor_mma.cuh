@@ -13,9 +13,12 @@
 // residues the CUDA-core K1 (k_tensor) produces -- the GPU parity tests compare them end to end.
 //
 // Tile: 128 sets (MMA M = TMEM lanes) x 8 queries (MMA N = 64 = 8 queries x 8 bytes) x one limb x a
-// block of TM_CB coefficients, walked in pairs (one 16-byte DB load serves c and c + 1; the epilogue
-// writes 16-byte (c, c + 1) vectors).  Per coefficient: 8 MMAs of K = 32 bytes for p = 8 (d0: 2, d2: 2,
-// d1: 4) into 192 TMEM columns; 256 columns per CTA, two CTAs per SM.
+// block of TM_CB coefficients, TM_CG = 4 per iteration.  The set operand comes from the DB packed once
+// into this layout (k_tm_dbpack, bm_db_tc_register: one contiguous 128 x 16 p-byte block per tile, limb
+// and coefficient), the query operand from k_tm_qexp; both stream into shared memory by cp.async one
+// iteration ahead.  Per coefficient: 8 MMAs of K = 32 bytes for p = 8 (d0: 2, d2: 2, d1: 4) into one of
+// two TMEM accumulator sets of 192 columns (the MMAs of one overlap the epilogue of the other); each
+// thread then stores 32 bytes (4 coefficients) per (pair, output) into D01 / D2 (dofs piece layout).
 // Shared-memory operands are in the canonical K-major SWIZZLE_NONE layout: 8-row x 16-byte core
 // matrices, LBO = the next core matrix along K, SBO = the next 8-row group (tools/probe/umma_i8_probe.cu
 // checked this encoding bit for bit on the B200).
@@ -27,7 +30,10 @@ namespace bm {
 constexpr int TM_M = 128;        // sets per tile (MMA M)
 constexpr int TM_Q = 8;          // queries per tile
 constexpr int TM_N = TM_Q * 8;   // MMA N: (query, byte u)
-constexpr int TM_CB = 64;        // coefficients per CTA
+#ifndef BM_TM_CB
+#define BM_TM_CB 64
+#endif
+constexpr int TM_CB = BM_TM_CB;  // coefficients per CTA
 
 // bytes of the expanded query operand per (limb, query tile, coefficient): [comp][g 8][kc P/2][8][16]
 BM_HD constexpr size_t tm_b_bytes(int P) { return (size_t)1024 * P; }
