@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 MATCH_KERNELS = ("k_tensor_intt", "k_modup_ntt", "k_ks_intt", "k_rescale_ntt", "k_ladder", "k_rot_digit", "k_digits",
-                 "k_rot_ks", "k_out_intt", "k_relin", "k_tensor")
+                 "k_rot_ks", "k_out_intt", "k_relin", "k_tensor", "k_tensor_mma", "k_tm_qexp")
 
 
 def launches(path, out):
@@ -31,8 +31,13 @@ def launches(path, out):
         k = r[iK].split("(")[0].replace("void ", "")
         if k.startswith("k_tensor<2"):  # bm_match's tensor; k_tensor<3> is f1's (level 2)
             k = "k_tensor"
+        elif k.startswith("bm::k_tensor_mma") or k.startswith("k_tensor_mma"):  # the tensor-core K1
+            k = "k_tensor_mma"
+        elif k.startswith("bm::k_tm_qexp") or k.startswith("k_tm_qexp"):  # its query operand
+            k = "k_tm_qexp"
         elif k.startswith("k_ladder_t<"):  # throughput ladder / latency-mode cluster ladder
-            k = "k_ladder" if ("false" in k or "<0>" in k) else "k_ladder_c2"
+            first = k[len("k_ladder_t<"):].split(",")[0].split(">")[0].strip()  # CL: the first argument
+            k = "k_ladder" if first in ("false", "0", "(bool)0") else "k_ladder_c2"
         tot[k] += float(r[iV].replace(",", ""))
         cnt[k] += 1
     match = {k: v for k, v in tot.items() if k in MATCH_KERNELS}
