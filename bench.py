@@ -440,7 +440,7 @@ def run_ours(args):
     # per-kernel-class device times (the library's CUDA events around every launch, on its launching
     # stream), a separate profiled pass of the same step on one stream
     roofline = profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws, W, order, n_sm, clocks,
-                            ms_step, groups)
+                            ms_step, groups, tc_k1=d_dbp is not None and "tensor_mma=0" not in args.opt)
 
     verify = None
     if not args.no_verify:
@@ -525,7 +525,7 @@ def run_ours(args):
 
 
 def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws, W, order, n_sm, clocks, ms_step,
-                 groups):
+                 groups, tc_k1=False):
     """Per-kernel-class device times: the library records CUDA events around each launch on its
     launching stream (bm_set_profiling); one stream, min(steps, 2) steps of the same work."""
     nsteps = max(1, min(args.steps, 2))
@@ -553,7 +553,8 @@ def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws
                 work = pun[i] * BFLY + pointwise[c] * pairs * nsteps * (rounds if i < 3 else 1)
             else:
                 work = mm[c] * pairs * nsteps * (rounds if i < 3 else 1)
-            step_work += work / nsteps
+            if not (tc_k1 and c == "tensor"):   # the tensor-core K1's byte MACs are not integer-pipe modmuls
+                step_work += work / nsteps
             per_class[c] = {"ms_per_step": pms[i] / nsteps, "launches": int(pla[i]),
                             "ms_per_launch": pms[i] / pla[i], "gmodmul_s": work / (pms[i] / 1e3) / 1e9,
                             "modmul_per_launch": work / pla[i]}
@@ -581,6 +582,9 @@ def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws
                           f"(4 IMAD + 3 IMAD.WIDE + 2 IMAD.HI at half rate)",
             "peak_measured": measured,
             "step_gmodmul_s": round(step_work / (ms_step / 1e3) / 1e9, 2),
+            "step_basis": ("integer-pipe kernels (digits, relin, ladder) over the whole step time; K1 runs on the "
+                           "tcgen05 tensor cores (its per_class entry counts the 8 N p modmul-equivalents of the "
+                           "CUDA-core K1)" if tc_k1 else "all kernels' algorithmic modmuls over the step time"),
             "step_frac": round(step_work / (ms_step / 1e3) / 1e9 / peak, 4),
             "per_class": {c: {k: round(v, 4) for k, v in d.items()} for c, d in per_class.items()}}
 
