@@ -303,3 +303,15 @@ def test_rng_modes(B):
         assert B.bm_get_option("chunk_pairs") == 33
     assert B.bm_get_option("chunk_pairs") == 16384
     assert B.bm_launch_count() >= 0
+    # the tensor-core K1's switch and the packed DB's size (host-only calls)
+    assert B.bm_get_option("tensor_mma") == 1
+    with pytest.raises(B.BMError):
+        B.bm_set_option("tensor_mma", 2)
+    with B.options(tensor_mma=0):
+        assert B.bm_get_option("tensor_mma") == 0
+    assert B.bm_get_option("tensor_mma") == 1
+    for d, p, n_sets, tiles in [(128, 8, 1, 1), (128, 8, 128, 1), (128, 8, 129, 2), (64, 4, 4096, 32)]:
+        assert B.bm_db_tc_bytes(B.bm_params_init(d, p), n_sets) == tiles * 2 * 8192 * 128 * 16 * p
+    assert B.bm_db_tc_bytes(B.bm_params_init(128, 1), 100) == 0        # p not 4 or 8: no tensor-core layout
+    assert B.bm_db_tc_bytes(B.bm_params_init(128, 16), 100) == 0
+    assert B.bm_db_tc_bytes(B.bm_params_init(128, 8), 0) == 0
