@@ -356,18 +356,24 @@ def bm_db_tc_bytes(prm, n_sets):
     return int(_lib.bm_db_tc_bytes(ctypes.byref(prm), n_sets))
 
 
+_TC_KEEP = {}   # d_db pointer -> (d_db, d_packed): the registered buffers stay alive until unregistered
+
+
 def bm_db_tc_register(prm, d_db, n_sets, d_packed, stream=None):
-    """Pack the DB into the tensor-core layout (d_packed: a CUDA uint8 tensor of >= bm_db_tc_bytes bytes,
-    kept alive by the caller) and register it: bm_match then runs K1 on the tensor cores for d_db."""
+    """Pack the DB into the tensor-core layout (d_packed: a CUDA uint8 tensor of >= bm_db_tc_bytes bytes)
+    and register it: bm_match then runs K1 on the tensor cores for d_db.  The binding holds references
+    to both tensors until bm_db_tc_unregister (d_db must not change meanwhile)."""
     if d_packed.numel() * d_packed.element_size() < bm_db_tc_bytes(prm, n_sets):
         raise ValueError("d_packed: smaller than bm_db_tc_bytes")
     _need(d_db, n_sets * prm.p * 4 * N, "d_db")
     _chk(_lib.bm_db_tc_register(ctypes.byref(prm), _dptr(d_db), n_sets, _dptr(d_packed),
                                 d_packed.numel() * d_packed.element_size(), _stream(stream)), "bm_db_tc_register")
+    _TC_KEEP[d_db.data_ptr()] = (d_db, d_packed)
 
 
 def bm_db_tc_unregister(d_db):
     _chk(_lib.bm_db_tc_unregister(_dptr(d_db)), "bm_db_tc_unregister")
+    _TC_KEEP.pop(d_db.data_ptr(), None)
 
 
 def _check_scan(prm, d_db, n_sets, d_q, nq, n_limbs=2):
