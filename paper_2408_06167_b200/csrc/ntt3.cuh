@@ -53,6 +53,10 @@ BM_HD int tw_pos(int k)
 template <int FROM, int TO>
 BM_D void xchg(uint64_t a[E], uint64_t *sm)
 {
+#if defined(BM_DIAG_XCHG) // tools/ntt_bench.cu diagnostic builds only (wrong results): 1 = barriers, no data; 2 = nothing
+    if (BM_DIAG_XCHG == 1) { BM_SYNCTHREADS(); BM_SYNCTHREADS(); }
+    return;
+#endif
     const int tid = threadIdx.x;
     constexpr bool local_w = (FROM != 1);          // writes stay in the warp's region
     constexpr bool local_r = (TO != 1);            // reads stay in the warp's region

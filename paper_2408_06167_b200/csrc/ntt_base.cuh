@@ -11,7 +11,12 @@ constexpr int SMEM_WORDS = N + N / 16; // 8704 u64 = 69,632 B: one word of paddi
 
 BM_D int pidx(int j) { return j + (j >> 4); }
 
+#if defined(BM_DIAG_TW) // tools/ntt_bench.cu diagnostic builds only (wrong results): twiddles as constant-bank operands, no loads
+__constant__ ulonglong2 c_diag_tw;
+BM_D ulonglong2 ldtw(const ulonglong2 *) { return c_diag_tw; }
+#else
 BM_D ulonglong2 ldtw(const ulonglong2 *p) { return __ldg(p); }
+#endif
 
 BM_D int brev13(int x) { return (int)(__brev((unsigned)x) >> 19); }
 
