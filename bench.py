@@ -546,7 +546,9 @@ def profile_pass(args, B, torch, prm, evk_dev, d_db, n_local, d_q, ring, gat, ws
     per_class, step_work = {}, 0.0
     # relin and ladder: the library counts the transforms it ran (component 0 split for the one-CTA
     # ladder: one transform fewer in K3 and in every ladder step but the last)
-    pointwise = {"relin": 20 * N_RING, "ladder": 6 * N_RING * prm.log_s}
+    # P-scaled one-CTA ladder (bm_build_info "pscale"): no P^-1 y^c products in the steps but the last
+    lad_pw = 6 * prm.log_s - (2 * (prm.log_s - 1) if "pscale" in B.bm_build_info() and order == 0 and prm.log_s else 0)
+    pointwise = {"relin": 20 * N_RING, "ladder": lad_pw * N_RING}
     for i, c in enumerate(B.PROFILE_CLASSES):
         if pla[i]:
             if c in pointwise and order in (0, 1):

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h> // header-only NVTX v3: named ranges for Nsight timelines (no-ops without a tool)
@@ -56,6 +57,8 @@ struct DevCtx {
     ulonglong2 *twf = nullptr; // [q1, q2][fwd, inv][N], FP64 form
     PrimeK pr[4] = {};
     ulonglong2 pinv[2], q1inv;
+    ulonglong2 q1invP;         // q1^-1 P mod q0 (LADDER_PSCALE)
+    PrimeK pr0s = {};          // pr[0] with N^-1 P^-1 for N^-1 (LADDER_PSCALE)
     ulonglong2 q2inv[2];       // f3: q2^-1 mod q0, q1
     ulonglong2 pinv2;          // f1: P^-1 mod q2
     uint64_t pmod[2];
@@ -187,6 +190,14 @@ int ctx_get(DevCtx **out)
         C->pinv[l] = shoup_pair(powmod_d(QP % q, q - 2, q), q);
     }
     C->q1inv = shoup_pair(powmod_d(Q1 % Q0, Q0 - 2, Q0), Q0);
+    {
+        const HostPrime &H = host_prime(0);
+        const uint64_t pi0 = C->pinv[0].x, nip = mulmod_h(H.ninv, pi0, Q0);
+        C->q1invP = shoup_pair(mulmod_h(C->q1inv.x, QP % Q0, Q0), Q0);
+        C->pr0s = C->pr[0];
+        C->pr0s.ninv = shoup_pair(nip, Q0);
+        C->pr0s.ninv_w1 = shoup_pair(mulmod_h(nip, H.inv[1], Q0), Q0);
+    }
     for (int v = 0; v < 8; v++) {
         C->tmc.w[0][v] = shoup_pair(powmod_d(2, 8 * v, Q0), Q0);
         C->tmc.w[1][v] = shoup_pair(powmod_d(2, 8 * v, Q1), Q1);
@@ -1119,6 +1130,8 @@ static int match_impl(const bm_params *prm, const bm_evk_dev *evk, const uint64_
     K.pinv[0] = C->pinv[0];
     K.pinv[1] = C->pinv[1];
     K.q1inv = C->q1inv;
+    K.q1invP = C->q1invP;
+    K.pr0s = C->pr0s;
     K.pmod[0] = C->pmod[0];
     K.pmod[1] = C->pmod[1];
     K.rlk = evk ? reinterpret_cast<const uint64_t *>(evk->rlk) : nullptr;
@@ -1629,6 +1642,14 @@ int bm_sync(void *stream)
 
 #define BM_STR2(x) #x
 #define BM_STR(x) BM_STR2(x)
-const char *bm_build_info(void) { return "libblindmatch sm_100a (nvcc " BM_STR(__CUDACC_VER_MAJOR__) "." BM_STR(__CUDACC_VER_MINOR__) ")"; }
+// "... ; ladder: split_c0 pscale" names the throughput ladder's exact rewritings this build uses (the
+// bench's algorithmic modmul count depends on them)
+const char *bm_build_info(void)
+{
+    static const std::string info = std::string("libblindmatch sm_100a (nvcc " BM_STR(__CUDACC_VER_MAJOR__) "." BM_STR(
+                                        __CUDACC_VER_MINOR__) "); ladder:") +
+                                    (LADDER_SPLIT_C0 ? " split_c0" : "") + (LADDER_PSCALE ? " pscale" : "");
+    return info.c_str();
+}
 
 } // extern "C"

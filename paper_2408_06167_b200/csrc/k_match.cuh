@@ -6,6 +6,24 @@
 // ================================================================== device constants
 __constant__ uint64_t c_cdt[19];
 
+// Component 0 split / P-scaled resident C of the throughput ladder (K3 and k_ladder_t<false, true>)
+#ifdef BM_LADDER_NO_SPLIT_C0
+constexpr bool LADDER_SPLIT_C0 = false;
+#else
+constexpr bool LADDER_SPLIT_C0 = true;
+#endif
+// The pairs K3 hands to the one-CTA throughput ladder (pi < split_lim) carry P C instead of C:
+// every update of the ladder is linear mod q0, so with C' = P C
+//   c'_c <- c'_c + [c = 0] sigma(c'_0) + sigma(c'_1) (P^-1 gk_r[c][q0]) - NTT_q0(y^c mod q0)
+// (the same folded keys), the digit is INTT_q0 with N^-1 P^-1 folded into its last stage (pr0s; the
+// exact integer x in [0, q0) as before), and the output leaves through the same constants -- the
+// P^-1 y^c product of every step but the last disappears (K3 folds P into its q1^-1 constant).
+#if defined(BM_LADDER_NO_PSCALE) || defined(BM_LADDER_NO_SPLIT_C0) || defined(BM_K3_NO_SPLIT)
+constexpr bool LADDER_PSCALE = false;
+#else
+constexpr bool LADDER_PSCALE = true;
+#endif
+
 // Workspace per (query, set) pair, 12 N u64:
 //   D01 [c][l][N]  d_c[q_l] (NTT)                       K1 -> K3
 //   D2  [l][N]     d2[q_l] (NTT)                        K1 -> K2, K3; then the ladder's scratch
@@ -16,6 +34,10 @@ struct MatchK {
     PrimeK pr[4];       // q0, q1, P, q2 (f1)
     ulonglong2 pinv[2]; // P^-1 mod q0, q1
     ulonglong2 q1inv;   // q1^-1 mod q0
+    // P-scaled throughput ladder (LADDER_PSCALE, below): q1^-1 P mod q0, and q0's constants with
+    // N^-1 P^-1 in place of N^-1 (the inverse transform that leaves the scaled domain)
+    ulonglong2 q1invP;
+    PrimeK pr0s;
     uint64_t pmod[2];   // P mod q0, q1
     const uint64_t *rlk, *gk; // PLANAR Shoup keys: poly k at [2k N, 2k N + N) = w, [2k N + N, 2k N + 2N) = w'
     const uint64_t *db, *qry;
@@ -572,7 +594,8 @@ __global__ void __launch_bounds__(T, 1) k_relin(MatchK K, CtBuf dst, int accumul
         const uint64_t z = R > (Q1 >> 1) ? R + (Q0 - Q1) : R;                      // centred, in q0
         a[e] = shoup4<0>(y, pinv0) + z + (f ? Q0 - 1 : 0);                         // < 6 q0
     }
-    const ulonglong2 q1inv = K.q1inv;
+    // pairs of the throughput ladder leave P-scaled (LADDER_PSCALE): q1^-1 P in place of q1^-1
+    const ulonglong2 q1inv = (LADDER_PSCALE && pi < K.split_lim) ? K.q1invP : K.q1inv;
     uint64_t *co = dst.at(pi, c);
     if (c == 0 && pi < K.split_lim) {
         // component 0 for the throughput ladder, split (k_ladder_t<false>, coef_acc_update): the NTT_q0 of
@@ -718,11 +741,6 @@ BM_D void tmem_ld16(uint32_t taddr, uint64_t v[E])
 // (k_ladder_t<false>) keeps c0 as two accumulators (coef_acc_update): 5 transforms per step, 6 in the
 // last one.
 constexpr size_t LADDER_SMEM_BYTES = 3 * SMEM_WORDS * sizeof(uint64_t);
-#ifdef BM_LADDER_NO_SPLIT_C0
-constexpr bool LADDER_SPLIT_C0 = false;
-#else
-constexpr bool LADDER_SPLIT_C0 = true;
-#endif
 
 
 // Latency mode (k_ladder_t<true>): when a launch has fewer pairs than half the SMs (a single query
@@ -841,6 +859,11 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
     // component 0 split by K3 (coef_acc_update): its coefficient-domain part starts the accumulator
     static_assert(!(CL && ACC), "the cluster ladders take component 0 unsplit");
     constexpr bool have_acc = ACC;
+    // PS: the resident C (and the accumulator) of these pairs is P C (LADDER_PSCALE, above): the
+    // inverse q0 transforms divide by P as well, and y^c enters reduced mod q0 instead of as P^-1 y^c
+    constexpr bool PS = ACC && LADDER_PSCALE;
+    const PrimeK &pr0i = PS ? K.pr0s : K.pr[0];
+    const uint64_t pneg = Q0 - K.pmod[0]; // -P mod q0
     BM_CHECK(!ACC || pi < K.split_lim);
     if (have_acc) {
 #pragma unroll
@@ -868,7 +891,7 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
         // digit: sigma_g(c1) -> INTT_q0 -> NTT_P
 #pragma unroll
         for (int e = 0; e < E; e++) a[e] = S1[nat_auto(nt, e, g)];
-        inv<0>(a, XB, K.pr[0]);
+        inv<0>(a, XB, pr0i);
         fwd<2, false>(a, XB, K.pr[2]); // lazy [0, 2P): Shoup operand only
         // P-limb key-switch products for both components; component 1's waits in the workspace
         if (CL) { // this rank's component only
@@ -905,8 +928,15 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
             if (!CL && c == 1) tmem_ld16(tks1, a); // component 1's P-limb product, parked in TMEM above
             inv<2>(a, XB, K.pr[2]);
             // P^-1 y^c mod q0 with y^c = y - [y > P/2] P:  P^-1 y - [y > P/2], < 5 q0
+            // (PS: y^c mod q0 itself, lazily: (y mod q0) + [y > P/2] (-P mod q0) < 3 q0; only component
+            // 1's last step, whose term leaves in coefficient form, takes the P^-1 product)
+            if (PS && (c == 0 || !last)) {
 #pragma unroll
-            for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+                for (int e = 0; e < E; e++) a[e] = reduce_lazy<0>(a[e]) + (a[e] > (QP >> 1) ? pneg : 0);
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) a[e] = shoup4<0>(a[e], pinv) + (a[e] > (QP >> 1) ? Q0 - 1 : 0);
+            }
             uint64_t *S = c ? S1 : S0;
             const uint64_t *gq = c ? gq1 : gq0;
 #ifndef BM_LADDER_NO_SPLIT_C0
@@ -927,10 +957,14 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
 #pragma unroll
                     for (int e = 0; e < E; e++) S0[nat_at(nt, e)] = a[e];
                 } else {
-                    inv<0>(a, XB, K.pr[0]); // canonical
+                    inv<0>(a, XB, pr0i); // canonical
                     uint64_t *o = K.out_at(pi, 0);
                     uint64_t t[E];
                     tmem_ld16(tacc, t); // [0, 2 q0)
+                    if (PS) { // the accumulator is P A: its one P^-1 product
+#pragma unroll
+                        for (int e = 0; e < E; e++) t[e] = shoup4<0>(t[e], pinv); // [0, 4 q0)
+                    }
 #pragma unroll
                     for (int e = 0; e < E; e++) o[j_M1(tid, e)] = reduce_bnd<0>(a[e] + t[e]);
                 }
@@ -975,7 +1009,7 @@ template <bool CL, bool ACC = false> __global__ void __launch_bounds__(T, 1) k_l
                     a[e] = reduce_lazy<0>(v); // [0, 2 q0) < 4 q0: inv<0>'s input bound; its output is canonical
 #endif
                 }
-                inv<0>(a, XB, K.pr[0]);
+                inv<0>(a, XB, pr0i);
                 uint64_t *o = K.out_at(pi, c);
                 uint64_t t[E];
                 tmem_ld16(ttsc, t);
