@@ -6,6 +6,14 @@ import json
 import sys
 
 
+def pct_int(rf):
+    """dominant kernel vs the integer roofline: executed modmuls (every line), and SURVEY 8(d)'s count
+    where the line carries both (bench lines since the P-scaled ladder: `frac` = 8(d), `executed`)"""
+    if "executed" in rf:
+        return f"{100 * rf['executed']['frac']:.1f}% executed, {100 * rf['frac']:.1f}% by §8(d)'s count"
+    return f"{100 * rf['frac']:.1f}%"
+
+
 def row(d):
     c = d["config"]
     v = d.get("verify") or {}
@@ -22,7 +30,7 @@ def row(d):
         top += f" (all {v['top1_agree_all']:.3f})"
     err = v.get("max_abs_score_err")
     return (f"| {cfg}{prefix} | {c['d']} | {c['p']} | {d['n_gpus']} | {d['value'] / 1e6:.2f} M | {d['ms_per_step']:.1f} | "
-            f"{100 * rf['hbm']['frac']:.2f}% | {100 * rf['frac']:.1f}% ({rf['kernel']}) / {100 * rf['step_frac']:.1f}% (step) | "
+            f"{100 * rf['hbm']['frac']:.2f}% | {pct_int(rf)} ({rf['kernel']}) / {100 * rf['step_frac']:.1f}% (step) | "
             f"{cpu.get('value', 0) / 1e3:.1f} K ({cpu.get('cores', '—')}) | {par} | "
             f"{'—' if err is None else f'{err:.1e}'} | {top} |")
 
